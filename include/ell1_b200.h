@@ -1,0 +1,161 @@
+/*
+ * ell1_b200.h — C ABI of the B200 (sm_100a) l1-minimization solver library.
+ *
+ * Plain C: device pointers, sizes, an opaque cudaStream_t (void*), int status.
+ * No torch / C++ types cross this boundary.  Every entry point names the
+ * reference interface it replaces (paths relative to /root/reference/pkg/src/ell1).
+ *
+ * Memory conventions
+ *   - Dictionaries live on the device COLUMN-MAJOR (element (i, j) at
+ *     A[j * ld + i]), ld >= d, ld % 32 == 0, rows d..ld-1 zero.  Build one from
+ *     a row-major float64 device copy with ell1_dict_build().
+ *   - d-vectors are allocated with ld entries (padding zero); n-vectors with
+ *     n (+ d for the [A, sI] extension) entries.  All solver vectors are float64.
+ *   - The library never allocates: callers query workspace sizes and pass
+ *     caller-owned device buffers.
+ *
+ * Status codes (return value of every call; solver state.status likewise)
+ */
+#ifndef ELL1_B200_H
+#define ELL1_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  ELL1_OK = 0,
+  ELL1_ZERO_DATA = 1,          /* ||A^T b||_inf == 0: x = 0 is optimal (early exit) */
+  ELL1_LAMBDA_NONPOS = 2,      /* resolved lambda <= 0 -> ValueError */
+  ELL1_BREAKDOWN = 3,          /* NumericalBreakdownError (backtracking / line search) */
+  ELL1_ILL_CONDITIONED = 4,    /* IllConditionedError */
+  ELL1_NOT_PD = 5,             /* NotPositiveDefiniteError */
+  ELL1_DEGENERATE = 6,         /* DegenerateSupportError */
+  ELL1_RUNNING = 7,            /* step budget of this launch used up; resumable */
+  ELL1_ERR_ARG = -1,           /* bad argument */
+  ELL1_ERR_CUDA = -2,          /* CUDA launch / runtime error */
+  ELL1_ERR_TIMEOUT = -3,       /* grid barrier timed out (kernel aborted cleanly) */
+  ELL1_ERR_NOCOOP = -4         /* device cannot co-schedule the persistent grid */
+};
+
+enum { ELL1_F64 = 0, ELL1_F32 = 1 };
+
+enum {                       /* user stopping rules (model.py:18-19) */
+  ELL1_STOP_NONE = 0,
+  ELL1_STOP_REL_OBJECTIVE = 1,
+  ELL1_STOP_REL_ESTIMATE = 2,
+  ELL1_STOP_GROUND_TRUTH = 3,
+  ELL1_STOP_KKT = 4
+};
+
+/* Device dictionary view: D = A (d x n) or the implicit [A, s I] (d x (n+d))
+ * of robust.ExtendedDictionary (robust.py:57-155) when ext != 0. */
+typedef struct {
+  const void* A;      /* column-major, ld-strided, dtype ELL1_F64 | ELL1_F32 */
+  int32_t dtype;
+  int32_t ext;        /* 1: append s*I columns */
+  int64_t d, n, ld;
+  double ext_scale;   /* s */
+} ell1_dict_t;
+
+/* Resumable solver state (device resident; the host reads it after a run). */
+typedef struct {
+  int32_t status;     /* ELL1_* */
+  int32_t phase;      /* 0 fresh, 1 iterating, 2 finished */
+  int32_t iterations;
+  int32_t converged;
+  int32_t hist;       /* stop-rule history length (0..2) */
+  int32_t ntrace;     /* trace rows written */
+  int32_t rot[10];    /* buffer rotation (internal) */
+  double scal[24];    /* solver scalars (internal; documented per solver) */
+} ell1_state_t;
+
+/* Common solver controls (SolverConfig, model.py:75-105). */
+typedef struct {
+  double lam;          /* lambda; < 0 => default 1e-2 * ||D^T b||_inf (model.py:126-129) */
+  double tol;
+  int32_t max_iter;
+  int32_t stop_kind;   /* ELL1_STOP_* */
+  double stop_thr;
+  const double* ground_truth;  /* device, n entries, or NULL */
+  double gt_norm;      /* ||ground_truth||_2 (host-computed) */
+} ell1_ctrl_t;
+
+/* FISTA options (shrinkage.py:251-260). */
+typedef struct {
+  double L0, eta, beta;
+  int32_t continuation;
+  int32_t exact_L;     /* 1: L fixed to L_exact (host passes spectral_norm_sq * (1 + 1e-9)) */
+  double L_exact;
+  const double* x0;    /* probe mode only: the point y to backtrack from (device, n(+d)) */
+  int32_t probe;       /* 1: shrinkage.backtrack_L (shrinkage.py:216-228): one backtracking
+                          search from y = x0 at fixed lambda, no zero-data / lambda checks */
+  int32_t _pad;
+} ell1_fista_opts_t;
+
+/* Output / scratch buffers of one solve (all device). */
+typedef struct {
+  void* workspace; size_t workspace_bytes;
+  ell1_state_t* state;
+  double* trace;       /* [max_iter + 2][4]: iteration, objective, residual_norm, support */
+  double* x;           /* n(+d): current iterate (valid at any exit) */
+  double* x_prev;      /* n(+d): previous iterate (observer payload) or NULL */
+  double* y;           /* n(+d): extrapolated point (observer payload) or NULL */
+  int32_t max_steps;   /* iterations this launch may take (<= 0: unlimited); resumable */
+  int32_t blocks;      /* persistent grid size (0: one CTA per SM) */
+} ell1_io_t;
+
+/* ---------------------------------------------------------------- setup */
+
+/* Convert a row-major float64 d x n device matrix into the column-major
+ * dictionary layout (dtype conversion included).  Replaces the host-side
+ * np.ascontiguousarray(A, float64) (model.py:51) + upload. */
+int ell1_dict_build(const double* A_rowmajor, int64_t d, int64_t n, int64_t ld,
+                    int32_t dtype, void* A_out, void* stream);
+
+/* max_j |(D^T b)_j| and ||b||_2 into out[0], out[1] (device).  Replaces the
+ * np.max(np.abs(A.T @ b)) of model.py:128 / shrinkage.py:245. */
+int ell1_correlation_max(const ell1_dict_t* D, const double* b, double* out,
+                         void* workspace, size_t workspace_bytes, void* stream);
+size_t ell1_correlation_workspace(const ell1_dict_t* D);
+
+/* Largest eigenvalue of D^T D by power iteration on the smaller Gram side
+ * (numerics.py:224-261); v0 = host-drawn default_rng(218751) start (length
+ * min(d, n_cols)), extra redraws in v0 + k*min(d,n_cols) (nredraw of them).
+ * out[0] = theta, out[1] = steps. */
+int ell1_spectral_norm_sq(const ell1_dict_t* D, const double* v0, int32_t nredraw,
+                          double tol, int32_t max_iter, double* out,
+                          void* workspace, size_t workspace_bytes, void* stream);
+size_t ell1_power_workspace(const ell1_dict_t* D);
+
+/* ------------------------------------------------------- _accel kernels */
+
+/* out = sgn(u) max(|u| - a, 0)  (_accel/_fastkernels.pyx:14-27). */
+int ell1_soft_threshold(const double* u, double a, double* out, int64_t n, void* stream);
+/* out = clamp(z, -1, 1)  (_accel/_fastkernels.pyx:30-43). */
+int ell1_project_box_linf(const double* z, double* out, int64_t n, void* stream);
+/* In-place LINPACK rank-1 update / downdate of an upper factor (row-major m x m),
+ * consuming v (_accel/_fastkernels.pyx:46-78).  status (device int) receives 0
+ * or failing pivot + 1 (downdate only). */
+int ell1_chol_update(double* R, double* v, int64_t m, int32_t* status, void* stream);
+int ell1_chol_downdate(double* R, double* v, int64_t m, int32_t* status, void* stream);
+
+/* --------------------------------------------------------------- solvers */
+
+/* Accelerated proximal gradient with backtracking and continuation —
+ * replaces shrinkage.fista_solve (shrinkage.py:231-298). */
+size_t ell1_fista_workspace(const ell1_dict_t* D, const ell1_ctrl_t* C, int32_t blocks);
+int ell1_fista(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C,
+               const ell1_fista_opts_t* O, const ell1_io_t* io, void* stream);
+
+/* library / device info */
+int ell1_device_sms(int32_t device);
+const char* ell1_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ELL1_B200_H */

@@ -1,0 +1,130 @@
+"""ctypes binding of libell1b200.so (the C ABI declared in include/ell1_b200.h).
+
+There is deliberately no fallback: if the library or a CUDA device is
+missing, every solver call raises DeviceError.
+"""
+
+import ctypes
+import os
+import threading
+
+from paper_1007_3753_b200.exceptions import DeviceError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libell1b200.so")
+
+OK, ZERO_DATA, LAMBDA_NONPOS, BREAKDOWN, ILL_CONDITIONED, NOT_PD, DEGENERATE, RUNNING = range(8)
+ERR_ARG, ERR_CUDA, ERR_TIMEOUT, ERR_NOCOOP = -1, -2, -3, -4
+F64, F32 = 0, 1
+STOP_CODES = {None: 0, "relative-objective": 1, "relative-estimate": 2,
+              "ground-truth-distance": 3, "kkt-residual": 4}
+
+_ERRTEXT = {ERR_ARG: "bad argument", ERR_CUDA: "CUDA runtime error",
+            ERR_TIMEOUT: "grid barrier timed out", ERR_NOCOOP: "persistent grid does not fit the device"}
+
+
+class Dict(ctypes.Structure):
+    _fields_ = [("A", ctypes.c_void_p), ("dtype", ctypes.c_int32), ("ext", ctypes.c_int32),
+                ("d", ctypes.c_int64), ("n", ctypes.c_int64), ("ld", ctypes.c_int64),
+                ("ext_scale", ctypes.c_double)]
+
+
+class State(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("phase", ctypes.c_int32),
+                ("iterations", ctypes.c_int32), ("converged", ctypes.c_int32),
+                ("hist", ctypes.c_int32), ("ntrace", ctypes.c_int32),
+                ("rot", ctypes.c_int32 * 10), ("scal", ctypes.c_double * 24)]
+
+
+class Ctrl(ctypes.Structure):
+    _fields_ = [("lam", ctypes.c_double), ("tol", ctypes.c_double),
+                ("max_iter", ctypes.c_int32), ("stop_kind", ctypes.c_int32),
+                ("stop_thr", ctypes.c_double), ("ground_truth", ctypes.c_void_p),
+                ("gt_norm", ctypes.c_double)]
+
+
+class FistaOpts(ctypes.Structure):
+    _fields_ = [("L0", ctypes.c_double), ("eta", ctypes.c_double), ("beta", ctypes.c_double),
+                ("continuation", ctypes.c_int32), ("exact_L", ctypes.c_int32),
+                ("L_exact", ctypes.c_double), ("x0", ctypes.c_void_p),
+                ("probe", ctypes.c_int32), ("_pad", ctypes.c_int32)]
+
+
+class IO(ctypes.Structure):
+    _fields_ = [("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
+                ("state", ctypes.c_void_p), ("trace", ctypes.c_void_p),
+                ("x", ctypes.c_void_p), ("x_prev", ctypes.c_void_p), ("y", ctypes.c_void_p),
+                ("max_steps", ctypes.c_int32), ("blocks", ctypes.c_int32)]
+
+
+assert ctypes.sizeof(State) == 256, ctypes.sizeof(State)
+
+_lock = threading.Lock()
+_lib = None
+_load_error = None
+
+P = ctypes.POINTER
+_SIGS = {
+    "ell1_dict_build": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                       ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_correlation_max": (ctypes.c_int, [P(Dict), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                            ctypes.c_size_t, ctypes.c_void_p]),
+    "ell1_correlation_workspace": (ctypes.c_size_t, [P(Dict)]),
+    "ell1_spectral_norm_sq": (ctypes.c_int, [P(Dict), ctypes.c_void_p, ctypes.c_int32, ctypes.c_double,
+                                             ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+                                             ctypes.c_size_t, ctypes.c_void_p]),
+    "ell1_power_workspace": (ctypes.c_size_t, [P(Dict)]),
+    "ell1_soft_threshold": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_void_p,
+                                           ctypes.c_int64, ctypes.c_void_p]),
+    "ell1_project_box_linf": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                             ctypes.c_void_p]),
+    "ell1_chol_update": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                        ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_chol_downdate": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                          ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_fista_workspace": (ctypes.c_size_t, [P(Dict), P(Ctrl), ctypes.c_int32]),
+    "ell1_fista": (ctypes.c_int, [P(Dict), ctypes.c_void_p, P(Ctrl), P(FistaOpts), P(IO),
+                                  ctypes.c_void_p]),
+    "ell1_device_sms": (ctypes.c_int, [ctypes.c_int32]),
+    "ell1_version": (ctypes.c_char_p, []),
+}
+
+# every symbol include/ell1_b200.h declares (checked by tests/test_abi.py)
+EXPORTS = tuple(_SIGS)
+
+
+def _load():
+    global _lib, _load_error
+    with _lock:
+        if _lib is not None or _load_error is not None:
+            return _lib
+        try:
+            lib = ctypes.CDLL(LIB_PATH)
+        except OSError as exc:
+            _load_error = "cannot load %s: %s (run `python -m paper_1007_3753_b200.build`)" % (
+                LIB_PATH, exc)
+            return None
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return _lib
+
+
+def available():
+    return _load() is not None
+
+
+def lib():
+    """The loaded library; raises DeviceError (no fallback) when missing."""
+    L = _load()
+    if L is None:
+        raise DeviceError(_load_error)
+    return L
+
+
+def check(rc, what):
+    if rc < 0:
+        raise DeviceError("%s failed: %s (status %d)" % (what, _ERRTEXT.get(rc, "error"), rc))
+    return rc

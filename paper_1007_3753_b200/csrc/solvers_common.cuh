@@ -1,0 +1,155 @@
+// solvers_common.cuh — launch plumbing + scalar helpers shared by the solver kernels.
+#pragma once
+#include "engine.cuh"
+#include <math.h>
+
+namespace ell1 {
+
+// Raw (type-erased) dictionary as the C ABI carries it.
+struct DictRaw {
+  const void* A;
+  int dtype, ext;
+  int64_t d, n, ld;
+  double s;
+};
+
+// Grid-shared scratch common to every persistent solver.
+struct GridBufs {
+  double* part;               // [nb][pstride]
+  int64_t pstride;
+  double* scal;               // [2][nb][SCAL]
+  unsigned long long* bar;
+  int* abort;
+  int64_t shcap;              // shared-memory doubles per CTA
+};
+
+template <class TA>
+__device__ __forceinline__ DictV<TA> dict_view(const DictRaw& R) {
+  DictV<TA> D;
+  D.A = reinterpret_cast<const TA*>(R.A);
+  D.d = R.d; D.n = R.n; D.ld = R.ld; D.ext = R.ext; D.s = R.s;
+  return D;
+}
+
+__device__ __forceinline__ void ctx_bind(Ctx& E, const GridBufs& g, double* smem) {
+  E.bar = g.bar; E.abort = g.abort; E.part = g.part; E.pstride = g.pstride;
+  E.scal = g.scal; E.sh = smem; E.shcap = g.shcap;
+}
+
+// shrinkage.py:184-196 — t' = (1 + sqrt(4t^2 + 1)) / 2, nudged down by ulps
+// until t'^2 - t' <= t^2 (the file is built with -fmad=false so this matches numpy).
+__device__ __forceinline__ double fista_t_next(double t) {
+  double tn = 0.5 * (1.0 + sqrt(4.0 * t * t + 1.0));
+  while (tn * tn - tn > t * t) tn = nextafter(tn, 1.0);
+  return tn;
+}
+
+// _fastkernels.pyx:14-27 (u > a -> u - a; u < -a -> u + a; else +0)
+__device__ __forceinline__ double soft1(double u, double a) {
+  return u > a ? u - a : (u < -a ? u + a : 0.0);
+}
+
+__device__ __forceinline__ double sgn(double x) { return x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : 0.0); }
+
+// Python max(a, b) for floats (first argument wins ties / NaN in b).
+__device__ __forceinline__ double pymax(double a, double b) { return b > a ? b : a; }
+
+// user stopping rule test (model.py:176-224) from reduced quantities
+__device__ __forceinline__ bool stop_fires(int kind, double thr, int hist, double F, double F_prev,
+                                           double dx2, double xp2, double gt2, double gtn, double kkt) {
+  switch (kind) {
+    case ELL1_STOP_REL_OBJECTIVE: return hist >= 2 && fabs(F - F_prev) <= thr * fabs(F_prev);
+    case ELL1_STOP_REL_ESTIMATE: return hist >= 2 && sqrt(dx2) <= thr * sqrt(xp2);
+    case ELL1_STOP_GROUND_TRUTH: return sqrt(gt2) <= thr * gtn;
+    case ELL1_STOP_KKT: return kkt <= thr;
+    default: return false;
+  }
+}
+
+}  // namespace ell1
+
+// ---------------------------------------------------------------- host side
+#include <cstdio>
+namespace ell1 {
+
+inline int sm_count(int dev) {
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  return v;
+}
+
+inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// Grid size: one CTA per SM at most, at least ~16 columns per CTA.
+inline int pick_blocks(int64_t n, int requested) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int sms = sm_count(dev);
+  if (sms <= 0) sms = 148;
+  int nb = requested > 0 ? requested : sms;
+  if (nb > sms) nb = sms;
+  int64_t by_cols = (n + 15) / 16;
+  if (by_cols < 1) by_cols = 1;
+  if (nb > by_cols) nb = (int)by_cols;
+  return nb < 1 ? 1 : nb;
+}
+
+// Bump allocator over a caller workspace (256-byte aligned pieces).
+struct Carve {
+  char* base;
+  size_t off, cap;
+  bool ok;
+  Carve(void* p, size_t c) : base((char*)p), off(0), cap(c), ok(true) {}
+  template <class T>
+  T* take(size_t count) {
+    size_t bytes = align_up((int64_t)(count * sizeof(T)), 256);
+    if (off + bytes > cap) { ok = false; return nullptr; }
+    T* p = reinterpret_cast<T*>(base + off);
+    off += bytes;
+    return p;
+  }
+};
+
+inline size_t grid_bytes(int nb, int64_t pstride) {
+  return align_up((int64_t)nb * pstride * 8, 256) + align_up((int64_t)2 * nb * SCAL * 8, 256) + 512;
+}
+
+inline bool carve_grid(Carve& cv, GridBufs& g, int nb, int64_t pstride) {
+  g.part = cv.take<double>((size_t)nb * pstride);
+  g.pstride = pstride;
+  g.scal = cv.take<double>((size_t)2 * nb * SCAL);
+  g.bar = cv.take<unsigned long long>(4);
+  g.abort = reinterpret_cast<int*>(g.bar + 2);
+  return cv.ok;
+}
+
+// Cooperative launch with the requested dynamic shared memory.
+template <class K, class Arg>
+inline int coop_launch(K kernel, int nb, size_t smem, cudaStream_t s, Arg& arg, unsigned long long* bar) {
+  if (cudaMemsetAsync(bar, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess) return ELL1_ERR_CUDA;
+  if (smem > 48 * 1024) {
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return ELL1_ERR_CUDA;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, NTHR, smem) != cudaSuccess) return ELL1_ERR_CUDA;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (per_sm < 1 || nb > per_sm * sm_count(dev)) return ELL1_ERR_NOCOOP;
+  void* args[] = {(void*)&arg};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)kernel, dim3(nb), dim3(NTHR), args, smem, s);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "ell1_b200: cooperative launch failed: %s\n", cudaGetErrorString(e));
+    return ELL1_ERR_CUDA;
+  }
+  return ELL1_OK;
+}
+
+inline size_t smem_bytes(int64_t n_cols, int nb, int nv, int64_t ld, int nv_t) {
+  int64_t s = engine_smem_doubles(n_cols, nb, nv);
+  int64_t want = ld * nv_t;                       // stage d-vectors for D^T r when they fit
+  if (want * 8 <= 160 * 1024 && want > s) s = want;
+  return (size_t)s * 8;
+}
+
+}  // namespace ell1

@@ -1,0 +1,171 @@
+"""Device-state manager: dictionaries uploaded once, workspaces, streams.
+
+PyTorch is used here only as plumbing — device allocation, host<->device
+copies and the current CUDA stream.  All arithmetic happens in
+libell1b200.so (csrc/).
+"""
+
+import ctypes
+
+import numpy as np
+
+from paper_1007_3753_b200 import _lib
+from paper_1007_3753_b200.exceptions import DeviceError
+
+_POWER_SEED = 218751   # numerics.py:224
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device available (the B200 path has no CPU fallback)")
+    return torch
+
+
+def current_device(ordinal=None):
+    torch = _torch()
+    if ordinal is None:
+        ordinal = torch.cuda.current_device()
+    return torch.device("cuda", int(ordinal))
+
+
+def stream_ptr(dev):
+    torch = _torch()
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def alloc_bytes(nbytes, dev):
+    torch = _torch()
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=dev)
+
+
+def to_device_vec(v, length, dev):
+    """float64 host vector -> zero-padded device vector of `length` entries."""
+    torch = _torch()
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    out = torch.zeros(length, dtype=torch.float64, device=dev)
+    if v.shape[0]:
+        out[: v.shape[0]].copy_(torch.from_numpy(v), non_blocking=False)
+    return out
+
+
+def _pad32(d):
+    return (int(d) + 31) // 32 * 32
+
+
+class DeviceDictionary:
+    """Read-only device copy of a dense dictionary A (d x n).
+
+    Layout: column-major, ld = d rounded up to 32 rows, float64 or float32
+    storage (``dtype``).  Pass an instance as ``ProblemInstance.A`` (or to
+    ``cab_solve``) to reuse the upload across solves; plain numpy arrays are
+    uploaded per call.  ``norm_sq`` mirrors DenseDictionary.norm_sq
+    (operators.py:53-56, cached spectral_norm_sq).
+    """
+
+    def __init__(self, A, dtype="float64", device=None):
+        torch = _torch()
+        L = _lib.lib()
+        self.device = current_device(device)
+        if isinstance(A, DeviceDictionary):
+            raise TypeError("already a DeviceDictionary")
+        if isinstance(A, torch.Tensor):
+            src = A.to(device=self.device, dtype=torch.float64).contiguous()
+        else:
+            host = np.ascontiguousarray(A, dtype=np.float64)
+            if host.ndim != 2:
+                raise ValueError("dictionary must be a matrix")
+            src = torch.from_numpy(host).to(self.device, non_blocking=False)
+        if src.ndim != 2:
+            raise ValueError("dictionary must be a matrix")
+        self.d, self.n = int(src.shape[0]), int(src.shape[1])
+        self.ld = _pad32(self.d)
+        self.dtype = {"float64": _lib.F64, "float32": _lib.F32}[str(dtype)]
+        tdt = torch.float64 if self.dtype == _lib.F64 else torch.float32
+        self.storage = torch.empty(self.n * self.ld, dtype=tdt, device=self.device)
+        rc = L.ell1_dict_build(ptr(src), self.d, self.n, self.ld, self.dtype,
+                               ptr(self.storage), stream_ptr(self.device))
+        _lib.check(rc, "ell1_dict_build")
+        self._norm_sq = None
+
+    # -- C ABI view --------------------------------------------------------
+    def view(self, ext=False, scale=0.0):
+        v = _lib.Dict()
+        v.A = self.storage.data_ptr()
+        v.dtype = self.dtype
+        v.ext = 1 if ext else 0
+        v.d, v.n, v.ld = self.d, self.n, self.ld
+        v.ext_scale = float(scale)
+        return v
+
+    @property
+    def shape(self):
+        return (self.d, self.n)
+
+    # -- operator-protocol hooks ------------------------------------------
+    def norm_sq(self):
+        """Largest eigenvalue of A^T A (numerics.spectral_norm_sq), cached."""
+        if self._norm_sq is None:
+            self._norm_sq = spectral_norm_sq_device(self)
+        return self._norm_sq
+
+
+def as_device_dictionary(A, config=None):
+    """Return (DeviceDictionary, owned) for whatever the caller passed as A."""
+    if isinstance(A, DeviceDictionary):
+        return A, False
+    dtype = "float64"
+    dev = None
+    if config is not None:
+        dtype = config.opt("dtype", "float64")
+        dev = config.opt("device", None)
+    return DeviceDictionary(A, dtype=dtype, device=dev), True
+
+
+def correlation_max(A, b, device=None):
+    """max |A^T b| computed on the device (model.py:126-129)."""
+    D, _ = as_device_dictionary(A) if not isinstance(A, DeviceDictionary) else (A, False)
+    return _corr(D, D.view(), b)[0]
+
+
+def _corr(D, view, b):
+    torch = _torch()
+    L = _lib.lib()
+    bd = to_device_vec(b, D.ld, D.device)
+    out = torch.zeros(2, dtype=torch.float64, device=D.device)
+    wsb = L.ell1_correlation_workspace(ctypes.byref(view))
+    ws = alloc_bytes(wsb, D.device)
+    rc = L.ell1_correlation_max(ctypes.byref(view), ptr(bd), ptr(out), ptr(ws), wsb,
+                                stream_ptr(D.device))
+    _lib.check(rc, "ell1_correlation_max")
+    o = out.cpu().numpy()
+    return float(o[0]), float(o[1])
+
+
+def spectral_norm_sq_device(D, tol=1e-6, max_iter=1000):
+    """Power iteration on the device with the reference's fixed start vector
+    (numerics.py:245-247: default_rng(218751), normalised; redraws follow the
+    same generator stream)."""
+    torch = _torch()
+    L = _lib.lib()
+    dim = D.d if D.d <= D.n else D.n
+    rng = np.random.default_rng(_POWER_SEED)
+    draws = []
+    for _ in range(4):
+        v = rng.standard_normal(dim)
+        v /= np.linalg.norm(v)
+        draws.append(v)
+    # start vector + 3 redraws, packed with stride dim (kernel indexes v0[k*dim + i])
+    vd = to_device_vec(np.concatenate(draws), 4 * dim, D.device)
+    out = torch.zeros(2, dtype=torch.float64, device=D.device)
+    view = D.view()
+    wsb = L.ell1_power_workspace(ctypes.byref(view))
+    ws = alloc_bytes(wsb, D.device)
+    rc = L.ell1_spectral_norm_sq(ctypes.byref(view), ptr(vd), 3, float(tol), int(max_iter),
+                                 ptr(out), ptr(ws), wsb, stream_ptr(D.device))
+    _lib.check(rc, "ell1_spectral_norm_sq")
+    return float(out.cpu().numpy()[0])

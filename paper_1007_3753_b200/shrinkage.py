@@ -1,0 +1,198 @@
+"""Shrinkage solvers on the B200 — drop-in for ell1.shrinkage.
+
+fista_solve runs as ONE persistent cooperative kernel (csrc/fista.cu): the
+backtracking search, t-sequence, continuation and stopping rules execute on
+the device in float64 with the reference's formulas; only the result (x,
+trace, state) comes back to the host.  The small scalar helpers
+(fista_t_next, bb_alpha, ContinuationSchedule) are pure host math on
+Python floats, identical to the reference's.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from paper_1007_3753_b200 import _lib, device
+from paper_1007_3753_b200._runner import Buffers, Prepared, byref, drive, host_vec, raise_for
+from paper_1007_3753_b200.model import SolverResult, TraceEntry
+
+_ALPHA_MIN = 1e-30
+_ALPHA_MAX = 1e30
+_MAX_DOUBLINGS = 50
+_MAX_BACKTRACK = 100
+
+
+@dataclass(frozen=True)
+class ContinuationSchedule:
+    """Decreasing lambda schedule (shrinkage.py:27-58)."""
+
+    lambda_start: float
+    beta: float
+    lambda_target: float
+
+    def __post_init__(self):
+        if not self.lambda_target > 0:
+            raise ValueError("lambda_target must be positive")
+        if self.lambda_start < self.lambda_target:
+            raise ValueError("lambda_start must be >= lambda_target")
+        if not 0 < self.beta < 1:
+            raise ValueError("beta must lie in (0, 1)")
+
+    def stages(self):
+        """Descending lambdas ending at lambda_target; >= 5 stages when descending."""
+        if self.lambda_start == self.lambda_target:
+            return [self.lambda_target]
+        out = [self.lambda_start]
+        while out[-1] > self.lambda_target:
+            out.append(max(out[-1] * self.beta, self.lambda_target))
+        if len(out) < 5:
+            q = (self.lambda_target / self.lambda_start) ** 0.25
+            out = [self.lambda_start * q ** i for i in range(5)]
+            out[-1] = self.lambda_target
+        return out
+
+
+@dataclass
+class FistaState:
+    """Momentum state after one accepted step (shrinkage.py:61-69)."""
+
+    x_prev: np.ndarray
+    x_cur: np.ndarray
+    t_prev: float
+    t_cur: float
+    L: float
+
+
+def bb_alpha(s, g):
+    """(s'g)/(s's) clamped to [1e-30, 1e30] (shrinkage.py:72-82)."""
+    s = np.asarray(s, dtype=np.float64)
+    g = np.asarray(g, dtype=np.float64)
+    ss = float(s @ s)
+    ratio = float(s @ g) / ss if ss > 0.0 else 0.0
+    return min(max(ratio, _ALPHA_MIN), _ALPHA_MAX)
+
+
+def default_schedule(P, lam_target):
+    """From 0.9 ||A^T b||_inf down to lam_target (shrinkage.py:85-88)."""
+    start = 0.9 * _corr_max(P)
+    return ContinuationSchedule(max(start, lam_target), 0.5, lam_target)
+
+
+def objective_delta(x, cand, Ax, Acand, g, lam):
+    """F(cand) - F(x) as a difference of cached products (shrinkage.py:91-102)."""
+    step = np.asarray(cand) - np.asarray(x)
+    dA = np.asarray(Acand) - np.asarray(Ax)
+    return (float(g @ step) + 0.5 * float(dA @ dA)
+            + lam * float(np.sum(np.abs(cand) - np.abs(x))))
+
+
+def fista_t_next(t):
+    """(1 + sqrt(4t^2 + 1)) / 2 nudged so t'^2 - t' <= t^2 (shrinkage.py:184-196)."""
+    if not t >= 1.0:
+        raise ValueError("t must be at least 1")
+    tn = 0.5 * (1.0 + np.sqrt(4.0 * t * t + 1.0))
+    while tn * tn - tn > t * t:
+        tn = np.nextafter(tn, 1.0)
+    return tn
+
+
+def _corr_max(P):
+    A = P.A
+    if hasattr(A, "device_extension"):
+        D, s = A.device_extension()
+        return device._corr(D, D.view(ext=True, scale=s), P.b)[0]
+    D, _ = device.as_device_dictionary(A)
+    return device._corr(D, D.view(), P.b)[0]
+
+
+def _fista_opts(config, prep, probe_x0=None, L0=None, eta=None, lam=None):
+    O = _lib.FistaOpts()
+    O.L0 = float(config.opt("L0", 1.0)) if L0 is None else float(L0)
+    O.eta = float(config.opt("eta", 1.5)) if eta is None else float(eta)
+    O.beta = float(config.opt("beta", 0.5))
+    O.continuation = 1 if config.opt("continuation", True) else 0
+    O.exact_L = 1 if config.opt("exact_L", False) else 0
+    O.L_exact = 0.0
+    O.x0 = None
+    O.probe = 0
+    if probe_x0 is not None:
+        O.x0 = probe_x0.data_ptr()
+        O.probe = 1
+        O.continuation = 0
+        O.exact_L = 0
+    return O
+
+
+def _launcher(prep, O, bufs):
+    L = _lib.lib()
+
+    def launch(io):
+        return L.ell1_fista(byref(prep.view), device.ptr(prep.b), byref(prep.ctrl), byref(O),
+                            byref(io), prep.stream)
+    return launch
+
+
+def fista_solve(P, config, observer=None):
+    """Accelerated shrinkage with per-iteration lambda continuation.
+
+    Same contract as ell1.shrinkage.fista_solve (shrinkage.py:231-298):
+    options L0 (1.0), eta (1.5), beta (0.5), continuation (True), exact_L
+    (False); observer receives (FistaState, y, lambda) after every step;
+    config.stopping honoured.  Extra options: dtype ("float64"/"float32"
+    dictionary storage), device (CUDA ordinal).
+    """
+    prep = Prepared(P, config)
+    O = _fista_opts(config, prep)
+    if O.exact_L:
+        A = P.A
+        sn = A.norm_sq() if hasattr(A, "norm_sq") else prep.D.norm_sq()
+        O.L_exact = sn * (1.0 + 1e-9)
+    L = _lib.lib()
+    wsb = L.ell1_fista_workspace(byref(prep.view), byref(prep.ctrl), 0)
+    bufs = Buffers(prep, wsb, config.max_iter + 2, want_prev=observer is not None,
+                   want_y=observer is not None)
+    launch = _launcher(prep, O, bufs)
+
+    step = None
+    if observer is not None:
+        def step(st):
+            xp = host_vec(bufs.x_prev)
+            xc = host_vec(bufs.x)
+            y = host_vec(bufs.y)
+            observer(FistaState(xp, xc, float(st.scal[1]), float(st.scal[2]), float(st.scal[0])),
+                     y, float(st.scal[9]))
+    st = drive(launch, bufs, step)
+    raise_for(st.status, {_lib.BREAKDOWN: "backtracking exceeded 100 growth steps",
+                          _lib.LAMBDA_NONPOS: "lambda must be positive"})
+    x = host_vec(bufs.x)
+    trace = bufs.read_trace(st.ntrace)
+    return SolverResult(x, int(st.iterations), prep.elapsed(), bool(st.converged), trace)
+
+
+def backtrack_L(y, L_prev, eta, lam, P):
+    """Smallest L = eta^j L_prev whose quadratic model majorizes F at the prox
+    point (shrinkage.py:216-228); returns (L, x_next).  Runs the FISTA kernel
+    in probe mode: one backtracking search from y at fixed lambda."""
+    if not L_prev > 0:
+        raise ValueError("L_prev must be positive")
+    if not eta > 1:
+        raise ValueError("eta must exceed 1")
+    from paper_1007_3753_b200.model import SolverConfig
+    cfg = SolverConfig(lam=None, tol=1e-6, max_iter=1)
+    prep = Prepared(P, cfg)
+    prep.ctrl.lam = float(lam)
+    y = np.asarray(y, dtype=np.float64)
+    yd = device.to_device_vec(y, prep.n, prep.dev)
+    O = _fista_opts(cfg, prep, probe_x0=yd, L0=L_prev, eta=eta)
+    L = _lib.lib()
+    wsb = L.ell1_fista_workspace(byref(prep.view), byref(prep.ctrl), 0)
+    bufs = Buffers(prep, wsb, 3)
+    st = drive(_launcher(prep, O, bufs), bufs)
+    raise_for(st.status, {_lib.BREAKDOWN: "backtracking exceeded 100 growth steps"})
+    return float(st.scal[0]), host_vec(bufs.x)
+
+
+def ist_solve(P, schedule, config, observer=None):
+    """SpaRSA-style IST over a continuation schedule (shrinkage.py:105-181)."""
+    from paper_1007_3753_b200._ist import ist_solve_device
+    return ist_solve_device(P, schedule, config, observer)
