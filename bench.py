@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""Benchmark: l1-min solves/sec on BASELINE config 2 (d=1024, n=4096, k=128,
+1% noise, fp64, default lambda, relative-estimate 1e-6) with the B200 FISTA
+kernel; one step = one complete solve.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference]
+
+N>1 (torchrun): "replicas only" — config 2 is a single instance, so each rank
+solves its own seeded instance (weak scaling, no data-path collective);
+timing is the max over ranks of the CUDA-event totals.
+
+--impl reference times the reference algorithm's CPU implementation (the
+numpy/OpenBLAS oracle port, all host cores) on the same workload.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "l1-min solves/sec"
+UNIT = "solves/s"
+WORKLOAD = ("cfg2: single noisy BPDN instance d=1024 n=4096 k=128 sigma=0.01||Ax0||/sqrt(d), "
+            "FISTA, lambda=1e-2||A^T b||_inf, stop relative-estimate 1e-6")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--dtype", default="float64", choices=["float64", "float32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-stream", action="store_true", help="skip the HBM streaming roofline leg")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_instance(rank):
+    from paper_1007_3753_b200 import synth
+    w = synth.Workload("cfg2", 1024, 4096, 128, seed=rank, noise_rel=0.01)
+    return synth.make_problem(w)
+
+
+def config(dtype="float64"):
+    from paper_1007_3753_b200.model import SolverConfig, StoppingRule
+    return SolverConfig(lam=None, tol=1e-6, stopping=StoppingRule("relative-estimate", 1e-6),
+                        options={"dtype": dtype})
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        loaded = [v for v in sm if v > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- CPU legs
+def cpu_solve_once(P):
+    import oracle  # CPU baseline / reference arm only
+    return oracle.fista(P.A, P.b, lam=None, tol=1e-6, stop=("relative-estimate", 1e-6))
+
+
+def cpu_baseline(P, budget_s=10.0):
+    n = 0
+    t0 = time.perf_counter()
+    its = 0
+    while True:
+        r = cpu_solve_once(P)
+        its += r.iterations
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s and n >= 2:
+            break
+    return {"value": n / el, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": "%d full cfg2 FISTA solves (numpy/OpenBLAS oracle port of "
+                      "shrinkage.fista_solve, %d iterations total) in %.1f s" % (n, its, el),
+            "iterations_per_sec": its / el}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    P = make_instance(0)
+    for _ in range(args.warmup):
+        cpu_solve_once(P)
+    t0 = time.perf_counter()
+    its = 0
+    for _ in range(args.steps):
+        its += cpu_solve_once(P).iterations
+    el = time.perf_counter() - t0
+    v = args.steps / el
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded numpy PCG64, reference generator recipe)",
+           "config": {"workload": WORKLOAD, "parallelism": "host cores (OpenBLAS threads)"},
+           "iterations_per_sec": its / el,
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                            "sample": "%d full cfg2 FISTA solves" % args.steps},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ----------------------------------------------------------------- GPU legs
+def stream_roofline(torch, dev):
+    """FISTA on a larger-than-L2 dictionary (d=16384, n=65536, fp32 storage =
+    4 GiB) for 16 iterations: every panel pass streams A from HBM."""
+    from paper_1007_3753_b200 import device as dv
+    from paper_1007_3753_b200.model import SolverConfig
+    from paper_1007_3753_b200.shrinkage import FistaPlan
+    d, n, k = 16384, 65536, 512
+    g = torch.Generator(device=dev)
+    g.manual_seed(4)
+    A = torch.randn(d, n, device=dev, dtype=torch.float32, generator=g)
+    A /= torch.linalg.vector_norm(A, dim=0, keepdim=True)
+    x0 = torch.zeros(n, device=dev, dtype=torch.float32)
+    idx = torch.randperm(n, device=dev, generator=g)[:k]
+    x0[idx] = torch.randn(k, device=dev, generator=g)
+    b = (A @ x0).double()
+    D = dv.DeviceDictionary(A, dtype="float32", device=dev.index)
+    del A
+    torch.cuda.empty_cache()
+
+    class _P:
+        pass
+    P = _P()
+    P.A, P.b, P.ground_truth = D, b.cpu().numpy(), None
+    P.n, P.d = n, d
+    plan = FistaPlan(P, SolverConfig(lam=None, tol=1e-12, max_iter=16,
+                                     options={"continuation": False}))
+    plan.launch()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 3
+    tot = 0.0
+    passes = 0.0
+    for _ in range(reps):
+        s.record()
+        plan.launch()
+        e.record()
+        torch.cuda.synchronize()
+        tot += s.elapsed_time(e) / 1e3
+        passes += plan.passes()
+    bytes_ = passes * d * n * 4
+    st = plan.bufs.read_state()
+    del plan, D
+    torch.cuda.empty_cache()
+    return {"shape": "d=16384 n=65536 fp32 storage (4 GiB), 16 FISTA iterations, fixed lambda",
+            "achieved_gbs": bytes_ / tot / 1e9, "passes_per_launch": passes / reps,
+            "ms_per_launch": 1e3 * tot / reps, "iterations": int(st.iterations)}
+
+
+def run_b200(args):
+    import torch
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if ws > 1 else 0)
+    torch.cuda.set_device(dev)
+
+    from paper_1007_3753_b200 import device as dv
+    from paper_1007_3753_b200.model import ProblemInstance
+    from paper_1007_3753_b200.shrinkage import FistaPlan, fista_solve
+
+    P = make_instance(rank)
+    cfg = config(args.dtype)
+    D = dv.DeviceDictionary(P.A, dtype=args.dtype, device=dev.index)
+    Pd = ProblemInstance.__new__(ProblemInstance)
+    Pd.A, Pd.b, Pd.ground_truth, Pd.noise_sigma = D, P.b, P.ground_truth, P.noise_sigma
+    plan = FistaPlan(Pd, cfg)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # 512 MiB > L2
+
+    for _ in range(max(args.warmup, 3)):
+        plan.launch()
+    torch.cuda.synchronize()
+    res = plan.result()
+    iters = res.iterations
+    passes = plan.passes()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    for s, e in ev:
+        flush.zero_()                      # evict A from L2 between timed steps
+        s.record()
+        plan.launch()
+        e.record()
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    ck = clocks.stop()
+    tot = sum(s.elapsed_time(e) for s, e in ev) / 1e3
+    t = torch.tensor([tot], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    tmax = float(t.item())
+    value = ws * args.steps / tmax
+    ms = 1e3 * tmax / args.steps
+
+    # end to end through the public API: pinned host A, b -> solve -> host x
+    e2e_steps = max(1, min(args.steps, 5))
+    pin_A = torch.from_numpy(P.A).pin_memory()
+    pin_b = torch.from_numpy(P.b).pin_memory()
+    Ph = ProblemInstance(pin_A.numpy(), pin_b.numpy(), ground_truth=P.ground_truth)
+    fista_solve(Ph, cfg)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    es.record()
+    for _ in range(e2e_steps):
+        r = fista_solve(Ph, cfg)
+    ee.record()
+    torch.cuda.synchronize()
+    te = torch.tensor([es.elapsed_time(ee) / 1e3], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+    e2e_val = ws * e2e_steps / float(te.item())
+    h2d = P.A.nbytes + P.b.nbytes
+    d2h = P.n * 8 + 4 * 8 * r.iterations + 256
+
+    out = None
+    if rank == 0:
+        import oracle  # checker: parity of the timed solve
+        ref = cpu_solve_once(P)
+        err = float(np.linalg.norm(res.x_star - ref.x) / np.linalg.norm(ref.x))
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
+            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+        peak = float(peaks.get("hbm_gbs", 6650.0))
+        peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+        sz = 8 if args.dtype == "float64" else 4
+        alg_bytes = passes * P.d * P.n * sz
+        achieved = alg_bytes / (tmax / args.steps) / 1e9
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "ncu_fista_cfg2.json")
+        if os.path.exists(prof):
+            try:
+                traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            except ValueError:
+                traffic = None
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+               "dtype": "f64" if args.dtype == "float64" else "f32 storage / f64 accumulate",
+               "data": "synthetic (seeded numpy PCG64, reference generator recipe)",
+               "config": {"workload": WORKLOAD, "solver": "fista", "parallelism":
+                          "replicas only (one independent instance per rank)" if ws > 1 else "single GPU",
+                          "l2": "512 MiB buffer written between timed steps (A is 32 MiB)"},
+               "iterations_per_solve": iters,
+               "iterations_per_sec": value * iters,
+               "parity": {"rel_err_vs_oracle": err, "iterations_oracle": ref.iterations,
+                          "iterations_b200": iters},
+               "gpu_launches": args.steps,
+               "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                       "d2h_bytes_per_step": int(d2h),
+                       "api": "paper_1007_3753_b200.shrinkage.fista_solve(P, config), pinned host A/b"},
+               "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                            "frac": achieved / peak, "traffic": traffic,
+                            "kernel": "fista_kernel<%s> (whole solve = 1 launch)" % (
+                                "double" if sz == 8 else "float"),
+                            "algorithmic_bytes_per_launch": alg_bytes,
+                            "passes_per_launch": passes,
+                            "peak_source": peak_src,
+                            "note": "A (32 MiB) is L2-resident after the first pass of a solve; "
+                                    "see roofline_stream for the HBM-streaming case"},
+               "clocks": ck}
+        if not args.no_stream and ws == 1:
+            try:
+                rs = stream_roofline(torch, dev)
+                rs["frac"] = rs["achieved_gbs"] / peak
+                rs["peak"] = peak
+                out["roofline_stream"] = rs
+            except Exception as exc:  # pragma: no cover - best effort leg
+                out["roofline_stream"] = {"error": str(exc)[:200]}
+        if ws == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(P)
+    if ws > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

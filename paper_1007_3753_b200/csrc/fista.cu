@@ -31,7 +31,7 @@ struct FistaArgs {
 };
 
 // state scalar slots
-enum { S_L = 0, S_TP, S_TC, S_LAM, S_LAMBAR, S_FPREV, S_C0, S_BN, S_FY, S_LAMUSED };
+enum { S_L = 0, S_TP, S_TC, S_LAM, S_LAMBAR, S_FPREV, S_C0, S_BN, S_FY, S_LAMUSED, S_PASSES };
 // rotation slots
 enum { R_IX = 0, R_IXP, R_IXN, R_IGX, R_IGXP, R_IRX, R_IRXP, R_IRN };
 
@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(FistaArgs a) {
   int it = 0, hist = 0;
   int ix = 0, ixp = 1, ixn = 2, igx = 0, igxp = 1, irx = 0, irxp = 1, irn = 2;
   double L = 0, tp = 1, tc = 1, lam = 0, lam_bar = 0, Fprev = 0, fy = 0, lam_used = 0;
+  double passes = 0;   // dictionary panel passes (roofline accounting)
   bool done = false, conv = false;
   int status = ELL1_OK;
 
@@ -94,6 +95,7 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(FistaArgs a) {
     for_owned(E, D, [&](int64_t j) { a.G[1][j] = a.G[0][j]; });
     lam_bar = lam = C.lam;
     L = O.L0;
+    passes = 2;
     tp = tc = 1.0;
     fy = 0.5 * fq[0];
     phase = 1;
@@ -133,6 +135,7 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(FistaArgs a) {
       status = ELL1_ZERO_DATA; conv = true; done = true;
       return;
     }
+    passes = 1;
     lam_bar = (C.lam < 0.0) ? 1e-2 * c0 : C.lam;
     if (!(lam_bar > 0.0)) { status = ELL1_LAMBDA_NONPOS; done = true; return; }
     L = O.exact_L ? O.L_exact : O.L0;
@@ -148,6 +151,7 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(FistaArgs a) {
     irx = vs->rot[R_IRX]; irxp = vs->rot[R_IRXP]; irn = vs->rot[R_IRN];
     L = vs->scal[S_L]; tp = vs->scal[S_TP]; tc = vs->scal[S_TC]; lam = vs->scal[S_LAM];
     lam_bar = vs->scal[S_LAMBAR]; Fprev = vs->scal[S_FPREV]; fy = vs->scal[S_FY];
+    passes = vs->scal[S_PASSES];
   }
 
   {
@@ -195,6 +199,7 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(FistaArgs a) {
           const double* xs[1] = {xn};
           panel_gemv<TA, 1>(E, D, xs);
         }
+        passes += 1;
         if (!grid_sync(E)) { status = ELL1_ERR_TIMEOUT; return; }
         gather<7>(E, S, 1u << 3);
         double q[2] = {0.0, 0.0};
@@ -230,6 +235,7 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(FistaArgs a) {
         double* os[1] = {a.G[igx]};
         panel_gemv_t<TA, 1>(E, D, rs, os);            // g_x = A^T r_next  (shrinkage.py:285)
       }
+      passes += 1;
       if (D.ext) {
         for (int64_t i = E.r0 + E.tid; i < E.r1; i += NTHR) a.G[igx][D.n + i] = s_ext * a.R[irx][i];
         __syncthreads();
@@ -298,6 +304,7 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(FistaArgs a) {
     st->scal[S_L] = L; st->scal[S_TP] = tp; st->scal[S_TC] = tc; st->scal[S_LAM] = lam;
     st->scal[S_LAMBAR] = lam_bar; st->scal[S_FPREV] = Fprev; st->scal[S_FY] = fy;
     st->scal[S_LAMUSED] = lam_used;
+    st->scal[S_PASSES] = passes;
   }
 }
 
@@ -518,15 +525,10 @@ extern "C" int ell1_fista(const ell1_dict_t* D, const double* b, const ell1_ctrl
   cudaStream_t s = (cudaStream_t)stream;
   const size_t smem = smem_bytes(D->n, nb, 1, D->ld, 1);
   a.g.shcap = (int64_t)(smem / 8);
-  // fresh solve: zero the padding rows of the residual ring once
-  int phase = 0;
-  if (cudaMemcpyAsync(&phase, &io->state->phase, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess)
-    return ELL1_ERR_CUDA;
-  if (cudaStreamSynchronize(s) != cudaSuccess) return ELL1_ERR_CUDA;
-  if (phase == 0) {
+  // padding rows of the residual ring must read as zero (never written by the kernel)
+  if (D->ld > D->d)
     for (int k = 0; k < 3; ++k)
-      if (cudaMemsetAsync(a.R[k], 0, D->ld * 8, s) != cudaSuccess) return ELL1_ERR_CUDA;
-  }
+      if (cudaMemsetAsync(a.R[k] + D->d, 0, (D->ld - D->d) * 8, s) != cudaSuccess) return ELL1_ERR_CUDA;
   int rc = (D->dtype == ELL1_F64) ? coop_launch(fista_kernel<double>, nb, smem, s, a, a.g.bar)
                                   : coop_launch(fista_kernel<float>, nb, smem, s, a, a.g.bar);
   return rc;

@@ -132,6 +132,64 @@ def _launcher(prep, O, bufs):
     return launch
 
 
+class FistaPlan:
+    """A prepared FISTA solve: dictionary and b resident on the device,
+    workspace allocated.  ``launch()`` enqueues the whole solve (one kernel)
+    on the current stream without synchronising; ``result()`` reads it back.
+    fista_solve is FistaPlan(P, config).solve(observer)."""
+
+    def __init__(self, P, config):
+        self.config = config
+        self.prep = prep = Prepared(P, config)
+        self.O = O = _fista_opts(config, prep)
+        if O.exact_L:
+            A = P.A
+            sn = A.norm_sq() if hasattr(A, "norm_sq") else prep.D.norm_sq()
+            O.L_exact = sn * (1.0 + 1e-9)
+        L = _lib.lib()
+        self.ws_bytes = L.ell1_fista_workspace(byref(prep.view), byref(prep.ctrl), 0)
+        self.bufs = None
+        self._launch = None
+
+    def _alloc(self, observed):
+        if self.bufs is None or (observed and self.bufs.y is None):
+            self.bufs = Buffers(self.prep, self.ws_bytes, self.config.max_iter + 2,
+                                want_prev=observed, want_y=observed)
+            self._launch = _launcher(self.prep, self.O, self.bufs)
+
+    def launch(self):
+        self._alloc(False)
+        self.bufs.state.zero_()
+        _lib.check(self._launch(self.bufs.io(0)), "ell1_fista")
+
+    def result(self, st=None):
+        st = st if st is not None else self.bufs.read_state()
+        raise_for(st.status, {_lib.BREAKDOWN: "backtracking exceeded 100 growth steps",
+                              _lib.LAMBDA_NONPOS: "lambda must be positive"})
+        x = host_vec(self.bufs.x)
+        trace = self.bufs.read_trace(st.ntrace)
+        return SolverResult(x, int(st.iterations), self.prep.elapsed(), bool(st.converged), trace)
+
+    def passes(self):
+        """Dictionary panel passes of the last solve (roofline accounting)."""
+        return float(self.bufs.read_state().scal[10])
+
+    def solve(self, observer=None):
+        self._alloc(observer is not None)
+        self.bufs.state.zero_()
+        bufs = self.bufs
+        step = None
+        if observer is not None:
+            def step(st):
+                xp = host_vec(bufs.x_prev)
+                xc = host_vec(bufs.x)
+                y = host_vec(bufs.y)
+                observer(FistaState(xp, xc, float(st.scal[1]), float(st.scal[2]),
+                                    float(st.scal[0])), y, float(st.scal[9]))
+        st = drive(self._launch, bufs, step)
+        return self.result(st)
+
+
 def fista_solve(P, config, observer=None):
     """Accelerated shrinkage with per-iteration lambda continuation.
 
@@ -141,32 +199,7 @@ def fista_solve(P, config, observer=None):
     config.stopping honoured.  Extra options: dtype ("float64"/"float32"
     dictionary storage), device (CUDA ordinal).
     """
-    prep = Prepared(P, config)
-    O = _fista_opts(config, prep)
-    if O.exact_L:
-        A = P.A
-        sn = A.norm_sq() if hasattr(A, "norm_sq") else prep.D.norm_sq()
-        O.L_exact = sn * (1.0 + 1e-9)
-    L = _lib.lib()
-    wsb = L.ell1_fista_workspace(byref(prep.view), byref(prep.ctrl), 0)
-    bufs = Buffers(prep, wsb, config.max_iter + 2, want_prev=observer is not None,
-                   want_y=observer is not None)
-    launch = _launcher(prep, O, bufs)
-
-    step = None
-    if observer is not None:
-        def step(st):
-            xp = host_vec(bufs.x_prev)
-            xc = host_vec(bufs.x)
-            y = host_vec(bufs.y)
-            observer(FistaState(xp, xc, float(st.scal[1]), float(st.scal[2]), float(st.scal[0])),
-                     y, float(st.scal[9]))
-    st = drive(launch, bufs, step)
-    raise_for(st.status, {_lib.BREAKDOWN: "backtracking exceeded 100 growth steps",
-                          _lib.LAMBDA_NONPOS: "lambda must be positive"})
-    x = host_vec(bufs.x)
-    trace = bufs.read_trace(st.ntrace)
-    return SolverResult(x, int(st.iterations), prep.elapsed(), bool(st.converged), trace)
+    return FistaPlan(P, config).solve(observer)
 
 
 def backtrack_L(y, L_prev, eta, lam, P):
