@@ -171,20 +171,76 @@ __device__ __forceinline__ void gather(const Ctx& E, double (&out)[K], unsigned 
   __syncthreads();
 }
 
+// ------------------------------------------------------------------ panel source
+// Where a CTA reads its dictionary panel from: global memory (streamed through
+// L2 with ld.global.nc) or a copy resident in shared memory for the whole
+// launch (when the panel fits next to the scratch area).
+template <class TA, bool SM>
+struct Src {
+  const TA* p;      // column c0 of the panel; column j at p + (j - c0) * ld
+};
+
+template <class TA>
+struct VecOf { static constexpr int VW = 16 / (int)sizeof(TA); };
+
+// 16-byte load of VW consecutive rows, widened to double
+template <class TA, bool SM>
+__device__ __forceinline__ void ld16(const TA* p, double (&a)[VecOf<TA>::VW]) {
+  if constexpr (SM) {
+    const unsigned addr = (unsigned)__cvta_generic_to_shared(p);
+    if constexpr (sizeof(TA) == 8) {
+      double x, y;
+      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(addr));
+      a[0] = x; a[1] = y;
+    } else {
+      float x, y, z, w;
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(addr));
+      a[0] = x; a[1] = y; a[2] = z; a[3] = w;
+    }
+  } else {
+    if constexpr (sizeof(TA) == 8) {
+      const double2 t = __ldg(reinterpret_cast<const double2*>(p));
+      a[0] = t.x; a[1] = t.y;
+    } else {
+      const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+      a[0] = t.x; a[1] = t.y; a[2] = t.z; a[3] = t.w;
+    }
+  }
+}
+
+// Copy this CTA's panel (columns [c0, c1), contiguous in the column-major
+// layout) into shared memory.  Returns the smem source.
+template <class TA>
+__device__ Src<TA, true> load_panel(const Ctx& E, const DictV<TA>& D, TA* dst) {
+  const int64_t cnt = (E.c1 - E.c0) * D.ld;              // multiple of 32 elements
+  const int4* src = reinterpret_cast<const int4*>(D.A + E.c0 * D.ld);
+  int4* d4 = reinterpret_cast<int4*>(dst);
+  const int64_t n4 = cnt * (int64_t)sizeof(TA) / 16;
+  for (int64_t k = E.tid; k < n4; k += NTHR) d4[k] = __ldg(src + k);
+  __syncthreads();
+  return Src<TA, true>{dst};
+}
+
+template <class TA>
+__device__ __forceinline__ Src<TA, false> global_panel(const Ctx& E, const DictV<TA>& D) {
+  return Src<TA, false>{D.A + E.c0 * D.ld};
+}
+
 // ------------------------------------------------------------------ panel GEMV
 // part[b][v * ld + i] = sum_{j in panel} A[i, j] * xs[v][j]   (all rows, all v < NV)
-template <class TA, int NV>
-__device__ void panel_gemv(const Ctx& E, const DictV<TA>& D, const double* const (&xs)[NV]) {
-  constexpr int VW = 16 / (int)sizeof(TA);        // rows per vector load
+template <class TA, bool SM, int NV>
+__device__ void panel_gemv(const Ctx& E, const DictV<TA>& D, Src<TA, SM> S, const double* const (&xs)[NV]) {
+  constexpr int VW = VecOf<TA>::VW;
+  constexpr int U = SM ? 4 : 8;                    // columns per unrolled group (loads in flight)
   const int64_t w = E.c1 - E.c0;
   double* xsm = E.sh;                              // staged x panel: NV * w
+  __syncthreads();
   for (int64_t k = E.tid; k < w; k += NTHR) {
 #pragma unroll
     for (int v = 0; v < NV; ++v) xsm[v * w + k] = ldcg(xs[v] + E.c0 + k);
   }
   __syncthreads();
   const int64_t nvec = D.ld / VW;                  // row-vectors per column
-  const TA* base = D.A + E.c0 * D.ld;
   double* out = E.part + (size_t)E.b * E.pstride;
   for (int64_t q = E.tid; q < nvec; q += NTHR) {
     double acc[NV][VW];
@@ -192,43 +248,29 @@ __device__ void panel_gemv(const Ctx& E, const DictV<TA>& D, const double* const
     for (int v = 0; v < NV; ++v)
 #pragma unroll
       for (int e = 0; e < VW; ++e) acc[v][e] = 0.0;
-    const TA* p = base + q * VW;
+    const TA* p = S.p + q * VW;
     int64_t j = 0;
-    for (; j + 4 <= w; j += 4) {
-      TA a[4][VW];
+    for (; j + U <= w; j += U) {
+      double a[U][VW];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if constexpr (sizeof(TA) == 8) {
-          const double2 t = __ldg(reinterpret_cast<const double2*>(p + (j + u) * D.ld));
-          a[u][0] = t.x; a[u][1] = t.y;
-        } else {
-          const float4 t = __ldg(reinterpret_cast<const float4*>(p + (j + u) * D.ld));
-          a[u][0] = t.x; a[u][1] = t.y; a[u][2] = t.z; a[u][3] = t.w;
-        }
-      }
+      for (int u = 0; u < U; ++u) ld16<TA, SM>(p + (j + u) * D.ld, a[u]);
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
           const double xv = xsm[v * w + j + u];
 #pragma unroll
-          for (int e = 0; e < VW; ++e) acc[v][e] = fma((double)a[u][e], xv, acc[v][e]);
+          for (int e = 0; e < VW; ++e) acc[v][e] = fma(a[u][e], xv, acc[v][e]);
         }
     }
     for (; j < w; ++j) {
-      TA a[VW];
-      if constexpr (sizeof(TA) == 8) {
-        const double2 t = __ldg(reinterpret_cast<const double2*>(p + j * D.ld));
-        a[0] = t.x; a[1] = t.y;
-      } else {
-        const float4 t = __ldg(reinterpret_cast<const float4*>(p + j * D.ld));
-        a[0] = t.x; a[1] = t.y; a[2] = t.z; a[3] = t.w;
-      }
+      double a[VW];
+      ld16<TA, SM>(p + j * D.ld, a);
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         const double xv = xsm[v * w + j];
 #pragma unroll
-        for (int e = 0; e < VW; ++e) acc[v][e] = fma((double)a[e], xv, acc[v][e]);
+        for (int e = 0; e < VW; ++e) acc[v][e] = fma(a[e], xv, acc[v][e]);
       }
     }
 #pragma unroll
@@ -241,79 +283,80 @@ __device__ void panel_gemv(const Ctx& E, const DictV<TA>& D, const double* const
 
 // ------------------------------------------------------------------ panel GEMV^T
 // outs[v][j] = sum_i A[i, j] * rs[v][i] for j in the panel (A-columns only).
-// rs are replicated d-vectors written during this launch; staged through
-// shared memory when they fit, else read through L2 (ld.global.cg).
-template <class TA, int NV>
-__device__ void panel_gemv_t(const Ctx& E, const DictV<TA>& D, const double* const (&rs)[NV],
-                             double* const (&outs)[NV]) {
-  constexpr int VW = 16 / (int)sizeof(TA);
+// Work unit = (column, row segment); segments balance narrow panels over the
+// 16 warps and are summed in a fixed order.  rs are replicated d-vectors
+// written during this launch; they are read through L1 after the grid
+// barrier's fence (which invalidates L1).
+template <class TA, bool SM, int NV>
+__device__ void panel_gemv_t(const Ctx& E, const DictV<TA>& D, Src<TA, SM> S,
+                             const double* const (&rs)[NV], double* const (&outs)[NV]) {
+  constexpr int VW = VecOf<TA>::VW;
+  const int64_t w = E.c1 - E.c0;
   const int64_t nvec = D.ld / VW;
-  const bool staged = (int64_t)NV * D.ld <= E.shcap;
-  const double* rv[NV];
-  if (staged) {
-    for (int64_t i = E.tid; i < D.ld; i += NTHR) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v) E.sh[v * D.ld + i] = ldcg(rs[v] + i);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int v = 0; v < NV; ++v) rv[v] = E.sh + v * D.ld;
-  } else {
-#pragma unroll
-    for (int v = 0; v < NV; ++v) rv[v] = rs[v];
-  }
-  for (int64_t j = E.c0 + E.warp; j < E.c1; j += NWARP) {
-    const TA* col = D.A + j * D.ld;
+  int64_t seg = (2 * NWARP + w - 1) / (w > 0 ? w : 1);
+  const int64_t maxseg = nvec / 32 > 0 ? nvec / 32 : 1;
+  if (seg > maxseg) seg = maxseg;
+  if (seg < 1) seg = 1;
+  if (seg * w * NV > E.shcap) seg = 1;
+  const int64_t seglen = (nvec + seg - 1) / seg;
+  const int64_t units = w * seg;
+  double* stage = E.sh;
+  __syncthreads();
+  for (int64_t u = E.warp; u < units; u += NWARP) {
+    const int64_t jl = u / seg, sg = u - jl * seg;
+    const TA* col = S.p + jl * D.ld;
+    const int64_t q0 = sg * seglen;
+    const int64_t q1 = min(nvec, q0 + seglen);
     double acc[NV][2];
 #pragma unroll
     for (int v = 0; v < NV; ++v) acc[v][0] = acc[v][1] = 0.0;
-    int64_t q = E.lane;
-    for (; q + 96 < nvec; q += 128) {
-      TA a[4][VW];
+    int64_t q = q0 + E.lane;
+    for (; q + 96 < q1; q += 128) {
+      double a[4][VW];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if constexpr (sizeof(TA) == 8) {
-          const double2 t = __ldg(reinterpret_cast<const double2*>(col) + q + 32 * u);
-          a[u][0] = t.x; a[u][1] = t.y;
-        } else {
-          const float4 t = __ldg(reinterpret_cast<const float4*>(col) + q + 32 * u);
-          a[u][0] = t.x; a[u][1] = t.y; a[u][2] = t.z; a[u][3] = t.w;
+      for (int k = 0; k < 4; ++k) ld16<TA, SM>(col + (q + 32 * k) * VW, a[k]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const double* rv = rs[v] + (q + 32 * k) * VW;
+#pragma unroll
+          for (int e = 0; e < VW; ++e) acc[v][k & 1] = fma(a[k][e], rv[e], acc[v][k & 1]);
         }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < NV; ++v)
-#pragma unroll
-          for (int e = 0; e < VW; ++e) {
-            const double r = staged ? rv[v][(q + 32 * u) * VW + e] : ldcg(rv[v] + (q + 32 * u) * VW + e);
-            acc[v][u & 1] = fma((double)a[u][e], r, acc[v][u & 1]);
-          }
     }
-    for (; q < nvec; q += 32) {
-      TA a[VW];
-      if constexpr (sizeof(TA) == 8) {
-        const double2 t = __ldg(reinterpret_cast<const double2*>(col) + q);
-        a[0] = t.x; a[1] = t.y;
-      } else {
-        const float4 t = __ldg(reinterpret_cast<const float4*>(col) + q);
-        a[0] = t.x; a[1] = t.y; a[2] = t.z; a[3] = t.w;
+    for (; q < q1; q += 32) {
+      double a[VW];
+      ld16<TA, SM>(col + q * VW, a);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const double* rv = rs[v] + q * VW;
+#pragma unroll
+        for (int e = 0; e < VW; ++e) acc[v][0] = fma(a[e], rv[e], acc[v][0]);
       }
-#pragma unroll
-      for (int v = 0; v < NV; ++v)
-#pragma unroll
-        for (int e = 0; e < VW; ++e) {
-          const double r = staged ? rv[v][q * VW + e] : ldcg(rv[v] + q * VW + e);
-          acc[v][0] = fma((double)a[e], r, acc[v][0]);
-        }
     }
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       const double s = warp_sum(acc[v][0] + acc[v][1]);
-      if (E.lane == 0) outs[v][j] = s;
+      if (E.lane == 0) {
+        if (seg == 1) outs[v][E.c0 + jl] = s;
+        else stage[(v * w + jl) * seg + sg] = s;
+      }
     }
   }
   __syncthreads();
+  if (seg > 1) {
+    for (int64_t t = E.tid; t < w * NV; t += NTHR) {
+      const int v = (int)(t / w);
+      const int64_t jl = t - (int64_t)v * w;
+      const double* st = stage + (v * w + jl) * seg;
+      double s = st[0];
+      for (int64_t k = 1; k < seg; ++k) s += st[k];
+#pragma unroll
+      for (int vv = 0; vv < NV; ++vv)
+        if (vv == v) outs[vv][E.c0 + jl] = s;
+    }
+    __syncthreads();
+  }
 }
 
 // ------------------------------------------------------------------ slice reduction
@@ -322,10 +365,11 @@ __device__ void panel_gemv_t(const Ctx& E, const DictV<TA>& D, const double* con
 // then f(i, sums) runs once per row (thread-parallel over rows).
 template <int NV, class F>
 __device__ void slice_reduce(const Ctx& E, int64_t ld, F&& f) {
-  constexpr int CH = 256;                          // rows per chunk (NV*CH doubles of smem)
+  int64_t CH = E.shcap / NV;                        // rows per chunk (NV*CH doubles of smem)
+  if (CH > 256) CH = 256;
   double* stage = E.sh;
   for (int64_t base = E.r0; base < E.r1; base += CH) {
-    const int rows = (int)min((int64_t)CH, E.r1 - base);
+    const int rows = (int)min(CH, E.r1 - base);
     const int items = rows * NV;
     for (int it = E.warp; it < items; it += NWARP) {
       const int v = it / rows, rr = it - v * rows;
@@ -356,13 +400,13 @@ __device__ __forceinline__ void for_owned(const Ctx& E, const DictV<TA>& D, F&& 
     for (int64_t i = E.r0 + E.tid; i < E.r1; i += NTHR) f(D.n + i);
 }
 
-// shared-memory doubles the engine needs for a given dictionary
-__host__ __device__ inline int64_t engine_smem_doubles(int64_t n, int nb, int nv) {
+// shared-memory scratch (doubles) the engine needs next to an optional panel
+__host__ __device__ inline int64_t engine_scratch_doubles(int64_t n, int nb, int nv, int kmax) {
   const int64_t w = (n + nb - 1) / nb + 1;
-  int64_t s = w * nv;
-  if (s < 256 * 4) s = 256 * 4;             // slice staging (CH * NV)
-  if (s < NWARP * 16 + 16) s = NWARP * 16 + 16;
-  return s;
+  int64_t s = w * nv * 2;                   // x staging / GEMV^T segment partials (>= 2 segs)
+  if (s < 64 * nv) s = 64 * nv;             // slice staging
+  if (s < NWARP * kmax + kmax) s = NWARP * kmax + kmax;   // block reductions of kmax scalars
+  return (s + 31) / 32 * 32;
 }
 
 }  // namespace ell1

@@ -35,13 +35,20 @@ enum { S_L = 0, S_TP, S_TC, S_LAM, S_LAMBAR, S_FPREV, S_C0, S_BN, S_FY, S_LAMUSE
 // rotation slots
 enum { R_IX = 0, R_IXP, R_IXN, R_IGX, R_IGXP, R_IRX, R_IRXP, R_IRN };
 
-template <class TA>
+template <class TA, bool SM>
 __global__ void __launch_bounds__(NTHR, 1) fista_kernel(FistaArgs a) {
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
   Ctx E;
   const DictV<TA> D = dict_view<TA>(a.D);
   ctx_init(E, D.d, D.n);
   ctx_bind(E, a.g, smem);
+  Src<TA, SM> PS;
+  if constexpr (SM) {
+    PS = load_panel<TA>(E, D, reinterpret_cast<TA*>(smem));
+    E.sh = smem + a.g.panel_bytes / 8;
+  } else {
+    PS = global_panel<TA>(E, D);
+  }
   const int64_t N = D.ncols();
   ell1_state_t* st = a.st;
   const double* b = a.b;
@@ -68,7 +75,7 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(FistaArgs a) {
     __syncthreads();
     {
       const double* xs[1] = {a.X[0]};
-      panel_gemv<TA, 1>(E, D, xs);
+      panel_gemv<TA, SM, 1>(E, D, PS, xs);
     }
     if (!grid_sync(E)) { status = ELL1_ERR_TIMEOUT; return; }
     double q[1] = {0.0};
@@ -87,7 +94,7 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(FistaArgs a) {
     {
       const double* rs[1] = {a.R[0]};
       double* os[1] = {a.G[0]};
-      panel_gemv_t<TA, 1>(E, D, rs, os);
+      panel_gemv_t<TA, SM, 1>(E, D, PS, rs, os);
     }
     if (D.ext)
       for (int64_t i = E.r0 + E.tid; i < E.r1; i += NTHR) a.G[0][D.n + i] = s_ext * a.R[0][i];
@@ -104,7 +111,7 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(FistaArgs a) {
     {
       const double* rs[1] = {b};
       double* os[1] = {a.G[0]};
-      panel_gemv_t<TA, 1>(E, D, rs, os);
+      panel_gemv_t<TA, SM, 1>(E, D, PS, rs, os);
     }
     double v[2] = {0.0, 0.0};   // max|c|, sum b^2 (slice)
     for_owned(E, D, [&](int64_t j) {
@@ -197,7 +204,7 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(FistaArgs a) {
         {
           __syncthreads();
           const double* xs[1] = {xn};
-          panel_gemv<TA, 1>(E, D, xs);
+          panel_gemv<TA, SM, 1>(E, D, PS, xs);
         }
         passes += 1;
         if (!grid_sync(E)) { status = ELL1_ERR_TIMEOUT; return; }
@@ -233,7 +240,7 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(FistaArgs a) {
       {
         const double* rs[1] = {a.R[irx]};
         double* os[1] = {a.G[igx]};
-        panel_gemv_t<TA, 1>(E, D, rs, os);            // g_x = A^T r_next  (shrinkage.py:285)
+        panel_gemv_t<TA, SM, 1>(E, D, PS, rs, os);            // g_x = A^T r_next  (shrinkage.py:285)
       }
       passes += 1;
       if (D.ext) {
@@ -328,7 +335,7 @@ __global__ void __launch_bounds__(NTHR, 1) corr_kernel(CorrArgs a) {
   {
     const double* rs[1] = {a.b};
     double* os[1] = {a.tmp};
-    panel_gemv_t<TA, 1>(E, D, rs, os);
+    panel_gemv_t<TA, false, 1>(E, D, global_panel<TA>(E, D), rs, os);
   }
   double v[2] = {0.0, 0.0};
   for_owned(E, D, [&](int64_t j) {
@@ -386,9 +393,9 @@ __global__ void __launch_bounds__(NTHR, 1) power_kernel(PowerArgs a) {
       {
         const double* rs[1] = {v};
         double* os[1] = {a.U};
-        panel_gemv_t<TA, 1>(E, D, rs, os);           // u = A^T v
+        panel_gemv_t<TA, false, 1>(E, D, global_panel<TA>(E, D), rs, os);           // u = A^T v
         const double* xs[1] = {a.U};
-        panel_gemv<TA, 1>(E, D, xs);                 // partial A u
+        panel_gemv<TA, false, 1>(E, D, global_panel<TA>(E, D), xs);                 // partial A u
       }
       if (!grid_sync(E)) return;
       double q[2] = {0.0, 0.0};
@@ -425,7 +432,7 @@ __global__ void __launch_bounds__(NTHR, 1) power_kernel(PowerArgs a) {
     } else {
       {
         const double* xs[1] = {v};
-        panel_gemv<TA, 1>(E, D, xs);                 // partial A v
+        panel_gemv<TA, false, 1>(E, D, global_panel<TA>(E, D), xs);                 // partial A v
       }
       if (!grid_sync(E)) return;
       slice_reduce<1>(E, D.ld, [&](int64_t i, const double* sums) { a.W[i] = sums[0]; });
@@ -433,7 +440,7 @@ __global__ void __launch_bounds__(NTHR, 1) power_kernel(PowerArgs a) {
       {
         const double* rs[1] = {a.W};
         double* os[1] = {a.U};
-        panel_gemv_t<TA, 1>(E, D, rs, os);           // w = A^T A v (panel)
+        panel_gemv_t<TA, false, 1>(E, D, global_panel<TA>(E, D), rs, os);           // w = A^T A v (panel)
       }
       double q[2] = {0.0, 0.0};
       for (int64_t j = E.c0 + E.tid; j < E.c1; j += NTHR) {
@@ -523,14 +530,20 @@ extern "C" int ell1_fista(const ell1_dict_t* D, const double* b, const ell1_ctrl
   a.x_out = io->x; a.xprev_out = io->x_prev; a.y_out = io->y;
   a.max_steps = io->max_steps;
   cudaStream_t s = (cudaStream_t)stream;
-  const size_t smem = smem_bytes(D->n, nb, 1, D->ld, 1);
-  a.g.shcap = (int64_t)(smem / 8);
+  const SmemPlan sp = plan_smem(a.D, nb, 1, io->max_steps <= 0, 7);
+  a.g.shcap = sp.scratch;
+  a.g.panel_bytes = sp.panel_bytes;
   // padding rows of the residual ring must read as zero (never written by the kernel)
   if (D->ld > D->d)
     for (int k = 0; k < 3; ++k)
       if (cudaMemsetAsync(a.R[k] + D->d, 0, (D->ld - D->d) * 8, s) != cudaSuccess) return ELL1_ERR_CUDA;
-  int rc = (D->dtype == ELL1_F64) ? coop_launch(fista_kernel<double>, nb, smem, s, a, a.g.bar)
-                                  : coop_launch(fista_kernel<float>, nb, smem, s, a, a.g.bar);
+  int rc;
+  if (D->dtype == ELL1_F64)
+    rc = sp.resident ? coop_launch(fista_kernel<double, true>, nb, sp.bytes, s, a, a.g.bar)
+                     : coop_launch(fista_kernel<double, false>, nb, sp.bytes, s, a, a.g.bar);
+  else
+    rc = sp.resident ? coop_launch(fista_kernel<float, true>, nb, sp.bytes, s, a, a.g.bar)
+                     : coop_launch(fista_kernel<float, false>, nb, sp.bytes, s, a, a.g.bar);
   return rc;
 }
 
@@ -552,8 +565,10 @@ extern "C" int ell1_correlation_max(const ell1_dict_t* D, const double* b, doubl
   if (!carve_grid(cv, a.g, nb, 32)) return ELL1_ERR_ARG;
   a.tmp = cv.take<double>(ncols_of(D));
   if (!cv.ok) return ELL1_ERR_ARG;
-  const size_t smem = smem_bytes(D->n, nb, 1, D->ld, 1);
-  a.g.shcap = (int64_t)(smem / 8);
+  const SmemPlan sp = plan_smem(a.D, nb, 1, false);
+  const size_t smem = sp.bytes;
+  a.g.shcap = sp.scratch;
+  a.g.panel_bytes = 0;
   cudaStream_t s = (cudaStream_t)stream;
   return (D->dtype == ELL1_F64) ? coop_launch(corr_kernel<double>, nb, smem, s, a, a.g.bar)
                                 : coop_launch(corr_kernel<float>, nb, smem, s, a, a.g.bar);
@@ -587,8 +602,10 @@ extern "C" int ell1_spectral_norm_sq(const ell1_dict_t* D, const double* v0, int
   if (cudaMemsetAsync(a.V[0], 0, m * 8, s) != cudaSuccess) return ELL1_ERR_CUDA;
   if (cudaMemsetAsync(a.V[1], 0, m * 8, s) != cudaSuccess) return ELL1_ERR_CUDA;
   if (cudaMemsetAsync(a.W, 0, m * 8, s) != cudaSuccess) return ELL1_ERR_CUDA;
-  const size_t smem = smem_bytes(D->n, nb, 1, D->ld, 1);
-  a.g.shcap = (int64_t)(smem / 8);
+  const SmemPlan sp = plan_smem(a.D, nb, 1, false);
+  const size_t smem = sp.bytes;
+  a.g.shcap = sp.scratch;
+  a.g.panel_bytes = 0;
   return (D->dtype == ELL1_F64) ? coop_launch(power_kernel<double>, nb, smem, s, a, a.g.bar)
                                 : coop_launch(power_kernel<float>, nb, smem, s, a, a.g.bar);
 }

@@ -20,7 +20,8 @@ struct GridBufs {
   double* scal;               // [2][nb][SCAL]
   unsigned long long* bar;
   int* abort;
-  int64_t shcap;              // shared-memory doubles per CTA
+  int64_t shcap;              // shared-memory scratch doubles per CTA
+  size_t panel_bytes;         // resident dictionary panel bytes (0: streamed)
 };
 
 template <class TA>
@@ -145,11 +146,43 @@ inline int coop_launch(K kernel, int nb, size_t smem, cudaStream_t s, Arg& arg, 
   return ELL1_OK;
 }
 
-inline size_t smem_bytes(int64_t n_cols, int nb, int nv, int64_t ld, int nv_t) {
-  int64_t s = engine_smem_doubles(n_cols, nb, nv);
-  int64_t want = ld * nv_t;                       // stage d-vectors for D^T r when they fit
-  if (want * 8 <= 160 * 1024 && want > s) s = want;
-  return (size_t)s * 8;
+// Shared-memory plan for a persistent solver: optionally the CTA's dictionary
+// panel (resident for the whole launch) followed by the engine scratch.
+struct SmemPlan {
+  bool resident;
+  size_t panel_bytes;
+  size_t bytes;          // total dynamic smem
+  int64_t scratch;       // scratch doubles
+};
+
+inline int max_smem_optin() {
+  int dev = 0, v = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) v = 48 * 1024;
+  return v - 128;      // static __shared__ (grid_sync flag) + slack
+}
+
+inline SmemPlan plan_smem(const DictRaw& D, int nb, int nv, bool allow_resident = true, int kmax = 16) {
+  SmemPlan p;
+  const int64_t w = (D.n + nb - 1) / nb;
+  const int64_t esz = D.dtype == ELL1_F64 ? 8 : 4;
+  const int64_t scratch_min = engine_scratch_doubles(D.n, nb, nv, kmax);
+  p.panel_bytes = (size_t)align_up(w * D.ld * esz, 128);
+  const int64_t cap = max_smem_optin();
+  if (allow_resident && (int64_t)p.panel_bytes + scratch_min * 8 <= cap) {
+    p.resident = true;
+    int64_t room = (cap - (int64_t)p.panel_bytes) / 8;
+    int64_t want = scratch_min > 2048 ? scratch_min : 2048;
+    p.scratch = (room < want ? room : want) / 32 * 32;
+  } else {
+    p.resident = false;
+    p.panel_bytes = 0;
+    int64_t want = scratch_min;
+    if (want < 4096) want = 4096;
+    p.scratch = want;
+  }
+  p.bytes = p.panel_bytes + (size_t)p.scratch * 8;
+  return p;
 }
 
 }  // namespace ell1
