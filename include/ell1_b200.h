@@ -106,6 +106,7 @@ typedef struct {
   double* y;           /* n(+d): extrapolated point (observer payload) or NULL */
   int32_t max_steps;   /* iterations this launch may take (<= 0: unlimited); resumable */
   int32_t blocks;      /* persistent grid size (0: one CTA per SM) */
+  unsigned long long* phase_ns;  /* optional diagnostics: [blocks][16] per-phase ns (NULL: off) */
 } ell1_io_t;
 
 /* ---------------------------------------------------------------- setup */

@@ -54,7 +54,8 @@ class IO(ctypes.Structure):
     _fields_ = [("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
                 ("state", ctypes.c_void_p), ("trace", ctypes.c_void_p),
                 ("x", ctypes.c_void_p), ("x_prev", ctypes.c_void_p), ("y", ctypes.c_void_p),
-                ("max_steps", ctypes.c_int32), ("blocks", ctypes.c_int32)]
+                ("max_steps", ctypes.c_int32), ("blocks", ctypes.c_int32),
+                ("phase_ns", ctypes.c_void_p)]
 
 
 assert ctypes.sizeof(State) == 256, ctypes.sizeof(State)

@@ -2,14 +2,18 @@
 //
 // Execution model: one cooperative launch runs a whole solve.
 // Each CTA owns
-//   * a contiguous panel of dictionary columns  [c0, c1)   (n-side vectors x, y, g ...)
+//   * a contiguous panel of dictionary columns  [c0, c1)   (w = c1 - c0)
 //   * a contiguous slice of rows                 [r0, r1)   (d-side reductions)
 //   * for the [A, sI] extension, the identity columns n + [r0, r1).
-// A matvec D v is computed as per-CTA partial d-vectors (panel GEMV) that are
-// reduced slice-by-slice after a grid barrier; D^T r is local to each panel.
-// Every scalar decision (backtracking accept, step sizes, stop rules) is
-// computed redundantly and bit-identically by all CTAs from deterministic
-// fixed-order reductions, so control flow needs no broadcast.
+// Owned n-side vectors (x, g, ...) live in SHARED memory, indexed by a local
+// column index k in [0, W): k < w is dictionary column c0 + k, k >= w is the
+// identity column n + r0 + (k - w).  The first `rc` panel columns are
+// resident in shared memory for the whole launch, the rest are streamed
+// from global memory (L2 / HBM).
+// D v is computed as per-CTA partial d-vectors (panel GEMV) reduced
+// slice-by-slice after a grid barrier; D^T r is local to each panel.
+// Every scalar decision is computed redundantly and bit-identically by all
+// CTAs from deterministic fixed-order reductions — no broadcast needed.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -30,11 +34,12 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
 // NaN-propagating max (np.max semantics)
-__device__ __forceinline__ double nmax(double a, double b) {
-  return (a > b || a != a) ? a : b;
-}
+__device__ __forceinline__ double nmax(double a, double b) { return (a > b || a != a) ? a : b; }
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -51,17 +56,21 @@ __device__ __forceinline__ double warp_max(double v) {
 template <class TA>
 struct DictV {
   const TA* A;
-  int64_t d, n, ld;   // ld == padded row count (dpad)
+  int64_t d, n, ld;   // ld == padded row count
   int ext;
   double s;
-  __device__ __forceinline__ int64_t ncols() const { return n + (ext ? d : 0); }
 };
 
+template <class TA>
+struct VecOf { static constexpr int VW = 16 / (int)sizeof(TA); };
+
 // ------------------------------------------------------------------ grid context
-struct Ctx {
-  int nb, b, tid, lane, warp;
+struct Ctx {            // lives in shared memory; written by thread 0 only
+  int nb, b;
+  int ok;             // result of the last grid barrier
   int64_t c0, c1;     // owned dictionary-column panel
   int64_t r0, r1;     // owned row slice
+  int w, W;           // panel width, owned local columns (w + slice for ext)
   unsigned long long* bar;
   int* abort;
   unsigned long long epoch;
@@ -71,65 +80,123 @@ struct Ctx {
   double* scal;       // [2][nb][SCAL]
   double* sh;         // shared scratch
   int64_t shcap;      // its capacity in doubles
+  unsigned long long* prof;   // optional per-CTA phase timers [nb][16]
+  unsigned long long tmark;
 };
 
-__device__ __forceinline__ void ctx_init(Ctx& E, int64_t d, int64_t n) {
+__device__ __forceinline__ int tix() { return (int)threadIdx.x; }
+__device__ __forceinline__ int lnx() { return (int)(threadIdx.x & 31); }
+__device__ __forceinline__ int wpx() { return (int)(threadIdx.x >> 5); }
+
+// thread 0 only (Ctx is a __shared__ object); callers __syncthreads afterwards
+__device__ __forceinline__ void ctx_init(Ctx& E, int64_t d, int64_t n, int ext) {
   E.nb = gridDim.x;
   E.b = blockIdx.x;
-  E.tid = threadIdx.x;
-  E.lane = threadIdx.x & 31;
-  E.warp = threadIdx.x >> 5;
+  E.ok = 1;
   E.c0 = (n * E.b) / E.nb;
   E.c1 = (n * (E.b + 1)) / E.nb;
   E.r0 = (d * E.b) / E.nb;
   E.r1 = (d * (E.b + 1)) / E.nb;
+  E.w = (int)(E.c1 - E.c0);
+  E.W = E.w + (ext ? (int)(E.r1 - E.r0) : 0);
   E.epoch = 0;
   E.nbar = 0;
+  E.prof = nullptr;
+  E.tmark = 0;
 }
 
-// Software grid barrier (sense-free monotone counter).  Returns false when a
-// peer CTA aborted or the wait timed out; callers then unwind cleanly.
+// global column index of local owned column k
+__device__ __forceinline__ int64_t gcol(const Ctx& E, int64_t n, int k) {
+  return k < E.w ? E.c0 + k : n + E.r0 + (k - E.w);
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// accumulate the time since the previous mark into phase k (thread 0 of each CTA)
+__device__ __forceinline__ void mark(Ctx& E, int k) {
+  if (E.prof != nullptr && tix() == 0) {
+    const unsigned long long t = gtimer();
+    if (k >= 0) E.prof[(size_t)E.b * 16 + k] += t - E.tmark;
+    E.tmark = t;
+  }
+}
+
+// Software grid barrier: release-add on a monotone counter, acquire-poll
+// until every CTA of this epoch arrived.  The acquire load orders (and
+// invalidates L1 for) everything read after the barrier.  Returns false
+// when a peer aborted or the wait timed out; callers unwind cleanly.
 __device__ bool grid_sync(Ctx& E) {
-  __shared__ int s_ok;
   __syncthreads();
-  E.epoch += (unsigned long long)E.nb;
-  E.nbar++;
-  if (E.tid == 0) {
-    __threadfence();
-    atomicAdd(E.bar, 1ULL);
+  if (tix() == 0) {
+    E.epoch += (unsigned long long)E.nb;
+    E.nbar++;
+    red_release_add(E.bar, 1ULL);        // MEMBAR.ALL.GPU + REDG: publishes the CTA's writes
     long long spins = 0;
     int ok = 1;
-    while (ld_acquire(E.bar) < E.epoch) {
-      if (((++spins) & 255) == 0) {
+    const unsigned long long target = E.epoch;
+    while (ld_acquire(E.bar) < target) {  // each acquire poll is LDG.STRONG.GPU + CCTL.IVALL
+      if (((++spins) & 1023) == 0) {
         if (*(volatile int*)E.abort) { ok = 0; break; }
         if (spins > SPIN_LIMIT) { atomicExch(E.abort, 1); ok = 0; break; }
-        __nanosleep(64);
       }
     }
-    __threadfence();
-    s_ok = ok;
+    E.ok = ok;
   }
   __syncthreads();
-  return s_ok != 0;
+  return E.ok != 0;
 }
 
 // ------------------------------------------------------------------ block reductions
 // K values reduced across the CTA in a fixed order; every thread gets the result.
+// Warp stage: a transpose-reduction over P = pow2 >= K slots costs
+// (P - 1) + (5 - log2 P) shuffles instead of 5K (shuffle throughput is the
+// limit with 16 warps); lane 4v.. then holds value v (P = 8).
 template <int K>
 __device__ __forceinline__ void block_reduce(const Ctx& E, double (&v)[K], unsigned maxmask) {
+  constexpr int P = K <= 1 ? 1 : K <= 2 ? 2 : K <= 4 ? 4 : K <= 8 ? 8 : 16;
+  constexpr int LOGP = P == 1 ? 0 : P == 2 ? 1 : P == 4 ? 2 : P == 8 ? 3 : 4;
+  static_assert(K <= 16, "block_reduce supports up to 16 values");
+  double p[P];
 #pragma unroll
-  for (int k = 0; k < K; ++k) v[k] = ((maxmask >> k) & 1u) ? warp_max(v[k]) : warp_sum(v[k]);
-  double* sh = E.sh;
-  if (E.lane == 0) {
+  for (int k = 0; k < P; ++k) p[k] = k < K ? v[k] : (((maxmask >> k) & 1u) ? -INFINITY : 0.0);
+  const int l = lnx();
+  int base = 0;                                  // value index held in slot 0
 #pragma unroll
-    for (int k = 0; k < K; ++k) sh[E.warp * K + k] = v[k];
+  for (int r = 0; r < LOGP; ++r) {
+    const int o = 16 >> r;                       // lane offset of this round
+    const int h = P >> (r + 1);                  // slots kept after the round
+    const bool upper = (l & o) != 0;
+    if (upper) base += h;
+#pragma unroll
+    for (int u = 0; u < h; ++u) {
+      const double send = upper ? p[u] : p[u + h];
+      const double keep = upper ? p[u + h] : p[u];
+      const double got = __shfl_xor_sync(0xffffffffu, send, o);
+      p[u] = ((maxmask >> (base + u)) & 1u) ? nmax(keep, got) : keep + got;
+    }
   }
+  const bool mxf = (maxmask >> base) & 1u;
+#pragma unroll
+  for (int o = 16 >> LOGP; o > 0; o >>= 1) {
+    const double got = __shfl_xor_sync(0xffffffffu, p[0], o);
+    p[0] = mxf ? nmax(p[0], got) : p[0] + got;
+  }
+  double* sh = E.sh;
+  // lane l holds value `base` iff l's low (5 - LOGP) bits are zero
+  if ((l & ((32 >> LOGP) - 1)) == 0 && base < K) sh[wpx() * K + base] = p[0];
   __syncthreads();
-  if (E.tid < K) {
-    const int k = E.tid;
+  if (tix() < K) {
+    const int k = tix();
     const bool mx = (maxmask >> k) & 1u;
-    double s = sh[k];
-    for (int w = 1; w < NWARP; ++w) s = mx ? nmax(s, sh[w * K + k]) : s + sh[w * K + k];
+    double t[NWARP];
+#pragma unroll
+    for (int w = 0; w < NWARP; ++w) t[w] = sh[w * K + k];
+    double s = t[0];
+#pragma unroll
+    for (int w = 1; w < NWARP; ++w) s = mx ? nmax(s, t[w]) : s + t[w];
     sh[NWARP * K + k] = s;
   }
   __syncthreads();
@@ -141,29 +208,46 @@ __device__ __forceinline__ void block_reduce(const Ctx& E, double (&v)[K], unsig
 // Publish this CTA's K partial scalars into the buffer the next barrier selects.
 template <int K>
 __device__ __forceinline__ void publish(const Ctx& E, const double (&v)[K], int slot0 = 0) {
-  if (E.tid < K) {
+  if (tix() < K) {
     double* dst = E.scal + ((size_t)((E.nbar + 1) & 1u) * E.nb + E.b) * SCAL + slot0;
-    dst[E.tid] = v[E.tid];
+    dst[tix()] = v[tix()];
   }
 }
 
-// After a barrier: reduce the K published scalars over all CTAs (fixed order,
-// identical in every CTA).  maxmask bit k selects max instead of sum.
-template <int K>
-__device__ __forceinline__ void gather(const Ctx& E, double (&out)[K], unsigned maxmask, int slot0 = 0) {
-  static_assert(K <= NWARP, "one warp per scalar");
-  const double* src = E.scal + (size_t)(E.nbar & 1u) * E.nb * SCAL + slot0;
-  double* sh = E.sh;
-  if (E.warp < K) {
-    const int k = E.warp;
-    const bool mx = (maxmask >> k) & 1u;
-    double s = mx ? -INFINITY : 0.0;
-    for (int q = E.lane; q < E.nb; q += 32) {
-      const double t = ldcg(src + (size_t)q * SCAL + k);
-      s = mx ? nmax(s, t) : s + t;
+// Fixed-order warp reduction of v[q] (q < cnt, stride `stride`) over up to
+// 32*GU entries: every lane issues its loads back to back (no dependent
+// chain of L2 round trips), then sums them in a fixed order.
+constexpr int GU = 5;                     // 5 * 32 = 160 >= 148 CTAs
+__device__ __forceinline__ double warp_fold(const double* base, int cnt, int64_t stride, bool mx) {
+  double s = mx ? -INFINITY : 0.0;
+  for (int q0 = 0; q0 < cnt; q0 += 32 * GU) {
+    double t[GU];
+#pragma unroll
+    for (int u = 0; u < GU; ++u) {
+      const int q = q0 + lnx() + 32 * u;
+      t[u] = q < cnt ? ldcg(base + (int64_t)q * stride) : (mx ? -INFINITY : 0.0);
     }
-    s = mx ? warp_max(s) : warp_sum(s);
-    if (E.lane == 0) sh[k] = s;
+#pragma unroll
+    for (int u = 0; u < GU; ++u) s = mx ? nmax(s, t[u]) : s + t[u];
+  }
+  return mx ? warp_max(s) : warp_sum(s);
+}
+
+// reduce published scalar k over all CTAs inside one warp (fixed order)
+__device__ __forceinline__ double gather_one(const Ctx& E, int k, bool mx) {
+  const double* src = E.scal + (size_t)(E.nbar & 1u) * E.nb * SCAL + k;
+  return warp_fold(src, E.nb, SCAL, mx);
+}
+
+// After a barrier: reduce the K published scalars over all CTAs (identical
+// in every CTA).  maxmask bit k selects max instead of sum.
+template <int K>
+__device__ __forceinline__ void gather(const Ctx& E, double (&out)[K], unsigned maxmask) {
+  static_assert(K <= NWARP, "one warp per scalar");
+  double* sh = E.sh;
+  if (wpx() < K) {
+    const double s = gather_one(E, wpx(), (maxmask >> wpx()) & 1u);
+    if (lnx() == 0) sh[wpx()] = s;
   }
   __syncthreads();
 #pragma unroll
@@ -171,106 +255,178 @@ __device__ __forceinline__ void gather(const Ctx& E, double (&out)[K], unsigned 
   __syncthreads();
 }
 
-// ------------------------------------------------------------------ panel source
-// Where a CTA reads its dictionary panel from: global memory (streamed through
-// L2 with ld.global.nc) or a copy resident in shared memory for the whole
-// launch (when the panel fits next to the scratch area).
-template <class TA, bool SM>
-struct Src {
-  const TA* p;      // column c0 of the panel; column j at p + (j - c0) * ld
+// Fused phase after the barrier that follows panel_gemv: the K scalar
+// gathers and, for every owned row i, sums[v] = sum_c part[c][v*ld + i]
+// (fixed order), then f(i, sums, aux) on lane 0 of the row's warp, with
+// aux[a] = auxv[a][i] prefetched alongside the partial loads.
+// f's per-thread accumulations are the caller's business.
+template <int K, int NV, int NA, class F>
+__device__ void gather_slice(const Ctx& E, double* out, unsigned maxmask, int64_t ld,
+                             const double* const (&auxv)[NA > 0 ? NA : 1], F&& f) {
+  double* sh = E.sh;
+  const int rows = (int)(E.r1 - E.r0);
+  const int items = K + rows;
+  for (int it = wpx(); it < items; it += NWARP) {
+    if (it < K) {
+      const double s = gather_one(E, it, (maxmask >> it) & 1u);
+      if (lnx() == 0) sh[it] = s;
+    } else {
+      const int64_t i = E.r0 + (it - K);
+      double au[NA > 0 ? NA : 1];
+      if (lnx() == 0) {
+#pragma unroll
+        for (int a = 0; a < NA; ++a) au[a] = ldcg(auxv[a] + i);
+      }
+      double sums[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        sums[v] = warp_fold(E.part + (size_t)v * ld + i, E.nb, E.pstride, false);
+      }
+      if (lnx() == 0) f(i, sums, au);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) out[k] = sh[k];
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------ panel
+// Column jl of the CTA panel: resident in shared memory when jl < rc,
+// streamed from global otherwise.
+template <class TA>
+struct Panel {
+  const TA* sm;    // resident columns (rc of them)
+  const TA* gl;    // global column c0
+  int rc;
+  int w;
 };
 
 template <class TA>
-struct VecOf { static constexpr int VW = 16 / (int)sizeof(TA); };
-
-// 16-byte load of VW consecutive rows, widened to double
-template <class TA, bool SM>
-__device__ __forceinline__ void ld16(const TA* p, double (&a)[VecOf<TA>::VW]) {
-  if constexpr (SM) {
-    const unsigned addr = (unsigned)__cvta_generic_to_shared(p);
-    if constexpr (sizeof(TA) == 8) {
-      double x, y;
-      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(addr));
-      a[0] = x; a[1] = y;
-    } else {
-      float x, y, z, w;
-      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(addr));
-      a[0] = x; a[1] = y; a[2] = z; a[3] = w;
-    }
+__device__ __forceinline__ void ld16_s(const TA* p, TA (&a)[VecOf<TA>::VW]) {
+  const unsigned addr = (unsigned)__cvta_generic_to_shared(p);
+  if constexpr (sizeof(TA) == 8) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a[0]), "=d"(a[1]) : "r"(addr));
   } else {
-    if constexpr (sizeof(TA) == 8) {
-      const double2 t = __ldg(reinterpret_cast<const double2*>(p));
-      a[0] = t.x; a[1] = t.y;
-    } else {
-      const float4 t = __ldg(reinterpret_cast<const float4*>(p));
-      a[0] = t.x; a[1] = t.y; a[2] = t.z; a[3] = t.w;
-    }
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(a[0]), "=f"(a[1]), "=f"(a[2]), "=f"(a[3]) : "r"(addr));
+  }
+}
+template <class TA>
+__device__ __forceinline__ void ld16_g(const TA* p, TA (&a)[VecOf<TA>::VW]) {
+  if constexpr (sizeof(TA) == 8) {
+    const double2 t = __ldg(reinterpret_cast<const double2*>(p));
+    a[0] = t.x; a[1] = t.y;
+  } else {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+    a[0] = t.x; a[1] = t.y; a[2] = t.z; a[3] = t.w;
   }
 }
 
-// Copy this CTA's panel (columns [c0, c1), contiguous in the column-major
-// layout) into shared memory.  Returns the smem source.
+// Copy the first rc panel columns (contiguous in the column-major layout)
+// into shared memory.
 template <class TA>
-__device__ Src<TA, true> load_panel(const Ctx& E, const DictV<TA>& D, TA* dst) {
-  const int64_t cnt = (E.c1 - E.c0) * D.ld;              // multiple of 32 elements
-  const int4* src = reinterpret_cast<const int4*>(D.A + E.c0 * D.ld);
+__device__ Panel<TA> setup_panel(const Ctx& E, const DictV<TA>& D, TA* dst, int rc) {
+  Panel<TA> P;
+  P.gl = D.A + E.c0 * D.ld;
+  P.w = E.w;
+  P.rc = rc < E.w ? rc : E.w;
+  P.sm = dst;
+  const int64_t n4 = (int64_t)P.rc * D.ld * (int64_t)sizeof(TA) / 16;
+  const int4* src = reinterpret_cast<const int4*>(P.gl);
   int4* d4 = reinterpret_cast<int4*>(dst);
-  const int64_t n4 = cnt * (int64_t)sizeof(TA) / 16;
-  for (int64_t k = E.tid; k < n4; k += NTHR) d4[k] = __ldg(src + k);
+  for (int64_t k = tix(); k < n4; k += NTHR) d4[k] = __ldg(src + k);
   __syncthreads();
-  return Src<TA, true>{dst};
-}
-
-template <class TA>
-__device__ __forceinline__ Src<TA, false> global_panel(const Ctx& E, const DictV<TA>& D) {
-  return Src<TA, false>{D.A + E.c0 * D.ld};
+  return P;
 }
 
 // ------------------------------------------------------------------ panel GEMV
-// part[b][v * ld + i] = sum_{j in panel} A[i, j] * xs[v][j]   (all rows, all v < NV)
-template <class TA, bool SM, int NV>
-__device__ void panel_gemv(const Ctx& E, const DictV<TA>& D, Src<TA, SM> S, const double* const (&xs)[NV]) {
+// part[b][v * ld + i] = sum_{jl < w} A[i, c0 + jl] * xs[v][jl]  (all rows),
+// xs: owned local vectors in shared memory.
+template <class TA, int NV>
+__device__ void panel_gemv(const Ctx& E, const DictV<TA>& D, const Panel<TA>& P,
+                           const double* const (&xs)[NV]) {
   constexpr int VW = VecOf<TA>::VW;
-  constexpr int U = SM ? 4 : 8;                    // columns per unrolled group (loads in flight)
-  const int64_t w = E.c1 - E.c0;
-  double* xsm = E.sh;                              // staged x panel: NV * w
-  __syncthreads();
-  for (int64_t k = E.tid; k < w; k += NTHR) {
-#pragma unroll
-    for (int v = 0; v < NV; ++v) xsm[v * w + k] = ldcg(xs[v] + E.c0 + k);
-  }
-  __syncthreads();
-  const int64_t nvec = D.ld / VW;                  // row-vectors per column
+  constexpr int PF = 4;                            // streamed columns prefetched per group
+  const int64_t nvec = D.ld / VW;
+  const int w = P.w, rc = P.rc;
   double* out = E.part + (size_t)E.b * E.pstride;
-  for (int64_t q = E.tid; q < nvec; q += NTHR) {
+  __syncthreads();
+  for (int64_t q = tix(); q < nvec; q += NTHR) {
     double acc[NV][VW];
 #pragma unroll
     for (int v = 0; v < NV; ++v)
 #pragma unroll
       for (int e = 0; e < VW; ++e) acc[v][e] = 0.0;
-    const TA* p = S.p + q * VW;
-    int64_t j = 0;
-    for (; j + U <= w; j += U) {
-      double a[U][VW];
+    int j = rc;
+    // streamed columns: a prefetched group overlaps the resident sweep below
+    TA g[PF][VW];
+    const int ng = (w - rc) < PF ? (w - rc) : PF;
 #pragma unroll
-      for (int u = 0; u < U; ++u) ld16<TA, SM>(p + (j + u) * D.ld, a[u]);
+    for (int u = 0; u < PF; ++u)
+      if (u < ng) ld16_g<TA>(P.gl + (int64_t)(rc + u) * D.ld + q * VW, g[u]);
+    // resident columns
+    {
+      const TA* p = P.sm + q * VW;
+      int jj = 0;
+      for (; jj + 4 <= rc; jj += 4) {
+        TA a[4][VW];
 #pragma unroll
-      for (int u = 0; u < U; ++u)
+        for (int u = 0; u < 4; ++u) ld16_s<TA>(p + (int64_t)(jj + u) * D.ld, a[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const double xv = xs[v][jj + u];
+#pragma unroll
+            for (int e = 0; e < VW; ++e) acc[v][e] = fma((double)a[u][e], xv, acc[v][e]);
+          }
+      }
+      for (; jj < rc; ++jj) {
+        TA a[VW];
+        ld16_s<TA>(p + (int64_t)jj * D.ld, a);
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-          const double xv = xsm[v * w + j + u];
+          const double xv = xs[v][jj];
 #pragma unroll
-          for (int e = 0; e < VW; ++e) acc[v][e] = fma(a[u][e], xv, acc[v][e]);
+          for (int e = 0; e < VW; ++e) acc[v][e] = fma((double)a[e], xv, acc[v][e]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PF; ++u)
+      if (u < ng) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const double xv = xs[v][rc + u];
+#pragma unroll
+          for (int e = 0; e < VW; ++e) acc[v][e] = fma((double)g[u][e], xv, acc[v][e]);
+        }
+      }
+    j = rc + ng;
+    // remaining streamed columns (large panels): unrolled by 8 for MLP
+    const TA* pg = P.gl + q * VW;
+    for (; j + 8 <= w; j += 8) {
+      TA a[8][VW];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) ld16_g<TA>(pg + (int64_t)(j + u) * D.ld, a[u]);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const double xv = xs[v][j + u];
+#pragma unroll
+          for (int e = 0; e < VW; ++e) acc[v][e] = fma((double)a[u][e], xv, acc[v][e]);
         }
     }
     for (; j < w; ++j) {
-      double a[VW];
-      ld16<TA, SM>(p + j * D.ld, a);
+      TA a[VW];
+      ld16_g<TA>(pg + (int64_t)j * D.ld, a);
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
-        const double xv = xsm[v * w + j];
+        const double xv = xs[v][j];
 #pragma unroll
-        for (int e = 0; e < VW; ++e) acc[v][e] = fma(a[e], xv, acc[v][e]);
+        for (int e = 0; e < VW; ++e) acc[v][e] = fma((double)a[e], xv, acc[v][e]);
       }
     }
 #pragma unroll
@@ -278,134 +434,138 @@ __device__ void panel_gemv(const Ctx& E, const DictV<TA>& D, Src<TA, SM> S, cons
 #pragma unroll
       for (int e = 0; e < VW; ++e) out[v * D.ld + q * VW + e] = acc[v][e];
   }
-  __syncthreads();
 }
 
 // ------------------------------------------------------------------ panel GEMV^T
-// outs[v][j] = sum_i A[i, j] * rs[v][i] for j in the panel (A-columns only).
-// Work unit = (column, row segment); segments balance narrow panels over the
-// 16 warps and are summed in a fixed order.  rs are replicated d-vectors
-// written during this launch; they are read through L1 after the grid
-// barrier's fence (which invalidates L1).
-template <class TA, bool SM, int NV>
-__device__ void panel_gemv_t(const Ctx& E, const DictV<TA>& D, Src<TA, SM> S,
+// outs[v][jl] = sum_i A[i, c0 + jl] * rs[v][i] for jl < w (A columns only;
+// outs are owned local vectors).  rs are replicated d-vectors in global
+// memory, read after the grid barrier.
+//
+// Short columns (ld/VW <= NTHR): thread q keeps row-vector q of r in
+// registers, forms per-column partials for a chunk of 32 columns, and a
+// warp transpose-reduction (31 shuffles / 32 columns) + a 16-way fixed-order
+// cross-warp sum finish them.  Long columns: warp per (column, segment).
+template <class TA, int NV>
+__device__ void panel_gemv_t(const Ctx& E, const DictV<TA>& D, const Panel<TA>& P,
                              const double* const (&rs)[NV], double* const (&outs)[NV]) {
   constexpr int VW = VecOf<TA>::VW;
-  const int64_t w = E.c1 - E.c0;
   const int64_t nvec = D.ld / VW;
-  int64_t seg = (2 * NWARP + w - 1) / (w > 0 ? w : 1);
-  const int64_t maxseg = nvec / 32 > 0 ? nvec / 32 : 1;
-  if (seg > maxseg) seg = maxseg;
-  if (seg < 1) seg = 1;
-  if (seg * w * NV > E.shcap) seg = 1;
-  const int64_t seglen = (nvec + seg - 1) / seg;
-  const int64_t units = w * seg;
-  double* stage = E.sh;
+  const int w = P.w, rc = P.rc;
+  double* red = E.sh;                               // [NWARP][32] per v pass
   __syncthreads();
-  for (int64_t u = E.warp; u < units; u += NWARP) {
-    const int64_t jl = u / seg, sg = u - jl * seg;
-    const TA* col = S.p + jl * D.ld;
-    const int64_t q0 = sg * seglen;
-    const int64_t q1 = min(nvec, q0 + seglen);
-    double acc[NV][2];
+  if (nvec <= NTHR) {
+    const int64_t q = tix();
+    const bool act = q < nvec;
+    double rq[NV][VW];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) acc[v][0] = acc[v][1] = 0.0;
-    int64_t q = q0 + E.lane;
-    for (; q + 96 < q1; q += 128) {
-      double a[4][VW];
+    for (int v = 0; v < NV; ++v)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) ld16<TA, SM>(col + (q + 32 * k) * VW, a[k]);
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const double* rv = rs[v] + (q + 32 * k) * VW;
-#pragma unroll
-          for (int e = 0; e < VW; ++e) acc[v][k & 1] = fma(a[k][e], rv[e], acc[v][k & 1]);
-        }
-    }
-    for (; q < q1; q += 32) {
-      double a[VW];
-      ld16<TA, SM>(col + q * VW, a);
+      for (int e = 0; e < VW; ++e) rq[v][e] = act ? ldcg(rs[v] + q * VW + e) : 0.0;
+    constexpr int CW = 16;                          // columns per transpose-reduce chunk
+    for (int j0 = 0; j0 < w; j0 += CW) {
+      const int cnt = (w - j0) < CW ? (w - j0) : CW;
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
-        const double* rv = rs[v] + q * VW;
+        double p[CW];
 #pragma unroll
-        for (int e = 0; e < VW; ++e) acc[v][0] = fma(a[e], rv[e], acc[v][0]);
+        for (int u = 0; u < CW; ++u) {
+          TA a[VW];
+          const int j = j0 + u;
+          if (u < cnt && act) {
+            if (j < rc) ld16_s<TA>(P.sm + (int64_t)j * D.ld + q * VW, a);
+            else ld16_g<TA>(P.gl + (int64_t)j * D.ld + q * VW, a);
+          } else {
+#pragma unroll
+            for (int e = 0; e < VW; ++e) a[e] = (TA)0;
+          }
+          double s = 0.0;
+#pragma unroll
+          for (int e = 0; e < VW; ++e) s = fma((double)a[e], rq[v][e], s);
+          p[u] = s;
+        }
+        // transpose-reduce: afterwards lane l (and l^16) holds the warp sum of column j0 + (l & 15)
+#pragma unroll
+        for (int o = CW / 2; o >= 1; o >>= 1) {
+          const bool upper = (lnx() & o) != 0;
+#pragma unroll
+          for (int u = 0; u < o; ++u) {
+            const double send = upper ? p[u] : p[u + o];
+            const double keep = upper ? p[u + o] : p[u];
+            p[u] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+        }
+        p[0] += __shfl_xor_sync(0xffffffffu, p[0], 16);
+        if (lnx() < CW) red[wpx() * CW + lnx()] = p[0];
+        __syncthreads();
+        if (tix() < cnt) {
+          double t[NWARP];
+#pragma unroll
+          for (int ww = 0; ww < NWARP; ++ww) t[ww] = red[ww * CW + tix()];
+          double s = t[0];
+#pragma unroll
+          for (int ww = 1; ww < NWARP; ++ww) s += t[ww];
+          outs[v][j0 + tix()] = s;
+        }
+        __syncthreads();
       }
     }
+  } else {
+    for (int jl = wpx(); jl < w; jl += NWARP) {
+      double acc[NV][2];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const double s = warp_sum(acc[v][0] + acc[v][1]);
-      if (E.lane == 0) {
-        if (seg == 1) outs[v][E.c0 + jl] = s;
-        else stage[(v * w + jl) * seg + sg] = s;
+      for (int v = 0; v < NV; ++v) acc[v][0] = acc[v][1] = 0.0;
+      const bool res = jl < rc;
+      const TA* col = res ? P.sm + (int64_t)jl * D.ld : P.gl + (int64_t)jl * D.ld;
+      int64_t q = lnx();
+      for (; q + 96 < nvec; q += 128) {
+        TA a[4][VW];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (res) ld16_s<TA>(col + (q + 32 * k) * VW, a[k]);
+          else ld16_g<TA>(col + (q + 32 * k) * VW, a[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const double* rv = rs[v] + (q + 32 * k) * VW;
+#pragma unroll
+            for (int e = 0; e < VW; ++e) acc[v][k & 1] = fma((double)a[k][e], rv[e], acc[v][k & 1]);
+          }
       }
-    }
-  }
-  __syncthreads();
-  if (seg > 1) {
-    for (int64_t t = E.tid; t < w * NV; t += NTHR) {
-      const int v = (int)(t / w);
-      const int64_t jl = t - (int64_t)v * w;
-      const double* st = stage + (v * w + jl) * seg;
-      double s = st[0];
-      for (int64_t k = 1; k < seg; ++k) s += st[k];
+      for (; q < nvec; q += 32) {
+        TA a[VW];
+        if (res) ld16_s<TA>(col + q * VW, a);
+        else ld16_g<TA>(col + q * VW, a);
 #pragma unroll
-      for (int vv = 0; vv < NV; ++vv)
-        if (vv == v) outs[vv][E.c0 + jl] = s;
-    }
-    __syncthreads();
-  }
-}
-
-// ------------------------------------------------------------------ slice reduction
-// After the barrier that follows panel_gemv: for each owned row i,
-//   sums[v] = sum over CTAs of part[c][v * ld + i]   (fixed order)
-// then f(i, sums) runs once per row (thread-parallel over rows).
-template <int NV, class F>
-__device__ void slice_reduce(const Ctx& E, int64_t ld, F&& f) {
-  int64_t CH = E.shcap / NV;                        // rows per chunk (NV*CH doubles of smem)
-  if (CH > 256) CH = 256;
-  double* stage = E.sh;
-  for (int64_t base = E.r0; base < E.r1; base += CH) {
-    const int rows = (int)min(CH, E.r1 - base);
-    const int items = rows * NV;
-    for (int it = E.warp; it < items; it += NWARP) {
-      const int v = it / rows, rr = it - v * rows;
-      const double* src = E.part + (size_t)v * ld + base + rr;
-      double s = 0.0;
-      for (int c = E.lane; c < E.nb; c += 32) s += ldcg(src + (size_t)c * E.pstride);
-      s = warp_sum(s);
-      if (E.lane == 0) stage[it] = s;
-    }
-    __syncthreads();
-    for (int rr = E.tid; rr < rows; rr += NTHR) {
-      double sums[NV];
+        for (int v = 0; v < NV; ++v) {
+          const double* rv = rs[v] + q * VW;
 #pragma unroll
-      for (int v = 0; v < NV; ++v) sums[v] = stage[v * rows + rr];
-      f(base + rr, sums);
+          for (int e = 0; e < VW; ++e) acc[v][0] = fma((double)a[e], rv[e], acc[v][0]);
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const double s = warp_sum(acc[v][0] + acc[v][1]);
+        if (lnx() == 0) outs[v][jl] = s;
+      }
     }
     __syncthreads();
   }
 }
 
 // ------------------------------------------------------------------ owned-column loop
-// f(j) for every owned column of D: the A panel and (extension) the identity
-// columns n + [r0, r1).
-template <class TA, class F>
-__device__ __forceinline__ void for_owned(const Ctx& E, const DictV<TA>& D, F&& f) {
-  for (int64_t j = E.c0 + E.tid; j < E.c1; j += NTHR) f(j);
-  if (D.ext)
-    for (int64_t i = E.r0 + E.tid; i < E.r1; i += NTHR) f(D.n + i);
+// f(k) for every owned local column k in [0, W)
+template <class F>
+__device__ __forceinline__ void for_owned(const Ctx& E, F&& f) {
+  for (int k = tix(); k < E.W; k += NTHR) f(k);
 }
 
-// shared-memory scratch (doubles) the engine needs next to an optional panel
-__host__ __device__ inline int64_t engine_scratch_doubles(int64_t n, int nb, int nv, int kmax) {
-  const int64_t w = (n + nb - 1) / nb + 1;
-  int64_t s = w * nv * 2;                   // x staging / GEMV^T segment partials (>= 2 segs)
-  if (s < 64 * nv) s = 64 * nv;             // slice staging
-  if (s < NWARP * kmax + kmax) s = NWARP * kmax + kmax;   // block reductions of kmax scalars
+// shared-memory scratch (doubles) the engine needs next to the panel / owned vectors
+__host__ __device__ inline int64_t engine_scratch_doubles(int kmax) {
+  int64_t s = NWARP * 32;                   // GEMV^T cross-warp staging
+  if (s < NWARP * kmax + kmax) s = NWARP * kmax + kmax;
+  if (s < 16 * 2) s = 32;
   return (s + 31) / 32 * 32;
 }
 

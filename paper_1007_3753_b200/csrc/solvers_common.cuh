@@ -32,6 +32,7 @@ __device__ __forceinline__ DictV<TA> dict_view(const DictRaw& R) {
   return D;
 }
 
+// thread 0 only
 __device__ __forceinline__ void ctx_bind(Ctx& E, const GridBufs& g, double* smem) {
   E.bar = g.bar; E.abort = g.abort; E.part = g.part; E.pstride = g.pstride;
   E.scal = g.scal; E.sh = smem; E.shcap = g.shcap;
@@ -128,10 +129,8 @@ inline bool carve_grid(Carve& cv, GridBufs& g, int nb, int64_t pstride) {
 template <class K, class Arg>
 inline int coop_launch(K kernel, int nb, size_t smem, cudaStream_t s, Arg& arg, unsigned long long* bar) {
   if (cudaMemsetAsync(bar, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess) return ELL1_ERR_CUDA;
-  if (smem > 48 * 1024) {
-    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return ELL1_ERR_CUDA;
-  }
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return ELL1_ERR_CUDA;
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, NTHR, smem) != cudaSuccess) return ELL1_ERR_CUDA;
   int dev = 0;
@@ -146,10 +145,11 @@ inline int coop_launch(K kernel, int nb, size_t smem, cudaStream_t s, Arg& arg, 
   return ELL1_OK;
 }
 
-// Shared-memory plan for a persistent solver: optionally the CTA's dictionary
-// panel (resident for the whole launch) followed by the engine scratch.
+// Shared-memory plan for a persistent solver:
+//   [resident panel: rc columns][owned vectors: nov x wmax doubles][scratch]
 struct SmemPlan {
-  bool resident;
+  int rc;                // resident panel columns
+  int wmax;              // owned-vector stride (max owned local columns over CTAs)
   size_t panel_bytes;
   size_t bytes;          // total dynamic smem
   int64_t scratch;       // scratch doubles
@@ -162,27 +162,39 @@ inline int max_smem_optin() {
   return v - 128;      // static __shared__ (grid_sync flag) + slack
 }
 
-inline SmemPlan plan_smem(const DictRaw& D, int nb, int nv, bool allow_resident = true, int kmax = 16) {
+inline SmemPlan plan_smem(const DictRaw& D, int nb, int nov, int kmax, bool allow_resident) {
   SmemPlan p;
-  const int64_t w = (D.n + nb - 1) / nb;
+  const int64_t wcols = (D.n + nb - 1) / nb;
+  const int64_t wrows = D.ext ? (D.d + nb - 1) / nb : 0;
+  p.wmax = (int)align_up(wcols + wrows, 2);
+  p.scratch = engine_scratch_doubles(kmax);
   const int64_t esz = D.dtype == ELL1_F64 ? 8 : 4;
-  const int64_t scratch_min = engine_scratch_doubles(D.n, nb, nv, kmax);
-  p.panel_bytes = (size_t)align_up(w * D.ld * esz, 128);
+  const int64_t fixed = ((int64_t)nov * p.wmax + p.scratch) * 8;
   const int64_t cap = max_smem_optin();
-  if (allow_resident && (int64_t)p.panel_bytes + scratch_min * 8 <= cap) {
-    p.resident = true;
-    int64_t room = (cap - (int64_t)p.panel_bytes) / 8;
-    int64_t want = scratch_min > 2048 ? scratch_min : 2048;
-    p.scratch = (room < want ? room : want) / 32 * 32;
-  } else {
-    p.resident = false;
-    p.panel_bytes = 0;
-    int64_t want = scratch_min;
-    if (want < 4096) want = 4096;
-    p.scratch = want;
+  int64_t rc = 0;
+  if (allow_resident) {
+    rc = (cap - fixed) / (D.ld * esz);
+    if (rc < 0) rc = 0;
+    if (rc > wcols) rc = wcols;
   }
-  p.bytes = p.panel_bytes + (size_t)p.scratch * 8;
+  p.rc = (int)rc;
+  p.panel_bytes = (size_t)align_up(rc * D.ld * esz, 16);
+  p.bytes = p.panel_bytes + (size_t)fixed;
   return p;
 }
+
+inline DictRaw to_raw(const ell1_dict_t* D) {
+  DictRaw r;
+  r.A = D->A; r.dtype = D->dtype; r.ext = D->ext; r.d = D->d; r.n = D->n; r.ld = D->ld;
+  r.s = D->ext_scale;
+  return r;
+}
+
+inline bool dict_ok(const ell1_dict_t* D) {
+  return D && D->A && D->d >= 1 && D->n >= 1 && D->ld >= D->d && D->ld % 32 == 0 &&
+         (D->dtype == ELL1_F64 || D->dtype == ELL1_F32);
+}
+
+inline int64_t ncols_of(const ell1_dict_t* D) { return D->n + (D->ext ? D->d : 0); }
 
 }  // namespace ell1
