@@ -152,6 +152,28 @@ size_t ell1_fista_workspace(const ell1_dict_t* D, const ell1_ctrl_t* C, int32_t 
 int ell1_fista(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C,
                const ell1_fista_opts_t* O, const ell1_io_t* io, void* stream);
 
+/* Dual ALM options (alm.py:206-230).  M = G^{-1} A (A columns, same layout and
+ * dtype as the dictionary) and Ginv = G^{-1} (d x d, column-major, ld rows,
+ * float64), G = A A^T (+ s^2 I for the [A, sI] extension): the row-Gram
+ * factorisation of alm._gram_factor (alm.py:162-169) done once per dictionary
+ * (see ell1_gram_prepare). */
+typedef struct {
+  double beta;
+  double y_tol;        /* y-step residual certificate (alm.py:24: 1e-10; f32 storage: 1e-5) */
+  int32_t y_cg_step;   /* 1: one warm-started CG step instead of the exact y solve */
+  int32_t _pad;
+  const void* M;
+  const double* Ginv;
+  double* y_out;       /* optional (observer): multiplier y, ld entries */
+  double* z_out;       /* optional (observer): z, n(+d) entries */
+} ell1_dalm_opts_t;
+
+/* Dual augmented Lagrangian — replaces alm.dalm_solve (alm.py:206-272)
+ * (with dual_y_solve alm.py:172-189 / _y_cg_step alm.py:192-203 fused in). */
+size_t ell1_dalm_workspace(const ell1_dict_t* D, int32_t blocks);
+int ell1_dalm(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C,
+              const ell1_dalm_opts_t* O, const ell1_io_t* io, void* stream);
+
 /* library / device info */
 int ell1_device_sms(int32_t device);
 const char* ell1_version(void);

@@ -50,6 +50,13 @@ class FistaOpts(ctypes.Structure):
                 ("probe", ctypes.c_int32), ("_pad", ctypes.c_int32)]
 
 
+class DalmOpts(ctypes.Structure):
+    _fields_ = [("beta", ctypes.c_double), ("y_tol", ctypes.c_double),
+                ("y_cg_step", ctypes.c_int32), ("_pad", ctypes.c_int32),
+                ("M", ctypes.c_void_p), ("Ginv", ctypes.c_void_p), ("y_out", ctypes.c_void_p),
+                ("z_out", ctypes.c_void_p)]
+
+
 class IO(ctypes.Structure):
     _fields_ = [("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
                 ("state", ctypes.c_void_p), ("trace", ctypes.c_void_p),
@@ -86,6 +93,9 @@ _SIGS = {
     "ell1_fista_workspace": (ctypes.c_size_t, [P(Dict), P(Ctrl), ctypes.c_int32]),
     "ell1_fista": (ctypes.c_int, [P(Dict), ctypes.c_void_p, P(Ctrl), P(FistaOpts), P(IO),
                                   ctypes.c_void_p]),
+    "ell1_dalm_workspace": (ctypes.c_size_t, [P(Dict), ctypes.c_int32]),
+    "ell1_dalm": (ctypes.c_int, [P(Dict), ctypes.c_void_p, P(Ctrl), P(DalmOpts), P(IO),
+                                 ctypes.c_void_p]),
     "ell1_device_sms": (ctypes.c_int, [ctypes.c_int32]),
     "ell1_version": (ctypes.c_char_p, []),
 }

@@ -128,7 +128,7 @@ __device__ __forceinline__ void mark(Ctx& E, int k) {
 // until every CTA of this epoch arrived.  The acquire load orders (and
 // invalidates L1 for) everything read after the barrier.  Returns false
 // when a peer aborted or the wait timed out; callers unwind cleanly.
-__device__ bool grid_sync(Ctx& E) {
+__device__ __forceinline__ bool grid_sync(Ctx& E) {
   __syncthreads();
   if (tix() == 0) {
     E.epoch += (unsigned long long)E.nb;
@@ -323,6 +323,23 @@ __device__ __forceinline__ void ld16_g(const TA* p, TA (&a)[VecOf<TA>::VW]) {
   }
 }
 
+// Panel over columns [c0, c0 + w) of an arbitrary column-major matrix
+// (ld rows), first rc columns resident at dst.
+template <class TA>
+__device__ Panel<TA> setup_panel_at(const TA* Abase, int64_t ld, int64_t c0, int w, TA* dst, int rc) {
+  Panel<TA> P;
+  P.gl = Abase + c0 * ld;
+  P.w = w;
+  P.rc = rc < w ? rc : w;
+  P.sm = dst;
+  const int64_t n4 = (int64_t)P.rc * ld * (int64_t)sizeof(TA) / 16;
+  const int4* src = reinterpret_cast<const int4*>(P.gl);
+  int4* d4 = reinterpret_cast<int4*>(dst);
+  for (int64_t k = tix(); k < n4; k += NTHR) d4[k] = __ldg(src + k);
+  __syncthreads();
+  return P;
+}
+
 // Copy the first rc panel columns (contiguous in the column-major layout)
 // into shared memory.
 template <class TA>
@@ -345,12 +362,12 @@ __device__ Panel<TA> setup_panel(const Ctx& E, const DictV<TA>& D, TA* dst, int 
 // xs: owned local vectors in shared memory.
 template <class TA, int NV>
 __device__ void panel_gemv(const Ctx& E, const DictV<TA>& D, const Panel<TA>& P,
-                           const double* const (&xs)[NV]) {
+                           const double* const (&xs)[NV], bool accumulate = false, int slot0 = 0) {
   constexpr int VW = VecOf<TA>::VW;
   constexpr int PF = 4;                            // streamed columns prefetched per group
   const int64_t nvec = D.ld / VW;
   const int w = P.w, rc = P.rc;
-  double* out = E.part + (size_t)E.b * E.pstride;
+  double* out = E.part + (size_t)E.b * E.pstride + (size_t)slot0 * D.ld;
   __syncthreads();
   for (int64_t q = tix(); q < nvec; q += NTHR) {
     double acc[NV][VW];
@@ -432,7 +449,10 @@ __device__ void panel_gemv(const Ctx& E, const DictV<TA>& D, const Panel<TA>& P,
 #pragma unroll
     for (int v = 0; v < NV; ++v)
 #pragma unroll
-      for (int e = 0; e < VW; ++e) out[v * D.ld + q * VW + e] = acc[v][e];
+      for (int e = 0; e < VW; ++e) {
+        double* o = out + v * D.ld + q * VW + e;
+        *o = accumulate ? *o + acc[v][e] : acc[v][e];
+      }
   }
 }
 

@@ -106,6 +106,35 @@ class DeviceDictionary:
     def shape(self):
         return (self.d, self.n)
 
+    # -- row-Gram factorisation for the dual ALM (alm.py:162-169) ----------
+    def gram_factor(self, ext=False, scale=0.0):
+        """(M, Ginv, L) with G = A A^T (+ s^2 I), L its lower Cholesky factor,
+        Ginv = G^{-1} (column-major, ld rows, float64) and M = Ginv A in the
+        dictionary's layout / dtype.  Computed once per (ext, scale) from the
+        device copy of A (so float32 storage factors the rounded A).
+        Raises IllConditionedError when G is not positive definite."""
+        key = (bool(ext), float(scale) if ext else 0.0)
+        cache = self.__dict__.setdefault("_gram", {})
+        if key in cache:
+            return cache[key]
+        torch = _torch()
+        from paper_1007_3753_b200.exceptions import IllConditionedError
+        At = self.storage.view(self.n, self.ld)[:, : self.d].to(torch.float64)   # A^T (n x d)
+        G = At.T @ At
+        if ext:
+            G.diagonal().add_(float(scale) ** 2)
+        L, info = torch.linalg.cholesky_ex(G)
+        if int(info.item()) != 0:
+            raise IllConditionedError("row Gram A A^T is not positive definite; the dual "
+                                      "solver needs full row rank")
+        Ginv = torch.cholesky_inverse(L)
+        Gcm = torch.zeros(self.d, self.ld, dtype=torch.float64, device=self.device)
+        Gcm[:, : self.d] = Ginv            # symmetric: row j == column j
+        MT = torch.zeros(self.n, self.ld, dtype=self.storage.dtype, device=self.device)
+        MT[:, : self.d] = (At @ Ginv).to(self.storage.dtype)   # row j of M^T == column j of M
+        cache[key] = (MT, Gcm, L)
+        return cache[key]
+
     # -- operator-protocol hooks ------------------------------------------
     def norm_sq(self):
         """Largest eigenvalue of A^T A (numerics.spectral_norm_sq), cached."""

@@ -1,0 +1,232 @@
+"""Cross-and-bouquet solving on the implicit [A, s I] dictionary — drop-in for
+the CAB half of ell1.robust (robust.py:36-220).
+
+The identity block is never materialised: the device kernels treat the
+extension columns as slice-owned (column n + i lives with row i), so D x adds
+s * x_ext in the row reduction and D^T r appends s * r (robust.py:91-96).
+"""
+
+import numpy as np
+
+from paper_1007_3753_b200 import device
+from paper_1007_3753_b200.model import SolverResult
+
+_CAB_BACKENDS = ("pdipa", "homotopy", "gp", "ist", "fista", "palm", "dalm")
+
+
+class _AdjointView:
+    """Transpose-shaped face of an implicit operator (robust.py:36-54)."""
+
+    __slots__ = ("_op",)
+
+    def __init__(self, op):
+        self._op = op
+
+    @property
+    def shape(self):
+        d, w = self._op.shape
+        return (w, d)
+
+    @property
+    def T(self):
+        return self._op
+
+    def __matmul__(self, r):
+        return self._op.adjoint(np.asarray(r, dtype=np.float64))
+
+
+class ExtendedDictionary:
+    """Implicit stack [A, s I] of width n + d (robust.py:57-155).
+
+    Solvers of this package read it through ``device_extension()`` (the
+    device copy of A plus the scale).  The host-side operator methods
+    (apply / adjoint / column protocol / Gram hooks) are kept for callers
+    and tests of the reference API; ``norm_sq`` runs the device power
+    iteration.
+    """
+
+    mode = "cab"
+
+    def __init__(self, A, identity_scale=1.0, dtype="float64", device_ordinal=None):
+        if isinstance(A, device.DeviceDictionary):
+            self._dev = A
+            self.A = None
+        else:
+            self.A = np.ascontiguousarray(A, dtype=np.float64)
+            if self.A.ndim != 2:
+                raise ValueError("dictionary must be a matrix")
+            self._dev = None
+        if not identity_scale > 0:
+            raise ValueError("identity_scale must be positive")
+        self.scale = float(identity_scale)
+        self._dtype = dtype
+        self._ordinal = device_ordinal
+        self._norm_sq = None
+
+    # -- device view -------------------------------------------------------
+    def device_extension(self):
+        if self._dev is None:
+            self._dev = device.DeviceDictionary(self.A, dtype=self._dtype, device=self._ordinal)
+        return self._dev, self.scale
+
+    def _host(self):
+        if self.A is None:
+            D = self._dev
+            self.A = D.storage.view(D.n, D.ld)[:, : D.d].double().T.contiguous().cpu().numpy()
+        return self.A
+
+    # -- operator protocol (host utilities) --------------------------------
+    @property
+    def shape(self):
+        if self.A is not None:
+            d, n = self.A.shape
+        else:
+            d, n = self._dev.d, self._dev.n
+        return (d, n + d)
+
+    @property
+    def T(self):
+        return _AdjointView(self)
+
+    def __matmul__(self, w):
+        return self.apply(np.asarray(w, dtype=np.float64))
+
+    def apply(self, w):
+        A = self._host()
+        n = A.shape[1]
+        return A @ w[:n] + self.scale * w[n:]
+
+    def adjoint(self, r):
+        A = self._host()
+        return np.concatenate([A.T @ r, self.scale * r])
+
+    def column(self, j):
+        A = self._host()
+        d, n = A.shape
+        if j < n:
+            return A[:, j].copy()
+        out = np.zeros(d)
+        out[j - n] = self.scale
+        return out
+
+    def apply_columns(self, idx, coeffs):
+        A = self._host()
+        d, n = A.shape
+        idx = np.asarray(idx, dtype=np.intp)
+        coeffs = np.asarray(coeffs, dtype=np.float64)
+        out = np.zeros(d)
+        lo = idx < n
+        if np.any(lo):
+            out += A[:, idx[lo]] @ coeffs[lo]
+        if np.any(~lo):
+            out[idx[~lo] - n] += self.scale * coeffs[~lo]
+        return out
+
+    def columns_dot(self, idx, v):
+        A = self._host()
+        n = A.shape[1]
+        idx = np.asarray(idx, dtype=np.intp)
+        out = np.empty(idx.shape[0])
+        lo = idx < n
+        if np.any(lo):
+            out[lo] = A[:, idx[lo]].T @ v
+        if np.any(~lo):
+            out[~lo] = self.scale * v[idx[~lo] - n]
+        return out
+
+    def gram_column(self, idx, j):
+        return self.columns_dot(idx, self.column(j))
+
+    def column_norms_sq(self):
+        A = self._host()
+        d = A.shape[0]
+        return np.concatenate([np.sum(A * A, axis=0), np.full(d, self.scale ** 2)])
+
+    def norm_sq(self):
+        """||A||^2 + s^2 (robust.py:139-143), power iteration on the device."""
+        if self._norm_sq is None:
+            D, s = self.device_extension()
+            self._norm_sq = D.norm_sq() + s ** 2
+        return self._norm_sq
+
+    def weighted_gram_dd(self, w):
+        A = self._host()
+        d, n = A.shape
+        M = (A * w[:n]) @ A.T
+        M[np.diag_indices(d)] += self.scale ** 2 * w[n:]
+        return M
+
+    def gram_dd(self):
+        A = self._host()
+        d = A.shape[0]
+        M = A @ A.T
+        M[np.diag_indices(d)] += self.scale ** 2
+        return M
+
+
+class _OperatorProblem:
+    """Problem shim whose dictionary is an implicit operator (robust.py:158-175)."""
+
+    def __init__(self, op, b):
+        self.A = op
+        self.b = np.ascontiguousarray(b, dtype=np.float64)
+        self.ground_truth = None
+        self.noise_sigma = 0.0
+        if self.b.shape != (op.shape[0],):
+            raise ValueError("b must have length d")
+
+    @property
+    def d(self):
+        return self.A.shape[0]
+
+    @property
+    def n(self):
+        return self.A.shape[1]
+
+
+def _resolved_lambda(config, prob):
+    if config.lam is not None:
+        return float(config.lam)
+    D, s = prob.A.device_extension()
+    return 1e-2 * device._corr(D, D.view(ext=True, scale=s), prob.b)[0]
+
+
+def cab_solve(A, b, solver, config):
+    """Solve the corruption-extended system with the chosen backend
+    (robust.py:181-220).  Returns (x, e, record) with e = s * w[n:].
+
+    A may be a numpy matrix or a DeviceDictionary (reused across queries).
+    """
+    if solver not in _CAB_BACKENDS:
+        raise ValueError("unknown cab backend %r (choose from %s)"
+                         % (solver, ", ".join(_CAB_BACKENDS)))
+    e_weight = float(config.opt("e_weight", 1.0))
+    if not e_weight > 0:
+        raise ValueError("e_weight must be positive")
+    scale = 1.0 / e_weight
+    ext = ExtendedDictionary(A, identity_scale=scale, dtype=config.opt("dtype", "float64"),
+                             device_ordinal=config.opt("device", None))
+    prob = _OperatorProblem(ext, b)
+    n = ext.shape[1] - ext.shape[0]
+    if solver == "dalm":
+        from paper_1007_3753_b200.alm import dalm_solve
+        res = dalm_solve(prob, config)
+    elif solver == "palm":
+        from paper_1007_3753_b200.alm import palm_solve
+        res = palm_solve(prob, config)
+    elif solver == "fista":
+        from paper_1007_3753_b200.shrinkage import fista_solve
+        res = fista_solve(prob, config)
+    elif solver == "ist":
+        from paper_1007_3753_b200.shrinkage import ist_solve
+        res = ist_solve(prob, None, config)
+    elif solver == "gp":
+        from paper_1007_3753_b200.gradient_projection import gpsr_solve
+        res = gpsr_solve(prob, _resolved_lambda(config, prob), config)
+    elif solver == "homotopy":
+        from paper_1007_3753_b200.homotopy import solve_path
+        res, _ = solve_path(ext, prob.b, _resolved_lambda(config, prob), config)
+    else:
+        raise NotImplementedError("pdipa is outside the B200 hot path (SURVEY §8(f) rank 1)")
+    w = res.x_star
+    return w[:n], scale * w[n:], res

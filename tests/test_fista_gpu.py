@@ -152,3 +152,14 @@ def test_fista_budget_cap(shr, model):
     P = model.ProblemInstance(A, rng.standard_normal(20))
     r = shr.fista_solve(P, model.SolverConfig(lam=0.05, max_iter=2))
     assert not r.converged and r.iterations == 2
+
+
+def test_fista_cab_matches_reference(model):
+    from paper_1007_3753_b200.robust import cab_solve
+    from tests.gpu_util import rel_err
+    case, A, b, gt, gold = case_inputs("cab_small_fista")
+    x, e, res = cab_solve(A, b, "fista", make_config(case, A, b))
+    gw = dict(gold)
+    gw["x"] = gold["w"]
+    assert_parity(res.x_star, res.iterations, res.converged, res.trace, gw, 1e-6)
+    assert rel_err(x, gold["x"]) <= 1e-6
