@@ -174,6 +174,21 @@ size_t ell1_dalm_workspace(const ell1_dict_t* D, int32_t blocks);
 int ell1_dalm(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C,
               const ell1_dalm_opts_t* O, const ell1_io_t* io, void* stream);
 
+/* Primal ALM options (alm.py:115-122): mu0, rho and tau = 1.01 * ||D||^2
+ * (numerics.spectral_norm_sq / ExtendedDictionary.norm_sq, computed with
+ * ell1_spectral_norm_sq). */
+typedef struct {
+  double mu0, rho, tau;
+  double* y_out;       /* optional (observer): multiplier y, ld entries */
+} ell1_palm_opts_t;
+
+/* Primal ALM with accelerated inner shrinkage — replaces alm.palm_solve
+ * (alm.py:96-159) and alm._inner_shrinkage (alm.py:71-93).  io->max_steps
+ * counts OUTER iterations (the observer granularity). */
+size_t ell1_palm_workspace(const ell1_dict_t* D, int32_t blocks);
+int ell1_palm(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C,
+              const ell1_palm_opts_t* O, const ell1_io_t* io, void* stream);
+
 /* library / device info */
 int ell1_device_sms(int32_t device);
 const char* ell1_version(void);

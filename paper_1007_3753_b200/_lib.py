@@ -57,6 +57,11 @@ class DalmOpts(ctypes.Structure):
                 ("z_out", ctypes.c_void_p)]
 
 
+class PalmOpts(ctypes.Structure):
+    _fields_ = [("mu0", ctypes.c_double), ("rho", ctypes.c_double), ("tau", ctypes.c_double),
+                ("y_out", ctypes.c_void_p)]
+
+
 class IO(ctypes.Structure):
     _fields_ = [("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
                 ("state", ctypes.c_void_p), ("trace", ctypes.c_void_p),
@@ -95,6 +100,9 @@ _SIGS = {
                                   ctypes.c_void_p]),
     "ell1_dalm_workspace": (ctypes.c_size_t, [P(Dict), ctypes.c_int32]),
     "ell1_dalm": (ctypes.c_int, [P(Dict), ctypes.c_void_p, P(Ctrl), P(DalmOpts), P(IO),
+                                 ctypes.c_void_p]),
+    "ell1_palm_workspace": (ctypes.c_size_t, [P(Dict), ctypes.c_int32]),
+    "ell1_palm": (ctypes.c_int, [P(Dict), ctypes.c_void_p, P(Ctrl), P(PalmOpts), P(IO),
                                  ctypes.c_void_p]),
     "ell1_device_sms": (ctypes.c_int, [ctypes.c_int32]),
     "ell1_version": (ctypes.c_char_p, []),
