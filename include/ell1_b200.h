@@ -189,6 +189,14 @@ size_t ell1_palm_workspace(const ell1_dict_t* D, int32_t blocks);
 int ell1_palm(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C,
               const ell1_palm_opts_t* O, const ell1_io_t* io, void* stream);
 
+/* Iterative shrinkage over a continuation schedule — replaces
+ * shrinkage.ist_solve (shrinkage.py:105-181).  stages: the schedule's lambda
+ * values (ContinuationSchedule.stages(), shrinkage.py:43-58), device memory.
+ * io->max_steps counts accepted steps (the observer granularity). */
+size_t ell1_ist_workspace(const ell1_dict_t* D, int32_t blocks);
+int ell1_ist(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C,
+             const double* stages, int32_t nstages, const ell1_io_t* io, void* stream);
+
 /* library / device info */
 int ell1_device_sms(int32_t device);
 const char* ell1_version(void);
