@@ -197,6 +197,15 @@ size_t ell1_ist_workspace(const ell1_dict_t* D, int32_t blocks);
 int ell1_ist(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C,
              const double* stages, int32_t nstages, const ell1_io_t* io, void* stream);
 
+/* Projected gradient on the nonnegative split — replaces
+ * gradient_projection.gpsr_solve (gradient_projection.py:114-192).  lam is the
+ * resolved penalty (> 0); z_out (optional, 2 * n(+d)) receives [x+; x-].
+ * state.rot[2]: 1 = "zero projected gradient before kkt tolerance",
+ * 2 = "projection backtracking stalled" (the reference's notes). */
+size_t ell1_gpsr_workspace(const ell1_dict_t* D, int32_t blocks);
+int ell1_gpsr(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C, double lam,
+              double* z_out, const ell1_io_t* io, void* stream);
+
 /* library / device info */
 int ell1_device_sms(int32_t device);
 const char* ell1_version(void);
