@@ -206,6 +206,16 @@ size_t ell1_gpsr_workspace(const ell1_dict_t* D, int32_t blocks);
 int ell1_gpsr(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C, double lam,
               double* z_out, const ell1_io_t* io, void* stream);
 
+/* Truncated-Newton log-barrier interior point with on-device diagonally
+ * preconditioned CG — replaces gradient_projection.tnipm_solve
+ * (gradient_projection.py:218-339) and numerics.pcg_solve (numerics.py:164-221).
+ * pcg_max_iter <= 0: the system dimension.  u_out optional.  state.rot[0] =
+ * number of Newton steps whose CG hit its cap (the reference's note). */
+size_t ell1_tnipm_workspace(const ell1_dict_t* D, int32_t blocks);
+int ell1_tnipm(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C, double lam,
+               double pcg_tol, int32_t pcg_max_iter, double* u_out, const ell1_io_t* io,
+               void* stream);
+
 /* library / device info */
 int ell1_device_sms(int32_t device);
 const char* ell1_version(void);

@@ -110,6 +110,9 @@ _SIGS = {
     "ell1_gpsr_workspace": (ctypes.c_size_t, [P(Dict), ctypes.c_int32]),
     "ell1_gpsr": (ctypes.c_int, [P(Dict), ctypes.c_void_p, P(Ctrl), ctypes.c_double, ctypes.c_void_p,
                                  P(IO), ctypes.c_void_p]),
+    "ell1_tnipm_workspace": (ctypes.c_size_t, [P(Dict), ctypes.c_int32]),
+    "ell1_tnipm": (ctypes.c_int, [P(Dict), ctypes.c_void_p, P(Ctrl), ctypes.c_double, ctypes.c_double,
+                                  ctypes.c_int32, ctypes.c_void_p, P(IO), ctypes.c_void_p]),
     "ell1_device_sms": (ctypes.c_int, [ctypes.c_int32]),
     "ell1_version": (ctypes.c_char_p, []),
 }

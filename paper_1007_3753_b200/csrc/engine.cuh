@@ -255,6 +255,17 @@ __device__ __forceinline__ void gather(const Ctx& E, double (&out)[K], unsigned 
   __syncthreads();
 }
 
+// Grid-wide reduction of K per-thread values in one barrier (block reduce,
+// publish, barrier, fixed-order gather).  Returns false on barrier failure.
+template <int K>
+__device__ __forceinline__ bool allreduce(Ctx& E, double (&v)[K], unsigned maxmask) {
+  block_reduce<K>(E, v, maxmask);
+  publish<K>(E, v);
+  if (!grid_sync(E)) return false;
+  gather<K>(E, v, maxmask);
+  return true;
+}
+
 // Fused phase after the barrier that follows panel_gemv: the K scalar
 // gathers and, for every owned row i, sums[v] = sum_c part[c][v*ld + i]
 // (fixed order), then f(i, sums, aux) on lane 0 of the row's warp, with
