@@ -216,6 +216,22 @@ int ell1_tnipm(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C, doub
                double pcg_tol, int32_t pcg_max_iter, double* u_out, const ell1_io_t* io,
                void* stream);
 
+/* LASSO solution path — replaces homotopy.solve_path / homotopy_solve
+ * (homotopy.py:128-261) with the active-set Cholesky upkeep of numerics
+ * chol_append / chol_delete (numerics.py:115-158) on the device.
+ * state.scal[0] = reached lambda; state.rot[0] = support size;
+ * state.rot[1] = 1 when the "ridge-regularized gram" fallback was used. */
+typedef struct {
+  double* c;           /* required: final correlations A^T(b - A x), n(+d) */
+  double* lam_path;    /* optional: lambda after each breakpoint (max_iter) */
+  int32_t* support;    /* optional: support list in insertion order (capacity) */
+  double* factor;      /* optional: upper factor, m x m row-major */
+} ell1_homotopy_out_t;
+int ell1_homotopy_capacity(const ell1_dict_t* D);
+size_t ell1_homotopy_workspace(const ell1_dict_t* D, int32_t blocks);
+int ell1_homotopy(const ell1_dict_t* D, const double* b, double target_lambda, int32_t max_iter,
+                  const ell1_homotopy_out_t* out, const ell1_io_t* io, void* stream);
+
 /* library / device info */
 int ell1_device_sms(int32_t device);
 const char* ell1_version(void);

@@ -62,6 +62,11 @@ class PalmOpts(ctypes.Structure):
                 ("y_out", ctypes.c_void_p)]
 
 
+class HomOut(ctypes.Structure):
+    _fields_ = [("c", ctypes.c_void_p), ("lam_path", ctypes.c_void_p), ("support", ctypes.c_void_p),
+                ("factor", ctypes.c_void_p)]
+
+
 class IO(ctypes.Structure):
     _fields_ = [("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
                 ("state", ctypes.c_void_p), ("trace", ctypes.c_void_p),
@@ -113,6 +118,10 @@ _SIGS = {
     "ell1_tnipm_workspace": (ctypes.c_size_t, [P(Dict), ctypes.c_int32]),
     "ell1_tnipm": (ctypes.c_int, [P(Dict), ctypes.c_void_p, P(Ctrl), ctypes.c_double, ctypes.c_double,
                                   ctypes.c_int32, ctypes.c_void_p, P(IO), ctypes.c_void_p]),
+    "ell1_homotopy_capacity": (ctypes.c_int, [P(Dict)]),
+    "ell1_homotopy_workspace": (ctypes.c_size_t, [P(Dict), ctypes.c_int32]),
+    "ell1_homotopy": (ctypes.c_int, [P(Dict), ctypes.c_void_p, ctypes.c_double, ctypes.c_int32,
+                                     P(HomOut), P(IO), ctypes.c_void_p]),
     "ell1_device_sms": (ctypes.c_int, [ctypes.c_int32]),
     "ell1_version": (ctypes.c_char_p, []),
 }
