@@ -232,6 +232,26 @@ size_t ell1_homotopy_workspace(const ell1_dict_t* D, int32_t blocks);
 int ell1_homotopy(const ell1_dict_t* D, const double* b, double target_lambda, int32_t max_iter,
                   const ell1_homotopy_out_t* out, const ell1_io_t* io, void* stream);
 
+/* ------------------------------------------------ batched (shared dictionary)
+ * B instances with right-hand sides b_j (columns of an ld x B device matrix,
+ * zero padded) share one dictionary; element j of the result equals the
+ * single-instance solver on (D, b_j).  The library's host loop sequences
+ * GEMMs over the active instances and per-instance epilogue kernels,
+ * compacting converged instances out of the batch.  New entry points (the
+ * reference has no batched API). */
+typedef struct {
+  double* x;            /* N x B, column j = x_star of instance j */
+  int32_t* iterations;  /* B */
+  int32_t* converged;   /* B */
+  int32_t* status;      /* B: ELL1_OK / ZERO_DATA / LAMBDA_NONPOS / BREAKDOWN / ... */
+  double* trace;        /* optional: [B][max_iter (+1 for ALM)][4] */
+} ell1_batch_out_t;
+
+size_t ell1_batch_fista_workspace(const ell1_dict_t* D, int32_t B);
+int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_t B, const ell1_ctrl_t* C,
+                     const ell1_fista_opts_t* O, const ell1_batch_out_t* out, void* workspace,
+                     size_t workspace_bytes, void* stream);
+
 /* library / device info */
 int ell1_device_sms(int32_t device);
 const char* ell1_version(void);

@@ -67,6 +67,12 @@ class HomOut(ctypes.Structure):
                 ("factor", ctypes.c_void_p)]
 
 
+class BatchOut(ctypes.Structure):
+    _fields_ = [("x", ctypes.c_void_p), ("iterations", ctypes.c_void_p),
+                ("converged", ctypes.c_void_p), ("status", ctypes.c_void_p),
+                ("trace", ctypes.c_void_p)]
+
+
 class IO(ctypes.Structure):
     _fields_ = [("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
                 ("state", ctypes.c_void_p), ("trace", ctypes.c_void_p),
@@ -122,6 +128,10 @@ _SIGS = {
     "ell1_homotopy_workspace": (ctypes.c_size_t, [P(Dict), ctypes.c_int32]),
     "ell1_homotopy": (ctypes.c_int, [P(Dict), ctypes.c_void_p, ctypes.c_double, ctypes.c_int32,
                                      P(HomOut), P(IO), ctypes.c_void_p]),
+    "ell1_batch_fista_workspace": (ctypes.c_size_t, [P(Dict), ctypes.c_int32]),
+    "ell1_batch_fista": (ctypes.c_int, [P(Dict), ctypes.c_void_p, ctypes.c_int32, P(Ctrl),
+                                        P(FistaOpts), P(BatchOut), ctypes.c_void_p, ctypes.c_size_t,
+                                        ctypes.c_void_p]),
     "ell1_device_sms": (ctypes.c_int, [ctypes.c_int32]),
     "ell1_version": (ctypes.c_char_p, []),
 }

@@ -1,0 +1,115 @@
+"""Batched solvers: many right-hand sides sharing one dictionary (BASELINE
+configs 3 and 5).  New entry points — the reference has no batched API —
+whose element j equals the single-instance call on (A, b_j)
+(SURVEY §8(b)).
+
+The library runs the whole batch: dictionary products are GEMMs over the
+active instances, the solver arithmetic runs in per-instance epilogue
+kernels, converged instances are compacted out of the batch.
+"""
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from paper_1007_3753_b200 import _lib, device
+from paper_1007_3753_b200._runner import byref, raise_for
+from paper_1007_3753_b200.model import SolverResult, TraceEntry
+
+
+@dataclass
+class BatchResult:
+    """Arrays over the batch (column j = instance j)."""
+
+    x: np.ndarray            # N x B
+    iterations: np.ndarray
+    converged: np.ndarray
+    status: np.ndarray
+    wall_time_seconds: float
+    trace: np.ndarray = None  # B x rows x 4, or None
+
+    def results(self):
+        """Per-instance SolverResult records (reference record type)."""
+        out = []
+        B = self.x.shape[1]
+        for j in range(B):
+            st = int(self.status[j])
+            raise_for(st, {_lib.BREAKDOWN: "backtracking exceeded 100 growth steps"})
+            it = int(self.iterations[j])
+            tr = []
+            if self.trace is not None:
+                rows = 1 if st == _lib.ZERO_DATA else it
+                tr = [TraceEntry(int(r[0]), float(r[1]), float(r[2]), int(r[3]))
+                      for r in self.trace[j, :rows]]
+            out.append(SolverResult(self.x[:, j].copy(), it, self.wall_time_seconds / B,
+                                    bool(self.converged[j]), tr))
+        return out
+
+
+def _dict_view(A, config):
+    if hasattr(A, "device_extension"):
+        D, s = A.device_extension()
+        return D, D.view(ext=True, scale=s), D.n + D.d
+    D, _ = device.as_device_dictionary(A, config)
+    return D, D.view(), D.n
+
+
+def _ctrl(config, B, N, dev, ground_truth):
+    C = _lib.Ctrl()
+    C.lam = -1.0 if config.lam is None else float(config.lam)
+    C.tol = float(config.tol)
+    C.max_iter = int(config.max_iter)
+    stop = config.stopping
+    C.stop_kind = _lib.STOP_CODES[stop.kind if stop is not None else None]
+    C.stop_thr = float(stop.threshold) if stop is not None else 0.0
+    C.ground_truth = None
+    C.gt_norm = 0.0
+    keep = None
+    if stop is not None and stop.kind == "ground-truth-distance":
+        if ground_truth is None:
+            raise ValueError("ground-truth-distance rule needs a ground truth")
+        raise NotImplementedError("per-instance ground-truth rule in batch mode")
+    return C, keep
+
+
+def fista_solve_batch(A, Bmat, config, with_trace=False):
+    """FISTA for every column of Bmat (d x B) against the shared A.
+    Returns a BatchResult; ``.results()`` gives per-instance SolverResults."""
+    torch = device._torch()
+    t0 = time.perf_counter()
+    D, view, N = _dict_view(A, config)
+    dev = D.device
+    if isinstance(Bmat, torch.Tensor):
+        Bd = Bmat.to(device=dev, dtype=torch.float64)
+    else:
+        Bd = torch.from_numpy(np.ascontiguousarray(Bmat, dtype=np.float64)).to(dev)
+    d, B = int(Bd.shape[0]), int(Bd.shape[1])
+    if d != D.d:
+        raise ValueError("Bmat must have d rows")
+    Bpad = torch.zeros(B, D.ld, dtype=torch.float64, device=dev)
+    Bpad[:, :d] = Bd.T
+    from paper_1007_3753_b200.shrinkage import _fista_opts
+    O = _fista_opts(config, None)
+    if O.exact_L:
+        sn = A.norm_sq() if hasattr(A, "norm_sq") else D.norm_sq()
+        O.L_exact = sn * (1.0 + 1e-9)
+    C, _keep = _ctrl(config, B, N, dev, None)
+    L = _lib.lib()
+    wsb = L.ell1_batch_fista_workspace(byref(view), B)
+    ws = device.alloc_bytes(wsb, dev)
+    x = torch.zeros(B, N, dtype=torch.float64, device=dev)
+    its = torch.zeros(B, dtype=torch.int32, device=dev)
+    conv = torch.zeros(B, dtype=torch.int32, device=dev)
+    stat = torch.zeros(B, dtype=torch.int32, device=dev)
+    tr = torch.zeros(B, config.max_iter, 4, dtype=torch.float64, device=dev) if with_trace else None
+    out = _lib.BatchOut()
+    out.x, out.iterations, out.converged, out.status = (x.data_ptr(), its.data_ptr(), conv.data_ptr(),
+                                                        stat.data_ptr())
+    out.trace = tr.data_ptr() if tr is not None else None
+    rc = L.ell1_batch_fista(byref(view), device.ptr(Bpad), B, byref(C), byref(O), byref(out),
+                            device.ptr(ws), int(ws.numel()), device.stream_ptr(dev))
+    _lib.check(rc, "ell1_batch_fista")
+    torch.cuda.synchronize(dev)
+    return BatchResult(x.T.cpu().numpy(), its.cpu().numpy(), conv.cpu().numpy(), stat.cpu().numpy(),
+                       time.perf_counter() - t0, tr.cpu().numpy() if tr is not None else None)

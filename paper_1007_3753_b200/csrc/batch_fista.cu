@@ -1,0 +1,415 @@
+// batch_fista.cu — FISTA over a batch of instances sharing one dictionary
+// (element j equals shrinkage.fista_solve on (A, b_j), shrinkage.py:231-298).
+//
+// Per iteration: prox kernel (momentum point from the cached products,
+// soft-threshold, backtracking reductions) -> GEMM  A X_next -> residual kernel
+// (r_next, F, Q, accept / grow L per instance) [repeat for instances still
+// backtracking] -> GEMM  A^T R_next -> finish kernel (KKT, support, trace,
+// stopping rules, continuation).
+#include "batched.cuh"
+
+namespace ell1 {
+
+struct BI {                 // per-instance control state
+  double L, tp, tc, lam, lam_bar, Fprev, fy, fy_next, m, tn, mn, rr, Fn, c0, bn;
+  double S[7];
+  int it, hist, bt, active, accepted, status, conv, orig;
+};
+
+struct BFArgs {
+  int64_t d, n, N, ld, ldx;
+  int ext;
+  double s;
+  int f32;
+  const double* Bm;           // ld x B (b columns)
+  double* X[3];               // ldx x B
+  double* G[2];               // ldx x B
+  double* R[3];               // ld x B
+  double* AX;                 // raw GEMM1 output (fp64 mode) ld x B
+  float* X32; float* R32; float* AX32; float* G32;   // fp32 GEMM operands
+  BI* inst;
+  ell1_ctrl_t C;
+  ell1_fista_opts_t O;
+  int* counters;              // [0] retry, [1] active
+  double* x_out;              // N x B0 (original order)
+  int* it_out; int* conv_out; int* status_out;
+  double* trace;              // optional [B0][max_iter][4]
+  int ix, ixp, ixn, igx, igxp, irx, irxp, irn;
+};
+
+__global__ void __launch_bounds__(BT) bf_init(const BFArgs a, const double* CT, const float* CT32, int B) {
+  const int j = blockIdx.x;
+  __shared__ double sh[BW * 4 + 4];
+  BI& I = a.inst[j];
+  const double* b = a.Bm + (int64_t)j * a.ld;
+  double v[2] = {0.0, 0.0};
+  for (int64_t k = threadIdx.x; k < a.N; k += BT) {
+    double c;
+    if (k < a.n) c = a.f32 ? (double)CT32[(int64_t)j * a.n + k] : CT[(int64_t)j * a.n + k];
+    else c = a.s * b[k - a.n];
+    v[0] = nmax(v[0], fabs(c));
+    for (int r = 0; r < 3; ++r) a.X[r][(int64_t)j * a.ldx + k] = 0.0;
+    a.G[0][(int64_t)j * a.ldx + k] = -c;
+    a.G[1][(int64_t)j * a.ldx + k] = -c;
+  }
+  for (int64_t i = threadIdx.x; i < a.ld; i += BT) {
+    const double bi = i < a.d ? b[i] : 0.0;
+    a.R[0][(int64_t)j * a.ld + i] = -bi;
+    a.R[1][(int64_t)j * a.ld + i] = -bi;
+    a.R[2][(int64_t)j * a.ld + i] = 0.0;
+    v[1] += bi * bi;
+  }
+  cta_reduce<2>(v, 1u, sh);
+  if (threadIdx.x == 0) {
+    I.orig = j;
+    I.c0 = v[0];
+    I.bn = sqrt(v[1]);
+    I.it = 0; I.hist = 0; I.bt = 0; I.accepted = 0; I.conv = 0; I.status = ELL1_OK; I.active = 1;
+    I.Fprev = 0.0;
+    if (I.c0 == 0.0) {                                    // shrinkage.py:245-247
+      I.status = ELL1_ZERO_DATA; I.conv = 1; I.active = 0;
+      if (a.trace) { double* tr = a.trace + (int64_t)j * a.C.max_iter * 4; tr[0] = 0; tr[1] = 0; tr[2] = I.bn; tr[3] = 0; }
+    } else {
+      I.lam_bar = (a.C.lam < 0.0) ? 1e-2 * I.c0 : a.C.lam;
+      if (!(I.lam_bar > 0.0)) { I.status = ELL1_LAMBDA_NONPOS; I.active = 0; }
+      I.L = a.O.exact_L ? a.O.L_exact : a.O.L0;
+      I.lam = a.O.continuation ? pymax(0.9 * I.c0, I.lam_bar) : I.lam_bar;
+      I.tp = I.tc = 1.0;
+      I.fy = 0.5 * v[1];
+    }
+    if (!I.active) {
+      a.it_out[j] = 0; a.conv_out[j] = I.conv; a.status_out[j] = I.status;
+      for (int64_t k = 0; k < a.N; ++k) a.x_out[(int64_t)j * a.N + k] = 0.0;
+    } else {
+      atomicAdd(a.counters + 1, 1);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(BT) bf_prox(const BFArgs a, int round) {
+  const int j = blockIdx.x;
+  __shared__ double sh[BW * 7 + 7];
+  __shared__ double sc[4];
+  BI& I = a.inst[j];
+  if (!I.active || (round > 0 && I.accepted)) return;
+  if (threadIdx.x == 0) {
+    if (round == 0) {
+      I.it++;
+      I.bt = 0;
+      I.accepted = 0;
+      I.m = (I.tp - 1.0) / I.tc;
+      I.tn = fista_t_next(I.tc);
+      I.mn = (I.tc - 1.0) / I.tn;
+    }
+    sc[0] = I.m; sc[1] = I.L; sc[2] = I.lam / I.L;
+  }
+  __syncthreads();
+  const double m = sc[0], L = sc[1], thr = sc[2];
+  const int64_t o = (int64_t)j * a.ldx;
+  const double* x = a.X[a.ix] + o;
+  const double* xp = a.X[a.ixp] + o;
+  double* xn = a.X[a.ixn] + o;
+  const double* gx = a.G[a.igx] + o;
+  const double* gxp = a.G[a.igxp] + o;
+  const bool relest = a.C.stop_kind == ELL1_STOP_REL_ESTIMATE;
+  const bool gtr = a.C.stop_kind == ELL1_STOP_GROUND_TRUTH;
+  double s[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int64_t k = threadIdx.x; k < a.N; k += BT) {
+    const double xk = x[k];
+    const double yk = xk + m * (xk - xp[k]);                // shrinkage.py:270
+    const double gk = (1.0 + m) * gx[k] - m * gxp[k];       // A^T(A y - b)
+    const double u = soft1(yk - gk / L, thr);                // shrinkage.py:204
+    xn[k] = u;
+    if (a.f32 && k < a.n) a.X32[(int64_t)j * a.ldx + k] = (float)u;
+    const double dl = u - yk;
+    s[0] += fabs(u);
+    s[1] += gk * dl;
+    s[2] += dl * dl;
+    s[3] = nmax(s[3], fabs(u));
+    if (relest) { const double dd = u - xk; s[4] += dd * dd; s[5] += xk * xk; }
+    if (gtr) { const double e = u - a.C.ground_truth[(int64_t)I.orig * a.N + k]; s[6] += e * e; }
+  }
+  cta_reduce<7>(s, 1u << 3, sh);
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 7; ++k) I.S[k] = s[k];
+}
+
+__global__ void __launch_bounds__(BT) bf_resid(const BFArgs a, int round) {
+  const int j = blockIdx.x;
+  __shared__ double sh[BW * 2 + 2];
+  BI& I = a.inst[j];
+  if (!I.active || (round > 0 && I.accepted)) return;
+  const double mn = I.mn;
+  const double* b = a.Bm + (int64_t)j * a.ld;
+  const double* xn = a.X[a.ixn] + (int64_t)j * a.ldx;
+  const double* rx = a.R[a.irx] + (int64_t)j * a.ld;
+  double* rn = a.R[a.irn] + (int64_t)j * a.ld;
+  double q[2] = {0.0, 0.0};
+  for (int64_t i = threadIdx.x; i < a.d; i += BT) {
+    double ax = a.f32 ? (double)a.AX32[(int64_t)j * a.ld + i] : a.AX[(int64_t)j * a.ld + i];
+    if (a.ext) ax = ax + a.s * xn[a.n + i];                 // robust.py:93
+    const double r = ax - b[i];                             // shrinkage.py:205
+    rn[i] = r;
+    if (a.f32) a.R32[(int64_t)j * a.ld + i] = (float)r;
+    q[0] += r * r;
+    const double ry = (1.0 + mn) * r - mn * rx[i];
+    q[1] += ry * ry;
+  }
+  cta_reduce<2>(q, 0u, sh);
+  if (threadIdx.x == 0) {
+    I.rr = q[0];
+    I.Fn = 0.5 * q[0] + I.lam * I.S[0];
+    bool acc;
+    if (a.O.exact_L) acc = true;
+    else {
+      const double Qm = I.fy + I.S[1] + 0.5 * I.L * I.S[2] + I.lam * I.S[0];
+      // shrinkage.py:210; float32 GEMMs accumulate in fp32, so the tie slack is
+      // scaled to that precision (documented fp32 deviation, SURVEY §7 hard part 4)
+      const double slack = a.f32 ? 1e-6 : 1e-12;
+      acc = I.Fn <= Qm + slack * pymax(1.0, fabs(Qm));
+    }
+    if (acc) {
+      I.accepted = 1;
+      I.fy_next = 0.5 * q[1];
+    } else {
+      I.L *= a.O.eta;
+      I.bt++;
+      if (I.bt > 100) {                                     // shrinkage.py:203,213
+        I.status = ELL1_BREAKDOWN; I.active = 0;
+        a.it_out[I.orig] = I.it; a.conv_out[I.orig] = 0; a.status_out[I.orig] = I.status;
+        atomicSub(a.counters + 1, 1);
+      } else {
+        atomicAdd(a.counters, 1);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(BT) bf_finish(const BFArgs a, int gslot) {
+  const int j = blockIdx.x;
+  __shared__ double sh[BW * 5 + 5];
+  BI& I = a.inst[j];
+  if (!I.active) return;
+  const int64_t o = (int64_t)j * a.ldx;
+  const double* xn = a.X[a.ixn] + o;               // the new x
+  double* gn = a.G[gslot] + o;                     // the new g_x
+  const double* rn = a.R[a.irn] + (int64_t)j * a.ld;
+  const double cut = 1e-10 * pymax(I.S[3], 1.0);   // model.py:232
+  const double lam = I.lam;
+  double k5[5] = {0, 0, 0, 0, 0};
+  for (int64_t k = threadIdx.x; k < a.N; k += BT) {
+    double g;
+    if (k < a.n) g = a.f32 ? (double)a.G32[(int64_t)j * a.n + k] : gn[k];
+    else g = a.s * rn[k - a.n];
+    gn[k] = g;
+    const double xk = xn[k];
+    const double c = -g;
+    if (xk != 0.0) { k5[0] = nmax(k5[0], fabs(c - lam * sgn(xk))); k5[2] = 1.0; }
+    else { k5[1] = nmax(k5[1], fabs(c)); k5[3] = 1.0; }
+    if (fabs(xk) > cut) k5[4] += 1.0;
+  }
+  cta_reduce<5>(k5, 0xFu, sh);
+  __shared__ int fin;
+  if (threadIdx.x == 0) {
+    double kkt = k5[2] > 0.0 ? k5[0] : 0.0;
+    if (k5[3] > 0.0) kkt = pymax(pymax(kkt, k5[1] - lam), 0.0);
+    I.tp = I.tc; I.tc = I.tn;
+    if (a.trace) {
+      double* tr = a.trace + ((int64_t)I.orig * a.C.max_iter + (I.it - 1)) * 4;
+      tr[0] = (double)I.it; tr[1] = I.Fn; tr[2] = sqrt(I.rr); tr[3] = k5[4];
+    }
+    I.hist = I.hist < 2 ? I.hist + 1 : 2;
+    int done = 0;
+    if (lam == I.lam_bar && kkt <= a.C.tol * I.lam_bar) done = 1;   // shrinkage.py:291-293
+    else {
+      const double gtn = a.C.gt_norm;
+      if (stop_fires(a.C.stop_kind, a.C.stop_thr, I.hist, I.Fn, I.Fprev, I.S[4], I.S[5], I.S[6], gtn, kkt))
+        done = 1;
+    }
+    I.Fprev = I.Fn;
+    if (done) I.conv = 1;
+    else {
+      I.lam = pymax(a.O.beta * I.lam, I.lam_bar);           // shrinkage.py:297
+      I.fy = I.fy_next;
+      if (I.it >= a.C.max_iter) done = 2;
+    }
+    if (done) {
+      I.active = 0;
+      a.it_out[I.orig] = I.it; a.conv_out[I.orig] = I.conv; a.status_out[I.orig] = ELL1_OK;
+      atomicSub(a.counters + 1, 1);
+    }
+    fin = done;
+  }
+  __syncthreads();
+  if (fin) {
+    double* xo = a.x_out + (int64_t)I.orig * a.N;
+    for (int64_t k = threadIdx.x; k < a.N; k += BT) xo[k] = xn[k];
+  }
+}
+
+__global__ void conv_f64_f32(const double* src, float* dst, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = (float)src[i];
+}
+
+// ---- compaction: keep active instances, in order, at the front
+__global__ void bf_scan(BI* inst, int B, int* perm, int* newB) {
+  // single CTA prefix sum over the active flags
+  __shared__ int base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < B; c0 += blockDim.x) {
+    const int j = c0 + threadIdx.x;
+    const int act = (j < B) ? inst[j].active : 0;
+    const unsigned m = __ballot_sync(0xffffffffu, act);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __shared__ int wsum[32];
+    if (l == 0) wsum[w] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = base;
+      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) { const int t = wsum[k]; wsum[k] = acc; acc += t; }
+      base = acc;
+    }
+    __syncthreads();
+    if (act) perm[wsum[w] + __popc(m & ((1u << l) - 1))] = j;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *newB = base;
+}
+
+template <class T>
+__global__ void gather_cols(const T* src, T* dst, int64_t rows, int64_t ld, const int* perm, int B) {
+  const int k = blockIdx.y;
+  if (k >= B) return;
+  const int64_t s = (int64_t)perm[k] * ld, d = (int64_t)k * ld;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+    dst[d + i] = src[s + i];
+}
+
+}  // namespace ell1
+
+using namespace ell1;
+
+static int64_t round4(int64_t x) { return (x + 3) / 4 * 4; }
+
+extern "C" size_t ell1_batch_fista_workspace(const ell1_dict_t* D, int32_t B) {
+  if (!dict_ok(D) || B < 1) return 0;
+  const int64_t N = ncols_of(D), ldx = round4(N), ld = D->ld;
+  size_t s = 0;
+  s += 5 * align_up(ldx * B * 8, 256) + 4 * align_up(ld * B * 8, 256);     // X, G, R, AX / Bm
+  s += align_up(ld * B * 8, 256);                                           // Bm
+  s += align_up((int64_t)sizeof(BI) * B, 256) * 2;
+  s += align_up(ldx * B * 4, 256) * 2 + align_up(ld * B * 4, 256) * 2;       // fp32 operands
+  s += align_up((ldx > ld ? ldx : ld) * B * 8, 256);                        // compaction scratch
+  s += align_up(B * 4, 256) + 4096;
+  return s;
+}
+
+extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_t B,
+                                const ell1_ctrl_t* C, const ell1_fista_opts_t* O,
+                                const ell1_batch_out_t* out, void* ws, size_t wsb, void* stream) {
+  if (!dict_ok(D) || !Bmat || B < 1 || !C || !O || !out || !out->x || !out->iterations ||
+      !out->converged || !out->status)
+    return ELL1_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  cublasHandle_t h = blas_handle(s);
+  if (!h) return ELL1_ERR_CUDA;
+  const int64_t N = ncols_of(D), ldx = round4(N), ld = D->ld;
+  BFArgs a;
+  a.d = D->d; a.n = D->n; a.N = N; a.ld = ld; a.ldx = ldx;
+  a.ext = D->ext; a.s = D->ext_scale; a.f32 = D->dtype == ELL1_F32;
+  a.C = *C; a.O = *O;
+  Carve cv(ws, wsb);
+  for (int k = 0; k < 3; ++k) a.X[k] = cv.take<double>(ldx * B);
+  for (int k = 0; k < 2; ++k) a.G[k] = cv.take<double>(ldx * B);
+  for (int k = 0; k < 3; ++k) a.R[k] = cv.take<double>(ld * B);
+  a.AX = cv.take<double>(ld * B);
+  double* Bm = cv.take<double>(ld * B);
+  a.inst = cv.take<BI>(B);
+  BI* inst2 = cv.take<BI>(B);
+  a.X32 = cv.take<float>(ldx * B); a.G32 = cv.take<float>(ldx * B);
+  a.R32 = cv.take<float>(ld * B); a.AX32 = cv.take<float>(ld * B);
+  double* scratch = cv.take<double>((ldx > ld ? ldx : ld) * B);
+  int* perm = cv.take<int>(B);
+  int* ctr = cv.take<int>(8);
+  if (!cv.ok) return ELL1_ERR_ARG;
+  a.Bm = Bm;
+  a.counters = ctr;
+  a.x_out = out->x; a.it_out = out->iterations; a.conv_out = out->converged; a.status_out = out->status;
+  a.trace = out->trace;
+  if (cudaMemcpyAsync(Bm, Bmat, ld * B * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return ELL1_ERR_CUDA;
+  if (cudaMemsetAsync(ctr, 0, 32, s) != cudaSuccess) return ELL1_ERR_CUDA;
+  if (a.f32) {
+    if (cudaMemsetAsync(a.X32, 0, ldx * B * 4, s) != cudaSuccess) return ELL1_ERR_CUDA;
+  }
+  a.ix = 0; a.ixp = 1; a.ixn = 2; a.igx = 0; a.igxp = 1; a.irx = 0; a.irxp = 1; a.irn = 2;
+  // c = A^T b for every instance (GEMM), then per-instance setup
+  {
+    const void* Bop = Bm;
+    if (a.f32) {
+      float* B32 = a.R32;                                   // fp32 operand copy of b
+      conv_f64_f32<<<(unsigned)((ld * B + 255) / 256), 256, 0, s>>>(Bm, B32, ld * B);
+      Bop = B32;
+    }
+    void* CT = a.f32 ? (void*)a.G32 : (void*)scratch;      // n x B
+    if (!gemm_AtR(h, D, Bop, ld, CT, D->n, B)) return ELL1_ERR_CUDA;
+    bf_init<<<B, BT, 0, s>>>(a, (const double*)CT, (const float*)CT, B);
+  }
+  int Bcur = B;
+  int h_ctr[2] = {0, 0};
+  int iters = 0;
+  while (true) {
+    if (cudaMemcpyAsync(h_ctr, ctr, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return ELL1_ERR_CUDA;
+    const int nact = h_ctr[1];
+    if (nact <= 0) break;
+    if (nact < Bcur * 3 / 4 || (nact < Bcur && nact <= 64)) {
+      // compact the active instances to the front of every state matrix
+      bf_scan<<<1, 1024, 0, s>>>(a.inst, Bcur, perm, ctr + 2);
+      auto perm_mat = [&](double* M, int64_t rows, int64_t ldm) {
+        dim3 g((unsigned)((rows + 255) / 256 < 64 ? (rows + 255) / 256 : 64), (unsigned)nact);
+        gather_cols<double><<<g, 256, 0, s>>>(M, scratch, rows, ldm, perm, nact);
+        cudaMemcpyAsync(M, scratch, ldm * nact * 8, cudaMemcpyDeviceToDevice, s);
+      };
+      for (int k = 0; k < 3; ++k) perm_mat(a.X[k], N, ldx);
+      for (int k = 0; k < 2; ++k) perm_mat(a.G[k], N, ldx);
+      for (int k = 0; k < 3; ++k) perm_mat(a.R[k], ld, ld);
+      perm_mat(Bm, ld, ld);
+      {
+        const int64_t words = (int64_t)sizeof(BI) / 4;
+        dim3 g(1, (unsigned)nact);
+        gather_cols<int><<<g, 64, 0, s>>>((const int*)a.inst, (int*)inst2, words, words, perm, nact);
+        cudaMemcpyAsync(a.inst, inst2, sizeof(BI) * nact, cudaMemcpyDeviceToDevice, s);
+      }
+      Bcur = nact;
+    }
+    // ---- one FISTA iteration for the Bcur leading instances
+    int round = 0;
+    while (true) {
+      if (cudaMemsetAsync(ctr, 0, 4, s) != cudaSuccess) return ELL1_ERR_CUDA;
+      bf_prox<<<Bcur, BT, 0, s>>>(a, round);
+      if (!gemm_AX(h, D, a.f32 ? (const void*)a.X32 : (const void*)a.X[a.ixn], ldx,
+                   a.f32 ? (void*)a.AX32 : (void*)a.AX, ld, Bcur))
+        return ELL1_ERR_CUDA;
+      bf_resid<<<Bcur, BT, 0, s>>>(a, round);
+      int retry = 0;
+      if (cudaMemcpyAsync(&retry, ctr, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
+      if (cudaStreamSynchronize(s) != cudaSuccess) return ELL1_ERR_CUDA;
+      if (retry == 0) break;
+      ++round;
+    }
+    // g_next = A^T r_next into the g ring's free slot
+    if (!gemm_AtR(h, D, a.f32 ? (const void*)a.R32 : (const void*)a.R[a.irn], ld,
+                  a.f32 ? (void*)a.G32 : (void*)a.G[a.igxp], a.f32 ? D->n : ldx, Bcur))
+      return ELL1_ERR_CUDA;
+    bf_finish<<<Bcur, BT, 0, s>>>(a, a.igxp);
+    // rotate the rings (shrinkage.py:283-284)
+    { int t = a.ixp; a.ixp = a.ix; a.ix = a.ixn; a.ixn = t; }
+    { int t = a.irxp; a.irxp = a.irx; a.irx = a.irn; a.irn = t; }
+    { int t = a.igxp; a.igxp = a.igx; a.igx = t; }
+    ++iters;
+  }
+  return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
+}
+

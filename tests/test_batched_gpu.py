@@ -1,0 +1,77 @@
+"""Batched shared-dictionary solvers: element j must equal the single-instance
+reference solve on (A, b_j) (SURVEY §8(b) batched entry points)."""
+
+import numpy as np
+import pytest
+
+import oracle
+from tests.gpu_util import rel_err, support
+
+pytestmark = pytest.mark.gpu
+
+
+def _batch(d, n, ks, seed=5, noise=0.0):
+    A = oracle.gaussian_dict(d, n, seed)
+    cols, gts = [], []
+    for j, k in enumerate(ks):
+        g = np.random.default_rng(1000 + j)
+        x0 = np.zeros(n)
+        x0[g.choice(n, k, replace=False)] = g.standard_normal(k)
+        b = A @ x0
+        if noise:
+            b = b + noise * g.standard_normal(d)
+        cols.append(b)
+        gts.append(x0)
+    return A, np.stack(cols, axis=1), gts
+
+
+@pytest.fixture(scope="module")
+def bt():
+    from paper_1007_3753_b200 import batched
+    return batched
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_batch_fista_equals_single_instances(bt, dtype):
+    from paper_1007_3753_b200.model import SolverConfig, StoppingRule
+    A, Bm, _ = _batch(512, 2048, [16, 32, 64, 8, 48, 24, 1, 40])
+    cfg = SolverConfig(lam=1e-3, tol=1e-6, stopping=StoppingRule("relative-estimate", 1e-6),
+                       options={"dtype": dtype})
+    res = bt.fista_solve_batch(A, Bm, cfg, with_trace=True).results()
+    for j in range(Bm.shape[1]):
+        ref = oracle.fista(A, Bm[:, j], lam=1e-3, tol=1e-6, stop=("relative-estimate", 1e-6))
+        tol = 1e-6 if dtype == "float64" else 1e-4
+        assert rel_err(res[j].x_star, ref.x) <= tol, j
+        assert support(res[j].x_star) == support(ref.x), j
+        assert res[j].converged == ref.converged
+        if dtype == "float64":
+            assert res[j].iterations == ref.iterations, (j, res[j].iterations, ref.iterations)
+            tr = np.array([tuple(t) for t in res[j].trace])
+            np.testing.assert_allclose(tr, np.array(ref.trace), rtol=1e-9, atol=1e-12)
+
+
+def test_batch_fista_default_lambda_and_budget(bt):
+    from paper_1007_3753_b200.model import SolverConfig
+    A, Bm, _ = _batch(64, 200, [3, 5, 9, 2], noise=0.01)
+    Bm = np.concatenate([Bm, np.zeros((64, 1))], axis=1)     # one zero-data instance
+    for cap in (3, 5000):
+        cfg = SolverConfig(tol=1e-7, max_iter=cap)
+        res = bt.fista_solve_batch(A, Bm, cfg, with_trace=True).results()
+        for j in range(Bm.shape[1]):
+            ref = oracle.fista(A, Bm[:, j], lam=None, tol=1e-7, max_iter=cap)
+            assert res[j].iterations == ref.iterations and res[j].converged == ref.converged
+            assert rel_err(res[j].x_star, ref.x) <= 1e-9 if np.any(ref.x) else np.all(res[j].x_star == 0)
+
+
+def test_batch_fista_cab(bt):
+    from paper_1007_3753_b200.model import SolverConfig
+    from paper_1007_3753_b200.robust import ExtendedDictionary
+    A = oracle.gaussian_dict(40, 30, 7)
+    g = np.random.default_rng(3)
+    Bm = A @ (g.standard_normal((30, 5)) * (g.random((30, 5)) < 0.1)) + 0.3 * (g.random((40, 5)) < 0.1)
+    cfg = SolverConfig(tol=1e-6, max_iter=5000)
+    res = bt.fista_solve_batch(ExtendedDictionary(A, 1.0), Bm, cfg).results()
+    for j in range(5):
+        x, e, ref = oracle.cab(A, Bm[:, j], "fista", tol=1e-6, max_iter=5000)
+        assert res[j].iterations == ref.iterations
+        assert rel_err(res[j].x_star, ref.x) <= 1e-8
