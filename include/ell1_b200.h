@@ -252,6 +252,13 @@ int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_t B, const 
                      const ell1_fista_opts_t* O, const ell1_batch_out_t* out, void* workspace,
                      size_t workspace_bytes, void* stream);
 
+/* Batched dual ALM (exact y-step; y_cg_step not supported in batch mode).
+ * trace rows: [B][max_iter + 1][4] (row 0 = the initial entry). */
+size_t ell1_batch_dalm_workspace(const ell1_dict_t* D, int32_t B);
+int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t B, const ell1_ctrl_t* C,
+                    const ell1_dalm_opts_t* O, const ell1_batch_out_t* out, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
 /* library / device info */
 int ell1_device_sms(int32_t device);
 const char* ell1_version(void);

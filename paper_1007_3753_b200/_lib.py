@@ -132,6 +132,10 @@ _SIGS = {
     "ell1_batch_fista": (ctypes.c_int, [P(Dict), ctypes.c_void_p, ctypes.c_int32, P(Ctrl),
                                         P(FistaOpts), P(BatchOut), ctypes.c_void_p, ctypes.c_size_t,
                                         ctypes.c_void_p]),
+    "ell1_batch_dalm_workspace": (ctypes.c_size_t, [P(Dict), ctypes.c_int32]),
+    "ell1_batch_dalm": (ctypes.c_int, [P(Dict), ctypes.c_void_p, ctypes.c_int32, P(Ctrl),
+                                       P(DalmOpts), P(BatchOut), ctypes.c_void_p, ctypes.c_size_t,
+                                       ctypes.c_void_p]),
     "ell1_device_sms": (ctypes.c_int, [ctypes.c_int32]),
     "ell1_version": (ctypes.c_char_p, []),
 }

@@ -28,6 +28,8 @@ class BatchResult:
     status: np.ndarray
     wall_time_seconds: float
     trace: np.ndarray = None  # B x rows x 4, or None
+    kind: str = "fista"
+    max_iter: int = 0
 
     def results(self):
         """Per-instance SolverResult records (reference record type)."""
@@ -35,15 +37,22 @@ class BatchResult:
         B = self.x.shape[1]
         for j in range(B):
             st = int(self.status[j])
-            raise_for(st, {_lib.BREAKDOWN: "backtracking exceeded 100 growth steps"})
+            raise_for(st, {_lib.BREAKDOWN: "backtracking exceeded 100 growth steps",
+                           _lib.ILL_CONDITIONED: "dual least-squares step failed its residual contract"})
             it = int(self.iterations[j])
             tr = []
             if self.trace is not None:
-                rows = 1 if st == _lib.ZERO_DATA else it
+                if st == _lib.ZERO_DATA:
+                    rows = 1
+                else:
+                    rows = it + 1 if self.kind == "dalm" else it
                 tr = [TraceEntry(int(r[0]), float(r[1]), float(r[2]), int(r[3]))
                       for r in self.trace[j, :rows]]
+            notes = ()
+            if self.kind == "dalm" and not self.converged[j] and it >= self.max_iter:
+                notes = ("iteration budget exhausted",)
             out.append(SolverResult(self.x[:, j].copy(), it, self.wall_time_seconds / B,
-                                    bool(self.converged[j]), tr))
+                                    bool(self.converged[j]), tr, notes))
         return out
 
 
@@ -71,6 +80,78 @@ def _ctrl(config, B, N, dev, ground_truth):
             raise ValueError("ground-truth-distance rule needs a ground truth")
         raise NotImplementedError("per-instance ground-truth rule in batch mode")
     return C, keep
+
+
+def _upload_rhs(Bmat, D):
+    torch = device._torch()
+    dev = D.device
+    if isinstance(Bmat, torch.Tensor):
+        Bd = Bmat.to(device=dev, dtype=torch.float64)
+    else:
+        Bd = torch.from_numpy(np.ascontiguousarray(Bmat, dtype=np.float64)).to(dev)
+    d, B = int(Bd.shape[0]), int(Bd.shape[1])
+    if d != D.d:
+        raise ValueError("Bmat must have d rows")
+    Bpad = torch.zeros(B, D.ld, dtype=torch.float64, device=dev)
+    Bpad[:, :d] = Bd.T
+    return Bpad, B
+
+
+def _outputs(B, N, rows, dev, with_trace):
+    torch = device._torch()
+    x = torch.zeros(B, N, dtype=torch.float64, device=dev)
+    its = torch.zeros(B, dtype=torch.int32, device=dev)
+    conv = torch.zeros(B, dtype=torch.int32, device=dev)
+    stat = torch.zeros(B, dtype=torch.int32, device=dev)
+    tr = torch.zeros(B, rows, 4, dtype=torch.float64, device=dev) if with_trace else None
+    out = _lib.BatchOut()
+    out.x, out.iterations, out.converged, out.status = (x.data_ptr(), its.data_ptr(), conv.data_ptr(),
+                                                        stat.data_ptr())
+    out.trace = tr.data_ptr() if tr is not None else None
+    return out, (x, its, conv, stat, tr)
+
+
+def _collect(bufs, t0, dev, trace_offset=0):
+    torch = device._torch()
+    x, its, conv, stat, tr = bufs
+    torch.cuda.synchronize(dev)
+    return BatchResult(x.T.cpu().numpy(), its.cpu().numpy(), conv.cpu().numpy(), stat.cpu().numpy(),
+                       time.perf_counter() - t0, tr.cpu().numpy() if tr is not None else None)
+
+
+def dalm_solve_batch(A, Bmat, config, with_trace=False):
+    """Dual ALM for every column of Bmat (d x B) against the shared A (or a
+    robust.ExtendedDictionary for CAB batches).  Element j equals
+    alm.dalm_solve on (A, b_j); option beta as in the reference."""
+    t0 = time.perf_counter()
+    D, view, N = _dict_view(A, config)
+    ext = bool(view.ext)
+    beta = float(config.opt("beta", 1.0))
+    if not beta > 0:
+        raise ValueError("beta must be positive")
+    if config.opt("y_cg_step", False):
+        raise NotImplementedError("y_cg_step is single-instance only")
+    MT, Gcm, _ = D.gram_factor(ext, view.ext_scale)
+    from paper_1007_3753_b200.alm import _Y_REFINE_TOL, _Y_REFINE_TOL_F32
+    O = _lib.DalmOpts()
+    O.beta = beta
+    O.y_tol = _Y_REFINE_TOL if D.dtype == _lib.F64 else _Y_REFINE_TOL_F32
+    O.y_cg_step = 0
+    O.M = MT.data_ptr()
+    O.Ginv = Gcm.data_ptr()
+    Bpad, B = _upload_rhs(Bmat, D)
+    C, _ = _ctrl(config, B, N, D.device, None)
+    L = _lib.lib()
+    wsb = L.ell1_batch_dalm_workspace(byref(view), B)
+    ws = device.alloc_bytes(wsb, D.device)
+    out, bufs = _outputs(B, N, config.max_iter + 1, D.device, with_trace)
+    rc = L.ell1_batch_dalm(byref(view), device.ptr(Bpad), B, byref(C), byref(O), byref(out),
+                           device.ptr(ws), int(ws.numel()), device.stream_ptr(D.device))
+    _lib.check(rc, "ell1_batch_dalm")
+    res = _collect(bufs, t0, D.device)
+    res.kind = "dalm"
+    res.max_iter = config.max_iter
+    return res
 
 
 def fista_solve_batch(A, Bmat, config, with_trace=False):

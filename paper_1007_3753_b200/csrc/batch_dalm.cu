@@ -1,0 +1,449 @@
+// batch_dalm.cu — dual ALM over a batch of instances sharing one dictionary
+// (element j equals alm.dalm_solve on (D, b_j), alm.py:206-272), e.g. the
+// cross-and-bouquet face-recognition batch of BASELINE config 3 on [A, sI].
+//
+// Per iteration (same algebra as csrc/dalm.cu, with M = G^{-1} A, Ginv = G^{-1}):
+//   z-kernel  : z = clamp(A^T y + x/beta), v = z - x/beta
+//   GEMMs     : M v, A z (+ Ginv v_ext for [A, sI])
+//   y-kernel  : y = M v + Ginv b / beta, rhs = A z - (A x - b)/beta
+//   GEMM      : A^T y
+//   x-kernel  : x_new = x - beta (z - A^T y)
+//   GEMM      : A [A^T y | x_new]   (one GEMM over 2B columns)
+//   c-kernel  : certificate, residual, gap, trace, stopping rules
+//   [refinement for instances failing the certificate: Ginv resid GEMM]
+#include "batched.cuh"
+
+namespace ell1 {
+
+struct DI {
+  double bn, l1_prev, by, rhs2, resid2, rr, l1, maxu;
+  double S[6];
+  int it, hist, active, status, conv, orig, refine, cnt;
+};
+
+struct BDArgs {
+  int64_t d, n, N, ld, ldx;
+  int ext, f32, cg;
+  double s, beta, ytol;
+  const double* Bm;         // ld x B
+  const double* C0;         // ld x B  (Ginv b)
+  double* X[2];             // ldx x B
+  double* Z;                // ldx x B
+  double* UX;               // ldx x 2B : [A^T y | x_new] GEMM operand (fp64)
+  double* V;                // ldx x B
+  double* Y[2];             // ld x B
+  double* AX;               // ld x B (A x of the current x)
+  double* RHS;              // ld x B
+  double* RES;              // ld x B
+  double* P1; double* P2;   // GEMM outputs ld x B / ld x 2B (fp64)
+  double* GEXT;             // ld x B (Ginv v_ext)
+  float* V32; float* Z32; float* UX32; float* Y32; float* P1f; float* P2f; float* P3f;
+  DI* inst;
+  ell1_ctrl_t C;
+  int* counters;            // [0] refine, [1] active
+  double* x_out; int* it_out; int* conv_out; int* status_out;
+  double* trace;            // [B0][max_iter + 1][4]
+  int ix, iy;
+};
+
+__device__ __forceinline__ double bd_rd(const BDArgs& a, const double* p64, const float* p32, int64_t i) {
+  return a.f32 ? (double)p32[i] : p64[i];
+}
+
+__global__ void __launch_bounds__(BT) bd_init(const BDArgs a) {
+  const int j = blockIdx.x;
+  __shared__ double sh[BW + 1];
+  DI& I = a.inst[j];
+  const double* b = a.Bm + (int64_t)j * a.ld;
+  double v[1] = {0.0};
+  for (int64_t i = threadIdx.x; i < a.ld; i += BT) {
+    const double bi = b[i];
+    v[0] += bi * bi;
+    a.AX[(int64_t)j * a.ld + i] = 0.0;
+    a.Y[0][(int64_t)j * a.ld + i] = 0.0;
+    a.Y[1][(int64_t)j * a.ld + i] = 0.0;
+  }
+  for (int64_t k = threadIdx.x; k < a.ldx; k += BT) {
+    a.X[0][(int64_t)j * a.ldx + k] = 0.0;
+    a.X[1][(int64_t)j * a.ldx + k] = 0.0;
+    a.UX[(int64_t)j * a.ldx + k] = 0.0;            // A^T y_0 = 0
+  }
+  cta_reduce<1>(v, 0u, sh);
+  if (threadIdx.x == 0) {
+    I.orig = j; I.it = 0; I.hist = 0; I.conv = 0; I.status = ELL1_OK; I.l1_prev = 0.0; I.refine = 0;
+    I.bn = sqrt(v[0]);
+    I.active = I.bn != 0.0;
+    if (a.trace) {
+      double* tr = a.trace + (int64_t)j * (a.C.max_iter + 1) * 4;
+      tr[0] = 0.0; tr[1] = 0.0; tr[2] = I.bn; tr[3] = 0.0;   // alm.py:233 (0.0 residual on zero data)
+    }
+    if (!I.active) {                                         // alm.py:223-226
+      I.status = ELL1_ZERO_DATA; I.conv = 1;
+      a.it_out[j] = 0; a.conv_out[j] = 1; a.status_out[j] = ELL1_ZERO_DATA;
+    } else {
+      atomicAdd(a.counters + 1, 1);
+    }
+  }
+  if (!I.active)
+    for (int64_t k = threadIdx.x; k < a.N; k += BT) a.x_out[(int64_t)j * a.N + k] = 0.0;
+}
+
+// z = clamp(A^T y + x/beta), v = z - x/beta (alm.py:239)
+__global__ void __launch_bounds__(BT) bd_z(const BDArgs a) {
+  const int j = blockIdx.x;
+  DI& I = a.inst[j];
+  if (!I.active) return;
+  if (threadIdx.x == 0) { I.it++; I.refine = 0; }
+  const int64_t o = (int64_t)j * a.ldx;
+  const double* x = a.X[a.ix] + o;
+  const double* u = a.UX + o;
+  for (int64_t k = threadIdx.x; k < a.N; k += BT) {
+    const double xb = x[k] / a.beta;
+    const double t = u[k] + xb;
+    const double z = t > 1.0 ? 1.0 : (t < -1.0 ? -1.0 : t);
+    a.Z[o + k] = z;
+    const double vv = k < a.n ? z - xb : a.s * (z - xb);
+    a.V[o + k] = vv;
+    if (a.f32 && k < a.n) { a.V32[o + k] = (float)vv; a.Z32[o + k] = (float)z; }
+  }
+}
+
+// y = M v + Ginv b / beta; rhs = A z - (A x - b)/beta (alm.py:179-180)
+__global__ void __launch_bounds__(BT) bd_y(const BDArgs a) {
+  const int j = blockIdx.x;
+  __shared__ double sh[BW * 2 + 2];
+  DI& I = a.inst[j];
+  if (!I.active) return;
+  const int64_t oj = (int64_t)j * a.ld;
+  const double* b = a.Bm + oj;
+  double* y = a.Y[a.iy ^ 1] + oj;
+  const double* zx = a.Z + (int64_t)j * a.ldx + a.n;
+  double q[2] = {0.0, 0.0};
+  for (int64_t i = threadIdx.x; i < a.d; i += BT) {
+    double mv = bd_rd(a, a.P1, a.P1f, oj + i);
+    if (a.ext) mv = mv + a.GEXT[oj + i];
+    const double yi = mv + a.C0[oj + i] / a.beta;
+    double az = bd_rd(a, a.P2, a.P2f, oj + i);
+    if (a.ext) az = az + a.s * zx[i];
+    const double rhs = az - (a.AX[oj + i] - b[i]) / a.beta;
+    y[i] = yi;
+    if (a.f32) a.Y32[oj + i] = (float)yi;
+    a.RHS[oj + i] = rhs;
+    q[0] += rhs * rhs;
+    q[1] += b[i] * yi;
+  }
+  cta_reduce<2>(q, 0u, sh);
+  if (threadIdx.x == 0) { I.rhs2 = q[0]; I.by = q[1]; }
+}
+
+// x_new = x - beta (z - A^T y) (alm.py:245-246); U = A^T y lives in UX[:, j]
+__global__ void __launch_bounds__(BT) bd_x(const BDArgs a, const double* Ut, const float* Ut32, int refine_only) {
+  const int j = blockIdx.x;
+  __shared__ double sh[BW * 6 + 6];
+  DI& I = a.inst[j];
+  if (!I.active || (refine_only && !I.refine)) return;
+  const int64_t o = (int64_t)j * a.ldx;
+  const double* x = a.X[a.ix] + o;
+  double* u = a.UX + o;                                   // [A^T y | x_new] block j
+  double* xn = a.UX + ((int64_t)gridDim.x + j) * a.ldx;   // second half of UX
+  const double* y = a.Y[a.iy ^ 1] + (int64_t)j * a.ld;
+  const bool relest = a.C.stop_kind == ELL1_STOP_REL_ESTIMATE;
+  double s[6] = {0, 0, 0, 0, 0, 0};                       // l1, max|Aty|, max|x|, dx2, xp2, -
+  for (int64_t k = threadIdx.x; k < a.N; k += BT) {
+    double uk;
+    if (k < a.n) uk = a.f32 ? (double)Ut32[(int64_t)j * a.n + k] : Ut[(int64_t)j * a.n + k];
+    else uk = a.s * y[k - a.n];                           // robust.py:96
+    u[k] = uk;
+    const double xo = x[k];
+    const double xv = xo - a.beta * (a.Z[o + k] - uk);
+    xn[k] = xv;
+    a.X[a.ix ^ 1][o + k] = xv;
+    if (a.f32 && k < a.n) {
+      a.UX32[o + k] = (float)uk;
+      a.UX32[((int64_t)gridDim.x + j) * a.ldx + k] = (float)xv;
+    }
+    s[0] += fabs(xv);
+    s[1] = nmax(s[1], fabs(uk));
+    s[2] = nmax(s[2], fabs(xv));
+    if (relest) { const double dd = xv - xo; s[3] += dd * dd; s[4] += xo * xo; }
+  }
+  cta_reduce<6>(s, 0x6u, sh);
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 6; ++k) I.S[k] = s[k];
+}
+
+// certificate, residual, trace, convergence (alm.py:181-188, 249-268)
+__global__ void __launch_bounds__(BT) bd_c(const BDArgs a, int refine_only) {
+  const int j = blockIdx.x;
+  const int B = gridDim.x;
+  __shared__ double sh[BW * 3 + 3];
+  __shared__ int fin;
+  DI& I = a.inst[j];
+  if (!I.active || (refine_only && !I.refine)) return;
+  const int64_t oj = (int64_t)j * a.ld;
+  const double* b = a.Bm + oj;
+  const double* u = a.UX + (int64_t)j * a.ldx;
+  const double* xn = a.UX + ((int64_t)B + j) * a.ldx;
+  const double cut = 1e-10 * pymax(I.S[2], 1.0);
+  double q[3] = {0.0, 0.0, 0.0};
+  for (int64_t i = threadIdx.x; i < a.d; i += BT) {
+    double aau = bd_rd(a, a.P2, a.P2f, ((int64_t)j) * a.ld + i);
+    double ax = bd_rd(a, a.P2, a.P2f, ((int64_t)B + j) * a.ld + i);
+    if (a.ext) { aau = aau + a.s * u[a.n + i]; ax = ax + a.s * xn[a.n + i]; }
+    const double resid = a.RHS[oj + i] - aau;
+    a.RES[oj + i] = resid;
+    a.AX[oj + i] = ax;
+    const double r = b[i] - ax;
+    q[0] += resid * resid;
+    q[1] += r * r;
+  }
+  for (int64_t k = threadIdx.x; k < a.N; k += BT) if (fabs(xn[k]) > cut) q[2] += 1.0;
+  cta_reduce<3>(q, 0u, sh);
+  if (threadIdx.x == 0) {
+    int done = 0;
+    I.resid2 = q[0]; I.rr = q[1]; I.cnt = (int)q[2];
+    if (!a.cg && sqrt(q[0]) > a.ytol * pymax(1.0, sqrt(I.rhs2))) {
+      if (I.refine) { I.status = ELL1_ILL_CONDITIONED; done = 3; }
+      else { I.refine = 1; atomicAdd(a.counters, 1); done = -1; }
+    }
+    if (done == 0) {
+      I.refine = 0;
+      const double rn = sqrt(I.rr);
+      const double l1 = I.S[0];
+      if (a.trace) {
+        double* tr = a.trace + ((int64_t)I.orig * (a.C.max_iter + 1) + I.it) * 4;
+        tr[0] = (double)I.it; tr[1] = l1; tr[2] = rn; tr[3] = (double)I.cnt;
+      }
+      const double rel = rn / I.bn;
+      const double gap = l1 - I.by / pymax(1.0, I.S[1]);
+      if (rel <= a.C.tol && gap <= a.C.tol * pymax(1.0, l1)) done = 1;
+      else if (a.C.stop_kind != ELL1_STOP_NONE) {
+        I.hist = I.hist < 2 ? I.hist + 1 : 2;
+        if (stop_fires(a.C.stop_kind, a.C.stop_thr, I.hist, l1, I.l1_prev, I.S[3], I.S[4], 0.0,
+                       a.C.gt_norm, rel))
+          done = 1;
+        I.l1_prev = l1;
+      }
+      if (!done && I.it >= a.C.max_iter) done = 2;
+    }
+    if (done > 0) {
+      I.conv = done == 1;
+      I.active = 0;
+      a.it_out[I.orig] = I.it; a.conv_out[I.orig] = I.conv;
+      a.status_out[I.orig] = done == 3 ? ELL1_ILL_CONDITIONED : ELL1_OK;
+      atomicSub(a.counters + 1, 1);
+    }
+    fin = done > 0;
+  }
+  __syncthreads();
+  if (fin) {
+    double* xo = a.x_out + (int64_t)I.orig * a.N;
+    for (int64_t k = threadIdx.x; k < a.N; k += BT) xo[k] = xn[k];
+  }
+}
+
+// refinement y += Ginv resid (alm.py:184), flagged instances only
+__global__ void __launch_bounds__(BT) bd_refine(const BDArgs a, const double* delta) {
+  const int j = blockIdx.x;
+  __shared__ double sh[BW + 1];
+  DI& I = a.inst[j];
+  if (!I.active || !I.refine) return;
+  const int64_t oj = (int64_t)j * a.ld;
+  double* y = a.Y[a.iy ^ 1] + oj;
+  const double* b = a.Bm + oj;
+  double q[1] = {0.0};
+  for (int64_t i = threadIdx.x; i < a.d; i += BT) {
+    const double yi = y[i] + delta[oj + i];
+    y[i] = yi;
+    if (a.f32) a.Y32[oj + i] = (float)yi;
+    q[0] += b[i] * yi;
+  }
+  cta_reduce<1>(q, 0u, sh);
+  if (threadIdx.x == 0) I.by = q[0];
+}
+
+__global__ void bd_scan(DI* inst, int B, int* perm, int* newB) {
+  __shared__ int base;
+  __shared__ int wsum[32];
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < B; c0 += blockDim.x) {
+    const int j = c0 + threadIdx.x;
+    const int act = (j < B) ? inst[j].active : 0;
+    const unsigned m = __ballot_sync(0xffffffffu, act);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) wsum[w] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = base;
+      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) { const int t = wsum[k]; wsum[k] = acc; acc += t; }
+      base = acc;
+    }
+    __syncthreads();
+    if (act) perm[wsum[w] + __popc(m & ((1u << l) - 1))] = j;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *newB = base;
+}
+
+template <class T>
+__global__ void bd_gather(const T* src, T* dst, int64_t rows, int64_t ld, const int* perm, int B) {
+  const int k = blockIdx.y;
+  if (k >= B) return;
+  const int64_t s = (int64_t)perm[k] * ld, d = (int64_t)k * ld;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+    dst[d + i] = src[s + i];
+}
+
+__global__ void bd_f2d(const double* src, float* dst, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = (float)src[i];
+}
+
+}  // namespace ell1
+
+using namespace ell1;
+
+static int64_t r4(int64_t x) { return (x + 3) / 4 * 4; }
+
+extern "C" size_t ell1_batch_dalm_workspace(const ell1_dict_t* D, int32_t B) {
+  if (!dict_ok(D) || B < 1) return 0;
+  const int64_t N = ncols_of(D), ldx = r4(N), ld = D->ld;
+  size_t s = 0;
+  s += 5 * align_up(ldx * B * 8, 256) + align_up(ldx * 2 * B * 8, 256);   // X[2], Z, V, scratch-x, UX
+  s += 9 * align_up(ld * B * 8, 256) + align_up(ld * 2 * B * 8, 256);      // Y[2], AX, RHS, RES, C0, Bm, P1, GEXT, P2
+  s += align_up(ldx * B * 4, 256) * 3 + align_up(ldx * 2 * B * 4, 256) + align_up(ld * B * 4, 256) * 3 +
+       align_up(ld * 2 * B * 4, 256);
+  s += 2 * align_up((int64_t)sizeof(DI) * B, 256) + align_up(B * 4, 256) + align_up(ldx * B * 8, 256);
+  return s + 8192;
+}
+
+extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t B, const ell1_ctrl_t* C,
+                               const ell1_dalm_opts_t* O, const ell1_batch_out_t* out, void* ws,
+                               size_t wsb, void* stream) {
+  if (!dict_ok(D) || !Bmat || B < 1 || !C || !O || !O->M || !O->Ginv || !(O->beta > 0) || !out ||
+      !out->x || !out->iterations || !out->converged || !out->status)
+    return ELL1_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  cublasHandle_t h = blas_handle(s);
+  if (!h) return ELL1_ERR_CUDA;
+  const int64_t N = ncols_of(D), ldx = r4(N), ld = D->ld, d = D->d;
+  BDArgs a;
+  a.d = d; a.n = D->n; a.N = N; a.ld = ld; a.ldx = ldx;
+  a.ext = D->ext; a.f32 = D->dtype == ELL1_F32; a.cg = O->y_cg_step;
+  a.s = D->ext_scale; a.beta = O->beta; a.ytol = O->y_tol;
+  a.C = *C;
+  if (a.cg) return ELL1_ERR_ARG;   // batched CG y-step: not provided (use the single-instance solver)
+  Carve cv(ws, wsb);
+  a.X[0] = cv.take<double>(ldx * B); a.X[1] = cv.take<double>(ldx * B);
+  a.Z = cv.take<double>(ldx * B); a.V = cv.take<double>(ldx * B);
+  double* xscr = cv.take<double>(ldx * B);
+  a.UX = cv.take<double>(ldx * 2 * B);
+  a.Y[0] = cv.take<double>(ld * B); a.Y[1] = cv.take<double>(ld * B);
+  a.AX = cv.take<double>(ld * B); a.RHS = cv.take<double>(ld * B); a.RES = cv.take<double>(ld * B);
+  double* C0 = cv.take<double>(ld * B);
+  double* Bm = cv.take<double>(ld * B);
+  a.P1 = cv.take<double>(ld * B); a.GEXT = cv.take<double>(ld * B);
+  a.P2 = cv.take<double>(ld * 2 * B);
+  a.V32 = cv.take<float>(ldx * B); a.Z32 = cv.take<float>(ldx * B);
+  float* T32 = cv.take<float>(ldx * B);
+  a.UX32 = cv.take<float>(ldx * 2 * B);
+  a.Y32 = cv.take<float>(ld * B); a.P1f = cv.take<float>(ld * B); a.P3f = cv.take<float>(ld * B);
+  a.P2f = cv.take<float>(ld * 2 * B);
+  a.inst = cv.take<DI>(B);
+  DI* inst2 = cv.take<DI>(B);
+  int* perm = cv.take<int>(B);
+  double* scratch = cv.take<double>(ldx * B);
+  int* ctr = cv.take<int>(8);
+  if (!cv.ok) return ELL1_ERR_ARG;
+  (void)xscr; (void)T32;
+  a.Bm = Bm; a.C0 = C0;
+  a.counters = ctr;
+  a.x_out = out->x; a.it_out = out->iterations; a.conv_out = out->converged; a.status_out = out->status;
+  a.trace = out->trace;
+  a.ix = 0; a.iy = 0;
+  if (cudaMemcpyAsync(Bm, Bmat, ld * B * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return ELL1_ERR_CUDA;
+  if (cudaMemsetAsync(ctr, 0, 32, s) != cudaSuccess) return ELL1_ERR_CUDA;
+  if (cudaMemsetAsync(a.UX32, 0, ldx * 2 * B * 4, s) != cudaSuccess) return ELL1_ERR_CUDA;
+  const double one = 1.0, zero = 0.0;
+  // C0 = Ginv B (Ginv column-major ld x d, float64)
+  if (cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)ld, B, (int)d, &one, O->Ginv, (int)ld, Bm, (int)ld,
+                  &zero, C0, (int)ld) != CUBLAS_STATUS_SUCCESS)
+    return ELL1_ERR_CUDA;
+  bd_init<<<B, BT, 0, s>>>(a);
+  ell1_dict_t MD = *D;
+  MD.A = O->M;                                              // M has A's layout / dtype
+  int Bcur = B;
+  while (true) {
+    int hc[2];
+    if (cudaMemcpyAsync(hc, ctr, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return ELL1_ERR_CUDA;
+    const int nact = hc[1];
+    if (nact <= 0) break;
+    if (nact < Bcur * 3 / 4 || (nact < Bcur && nact <= 64)) {
+      bd_scan<<<1, 1024, 0, s>>>(a.inst, Bcur, perm, ctr + 2);
+      auto pm = [&](double* M, int64_t rows, int64_t ldm) {
+        dim3 g((unsigned)((rows + 255) / 256 < 64 ? (rows + 255) / 256 : 64), (unsigned)nact);
+        bd_gather<double><<<g, 256, 0, s>>>(M, scratch, rows, ldm, perm, nact);
+        cudaMemcpyAsync(M, scratch, ldm * nact * 8, cudaMemcpyDeviceToDevice, s);
+      };
+      pm(a.X[a.ix], N, ldx);
+      pm(a.UX, N, ldx);                                     // A^T y of the current y
+      pm(a.Y[a.iy], ld, ld);
+      pm(a.AX, ld, ld);
+      pm(C0, ld, ld);
+      pm(Bm, ld, ld);
+      {
+        const int64_t words = (int64_t)sizeof(DI) / 4;
+        bd_gather<int><<<dim3(1, (unsigned)nact), 64, 0, s>>>((const int*)a.inst, (int*)inst2, words, words, perm, nact);
+        cudaMemcpyAsync(a.inst, inst2, sizeof(DI) * nact, cudaMemcpyDeviceToDevice, s);
+      }
+      Bcur = nact;
+    }
+    // ---- one DALM iteration over Bcur instances
+    bd_z<<<Bcur, BT, 0, s>>>(a);
+    {
+      const void* Vop = a.f32 ? (const void*)a.V32 : (const void*)a.V;
+      const void* Zop = a.f32 ? (const void*)a.Z32 : (const void*)a.Z;
+      if (!gemm_AX(h, &MD, Vop, ldx, a.f32 ? (void*)a.P1f : (void*)a.P1, ld, Bcur)) return ELL1_ERR_CUDA;
+      if (!gemm_AX(h, D, Zop, ldx, a.f32 ? (void*)a.P2f : (void*)a.P2, ld, Bcur)) return ELL1_ERR_CUDA;
+      if (a.ext) {
+        // identity block of M: s Ginv v_ext (s folded into v_ext by bd_z)
+        if (cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)ld, Bcur, (int)d, &one, O->Ginv, (int)ld,
+                        a.V + D->n, (int)ldx, &zero, a.GEXT, (int)ld) != CUBLAS_STATUS_SUCCESS)
+          return ELL1_ERR_CUDA;
+      }
+    }
+    bd_y<<<Bcur, BT, 0, s>>>(a);
+    int refine_only = 0;
+    while (true) {
+      // U = A^T y_new (n x B), then x_new, then A [U | x_new]
+      void* Ut = a.f32 ? (void*)T32 : (void*)scratch;
+      if (!gemm_AtR(h, D, a.f32 ? (const void*)a.Y32 : (const void*)a.Y[a.iy ^ 1], ld, Ut, D->n, Bcur))
+        return ELL1_ERR_CUDA;
+      // UX holds [U | x_new] for the Bcur instances: x_new block starts at column Bcur
+      bd_x<<<Bcur, BT, 0, s>>>(a, (const double*)Ut, (const float*)Ut, refine_only);
+      if (a.f32) {
+        // UX32 layout: [U | x_new] with Bcur columns each
+        if (!gemm_AX(h, D, a.UX32, ldx, a.P2f, ld, 2 * Bcur)) return ELL1_ERR_CUDA;
+      } else {
+        if (!gemm_AX(h, D, a.UX, ldx, a.P2, ld, 2 * Bcur)) return ELL1_ERR_CUDA;
+      }
+      if (cudaMemsetAsync(ctr, 0, 4, s) != cudaSuccess) return ELL1_ERR_CUDA;
+      bd_c<<<Bcur, BT, 0, s>>>(a, refine_only);
+      int nref = 0;
+      if (cudaMemcpyAsync(&nref, ctr, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
+      if (cudaStreamSynchronize(s) != cudaSuccess) return ELL1_ERR_CUDA;
+      if (nref == 0) break;
+      // y += Ginv resid for the flagged instances (alm.py:184)
+      if (cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)ld, Bcur, (int)d, &one, O->Ginv, (int)ld, a.RES,
+                      (int)ld, &zero, a.GEXT, (int)ld) != CUBLAS_STATUS_SUCCESS)
+        return ELL1_ERR_CUDA;
+      bd_refine<<<Bcur, BT, 0, s>>>(a, a.GEXT);
+      refine_only = 1;
+    }
+    a.ix ^= 1;
+    a.iy ^= 1;
+  }
+  return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
+}

@@ -75,3 +75,38 @@ def test_batch_fista_cab(bt):
         x, e, ref = oracle.cab(A, Bm[:, j], "fista", tol=1e-6, max_iter=5000)
         assert res[j].iterations == ref.iterations
         assert rel_err(res[j].x_star, ref.x) <= 1e-8
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_batch_dalm_equals_single_instances(bt, dtype):
+    from paper_1007_3753_b200.model import SolverConfig, StoppingRule
+    A, Bm, _ = _batch(128, 512, [4, 8, 16, 2, 12, 6])
+    cfg = SolverConfig(tol=1e-6, max_iter=3000, stopping=StoppingRule("relative-estimate", 1e-6),
+                       options={"dtype": dtype})
+    res = bt.dalm_solve_batch(A, Bm, cfg, with_trace=True).results()
+    for j in range(Bm.shape[1]):
+        ref = oracle.dalm(A, Bm[:, j], tol=1e-6, max_iter=3000, stop=("relative-estimate", 1e-6))
+        tol = 1e-6 if dtype == "float64" else 1e-4
+        assert rel_err(res[j].x_star, ref.x) <= tol, j
+        assert support(res[j].x_star) == support(ref.x), j
+        if dtype == "float64":
+            assert res[j].iterations == ref.iterations, (j, res[j].iterations, ref.iterations)
+            tr = np.array([tuple(t) for t in res[j].trace])
+            np.testing.assert_allclose(tr, np.array(ref.trace), rtol=1e-8, atol=1e-10)
+
+
+def test_batch_dalm_cab_matches_reference(bt):
+    from paper_1007_3753_b200.model import SolverConfig
+    from paper_1007_3753_b200.robust import ExtendedDictionary
+    from tests.golden.cases import build_inputs
+    A, b, _ = build_inputs(dict(kind="cab", d=40, n=30, k=3, seed=7, m=4))
+    g = np.random.default_rng(11)
+    Bm = np.stack([b] + [A @ (g.standard_normal(30) * (g.random(30) < 0.1)) + 0.5 * (g.random(40) < 0.1)
+                         for _ in range(4)], axis=1)
+    cfg = SolverConfig(tol=1e-6, max_iter=5000)
+    res = bt.dalm_solve_batch(ExtendedDictionary(A, 1.0), Bm, cfg, with_trace=True).results()
+    for j in range(Bm.shape[1]):
+        x, e, ref = oracle.cab(A, Bm[:, j], "dalm", tol=1e-6, max_iter=5000)
+        assert res[j].iterations == ref.iterations, j
+        assert rel_err(res[j].x_star, ref.x) <= 1e-8
+        assert res[j].notes == ref.notes
