@@ -259,6 +259,14 @@ int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t B, const e
                     const ell1_dalm_opts_t* O, const ell1_batch_out_t* out, void* workspace,
                     size_t workspace_bytes, void* stream);
 
+/* SRC labels for a CAB batch (BASELINE config 3): label_j = argmin_c
+ * ||b_j - e_j - A_c x_{j,c}||, classes = contiguous column ranges
+ * [class_offsets[c], class_offsets[c+1]); W (ldw x B, ldw >= n + d) holds the
+ * stacked solutions [x; e/s] of the [A, sI] solves; nclasses <= 64. */
+int ell1_src_classify(const ell1_dict_t* D, const double* Bmat, int32_t B, const double* W,
+                      int64_t ldw, const int32_t* class_offsets, int32_t nclasses, int32_t* labels,
+                      double* class_resid, void* stream);
+
 /* library / device info */
 int ell1_device_sms(int32_t device);
 const char* ell1_version(void);

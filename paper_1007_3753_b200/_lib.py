@@ -136,6 +136,9 @@ _SIGS = {
     "ell1_batch_dalm": (ctypes.c_int, [P(Dict), ctypes.c_void_p, ctypes.c_int32, P(Ctrl),
                                        P(DalmOpts), P(BatchOut), ctypes.c_void_p, ctypes.c_size_t,
                                        ctypes.c_void_p]),
+    "ell1_src_classify": (ctypes.c_int, [P(Dict), ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
+                                         ctypes.c_int64, ctypes.c_void_p, ctypes.c_int32,
+                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "ell1_device_sms": (ctypes.c_int, [ctypes.c_int32]),
     "ell1_version": (ctypes.c_char_p, []),
 }

@@ -115,8 +115,45 @@ def _collect(bufs, t0, dev, trace_offset=0):
     torch = device._torch()
     x, its, conv, stat, tr = bufs
     torch.cuda.synchronize(dev)
-    return BatchResult(x.T.cpu().numpy(), its.cpu().numpy(), conv.cpu().numpy(), stat.cpu().numpy(),
-                       time.perf_counter() - t0, tr.cpu().numpy() if tr is not None else None)
+    res = BatchResult(x.T.cpu().numpy(), its.cpu().numpy(), conv.cpu().numpy(), stat.cpu().numpy(),
+                      time.perf_counter() - t0, tr.cpu().numpy() if tr is not None else None)
+    res._device_x = x          # B x N device copy (for on-device post-processing)
+    return res
+
+
+def src_classify(A, class_labels, Bmat, config):
+    """Cross-and-bouquet SRC (BASELINE config 3): solve every query on
+    [A, I/e_weight] with the batched dual ALM (robust.cab_solve semantics,
+    robust.py:181-220), then label_j = argmin_c ||b_j - e_j - A_c x_{j,c}||.
+    class_labels: class id of each column of A (columns of a class contiguous).
+    Returns (labels, class_residuals (B x C), BatchResult)."""
+    torch = device._torch()
+    from paper_1007_3753_b200.robust import ExtendedDictionary
+    e_weight = float(config.opt("e_weight", 1.0))
+    if not e_weight > 0:
+        raise ValueError("e_weight must be positive")
+    ext = A if hasattr(A, "device_extension") else ExtendedDictionary(
+        A, 1.0 / e_weight, dtype=config.opt("dtype", "float64"), device_ordinal=config.opt("device", None))
+    res = dalm_solve_batch(ext, Bmat, config)
+    D, s = ext.device_extension()
+    view = D.view(ext=True, scale=s)
+    lab = np.asarray(class_labels)
+    if np.any(np.diff(lab) < 0):
+        raise ValueError("columns of a class must be contiguous (sorted class labels)")
+    ncls = int(lab.max()) + 1
+    offs = np.searchsorted(lab, np.arange(ncls + 1)).astype(np.int32)
+    dev = D.device
+    offd = torch.from_numpy(offs).to(dev)
+    Bpad, B = _upload_rhs(Bmat, D)
+    W = res._device_x.contiguous()                       # B x (n + d)
+    labels = torch.zeros(B, dtype=torch.int32, device=dev)
+    resid = torch.zeros(B, ncls, dtype=torch.float64, device=dev)
+    rc = _lib.lib().ell1_src_classify(byref(view), device.ptr(Bpad), B, device.ptr(W), int(W.shape[1]),
+                                      device.ptr(offd), ncls, device.ptr(labels), device.ptr(resid),
+                                      device.stream_ptr(dev))
+    _lib.check(rc, "ell1_src_classify")
+    torch.cuda.synchronize(dev)
+    return labels.cpu().numpy(), resid.cpu().numpy(), res
 
 
 def dalm_solve_batch(A, Bmat, config, with_trace=False):

@@ -1,0 +1,83 @@
+// src_classify.cu — sparse-representation classification labels for a CAB
+// batch (BASELINE config 3): label_j = argmin_c || b_j - e_j - A_c x_{j,c} ||_2,
+// A_c the (contiguous) columns of class c.  One CTA per query; each thread
+// owns rows of the residual and accumulates every class's squared residual,
+// then a fixed-order CTA reduction picks the class (lowest index on ties,
+// numpy argmin).  The class rule is new code applied identically to the
+// reference outputs in the tests (the reference's harness uses max group
+// energy, bench.py:292-293).
+#include "batched.cuh"
+
+namespace ell1 {
+
+constexpr int SRC_MAXC = 64;
+
+template <class TA>
+__global__ void __launch_bounds__(BT) src_kernel(const TA* A, int64_t d, int64_t ld, const double* Bm,
+                                                 int64_t ldb, const double* W, int64_t ldw, int64_t n,
+                                                 double s, const int32_t* off, int ncls, int32_t* labels,
+                                                 double* resid) {
+  const int j = blockIdx.x;
+  __shared__ double red[BW * SRC_MAXC];
+  const double* b = Bm + (int64_t)j * ldb;
+  const double* w = W + (int64_t)j * ldw;          // [x (n); e_raw (d)]  (e = s * e_raw)
+  double acc[SRC_MAXC];
+#pragma unroll
+  for (int c = 0; c < SRC_MAXC; ++c) acc[c] = 0.0;
+  for (int64_t i = threadIdx.x; i < d; i += BT) {
+    const double base = b[i] - s * w[n + i];
+#pragma unroll
+    for (int c = 0; c < SRC_MAXC; ++c) {
+      if (c < ncls) {
+        double part = 0.0;
+        for (int k = off[c]; k < off[c + 1]; ++k) {
+          const double xk = w[k];
+          if (xk != 0.0) part = fma((double)A[(int64_t)k * ld + i], xk, part);
+        }
+        const double r = base - part;
+        acc[c] += r * r;
+      }
+    }
+  }
+  const int wp = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 0; c < SRC_MAXC; ++c) {
+    if (c < ncls) {
+      const double v = warp_sum(acc[c]);
+      if (l == 0) red[wp * SRC_MAXC + c] = v;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int best = 0;
+    double bv = INFINITY;
+    for (int c = 0; c < ncls; ++c) {
+      double t = 0.0;
+      for (int ww = 0; ww < BW; ++ww) t += red[ww * SRC_MAXC + c];
+      if (resid) resid[(int64_t)j * ncls + c] = sqrt(t);
+      if (t < bv) { bv = t; best = c; }
+    }
+    labels[j] = best;
+  }
+}
+
+}  // namespace ell1
+
+using namespace ell1;
+
+extern "C" int ell1_src_classify(const ell1_dict_t* D, const double* Bmat, int32_t B, const double* W,
+                                 int64_t ldw, const int32_t* class_offsets, int32_t nclasses,
+                                 int32_t* labels, double* class_resid, void* stream) {
+  if (!dict_ok(D) || !Bmat || !W || !class_offsets || !labels || B < 1 || nclasses < 1 ||
+      nclasses > SRC_MAXC || ldw < D->n + (D->ext ? D->d : 0))
+    return ELL1_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const double sc = D->ext ? D->ext_scale : 0.0;
+  if (D->dtype == ELL1_F64)
+    src_kernel<double><<<B, BT, 0, s>>>((const double*)D->A, D->d, D->ld, Bmat, D->ld, W, ldw, D->n, sc,
+                                        class_offsets, nclasses, labels, class_resid);
+  else
+    src_kernel<float><<<B, BT, 0, s>>>((const float*)D->A, D->d, D->ld, Bmat, D->ld, W, ldw, D->n, sc,
+                                       class_offsets, nclasses, labels, class_resid);
+  return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
+}

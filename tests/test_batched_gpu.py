@@ -110,3 +110,29 @@ def test_batch_dalm_cab_matches_reference(bt):
         assert res[j].iterations == ref.iterations, j
         assert rel_err(res[j].x_star, ref.x) <= 1e-8
         assert res[j].notes == ref.notes
+
+
+def _src_host(A, lab, b, w, s):
+    n = A.shape[1]
+    x, e = w[:n], s * w[n:]
+    out = []
+    for c in range(int(lab.max()) + 1):
+        m = lab == c
+        out.append(np.linalg.norm(b - e - A[:, m] @ x[m]))
+    return int(np.argmin(out)), np.array(out)
+
+
+def test_src_labels_match_reference_rule(bt):
+    # a scaled-down config 3: 6 classes x 8 columns, d=96, 20% corrupted queries
+    from paper_1007_3753_b200 import synth
+    from paper_1007_3753_b200.model import SolverConfig
+    A, lab = synth.cab_dictionary(d=96, classes=6, per_class=8, subspace=3, seed=2)
+    Bq, truth = synth.cab_queries(A, lab, 10, fraction=0.2, seed=3)
+    cfg = SolverConfig(tol=1e-4, max_iter=4000, options={"beta": 0.1})
+    labels, resid, res = bt.src_classify(A, lab, Bq.T, cfg)
+    for j in range(Bq.shape[0]):
+        x, e, ref = oracle.cab(A, Bq[j], "dalm", tol=1e-4, max_iter=4000, opts={"beta": 0.1})
+        want, wres = _src_host(A, lab, Bq[j], np.concatenate([x, e]), 1.0)
+        assert labels[j] == want, j
+        np.testing.assert_allclose(resid[j], wres, rtol=1e-5, atol=1e-8)
+    assert np.mean(labels == truth) >= 0.8
