@@ -267,6 +267,28 @@ int ell1_src_classify(const ell1_dict_t* D, const double* Bmat, int32_t B, const
                       int64_t ldw, const int32_t* class_offsets, int32_t nclasses, int32_t* labels,
                       double* class_resid, void* stream);
 
+/* ----------------------------------------- column-sharded primitives (config 4)
+ * Device building blocks of the multi-GPU FISTA (one rank per GPU, one NCCL
+ * allreduce of the d-length partial A x per iteration).  The
+ * shard-level scalar partials (out8, 8 doubles) are combined across ranks by
+ * the host driver (paper_1007_3753_b200/sharded.py). */
+size_t ell1_gemv_workspace(const ell1_dict_t* D);
+/* y (ld) = D x (n), fixed-order reduction  (DenseDictionary.apply, operators.py:27-28) */
+int ell1_gemv(const ell1_dict_t* D, const double* x, double* y, void* ws, size_t ws_bytes, void* stream);
+/* g (n) = D^T r (ld)  (DenseDictionary.adjoint, operators.py:30-31) */
+int ell1_gemv_t(const ell1_dict_t* D, const double* r, double* g, void* ws, size_t ws_bytes, void* stream);
+/* x_next = soft(y - g_y/L, lam/L) on a shard; out8 = {sum|xn|, g_y.dl, dl.dl, max|xn|,
+ * ||xn - x||^2, ||x||^2, ||xn - gt||^2, 0} (shrinkage.py:199-213); ws >= 296*8*8 bytes */
+int ell1_shard_prox(int64_t n, const double* x, const double* xp, const double* gx, const double* gxp,
+                    double* xn, double m, double L, double lam, const double* gt, double* out8,
+                    void* ws, void* stream);
+/* KKT / support partials of a shard: out8 = {max_on, max_off, any_on, any_off, count, ...} */
+int ell1_shard_kkt(int64_t n, const double* x, const double* g, double lam, double cut, double* out8,
+                   void* ws, void* stream);
+/* r_next = ax - b, out8 = {||r_next||^2, ||(1+mn) r_next - mn r_x||^2, ...} */
+int ell1_shard_resid(int64_t d, const double* ax, const double* b, const double* rx, double mn, double* rn,
+                     double* out8, void* ws, void* stream);
+
 /* library / device info */
 int ell1_device_sms(int32_t device);
 const char* ell1_version(void);

@@ -139,6 +139,17 @@ _SIGS = {
     "ell1_src_classify": (ctypes.c_int, [P(Dict), ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
                                          ctypes.c_int64, ctypes.c_void_p, ctypes.c_int32,
                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_gemv_workspace": (ctypes.c_size_t, [P(Dict)]),
+    "ell1_gemv": (ctypes.c_int, [P(Dict), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                 ctypes.c_size_t, ctypes.c_void_p]),
+    "ell1_gemv_t": (ctypes.c_int, [P(Dict), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                   ctypes.c_size_t, ctypes.c_void_p]),
+    "ell1_shard_prox": (ctypes.c_int, [ctypes.c_int64] + [ctypes.c_void_p] * 5 +
+                        [ctypes.c_double] * 3 + [ctypes.c_void_p] * 4),
+    "ell1_shard_kkt": (ctypes.c_int, [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
+                                      ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_shard_resid": (ctypes.c_int, [ctypes.c_int64] + [ctypes.c_void_p] * 3 + [ctypes.c_double] +
+                         [ctypes.c_void_p] * 4),
     "ell1_device_sms": (ctypes.c_int, [ctypes.c_int32]),
     "ell1_version": (ctypes.c_char_p, []),
 }

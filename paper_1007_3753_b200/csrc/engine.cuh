@@ -541,44 +541,56 @@ __device__ void panel_gemv_t(const Ctx& E, const DictV<TA>& D, const Panel<TA>& 
       }
     }
   } else {
-    for (int jl = wpx(); jl < w; jl += NWARP) {
-      double acc[NV][2];
+    // Long columns: column groups of NWARP x CPW; r is staged through shared
+    // memory in row chunks shared by every warp of the group, so each r
+    // element is read from L2 once per group instead of once per column.
+    constexpr int CPW = 4;
+    int64_t rch = E.shcap / (VW * NV);
+    if (rch > 1024) rch = 1024;
+    rch = rch / 32 * 32;
+    if (rch < 32) rch = 32;
+    double* rsm = E.sh;
+    for (int jg = 0; jg < w; jg += NWARP * CPW) {
+      double acc[CPW][NV];
 #pragma unroll
-      for (int v = 0; v < NV; ++v) acc[v][0] = acc[v][1] = 0.0;
-      const bool res = jl < rc;
-      const TA* col = res ? P.sm + (int64_t)jl * D.ld : P.gl + (int64_t)jl * D.ld;
-      int64_t q = lnx();
-      for (; q + 96 < nvec; q += 128) {
-        TA a[4][VW];
+      for (int c = 0; c < CPW; ++c)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (res) ld16_s<TA>(col + (q + 32 * k) * VW, a[k]);
-          else ld16_g<TA>(col + (q + 32 * k) * VW, a[k]);
-        }
+        for (int v = 0; v < NV; ++v) acc[c][v] = 0.0;
+      for (int64_t rb = 0; rb < nvec; rb += rch) {
+        const int64_t rcnt = min(rch, nvec - rb);
+        for (int64_t t = tix(); t < rcnt * VW; t += NTHR)
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+          for (int v = 0; v < NV; ++v) rsm[v * rch * VW + t] = ldcg(rs[v] + rb * VW + t);
+        __syncthreads();
 #pragma unroll
-          for (int v = 0; v < NV; ++v) {
-            const double* rv = rs[v] + (q + 32 * k) * VW;
+        for (int c = 0; c < CPW; ++c) {
+          const int jl = jg + wpx() * CPW + c;
+          if (jl < w) {
+            const bool res = jl < rc;
+            const TA* col = (res ? P.sm : P.gl) + (int64_t)jl * D.ld + rb * VW;
+            for (int64_t q = lnx(); q < rcnt; q += 32) {
+              TA a[VW];
+              if (res) ld16_s<TA>(col + q * VW, a);
+              else ld16_g<TA>(col + q * VW, a);
 #pragma unroll
-            for (int e = 0; e < VW; ++e) acc[v][k & 1] = fma((double)a[k][e], rv[e], acc[v][k & 1]);
+              for (int v = 0; v < NV; ++v) {
+                const double* rv = rsm + v * rch * VW + q * VW;
+#pragma unroll
+                for (int e = 0; e < VW; ++e) acc[c][v] = fma((double)a[e], rv[e], acc[c][v]);
+              }
+            }
           }
+        }
+        __syncthreads();
       }
-      for (; q < nvec; q += 32) {
-        TA a[VW];
-        if (res) ld16_s<TA>(col + q * VW, a);
-        else ld16_g<TA>(col + q * VW, a);
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) {
+        const int jl = jg + wpx() * CPW + c;
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-          const double* rv = rs[v] + q * VW;
-#pragma unroll
-          for (int e = 0; e < VW; ++e) acc[v][0] = fma((double)a[e], rv[e], acc[v][0]);
+          const double s = warp_sum(acc[c][v]);
+          if (jl < w && lnx() == 0) outs[v][jl] = s;
         }
-      }
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const double s = warp_sum(acc[v][0] + acc[v][1]);
-        if (lnx() == 0) outs[v][jl] = s;
       }
     }
     __syncthreads();

@@ -169,6 +169,13 @@ inline SmemPlan plan_smem(const DictRaw& D, int nb, int nov, int kmax, bool allo
   p.wmax = (int)align_up(wcols + wrows, 2);
   p.scratch = engine_scratch_doubles(kmax);
   const int64_t esz = D.dtype == ELL1_F64 ? 8 : 4;
+  // long columns (GEMV^T row chunks of r staged in shared memory, NV <= 2)
+  const int64_t vw = 16 / esz;
+  if (D.ld / vw > NTHR) {
+    int64_t want = 2 * 1024 * vw;
+    if (want > 16384) want = 16384;
+    if (p.scratch < want) p.scratch = want;
+  }
   const int64_t fixed = ((int64_t)nov * p.wmax + p.scratch) * 8;
   const int64_t cap = max_smem_optin();
   int64_t rc = 0;
