@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--dtype", default="float64", choices=["float64", "float32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-stream", action="store_true", help="skip the HBM streaming roofline leg")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the config 3/4/5 and all-solver legs")
     return ap.parse_args()
 
 
@@ -218,6 +220,207 @@ def stream_roofline(torch, dev):
             "ms_per_launch": 1e3 * tot / reps, "iterations": int(st.iterations)}
 
 
+def _events(torch):
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
+def leg_cfg4(torch, dev, ws, rank, iters=8, reps=2):
+    """BASELINE config 4: one d=65536 x n=262144 fp32 instance (64 GiB),
+    columns sharded over the ranks, FISTA with one NCCL allreduce of the
+    d-length partial A x per iteration (strong scaling: total work fixed).
+    Dictionary generated on the device (seeded Philox per 2048-column global
+    chunk, so A is the same matrix for every world size); A >> L2, so every
+    panel pass streams from HBM."""
+    from paper_1007_3753_b200 import device as dv
+    from paper_1007_3753_b200.model import SolverConfig
+    from paper_1007_3753_b200.sharded import (DeviceShardOps, ShardedDictionary, ShardedFista,
+                                              column_range)
+    d, n, k = 65536, 262144, 2048
+    c0, c1 = column_range(n, rank, ws)
+    nl = c1 - c0
+    storage = torch.empty(nl, d, dtype=torch.float32, device=dev)
+    CH = 2048
+    g = torch.Generator(device=dev)
+    for j0 in range(c0 // CH * CH, c1, CH):
+        g.manual_seed(7000003 + j0 // CH)
+        blk = torch.randn(CH, d, generator=g, device=dev, dtype=torch.float32)
+        blk /= torch.linalg.vector_norm(blk, dim=1, keepdim=True)
+        a, e = max(j0, c0), min(j0 + CH, c1)
+        storage[a - c0:e - c0] = blk[a - j0:e - j0]
+        del blk
+    torch.cuda.empty_cache()
+    D = dv.DeviceDictionary.wrap(storage, d)
+    shard = ShardedDictionary(D, c0, n, None)
+    ops = DeviceShardOps(shard)
+    rng = np.random.default_rng(44)
+    x0 = np.zeros(n)
+    x0[rng.choice(n, k, replace=False)] = rng.standard_normal(k)
+    xl = ops.from_host_n(x0[c0:c1])
+    bd = ops.zeros_d()
+    ops.gemv(xl, bd)
+    ops.allreduce_(bd)
+    b = ops.to_host_d(bd)
+    sigma = 1e-3 * float(np.linalg.norm(b)) / np.sqrt(d)
+    b = b + sigma * rng.standard_normal(d)
+    # kernel roofline: the two panel passes alone
+    gt_ev, g_ev = _events(torch), _events(torch)
+    r = ops.from_host_d(b)
+    gl = ops.zeros_n()
+    for _ in range(2):
+        ops.gemv(xl, bd)
+        ops.gemv_t(r, gl)
+    torch.cuda.synchronize()
+    K = 5
+    g_ev[0].record()
+    for _ in range(K):
+        ops.gemv(xl, bd)
+    g_ev[1].record()
+    gt_ev[0].record()
+    for _ in range(K):
+        ops.gemv_t(r, gl)
+    gt_ev[1].record()
+    torch.cuda.synchronize()
+    shard_bytes = nl * d * 4
+    t_gemv = g_ev[0].elapsed_time(g_ev[1]) / 1e3 / K
+    t_gemvt = gt_ev[0].elapsed_time(gt_ev[1]) / 1e3 / K
+    cfg = SolverConfig(lam=None, tol=1e-6, max_iter=iters)
+    drv = ShardedFista(ops, b, n, cfg)
+    drv.solve()                                   # warm-up
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    s, e = _events(torch)
+    s.record()
+    passes = 0
+    its = 0
+    for _ in range(reps):
+        res = drv.solve()
+        passes += drv.passes
+        its += res.iterations
+    e.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([s.elapsed_time(e) / 1e3], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    tmax = float(t.item())
+    out = {"workload": "cfg4: d=65536 n=262144 fp32 storage (64 GiB) k=2048, 1e-3 relative noise, "
+                       "FISTA, default lambda, %d iterations per solve" % iters,
+           "n_gpus": ws, "scaling": "strong", "parallelism": "column-sharded, NCCL allreduce of "
+           "A_r x_r per backtracking trial" if ws > 1 else "single GPU (whole dictionary)",
+           "iterations_per_sec": its / tmax, "ms_per_iteration": 1e3 * tmax / its,
+           "passes_per_iteration": passes / its,
+           "achieved_gbs_per_gpu": passes * shard_bytes / tmax / 1e9,
+           "gemv_gbs": shard_bytes / t_gemv / 1e9, "gemv_t_gbs": shard_bytes / t_gemvt / 1e9,
+           "l2": "none needed (64 GiB dictionary >> 126 MB L2)"}
+    del drv, ops, shard, D, storage
+    torch.cuda.empty_cache()
+    return out
+
+
+def leg_cfg3(torch, dev, queries=1024):
+    """BASELINE config 3: CAB [A I] (d=1024, 38 classes x 32 columns), 1024
+    corrupted queries, batched dual ALM in fp32 storage + SRC labels."""
+    from paper_1007_3753_b200 import synth
+    from paper_1007_3753_b200.batched import src_classify
+    from paper_1007_3753_b200.model import SolverConfig
+    from paper_1007_3753_b200.robust import ExtendedDictionary
+    A, lab = synth.cab_dictionary(d=1024, classes=38, per_class=32, subspace=9, seed=0)
+    Bq, truth = synth.cab_queries(A, lab, queries, fraction=0.2, seed=1)
+    cfg = SolverConfig(tol=1e-4, max_iter=2000, options={"dtype": "float32"})
+    ext = ExtendedDictionary(A, 1.0, dtype="float32", device_ordinal=dev.index)
+    Bmat = np.ascontiguousarray(Bq.T)
+    src_classify(ext, lab, Bmat, cfg)             # warm-up (Gram factor cached)
+    torch.cuda.synchronize()
+    s, e = _events(torch)
+    s.record()
+    labels, _, res = src_classify(ext, lab, Bmat, cfg)
+    e.record()
+    torch.cuda.synchronize()
+    t = s.elapsed_time(e) / 1e3
+    its = res.iterations.astype(np.int64)
+    return {"workload": "cfg3: CAB [A I] 1024 x 2240, %d queries, batched DALM fp32 storage, "
+                        "tol 1e-4, min-class-residual labels" % queries,
+            "queries_per_sec": queries / t, "ms_per_batch": 1e3 * t,
+            "mean_iterations": float(its.mean()), "max_iterations": int(its.max()),
+            "accuracy_vs_truth": float(np.mean(labels == truth)),
+            "note": "timed through the public call (host queries in, labels out)"}
+
+
+def leg_cfg5(torch, dev, B=1024):
+    """BASELINE config 5 point: B instances sharing one A (512 x 2048), k ~
+    U[16, 256], batched FISTA fp64 (relative-estimate 1e-6)."""
+    from paper_1007_3753_b200 import synth
+    from paper_1007_3753_b200 import device as dv
+    from paper_1007_3753_b200.batched import fista_solve_batch
+    from paper_1007_3753_b200.model import SolverConfig, StoppingRule
+    d, n = 512, 2048
+    A = synth.gen_gaussian_dict(d, n, 5)
+    rng = np.random.default_rng(55)
+    X = np.zeros((n, B))
+    for j in range(B):
+        kk = int(rng.integers(16, 257))
+        X[rng.choice(n, kk, replace=False), j] = rng.standard_normal(kk)
+    Bmat = A @ X
+    D = dv.DeviceDictionary(A, dtype="float64", device=dev.index)
+    cfg = SolverConfig(lam=None, tol=1e-6, max_iter=5000,
+                       stopping=StoppingRule("relative-estimate", 1e-6))
+    fista_solve_batch(D, Bmat[:, :64], cfg)
+    torch.cuda.synchronize()
+    s, e = _events(torch)
+    s.record()
+    res = fista_solve_batch(D, Bmat, cfg)
+    e.record()
+    torch.cuda.synchronize()
+    t = s.elapsed_time(e) / 1e3
+    its = res.iterations.astype(np.int64)
+    return {"workload": "cfg5: B=%d instances, shared A 512 x 2048 fp64, k~U[16,256], batched "
+                        "FISTA, relative-estimate 1e-6" % B,
+            "solves_per_sec": B / t, "ms_per_batch": 1e3 * t, "iterations_per_sec": float(its.sum()) / t,
+            "mean_iterations": float(its.mean()), "converged": int(res.converged.sum()),
+            "note": "timed through the public call (host B in, host X out)"}
+
+
+def leg_solvers_cfg2(torch, P, reps=3):
+    """Every single-instance solver on the cfg2 instance (ms per solve)."""
+    from paper_1007_3753_b200 import device as dv
+    from paper_1007_3753_b200.alm import dalm_solve, palm_solve
+    from paper_1007_3753_b200.gradient_projection import gpsr_solve, tnipm_solve
+    from paper_1007_3753_b200.homotopy import homotopy_solve
+    from paper_1007_3753_b200.model import ProblemInstance, SolverConfig, StoppingRule
+    from paper_1007_3753_b200.shrinkage import fista_solve, ist_solve
+    D = dv.DeviceDictionary(P.A)
+    Pd = ProblemInstance.__new__(ProblemInstance)
+    Pd.A, Pd.b, Pd.ground_truth, Pd.noise_sigma = D, P.b, P.ground_truth, P.noise_sigma
+    lam = 1e-2 * float(np.max(np.abs(P.A.T @ P.b)))
+    rel = StoppingRule("relative-estimate", 1e-6)
+    cfg = SolverConfig(lam=None, tol=1e-6, stopping=rel)
+    cfgl = SolverConfig(lam=lam, tol=1e-6, stopping=rel)
+    runs = {"fista": lambda: fista_solve(Pd, cfg),
+            "ist": lambda: ist_solve(Pd, None, cfg),
+            "palm": lambda: palm_solve(Pd, cfg),
+            "dalm": lambda: dalm_solve(Pd, cfg),
+            "gpsr": lambda: gpsr_solve(Pd, lam, cfgl),
+            "tnipm": lambda: tnipm_solve(Pd, lam, cfgl),
+            "homotopy": lambda: homotopy_solve(Pd, lam, SolverConfig())}
+    out = {}
+    for name, fn in runs.items():
+        try:
+            fn()
+            torch.cuda.synchronize()
+            s, e = _events(torch)
+            s.record()
+            for _ in range(reps):
+                r = fn()
+            e.record()
+            torch.cuda.synchronize()
+            ms = s.elapsed_time(e) / reps
+            out[name] = {"ms_per_solve": round(ms, 3), "iterations": int(r.iterations),
+                         "converged": bool(r.converged)}
+        except Exception as exc:  # pragma: no cover - report, do not abort the bench
+            out[name] = {"error": str(exc)[:160]}
+    return out
+
+
 def run_b200(args):
     import torch
     ws, rank, local = dist_env()
@@ -346,8 +549,26 @@ def run_b200(args):
                 out["roofline_stream"] = rs
             except Exception as exc:  # pragma: no cover - best effort leg
                 out["roofline_stream"] = {"error": str(exc)[:200]}
+        if not args.no_secondary and ws == 1:
+            sec = {}
+            for name, fn in (("solvers_cfg2", lambda: leg_solvers_cfg2(torch, P)),
+                             ("cfg3", lambda: leg_cfg3(torch, dev)),
+                             ("cfg5", lambda: leg_cfg5(torch, dev))):
+                try:
+                    sec[name] = fn()
+                except Exception as exc:  # pragma: no cover - best effort leg
+                    sec[name] = {"error": str(exc)[:200]}
+            out["secondary"] = sec
         if ws == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(P)
+    if not args.no_secondary:
+        # config 4 runs on every rank (column-sharded, collective)
+        try:
+            c4 = leg_cfg4(torch, dev, ws, rank)
+        except Exception as exc:  # pragma: no cover - best effort leg
+            c4 = {"error": str(exc)[:200]}
+        if out is not None:
+            out.setdefault("secondary", {})["cfg4"] = c4
     if ws > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()

@@ -92,6 +92,27 @@ class DeviceDictionary:
         _lib.check(rc, "ell1_dict_build")
         self._norm_sq = None
 
+    @classmethod
+    def wrap(cls, storage, d):
+        """Adopt a device tensor already in the library layout: ``storage`` is
+        (n, ld) row-major (= column-major A with leading dimension ld, the
+        first d rows of each column used, padding rows zero), float64 or
+        float32.  No copy (large dictionaries generated on the device)."""
+        torch = _torch()
+        _lib.lib()
+        if storage.ndim != 2 or not storage.is_cuda or not storage.is_contiguous():
+            raise ValueError("storage must be a contiguous (n, ld) CUDA tensor")
+        ld = int(storage.shape[1])
+        if ld % 32 or ld < int(d):
+            raise ValueError("ld must be a multiple of 32 and >= d")
+        self = cls.__new__(cls)
+        self.device = storage.device
+        self.d, self.n, self.ld = int(d), int(storage.shape[0]), ld
+        self.dtype = {torch.float64: _lib.F64, torch.float32: _lib.F32}[storage.dtype]
+        self.storage = storage.view(-1)
+        self._norm_sq = None
+        return self
+
     # -- C ABI view --------------------------------------------------------
     def view(self, ext=False, scale=0.0):
         v = _lib.Dict()

@@ -313,12 +313,16 @@ class ShardedFista:
         self.b = o.from_host_d(self.b_host)
         self.gt = o.from_host_n(gt_local) if gt_local is not None else None
         self.gt_norm = float(gt_norm)
+        self.passes = 0        # panel passes (A x or A^T r) of the last solve
+        self.trials = 0
+        self._reset()
+
+    def _reset(self):
+        o = self.ops
         # iterate buffers (swapped, never copied)
         self.x, self.xp, self.xn = o.zeros_n(), o.zeros_n(), o.zeros_n()
         self.gx, self.gxp, self.gn = o.zeros_n(), o.zeros_n(), o.zeros_n()
         self.rx, self.rn, self.ax = o.zeros_d(), o.zeros_d(), o.zeros_d()
-        self.passes = 0        # panel passes (A x or A^T r) of the last solve
-        self.trials = 0
 
     def _kkt(self, x, g, lam, cut):
         self.ops.kkt(x, g, lam, cut)
@@ -337,7 +341,10 @@ class ShardedFista:
         beta = float(cfg.opt("beta", 0.5))
         exact = bool(cfg.opt("exact_L", False))
         bn2 = float(self.b_host @ self.b_host)
+        if self.passes:
+            self._reset()
         self.passes = 0
+        self.trials = 0
         # r_x = A 0 - b = -b ; g_x = A^T r_x = -A^T b ; c0 = max|A^T b|
         o.resid(self.ax, self.b, self.rx, 0.0, self.rx)          # ax == 0 -> rx = -b
         o.gemv_t(self.rx, self.gx)
