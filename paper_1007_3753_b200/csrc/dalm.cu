@@ -456,7 +456,7 @@ extern "C" size_t ell1_dalm_workspace(const ell1_dict_t* D, int32_t blocks) {
   if (!dict_ok(D)) return 0;
   const int nb = pick_blocks(D->n, blocks);
   const int64_t N = ncols_of(D);
-  return grid_bytes(nb, 2 * D->ld) + 4 * align_up(N * 8, 256) + 7 * align_up(D->ld * 8, 256) + 4096;
+  return grid_bytes(nb, D->d, 2) + 4 * align_up(N * 8, 256) + 7 * align_up(D->ld * 8, 256) + 4096;
 }
 
 extern "C" int ell1_dalm(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C,
@@ -475,7 +475,7 @@ extern "C" int ell1_dalm(const ell1_dict_t* D, const double* b, const ell1_ctrl_
   a.ytol = O->y_tol;
   a.cg = O->y_cg_step;
   Carve cv(io->workspace, io->workspace_bytes);
-  if (!carve_grid(cv, a.g, nb, 2 * D->ld)) return ELL1_ERR_ARG;
+  if (!carve_grid(cv, a.g, nb, D->d, 2)) return ELL1_ERR_ARG;
   a.Xg[0] = cv.take<double>(N); a.Xg[1] = cv.take<double>(N);
   a.Zg = cv.take<double>(N); a.Ug = cv.take<double>(N);
   a.Y[0] = cv.take<double>(D->ld); a.Y[1] = cv.take<double>(D->ld);

@@ -38,6 +38,27 @@ __device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned 
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ double2 ldcg2(const double* p) {
+  return __ldcg(reinterpret_cast<const double2*>(p));
+}
+
+// Per-CTA stride of K published scalars: a power of two >= 2.
+__host__ __device__ constexpr int kpad(int K) {
+  return K <= 2 ? 2 : K <= 4 ? 4 : K <= 8 ? 8 : K <= 16 ? 16 : 32;
+}
+
+// Row-slice stride of the partial regions: the largest slice (ceil(d / nb)
+// rows) padded to a power of two (<= 32 rows) or to an even count.
+__host__ __device__ inline int rpad(int64_t d, int nb) {
+  const int64_t rows = (d + nb - 1) / nb;
+  if (rows <= 32) {
+    int p = 2;
+    while (p < rows) p <<= 1;
+    return p;
+  }
+  return (int)((rows + 1) / 2 * 2);
+}
+
 // NaN-propagating max (np.max semantics)
 __device__ __forceinline__ double nmax(double a, double b) { return (a > b || a != a) ? a : b; }
 
@@ -75,13 +96,15 @@ struct Ctx {            // lives in shared memory; written by thread 0 only
   int* abort;
   unsigned long long epoch;
   unsigned nbar;      // barriers passed (selects scalar double-buffer)
-  double* part;       // [nb][pstride] d-vector partials
-  int64_t pstride;
+  double* part;       // d-vector partials, slice-major (see panel_gemv)
+  int64_t pvec;       // doubles per vector slot of `part` (nb * nb * rp)
+  int rp;             // padded row-slice stride (rpad(d, nb))
   double* scal;       // [2][nb][SCAL]
   double* sh;         // shared scratch
   int64_t shcap;      // its capacity in doubles
   unsigned long long* prof;   // optional per-CTA phase timers [nb][16]
   unsigned long long tmark;
+  unsigned long long pacc[16];  // phase accumulators (flushed to prof at mark(-1))
 };
 
 __device__ __forceinline__ int tix() { return (int)threadIdx.x; }
@@ -103,6 +126,7 @@ __device__ __forceinline__ void ctx_init(Ctx& E, int64_t d, int64_t n, int ext) 
   E.nbar = 0;
   E.prof = nullptr;
   E.tmark = 0;
+  for (int k = 0; k < 16; ++k) E.pacc[k] = 0;
 }
 
 // global column index of local owned column k
@@ -115,11 +139,18 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-// accumulate the time since the previous mark into phase k (thread 0 of each CTA)
+// accumulate the time since the previous mark into phase k (thread 0 of each
+// CTA) in shared memory; mark(E, -1) (iteration start) stores the running
+// totals to prof with plain stores, so no L2 round trip sits inside a phase.
 __device__ __forceinline__ void mark(Ctx& E, int k) {
   if (E.prof != nullptr && tix() == 0) {
     const unsigned long long t = gtimer();
-    if (k >= 0) E.prof[(size_t)E.b * 16 + k] += t - E.tmark;
+    if (k >= 0) {
+      E.pacc[k] += t - E.tmark;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) E.prof[(size_t)E.b * 16 + q] = E.pacc[q];
+    }
     E.tmark = t;
   }
 }
@@ -205,53 +236,93 @@ __device__ __forceinline__ void block_reduce(const Ctx& E, double (&v)[K], unsig
   __syncthreads();
 }
 
-// Publish this CTA's K partial scalars into the buffer the next barrier selects.
+// Publish this CTA's K partial scalars into the buffer the next barrier
+// selects: scal[buf][b * kpad(K) + k] (pad slots zero).
 template <int K>
-__device__ __forceinline__ void publish(const Ctx& E, const double (&v)[K], int slot0 = 0) {
-  if (tix() < K) {
-    double* dst = E.scal + ((size_t)((E.nbar + 1) & 1u) * E.nb + E.b) * SCAL + slot0;
-    dst[tix()] = v[tix()];
+__device__ __forceinline__ void publish(const Ctx& E, const double (&v)[K]) {
+  constexpr int KP = kpad(K);
+  if (tix() == 0) {
+    double* dst = E.scal + (size_t)((E.nbar + 1) & 1u) * E.nb * SCAL + (size_t)E.b * KP;
+#pragma unroll
+    for (int k = 0; k < KP; ++k) dst[k] = k < K ? v[k] : 0.0;
   }
 }
 
-// Fixed-order warp reduction of v[q] (q < cnt, stride `stride`) over up to
-// 32*GU entries: every lane issues its loads back to back (no dependent
-// chain of L2 round trips), then sums them in a fixed order.
-constexpr int GU = 5;                     // 5 * 32 = 160 >= 148 CTAs
-__device__ __forceinline__ double warp_fold(const double* base, int cnt, int64_t stride, bool mx) {
-  double s = mx ? -INFINITY : 0.0;
-  for (int q0 = 0; q0 < cnt; q0 += 32 * GU) {
-    double t[GU];
+// Published scalar k of CTA q (K published per CTA) in the current buffer.
+__device__ __forceinline__ const double* published(const Ctx& E, int K, int q, int k) {
+  return E.scal + (size_t)(E.nbar & 1u) * E.nb * SCAL + (size_t)q * kpad(K) + k;
+}
+
+// ----------------------------------------------------------------------------
+// Cross-CTA reductions over "regions": nb rows (one per CTA) of RP doubles
+// (RP a power of two in [2, 32]); entry j of the result = op over rows c of
+// R[c * RP + j], op = max where maxmask bit j is set, else +.
+// Every warp-wide load covers 64 consecutive doubles (16 B per lane, 4 L2
+// lines), so a region of nb rows costs ceil(nb * RP / 64) warp loads — the
+// loads of a warp are issued back to back (one L2 round trip).
+// region_partial: warps wr in [0, nw) each fold a fixed subset of rows into
+// lanes, reduce lanes holding the same entries, and leave entry j of their
+// partial in red_row[j] (j < RP).  region_fold combines the nw partials in
+// warp order.  The order of every combine is fixed, so results are
+// bit-identical in every CTA.
+constexpr int RU = 6;   // warp loads in flight per round
+
+__device__ __forceinline__ double rop(bool mx, double a, double b) { return mx ? nmax(a, b) : a + b; }
+
+__device__ __forceinline__ void region_partial(const double* R, int nb, int RP, unsigned maxmask,
+                                               int wr, int nw, double* red_row) {
+  const int l = lnx();
+  const int G = 64 / RP;                      // rows per warp load
+  const int j = (2 * l) & (RP - 1);
+  const int cl = (2 * l) / RP;
+  const bool m0 = (maxmask >> j) & 1u, m1 = (maxmask >> (j + 1)) & 1u;
+  const double i0 = m0 ? -INFINITY : 0.0, i1 = m1 ? -INFINITY : 0.0;
+  double a0 = i0, a1 = i1;
+  const int ninstr = (nb + G - 1) / G;
+  for (int u0 = wr; u0 < ninstr; u0 += nw * RU) {
+    double2 t[RU];
 #pragma unroll
-    for (int u = 0; u < GU; ++u) {
-      const int q = q0 + lnx() + 32 * u;
-      t[u] = q < cnt ? ldcg(base + (int64_t)q * stride) : (mx ? -INFINITY : 0.0);
+    for (int uu = 0; uu < RU; ++uu) {
+      const int u = u0 + uu * nw;
+      const int c = u * G + cl;
+      if (u < ninstr && c < nb) t[uu] = ldcg2(R + (size_t)c * RP + j);
+      else t[uu] = make_double2(i0, i1);
     }
 #pragma unroll
-    for (int u = 0; u < GU; ++u) s = mx ? nmax(s, t[u]) : s + t[u];
+    for (int uu = 0; uu < RU; ++uu) { a0 = rop(m0, a0, t[uu].x); a1 = rop(m1, a1, t[uu].y); }
   }
-  return mx ? warp_max(s) : warp_sum(s);
+  for (int o = RP / 2; o < 32; o <<= 1) {
+    const double b0 = __shfl_xor_sync(0xffffffffu, a0, o);
+    const double b1 = __shfl_xor_sync(0xffffffffu, a1, o);
+    a0 = rop(m0, a0, b0);
+    a1 = rop(m1, a1, b1);
+  }
+  if (2 * l < RP) { red_row[2 * l] = a0; red_row[2 * l + 1] = a1; }
 }
 
-// reduce published scalar k over all CTAs inside one warp (fixed order)
-__device__ __forceinline__ double gather_one(const Ctx& E, int k, bool mx) {
-  const double* src = E.scal + (size_t)(E.nbar & 1u) * E.nb * SCAL + k;
-  return warp_fold(src, E.nb, SCAL, mx);
+__device__ __forceinline__ double region_fold(const double* red, int wl, int nw, int j, bool mx) {
+  double s = red[wl * 32 + j];
+  for (int w = 1; w < nw; ++w) s = rop(mx, s, red[(wl + w) * 32 + j]);
+  return s;
 }
 
 // After a barrier: reduce the K published scalars over all CTAs (identical
 // in every CTA).  maxmask bit k selects max instead of sum.
 template <int K>
 __device__ __forceinline__ void gather(const Ctx& E, double (&out)[K], unsigned maxmask) {
-  static_assert(K <= NWARP, "one warp per scalar");
-  double* sh = E.sh;
-  if (wpx() < K) {
-    const double s = gather_one(E, wpx(), (maxmask >> wpx()) & 1u);
-    if (lnx() == 0) sh[wpx()] = s;
+  static_assert(K <= 16, "up to 16 scalars");
+  constexpr int KP = kpad(K);
+  double* red = E.sh;                         // [NWARP][32]; results at red[16 + k]
+  const double* src = E.scal + (size_t)(E.nbar & 1u) * E.nb * SCAL;
+  region_partial(src, E.nb, KP, maxmask, wpx(), NWARP, red + wpx() * 32);
+  __syncthreads();
+  if (tix() < K) {
+    const double r = region_fold(red, 0, NWARP, tix(), (maxmask >> tix()) & 1u);
+    red[16 + tix()] = r;                      // row 0 upper half: never read by the folds
   }
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < K; ++k) out[k] = sh[k];
+  for (int k = 0; k < K; ++k) out[k] = red[16 + k];
   __syncthreads();
 }
 
@@ -267,39 +338,108 @@ __device__ __forceinline__ bool allreduce(Ctx& E, double (&v)[K], unsigned maxma
 }
 
 // Fused phase after the barrier that follows panel_gemv: the K scalar
-// gathers and, for every owned row i, sums[v] = sum_c part[c][v*ld + i]
-// (fixed order), then f(i, sums, aux) on lane 0 of the row's warp, with
-// aux[a] = auxv[a][i] prefetched alongside the partial loads.
-// f's per-thread accumulations are the caller's business.
+// gathers and, for every owned row i, sums[v] = sum_c part_v[c][i] (fixed
+// order), then f(i, sums, aux) with aux[a] = auxv[a][i] prefetched
+// alongside the partial loads.  f runs on one thread per row; its
+// per-thread accumulations are the caller's business.
+// Small slices (rp <= 32): the scalar region and the NV partial regions are
+// reduced concurrently by disjoint warp groups (one L2 round trip).  Large
+// slices: one warp per 64-row chunk walks the nb partials with 16-byte loads.
 template <int K, int NV, int NA, class F>
-__device__ void gather_slice(const Ctx& E, double* out, unsigned maxmask, int64_t ld,
+__device__ void gather_slice(const Ctx& E, double* out, unsigned maxmask, int64_t /*ld*/,
                              const double* const (&auxv)[NA > 0 ? NA : 1], F&& f) {
-  double* sh = E.sh;
+  static_assert(K <= 16, "up to 16 scalars");
+  constexpr int KP = kpad(K);
+  double* red = E.sh;
   const int rows = (int)(E.r1 - E.r0);
-  const int items = K + rows;
-  for (int it = wpx(); it < items; it += NWARP) {
-    if (it < K) {
-      const double s = gather_one(E, it, (maxmask >> it) & 1u);
-      if (lnx() == 0) sh[it] = s;
-    } else {
-      const int64_t i = E.r0 + (it - K);
-      double au[NA > 0 ? NA : 1];
-      if (lnx() == 0) {
+  const int RP = E.rp;
+  const int nb = E.nb;
+  const double* own = E.part + (size_t)E.b * nb * RP;     // this CTA's region in slot 0
+  if (RP <= 32) {
+    constexpr int R = (K > 0 ? 1 : 0) + NV;
+    double au[NA > 0 ? NA : 1];
+    const int jt = tix();
+    if (jt < rows) {
 #pragma unroll
-        for (int a = 0; a < NA; ++a) au[a] = ldcg(auxv[a] + i);
-      }
+      for (int a = 0; a < NA; ++a) au[a] = ldcg(auxv[a] + E.r0 + jt);
+    }
+    const int w = wpx();
+    const int r = ((w + 1) * R - 1) / NWARP;
+    const int wl = (NWARP * r) / R, nw = (NWARP * (r + 1)) / R - wl;
+    if (K > 0 && r == 0) {
+      region_partial(E.scal + (size_t)(E.nbar & 1u) * nb * SCAL, nb, KP, maxmask, w - wl, nw,
+                     red + w * 32);
+    } else {
+      const int v = r - (K > 0 ? 1 : 0);
+      region_partial(own + (size_t)v * E.pvec, nb, RP, 0u, w - wl, nw, red + w * 32);
+    }
+    __syncthreads();
+    if (jt < rows) {
       double sums[NV];
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
-        sums[v] = warp_fold(E.part + (size_t)v * ld + i, E.nb, E.pstride, false);
+        const int rr = v + (K > 0 ? 1 : 0);
+        const int l0 = (NWARP * rr) / R, n0 = (NWARP * (rr + 1)) / R - l0;
+        sums[v] = region_fold(red, l0, n0, jt, false);
       }
-      if (lnx() == 0) f(i, sums, au);
+      f(E.r0 + jt, sums, au);
     }
-  }
-  __syncthreads();
+    if (K > 0) {
+      const int k = jt - 32;
+      const int n0 = NWARP / R;                 // scalar region: warps [0, NWARP / R)
+      double sk = 0.0;
+      if (k >= 0 && k < K) sk = region_fold(red, 0, n0, k, (maxmask >> k) & 1u);
+      // red[16 + k] lies in warp 0's row, upper half: no fold reads it
+      if (k >= 0 && k < K) red[16 + k] = sk;
+      __syncthreads();
+      for (int q = 0; q < K; ++q) out[q] = red[16 + q];
+    }
+    __syncthreads();
+  } else {
+    if (K > 0) {
+      double tmp[K > 0 ? K : 1];
+      gather<(K > 0 ? K : 1)>(E, *reinterpret_cast<double(*)[K > 0 ? K : 1]>(tmp), maxmask);
+      for (int q = 0; q < K; ++q) out[q] = tmp[q];
+    }
+    for (int h = wpx(); h * 64 < rows; h += NWARP) {
+      const int j = h * 64 + 2 * lnx();
+      if (j < rows) {
+        double acc[NV][2];
 #pragma unroll
-  for (int k = 0; k < K; ++k) out[k] = sh[k];
-  __syncthreads();
+        for (int v = 0; v < NV; ++v) {
+          const double* Rv = own + (size_t)v * E.pvec + j;
+          double s0 = 0.0, s1 = 0.0;
+          int c = 0;
+          for (; c + 4 <= nb; c += 4) {
+            double2 t[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) t[u] = ldcg2(Rv + (size_t)(c + u) * RP);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { s0 += t[u].x; s1 += t[u].y; }
+          }
+          for (; c < nb; ++c) {
+            const double2 t = ldcg2(Rv + (size_t)c * RP);
+            s0 += t.x; s1 += t.y;
+          }
+          acc[v][0] = s0; acc[v][1] = s1;
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (j + e < rows) {
+            const int64_t i = E.r0 + j + e;
+            double au[NA > 0 ? NA : 1];
+#pragma unroll
+            for (int a = 0; a < NA; ++a) au[a] = ldcg(auxv[a] + i);
+            double sums[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) sums[v] = acc[v][e];
+            f(i, sums, au);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
 }
 
 // ------------------------------------------------------------------ panel
@@ -369,8 +509,15 @@ __device__ Panel<TA> setup_panel(const Ctx& E, const DictV<TA>& D, TA* dst, int 
 }
 
 // ------------------------------------------------------------------ panel GEMV
-// part[b][v * ld + i] = sum_{jl < w} A[i, c0 + jl] * xs[v][jl]  (all rows),
+// Partial of CTA b for row i of vector slot s:  sum_{jl < w} A[i, c0 + jl] xs[v][jl]
+// stored slice-major — in the region of the row's owner o (the CTA whose
+// row slice holds i):  part[s * pvec + o * (nb * rp) + b * rp + (i - r0(o))].
+// The owner then reads its nb x rp region with fully coalesced loads.
 // xs: owned local vectors in shared memory.
+__device__ __forceinline__ int64_t slice_r0(int64_t d, int nb, int64_t o) { return (d * o) / nb; }
+__device__ __forceinline__ int64_t slice_owner(int64_t d, int nb, int64_t i) {
+  return ((i + 1) * nb - 1) / d;
+}
 template <class TA, int NV>
 __device__ void panel_gemv(const Ctx& E, const DictV<TA>& D, const Panel<TA>& P,
                            const double* const (&xs)[NV], bool accumulate = false, int slot0 = 0) {
@@ -378,7 +525,8 @@ __device__ void panel_gemv(const Ctx& E, const DictV<TA>& D, const Panel<TA>& P,
   constexpr int PF = 4;                            // streamed columns prefetched per group
   const int64_t nvec = D.ld / VW;
   const int w = P.w, rc = P.rc;
-  double* out = E.part + (size_t)E.b * E.pstride + (size_t)slot0 * D.ld;
+  double* out = E.part + (size_t)slot0 * E.pvec + (size_t)E.b * E.rp;
+  const int64_t reg = (int64_t)E.nb * E.rp;      // region stride (one owner)
   __syncthreads();
   for (int64_t q = tix(); q < nvec; q += NTHR) {
     double acc[NV][VW];
@@ -457,13 +605,24 @@ __device__ void panel_gemv(const Ctx& E, const DictV<TA>& D, const Panel<TA>& P,
         for (int e = 0; e < VW; ++e) acc[v][e] = fma((double)a[e], xv, acc[v][e]);
       }
     }
-#pragma unroll
-    for (int v = 0; v < NV; ++v)
+    {
+      const int64_t i0 = q * VW;
+      int64_t ow = i0 < D.d ? slice_owner(D.d, E.nb, i0) : 0;
+      int64_t r0 = slice_r0(D.d, E.nb, ow), r1 = slice_r0(D.d, E.nb, ow + 1);
 #pragma unroll
       for (int e = 0; e < VW; ++e) {
-        double* o = out + v * D.ld + q * VW + e;
-        *o = accumulate ? *o + acc[v][e] : acc[v][e];
+        const int64_t i = i0 + e;
+        if (i < D.d) {
+          while (i >= r1) { ++ow; r0 = r1; r1 = slice_r0(D.d, E.nb, ow + 1); }
+          double* o = out + ow * reg + (i - r0);
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            double* ov = o + (size_t)v * E.pvec;
+            *ov = accumulate ? *ov + acc[v][e] : acc[v][e];
+          }
+        }
       }
+    }
   }
 }
 
@@ -606,7 +765,7 @@ __device__ __forceinline__ void for_owned(const Ctx& E, F&& f) {
 
 // shared-memory scratch (doubles) the engine needs next to the panel / owned vectors
 __host__ __device__ inline int64_t engine_scratch_doubles(int kmax) {
-  int64_t s = NWARP * 32;                   // GEMV^T cross-warp staging
+  int64_t s = NWARP * 32;                   // GEMV^T / gather cross-warp staging
   if (s < NWARP * kmax + kmax) s = NWARP * kmax + kmax;
   if (s < 16 * 2) s = 32;
   return (s + 31) / 32 * 32;

@@ -641,7 +641,7 @@ extern "C" size_t ell1_fista_workspace(const ell1_dict_t* D, const ell1_ctrl_t* 
   (void)C;
   const int nb = pick_blocks(D->n, blocks);
   const int64_t N = ncols_of(D);
-  size_t b = grid_bytes(nb, D->ld);
+  size_t b = grid_bytes(nb, D->d, 1);
   b += 5 * align_up(N * 8, 256) + 3 * align_up(D->ld * 8, 256) + 4096;
   return b;
 }
@@ -658,7 +658,7 @@ extern "C" int ell1_fista(const ell1_dict_t* D, const double* b, const ell1_ctrl
   a.C = *C;
   a.O = *O;
   Carve cv(io->workspace, io->workspace_bytes);
-  if (!carve_grid(cv, a.g, nb, D->ld)) return ELL1_ERR_ARG;
+  if (!carve_grid(cv, a.g, nb, D->d, 1)) return ELL1_ERR_ARG;
   for (int k = 0; k < 3; ++k) a.Xg[k] = cv.take<double>(N);
   for (int k = 0; k < 2; ++k) a.Gg[k] = cv.take<double>(N);
   for (int k = 0; k < 3; ++k) a.R[k] = cv.take<double>(D->ld);
@@ -685,7 +685,7 @@ extern "C" int ell1_fista(const ell1_dict_t* D, const double* b, const ell1_ctrl
 extern "C" size_t ell1_correlation_workspace(const ell1_dict_t* D) {
   if (!dict_ok(D)) return 0;
   const int nb = pick_blocks(D->n, 0);
-  return grid_bytes(nb, 32) + 1024;
+  return grid_bytes(nb, D->d, 0) + 1024;
 }
 
 extern "C" int ell1_correlation_max(const ell1_dict_t* D, const double* b, double* out,
@@ -697,7 +697,7 @@ extern "C" int ell1_correlation_max(const ell1_dict_t* D, const double* b, doubl
   a.b = b;
   a.out = out;
   Carve cv(ws, wsb);
-  if (!carve_grid(cv, a.g, nb, 32)) return ELL1_ERR_ARG;
+  if (!carve_grid(cv, a.g, nb, D->d, 0)) return ELL1_ERR_ARG;
   const SmemPlan sp = plan_smem(a.D, nb, 1, 2, false);
   a.g.shcap = sp.scratch;
   a.g.panel_bytes = 0;
@@ -710,7 +710,7 @@ extern "C" int ell1_correlation_max(const ell1_dict_t* D, const double* b, doubl
 extern "C" size_t ell1_power_workspace(const ell1_dict_t* D) {
   if (!dict_ok(D)) return 0;
   const int nb = pick_blocks(D->n, 0);
-  return grid_bytes(nb, D->ld) + 3 * align_up(D->ld * 8, 256) + 2048;
+  return grid_bytes(nb, D->d, 1) + 3 * align_up(D->ld * 8, 256) + 2048;
 }
 
 extern "C" int ell1_spectral_norm_sq(const ell1_dict_t* D, const double* v0, int32_t nredraw,
@@ -723,7 +723,7 @@ extern "C" int ell1_spectral_norm_sq(const ell1_dict_t* D, const double* v0, int
   a.D.ext = 0;
   a.v0 = v0; a.nredraw = nredraw; a.tol = tol; a.max_iter = max_iter; a.out = out;
   Carve cv(ws, wsb);
-  if (!carve_grid(cv, a.g, nb, D->ld)) return ELL1_ERR_ARG;
+  if (!carve_grid(cv, a.g, nb, D->d, 1)) return ELL1_ERR_ARG;
   a.V[0] = cv.take<double>(D->ld);
   a.V[1] = cv.take<double>(D->ld);
   a.W = cv.take<double>(D->ld);

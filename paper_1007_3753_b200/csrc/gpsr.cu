@@ -340,7 +340,7 @@ extern "C" size_t ell1_gpsr_workspace(const ell1_dict_t* D, int32_t blocks) {
   if (!dict_ok(D)) return 0;
   const int nb = pick_blocks(D->n, blocks);
   const int64_t N = ncols_of(D);
-  return grid_bytes(nb, 2 * D->ld) + 3 * align_up(N * 8, 256) + 2 * align_up(D->ld * 8, 256) + 4096;
+  return grid_bytes(nb, D->d, 2) + 3 * align_up(N * 8, 256) + 2 * align_up(D->ld * 8, 256) + 4096;
 }
 
 extern "C" int ell1_gpsr(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C, double lam,
@@ -355,7 +355,7 @@ extern "C" int ell1_gpsr(const ell1_dict_t* D, const double* b, const ell1_ctrl_
   a.C = *C;
   a.lam = lam;
   Carve cv(io->workspace, io->workspace_bytes);
-  if (!carve_grid(cv, a.g, nb, 2 * D->ld)) return ELL1_ERR_ARG;
+  if (!carve_grid(cv, a.g, nb, D->d, 2)) return ELL1_ERR_ARG;
   a.Zg[0] = cv.take<double>(N); a.Zg[1] = cv.take<double>(N); a.Gxg = cv.take<double>(N);
   a.R[0] = cv.take<double>(D->ld); a.R[1] = cv.take<double>(D->ld);
   if (!cv.ok) return ELL1_ERR_ARG;

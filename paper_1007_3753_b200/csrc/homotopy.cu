@@ -408,12 +408,11 @@ __global__ void __launch_bounds__(NTHR, 1) homotopy_kernel(const __grid_constant
           // by publishing again (cheap, scalars only)
           double fix[3];
           {
-            const double* src = E.scal + (size_t)(E.nbar & 1u) * E.nb * SCAL;
             for (int t = 0; t < 3; ++t) {
               double best = -INFINITY;
               for (int q = lnx(); q < E.nb; q += 32) {
-                const double val = ldcg(src + (size_t)q * SCAL + 2 + t);
-                const double idx = ldcg(src + (size_t)q * SCAL + 5 + t);
+                const double val = ldcg(published(E, 8, q, 2 + t));
+                const double idx = ldcg(published(E, 8, q, 5 + t));
                 if (val == G8[2 + t]) best = nmax(best, idx);
               }
               fix[t] = warp_max(best);
@@ -758,7 +757,7 @@ extern "C" size_t ell1_homotopy_workspace(const ell1_dict_t* D, int32_t blocks) 
   const int nb = pick_blocks(D->n, blocks);
   const int64_t N = ncols_of(D);
   const int64_t m = hom_mmax(D);
-  return grid_bytes(nb, D->ld) + 2 * align_up(m * m * 8, 256) + 2 * align_up(m * 4, 256) +
+  return grid_bytes(nb, D->d, 1) + 2 * align_up(m * m * 8, 256) + 2 * align_up(m * 4, 256) +
          align_up(N * 4, 256) + 3 * align_up(m * 8, 256) + align_up(N * 8, 256) +
          3 * align_up(D->ld * 8, 256) + 4096;
 }
@@ -781,7 +780,7 @@ extern "C" int ell1_homotopy(const ell1_dict_t* D, const double* b, double targe
   a.mmax = hom_mmax(D);
   const int64_t m = a.mmax;
   Carve cv(io->workspace, io->workspace_bytes);
-  if (!carve_grid(cv, a.g, nb, D->ld)) return ELL1_ERR_ARG;
+  if (!carve_grid(cv, a.g, nb, D->d, 1)) return ELL1_ERR_ARG;
   a.R = cv.take<double>(m * m); a.G = cv.take<double>(m * m);
   a.sup = cv.take<int>(m); a.posof = cv.take<int>(N);
   a.sgn = cv.take<double>(m); a.dI = cv.take<double>(m); a.gcol = cv.take<double>(m);

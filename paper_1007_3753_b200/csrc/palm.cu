@@ -294,7 +294,7 @@ extern "C" size_t ell1_palm_workspace(const ell1_dict_t* D, int32_t blocks) {
   if (!dict_ok(D)) return 0;
   const int nb = pick_blocks(D->n, blocks);
   const int64_t N = ncols_of(D);
-  return grid_bytes(nb, D->ld) + 2 * align_up(N * 8, 256) + 2 * align_up(D->ld * 8, 256) + 4096;
+  return grid_bytes(nb, D->d, 1) + 2 * align_up(N * 8, 256) + 2 * align_up(D->ld * 8, 256) + 4096;
 }
 
 extern "C" int ell1_palm(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C,
@@ -309,7 +309,7 @@ extern "C" int ell1_palm(const ell1_dict_t* D, const double* b, const ell1_ctrl_
   a.C = *C;
   a.mu0 = O->mu0; a.rho = O->rho; a.tau = O->tau;
   Carve cv(io->workspace, io->workspace_bytes);
-  if (!carve_grid(cv, a.g, nb, D->ld)) return ELL1_ERR_ARG;
+  if (!carve_grid(cv, a.g, nb, D->d, 1)) return ELL1_ERR_ARG;
   a.Xg[0] = cv.take<double>(N);
   a.Xg[1] = cv.take<double>(N);
   a.Yd = cv.take<double>(D->ld);

@@ -37,16 +37,25 @@ __global__ void __launch_bounds__(NTHR, 1) gemv_partial_kernel(const __grid_cons
   panel_gemv<TA, 1>(E, D, PN, xs);
 }
 
-// y[i] = sum_c part[c][i] in fixed order (one warp per row)
-__global__ void __launch_bounds__(NTHR) gemv_reduce_kernel(const double* part, int64_t pstride, int nb,
-                                                           int64_t d, double* y) {
-  const int64_t row0 = (int64_t)blockIdx.x * NWARP;
-  const int64_t i = row0 + (threadIdx.x >> 5);
-  if (i >= d) return;
-  __shared__ Ctx E;   // unused; warp_fold is self-contained
-  (void)E;
-  const double s = warp_fold(part + i, nb, pstride, false);
-  if ((threadIdx.x & 31) == 0) y[i] = s;
+// y[r0(o) + j] = sum_c part[o][c][j] in fixed order (block o reduces the
+// region of row slice o; 16-byte loads, consecutive threads -> consecutive rows)
+__global__ void __launch_bounds__(NTHR) gemv_reduce_kernel(const double* part, int rp, int nb, int64_t d,
+                                                           double* y) {
+  const int o = blockIdx.x;
+  const int64_t r0 = (d * o) / nb, r1 = (d * (o + 1)) / nb;
+  const int rows = (int)(r1 - r0);
+  const double* R = part + (size_t)o * nb * rp;
+  for (int j = 2 * (int)threadIdx.x; j < rows; j += 2 * NTHR) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll 4
+    for (int c = 0; c < nb; ++c) {
+      const double2 t = ldcg2(R + (size_t)c * rp + j);
+      s0 += t.x;
+      s1 += t.y;
+    }
+    y[r0 + j] = s0;
+    if (j + 1 < rows) y[r0 + j + 1] = s1;
+  }
 }
 
 template <class TA>
@@ -156,7 +165,7 @@ using namespace ell1;
 extern "C" size_t ell1_gemv_workspace(const ell1_dict_t* D) {
   if (!dict_ok(D)) return 0;
   const int nb = pick_blocks(D->n, 0);
-  return grid_bytes(nb, D->ld) + (size_t)EW_BLOCKS * SP * 8 + 4096;
+  return grid_bytes(nb, D->d, 1) + (size_t)EW_BLOCKS * SP * 8 + 4096;
 }
 
 extern "C" int ell1_gemv(const ell1_dict_t* D, const double* x, double* y, void* ws, size_t wsb, void* stream) {
@@ -167,7 +176,7 @@ extern "C" int ell1_gemv(const ell1_dict_t* D, const double* x, double* y, void*
   a.D.ext = 0;
   a.x = x; a.y = y;
   Carve cv(ws, wsb);
-  if (!carve_grid(cv, a.g, nb, D->ld)) return ELL1_ERR_ARG;
+  if (!carve_grid(cv, a.g, nb, D->d, 1)) return ELL1_ERR_ARG;
   const SmemPlan sp = plan_smem(a.D, nb, 0, 2, false);
   a.g.shcap = sp.scratch;
   a.g.panel_bytes = 0;
@@ -179,7 +188,7 @@ extern "C" int ell1_gemv(const ell1_dict_t* D, const double* x, double* y, void*
     cudaFuncSetAttribute(gemv_partial_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.bytes);
     gemv_partial_kernel<float><<<nb, NTHR, sp.bytes, s>>>(a);
   }
-  gemv_reduce_kernel<<<(unsigned)((D->d + NWARP - 1) / NWARP), NTHR, 0, s>>>(a.g.part, a.g.pstride, nb, D->d, y);
+  gemv_reduce_kernel<<<nb, NTHR, 0, s>>>(a.g.part, a.g.rp, nb, D->d, y);
   return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
 }
 
@@ -191,7 +200,7 @@ extern "C" int ell1_gemv_t(const ell1_dict_t* D, const double* r, double* g, voi
   a.D.ext = 0;
   a.x = r; a.y = g;
   Carve cv(ws, wsb);
-  if (!carve_grid(cv, a.g, nb, D->ld)) return ELL1_ERR_ARG;
+  if (!carve_grid(cv, a.g, nb, D->d, 1)) return ELL1_ERR_ARG;
   const SmemPlan sp = plan_smem(a.D, nb, 0, 2, false);
   a.g.shcap = sp.scratch;
   a.g.panel_bytes = 0;

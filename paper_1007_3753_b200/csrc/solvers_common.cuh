@@ -15,8 +15,9 @@ struct DictRaw {
 
 // Grid-shared scratch common to every persistent solver.
 struct GridBufs {
-  double* part;               // [nb][pstride]
-  int64_t pstride;
+  double* part;               // nv slots of pvec doubles (slice-major partials)
+  int64_t pvec;
+  int rp;
   double* scal;               // [2][nb][SCAL]
   unsigned long long* bar;
   int* abort;
@@ -34,7 +35,7 @@ __device__ __forceinline__ DictV<TA> dict_view(const DictRaw& R) {
 
 // thread 0 only
 __device__ __forceinline__ void ctx_bind(Ctx& E, const GridBufs& g, double* smem) {
-  E.bar = g.bar; E.abort = g.abort; E.part = g.part; E.pstride = g.pstride;
+  E.bar = g.bar; E.abort = g.abort; E.part = g.part; E.pvec = g.pvec; E.rp = g.rp;
   E.scal = g.scal; E.sh = smem; E.shcap = g.shcap;
 }
 
@@ -112,13 +113,17 @@ struct Carve {
   }
 };
 
-inline size_t grid_bytes(int nb, int64_t pstride) {
-  return align_up((int64_t)nb * pstride * 8, 256) + align_up((int64_t)2 * nb * SCAL * 8, 256) + 512;
+// Grid scratch for nv partial d-vectors of a d-row operator over nb CTAs.
+inline size_t grid_bytes(int nb, int64_t d, int nv) {
+  const int64_t pvec = (int64_t)nb * nb * rpad(d, nb);
+  return align_up((int64_t)(nv > 0 ? nv : 1) * pvec * 8, 256) + align_up((int64_t)2 * nb * SCAL * 8, 256) +
+         512;
 }
 
-inline bool carve_grid(Carve& cv, GridBufs& g, int nb, int64_t pstride) {
-  g.part = cv.take<double>((size_t)nb * pstride);
-  g.pstride = pstride;
+inline bool carve_grid(Carve& cv, GridBufs& g, int nb, int64_t d, int nv) {
+  g.rp = rpad(d, nb);
+  g.pvec = (int64_t)nb * nb * g.rp;
+  g.part = cv.take<double>((size_t)(nv > 0 ? nv : 1) * g.pvec);
   g.scal = cv.take<double>((size_t)2 * nb * SCAL);
   g.bar = cv.take<unsigned long long>(4);
   g.abort = reinterpret_cast<int*>(g.bar + 2);

@@ -535,7 +535,7 @@ extern "C" size_t ell1_tnipm_workspace(const ell1_dict_t* D, int32_t blocks) {
   if (!dict_ok(D)) return 0;
   const int nb = pick_blocks(D->n, blocks);
   const int64_t N = ncols_of(D);
-  return grid_bytes(nb, D->ld) + 2 * align_up(N * 8, 256) + 3 * align_up(D->ld * 8, 256) + 4096;
+  return grid_bytes(nb, D->d, 1) + 2 * align_up(N * 8, 256) + 3 * align_up(D->ld * 8, 256) + 4096;
 }
 
 extern "C" int ell1_tnipm(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C, double lam,
@@ -553,7 +553,7 @@ extern "C" int ell1_tnipm(const ell1_dict_t* D, const double* b, const ell1_ctrl
   a.pcg_tol = pcg_tol;
   a.pcg_cap = pcg_max_iter;
   Carve cv(io->workspace, io->workspace_bytes);
-  if (!carve_grid(cv, a.g, nb, D->ld)) return ELL1_ERR_ARG;
+  if (!carve_grid(cv, a.g, nb, D->d, 1)) return ELL1_ERR_ARG;
   a.Xg[0] = cv.take<double>(N); a.Xg[1] = cv.take<double>(N);
   a.Rv = cv.take<double>(D->ld); a.APd = cv.take<double>(D->ld); a.ADX = cv.take<double>(D->ld);
   if (!cv.ok) return ELL1_ERR_ARG;
