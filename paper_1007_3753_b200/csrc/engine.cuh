@@ -143,7 +143,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // CTA) in shared memory; mark(E, -1) (iteration start) stores the running
 // totals to prof with plain stores, so no L2 round trip sits inside a phase.
 __device__ __forceinline__ void mark(Ctx& E, int k) {
-  if (E.prof != nullptr && tix() == 0) {
+  if (tix() == 0 && E.prof != nullptr) {
     const unsigned long long t = gtimer();
     if (k >= 0) {
       E.pacc[k] += t - E.tmark;
@@ -454,14 +454,17 @@ struct Panel {
 };
 
 template <class TA>
-__device__ __forceinline__ void ld16_s(const TA* p, TA (&a)[VecOf<TA>::VW]) {
-  const unsigned addr = (unsigned)__cvta_generic_to_shared(p);
+__device__ __forceinline__ void ld16_sa(unsigned addr, TA (&a)[VecOf<TA>::VW]) {
   if constexpr (sizeof(TA) == 8) {
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a[0]), "=d"(a[1]) : "r"(addr));
   } else {
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                  : "=f"(a[0]), "=f"(a[1]), "=f"(a[2]), "=f"(a[3]) : "r"(addr));
   }
+}
+template <class TA>
+__device__ __forceinline__ void ld16_s(const TA* p, TA (&a)[VecOf<TA>::VW]) {
+  ld16_sa<TA>((unsigned)__cvta_generic_to_shared(p), a);
 }
 template <class TA>
 __device__ __forceinline__ void ld16_g(const TA* p, TA (&a)[VecOf<TA>::VW]) {
@@ -514,8 +517,13 @@ __device__ Panel<TA> setup_panel(const Ctx& E, const DictV<TA>& D, TA* dst, int 
 // row slice holds i):  part[s * pvec + o * (nb * rp) + b * rp + (i - r0(o))].
 // The owner then reads its nb x rp region with fully coalesced loads.
 // xs: owned local vectors in shared memory.
-__device__ __forceinline__ int64_t slice_r0(int64_t d, int nb, int64_t o) { return (d * o) / nb; }
+// (32-bit arithmetic when d * nb fits, which covers every practical shape)
+__device__ __forceinline__ int64_t slice_r0(int64_t d, int nb, int64_t o) {
+  if (d * nb < 0xFFFFFFFFLL) return (int64_t)((unsigned)d * (unsigned)o / (unsigned)nb);
+  return (d * o) / nb;
+}
 __device__ __forceinline__ int64_t slice_owner(int64_t d, int nb, int64_t i) {
+  if (d * nb < 0xFFFFFFFFLL) return (int64_t)((((unsigned)i + 1u) * (unsigned)nb - 1u) / (unsigned)d);
   return ((i + 1) * nb - 1) / d;
 }
 template <class TA, int NV>
@@ -543,12 +551,13 @@ __device__ void panel_gemv(const Ctx& E, const DictV<TA>& D, const Panel<TA>& P,
       if (u < ng) ld16_g<TA>(P.gl + (int64_t)(rc + u) * D.ld + q * VW, g[u]);
     // resident columns
     {
-      const TA* p = P.sm + q * VW;
+      const unsigned p = (unsigned)__cvta_generic_to_shared(P.sm + q * VW);
+      const unsigned cst = (unsigned)(D.ld * sizeof(TA));
       int jj = 0;
       for (; jj + 4 <= rc; jj += 4) {
         TA a[4][VW];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) ld16_s<TA>(p + (int64_t)(jj + u) * D.ld, a[u]);
+        for (int u = 0; u < 4; ++u) ld16_sa<TA>(p + (unsigned)(jj + u) * cst, a[u]);
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -560,7 +569,7 @@ __device__ void panel_gemv(const Ctx& E, const DictV<TA>& D, const Panel<TA>& P,
       }
       for (; jj < rc; ++jj) {
         TA a[VW];
-        ld16_s<TA>(p + (int64_t)jj * D.ld, a);
+        ld16_sa<TA>(p + (unsigned)jj * cst, a);
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
           const double xv = xs[v][jj];
@@ -635,42 +644,87 @@ __device__ void panel_gemv(const Ctx& E, const DictV<TA>& D, const Panel<TA>& P,
 // registers, forms per-column partials for a chunk of 32 columns, and a
 // warp transpose-reduction (31 shuffles / 32 columns) + a 16-way fixed-order
 // cross-warp sum finish them.  Long columns: warp per (column, segment).
+// Operands of the short-column GEMV^T that can be loaded ahead of time
+// (before the decision that needs them is known): thread q's slice of r and
+// the first streamed (non-resident) panel column.  Issuing these loads early
+// overlaps their L2 latency with other work.
+template <class TA, int NV>
+struct GtPre {
+  double rq[NV][VecOf<TA>::VW];
+  TA g[VecOf<TA>::VW];
+};
+
+template <class TA, int NV>
+__device__ __forceinline__ void gemv_t_prefetch(const DictV<TA>& D, const Panel<TA>& P,
+                                                const double* const (&rs)[NV], GtPre<TA, NV>& pre) {
+  constexpr int VW = VecOf<TA>::VW;
+  const int64_t nvec = D.ld / VW;
+  if (nvec > NTHR) return;                          // long columns stage r themselves
+  const int64_t q = tix();
+  const bool act = q < nvec;
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int e = 0; e < VW; ++e) pre.rq[v][e] = act ? ldcg(rs[v] + q * VW + e) : 0.0;
+  if (act && P.rc < P.w) ld16_g<TA>(P.gl + (int64_t)P.rc * D.ld + q * VW, pre.g);
+  else {
+#pragma unroll
+    for (int e = 0; e < VW; ++e) pre.g[e] = (TA)0;
+  }
+}
+
+template <class TA, int NV>
+__device__ void panel_gemv_t_pre(const Ctx& E, const DictV<TA>& D, const Panel<TA>& P,
+                                 const GtPre<TA, NV>& pre, const double* const (&rs)[NV],
+                                 double* const (&outs)[NV]);
+
 template <class TA, int NV>
 __device__ void panel_gemv_t(const Ctx& E, const DictV<TA>& D, const Panel<TA>& P,
                              const double* const (&rs)[NV], double* const (&outs)[NV]) {
+  GtPre<TA, NV> pre;
+  gemv_t_prefetch<TA, NV>(D, P, rs, pre);
+  panel_gemv_t_pre<TA, NV>(E, D, P, pre, rs, outs);
+}
+
+template <class TA, int NV>
+__device__ void panel_gemv_t_pre(const Ctx& E, const DictV<TA>& D, const Panel<TA>& P,
+                                 const GtPre<TA, NV>& pre, const double* const (&rs)[NV],
+                                 double* const (&outs)[NV]) {
   constexpr int VW = VecOf<TA>::VW;
   const int64_t nvec = D.ld / VW;
   const int w = P.w, rc = P.rc;
-  double* red = E.sh;                               // [NWARP][32] per v pass
+  double* red = E.sh;                               // [NWARP][CW] per v pass
   __syncthreads();
   if (nvec <= NTHR) {
     const int64_t q = tix();
     const bool act = q < nvec;
-    double rq[NV][VW];
-#pragma unroll
-    for (int v = 0; v < NV; ++v)
-#pragma unroll
-      for (int e = 0; e < VW; ++e) rq[v][e] = act ? ldcg(rs[v] + q * VW + e) : 0.0;
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(P.sm + q * VW);
+    const unsigned cst = (unsigned)(D.ld * sizeof(TA));
     constexpr int CW = 16;                          // columns per transpose-reduce chunk
+    int cb = 0;                                     // staging buffer (double-buffered: one sync per chunk)
     for (int j0 = 0; j0 < w; j0 += CW) {
       const int cnt = (w - j0) < CW ? (w - j0) : CW;
 #pragma unroll
-      for (int v = 0; v < NV; ++v) {
+      for (int v = 0; v < NV; ++v, cb ^= 1) {
+        double* rb = red + cb * (NWARP * CW);
         double p[CW];
 #pragma unroll
         for (int u = 0; u < CW; ++u) {
           TA a[VW];
           const int j = j0 + u;
           if (u < cnt && act) {
-            if (j < rc) ld16_s<TA>(P.sm + (int64_t)j * D.ld + q * VW, a);
-            else ld16_g<TA>(P.gl + (int64_t)j * D.ld + q * VW, a);
+            if (j < rc) ld16_sa<TA>(sbase + (unsigned)j * cst, a);
+            else if (j == rc) {
+#pragma unroll
+              for (int e = 0; e < VW; ++e) a[e] = pre.g[e];
+            } else ld16_g<TA>(P.gl + (int64_t)j * D.ld + q * VW, a);
           } else {
 #pragma unroll
             for (int e = 0; e < VW; ++e) a[e] = (TA)0;
           }
           double s = 0.0;
 #pragma unroll
-          for (int e = 0; e < VW; ++e) s = fma((double)a[e], rq[v][e], s);
+          for (int e = 0; e < VW; ++e) s = fma((double)a[e], pre.rq[v][e], s);
           p[u] = s;
         }
         // transpose-reduce: afterwards lane l (and l^16) holds the warp sum of column j0 + (l & 15)
@@ -685,20 +739,20 @@ __device__ void panel_gemv_t(const Ctx& E, const DictV<TA>& D, const Panel<TA>& 
           }
         }
         p[0] += __shfl_xor_sync(0xffffffffu, p[0], 16);
-        if (lnx() < CW) red[wpx() * CW + lnx()] = p[0];
+        if (lnx() < CW) rb[wpx() * CW + lnx()] = p[0];
         __syncthreads();
         if (tix() < cnt) {
           double t[NWARP];
 #pragma unroll
-          for (int ww = 0; ww < NWARP; ++ww) t[ww] = red[ww * CW + tix()];
+          for (int ww = 0; ww < NWARP; ++ww) t[ww] = rb[ww * CW + tix()];
           double s = t[0];
 #pragma unroll
           for (int ww = 1; ww < NWARP; ++ww) s += t[ww];
           outs[v][j0 + tix()] = s;
         }
-        __syncthreads();
       }
     }
+    __syncthreads();
   } else {
     // Long columns: column groups of NWARP x CPW; r is staged through shared
     // memory in row chunks shared by every warp of the group, so each r

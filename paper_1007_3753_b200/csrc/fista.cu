@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(const __grid_constant__ 
         });
       }
       mark(E, 0);
+      GtPre<TA, 1> gpre;
       while (true) {                                      // backtracking (shrinkage.py:199-213)
         T0 {
           if (V.bt > 100) { V.status = ELL1_BREAKDOWN; V.quit = 1; }   // shrinkage.py:203,213
@@ -339,6 +340,12 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(const __grid_constant__ 
         if (!grid_sync(E)) { T0 V.status = ELL1_ERR_TIMEOUT; goto out; }
         mark(E, 5);
         {
+          // r_next is complete: start loading the GEMV^T operands now so their
+          // L2 latency overlaps the decision round trip (used only on accept)
+          {
+            const double* rs[1] = {a.R[V.irn]};
+            gemv_t_prefetch<TA, 1>(D, PN, rs, gpre);
+          }
           double Q2[2];
           gather<2>(E, Q2, 0u);
           T0 {
@@ -375,7 +382,7 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(const __grid_constant__ 
       {
         const double* rs[1] = {a.R[V.irx]};
         double* os[1] = {Gp(V.igx)};
-        panel_gemv_t<TA, 1>(E, D, PN, rs, os);           // g_x = A^T r_next  (shrinkage.py:285)
+        panel_gemv_t_pre<TA, 1>(E, D, PN, gpre, rs, os);   // g_x = A^T r_next  (shrinkage.py:285)
       }
       mark(E, 7);
       {
