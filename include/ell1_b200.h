@@ -144,6 +144,35 @@ int ell1_project_box_linf(const double* z, double* out, int64_t n, void* stream)
 int ell1_chol_update(double* R, double* v, int64_t m, int32_t* status, void* stream);
 int ell1_chol_downdate(double* R, double* v, int64_t m, int32_t* status, void* stream);
 
+/* ------------------------------------------------ numerics / operator utilities
+ * (csrc/linalg.cu).  Factors are row-major m x m
+ * upper triangles R with R^T R = G. */
+/* R = chol(G) upper; *status 0, or 1 when G is not positive definite
+ * (numerics.chol_factor, numerics.py:75-87). */
+int ell1_chol_factor(const double* G, double* R, int64_t m, int32_t* status, void* stream);
+/* out = (R^T R)^{-1} rhs by two triangular solves (CholFactor.solve, numerics.py:62-65). */
+int ell1_chol_solve(const double* R, const double* rhs, double* out, int64_t m, void* stream);
+/* Rout ((m+1) x (m+1)) = factor of [[G, g], [g^T, diag]]; work: m doubles;
+ * *status 1 when the extension is not PD (numerics.chol_append, numerics.py:115-137). */
+int ell1_chol_append(const double* R, int64_t m, const double* g, double diag, double* Rout,
+                     double* work, int32_t* status, void* stream);
+/* out[j] = sum_i A_ij^2 (DenseDictionary.column_norms_sq, operators.py:44-45). */
+int ell1_column_norms_sq(const ell1_dict_t* D, double* out, void* stream);
+/* G (d x d) = A diag(w) A^T, w == NULL -> A A^T (operators.py:53-58; cuBLAS DGEMM). */
+size_t ell1_gram_dd_workspace(const ell1_dict_t* D);
+int ell1_gram_dd(const ell1_dict_t* D, const double* w, double* G, void* ws, size_t ws_bytes, void* stream);
+/* out = a x + b y (y may be NULL) and *out = sum x_i^2 (fixed order) — the
+ * vector steps of dual_y_solve (alm.py:172-189). */
+int ell1_axpby(int64_t n, double a, const double* x, double b, const double* y, double* out, void* stream);
+int ell1_sumsq(int64_t n, const double* x, double* out, void* stream);
+/* Jacobi-preconditioned CG on a dense symmetric M (D with d == n; diag NULL ->
+ * identity); out4 = {converged, iterations, residual / ||rhs||, status}
+ * (numerics.pcg_solve, numerics.py:164-221; status ELL1_BREAKDOWN on
+ * non-finite curvature / residual). */
+size_t ell1_pcg_workspace(const ell1_dict_t* M);
+int ell1_pcg_dense(const ell1_dict_t* M, const double* rhs, const double* diag, double tol,
+                   int32_t max_iter, double* x, double* out4, void* ws, size_t ws_bytes, void* stream);
+
 /* --------------------------------------------------------------- solvers */
 
 /* Accelerated proximal gradient with backtracking and continuation —

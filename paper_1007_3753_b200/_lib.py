@@ -106,6 +106,23 @@ _SIGS = {
                                         ctypes.c_void_p, ctypes.c_void_p]),
     "ell1_chol_downdate": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                           ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_chol_factor": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                        ctypes.c_void_p]),
+    "ell1_chol_solve": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                       ctypes.c_void_p]),
+    "ell1_chol_append": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_double,
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_column_norms_sq": (ctypes.c_int, [P(Dict), ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_gram_dd_workspace": (ctypes.c_size_t, [P(Dict)]),
+    "ell1_gram_dd": (ctypes.c_int, [P(Dict), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                    ctypes.c_void_p]),
+    "ell1_pcg_workspace": (ctypes.c_size_t, [P(Dict)]),
+    "ell1_pcg_dense": (ctypes.c_int, [P(Dict), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_int32,
+                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                      ctypes.c_void_p]),
+    "ell1_axpby": (ctypes.c_int, [ctypes.c_int64, ctypes.c_double, ctypes.c_void_p, ctypes.c_double,
+                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_sumsq": (ctypes.c_int, [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "ell1_fista_workspace": (ctypes.c_size_t, [P(Dict), P(Ctrl), ctypes.c_int32]),
     "ell1_fista": (ctypes.c_int, [P(Dict), ctypes.c_void_p, P(Ctrl), P(FistaOpts), P(IO),
                                   ctypes.c_void_p]),

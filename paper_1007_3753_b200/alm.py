@@ -14,32 +14,11 @@ from paper_1007_3753_b200 import _lib, device
 from paper_1007_3753_b200._runner import Buffers, Prepared, byref, drive, host_vec, raise_for
 from paper_1007_3753_b200.exceptions import IllConditionedError
 from paper_1007_3753_b200.model import SolverResult, TraceEntry
+from paper_1007_3753_b200.numerics import CholFactor  # noqa: F401  (alm.CholFactor in the reference)
 
 _INNER_CAP = 200        # alm.py:23
 _Y_REFINE_TOL = 1e-10   # alm.py:24
 _Y_REFINE_TOL_F32 = 1e-5  # documented fp32-storage scaling of the certificate
-
-
-class CholFactor:
-    """Upper factor R with R^T R = G (numerics.py:47-72), host copy."""
-
-    __slots__ = ("R",)
-
-    def __init__(self, R):
-        R = np.ascontiguousarray(R, dtype=np.float64)
-        if R.ndim != 2 or R.shape[0] != R.shape[1]:
-            raise ValueError("factor must be square, got shape %r" % (R.shape,))
-        self.R = R
-
-    @property
-    def dim(self):
-        return self.R.shape[0]
-
-    def matrix(self):
-        return self.R.T @ self.R
-
-    def copy(self):
-        return CholFactor(self.R.copy())
 
 
 @dataclass
@@ -148,3 +127,61 @@ def palm_solve(P, config, observer=None):
     (alm.py:96-159)."""
     from paper_1007_3753_b200._palm import palm_solve_device
     return palm_solve_device(P, config, observer)
+
+
+def dual_y_solve(state, A, z_next, b):
+    """Least-squares multiplier step of the dual iteration (alm.py:172-189):
+    solve beta A A^T y = beta A z_next - (A x - b) through state.gram_chol,
+    certify ||rhs - A A^T y|| <= 1e-10 max(1, ||rhs||), refine once, else
+    IllConditionedError.  Products, solves and norms run on the device."""
+    import ctypes
+    from paper_1007_3753_b200.operators import DenseDictionary
+    torch = device._torch()
+    op = A if isinstance(A, DenseDictionary) else DenseDictionary(A)
+    D = op.device_dictionary()
+    dev, d, n = D.device, D.d, D.n
+    L = _lib.lib()
+    st = device.stream_ptr(dev)
+    R = np.ascontiguousarray(state.gram_chol.R, dtype=np.float64)
+    if R.shape != (d, d):
+        raise ValueError("gram factor must be d x d")
+    Rd = torch.from_numpy(R).to(dev)
+    zd = device.to_device_vec(np.asarray(z_next, np.float64), n, dev)
+    xd = device.to_device_vec(np.asarray(state.x, np.float64), n, dev)
+    bd = device.to_device_vec(np.asarray(b, np.float64), D.ld, dev)
+    Az = op._apply_dev(zd)
+    Ax = op._apply_dev(xd)
+    t = torch.empty_like(Ax)
+    _lib.check(L.ell1_axpby(d, 1.0, device.ptr(Ax), -1.0, device.ptr(bd), device.ptr(t), st), "ell1_axpby")
+    rhs = torch.zeros_like(Ax)
+    _lib.check(L.ell1_axpby(d, 1.0, device.ptr(Az), -1.0 / float(state.beta), device.ptr(t), device.ptr(rhs), st),
+               "ell1_axpby")
+    s2 = torch.zeros(2, dtype=torch.float64, device=dev)
+
+    def solve(v):
+        out = torch.zeros_like(v)
+        _lib.check(L.ell1_chol_solve(device.ptr(Rd), device.ptr(v), device.ptr(out), d, st), "ell1_chol_solve")
+        return out
+
+    def residual(y):
+        AAy = op._apply_dev(op._adjoint_dev(y))
+        res = torch.zeros_like(y)
+        _lib.check(L.ell1_axpby(d, 1.0, device.ptr(rhs), -1.0, device.ptr(AAy), device.ptr(res), st),
+                   "ell1_axpby")
+        _lib.check(L.ell1_sumsq(d, device.ptr(res), device.ptr(s2[1:]), st), "ell1_sumsq")
+        return res
+
+    y = solve(rhs)
+    _lib.check(L.ell1_sumsq(d, device.ptr(rhs), device.ptr(s2), st), "ell1_sumsq")
+    res = residual(y)
+    h = s2.cpu().numpy()
+    scale = max(1.0, float(np.sqrt(h[0])))
+    if float(np.sqrt(h[1])) > _Y_REFINE_TOL * scale:
+        dy = solve(res)
+        y2 = torch.zeros_like(y)
+        _lib.check(L.ell1_axpby(d, 1.0, device.ptr(y), 1.0, device.ptr(dy), device.ptr(y2), st), "ell1_axpby")
+        y = y2
+        residual(y)
+        if float(np.sqrt(s2.cpu().numpy()[1])) > _Y_REFINE_TOL * scale:
+            raise IllConditionedError("dual least-squares step failed its residual contract")
+    return y[:d].cpu().numpy()

@@ -80,6 +80,26 @@ __global__ void chol_rank1_kernel(double* R, double* v, int64_t m, int sign, int
   if (threadIdx.x == 0 && status) *status = fail;
 }
 
+__global__ void axpby_kernel(int64_t n, double a, const double* __restrict__ x, double b,
+                             const double* __restrict__ y, double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = a * x[i] + (y ? b * y[i] : 0.0);
+}
+
+// sum of squares, one CTA, fixed order (per-thread strided partials, tree)
+__global__ void sumsq_kernel(int64_t n, const double* __restrict__ x, double* out) {
+  __shared__ double sh[1024];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = fma(x[i], x[i], s);
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
 int grid_for(int64_t n) {
   int64_t g = (n + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
@@ -129,6 +149,20 @@ extern "C" int ell1_chol_downdate(double* R, double* v, int64_t m, int32_t* stat
   if (m < 0) return ELL1_ERR_ARG;
   if (m == 0) return cudaMemsetAsync(status, 0, 4, (cudaStream_t)stream) == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
   chol_rank1_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(R, v, m, -1, status);
+  return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
+}
+
+extern "C" int ell1_axpby(int64_t n, double a, const double* x, double b, const double* y, double* out,
+                          void* stream) {
+  if (n < 0 || !x || !out) return ELL1_ERR_ARG;
+  if (n == 0) return ELL1_OK;
+  axpby_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(n, a, x, b, y, out);
+  return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
+}
+
+extern "C" int ell1_sumsq(int64_t n, const double* x, double* out, void* stream) {
+  if (n < 0 || !out || (n > 0 && !x)) return ELL1_ERR_ARG;
+  sumsq_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(n, x, out);
   return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
 }
 

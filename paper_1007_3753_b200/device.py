@@ -168,6 +168,8 @@ def as_device_dictionary(A, config=None):
     """Return (DeviceDictionary, owned) for whatever the caller passed as A."""
     if isinstance(A, DeviceDictionary):
         return A, False
+    if hasattr(A, "device_dictionary"):          # operators.DenseDictionary
+        return A.device_dictionary(), False
     dtype = "float64"
     dev = None
     if config is not None:
