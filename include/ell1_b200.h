@@ -288,6 +288,19 @@ int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t B, const e
                     const ell1_dalm_opts_t* O, const ell1_batch_out_t* out, void* workspace,
                     size_t workspace_bytes, void* stream);
 
+/* Batched Homotopy (BASELINE config 5): the LASSO path to `target` for every
+ * column of Bmat (ld x B, device, zero padded) against the shared plain
+ * dictionary D (ext unsupported) — element j equals homotopy_solve on (A, b_j)
+ * (homotopy.py:128-261).  out->trace (optional): B x max_iter x 4.  lam_out
+ * (optional, B): the lambda reached; notes (optional, B): 1 when a
+ * ridge-regularised Gram was used.  Support capacity per instance:
+ * ell1_batch_homotopy_capacity (exceeding it -> ELL1_DEGENERATE). */
+int ell1_batch_homotopy_capacity(const ell1_dict_t* D);
+size_t ell1_batch_homotopy_workspace(const ell1_dict_t* D, int32_t B);
+int ell1_batch_homotopy(const ell1_dict_t* D, const double* Bmat, int32_t B, double target, int32_t max_iter,
+                        const ell1_batch_out_t* out, double* lam_out, int32_t* notes, void* ws,
+                        size_t ws_bytes, void* stream);
+
 /* SRC labels for a CAB batch (BASELINE config 3): label_j = argmin_c
  * ||b_j - e_j - A_c x_{j,c}||, classes = contiguous column ranges
  * [class_offsets[c], class_offsets[c+1]); W (ldw x B, ldw >= n + d) holds the

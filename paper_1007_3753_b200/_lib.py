@@ -153,6 +153,11 @@ _SIGS = {
     "ell1_batch_dalm": (ctypes.c_int, [P(Dict), ctypes.c_void_p, ctypes.c_int32, P(Ctrl),
                                        P(DalmOpts), P(BatchOut), ctypes.c_void_p, ctypes.c_size_t,
                                        ctypes.c_void_p]),
+    "ell1_batch_homotopy_capacity": (ctypes.c_int, [P(Dict)]),
+    "ell1_batch_homotopy_workspace": (ctypes.c_size_t, [P(Dict), ctypes.c_int32]),
+    "ell1_batch_homotopy": (ctypes.c_int, [P(Dict), ctypes.c_void_p, ctypes.c_int32, ctypes.c_double,
+                                           ctypes.c_int32, P(BatchOut), ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "ell1_src_classify": (ctypes.c_int, [P(Dict), ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
                                          ctypes.c_int64, ctypes.c_void_p, ctypes.c_int32,
                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),

@@ -30,6 +30,8 @@ class BatchResult:
     trace: np.ndarray = None  # B x rows x 4, or None
     kind: str = "fista"
     max_iter: int = 0
+    lam: np.ndarray = None     # homotopy: lambda reached per instance
+    notes: np.ndarray = None   # homotopy: ridge flag per instance
 
     def results(self):
         """Per-instance SolverResult records (reference record type)."""
@@ -38,7 +40,9 @@ class BatchResult:
         for j in range(B):
             st = int(self.status[j])
             raise_for(st, {_lib.BREAKDOWN: "backtracking exceeded 100 growth steps",
-                           _lib.ILL_CONDITIONED: "dual least-squares step failed its residual contract"})
+                           _lib.ILL_CONDITIONED: "dual least-squares step failed its residual contract",
+                           _lib.NOT_PD: "active-set Gram is singular",
+                           _lib.DEGENERATE: "active-set Gram is singular"})
             it = int(self.iterations[j])
             tr = []
             if self.trace is not None:
@@ -51,6 +55,8 @@ class BatchResult:
             notes = ()
             if self.kind == "dalm" and not self.converged[j] and it >= self.max_iter:
                 notes = ("iteration budget exhausted",)
+            if self.kind == "homotopy" and self.notes is not None and self.notes[j]:
+                notes = ("ridge-regularized gram",)
             out.append(SolverResult(self.x[:, j].copy(), it, self.wall_time_seconds / B,
                                     bool(self.converged[j]), tr, notes))
         return out
@@ -231,3 +237,39 @@ def fista_solve_batch(A, Bmat, config, with_trace=False):
     torch.cuda.synchronize(dev)
     return BatchResult(x.T.cpu().numpy(), its.cpu().numpy(), conv.cpu().numpy(), stat.cpu().numpy(),
                        time.perf_counter() - t0, tr.cpu().numpy() if tr is not None else None)
+
+
+def homotopy_solve_batch(A, Bmat, target_lambda, config, with_trace=False):
+    """LASSO path to target_lambda for every column of Bmat (d x B) against the
+    shared dictionary A (BASELINE config 5, batched Homotopy).  Element j
+    equals homotopy.homotopy_solve on (A, b_j) (homotopy.py:128-261): same
+    breakpoints, trace (one entry per breakpoint), notes and lambda reached
+    (``.lam``).  Plain dictionaries only (no [A, sI] extension)."""
+    torch = device._torch()
+    if target_lambda < 0:
+        raise ValueError("target lambda must be nonnegative")
+    t0 = time.perf_counter()
+    if hasattr(A, "device_extension"):
+        raise NotImplementedError("batched Homotopy runs on plain dictionaries")
+    D, view, N = _dict_view(A, config)
+    dev = D.device
+    Bpad, B = _upload_rhs(Bmat, D)
+    L = _lib.lib()
+    wsb = L.ell1_batch_homotopy_workspace(byref(view), B)
+    if wsb == 0:
+        raise ValueError("unsupported dictionary for batched Homotopy")
+    ws = device.alloc_bytes(wsb, dev)
+    rows = max(int(config.max_iter), 1)
+    out, bufs = _outputs(B, N, rows, dev, with_trace)
+    lam = torch.zeros(B, dtype=torch.float64, device=dev)
+    notes = torch.zeros(B, dtype=torch.int32, device=dev)
+    rc = L.ell1_batch_homotopy(byref(view), device.ptr(Bpad), B, float(target_lambda), int(config.max_iter),
+                               byref(out), device.ptr(lam), device.ptr(notes), device.ptr(ws),
+                               int(ws.numel()), device.stream_ptr(dev))
+    _lib.check(rc, "ell1_batch_homotopy")
+    res = _collect(bufs, t0, dev)
+    res.kind = "homotopy"
+    res.max_iter = config.max_iter
+    res.lam = lam.cpu().numpy()
+    res.notes = notes.cpu().numpy()
+    return res

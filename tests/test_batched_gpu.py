@@ -136,3 +136,73 @@ def test_src_labels_match_reference_rule(bt):
         assert labels[j] == want, j
         np.testing.assert_allclose(resid[j], wres, rtol=1e-5, atol=1e-8)
     assert np.mean(labels == truth) >= 0.8
+
+
+def _hom_check(res_j, ref, lam_j, lam_ref, rtol):
+    out = ref
+    assert res_j.iterations == out.iterations
+    assert res_j.converged == out.converged
+    assert rel_err(res_j.x_star, out.x) <= rtol
+    assert support(res_j.x_star) == support(out.x)
+    assert len(res_j.trace) == len(out.trace)
+    tr = np.array([tuple(t) for t in res_j.trace], dtype=np.float64).reshape(-1, 4)
+    tg = np.array(out.trace, dtype=np.float64).reshape(-1, 4)
+    np.testing.assert_array_equal(tr[:, 0], tg[:, 0])
+    np.testing.assert_array_equal(tr[:, 3], tg[:, 3])
+    np.testing.assert_allclose(tr[:, 1:3], tg[:, 1:3], rtol=max(rtol, 1e-9), atol=1e-12)
+    assert abs(lam_j - lam_ref) <= 1e-9 * max(lam_ref, 1e-30)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_batch_homotopy_equals_oracle(bt, dtype):
+    """config 5 shape: shared 512 x 2048, k in [16, 256], noisy right-hand sides."""
+    from paper_1007_3753_b200.model import SolverConfig
+    ks = [16, 64, 128, 256, 40, 1, 200, 90]
+    A, Bm, _ = _batch(512, 2048, ks, seed=6, noise=1e-3)
+    Ah = A if dtype == "float64" else A.astype(np.float32).astype(np.float64)
+    target = 1e-3
+    cfg = SolverConfig(max_iter=5000, options={"dtype": dtype})
+    res = bt.homotopy_solve_batch(A, Bm, target, cfg, with_trace=True)
+    per = res.results()
+    for j in range(len(ks)):
+        ref = oracle.homotopy(Ah, Bm[:, j], target)
+        _hom_check(per[j], ref[0], res.lam[j], ref[1], 1e-8)
+
+
+def test_batch_homotopy_equals_single_gpu(bt):
+    from paper_1007_3753_b200.homotopy import solve_path
+    from paper_1007_3753_b200.model import SolverConfig
+    A, Bm, _ = _batch(128, 400, [5, 20, 60, 100, 3], seed=9, noise=1e-2)
+    cfg = SolverConfig(max_iter=3000)
+    target = 0.05
+    res = bt.homotopy_solve_batch(A, Bm, target, cfg, with_trace=True)
+    per = res.results()
+    for j in range(Bm.shape[1]):
+        single, lam = solve_path(A, Bm[:, j], target, cfg)
+        assert per[j].iterations == single.iterations
+        assert rel_err(per[j].x_star, single.x_star) <= 1e-9
+        assert per[j].notes == single.notes
+        assert abs(res.lam[j] - lam) <= 1e-9 * lam
+
+
+def test_batch_homotopy_edge_cases(bt):
+    """zero right-hand side, target above lambda0, iteration budget, and a
+    square orthonormal dictionary (soft-threshold closed form)."""
+    from paper_1007_3753_b200.model import SolverConfig
+    rng = np.random.default_rng(3)
+    Q, _ = np.linalg.qr(rng.standard_normal((16, 16)))
+    b = rng.standard_normal(16)
+    Bm = np.stack([b, np.zeros(16), 0.01 * b, b], axis=1)
+    res = bt.homotopy_solve_batch(Q, Bm, 0.3, SolverConfig(max_iter=100), with_trace=True)
+    per = res.results()
+    np.testing.assert_allclose(per[0].x_star, oracle.soft(Q.T @ b, 0.3), atol=1e-10)
+    assert per[1].iterations == 0 and per[1].converged and len(per[1].trace) == 1
+    assert per[2].iterations == 0 and per[2].converged        # target above lambda0
+    for j in range(4):
+        ref = oracle.homotopy(Q, Bm[:, j], 0.3)
+        _hom_check(per[j], ref[0], res.lam[j], ref[1], 1e-9)
+    short = bt.homotopy_solve_batch(Q, Bm[:, :1], 0.0, SolverConfig(max_iter=3), with_trace=True)
+    r0 = short.results()[0]
+    assert r0.iterations == 3 and not r0.converged
+    ref = oracle.homotopy(Q, b, 0.0, max_iter=3)
+    _hom_check(r0, ref[0], short.lam[0], ref[1], 1e-9)
