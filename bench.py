@@ -352,12 +352,17 @@ def leg_cfg3(torch, dev, queries=1024):
             "note": "timed through the public call (host queries in, labels out)"}
 
 
-def leg_cfg5(torch, dev, B=1024):
-    """BASELINE config 5 point: B instances sharing one A (512 x 2048), k ~
-    U[16, 256], batched FISTA fp64 (relative-estimate 1e-6)."""
+def leg_cfg5(torch, dev, ws=1, B=1024, cpu_sample=8):
+    """BASELINE config 5 point: B instances sharing one A (512 x 2048, fp64),
+    k ~ U[16, 256], noiseless b = A x0; batched FISTA (lambda 1e-3,
+    relative-estimate 1e-6), batched dual ALM (relative-estimate 1e-6) and
+    batched Homotopy (target lambda 1e-3).  N > 1: instances dealt
+    round-robin across the ranks (A replicated, no per-iteration
+    communication), time = max over ranks (strong scaling, B fixed)."""
     from paper_1007_3753_b200 import synth
     from paper_1007_3753_b200 import device as dv
-    from paper_1007_3753_b200.batched import fista_solve_batch
+    from paper_1007_3753_b200.batched import dalm_solve_batch, fista_solve_batch, homotopy_solve_batch
+    from paper_1007_3753_b200.distributed import solve_batch_sharded
     from paper_1007_3753_b200.model import SolverConfig, StoppingRule
     d, n = 512, 2048
     A = synth.gen_gaussian_dict(d, n, 5)
@@ -368,22 +373,52 @@ def leg_cfg5(torch, dev, B=1024):
         X[rng.choice(n, kk, replace=False), j] = rng.standard_normal(kk)
     Bmat = A @ X
     D = dv.DeviceDictionary(A, dtype="float64", device=dev.index)
-    cfg = SolverConfig(lam=None, tol=1e-6, max_iter=5000,
-                       stopping=StoppingRule("relative-estimate", 1e-6))
-    fista_solve_batch(D, Bmat[:, :64], cfg)
-    torch.cuda.synchronize()
-    s, e = _events(torch)
-    s.record()
-    res = fista_solve_batch(D, Bmat, cfg)
-    e.record()
-    torch.cuda.synchronize()
-    t = s.elapsed_time(e) / 1e3
-    its = res.iterations.astype(np.int64)
-    return {"workload": "cfg5: B=%d instances, shared A 512 x 2048 fp64, k~U[16,256], batched "
-                        "FISTA, relative-estimate 1e-6" % B,
-            "solves_per_sec": B / t, "ms_per_batch": 1e3 * t, "iterations_per_sec": float(its.sum()) / t,
-            "mean_iterations": float(its.mean()), "converged": int(res.converged.sum()),
-            "note": "timed through the public call (host B in, host X out)"}
+    rel = StoppingRule("relative-estimate", 1e-6)
+    legs = {
+        "fista": (fista_solve_batch, SolverConfig(lam=1e-3, tol=1e-6, max_iter=5000, stopping=rel), {}),
+        "dalm": (dalm_solve_batch, SolverConfig(tol=1e-6, max_iter=5000, stopping=rel), {}),
+        "homotopy": (homotopy_solve_batch, SolverConfig(max_iter=5000), {"target_lambda": 1e-3}),
+    }
+    out = {"workload": "cfg5: B=%d instances, shared A 512 x 2048 fp64, k~U[16,256], noiseless" % B,
+           "n_gpus": ws, "scaling": "strong (B fixed, instances dealt across ranks)",
+           "note": "timed through the public call (host B in, host X out), max over ranks"}
+    for name, (fn, cfg, kw) in legs.items():
+        def run(Bm, fn=fn, cfg=cfg, kw=kw):
+            if "target_lambda" in kw:
+                return solve_batch_sharded(lambda A_, B_, c_: fn(A_, B_, kw["target_lambda"], c_), D, Bm, cfg)
+            return solve_batch_sharded(fn, D, Bm, cfg)
+        run(Bmat[:, : 16 * ws])                     # warm-up (Gram factor, cuBLAS handles)
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+        s, e = _events(torch)
+        s.record()
+        res = run(Bmat)
+        e.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([s.elapsed_time(e) / 1e3], dtype=torch.float64, device=dev)
+        if ws > 1:
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t = float(t.item())
+        its = res.iterations.astype(np.int64)
+        unit = "breakpoints_per_sec" if name == "homotopy" else "iterations_per_sec"
+        out[name] = {"solves_per_sec": B / t, "ms_per_batch": 1e3 * t, unit: float(its.sum()) / t,
+                     "mean_iterations": float(its.mean()), "converged": int(res.converged.sum())}
+    if ws == 1 and cpu_sample > 0:
+        # CPU reference port on a bounded sample of the same instances (all host cores)
+        import oracle
+        t0 = time.perf_counter()
+        for j in range(cpu_sample):
+            oracle.fista(A, Bmat[:, j], lam=1e-3, tol=1e-6, stop=("relative-estimate", 1e-6))
+        tf = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        for j in range(cpu_sample):
+            oracle.homotopy(A, Bmat[:, j], 1e-3)
+        th = time.perf_counter() - t0
+        out["cpu_baseline"] = {"fista_solves_per_sec": cpu_sample / tf,
+                               "homotopy_solves_per_sec": cpu_sample / th, "cores": os.cpu_count(),
+                               "kind": "port", "sample": "first %d instances, one at a time" % cpu_sample}
+    return out
 
 
 def leg_solvers_cfg2(torch, P, reps=3):
@@ -563,7 +598,7 @@ def run_b200(args):
             sec = {}
             for name, fn in (("solvers_cfg2", lambda: leg_solvers_cfg2(torch, P)),
                              ("cfg3", lambda: leg_cfg3(torch, dev)),
-                             ("cfg5", lambda: leg_cfg5(torch, dev))):
+                             ("cfg5", lambda: leg_cfg5(torch, dev, ws))):
                 try:
                     sec[name] = fn()
                 except Exception as exc:  # pragma: no cover - best effort leg

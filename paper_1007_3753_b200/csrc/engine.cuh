@@ -38,6 +38,14 @@ __device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned 
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// E.sh (and everything carved from it) lives in shared memory; telling the
+// compiler lets it emit LDS/STS instead of generic LD/ST, which it cannot
+// infer through the pointer stored in the shared Ctx.
+__device__ __forceinline__ double* shmem(double* p) {
+  __builtin_assume(__isShared(p));
+  return p;
+}
+
 __device__ __forceinline__ double2 ldcg2(const double* p) {
   return __ldcg(reinterpret_cast<const double2*>(p));
 }
@@ -215,7 +223,7 @@ __device__ __forceinline__ void block_reduce(const Ctx& E, double (&v)[K], unsig
     const double got = __shfl_xor_sync(0xffffffffu, p[0], o);
     p[0] = mxf ? nmax(p[0], got) : p[0] + got;
   }
-  double* sh = E.sh;
+  double* sh = shmem(E.sh);
   // lane l holds value `base` iff l's low (5 - LOGP) bits are zero
   if ((l & ((32 >> LOGP) - 1)) == 0 && base < K) sh[wpx() * K + base] = p[0];
   __syncthreads();
@@ -312,7 +320,7 @@ template <int K>
 __device__ __forceinline__ void gather(const Ctx& E, double (&out)[K], unsigned maxmask) {
   static_assert(K <= 16, "up to 16 scalars");
   constexpr int KP = kpad(K);
-  double* red = E.sh;                         // [NWARP][32]; results at red[16 + k]
+  double* red = shmem(E.sh);                  // [NWARP][32]; results at red[16 + k]
   const double* src = E.scal + (size_t)(E.nbar & 1u) * E.nb * SCAL;
   region_partial(src, E.nb, KP, maxmask, wpx(), NWARP, red + wpx() * 32);
   __syncthreads();
@@ -350,7 +358,7 @@ __device__ void gather_slice(const Ctx& E, double* out, unsigned maxmask, int64_
                              const double* const (&auxv)[NA > 0 ? NA : 1], F&& f) {
   static_assert(K <= 16, "up to 16 scalars");
   constexpr int KP = kpad(K);
-  double* red = E.sh;
+  double* red = shmem(E.sh);
   const int rows = (int)(E.r1 - E.r0);
   const int RP = E.rp;
   const int nb = E.nb;
@@ -693,7 +701,7 @@ __device__ void panel_gemv_t_pre(const Ctx& E, const DictV<TA>& D, const Panel<T
   constexpr int VW = VecOf<TA>::VW;
   const int64_t nvec = D.ld / VW;
   const int w = P.w, rc = P.rc;
-  double* red = E.sh;                               // [NWARP][CW] per v pass
+  double* red = shmem(E.sh);                        // [NWARP][CW] per v pass
   __syncthreads();
   if (nvec <= NTHR) {
     const int64_t q = tix();
@@ -762,7 +770,7 @@ __device__ void panel_gemv_t_pre(const Ctx& E, const DictV<TA>& D, const Panel<T
     if (rch > 1024) rch = 1024;
     rch = rch / 32 * 32;
     if (rch < 32) rch = 32;
-    double* rsm = E.sh;
+    double* rsm = shmem(E.sh);
     for (int jg = 0; jg < w; jg += NWARP * CPW) {
       double acc[CPW][NV];
 #pragma unroll
@@ -787,9 +795,13 @@ __device__ void panel_gemv_t_pre(const Ctx& E, const DictV<TA>& D, const Panel<T
               else ld16_g<TA>(col + q * VW, a);
 #pragma unroll
               for (int v = 0; v < NV; ++v) {
-                const double* rv = rsm + v * rch * VW + q * VW;
+                const double2* rv = reinterpret_cast<const double2*>(rsm + v * rch * VW + q * VW);
 #pragma unroll
-                for (int e = 0; e < VW; ++e) acc[c][v] = fma((double)a[e], rv[e], acc[c][v]);
+                for (int e2 = 0; e2 < VW / 2; ++e2) {
+                  const double2 t = rv[e2];
+                  acc[c][v] = fma((double)a[2 * e2], t.x, acc[c][v]);
+                  acc[c][v] = fma((double)a[2 * e2 + 1], t.y, acc[c][v]);
+                }
               }
             }
           }
