@@ -188,6 +188,36 @@ __device__ __forceinline__ bool grid_sync(Ctx& E) {
   return E.ok != 0;
 }
 
+// Split-phase form of grid_sync: arrive publishes this CTA's writes and
+// counts it in; work placed between arrive and wait (by any thread) must not
+// read data other CTAs write before the barrier — it overlaps the barrier's
+// latency (thread-0 scalar bookkeeping, mostly).  No publish/gather between
+// the two (the scalar double-buffer flips at arrive).
+__device__ __forceinline__ void grid_arrive(Ctx& E) {
+  __syncthreads();
+  if (tix() == 0) {
+    E.epoch += (unsigned long long)E.nb;
+    E.nbar++;
+    red_release_add(E.bar, 1ULL);
+  }
+}
+__device__ __forceinline__ bool grid_wait(Ctx& E) {
+  if (tix() == 0) {
+    long long spins = 0;
+    int ok = 1;
+    const unsigned long long target = E.epoch;
+    while (ld_acquire(E.bar) < target) {
+      if (((++spins) & 1023) == 0) {
+        if (*(volatile int*)E.abort) { ok = 0; break; }
+        if (spins > SPIN_LIMIT) { atomicExch(E.abort, 1); ok = 0; break; }
+      }
+    }
+    E.ok = ok;
+  }
+  __syncthreads();
+  return E.ok != 0;
+}
+
 // ------------------------------------------------------------------ block reductions
 // K values reduced across the CTA in a fixed order; every thread gets the result.
 // Warp stage: a transpose-reduction over P = pow2 >= K slots costs

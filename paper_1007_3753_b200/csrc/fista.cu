@@ -49,11 +49,11 @@ struct FistaV {
   double L, tp, tc, lam, lam_bar, Fprev, fy, lam_used, passes;
   double m, tn, mn, thr;
   double f_F, f_rr, f_lam, f_s4, f_s5, f_s6;
-  double kb[5];
+  double cut;
   double S[12];
   double Q2[2];
   double rr, Fn;
-  int it, hist, steps, pend, f_it, conv, status, stop_prev, accept, bt, quit, phase;
+  int it, hist, steps, pend, f_it, conv, status, stop_prev, accept, bt, quit, phase, fin;
   int ix, ixp, ixn, igx, igxp, irx, irxp, irn;
 };
 
@@ -228,189 +228,198 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(const __grid_constant__ 
     const bool relest = C.stop_kind == ELL1_STOP_REL_ESTIMATE;
     const bool gtr = C.stop_kind == ELL1_STOP_GROUND_TRUTH;
     const bool tw = E.b == 0;                             // CTA 0 writes the trace
-    while (true) {
-      T0 V.quit = (V.it >= C.max_iter || (a.max_steps > 0 && V.steps >= a.max_steps));
-      __syncthreads();
-      if (V.quit) {
-        if (V.pend) {                                     // flush the pending KKT reduction
-          publish<5>(E, V.kb);
-          if (!grid_sync(E)) { T0 V.status = ELL1_ERR_TIMEOUT; goto out; }
-          double K[5];
-          gather<5>(E, K, 0xFu);
-          T0 {
-            if (fista_finalize(V, C, a.trace, tw, K)) V.conv = 1;
-            V.pend = 0;
-          }
-          __syncthreads();
-        }
-        break;
-      }
-      mark(E, -1);
-      T0 {
-        V.it++; V.steps++; V.bt = 0; V.stop_prev = 0; V.accept = 0;
+    // Per-thread partials carried into the next reduction: [0..6] the prox /
+    // backtracking sums of the current trial, [7..11] the KKT / support
+    // partials of the previous accepted iterate (shrinkage.py:289-293, computed
+    // right after its A^T r and reduced together with the next trial's sums).
+    double s12[12];
+    GtPre<TA, 1> gpre;
+    // thread 0: start an iteration (shrinkage.py:269-270 momentum, t sequence)
+    auto begin_iter = [&]() {
+      V.quit = (V.it >= C.max_iter || (a.max_steps > 0 && V.steps >= a.max_steps));
+      if (!V.quit) {
+        V.it++; V.steps++; V.bt = 0; V.stop_prev = 0;   // (accept is set by every decision)
         V.m = (V.tp - 1.0) / V.tc;
         V.tn = fista_t_next(V.tc);
         V.mn = (V.tc - 1.0) / V.tn;                       // momentum of the next iteration
+        V.thr = V.lam / V.L;
       }
-      __syncthreads();
-      {
-        const double m = V.m;
-        const double* x = Xp(V.ix);
-        const double* xp = Xp(V.ixp);
-        const double* gx = Gp(V.igx);
-        const double* gxp = Gp(V.igxp);
-        for_owned(E, [&](int k) {
+    };
+    // prox trial over the owned columns (shrinkage.py:204-208), optionally
+    // forming y and g_y first (linear combinations of cached products)
+    auto prox = [&](bool form_y) {
+      const double L = V.L, thr = V.thr, m = V.m;
+      const double* x = Xp(V.ix);
+      const double* xp = Xp(V.ixp);
+      const double* gx = Gp(V.igx);
+      const double* gxp = Gp(V.igxp);
+      double* xn = Xp(V.ixn);
+      for_owned(E, [&](int k) {
+        double yj, gj;
+        if (form_y) {
           const double xj = x[k];
-          Y[k] = xj + m * (xj - xp[k]);                   // shrinkage.py:270
-          GY[k] = (1.0 + m) * gx[k] - m * gxp[k];         // = A^T(A y - b)
-        });
-      }
+          yj = xj + m * (xj - xp[k]);                       // shrinkage.py:270
+          gj = (1.0 + m) * gx[k] - m * gxp[k];              // = A^T(A y - b)
+          Y[k] = yj; GY[k] = gj;
+        } else {
+          yj = Y[k]; gj = GY[k];
+        }
+        const double u = soft1(yj - gj / L, thr);           // shrinkage.py:204
+        xn[k] = u;
+        const double dl = u - yj;
+        s12[0] += fabs(u);
+        s12[1] += gj * dl;
+        s12[2] += dl * dl;
+        s12[3] = nmax(s12[3], fabs(u));
+        if (relest) { const double xo = x[k]; const double dd = u - xo; s12[4] += dd * dd; s12[5] += xo * xo; }
+        if (gtr) { const double e = u - C.ground_truth[gcol(E, D.n, k)]; s12[6] += e * e; }
+      });
+    };
+    auto zero12 = [&]() {
+#pragma unroll
+      for (int k = 0; k < 12; ++k) s12[k] = 0.0;
+    };
+    T0 begin_iter();
+    __syncthreads();
+    zero12();
+    if (!V.quit) prox(true);
+    while (!V.quit) {
+      mark(E, -1);
+      block_reduce<12>(E, s12, (1u << 3) | (0xFu << 7));
+      publish<12>(E, s12);
       mark(E, 0);
-      GtPre<TA, 1> gpre;
-      while (true) {                                      // backtracking (shrinkage.py:199-213)
-        T0 {
-          if (V.bt > 100) { V.status = ELL1_BREAKDOWN; V.quit = 1; }   // shrinkage.py:203,213
-          V.thr = V.lam / V.L;
-        }
-        __syncthreads();
-        if (V.quit) goto out;
-        {
-          const double L = V.L, thr = V.thr;
-          const double* x = Xp(V.ix);
-          double* xn = Xp(V.ixn);
-          double s7[7] = {0, 0, 0, 0, 0, 0, 0};
-          for_owned(E, [&](int k) {
-            const double yj = Y[k], gj = GY[k];
-            const double u = soft1(yj - gj / L, thr);     // shrinkage.py:204
-            xn[k] = u;
-            const double dl = u - yj;
-            s7[0] += fabs(u);
-            s7[1] += gj * dl;
-            s7[2] += dl * dl;
-            s7[3] = nmax(s7[3], fabs(u));
-            if (relest) { const double xo = x[k]; const double dd = u - xo; s7[4] += dd * dd; s7[5] += xo * xo; }
-            if (gtr) { const double e = u - C.ground_truth[gcol(E, D.n, k)]; s7[6] += e * e; }
-          });
-          mark(E, 9);
-          block_reduce<7>(E, s7, 1u << 3);
-          const bool carry = V.pend && V.bt == 0;         // KKT partials of iteration it-1 ride along
-          double s[12];
-          for (int k = 0; k < 7; ++k) s[k] = s7[k];
-          for (int k = 0; k < 5; ++k) s[7 + k] = carry ? V.kb[k] : 0.0;
-          publish<12>(E, s);
-          mark(E, 1);
-          const double* xs[1] = {xn};
-          panel_gemv<TA, 1>(E, D, PN, xs);
-          mark(E, 2);
-        }
-        if (!grid_sync(E)) { T0 V.status = ELL1_ERR_TIMEOUT; goto out; }
-        mark(E, 3);
-        {
-          double Sg[12];
-          double q[2] = {0.0, 0.0};
-          const double mn = V.mn;
-          const double* xn = Xp(V.ixn);
-          double* rnv = a.R[V.irn];
-          const double* aux[2] = {b, a.R[V.irx]};
-          gather_slice<12, 1, 2>(E, Sg, (1u << 3) | (0xFu << 7), D.ld, aux,
-                                 [&](int64_t i, const double* sums, const double* au) {
-            double ax = sums[0];
-            if (D.ext) ax = ax + s_ext * xn[E.w + (int)(i - E.r0)];   // robust.py:93
-            const double r = ax - au[0];                  // shrinkage.py:205
-            rnv[i] = r;
-            q[0] += r * r;
-            const double ry = (1.0 + mn) * r - mn * au[1];
-            q[1] += ry * ry;
-          });
-          mark(E, 10);
-          T0 {
-            V.passes += 1;
-            for (int k = 0; k < 12; ++k) V.S[k] = Sg[k];
-            if (V.pend && V.bt == 0) {
-              V.pend = 0;
-              if (fista_finalize(V, C, a.trace, tw, Sg + 7)) V.stop_prev = 1;
-            }
-          }
-          __syncthreads();
-          if (V.stop_prev) break;
-          block_reduce<2>(E, q, 0u);
-          publish<2>(E, q);
-          mark(E, 4);
-        }
-        if (!grid_sync(E)) { T0 V.status = ELL1_ERR_TIMEOUT; goto out; }
-        mark(E, 5);
-        {
-          // r_next is complete: start loading the GEMV^T operands now so their
-          // L2 latency overlaps the decision round trip (used only on accept)
-          {
-            const double* rs[1] = {a.R[V.irn]};
-            gemv_t_prefetch<TA, 1>(D, PN, rs, gpre);
-          }
-          double Q2[2];
-          gather<2>(E, Q2, 0u);
-          T0 {
-            V.Q2[0] = Q2[0]; V.Q2[1] = Q2[1];
-            V.rr = Q2[0];
-            V.Fn = 0.5 * V.rr + V.lam * V.S[0];
-            if (O.exact_L) {
-              V.accept = 1;                                 // shrinkage.py:534-538
-            } else {
-              const double Qm = V.fy + V.S[1] + 0.5 * V.L * V.S[2] + V.lam * V.S[0];
-              V.accept = V.Fn <= Qm + 1e-12 * pymax(1.0, fabs(Qm));   // shrinkage.py:210
-              if (!V.accept) { V.L *= O.eta; V.bt++; }
-            }
-          }
-          __syncthreads();
-          if (V.accept) break;
-        }
+      {
+        const double* xs[1] = {Xp(V.ixn)};
+        panel_gemv<TA, 1>(E, D, PN, xs);
       }
+      mark(E, 1);
+      if (!grid_sync(E)) { T0 V.status = ELL1_ERR_TIMEOUT; goto out; }
+      mark(E, 2);
+      {
+        double Sg[12];
+        double q[2] = {0.0, 0.0};
+        const double mn = V.mn;
+        const double* xn = Xp(V.ixn);
+        double* rnv = a.R[V.irn];
+        const double* aux[2] = {b, a.R[V.irx]};
+        gather_slice<12, 1, 2>(E, Sg, (1u << 3) | (0xFu << 7), D.ld, aux,
+                               [&](int64_t i, const double* sums, const double* au) {
+          double ax = sums[0];
+          if (D.ext) ax = ax + s_ext * xn[E.w + (int)(i - E.r0)];   // robust.py:93
+          const double r = ax - au[0];                  // shrinkage.py:205
+          rnv[i] = r;
+          q[0] += r * r;
+          const double ry = (1.0 + mn) * r - mn * au[1];
+          q[1] += ry * ry;
+        });
+        mark(E, 3);
+        T0 {
+          V.passes += 1;
+          for (int k = 0; k < 12; ++k) V.S[k] = Sg[k];
+          V.fin = V.pend && V.bt == 0;                  // iteration it-1 is finalised now
+          if (V.fin) V.pend = 0;
+        }
+        block_reduce<2>(E, q, 0u);
+        publish<2>(E, q);
+      }
+      mark(E, 4);
+      grid_arrive(E);
+      // trace row / convergence / stop rule of iteration it-1, hidden behind the barrier
+      T0 { if (V.fin && fista_finalize(V, C, a.trace, tw, V.S + 7)) V.stop_prev = 1; }
+      if (!grid_wait(E)) { T0 V.status = ELL1_ERR_TIMEOUT; goto out; }
+      mark(E, 5);
       if (V.stop_prev) {                                  // iteration it-1 was the answer
         T0 { V.it--; V.conv = 1; }
         __syncthreads();
         break;
       }
-      T0 {                                                // accept (shrinkage.py:283-284)
-        int t = V.ixp; V.ixp = V.ix; V.ix = V.ixn; V.ixn = t;
-        t = V.irxp; V.irxp = V.irx; V.irx = V.irn; V.irn = t;
-        t = V.igxp; V.igxp = V.igx; V.igx = t;
-        V.tp = V.tc; V.tc = V.tn;
-        V.lam_used = V.lam;
-        V.passes += 1;
+      {
+        // r_next is complete: start the GEMV^T operand loads now so their L2
+        // latency overlaps the decision round trip (used only on accept)
+        {
+          const double* rs[1] = {a.R[V.irn]};
+          gemv_t_prefetch<TA, 1>(D, PN, rs, gpre);
+        }
+        double Q2[2];
+        gather<2>(E, Q2, 0u);
+        T0 {
+          V.rr = Q2[0];
+          V.Fn = 0.5 * V.rr + V.lam * V.S[0];
+          if (O.exact_L) {
+            V.accept = 1;                                   // shrinkage.py:534-538
+          } else {
+            const double Qm = V.fy + V.S[1] + 0.5 * V.L * V.S[2] + V.lam * V.S[0];
+            V.accept = V.Fn <= Qm + 1e-12 * pymax(1.0, fabs(Qm));   // shrinkage.py:210
+          }
+          if (V.accept) {                                   // shrinkage.py:283-284, 297
+            int t = V.ixp; V.ixp = V.ix; V.ix = V.ixn; V.ixn = t;
+            t = V.irxp; V.irxp = V.irx; V.irx = V.irn; V.irn = t;
+            t = V.igxp; V.igxp = V.igx; V.igx = t;
+            V.tp = V.tc; V.tc = V.tn;
+            V.lam_used = V.lam;
+            V.passes += 1;
+            V.pend = 1;
+            V.f_it = V.it; V.f_F = V.Fn; V.f_rr = V.rr; V.f_lam = V.lam;
+            V.f_s4 = V.S[4]; V.f_s5 = V.S[5]; V.f_s6 = V.S[6];
+            V.cut = 1e-10 * pymax(V.S[3], 1.0);             // model.py:232
+            V.lam = pymax(O.beta * V.lam, V.lam_bar);       // speculative continuation
+            V.fy = 0.5 * Q2[1];
+            begin_iter();
+          } else {
+            V.L *= O.eta;
+            V.bt++;
+            if (V.bt > 100) { V.status = ELL1_BREAKDOWN; V.quit = 1; }   // shrinkage.py:203,213
+            V.thr = V.lam / V.L;
+          }
+        }
+        __syncthreads();
       }
-      __syncthreads();
       mark(E, 6);
+      if (!V.accept) {
+        if (V.quit) goto out;
+        zero12();
+        prox(false);
+        mark(E, 9);
+        continue;
+      }
       {
         const double* rs[1] = {a.R[V.irx]};
         double* os[1] = {Gp(V.igx)};
         panel_gemv_t_pre<TA, 1>(E, D, PN, gpre, rs, os);   // g_x = A^T r_next  (shrinkage.py:285)
       }
       mark(E, 7);
+      zero12();
       {
-        double k5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};        // max_on, max_off, any_on, any_off, support
-        const double cut = 1e-10 * pymax(V.S[3], 1.0);   // model.py:232
+        // KKT / support partials of the accepted iterate (model.py:160-173, 227-233)
+        const double cut = V.cut;
+        const double lamk = V.lam_used;
         const double* xc = Xp(V.ix);
         double* gc = Gp(V.igx);
         const double* rnow = a.R[V.irx];
-        const double lamk = V.lam;
         for_owned(E, [&](int k) {
           if (k >= E.w) gc[k] = s_ext * rnow[E.r0 + (k - E.w)];
           const double xj = xc[k];
           const double c = -gc[k];
-          if (xj != 0.0) { k5[0] = nmax(k5[0], fabs(c - lamk * sgn(xj))); k5[2] = 1.0; }
-          else { k5[1] = nmax(k5[1], fabs(c)); k5[3] = 1.0; }
-          if (fabs(xj) > cut) k5[4] += 1.0;
+          if (xj != 0.0) { s12[7] = nmax(s12[7], fabs(c - lamk * sgn(xj))); s12[9] = 1.0; }
+          else { s12[8] = nmax(s12[8], fabs(c)); s12[10] = 1.0; }
+          if (fabs(xj) > cut) s12[11] += 1.0;
         });
+      }
+      if (V.quit) {                                       // budget reached: flush the pending KKT
+        double k5[5] = {s12[7], s12[8], s12[9], s12[10], s12[11]};
         block_reduce<5>(E, k5, 0xFu);
+        publish<5>(E, k5);
+        if (!grid_sync(E)) { T0 V.status = ELL1_ERR_TIMEOUT; goto out; }
+        double K[5];
+        gather<5>(E, K, 0xFu);
         T0 {
-          for (int k = 0; k < 5; ++k) V.kb[k] = k5[k];
-          V.pend = 1;
-          V.f_it = V.it; V.f_F = V.Fn; V.f_rr = V.rr; V.f_lam = V.lam;
-          V.f_s4 = V.S[4]; V.f_s5 = V.S[5]; V.f_s6 = V.S[6];
-          V.lam = pymax(O.beta * V.lam, V.lam_bar);      // shrinkage.py:297 (speculative)
-          V.fy = 0.5 * V.Q2[1];
+          if (fista_finalize(V, C, a.trace, tw, K)) V.conv = 1;
+          V.pend = 0;
         }
         __syncthreads();
+        break;
       }
+      prox(true);                                         // next iteration's first trial (same thread per k)
       mark(E, 8);
     }
     T0 if (!V.conv && V.it < C.max_iter && a.max_steps > 0) V.status = ELL1_RUNNING;

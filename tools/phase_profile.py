@@ -11,8 +11,8 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-NAMES = ["y/gy", "reduce7+pub", "gemv", "barrierA", "fin+q+pub", "barrierB", "decide",
-         "gemv_t", "kktpart", "prox loop", "gath+slice"]
+NAMES = ["reduce12+pub", "gemv", "barrierA", "gath+slice", "q+pub", "barrierB+fin", "decide",
+         "gemv_t", "kkt+y+prox", "retry prox", "-"]
 
 
 def main():
