@@ -47,7 +47,7 @@ constexpr int FISTA_OV = 7;      // owned vectors: x ring (3), g ring (2), y, g_
 // would miss in L1 after every grid barrier.
 struct FistaV {
   double L, tp, tc, lam, lam_bar, Fprev, fy, lam_used, passes;
-  double m, tn, mn, thr;
+  double m, tn, mn, thr, tn2, mn2, lam2, thr2;
   double f_F, f_rr, f_lam, f_s4, f_s5, f_s6;
   double cut;
   double S[12];
@@ -324,8 +324,19 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(const __grid_constant__ 
       }
       mark(E, 4);
       grid_arrive(E);
-      // trace row / convergence / stop rule of iteration it-1, hidden behind the barrier
-      T0 { if (V.fin && fista_finalize(V, C, a.trace, tw, V.S + 7)) V.stop_prev = 1; }
+      // hidden behind the barrier (three threads in parallel): the trace row /
+      // convergence / stop rule of iteration it-1, and the scalars iteration
+      // it+1 starts with should this trial be accepted (t sequence, momenta,
+      // continuation, threshold) — identical expressions, computed early
+      if (tix() == 0) {
+        if (V.fin && fista_finalize(V, C, a.trace, tw, V.S + 7)) V.stop_prev = 1;
+      } else if (tix() == 32) {
+        V.tn2 = fista_t_next(V.tn);
+        V.mn2 = (V.tn - 1.0) / V.tn2;
+      } else if (tix() == 64) {
+        V.lam2 = pymax(O.beta * V.lam, V.lam_bar);        // shrinkage.py:297
+        V.thr2 = V.lam2 / V.L;
+      }
       if (!grid_wait(E)) { T0 V.status = ELL1_ERR_TIMEOUT; goto out; }
       mark(E, 5);
       if (V.stop_prev) {                                  // iteration it-1 was the answer
@@ -362,9 +373,17 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(const __grid_constant__ 
             V.f_it = V.it; V.f_F = V.Fn; V.f_rr = V.rr; V.f_lam = V.lam;
             V.f_s4 = V.S[4]; V.f_s5 = V.S[5]; V.f_s6 = V.S[6];
             V.cut = 1e-10 * pymax(V.S[3], 1.0);             // model.py:232
-            V.lam = pymax(O.beta * V.lam, V.lam_bar);       // speculative continuation
+            V.lam = V.lam2;                                 // speculative continuation
             V.fy = 0.5 * Q2[1];
-            begin_iter();
+            // begin iteration it+1 with the scalars prepared behind the barrier
+            V.quit = (V.it >= C.max_iter || (a.max_steps > 0 && V.steps >= a.max_steps));
+            if (!V.quit) {
+              V.it++; V.steps++; V.bt = 0; V.stop_prev = 0;
+              V.m = V.mn;                                   // (t_prev - 1) / t with t_prev, t rotated
+              V.tn = V.tn2;
+              V.mn = V.mn2;
+              V.thr = V.thr2;
+            }
           } else {
             V.L *= O.eta;
             V.bt++;

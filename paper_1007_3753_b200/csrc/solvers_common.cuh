@@ -167,12 +167,14 @@ inline int max_smem_optin() {
   return v - 128;      // static __shared__ (grid_sync flag) + slack
 }
 
-inline SmemPlan plan_smem(const DictRaw& D, int nb, int nov, int kmax, bool allow_resident) {
+inline SmemPlan plan_smem(const DictRaw& D, int nb, int nov, int kmax, bool allow_resident,
+                          int64_t min_scratch = 0) {
   SmemPlan p;
   const int64_t wcols = (D.n + nb - 1) / nb;
   const int64_t wrows = D.ext ? (D.d + nb - 1) / nb : 0;
   p.wmax = (int)align_up(wcols + wrows, 2);
   p.scratch = engine_scratch_doubles(kmax);
+  if (p.scratch < min_scratch) p.scratch = align_up(min_scratch, 32);
   const int64_t esz = D.dtype == ELL1_F64 ? 8 : 4;
   // long columns (GEMV^T row chunks of r staged in shared memory, NV <= 2)
   const int64_t vw = 16 / esz;

@@ -12,7 +12,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 NAMES = ["reduce12+pub", "gemv", "barrierA", "gath+slice", "q+pub", "barrierB+fin", "decide",
-         "gemv_t", "kkt+y+prox", "retry prox", "-"]
+         "issue+gemv_t", "kkt+y+prox", "retry prox", "-"]
 
 
 def main():
