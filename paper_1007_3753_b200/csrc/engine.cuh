@@ -274,6 +274,58 @@ __device__ __forceinline__ void block_reduce(const Ctx& E, double (&v)[K], unsig
   __syncthreads();
 }
 
+// block_reduce whose results land in warp 0 only (thread 0 publishes them):
+// one __syncthreads instead of three.  The caller must __syncthreads before
+// E.sh is written again (panel_gemv / panel_gemv_t start with one).
+template <int K>
+__device__ __forceinline__ void block_reduce_w0(const Ctx& E, double (&v)[K], unsigned maxmask) {
+  constexpr int P = K <= 1 ? 1 : K <= 2 ? 2 : K <= 4 ? 4 : K <= 8 ? 8 : 16;
+  constexpr int LOGP = P == 1 ? 0 : P == 2 ? 1 : P == 4 ? 2 : P == 8 ? 3 : 4;
+  static_assert(K <= 16, "block_reduce supports up to 16 values");
+  double p[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) p[k] = k < K ? v[k] : (((maxmask >> k) & 1u) ? -INFINITY : 0.0);
+  const int l = lnx();
+  int base = 0;
+#pragma unroll
+  for (int r = 0; r < LOGP; ++r) {
+    const int o = 16 >> r;
+    const int h = P >> (r + 1);
+    const bool upper = (l & o) != 0;
+    if (upper) base += h;
+#pragma unroll
+    for (int u = 0; u < h; ++u) {
+      const double send = upper ? p[u] : p[u + h];
+      const double keep = upper ? p[u + h] : p[u];
+      const double got = __shfl_xor_sync(0xffffffffu, send, o);
+      p[u] = ((maxmask >> (base + u)) & 1u) ? nmax(keep, got) : keep + got;
+    }
+  }
+  const bool mxf = (maxmask >> base) & 1u;
+#pragma unroll
+  for (int o = 16 >> LOGP; o > 0; o >>= 1) {
+    const double got = __shfl_xor_sync(0xffffffffu, p[0], o);
+    p[0] = mxf ? nmax(p[0], got) : p[0] + got;
+  }
+  double* sh = shmem(E.sh);
+  if ((l & ((32 >> LOGP) - 1)) == 0 && base < K) sh[wpx() * K + base] = p[0];
+  __syncthreads();
+  if (wpx() == 0) {
+    double s = 0.0;
+    if (l < K) {
+      const bool mx = (maxmask >> l) & 1u;
+      double t[NWARP];
+#pragma unroll
+      for (int w = 0; w < NWARP; ++w) t[w] = sh[w * K + l];
+      s = t[0];
+#pragma unroll
+      for (int w = 1; w < NWARP; ++w) s = mx ? nmax(s, t[w]) : s + t[w];
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = __shfl_sync(0xffffffffu, s, k);
+  }
+}
+
 // Publish this CTA's K partial scalars into the buffer the next barrier
 // selects: scal[buf][b * kpad(K) + k] (pad slots zero).
 template <int K>
@@ -383,7 +435,9 @@ __device__ __forceinline__ bool allreduce(Ctx& E, double (&v)[K], unsigned maxma
 // Small slices (rp <= 32): the scalar region and the NV partial regions are
 // reduced concurrently by disjoint warp groups (one L2 round trip).  Large
 // slices: one warp per 64-row chunk walks the nb partials with 16-byte loads.
-template <int K, int NV, int NA, class F>
+// SHOUT: `out` is a shared-memory array written by the folding threads and
+// valid for every thread on return (saves the broadcast round).
+template <int K, int NV, int NA, bool SHOUT = false, class F>
 __device__ void gather_slice(const Ctx& E, double* out, unsigned maxmask, int64_t /*ld*/,
                              const double* const (&auxv)[NA > 0 ? NA : 1], F&& f) {
   static_assert(K <= 16, "up to 16 scalars");
@@ -428,16 +482,28 @@ __device__ void gather_slice(const Ctx& E, double* out, unsigned maxmask, int64_
       double sk = 0.0;
       if (k >= 0 && k < K) sk = region_fold(red, 0, n0, k, (maxmask >> k) & 1u);
       // red[16 + k] lies in warp 0's row, upper half: no fold reads it
-      if (k >= 0 && k < K) red[16 + k] = sk;
+      if (k >= 0 && k < K) {
+        if (SHOUT) out[k] = sk;
+        else red[16 + k] = sk;
+      }
       __syncthreads();
-      for (int q = 0; q < K; ++q) out[q] = red[16 + q];
+      if (!SHOUT) {
+        for (int q = 0; q < K; ++q) out[q] = red[16 + q];
+        __syncthreads();
+      }
+    } else {
+      __syncthreads();
     }
-    __syncthreads();
   } else {
     if (K > 0) {
       double tmp[K > 0 ? K : 1];
       gather<(K > 0 ? K : 1)>(E, *reinterpret_cast<double(*)[K > 0 ? K : 1]>(tmp), maxmask);
-      for (int q = 0; q < K; ++q) out[q] = tmp[q];
+      if (SHOUT) {
+        if (tix() == 0)
+          for (int q = 0; q < K; ++q) out[q] = tmp[q];
+      } else {
+        for (int q = 0; q < K; ++q) out[q] = tmp[q];
+      }
     }
     for (int h = wpx(); h * 64 < rows; h += NWARP) {
       const int j = h * 64 + 2 * lnx();

@@ -77,7 +77,10 @@ __device__ bool fista_finalize(FistaV& V, const ell1_ctrl_t& C, double* trace, b
 
 #define T0 if (threadIdx.x == 0)
 
-template <class TA>
+// PROF: phase timers (tools/phase_profile.py); the production variant has none.
+#define MARK(k) do { if constexpr (PROF) mark(E, k); } while (0)
+
+template <class TA, bool PROF>
 __global__ void __launch_bounds__(NTHR, 1) fista_kernel(const __grid_constant__ FistaArgs a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ Ctx E;
@@ -284,25 +287,24 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(const __grid_constant__ 
     zero12();
     if (!V.quit) prox(true);
     while (!V.quit) {
-      mark(E, -1);
-      block_reduce<12>(E, s12, (1u << 3) | (0xFu << 7));
+      MARK(-1);
+      block_reduce_w0<12>(E, s12, (1u << 3) | (0xFu << 7));   // panel_gemv syncs before E.sh reuse
       publish<12>(E, s12);
-      mark(E, 0);
+      MARK(0);
       {
         const double* xs[1] = {Xp(V.ixn)};
         panel_gemv<TA, 1>(E, D, PN, xs);
       }
-      mark(E, 1);
+      MARK(1);
       if (!grid_sync(E)) { T0 V.status = ELL1_ERR_TIMEOUT; goto out; }
-      mark(E, 2);
+      MARK(2);
       {
-        double Sg[12];
         double q[2] = {0.0, 0.0};
         const double mn = V.mn;
         const double* xn = Xp(V.ixn);
         double* rnv = a.R[V.irn];
         const double* aux[2] = {b, a.R[V.irx]};
-        gather_slice<12, 1, 2>(E, Sg, (1u << 3) | (0xFu << 7), D.ld, aux,
+        gather_slice<12, 1, 2, true>(E, V.S, (1u << 3) | (0xFu << 7), D.ld, aux,
                                [&](int64_t i, const double* sums, const double* au) {
           double ax = sums[0];
           if (D.ext) ax = ax + s_ext * xn[E.w + (int)(i - E.r0)];   // robust.py:93
@@ -312,17 +314,16 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(const __grid_constant__ 
           const double ry = (1.0 + mn) * r - mn * au[1];
           q[1] += ry * ry;
         });
-        mark(E, 3);
+        MARK(3);
         T0 {
           V.passes += 1;
-          for (int k = 0; k < 12; ++k) V.S[k] = Sg[k];
           V.fin = V.pend && V.bt == 0;                  // iteration it-1 is finalised now
           if (V.fin) V.pend = 0;
         }
         block_reduce<2>(E, q, 0u);
         publish<2>(E, q);
       }
-      mark(E, 4);
+      MARK(4);
       grid_arrive(E);
       // hidden behind the barrier (three threads in parallel): the trace row /
       // convergence / stop rule of iteration it-1, and the scalars iteration
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(const __grid_constant__ 
         V.thr2 = V.lam2 / V.L;
       }
       if (!grid_wait(E)) { T0 V.status = ELL1_ERR_TIMEOUT; goto out; }
-      mark(E, 5);
+      MARK(5);
       if (V.stop_prev) {                                  // iteration it-1 was the answer
         T0 { V.it--; V.conv = 1; }
         __syncthreads();
@@ -393,12 +394,12 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(const __grid_constant__ 
         }
         __syncthreads();
       }
-      mark(E, 6);
+      MARK(6);
       if (!V.accept) {
         if (V.quit) goto out;
         zero12();
         prox(false);
-        mark(E, 9);
+        MARK(9);
         continue;
       }
       {
@@ -406,7 +407,7 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(const __grid_constant__ 
         double* os[1] = {Gp(V.igx)};
         panel_gemv_t_pre<TA, 1>(E, D, PN, gpre, rs, os);   // g_x = A^T r_next  (shrinkage.py:285)
       }
-      mark(E, 7);
+      MARK(7);
       zero12();
       {
         // KKT / support partials of the accepted iterate (model.py:160-173, 227-233)
@@ -439,7 +440,7 @@ __global__ void __launch_bounds__(NTHR, 1) fista_kernel(const __grid_constant__ 
         break;
       }
       prox(true);                                         // next iteration's first trial (same thread per k)
-      mark(E, 8);
+      MARK(8);
     }
     T0 if (!V.conv && V.it < C.max_iter && a.max_steps > 0) V.status = ELL1_RUNNING;
     __syncthreads();
@@ -713,8 +714,11 @@ extern "C" int ell1_fista(const ell1_dict_t* D, const double* b, const ell1_ctrl
   if (D->ld > D->d)
     for (int k = 0; k < 3; ++k)
       if (cudaMemsetAsync(a.R[k] + D->d, 0, (D->ld - D->d) * 8, s) != cudaSuccess) return ELL1_ERR_CUDA;
-  return (D->dtype == ELL1_F64) ? coop_launch(fista_kernel<double>, nb, sp.bytes, s, a, a.g.bar)
-                                : coop_launch(fista_kernel<float>, nb, sp.bytes, s, a, a.g.bar);
+  if (a.prof)
+    return (D->dtype == ELL1_F64) ? coop_launch(fista_kernel<double, true>, nb, sp.bytes, s, a, a.g.bar)
+                                  : coop_launch(fista_kernel<float, true>, nb, sp.bytes, s, a, a.g.bar);
+  return (D->dtype == ELL1_F64) ? coop_launch(fista_kernel<double, false>, nb, sp.bytes, s, a, a.g.bar)
+                                : coop_launch(fista_kernel<float, false>, nb, sp.bytes, s, a, a.g.bar);
 }
 
 extern "C" size_t ell1_correlation_workspace(const ell1_dict_t* D) {
