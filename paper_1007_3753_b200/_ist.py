@@ -28,5 +28,5 @@ def ist_solve_device(P, schedule, config, observer=None):
             observer(host_vec(bufs.x), float(st.scal[1]), float(st.scal[4]))
     st = drive(launch, bufs, step)
     raise_for(st.status, {})
-    return SolverResult(host_vec(bufs.x), int(st.iterations), prep.elapsed(), bool(st.converged),
+    return SolverResult(bufs.x_host(), int(st.iterations), prep.elapsed(), bool(st.converged),
                         bufs.read_trace(st.ntrace))

@@ -39,7 +39,7 @@ def palm_solve_device(P, config, observer=None):
             observer(AlmState(host_vec(bufs.x), host_vec(yb, prep.d), float(st.scal[4]), rho, O.tau))
     st = _drive_outer(launch, bufs, step)
     raise_for(st.status, {})
-    x = host_vec(bufs.x)
+    x = bufs.x_host()
     trace = bufs.read_trace(st.ntrace)
     notes = ()
     if not st.converged and st.iterations >= config.max_iter:

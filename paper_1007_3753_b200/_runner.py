@@ -71,20 +71,32 @@ class Prepared:
 
 
 class Buffers:
-    """Workspace + state + trace + output vectors of one solve."""
+    """Workspace + state + trace + output vectors of one solve.
+
+    state (256 bytes), x and the trace share one device allocation so a
+    finished solve is read back with a single device->host copy
+    (``read_all``) instead of one synchronising copy per field."""
+
+    SNAP_ROWS = 4096           # trace rows included in the single read-back
 
     def __init__(self, prep, ws_bytes, trace_rows, want_prev=False, want_y=False):
         torch = device._torch()
         dev = prep.dev
         self.ws = device.alloc_bytes(ws_bytes, dev)
         self.ws_bytes = int(self.ws.numel())
-        self.state = torch.zeros(256, dtype=torch.uint8, device=dev)
-        self.trace = torch.zeros(max(trace_rows, 1) * 4, dtype=torch.float64, device=dev)
-        self.x = torch.zeros(prep.n, dtype=torch.float64, device=dev)
-        self.x_prev = torch.zeros(prep.n, dtype=torch.float64, device=dev) if want_prev else None
-        self.y = torch.zeros(prep.n, dtype=torch.float64, device=dev) if want_y else None
+        n = int(prep.n)
+        rows = max(int(trace_rows), 1)
+        self.n = n
+        self.blob = torch.zeros(32 + n + rows * 4, dtype=torch.float64, device=dev)
+        self.state = self.blob[:32].view(torch.uint8)
+        self.x = self.blob[32:32 + n]
+        self.trace = self.blob[32 + n:]
+        self.x_prev = torch.zeros(n, dtype=torch.float64, device=dev) if want_prev else None
+        self.y = torch.zeros(n, dtype=torch.float64, device=dev) if want_y else None
+        self._snap = None
 
     def io(self, max_steps=0, blocks=0):
+        self._snap = None
         io = _lib.IO()
         io.workspace = self.ws.data_ptr()
         io.workspace_bytes = self.ws_bytes
@@ -97,14 +109,28 @@ class Buffers:
         io.blocks = int(blocks)
         return io
 
+    def read_all(self):
+        """One copy of state + x + the leading trace rows; returns the state."""
+        rows = min(self.trace.numel() // 4, self.SNAP_ROWS)
+        self._snap = self.blob[: 32 + self.n + 4 * rows].cpu().numpy()
+        return _lib.State.from_buffer_copy(self._snap[:32].tobytes())
+
     def read_state(self):
         raw = self.state.cpu().numpy().tobytes()
         return _lib.State.from_buffer_copy(raw)
 
+    def x_host(self):
+        if self._snap is not None:
+            return self._snap[32:32 + self.n].copy()
+        return host_vec(self.x)
+
     def read_trace(self, rows):
         if rows <= 0:
             return []
-        t = self.trace[: rows * 4].cpu().numpy().reshape(rows, 4)
+        if self._snap is not None and rows <= self.SNAP_ROWS:
+            t = self._snap[32 + self.n: 32 + self.n + rows * 4].reshape(rows, 4)
+        else:
+            t = self.trace[: rows * 4].cpu().numpy().reshape(rows, 4)
         return [TraceEntry(int(r[0]), float(r[1]), float(r[2]), int(r[3])) for r in t]
 
 
@@ -131,8 +157,7 @@ def drive(launch, bufs, observer_step=None):
     the host in between (the reference's per-iteration callback)."""
     if observer_step is None:
         _lib.check(launch(bufs.io(0)), "solver launch")
-        st = bufs.read_state()
-        return st
+        return bufs.read_all()
     while True:
         before = bufs.read_state().iterations
         _lib.check(launch(bufs.io(1)), "solver launch")

@@ -35,5 +35,5 @@ def tnipm_solve_device(P, lam, config, observer=None):
     notes = ()
     if st.rot[0]:
         notes = ("pcg hit its iteration cap %d times" % st.rot[0],)
-    return SolverResult(host_vec(bufs.x), int(st.iterations), prep.elapsed(), bool(st.converged),
+    return SolverResult(bufs.x_host(), int(st.iterations), prep.elapsed(), bool(st.converged),
                         bufs.read_trace(st.ntrace), notes)

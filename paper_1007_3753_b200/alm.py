@@ -107,14 +107,14 @@ def dalm_solve(P, config, observer=None):
         chol = CholFactor(Lfac.T.contiguous().cpu().numpy())
 
         def step(st):
-            x = host_vec(bufs.x)
+            x = bufs.x_host()
             xp = host_vec(bufs.x_prev)
             observer(DalmState(x, host_vec(yb, prep.d), host_vec(zb), beta, chol), xp)
     st = drive(launch, bufs, step)
     raise_for(st.status, {_lib.ILL_CONDITIONED: "dual least-squares step failed its residual "
                                                  "contract" if not cg_mode else
                           "row Gram lost positive definiteness"})
-    x = host_vec(bufs.x)
+    x = bufs.x_host()
     trace = bufs.read_trace(st.ntrace)
     notes = ()
     if not st.converged and st.iterations >= config.max_iter:

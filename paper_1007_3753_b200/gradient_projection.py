@@ -122,7 +122,7 @@ def gpsr_solve(P, lam, config, observer=None):
     st = drive(launch, bufs, step)
     raise_for(st.status, {})
     notes = (_GPSR_NOTES[st.rot[2]],) if st.rot[2] in _GPSR_NOTES else ()
-    return SolverResult(host_vec(bufs.x), int(st.iterations), prep.elapsed(), bool(st.converged),
+    return SolverResult(bufs.x_host(), int(st.iterations), prep.elapsed(), bool(st.converged),
                         bufs.read_trace(st.ntrace), notes)
 
 

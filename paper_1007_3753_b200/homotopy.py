@@ -150,7 +150,7 @@ def solve_path(D, b, target_lambda, config, path_csv=None, observer=None):
                           _lib.DEGENERATE: "active-set Gram is singular"})
     trace = bufs.read_trace(st.ntrace)
     notes = ("ridge-regularized gram",) if st.rot[1] else ()
-    x = host_vec(bufs.x)
+    x = bufs.x_host()
     lam = float(st.scal[0])
     if path_csv is not None:
         if st.status == _lib.ZERO_DATA:

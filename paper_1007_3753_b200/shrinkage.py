@@ -166,7 +166,7 @@ class FistaPlan:
         st = st if st is not None else self.bufs.read_state()
         raise_for(st.status, {_lib.BREAKDOWN: "backtracking exceeded 100 growth steps",
                               _lib.LAMBDA_NONPOS: "lambda must be positive"})
-        x = host_vec(self.bufs.x)
+        x = self.bufs.x_host()
         trace = self.bufs.read_trace(st.ntrace)
         return SolverResult(x, int(st.iterations), self.prep.elapsed(), bool(st.converged), trace)
 
