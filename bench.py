@@ -554,11 +554,11 @@ def run_b200(args):
         alg_bytes = passes * P.d * P.n * sz
         achieved = alg_bytes / (tmax / args.steps) / 1e9
         traffic = None
-        prof = os.path.join(ROOT, "profiles", "ncu_fista_cfg2.json")
-        if os.path.exists(prof):
+        prof = os.path.join(ROOT, "profiles", "r01_ncu_fista_cfg2.json")
+        if os.path.exists(prof) and args.dtype == "float64":
             try:
-                traffic = json.load(open(prof)).get("dram_bytes_per_launch")
-            except ValueError:
+                traffic = json.load(open(prof))["kernels"][0].get("dram_traffic_bytes")
+            except (ValueError, KeyError, IndexError):
                 traffic = None
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,

@@ -858,50 +858,107 @@ __device__ void panel_gemv_t_pre(const Ctx& E, const DictV<TA>& D, const Panel<T
     }
     __syncthreads();
   } else {
-    // Long columns: column groups of NWARP x CPW; r is staged through shared
-    // memory in row chunks shared by every warp of the group, so each r
-    // element is read from L2 once per group instead of once per column.
-    constexpr int CPW = 4;
-    int64_t rch = E.shcap / (VW * NV);
-    if (rch > 1024) rch = 1024;
+    // Long columns: column groups of NWARP x CPW (a warp per CPW columns, lanes
+    // over rows).  r is staged through shared memory in row chunks shared by
+    // every warp of the group, double-buffered: the next chunk's loads are in
+    // flight (registers) while the current one is consumed, one __syncthreads
+    // per chunk.  The CPW columns of a warp are walked together, so each lane
+    // keeps CPW independent 16-byte loads of A in flight.
+    constexpr int CPW = sizeof(TA) == 8 ? 2 : 4;        // columns per warp
+    constexpr int QU = sizeof(TA) == 8 ? 2 : 1;         // row steps per lane in flight
+    constexpr int SPT = 4;                              // staged doubles per thread per chunk
+    int64_t rch = (int64_t)NTHR * SPT / (VW * NV);      // row vectors per chunk
+    while (rch * VW * NV * 2 > E.shcap && rch > 32) rch /= 2;
     rch = rch / 32 * 32;
-    if (rch < 32) rch = 32;
-    double* rsm = shmem(E.sh);
+    double* const stg0 = shmem(E.sh);
+    double* const stg1 = stg0 + rch * VW * NV;
+    const int64_t nch = (nvec + rch - 1) / rch;
+    const int64_t sdbl = rch * VW;                      // staged doubles per vector per chunk
+    // staging: thread t moves doubles t, t + NTHR, ... of the chunk (all vectors)
+#define ELL1_STAGE_LOAD(ch, buf)                                                     \
+  do {                                                                              \
+    const int64_t rb_ = (ch) * rch;                                                 \
+    const int64_t cnt_ = min(rch, nvec - rb_) * VW;                                 \
+    _Pragma("unroll") for (int u = 0; u < SPT; ++u) {                               \
+      const int64_t t = tix() + (int64_t)u * NTHR;                                  \
+      double val_ = 0.0;                                                            \
+      _Pragma("unroll") for (int v = 0; v < NV; ++v) {                              \
+        const int64_t o = t - (int64_t)v * sdbl;                                    \
+        if (o >= 0 && o < cnt_) val_ = ldcg(rs[v] + rb_ * VW + o);                  \
+      }                                                                             \
+      buf[u] = val_;                                                                \
+    }                                                                               \
+  } while (0)
+#define ELL1_STAGE_STORE(dst, buf)                                                   \
+  do {                                                                              \
+    _Pragma("unroll") for (int u = 0; u < SPT; ++u) {                               \
+      const int64_t t = tix() + (int64_t)u * NTHR;                                  \
+      if (t < NV * sdbl) (dst)[t] = buf[u];                                         \
+    }                                                                               \
+  } while (0)
     for (int jg = 0; jg < w; jg += NWARP * CPW) {
       double acc[CPW][NV];
 #pragma unroll
       for (int c = 0; c < CPW; ++c)
 #pragma unroll
         for (int v = 0; v < NV; ++v) acc[c][v] = 0.0;
-      for (int64_t rb = 0; rb < nvec; rb += rch) {
+      const TA* colp[CPW];
+      bool resc[CPW], live[CPW];
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) {
+        const int jl = jg + wpx() * CPW + c;
+        live[c] = jl < w;
+        resc[c] = jl < rc;
+        colp[c] = (resc[c] ? P.sm : P.gl) + (int64_t)(live[c] ? jl : 0) * D.ld;
+      }
+      double buf[SPT];
+      ELL1_STAGE_LOAD(0, buf);
+      ELL1_STAGE_STORE(stg0, buf);
+      __syncthreads();
+      for (int64_t ch = 0; ch < nch; ++ch) {
+        const bool more = ch + 1 < nch;
+        if (more) ELL1_STAGE_LOAD(ch + 1, buf);          // in flight during the sweep
+        const double* cur = (ch & 1) ? stg1 : stg0;
+        const int64_t rb = ch * rch;
         const int64_t rcnt = min(rch, nvec - rb);
-        for (int64_t t = tix(); t < rcnt * VW; t += NTHR)
+        for (int64_t q0 = lnx(); q0 < rcnt; q0 += 32 * QU) {
+          TA a[QU][CPW][VW];
 #pragma unroll
-          for (int v = 0; v < NV; ++v) rsm[v * rch * VW + t] = ldcg(rs[v] + rb * VW + t);
-        __syncthreads();
+          for (int h = 0; h < QU; ++h) {
+            const int64_t q = q0 + 32 * h;
 #pragma unroll
-        for (int c = 0; c < CPW; ++c) {
-          const int jl = jg + wpx() * CPW + c;
-          if (jl < w) {
-            const bool res = jl < rc;
-            const TA* col = (res ? P.sm : P.gl) + (int64_t)jl * D.ld + rb * VW;
-            for (int64_t q = lnx(); q < rcnt; q += 32) {
-              TA a[VW];
-              if (res) ld16_s<TA>(col + q * VW, a);
-              else ld16_g<TA>(col + q * VW, a);
+            for (int c = 0; c < CPW; ++c) {
+              if (live[c] && q < rcnt) {
+                const TA* pa = colp[c] + (rb + q) * VW;
+                if (resc[c]) ld16_s<TA>(pa, a[h][c]);
+                else ld16_g<TA>(pa, a[h][c]);
+              } else {
+#pragma unroll
+                for (int e = 0; e < VW; ++e) a[h][c][e] = (TA)0;
+              }
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < QU; ++h) {
+            const int64_t q = q0 + 32 * h;
+            if (q < rcnt) {
 #pragma unroll
               for (int v = 0; v < NV; ++v) {
-                const double2* rv = reinterpret_cast<const double2*>(rsm + v * rch * VW + q * VW);
+                const double2* rv = reinterpret_cast<const double2*>(cur + v * sdbl + q * VW);
 #pragma unroll
                 for (int e2 = 0; e2 < VW / 2; ++e2) {
                   const double2 t = rv[e2];
-                  acc[c][v] = fma((double)a[2 * e2], t.x, acc[c][v]);
-                  acc[c][v] = fma((double)a[2 * e2 + 1], t.y, acc[c][v]);
+#pragma unroll
+                  for (int c = 0; c < CPW; ++c) {
+                    acc[c][v] = fma((double)a[h][c][2 * e2], t.x, acc[c][v]);
+                    acc[c][v] = fma((double)a[h][c][2 * e2 + 1], t.y, acc[c][v]);
+                  }
                 }
               }
             }
           }
         }
+        if (more) ELL1_STAGE_STORE(((ch + 1) & 1) ? stg1 : stg0, buf);
         __syncthreads();
       }
 #pragma unroll
@@ -914,6 +971,8 @@ __device__ void panel_gemv_t_pre(const Ctx& E, const DictV<TA>& D, const Panel<T
         }
       }
     }
+#undef ELL1_STAGE_LOAD
+#undef ELL1_STAGE_STORE
     __syncthreads();
   }
 }
