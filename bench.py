@@ -323,6 +323,11 @@ def leg_cfg4(torch, dev, ws, rank, iters=8, reps=2):
     return out
 
 
+def _lib_mode():
+    from paper_1007_3753_b200 import _lib
+    return int(_lib.lib().ell1_blas_fp32_mode())
+
+
 def leg_cfg3(torch, dev, queries=1024):
     """BASELINE config 3: CAB [A I] (d=1024, 38 classes x 32 columns), 1024
     corrupted queries, batched dual ALM in fp32 storage + SRC labels."""
@@ -349,6 +354,8 @@ def leg_cfg3(torch, dev, queries=1024):
             "queries_per_sec": queries / t, "ms_per_batch": 1e3 * t,
             "mean_iterations": float(its.mean()), "max_iterations": int(its.max()),
             "accuracy_vs_truth": float(np.mean(labels == truth)),
+            "fp32_gemm": {2: "3xTF32 split GEMMs (tensor pipe)", 0: "cuBLAS SIMT SGEMM"}.get(
+                _lib_mode(), "unknown"),
             "note": "timed through the public call (host queries in, labels out)"}
 
 

@@ -331,6 +331,10 @@ int ell1_shard_kkt(int64_t n, const double* x, const double* g, double lam, doub
 int ell1_shard_resid(int64_t d, const double* ax, const double* b, const double* rx, double mn, double* rn,
                      double* out8, void* ws, void* stream);
 
+/* fp32 GEMM path of the batched solvers (2: 3xTF32 split GEMMs on the tensor
+ * pipe, opt-in with ELL1_FP32_GEMM=tf32x3; 0: SIMT SGEMM; -1: not used yet). */
+int ell1_blas_fp32_mode(void);
+
 /* library / device info */
 int ell1_device_sms(int32_t device);
 const char* ell1_version(void);

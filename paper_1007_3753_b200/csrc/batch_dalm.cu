@@ -315,6 +315,8 @@ extern "C" size_t ell1_batch_dalm_workspace(const ell1_dict_t* D, int32_t B) {
   s += align_up(ldx * B * 4, 256) * 3 + align_up(ldx * 2 * B * 4, 256) + align_up(ld * B * 4, 256) * 3 +
        align_up(ld * 2 * B * 4, 256);
   s += 2 * align_up((int64_t)sizeof(DI) * B, 256) + align_up(B * 4, 256) + align_up(ldx * B * 8, 256);
+  if (D->dtype == ELL1_F32)                                  // splits of A and M + operand scratch
+    s += (size_t)(f32split_floats(D, (ldx > ld ? ldx : ld) * 2 * B) + 2 * align_up(D->n * D->ld, 64)) * 4 + 2048;
   return s + 8192;
 }
 
@@ -357,6 +359,20 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   int* ctr = cv.take<int>(8);
   if (!cv.ok) return ELL1_ERR_ARG;
   (void)xscr; (void)T32;
+  F32Split spA, spM;
+  const F32Split* pA = nullptr;
+  const F32Split* pM = nullptr;
+  if (a.f32) {
+    if (!f32split_setup(spA, cv, D, (ldx > ld ? ldx : ld) * 2 * B, s)) return ELL1_ERR_ARG;
+    ell1_dict_t MDs = *D;
+    MDs.A = O->M;
+    float* mh = cv.take<float>(D->n * D->ld);
+    float* ml = cv.take<float>(D->n * D->ld);
+    if (!cv.ok || !split_tf32((const float*)O->M, mh, ml, D->n * D->ld, s)) return ELL1_ERR_ARG;
+    spM = spA;                                               // shares the operand scratch
+    spM.Ahi = mh; spM.Alo = ml;
+    pA = &spA; pM = &spM;
+  }
   a.Bm = Bm; a.C0 = C0;
   a.counters = ctr;
   a.x_out = out->x; a.it_out = out->iterations; a.conv_out = out->converged; a.status_out = out->status;
@@ -405,8 +421,8 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
     {
       const void* Vop = a.f32 ? (const void*)a.V32 : (const void*)a.V;
       const void* Zop = a.f32 ? (const void*)a.Z32 : (const void*)a.Z;
-      if (!gemm_AX(h, &MD, Vop, ldx, a.f32 ? (void*)a.P1f : (void*)a.P1, ld, Bcur)) return ELL1_ERR_CUDA;
-      if (!gemm_AX(h, D, Zop, ldx, a.f32 ? (void*)a.P2f : (void*)a.P2, ld, Bcur)) return ELL1_ERR_CUDA;
+      if (!gemm_AX(h, &MD, Vop, ldx, a.f32 ? (void*)a.P1f : (void*)a.P1, ld, Bcur, pM)) return ELL1_ERR_CUDA;
+      if (!gemm_AX(h, D, Zop, ldx, a.f32 ? (void*)a.P2f : (void*)a.P2, ld, Bcur, pA)) return ELL1_ERR_CUDA;
       if (a.ext) {
         // identity block of M: s Ginv v_ext (s folded into v_ext by bd_z)
         if (cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)ld, Bcur, (int)d, &one, O->Ginv, (int)ld,
@@ -419,13 +435,13 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
     while (true) {
       // U = A^T y_new (n x B), then x_new, then A [U | x_new]
       void* Ut = a.f32 ? (void*)T32 : (void*)scratch;
-      if (!gemm_AtR(h, D, a.f32 ? (const void*)a.Y32 : (const void*)a.Y[a.iy ^ 1], ld, Ut, D->n, Bcur))
+      if (!gemm_AtR(h, D, a.f32 ? (const void*)a.Y32 : (const void*)a.Y[a.iy ^ 1], ld, Ut, D->n, Bcur, pA))
         return ELL1_ERR_CUDA;
       // UX holds [U | x_new] for the Bcur instances: x_new block starts at column Bcur
       bd_x<<<Bcur, BT, 0, s>>>(a, (const double*)Ut, (const float*)Ut, refine_only);
       if (a.f32) {
         // UX32 layout: [U | x_new] with Bcur columns each
-        if (!gemm_AX(h, D, a.UX32, ldx, a.P2f, ld, 2 * Bcur)) return ELL1_ERR_CUDA;
+        if (!gemm_AX(h, D, a.UX32, ldx, a.P2f, ld, 2 * Bcur, pA)) return ELL1_ERR_CUDA;
       } else {
         if (!gemm_AX(h, D, a.UX, ldx, a.P2, ld, 2 * Bcur)) return ELL1_ERR_CUDA;
       }

@@ -303,6 +303,7 @@ extern "C" size_t ell1_batch_fista_workspace(const ell1_dict_t* D, int32_t B) {
   s += align_up(ldx * B * 4, 256) * 2 + align_up(ld * B * 4, 256) * 2;       // fp32 operands
   s += align_up((ldx > ld ? ldx : ld) * B * 8, 256);                        // compaction scratch
   s += align_up(B * 4, 256) + 4096;
+  if (D->dtype == ELL1_F32) s += (size_t)f32split_floats(D, (ldx > ld ? ldx : ld) * B) * 4 + 1024;
   return s;
 }
 
@@ -334,6 +335,12 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
   int* perm = cv.take<int>(B);
   int* ctr = cv.take<int>(8);
   if (!cv.ok) return ELL1_ERR_ARG;
+  F32Split sp;
+  const F32Split* spp = nullptr;
+  if (a.f32) {
+    if (!f32split_setup(sp, cv, D, (ldx > ld ? ldx : ld) * B, s)) return ELL1_ERR_ARG;
+    spp = &sp;
+  }
   a.Bm = Bm;
   a.counters = ctr;
   a.x_out = out->x; a.it_out = out->iterations; a.conv_out = out->converged; a.status_out = out->status;
@@ -353,7 +360,7 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
       Bop = B32;
     }
     void* CT = a.f32 ? (void*)a.G32 : (void*)scratch;      // n x B
-    if (!gemm_AtR(h, D, Bop, ld, CT, D->n, B)) return ELL1_ERR_CUDA;
+    if (!gemm_AtR(h, D, Bop, ld, CT, D->n, B, spp)) return ELL1_ERR_CUDA;
     bf_init<<<B, BT, 0, s>>>(a, (const double*)CT, (const float*)CT, B);
   }
   int Bcur = B;
@@ -390,7 +397,7 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
       if (cudaMemsetAsync(ctr, 0, 4, s) != cudaSuccess) return ELL1_ERR_CUDA;
       bf_prox<<<Bcur, BT, 0, s>>>(a, round);
       if (!gemm_AX(h, D, a.f32 ? (const void*)a.X32 : (const void*)a.X[a.ixn], ldx,
-                   a.f32 ? (void*)a.AX32 : (void*)a.AX, ld, Bcur))
+                   a.f32 ? (void*)a.AX32 : (void*)a.AX, ld, Bcur, spp))
         return ELL1_ERR_CUDA;
       bf_resid<<<Bcur, BT, 0, s>>>(a, round);
       int retry = 0;
@@ -401,7 +408,7 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
     }
     // g_next = A^T r_next into the g ring's free slot
     if (!gemm_AtR(h, D, a.f32 ? (const void*)a.R32 : (const void*)a.R[a.irn], ld,
-                  a.f32 ? (void*)a.G32 : (void*)a.G[a.igxp], a.f32 ? D->n : ldx, Bcur))
+                  a.f32 ? (void*)a.G32 : (void*)a.G[a.igxp], a.f32 ? D->n : ldx, Bcur, spp))
       return ELL1_ERR_CUDA;
     bf_finish<<<Bcur, BT, 0, s>>>(a, a.igxp);
     // rotate the rings (shrinkage.py:283-284)
