@@ -390,10 +390,12 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   ell1_dict_t MD = *D;
   MD.A = O->M;                                              // M has A's layout / dtype
   int Bcur = B;
+  // hc = {refine flags, active instances}: read once here, then together with
+  // every certificate round's refine count (one device->host sync per iteration)
+  int hc[2] = {0, 0};
+  if (cudaMemcpyAsync(hc, ctr, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return ELL1_ERR_CUDA;
   while (true) {
-    int hc[2];
-    if (cudaMemcpyAsync(hc, ctr, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
-    if (cudaStreamSynchronize(s) != cudaSuccess) return ELL1_ERR_CUDA;
     const int nact = hc[1];
     if (nact <= 0) break;
     if (nact < Bcur * 3 / 4 || (nact < Bcur && nact <= 64)) {
@@ -447,10 +449,9 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
       }
       if (cudaMemsetAsync(ctr, 0, 4, s) != cudaSuccess) return ELL1_ERR_CUDA;
       bd_c<<<Bcur, BT, 0, s>>>(a, refine_only);
-      int nref = 0;
-      if (cudaMemcpyAsync(&nref, ctr, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
+      if (cudaMemcpyAsync(hc, ctr, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
       if (cudaStreamSynchronize(s) != cudaSuccess) return ELL1_ERR_CUDA;
-      if (nref == 0) break;
+      if (hc[0] == 0) break;
       // y += Ginv resid for the flagged instances (alm.py:184)
       if (cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)ld, Bcur, (int)d, &one, O->Ginv, (int)ld, a.RES,
                       (int)ld, &zero, a.GEXT, (int)ld) != CUBLAS_STATUS_SUCCESS)

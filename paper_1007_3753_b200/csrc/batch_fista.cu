@@ -1,11 +1,18 @@
 // batch_fista.cu — FISTA over a batch of instances sharing one dictionary
 // (element j equals shrinkage.fista_solve on (A, b_j), shrinkage.py:231-298).
 //
-// Per iteration: prox kernel (momentum point from the cached products,
-// soft-threshold, backtracking reductions) -> GEMM  A X_next -> residual kernel
-// (r_next, F, Q, accept / grow L per instance) [repeat for instances still
-// backtracking] -> GEMM  A^T R_next -> finish kernel (KKT, support, trace,
-// stopping rules, continuation).
+// One host round = one backtracking trial of every active instance:
+//   bf_prox   momentum point (new iteration) or the stored one (retry),
+//             soft-threshold, backtracking reductions
+//   GEMM      A X_next
+//   bf_resid  r_next, F, Q: accept, or grow L and mark the instance for a retry
+//   GEMM      A^T R_next  (speculative for instances that will retry)
+//   bf_finish accepted: KKT, support, trace, stopping rules, continuation;
+//             retrying: copy its columns so the global ring rotation leaves
+//             its state unchanged
+// Instances run their own backtracking independently, so the host never
+// waits for a retry decision: it reads one device counter every few rounds
+// (termination / compaction of finished instances).
 #include "batched.cuh"
 
 namespace ell1 {
@@ -13,7 +20,7 @@ namespace ell1 {
 struct BI {                 // per-instance control state
   double L, tp, tc, lam, lam_bar, Fprev, fy, fy_next, m, tn, mn, rr, Fn, c0, bn;
   double S[7];
-  int it, hist, bt, active, accepted, status, conv, orig;
+  int it, hist, bt, active, accepted, status, conv, orig, retry;
 };
 
 struct BFArgs {
@@ -26,6 +33,7 @@ struct BFArgs {
   double* G[2];               // ldx x B
   double* R[3];               // ld x B
   double* AX;                 // raw GEMM1 output (fp64 mode) ld x B
+  double* Y; double* GY;      // momentum point and its gradient (ldx x B), kept for retries
   float* X32; float* R32; float* AX32; float* G32;   // fp32 GEMM operands
   BI* inst;
   ell1_ctrl_t C;
@@ -64,7 +72,7 @@ __global__ void __launch_bounds__(BT) bf_init(const BFArgs a, const double* CT, 
     I.orig = j;
     I.c0 = v[0];
     I.bn = sqrt(v[1]);
-    I.it = 0; I.hist = 0; I.bt = 0; I.accepted = 0; I.conv = 0; I.status = ELL1_OK; I.active = 1;
+    I.it = 0; I.hist = 0; I.bt = 0; I.accepted = 0; I.conv = 0; I.status = ELL1_OK; I.active = 1; I.retry = 0;
     I.Fprev = 0.0;
     if (I.c0 == 0.0) {                                    // shrinkage.py:245-247
       I.status = ELL1_ZERO_DATA; I.conv = 1; I.active = 0;
@@ -86,38 +94,49 @@ __global__ void __launch_bounds__(BT) bf_init(const BFArgs a, const double* CT, 
   }
 }
 
-__global__ void __launch_bounds__(BT) bf_prox(const BFArgs a, int round) {
+__global__ void __launch_bounds__(BT) bf_prox(const BFArgs a) {
   const int j = blockIdx.x;
   __shared__ double sh[BW * 7 + 7];
   __shared__ double sc[4];
+  __shared__ int fresh;
   BI& I = a.inst[j];
-  if (!I.active || (round > 0 && I.accepted)) return;
+  if (!I.active) return;
   if (threadIdx.x == 0) {
-    if (round == 0) {
+    fresh = !I.retry;
+    if (fresh) {                                            // a new iteration
       I.it++;
       I.bt = 0;
-      I.accepted = 0;
       I.m = (I.tp - 1.0) / I.tc;
       I.tn = fista_t_next(I.tc);
       I.mn = (I.tc - 1.0) / I.tn;
     }
+    I.accepted = 0;
     sc[0] = I.m; sc[1] = I.L; sc[2] = I.lam / I.L;
   }
   __syncthreads();
   const double m = sc[0], L = sc[1], thr = sc[2];
+  const bool fr = fresh;
   const int64_t o = (int64_t)j * a.ldx;
   const double* x = a.X[a.ix] + o;
   const double* xp = a.X[a.ixp] + o;
   double* xn = a.X[a.ixn] + o;
   const double* gx = a.G[a.igx] + o;
   const double* gxp = a.G[a.igxp] + o;
+  double* Y = a.Y + o;
+  double* GY = a.GY + o;
   const bool relest = a.C.stop_kind == ELL1_STOP_REL_ESTIMATE;
   const bool gtr = a.C.stop_kind == ELL1_STOP_GROUND_TRUTH;
   double s[7] = {0, 0, 0, 0, 0, 0, 0};
   for (int64_t k = threadIdx.x; k < a.N; k += BT) {
     const double xk = x[k];
-    const double yk = xk + m * (xk - xp[k]);                // shrinkage.py:270
-    const double gk = (1.0 + m) * gx[k] - m * gxp[k];       // A^T(A y - b)
+    double yk, gk;
+    if (fr) {
+      yk = xk + m * (xk - xp[k]);                           // shrinkage.py:270
+      gk = (1.0 + m) * gx[k] - m * gxp[k];                  // A^T(A y - b)
+      Y[k] = yk; GY[k] = gk;
+    } else {
+      yk = Y[k]; gk = GY[k];
+    }
     const double u = soft1(yk - gk / L, thr);                // shrinkage.py:204
     xn[k] = u;
     if (a.f32 && k < a.n) a.X32[(int64_t)j * a.ldx + k] = (float)u;
@@ -134,11 +153,11 @@ __global__ void __launch_bounds__(BT) bf_prox(const BFArgs a, int round) {
     for (int k = 0; k < 7; ++k) I.S[k] = s[k];
 }
 
-__global__ void __launch_bounds__(BT) bf_resid(const BFArgs a, int round) {
+__global__ void __launch_bounds__(BT) bf_resid(const BFArgs a) {
   const int j = blockIdx.x;
   __shared__ double sh[BW * 2 + 2];
   BI& I = a.inst[j];
-  if (!I.active || (round > 0 && I.accepted)) return;
+  if (!I.active) return;
   const double mn = I.mn;
   const double* b = a.Bm + (int64_t)j * a.ld;
   const double* xn = a.X[a.ixn] + (int64_t)j * a.ldx;
@@ -170,16 +189,16 @@ __global__ void __launch_bounds__(BT) bf_resid(const BFArgs a, int round) {
     }
     if (acc) {
       I.accepted = 1;
+      I.retry = 0;
       I.fy_next = 0.5 * q[1];
     } else {
       I.L *= a.O.eta;
       I.bt++;
+      I.retry = 1;
       if (I.bt > 100) {                                     // shrinkage.py:203,213
         I.status = ELL1_BREAKDOWN; I.active = 0;
         a.it_out[I.orig] = I.it; a.conv_out[I.orig] = 0; a.status_out[I.orig] = I.status;
         atomicSub(a.counters + 1, 1);
-      } else {
-        atomicAdd(a.counters, 1);
       }
     }
   }
@@ -191,6 +210,22 @@ __global__ void __launch_bounds__(BT) bf_finish(const BFArgs a, int gslot) {
   BI& I = a.inst[j];
   if (!I.active) return;
   const int64_t o = (int64_t)j * a.ldx;
+  if (I.retry) {
+    // rejected trial: after the global rotation (x_prev <- x <- x_next,
+    // r likewise, g_x <-> g slot) this instance must see its current state
+    // again, so place it where the rotation will look for it
+    const int64_t orr = (int64_t)j * a.ld;
+    for (int64_t k = threadIdx.x; k < a.N; k += BT) {
+      a.X[a.ixn][o + k] = a.X[a.ix][o + k];
+      a.X[a.ix][o + k] = a.X[a.ixp][o + k];
+      a.G[gslot][o + k] = a.G[a.igx][o + k];
+    }
+    for (int64_t i = threadIdx.x; i < a.ld; i += BT) {
+      a.R[a.irn][orr + i] = a.R[a.irx][orr + i];
+      a.R[a.irx][orr + i] = a.R[a.irxp][orr + i];
+    }
+    return;
+  }
   const double* xn = a.X[a.ixn] + o;               // the new x
   double* gn = a.G[gslot] + o;                     // the new g_x
   const double* rn = a.R[a.irn] + (int64_t)j * a.ld;
@@ -297,7 +332,7 @@ extern "C" size_t ell1_batch_fista_workspace(const ell1_dict_t* D, int32_t B) {
   if (!dict_ok(D) || B < 1) return 0;
   const int64_t N = ncols_of(D), ldx = round4(N), ld = D->ld;
   size_t s = 0;
-  s += 5 * align_up(ldx * B * 8, 256) + 4 * align_up(ld * B * 8, 256);     // X, G, R, AX / Bm
+  s += 7 * align_up(ldx * B * 8, 256) + 4 * align_up(ld * B * 8, 256);     // X, G, Y, GY, R, AX / Bm
   s += align_up(ld * B * 8, 256);                                           // Bm
   s += align_up((int64_t)sizeof(BI) * B, 256) * 2;
   s += align_up(ldx * B * 4, 256) * 2 + align_up(ld * B * 4, 256) * 2;       // fp32 operands
@@ -324,6 +359,8 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
   Carve cv(ws, wsb);
   for (int k = 0; k < 3; ++k) a.X[k] = cv.take<double>(ldx * B);
   for (int k = 0; k < 2; ++k) a.G[k] = cv.take<double>(ldx * B);
+  a.Y = cv.take<double>(ldx * B);
+  a.GY = cv.take<double>(ldx * B);
   for (int k = 0; k < 3; ++k) a.R[k] = cv.take<double>(ld * B);
   a.AX = cv.take<double>(ld * B);
   double* Bm = cv.take<double>(ld * B);
@@ -365,57 +402,51 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
   }
   int Bcur = B;
   int h_ctr[2] = {0, 0};
-  int iters = 0;
-  while (true) {
-    if (cudaMemcpyAsync(h_ctr, ctr, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
-    if (cudaStreamSynchronize(s) != cudaSuccess) return ELL1_ERR_CUDA;
-    const int nact = h_ctr[1];
-    if (nact <= 0) break;
-    if (nact < Bcur * 3 / 4 || (nact < Bcur && nact <= 64)) {
-      // compact the active instances to the front of every state matrix
-      bf_scan<<<1, 1024, 0, s>>>(a.inst, Bcur, perm, ctr + 2);
-      auto perm_mat = [&](double* M, int64_t rows, int64_t ldm) {
-        dim3 g((unsigned)((rows + 255) / 256 < 64 ? (rows + 255) / 256 : 64), (unsigned)nact);
-        gather_cols<double><<<g, 256, 0, s>>>(M, scratch, rows, ldm, perm, nact);
-        cudaMemcpyAsync(M, scratch, ldm * nact * 8, cudaMemcpyDeviceToDevice, s);
-      };
-      for (int k = 0; k < 3; ++k) perm_mat(a.X[k], N, ldx);
-      for (int k = 0; k < 2; ++k) perm_mat(a.G[k], N, ldx);
-      for (int k = 0; k < 3; ++k) perm_mat(a.R[k], ld, ld);
-      perm_mat(Bm, ld, ld);
-      {
-        const int64_t words = (int64_t)sizeof(BI) / 4;
-        dim3 g(1, (unsigned)nact);
-        gather_cols<int><<<g, 64, 0, s>>>((const int*)a.inst, (int*)inst2, words, words, perm, nact);
-        cudaMemcpyAsync(a.inst, inst2, sizeof(BI) * nact, cudaMemcpyDeviceToDevice, s);
-      }
-      Bcur = nact;
-    }
-    // ---- one FISTA iteration for the Bcur leading instances
-    int round = 0;
-    while (true) {
-      if (cudaMemsetAsync(ctr, 0, 4, s) != cudaSuccess) return ELL1_ERR_CUDA;
-      bf_prox<<<Bcur, BT, 0, s>>>(a, round);
-      if (!gemm_AX(h, D, a.f32 ? (const void*)a.X32 : (const void*)a.X[a.ixn], ldx,
-                   a.f32 ? (void*)a.AX32 : (void*)a.AX, ld, Bcur, spp))
-        return ELL1_ERR_CUDA;
-      bf_resid<<<Bcur, BT, 0, s>>>(a, round);
-      int retry = 0;
-      if (cudaMemcpyAsync(&retry, ctr, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
+  constexpr int SYNC_EVERY = 8;          // rounds between reads of the active count
+  for (int64_t round = 0;; ++round) {
+    if (round % SYNC_EVERY == 0) {
+      if (cudaMemcpyAsync(h_ctr, ctr, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
       if (cudaStreamSynchronize(s) != cudaSuccess) return ELL1_ERR_CUDA;
-      if (retry == 0) break;
-      ++round;
+      const int nact = h_ctr[1];
+      if (nact <= 0) break;
+      if (nact < Bcur * 3 / 4 || (nact < Bcur && nact <= 64)) {
+        // compact the active instances to the front of every state matrix
+        bf_scan<<<1, 1024, 0, s>>>(a.inst, Bcur, perm, ctr + 2);
+        auto perm_mat = [&](double* M, int64_t rows, int64_t ldm) {
+          dim3 g((unsigned)((rows + 255) / 256 < 64 ? (rows + 255) / 256 : 64), (unsigned)nact);
+          gather_cols<double><<<g, 256, 0, s>>>(M, scratch, rows, ldm, perm, nact);
+          cudaMemcpyAsync(M, scratch, ldm * nact * 8, cudaMemcpyDeviceToDevice, s);
+        };
+        for (int k = 0; k < 3; ++k) perm_mat(a.X[k], N, ldx);
+        for (int k = 0; k < 2; ++k) perm_mat(a.G[k], N, ldx);
+        perm_mat(a.Y, N, ldx);
+        perm_mat(a.GY, N, ldx);
+        for (int k = 0; k < 3; ++k) perm_mat(a.R[k], ld, ld);
+        perm_mat(Bm, ld, ld);
+        {
+          const int64_t words = (int64_t)sizeof(BI) / 4;
+          dim3 g(1, (unsigned)nact);
+          gather_cols<int><<<g, 64, 0, s>>>((const int*)a.inst, (int*)inst2, words, words, perm, nact);
+          cudaMemcpyAsync(a.inst, inst2, sizeof(BI) * nact, cudaMemcpyDeviceToDevice, s);
+        }
+        Bcur = nact;
+      }
     }
-    // g_next = A^T r_next into the g ring's free slot
+    // ---- one backtracking trial for each of the Bcur leading instances
+    bf_prox<<<Bcur, BT, 0, s>>>(a);
+    if (!gemm_AX(h, D, a.f32 ? (const void*)a.X32 : (const void*)a.X[a.ixn], ldx,
+                 a.f32 ? (void*)a.AX32 : (void*)a.AX, ld, Bcur, spp))
+      return ELL1_ERR_CUDA;
+    bf_resid<<<Bcur, BT, 0, s>>>(a);
+    // g_next = A^T r_next into the g ring's free slot (speculative for retries)
     if (!gemm_AtR(h, D, a.f32 ? (const void*)a.R32 : (const void*)a.R[a.irn], ld,
                   a.f32 ? (void*)a.G32 : (void*)a.G[a.igxp], a.f32 ? D->n : ldx, Bcur, spp))
       return ELL1_ERR_CUDA;
     bf_finish<<<Bcur, BT, 0, s>>>(a, a.igxp);
-    // rotate the rings (shrinkage.py:283-284)
+    // rotate the rings (shrinkage.py:283-284); retrying instances pre-compensated
     { int t = a.ixp; a.ixp = a.ix; a.ix = a.ixn; a.ixn = t; }
     { int t = a.irxp; a.irxp = a.irx; a.irx = a.irn; a.irn = t; }
     { int t = a.igxp; a.igxp = a.igx; a.igx = t; }
-    ++iters;
   }
   return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
 }

@@ -130,6 +130,23 @@ __device__ bool ridge_chol(const HB& a, const int* sup, int m, double* R, int ld
   return gram_chol(a, sup, m, sc[3], R, ldr, row, sc);
 }
 
+// sum_p A[sup[p], i] * w[p] in support order (same rounding as the plain
+// loop), 8 column loads in flight per thread
+__device__ __forceinline__ double sup_dot(const double* A, int64_t ld, const int* sup, int m, int64_t i,
+                                          const double* w) {
+  double acc = 0.0;
+  int p = 0;
+  for (; p + 8 <= m; p += 8) {
+    double av[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) av[u] = A[(int64_t)sup[p + u] * ld + i];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc = fma(av[u], w[p + u], acc);
+  }
+  for (; p < m; ++p) acc = fma(A[(int64_t)sup[p] * ld + i], w[p], acc);
+  return acc;
+}
+
 // ---- setup: lambda0, first atom (homotopy.py:142-177); C holds A^T b (slot = instance)
 __global__ void __launch_bounds__(NTHR) hb_init(HB a, int B) {
   const int j = blockIdx.x;
@@ -262,7 +279,7 @@ __global__ void __launch_bounds__(NTHR) hb_dir(HB a, int nact) {
   for (int64_t i = tix(); i < a.ld; i += NTHR) {
     double acc = 0.0;
     if (i < a.d)
-      for (int p = 0; p < m; ++p) acc = fma(a.A[(int64_t)sup[p] * a.ld + i], zs[p], acc);
+      acc = sup_dot(a.A, a.ld, sup, m, i, zs);
     Vs[i] = acc;
   }
 }
@@ -451,7 +468,7 @@ __global__ void __launch_bounds__(NTHR) hb_step(HB a, int nact) {
     double r = 0.0;
     if (i < a.d) {
       double acc = 0.0;
-      for (int p = 0; p < mn; ++p) acc = fma(a.A[(int64_t)sup[p] * a.ld + i], row[p], acc);
+      acc = sup_dot(a.A, a.ld, sup, mn, i, row);
       r = b[i] - acc;
       q3[0] += r * r;
     }

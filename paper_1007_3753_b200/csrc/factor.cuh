@@ -48,7 +48,16 @@ static __device__ void trsv_R(const double* R, int ldr, int m, double* z, double
     // z_B -= R[B, > B] d_{>B}: one warp per row, lanes over the row
     for (int k = wpx(); k < nbk; k += NWARP) {
       double acc = 0.0;
-      for (int j = kb + nbk + lnx(); j < m; j += 32) acc = fma(R[(size_t)(kb + k) * ldr + j], z[j], acc);
+      const double* row = R + (size_t)(kb + k) * ldr;
+      int j = kb + nbk + lnx();
+      for (; j + 96 < m; j += 128) {                          // 4 loads in flight per lane
+        const double r0 = row[j], r1 = row[j + 32], r2 = row[j + 64], r3 = row[j + 96];
+        acc = fma(r0, z[j], acc);
+        acc = fma(r1, z[j + 32], acc);
+        acc = fma(r2, z[j + 64], acc);
+        acc = fma(r3, z[j + 96], acc);
+      }
+      for (; j < m; j += 32) acc = fma(row[j], z[j], acc);
       acc = warp_sum(acc);
       if (lnx() == 0) z[kb + k] = z[kb + k] - acc;
     }
