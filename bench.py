@@ -435,6 +435,7 @@ def leg_solvers_cfg2(torch, P, reps=3):
     from paper_1007_3753_b200.gradient_projection import gpsr_solve, tnipm_solve
     from paper_1007_3753_b200.homotopy import homotopy_solve
     from paper_1007_3753_b200.model import ProblemInstance, SolverConfig, StoppingRule
+    from paper_1007_3753_b200.pdipa import pdipa_solve
     from paper_1007_3753_b200.shrinkage import fista_solve, ist_solve
     D = dv.DeviceDictionary(P.A)
     Pd = ProblemInstance.__new__(ProblemInstance)
@@ -449,7 +450,8 @@ def leg_solvers_cfg2(torch, P, reps=3):
             "dalm": lambda: dalm_solve(Pd, cfg),
             "gpsr": lambda: gpsr_solve(Pd, lam, cfgl),
             "tnipm": lambda: tnipm_solve(Pd, lam, cfgl),
-            "homotopy": lambda: homotopy_solve(Pd, lam, SolverConfig())}
+            "homotopy": lambda: homotopy_solve(Pd, lam, SolverConfig()),
+            "pdipa": lambda: pdipa_solve(Pd, SolverConfig(tol=1e-6))}
     out = {}
     for name, fn in runs.items():
         try:

@@ -331,6 +331,35 @@ int ell1_shard_kkt(int64_t n, const double* x, const double* g, double lam, doub
 int ell1_shard_resid(int64_t d, const double* ax, const double* b, const double* rx, double mn, double* rn,
                      double* out8, void* ws, void* stream);
 
+/* ---------------------------------------------- PDIPA vector kernels (pdipa.cu)
+ * Primal-dual interior point on the split LP min 1'v, [A, -A] v = b, v >= 0
+ * (pdipa.py:97-185; split = 1: vectors of length 2n against n columns; split = 0:
+ * an explicit A_ext with n columns, newton_kkt_step pdipa.py:65-94).  Scalar
+ * outputs are fixed-order reductions; ws >= ell1_pd_workspace() bytes. */
+size_t ell1_pd_workspace(void);
+/* u = x[:n] - x[n:] (or x), out[0] = max|u| */
+int ell1_pd_split(int64_t n, int32_t split, const double* x, double* u, double* out, void* ws, void* stream);
+/* rp = b - Ax, rd = c - A_ext^T y - z (c NULL = ones); out4 = {|rp|^2, b.y, |rd|^2, c.x} */
+int ell1_pd_resid(int64_t d, int64_t n, int32_t split, const double* Ax, const double* b, const double* y,
+                  const double* Aty, const double* x, const double* z, const double* c, double* rp, double* rd,
+                  double* out4, void* ws, void* stream);
+/* rc = mu_hat - x z, w = x / z, wsum = w+ + w-, vd = (rc/z - w rd)+ - (...)- (pdipa.py:55-58, 150-153) */
+int ell1_pd_prep(int64_t n, int32_t split, const double* x, const double* z, const double* rd, double mu_hat,
+                 double* rc, double* w, double* wsum, double* vd, void* stream);
+/* dz = rd - A_ext^T dy, dx = rc / z - w dz; out4 = {min_{dx<0} -x/dx, min_{dz<0} -z/dz,
+ * any non-finite in dx, dz, dy, |z dx + x dz - rc|^2} (pdipa.py:35-40, 59-61, 86-92) */
+int ell1_pd_direction(int64_t n, int32_t split, int64_t d, const double* Atdy, const double* dy,
+                      const double* rd, const double* rc, const double* x, const double* z, const double* w,
+                      double* dx, double* dz, double* out4, void* ws, void* stream);
+/* out[0] = (x + ap dx) . (z + ad dz)   (pdipa.py:165-169) */
+int ell1_pd_mu(int64_t N2, const double* x, const double* dx, double ap, const double* z, const double* dz,
+               double ad, double* out, void* ws, void* stream);
+/* x += ap dx, z += ad dz, y += ad dy   (pdipa.py:176-179) */
+int ell1_pd_update(int64_t N2, int64_t d, double* x, const double* dx, double ap, double* z, const double* dz,
+                   double ad, double* y, const double* dy, void* stream);
+/* M[i][i] += alpha v[i] (v NULL: none), *trace = sum_i M[i][i]  (jitter, robust.py:148) */
+int ell1_pd_diag(int64_t d, int64_t ldm, double* M, double alpha, const double* v, double* trace, void* stream);
+
 /* fp32 GEMM path of the batched solvers (2: 3xTF32 split GEMMs on the tensor
  * pipe, opt-in with ELL1_FP32_GEMM=tf32x3; 0: SIMT SGEMM; -1: not used yet). */
 int ell1_blas_fp32_mode(void);

@@ -79,6 +79,9 @@ class Dense:
     def row_gram(self):                       # alm.py:164 (A @ A.T)
         return self.M @ self.M.T
 
+    def wgram(self, w):                       # operators.py:53-55
+        return (self.M * w) @ self.M.T
+
     def norm_sq(self):
         if self._nsq is None:
             self._nsq = power_norm_sq(self.M)
@@ -156,6 +159,12 @@ class Stacked:
         if self._nsq is None:
             self._nsq = power_norm_sq(self.M) + self.s ** 2
         return self._nsq
+
+    def wgram(self, w):                       # robust.py:145-149
+        d, n = self.M.shape
+        G = (self.M * w[:n]) @ self.M.T
+        G[np.diag_indices(d)] += self.s ** 2 * w[n:]
+        return G
 
 
 def as_op(A):
@@ -1121,6 +1130,130 @@ def homotopy(A, b, target, max_iter=5000, watch=None):
 
 
 # ----------------------------------------------------------------------------
+# PDIPA: primal-dual interior point on the split LP (pdipa.py:1-185)
+# ----------------------------------------------------------------------------
+
+PD_BOUNDARY = 0.99      # pdipa.py:19
+PD_SIGMA = 0.1          # pdipa.py:20
+PD_FEAS = 1e-8          # pdipa.py:21
+PD_GAP = 1e-6           # pdipa.py:22
+
+
+def pd_boundary(v, dv):
+    """Damped step to the boundary of v > 0 (pdipa.py:35-40)."""
+    neg = dv < 0
+    if not np.any(neg):
+        return 1.0
+    return min(1.0, PD_BOUNDARY * float(np.min(-v[neg] / dv[neg])))
+
+
+def pd_factor(M):
+    """Cholesky with one jitter retry (pdipa.py:43-52) -> upper factor."""
+    try:
+        return chol_upper(M)
+    except NotPD:
+        jit = 1e-12 * max(np.trace(M) / M.shape[0], 1.0)
+        try:
+            return chol_upper(M + jit * np.eye(M.shape[0]))
+        except NotPD as exc:
+            raise IllConditioned("weighted normal matrix is singular") from exc
+
+
+def pd_eliminate(x, z, rp, rd, rc, ext_mv, ext_rmv, M):
+    """Eliminate dz then dx (pdipa.py:55-62)."""
+    w = x / z
+    rhs = rp - ext_mv(rc / z - w * rd)
+    dy = chol_solve(pd_factor(M), rhs)
+    dz = rd - ext_rmv(dy)
+    dx = rc / z - w * dz
+    return dx, dy, dz
+
+
+def pd_newton(x, y, z, A_ext, b, mu_hat, c=None):
+    """Newton direction with the 1e-8 residual contract (pdipa.py:65-94)."""
+    A_ext = np.asarray(A_ext, dtype=np.float64)
+    if c is None:
+        c = np.ones(x.shape[0])
+    rp = b - A_ext @ x
+    rd = c - A_ext.T @ y - z
+    rc = mu_hat - x * z
+    M = (A_ext * (x / z)) @ A_ext.T
+    dx, dy, dz = pd_eliminate(x, z, rp, rd, rc, lambda u: A_ext @ u, lambda v: A_ext.T @ v, M)
+    scale = max(1.0, np.linalg.norm(rp), np.linalg.norm(rd), np.linalg.norm(rc))
+    ok = (np.linalg.norm(A_ext @ dx - rp) <= 1e-8 * scale
+          and np.linalg.norm(A_ext.T @ dy + dz - rd) <= 1e-8 * scale
+          and np.linalg.norm(z * dx + x * dz - rc) <= 1e-8 * scale)
+    if not ok or not (np.all(np.isfinite(dx)) and np.all(np.isfinite(dy)) and np.all(np.isfinite(dz))):
+        raise IllConditioned("Newton system residual did not close")
+    return dx, dy, dz
+
+
+def pdipa(A, b, tol=1e-6, max_iter=5000, stop=None, gt=None, watch=None):
+    """min ||x||_1 s.t. A x = b as the LP min 1'v, [A, -A] v = b, v >= 0
+    (pdipa.py:97-185).  Returns Outcome with x = v[:n] - v[n:]."""
+    op = as_op(A)
+    b = np.asarray(b, dtype=np.float64)
+    d, n = op.shape
+    if np.linalg.norm(b) == 0.0:
+        return Outcome(np.zeros(n), 0, True, [(0, 0.0, 0.0, 0)], ())
+    nn = 2 * n
+    c = np.ones(nn)
+    x = np.ones(nn)
+    y = np.zeros(d)
+    z = np.ones(nn)
+    mu = float(x @ z) / nn
+    b_scale = max(1.0, float(np.linalg.norm(b)))
+    c_scale = 1.0 + np.sqrt(nn)
+    gap_tol = min(tol, PD_GAP)
+    ext_mv = lambda u: op.mv(u[:n] - u[n:])
+    def ext_rmv(v):
+        t = op.rmv(v)
+        return np.concatenate([t, -t])
+    trace, notes = [], []
+    conv = False
+    it = 0
+    while it < max_iter:
+        rp = b - ext_mv(x)
+        rd = c - ext_rmv(y) - z
+        obj = float(c @ x)
+        gap = obj - float(b @ y)
+        trace.append((it, obj, float(np.linalg.norm(rp)), count_support(x[:n] - x[n:])))
+        if (np.linalg.norm(rp) <= PD_FEAS * b_scale and np.linalg.norm(rd) <= PD_FEAS * c_scale
+                and gap <= gap_tol * (1.0 + abs(obj))):
+            conv = True
+            break
+        it += 1
+        rc = PD_SIGMA * mu - x * z
+        w = x / z
+        M = op.wgram(w[:n] + w[n:])
+        try:
+            dx, dy, dz = pd_eliminate(x, z, rp, rd, rc, ext_mv, ext_rmv, M)
+        except IllConditioned:
+            notes.append("stopped on ill-conditioned normal matrix")
+            break
+        if not (np.all(np.isfinite(dx)) and np.all(np.isfinite(dy)) and np.all(np.isfinite(dz))):
+            notes.append("stopped on non-finite step")
+            break
+        ap = pd_boundary(x, dx)
+        ad = pd_boundary(z, dz)
+        for _ in range(40):
+            xn = x + ap * dx
+            zn = z + ad * dz
+            mun = float(xn @ zn) / nn
+            if mun < mu:
+                break
+            ap *= 0.5
+            ad *= 0.5
+        else:
+            notes.append("stopped on stalled duality measure")
+            break
+        x, y, z, mu = xn, y + ad * dy, zn, mun
+        if watch is not None:
+            watch(x.copy(), y.copy(), z.copy(), mu)
+    return Outcome(x[:n] - x[n:], it, conv, trace, tuple(notes))
+
+
+# ----------------------------------------------------------------------------
 # CAB router (robust.py:181-220) for the first-order backends
 # ----------------------------------------------------------------------------
 
@@ -1151,6 +1284,8 @@ def cab(A, b, solver, lam=None, tol=1e-6, max_iter=5000, stop=None, opts=None):
         res = gpsr(op, b, lam=lam_r, **kw)
     elif solver == "homotopy":
         res, _ = homotopy(op, b, lam_r, max_iter=max_iter)
+    elif solver == "pdipa":
+        res = pdipa(op, b, **kw)
     else:
         raise ValueError("unknown cab backend %r" % (solver,))
     w = res.x

@@ -172,6 +172,20 @@ _SIGS = {
                                       ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "ell1_shard_resid": (ctypes.c_int, [ctypes.c_int64] + [ctypes.c_void_p] * 3 + [ctypes.c_double] +
                          [ctypes.c_void_p] * 4),
+    "ell1_pd_workspace": (ctypes.c_size_t, []),
+    "ell1_pd_split": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32] + [ctypes.c_void_p] * 5),
+    "ell1_pd_resid": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32] + [ctypes.c_void_p] * 12),
+    "ell1_pd_prep": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32] + [ctypes.c_void_p] * 3 + [ctypes.c_double]
+                     + [ctypes.c_void_p] * 5),
+    "ell1_pd_direction": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int64] + [ctypes.c_void_p] * 12),
+    "ell1_pd_mu": (ctypes.c_int, [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
+                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_void_p,
+                                  ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_pd_update": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                      ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
+                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_pd_diag": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_double,
+                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "ell1_blas_fp32_mode": (ctypes.c_int, []),
     "ell1_device_sms": (ctypes.c_int, [ctypes.c_int32]),
     "ell1_version": (ctypes.c_char_p, []),

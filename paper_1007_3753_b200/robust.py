@@ -226,7 +226,8 @@ def cab_solve(A, b, solver, config):
     elif solver == "homotopy":
         from paper_1007_3753_b200.homotopy import solve_path
         res, _ = solve_path(ext, prob.b, _resolved_lambda(config, prob), config)
-    else:
-        raise NotImplementedError("pdipa is outside the B200 hot path (SURVEY §8(f) rank 1)")
+    else:                                                   # "pdipa" (robust.py:204-205)
+        from paper_1007_3753_b200.pdipa import pdipa_solve
+        res = pdipa_solve(prob, config)
     w = res.x_star
     return w[:n], scale * w[n:], res

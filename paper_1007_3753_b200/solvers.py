@@ -1,11 +1,10 @@
 """Name-based dispatch used by the reference's callers (ell1.bench.solve_named,
-bench.py:31-62): one problem to a solver family by name, "gp" = "gpsr".
-Every family except PDIPA runs on the B200 path; PDIPA is SURVEY §8(f) rank 1
-(not yet built) and raises NotImplementedError rather than falling back."""
+bench.py:31-62): one problem to a solver family by name, "gp" = "gpsr"."""
 
 from paper_1007_3753_b200.alm import dalm_solve, palm_solve
 from paper_1007_3753_b200.gradient_projection import gpsr_solve, tnipm_solve
 from paper_1007_3753_b200.homotopy import homotopy_solve
+from paper_1007_3753_b200.pdipa import pdipa_solve
 from paper_1007_3753_b200.shrinkage import fista_solve, ist_solve
 
 SOLVER_NAMES = ("pdipa", "homotopy", "gpsr", "tnipm", "ist", "fista", "palm", "dalm")
@@ -16,7 +15,7 @@ def solve_named(name, P, config):
     if name == "gp":
         name = "gpsr"
     if name == "pdipa":
-        raise NotImplementedError("pdipa has no B200 implementation yet (SURVEY §8(f) rank 1)")
+        return pdipa_solve(P, config)
     if name == "homotopy":
         return homotopy_solve(P, config.resolved_lambda(P), config)
     if name == "gpsr":

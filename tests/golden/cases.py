@@ -81,6 +81,13 @@ for s in (1300, 1301):
     _add("homotopy_small_%d" % s, _gs(40, 20, 3, s, 0.02), "homotopy",
          dict(lam_rel=0.01))
 
+# ---- PDIPA: equality-constrained interior point -------
+for s in (1600, 1601, 1602):
+    _add("pdipa_small_%d" % s, _gs(40, 20, 1 + s % 4, s, 0.0), "pdipa", dict(tol=1e-6))
+_add("pdipa_small_noisy", _gs(60, 30, 4, 1603, 0.02), "pdipa", dict(tol=1e-8))
+_add("pdipa_small_budget", _gs(40, 20, 3, 1604, 0.0), "pdipa", dict(max_iter=2))
+_add("pdipa_qr", dict(kind="qr", d=8, seed=33), "pdipa", dict(tol=1e-9))
+
 # ---- BASELINE config 1: 500 x 1000, k=50, noiseless, lambda 1e-3, rel-est --
 _add("cfg1_fista", _wl(500, 1000, 50), "fista",
      dict(lam=1e-3, tol=1e-6, stopping=REL), size="cfg1")
@@ -90,6 +97,7 @@ _add("cfg1_dalm", _wl(500, 1000, 50), "dalm",
      dict(tol=1e-6, stopping=REL), size="cfg1")
 _add("cfg1_dalm_native", _wl(500, 1000, 50), "dalm",
      dict(tol=1e-6), size="cfg1")
+_add("cfg1_pdipa", _wl(500, 1000, 50), "pdipa", dict(tol=1e-6), size="cfg1")
 
 # ---- BASELINE config 2: 1024 x 4096, k=128, 1% noise, default lambda -------
 _cfg2 = _wl(1024, 4096, 128, 0, 0.01)
@@ -101,6 +109,7 @@ _add("cfg2_tnipm", _cfg2, "tnipm", dict(tol=1e-6, stopping=REL), size="cfg2")
 _add("cfg2_homotopy", _cfg2, "homotopy", dict(), size="cfg2")
 _add("cfg2_palm", _cfg2, "palm", dict(tol=1e-6, stopping=REL), size="cfg2")
 _add("cfg2_dalm_budget", _cfg2, "dalm", dict(tol=1e-6, max_iter=200), size="cfg2")
+_add("cfg2_pdipa", _cfg2, "pdipa", dict(tol=1e-6), size="cfg2")
 
 # ---- config-5 shape: 512 x 2048, lambda 1e-3 -------------------------------
 for k in (16, 64):
@@ -112,7 +121,7 @@ for k in (16, 64):
          dict(lam=1e-3), size="cfg5")
 
 # ---- CAB ([A, I]) small ----------------------------------------------------
-for solver in ("dalm", "fista"):
+for solver in ("dalm", "fista", "pdipa"):
     _add("cab_small_%s" % solver, dict(kind="cab", d=40, n=30, k=3, seed=7, m=4),
          "cab:" + solver, dict(tol=1e-6, max_iter=5000))
 

@@ -27,7 +27,7 @@ from tests.golden.cases import CASES, build_inputs, resolve_lambda  # noqa: E402
 
 def run_reference(case):
     import ell1
-    from ell1 import alm, gradient_projection, homotopy, robust, shrinkage
+    from ell1 import alm, gradient_projection, homotopy, pdipa, robust, shrinkage
     from ell1.model import ProblemInstance, SolverConfig, StoppingRule
 
     assert ell1.kernels_compiled, "build the reference's _accel first"
@@ -66,6 +66,8 @@ def run_reference(case):
             target = lam if lam is not None else config.resolved_lambda(P)
             extra["target"] = target
             res = homotopy.homotopy_solve(P, target, config)
+        elif solver == "pdipa":
+            res = pdipa.pdipa_solve(P, config)
         else:
             raise ValueError(solver)
         x = res.x_star

@@ -37,6 +37,8 @@ def run_oracle(case):
     elif s == "homotopy":
         target = lam if lam is not None else 1e-2 * float(np.max(np.abs(A.T @ b)))
         res, _ = oracle.homotopy(A, b, target, max_iter=kw["max_iter"])
+    elif s == "pdipa":
+        res = oracle.pdipa(A, b, gt=gt, **kw)
     else:
         raise ValueError(s)
     return res, res.x, extra

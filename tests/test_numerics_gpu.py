@@ -241,10 +241,7 @@ def test_solve_named_dispatch():
     g = solve_named("gp", P, cfg)
     assert g.iterations == gpsr_solve(P, 1e-2, cfg).iterations
     for name in SOLVER_NAMES:
-        if name != "pdipa":
-            r = solve_named(name, P, cfg)
-            assert r.x_star.shape == (60,)
+        r = solve_named(name, P, cfg)
+        assert r.x_star.shape == (60,)
     with pytest.raises(ValueError):
         solve_named("nope", P, cfg)
-    with pytest.raises(NotImplementedError):
-        solve_named("pdipa", P, cfg)
