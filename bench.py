@@ -43,7 +43,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-stream", action="store_true", help="skip the HBM streaming roofline leg")
     ap.add_argument("--no-secondary", action="store_true",
-                    help="skip the config 3/4/5 and all-solver legs")
+                    help="skip the config 1/3/4/5 and all-solver legs")
+    ap.add_argument("--cfg5-sweep", action="store_true", help="add the config-5 batch-size sweep leg")
     return ap.parse_args()
 
 
@@ -428,6 +429,84 @@ def leg_cfg5(torch, dev, ws=1, B=1024, cpu_sample=8):
     return out
 
 
+def leg_cfg1(torch, reps=5):
+    """BASELINE config 1 (configs[0], the reference's CPU-runnable case):
+    d=500, n=1000, k=50 noiseless, fp64; FISTA / PALM / DALM at lambda 1e-3,
+    relative change in x < 1e-6; solves/s next to the CPU port."""
+    from paper_1007_3753_b200 import device as dv, synth
+    from paper_1007_3753_b200.alm import dalm_solve, palm_solve
+    from paper_1007_3753_b200.model import ProblemInstance, SolverConfig, StoppingRule
+    from paper_1007_3753_b200.shrinkage import fista_solve
+    import oracle
+    P = synth.make_problem(synth.CFG1)
+    D = dv.DeviceDictionary(P.A)
+    Pd = ProblemInstance.__new__(ProblemInstance)
+    Pd.A, Pd.b, Pd.ground_truth, Pd.noise_sigma = D, P.b, P.ground_truth, P.noise_sigma
+    rel = StoppingRule("relative-estimate", 1e-6)
+    out = {"workload": "cfg1: d=500 n=1000 k=50 noiseless fp64, lambda 1e-3, relative change in x < 1e-6"}
+    legs = {"fista": (lambda: fista_solve(Pd, SolverConfig(lam=1e-3, tol=1e-6, stopping=rel)),
+                      lambda: oracle.fista(P.A, P.b, lam=1e-3, tol=1e-6, stop=("relative-estimate", 1e-6))),
+            "palm": (lambda: palm_solve(Pd, SolverConfig(tol=1e-6, stopping=rel)),
+                     lambda: oracle.palm(P.A, P.b, tol=1e-6, stop=("relative-estimate", 1e-6))),
+            "dalm": (lambda: dalm_solve(Pd, SolverConfig(tol=1e-6, stopping=rel)),
+                     lambda: oracle.dalm(P.A, P.b, tol=1e-6, stop=("relative-estimate", 1e-6)))}
+    for name, (gpu, cpu) in legs.items():
+        r = gpu()
+        torch.cuda.synchronize()
+        s, e = _events(torch)
+        s.record()
+        for _ in range(reps):
+            r = gpu()
+        e.record()
+        torch.cuda.synchronize()
+        t = s.elapsed_time(e) / 1e3 / reps
+        t0 = time.perf_counter()
+        rc = cpu()
+        tc = time.perf_counter() - t0
+        err = float(np.linalg.norm(r.x_star - rc.x) / max(np.linalg.norm(rc.x), 1e-300))
+        out[name] = {"solves_per_sec": 1.0 / t, "ms_per_solve": 1e3 * t, "iterations": int(r.iterations),
+                     "cpu_port_solves_per_sec": 1.0 / tc, "cpu_iterations": int(rc.iterations),
+                     "rel_err_vs_oracle": err}
+    out["cpu_cores"] = os.cpu_count()
+    return out
+
+
+def leg_cfg5_sweep(torch, dev, sizes=(1, 16, 256, 1024, 8192)):
+    """BASELINE config 5 batch-size sweep (FISTA fp64 and fp32, Homotopy fp64)."""
+    from paper_1007_3753_b200 import synth
+    from paper_1007_3753_b200 import device as dv
+    from paper_1007_3753_b200.batched import fista_solve_batch, homotopy_solve_batch
+    from paper_1007_3753_b200.model import SolverConfig, StoppingRule
+    d, n = 512, 2048
+    A = synth.gen_gaussian_dict(d, n, 5)
+    rng = np.random.default_rng(55)
+    Bmax = max(sizes)
+    X = np.zeros((n, Bmax))
+    for j in range(Bmax):
+        kk = int(rng.integers(16, 257))
+        X[rng.choice(n, kk, replace=False), j] = rng.standard_normal(kk)
+    Bmat = A @ X
+    rel = StoppingRule("relative-estimate", 1e-6)
+    D64 = dv.DeviceDictionary(A, dtype="float64", device=dev.index)
+    D32 = dv.DeviceDictionary(A, dtype="float32", device=dev.index)
+    rows = []
+    for B in sizes:
+        row = {"B": B}
+        for name, fn in (("fista_f64", lambda Bm: fista_solve_batch(D64, Bm, SolverConfig(lam=1e-3, stopping=rel))),
+                         ("fista_f32", lambda Bm: fista_solve_batch(D32, Bm, SolverConfig(lam=1e-3, stopping=rel))),
+                         ("homotopy_f64", lambda Bm: homotopy_solve_batch(D64, Bm, 1e-3, SolverConfig()))):
+            s, e = _events(torch)
+            torch.cuda.synchronize()
+            s.record()
+            r = fn(np.ascontiguousarray(Bmat[:, :B]))
+            e.record()
+            torch.cuda.synchronize()
+            t = s.elapsed_time(e) / 1e3
+            row[name] = {"solves_per_sec": B / t, "iterations_per_sec": float(r.iterations.sum()) / t}
+        rows.append(row)
+    return {"workload": "cfg5 sweep: shared A 512 x 2048, k~U[16,256], lambda 1e-3", "rows": rows}
+
+
 def leg_solvers_cfg2(torch, P, reps=3):
     """Every single-instance solver on the cfg2 instance (ms per solve)."""
     from paper_1007_3753_b200 import device as dv
@@ -605,9 +684,13 @@ def run_b200(args):
                 out["roofline_stream"] = {"error": str(exc)[:200]}
         if not args.no_secondary and ws == 1:
             sec = {}
-            for name, fn in (("solvers_cfg2", lambda: leg_solvers_cfg2(torch, P)),
-                             ("cfg3", lambda: leg_cfg3(torch, dev)),
-                             ("cfg5", lambda: leg_cfg5(torch, dev, ws))):
+            legs2 = [("cfg1", lambda: leg_cfg1(torch))]
+            if args.cfg5_sweep:
+                legs2.append(("cfg5_sweep", lambda: leg_cfg5_sweep(torch, dev)))
+            legs2 += [("solvers_cfg2", lambda: leg_solvers_cfg2(torch, P)),
+                      ("cfg3", lambda: leg_cfg3(torch, dev)),
+                      ("cfg5", lambda: leg_cfg5(torch, dev, ws))]
+            for name, fn in legs2:
                 try:
                     sec[name] = fn()
                 except Exception as exc:  # pragma: no cover - best effort leg

@@ -127,6 +127,63 @@ def _collect(bufs, t0, dev, trace_offset=0):
     return res
 
 
+SMALL_B = 4     # below this, one persistent single-instance launch per column wins
+
+
+def _ncols(Bmat):
+    shape = getattr(Bmat, "shape", None)
+    if shape is None:
+        shape = np.shape(Bmat)
+    return int(shape[1]) if len(shape) == 2 else None
+
+
+def _small_batch(kind, A, Bmat, config, with_trace, target=None):
+    """Batches of a few instances run as consecutive single-instance solves
+    (each one persistent launch) — the batched round loop is launch-bound at
+    tiny B.  Same semantics: element j is the single-instance call."""
+    from paper_1007_3753_b200 import homotopy as hom
+    from paper_1007_3753_b200.alm import dalm_solve
+    from paper_1007_3753_b200.model import ProblemInstance
+    from paper_1007_3753_b200.shrinkage import fista_solve
+    t0 = time.perf_counter()
+    if hasattr(Bmat, "detach"):
+        Bmat = Bmat.detach().cpu().numpy()
+    Bmat = np.asarray(Bmat, dtype=np.float64)
+    B = Bmat.shape[1]
+    D, view, N = _dict_view(A, config)
+    xs, its, conv, stat, lams, notes, traces = [], [], [], [], [], [], []
+    for j in range(B):
+        P = ProblemInstance.__new__(ProblemInstance)
+        P.A, P.b, P.ground_truth, P.noise_sigma = A if hasattr(A, "device_extension") else D, \
+            np.ascontiguousarray(Bmat[:, j]), None, None
+        if kind == "fista":
+            r = fista_solve(P, config)
+        elif kind == "dalm":
+            r = dalm_solve(P, config)
+        else:
+            r, lam = hom.solve_path(P.A, P.b, target, config)
+            lams.append(lam)
+        xs.append(r.x_star)
+        its.append(r.iterations)
+        conv.append(int(r.converged))
+        zero = len(r.trace) and r.iterations == 0 and r.converged
+        stat.append(_lib.ZERO_DATA if zero else _lib.OK)
+        notes.append(1 if r.notes and "ridge-regularized gram" in r.notes else 0)
+        traces.append(np.array([tuple(t) for t in r.trace], dtype=np.float64).reshape(-1, 4))
+    tr = None
+    if with_trace:
+        rows = max(int(config.max_iter), 1) + (1 if kind == "dalm" else 0)
+        tr = np.zeros((B, rows, 4))
+        for j, t in enumerate(traces):
+            tr[j, : t.shape[0]] = t[:rows]
+    res = BatchResult(np.stack(xs, axis=1), np.array(its, np.int32), np.array(conv, np.int32),
+                      np.array(stat, np.int32), time.perf_counter() - t0, tr, kind, config.max_iter)
+    if kind == "homotopy":
+        res.lam = np.array(lams)
+        res.notes = np.array(notes, np.int32)
+    return res
+
+
 def src_classify(A, class_labels, Bmat, config):
     """Cross-and-bouquet SRC (BASELINE config 3): solve every query on
     [A, I/e_weight] with the batched dual ALM (robust.cab_solve semantics,
@@ -166,6 +223,8 @@ def dalm_solve_batch(A, Bmat, config, with_trace=False):
     """Dual ALM for every column of Bmat (d x B) against the shared A (or a
     robust.ExtendedDictionary for CAB batches).  Element j equals
     alm.dalm_solve on (A, b_j); option beta as in the reference."""
+    if (_ncols(Bmat) or SMALL_B) < SMALL_B:
+        return _small_batch("dalm", A, Bmat, config, with_trace)
     t0 = time.perf_counter()
     D, view, N = _dict_view(A, config)
     ext = bool(view.ext)
@@ -200,6 +259,8 @@ def dalm_solve_batch(A, Bmat, config, with_trace=False):
 def fista_solve_batch(A, Bmat, config, with_trace=False):
     """FISTA for every column of Bmat (d x B) against the shared A.
     Returns a BatchResult; ``.results()`` gives per-instance SolverResults."""
+    if (_ncols(Bmat) or SMALL_B) < SMALL_B:
+        return _small_batch("fista", A, Bmat, config, with_trace)
     torch = device._torch()
     t0 = time.perf_counter()
     D, view, N = _dict_view(A, config)
@@ -248,9 +309,11 @@ def homotopy_solve_batch(A, Bmat, target_lambda, config, with_trace=False):
     torch = device._torch()
     if target_lambda < 0:
         raise ValueError("target lambda must be nonnegative")
-    t0 = time.perf_counter()
     if hasattr(A, "device_extension"):
         raise NotImplementedError("batched Homotopy runs on plain dictionaries")
+    if (_ncols(Bmat) or SMALL_B) < SMALL_B:
+        return _small_batch("homotopy", A, Bmat, config, with_trace, target=float(target_lambda))
+    t0 = time.perf_counter()
     D, view, N = _dict_view(A, config)
     dev = D.device
     Bpad, B = _upload_rhs(Bmat, D)

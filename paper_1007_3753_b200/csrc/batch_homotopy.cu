@@ -25,6 +25,31 @@
 
 namespace ell1 {
 
+// Threads per instance CTA.  Measured at config 5 (B=256): 512 beats 128 —
+// the row / column sweeps of an instance dominate its dependent chains, and
+// two 512-thread CTAs per SM already hold every instance of a 296-wide wave.
+constexpr int HBT = 512;
+constexpr int HBW = HBT / 32;
+
+// fixed-order CTA reduction of K values (sum / max by mask); all threads get them
+template <int K>
+__device__ __forceinline__ void hb_reduce(double (&v)[K], unsigned maxmask, double* sh) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = ((maxmask >> k) & 1u) ? warp_max(v[k]) : warp_sum(v[k]);
+  if (lnx() == 0)
+#pragma unroll
+    for (int k = 0; k < K; ++k) sh[wpx() * K + k] = v[k];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const bool mx = (maxmask >> k) & 1u;
+    double s = sh[k];
+    for (int w = 1; w < HBW; ++w) s = mx ? nmax(s, sh[w * K + k]) : s + sh[w * K + k];
+    v[k] = s;
+  }
+  __syncthreads();
+}
+
 struct HI {                 // per-instance state (instance-indexed)
   double lam, lam0, floor, gamma, rr, l1, top, cnt;
   int it, m, status, conv, note, done, ridge, pend, redo, finish;
@@ -70,7 +95,7 @@ __device__ void cta_argmin(double& v, int& i, double* shv, int* shi) {
   if (lnx() == 0) { shv[wpx()] = v; shi[wpx()] = i; }
   __syncthreads();
   v = shv[0]; i = shi[0];
-  for (int w = 1; w < NWARP; ++w) argmin_pair(v, i, shv[w], shi[w]);
+  for (int w = 1; w < HBW; ++w) argmin_pair(v, i, shv[w], shi[w]);
   __syncthreads();
 }
 
@@ -81,7 +106,7 @@ __device__ bool gram_chol(const HB& a, const int* sup, int m, double shift, doub
                           double* row, double* sc) {
   for (int k = 0; k < m; ++k) {
     const double* ak = a.A + (int64_t)sup[k] * a.ld;
-    for (int j = k + wpx(); j < m; j += NWARP) {
+    for (int j = k + wpx(); j < m; j += HBW) {
       const double* aj = a.A + (int64_t)sup[j] * a.ld;
       double acc = 0.0;
       for (int64_t i = lnx(); i < a.d; i += 32) acc = fma(ak[i], aj[i], acc);
@@ -97,7 +122,7 @@ __device__ bool gram_chol(const HB& a, const int* sup, int m, double shift, doub
     __syncthreads();
     if (!(sc[0] > 0.0)) return false;
     const double rkk = sqrt(sc[0]);
-    for (int j = k + tix(); j < m; j += NTHR) {
+    for (int j = k + tix(); j < m; j += HBT) {
       if (j == k) { R[(size_t)k * ldr + k] = rkk; continue; }
       double s = row[j];
       for (int i = 0; i < k; ++i) s -= R[(size_t)i * ldr + k] * R[(size_t)i * ldr + j];
@@ -109,10 +134,9 @@ __device__ bool gram_chol(const HB& a, const int* sup, int m, double shift, doub
 }
 
 // ridge factor (homotopy.py:118-125): G + 1e-12 max(tr G, 1) I
-__device__ bool ridge_chol(const HB& a, const int* sup, int m, double* R, int ldr, double* row, double* sc,
-                           Ctx& E) {
+__device__ bool ridge_chol(const HB& a, const int* sup, int m, double* R, int ldr, double* row, double* sc) {
   double tr[1] = {0.0};
-  for (int p = wpx(); p < m; p += NWARP) {
+  for (int p = wpx(); p < m; p += HBW) {
     const double* ap = a.A + (int64_t)sup[p] * a.ld;
     double acc = 0.0;
     for (int64_t i = lnx(); i < a.d; i += 32) acc = fma(ap[i], ap[i], acc);
@@ -126,7 +150,7 @@ __device__ bool ridge_chol(const HB& a, const int* sup, int m, double* R, int ld
     sc[3] = 1e-12 * pymax(t, 1.0);
   }
   __syncthreads();
-  (void)tr; (void)E;
+  (void)tr;
   return gram_chol(a, sup, m, sc[3], R, ldr, row, sc);
 }
 
@@ -148,15 +172,12 @@ __device__ __forceinline__ double sup_dot(const double* A, int64_t ld, const int
 }
 
 // ---- setup: lambda0, first atom (homotopy.py:142-177); C holds A^T b (slot = instance)
-__global__ void __launch_bounds__(NTHR) hb_init(HB a, int B) {
+__global__ void __launch_bounds__(HBT) hb_init(HB a, int B) {
   const int j = blockIdx.x;
   if (j >= B) return;
-  __shared__ Ctx E;
-  __shared__ double sh[NWARP * 4 + 8];
-  __shared__ double shv[NWARP];
-  __shared__ int shi[NWARP];
-  T0 E.sh = sh;
-  __syncthreads();
+  __shared__ double sh[HBW * 4 + 8];
+  __shared__ double shv[HBW];
+  __shared__ int shi[HBW];
   HI& S = a.st[j];
   const double* c = a.C + (int64_t)j * a.n;
   double* X = a.X + (int64_t)j * a.n;
@@ -164,17 +185,17 @@ __global__ void __launch_bounds__(NTHR) hb_init(HB a, int B) {
   int* pos = a.posof + (int64_t)j * a.n;
   const double* b = a.Bm + (int64_t)j * a.ld;
   double v[2] = {0.0, 0.0};
-  for (int64_t k = tix(); k < a.n; k += NTHR) {
+  for (int64_t k = tix(); k < a.n; k += HBT) {
     const double ck = c[k];
     Ci[k] = ck; X[k] = 0.0; pos[k] = -1;
     v[0] = nmax(v[0], fabs(ck));
   }
-  for (int64_t i = tix(); i < a.d; i += NTHR) v[1] += b[i] * b[i];
-  block_reduce<2>(E, v, 1u);
+  for (int64_t i = tix(); i < a.d; i += HBT) v[1] += b[i] * b[i];
+  hb_reduce<2>(v, 1u, sh);
   const double lam0 = v[0];
   double bv = INFINITY;
   int bi = 0x7fffffff;
-  for (int64_t k = tix(); k < a.n; k += NTHR)
+  for (int64_t k = tix(); k < a.n; k += HBT)
     if (fabs(c[k]) == lam0) argmin_pair(bv, bi, 0.0, (int)k);
   cta_argmin(bv, bi, shv, shi);
   const double bn = sqrt(v[1]);
@@ -193,8 +214,8 @@ __global__ void __launch_bounds__(NTHR) hb_init(HB a, int B) {
   // first atom: R = [||a_j0||]
   const double* col = a.A + (int64_t)bi * a.ld;
   double q[1] = {0.0};
-  for (int64_t i = tix(); i < a.d; i += NTHR) q[0] += col[i] * col[i];
-  block_reduce<1>(E, q, 0u);
+  for (int64_t i = tix(); i < a.d; i += HBT) q[0] += col[i] * col[i];
+  hb_reduce<1>(q, 0u, sh);
   T0 {
     S.lam = lam0; S.lam0 = lam0; S.floor = pymax(a.target, 1e-12 * lam0);
     S.it = 0; S.m = 1; S.conv = 0; S.done = 0; S.note = 0; S.pend = 0; S.redo = 0; S.ridge = 0;
@@ -208,15 +229,12 @@ __global__ void __launch_bounds__(NTHR) hb_init(HB a, int B) {
 }
 
 // ---- finalise the previous breakpoint, then the direction of the next one
-__global__ void __launch_bounds__(NTHR) hb_dir(HB a, int nact) {
+__global__ void __launch_bounds__(HBT) hb_dir(HB a, int nact) {
   const int s = blockIdx.x;
   if (s >= nact) return;
   extern __shared__ __align__(16) double dsm[];
-  __shared__ Ctx E;
-  __shared__ double sh[NWARP * 4 + 8];
+  __shared__ double sh[HBW * 4 + 8];
   __shared__ int flag;
-  T0 E.sh = sh;
-  __syncthreads();
   const int j = a.act[s];
   HI& S = a.st[j];
   const int ldr = a.mmax;
@@ -228,12 +246,12 @@ __global__ void __launch_bounds__(NTHR) hb_dir(HB a, int nact) {
     // fresh correlations (homotopy.py:224-234)
     const double* c = a.C + (int64_t)s * a.n;
     double v[1] = {0.0};
-    for (int64_t k = tix(); k < a.n; k += NTHR) {
+    for (int64_t k = tix(); k < a.n; k += HBT) {
       const double ck = c[k];
       Ci[k] = ck;
       v[0] = nmax(v[0], fabs(ck));
     }
-    block_reduce<1>(E, v, 1u);
+    hb_reduce<1>(v, 1u, sh);
     T0 {
       double lam;
       if (S.finish) lam = a.target;
@@ -263,20 +281,20 @@ __global__ void __launch_bounds__(NTHR) hb_dir(HB a, int nact) {
   }
   __syncthreads();
   if (flag) {
-    for (int64_t i = tix(); i < a.ld; i += NTHR) Vs[i] = 0.0;
+    for (int64_t i = tix(); i < a.ld; i += HBT) Vs[i] = 0.0;
     return;
   }
   const int m = S.m;
   const int* sup = a.sup + (size_t)j * a.mmax;
   const double* R = a.R + (size_t)j * a.mmax * a.mmax;
   double* dI = a.dI + (size_t)j * a.mmax;
-  for (int p = tix(); p < m; p += NTHR) zs[p] = sgn(Ci[sup[p]]);
+  for (int p = tix(); p < m; p += HBT) zs[p] = sgn(Ci[sup[p]]);
   __syncthreads();
-  trsv_RT(R, ldr, m, zs, tile);
-  trsv_R(R, ldr, m, zs, tile);
-  for (int p = tix(); p < m; p += NTHR) dI[p] = zs[p];
+  trsv_RT<HBT>(R, ldr, m, zs, tile);
+  trsv_R<HBT>(R, ldr, m, zs, tile);
+  for (int p = tix(); p < m; p += HBT) dI[p] = zs[p];
   // v = A_I d_I (rows over threads, support columns in order)
-  for (int64_t i = tix(); i < a.ld; i += NTHR) {
+  for (int64_t i = tix(); i < a.ld; i += HBT) {
     double acc = 0.0;
     if (i < a.d)
       acc = sup_dot(a.A, a.ld, sup, m, i, zs);
@@ -285,18 +303,15 @@ __global__ void __launch_bounds__(NTHR) hb_dir(HB a, int nact) {
 }
 
 // ---- drift check, step lengths, event, factor update, residual
-__global__ void __launch_bounds__(NTHR) hb_step(HB a, int nact) {
+__global__ void __launch_bounds__(HBT) hb_step(HB a, int nact) {
   const int s = blockIdx.x;
   if (s >= nact) return;
   extern __shared__ __align__(16) double dsm[];
-  __shared__ Ctx E;
-  __shared__ double sh[NWARP * 8 + 16];
-  __shared__ double shv[NWARP];
-  __shared__ int shi[NWARP];
+  __shared__ double sh[HBW * 8 + 16];
+  __shared__ double shv[HBW];
+  __shared__ int shi[HBW];
   __shared__ double sc[4];
   __shared__ int dec[4];               // 0: refactor, 1: event(0 add / 1 remove / 2 finish), 2: ip, 3: im
-  T0 E.sh = sh;
-  __syncthreads();
   const int j = a.act[s];
   HI& S = a.st[j];
   const int ldr = a.mmax;
@@ -313,7 +328,7 @@ __global__ void __launch_bounds__(NTHR) hb_step(HB a, int nact) {
   const double* dI = a.dI + (size_t)j * a.mmax;
   const double* b = a.Bm + (int64_t)j * a.ld;
   if (S.done) {
-    for (int64_t i = tix(); i < a.ld; i += NTHR) Rs[i] = 0.0;
+    for (int64_t i = tix(); i < a.ld; i += HBT) Rs[i] = 0.0;
     return;
   }
   const int m = S.m;
@@ -321,13 +336,13 @@ __global__ void __launch_bounds__(NTHR) hb_step(HB a, int nact) {
   // drift ||w_I - sgn||, ||sgn|| (homotopy.py:48-52; w_I == A_I^T v)
   {
     double q[2] = {0.0, 0.0};
-    for (int p = tix(); p < m; p += NTHR) {
+    for (int p = tix(); p < m; p += HBT) {
       const double sg = sgn(Ci[sup[p]]);
       const double e = w[sup[p]] - sg;
       q[0] += e * e;
       q[1] += sg * sg;
     }
-    block_reduce<2>(E, q, 0u);
+    hb_reduce<2>(q, 0u, sh);
     T0 {
       const double tol = 1e-6 * pymax(1.0, sqrt(q[1]));
       dec[0] = (!(sqrt(q[0]) <= tol) && S.ridge != 2) ? 1 : 0;
@@ -341,14 +356,14 @@ __global__ void __launch_bounds__(NTHR) hb_step(HB a, int nact) {
     if (ok) {
       T0 S.ridge = 1;
     } else {
-      const bool ok2 = ridge_chol(a, sup, m, R, ldr, row, sc, E);
+      const bool ok2 = ridge_chol(a, sup, m, R, ldr, row, sc);
       T0 {
         S.ridge = 2; S.note = 1;
         if (!ok2) { S.status = ELL1_NOT_PD; S.done = 1; }
       }
     }
     T0 S.redo = 1;
-    for (int64_t i = tix(); i < a.ld; i += NTHR) Rs[i] = 0.0;
+    for (int64_t i = tix(); i < a.ld; i += HBT) Rs[i] = 0.0;
     return;
   }
   // step lengths (homotopy.py:78-105): gamma+ over the inactive set, gamma- over the support
@@ -356,7 +371,7 @@ __global__ void __launch_bounds__(NTHR) hb_step(HB a, int nact) {
     const double floor = 1e-10 * pymax(lam, 1e-30);
     double v1 = INFINITY, v2 = INFINITY, vm = INFINITY;
     int i1 = 0x7fffffff, i2 = 0x7fffffff, im = 0x7fffffff;
-    for (int64_t k = tix(); k < a.n; k += NTHR) {
+    for (int64_t k = tix(); k < a.n; k += HBT) {
       const int p = pos[k];
       const double wk = w[k];
       if (p >= 0) {
@@ -395,7 +410,7 @@ __global__ void __launch_bounds__(NTHR) hb_step(HB a, int nact) {
   }
   const double gamma = sc[0];
   const int ev = dec[1];
-  for (int p = tix(); p < m; p += NTHR) X[sup[p]] = X[sup[p]] + gamma * dI[p];
+  for (int p = tix(); p < m; p += HBT) X[sup[p]] = X[sup[p]] + gamma * dI[p];
   __syncthreads();
   int mn = m;
   if (ev == 1) {
@@ -404,16 +419,16 @@ __global__ void __launch_bounds__(NTHR) hb_step(HB a, int nact) {
     const int p0 = pos[im];
     T0 X[im] = 0.0;
     for (int i = 0; i < p0; ++i) {                         // rows above: shift columns > p0 left
-      for (int jj = p0 + 1 + tix(); jj < m; jj += NTHR) row[jj] = R[(size_t)i * ldr + jj];
+      for (int jj = p0 + 1 + tix(); jj < m; jj += HBT) row[jj] = R[(size_t)i * ldr + jj];
       __syncthreads();
-      for (int jj = p0 + 1 + tix(); jj < m; jj += NTHR) R[(size_t)i * ldr + jj - 1] = row[jj];
+      for (int jj = p0 + 1 + tix(); jj < m; jj += HBT) R[(size_t)i * ldr + jj - 1] = row[jj];
       __syncthreads();
     }
     if (p0 < m - 1) {
       const int mt = m - p0 - 1;
-      for (int jj = tix(); jj < mt; jj += NTHR) zs[jj] = R[(size_t)p0 * ldr + p0 + 1 + jj];
+      for (int jj = tix(); jj < mt; jj += HBT) zs[jj] = R[(size_t)p0 * ldr + p0 + 1 + jj];
       __syncthreads();
-      chol_update_shift(R, ldr, p0 + 1, p0, mt, zs, sc);
+      chol_update_shift<HBT>(R, ldr, p0 + 1, p0, mt, zs, sc);
     }
     T0 {
       for (int p = p0; p < m - 1; ++p) { const int c = sup[p + 1]; sup[p] = c; pos[c] = p; }
@@ -424,7 +439,7 @@ __global__ void __launch_bounds__(NTHR) hb_step(HB a, int nact) {
     // add ip: chol_append (numerics.py:115-137); NotPD -> ridge over the grown support
     const int ip = dec[2];
     const double* acol = a.A + (int64_t)ip * a.ld;
-    for (int p = wpx(); p < m; p += NWARP) {
+    for (int p = wpx(); p < m; p += HBW) {
       const double* ap = a.A + (int64_t)sup[p] * a.ld;
       double acc = 0.0;
       for (int64_t i = lnx(); i < a.d; i += 32) acc = fma(ap[i], acol[i], acc);
@@ -432,16 +447,16 @@ __global__ void __launch_bounds__(NTHR) hb_step(HB a, int nact) {
       if (lnx() == 0) zs[p] = acc;
     }
     double q[1] = {0.0};
-    for (int64_t i = tix(); i < a.d; i += NTHR) q[0] += acol[i] * acol[i];
-    block_reduce<1>(E, q, 0u);
-    trsv_RT(R, ldr, m, zs, tile);
+    for (int64_t i = tix(); i < a.d; i += HBT) q[0] += acol[i] * acol[i];
+    hb_reduce<1>(q, 0u, sh);
+    trsv_RT<HBT>(R, ldr, m, zs, tile);
     double uu[1] = {0.0};
-    for (int p = tix(); p < m; p += NTHR) uu[0] += zs[p] * zs[p];
-    block_reduce<1>(E, uu, 0u);
+    for (int p = tix(); p < m; p += HBT) uu[0] += zs[p] * zs[p];
+    hb_reduce<1>(uu, 0u, sh);
     const double d2 = q[0] - uu[0];
     const bool fits = m < ldr;
     if (d2 > 0.0 && fits) {
-      for (int p = tix(); p < m; p += NTHR) R[(size_t)p * ldr + m] = zs[p];
+      for (int p = tix(); p < m; p += HBT) R[(size_t)p * ldr + m] = zs[p];
       T0 {
         R[(size_t)m * ldr + m] = sqrt(d2);
         sup[m] = ip; pos[ip] = m;
@@ -453,7 +468,7 @@ __global__ void __launch_bounds__(NTHR) hb_step(HB a, int nact) {
     } else {
       T0 { sup[m] = ip; pos[ip] = m; }
       __syncthreads();
-      const bool ok2 = ridge_chol(a, sup, m + 1, R, ldr, row, sc, E);
+      const bool ok2 = ridge_chol(a, sup, m + 1, R, ldr, row, sc);
       T0 { S.note = 1; if (!ok2) { S.status = ELL1_NOT_PD; S.done = 1; } }
     }
     if (fits) mn = m + 1;
@@ -461,10 +476,10 @@ __global__ void __launch_bounds__(NTHR) hb_step(HB a, int nact) {
   __syncthreads();
   T0 S.m = mn;
   // r = b - A_I x_I, ||r||^2, ||x||_1, max|x|, support count (homotopy.py:224-226)
-  for (int p = tix(); p < mn; p += NTHR) row[p] = X[sup[p]];
+  for (int p = tix(); p < mn; p += HBT) row[p] = X[sup[p]];
   __syncthreads();
   double q3[3] = {0.0, 0.0, 0.0};
-  for (int64_t i = tix(); i < a.ld; i += NTHR) {
+  for (int64_t i = tix(); i < a.ld; i += HBT) {
     double r = 0.0;
     if (i < a.d) {
       double acc = 0.0;
@@ -474,12 +489,12 @@ __global__ void __launch_bounds__(NTHR) hb_step(HB a, int nact) {
     }
     Rs[i] = r;
   }
-  for (int64_t k = tix(); k < a.n; k += NTHR) { const double xk = fabs(X[k]); q3[1] += xk; q3[2] = nmax(q3[2], xk); }
-  block_reduce<3>(E, q3, 0x4u);
+  for (int64_t k = tix(); k < a.n; k += HBT) { const double xk = fabs(X[k]); q3[1] += xk; q3[2] = nmax(q3[2], xk); }
+  hb_reduce<3>(q3, 0x4u, sh);
   const double cut = 1e-10 * pymax(q3[2], 1.0);
   double c1[1] = {0.0};
-  for (int64_t k = tix(); k < a.n; k += NTHR) if (fabs(X[k]) > cut) c1[0] += 1.0;
-  block_reduce<1>(E, c1, 0u);
+  for (int64_t k = tix(); k < a.n; k += HBT) if (fabs(X[k]) > cut) c1[0] += 1.0;
+  hb_reduce<1>(c1, 0u, sh);
   T0 { S.rr = q3[0]; S.l1 = q3[1]; S.top = q3[2]; S.cnt = c1[0]; S.pend = 1; }
 }
 
@@ -619,7 +634,7 @@ extern "C" int ell1_batch_homotopy(const ell1_dict_t* D, const double* Bmat, int
   if (cudaMemcpyAsync(Bm, Bmat, ld * B * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return ELL1_ERR_CUDA;
   // c = A^T b for every instance, then lambda0 / first atom
   if (!dgemm_AtX(h, a, Bm, a.C, B)) return ELL1_ERR_CUDA;
-  hb_init<<<B, NTHR, 0, s>>>(a, B);
+  hb_init<<<B, HBT, 0, s>>>(a, B);
   // identity active list
   {
     std::vector<int> ident(B);
@@ -640,7 +655,7 @@ extern "C" int ell1_batch_homotopy(const ell1_dict_t* D, const double* Bmat, int
   while (nact > 0) {
     a.act = act;
     a.V = Vcur;
-    hb_dir<<<nact, NTHR, smem, s>>>(a, nact);
+    hb_dir<<<nact, HBT, smem, s>>>(a, nact);
     // drop finished instances from the GEMM operands
     hb_scan<<<1, 1024, 0, s>>>(a.st, act, nact, perm, ctr);
     int nn = 0;
@@ -657,7 +672,7 @@ extern "C" int ell1_batch_homotopy(const ell1_dict_t* D, const double* Bmat, int
       a.V = Vcur;
     }
     if (!dgemm_AtX(h, a, a.V, a.W, nact)) return ELL1_ERR_CUDA;
-    hb_step<<<nact, NTHR, smem, s>>>(a, nact);
+    hb_step<<<nact, HBT, smem, s>>>(a, nact);
     if (!dgemm_AtX(h, a, a.Rr, a.C, nact)) return ELL1_ERR_CUDA;
   }
   hb_out<<<B, 256, 0, s>>>(a, B, out->x, out->iterations, out->converged, out->status, notes);

@@ -8,11 +8,12 @@
 namespace ell1 {
 
 // Solve R^T z = z (in place, z in shared memory), R upper m x m row-major.
+template <int NT = NTHR>
 static __device__ void trsv_RT(const double* R, int ldr, int m, double* z, double* tile) {
   for (int kb = 0; kb < m; kb += 32) {
     const int nbk = min(32, m - kb);
     // stage the 32 x 32 diagonal block
-    for (int t = tix(); t < 32 * 32; t += NTHR) {
+    for (int t = tix(); t < 32 * 32; t += NT) {
       const int i = t >> 5, j = t & 31;
       tile[t] = (i < nbk && j < nbk) ? R[(size_t)(kb + i) * ldr + kb + j] : 0.0;
     }
@@ -30,7 +31,7 @@ static __device__ void trsv_RT(const double* R, int ldr, int m, double* z, doubl
     }
     __syncthreads();
     // trailing update: z_j -= sum_{k in block} R[k][j] z_k  (rows of R: coalesced)
-    for (int j = kb + nbk + tix(); j < m; j += NTHR) {
+    for (int j = kb + nbk + tix(); j < m; j += NT) {
       double acc = 0.0;
       for (int k = 0; k < nbk; ++k) acc = fma(R[(size_t)(kb + k) * ldr + j], z[kb + k], acc);
       z[j] = z[j] - acc;
@@ -40,13 +41,14 @@ static __device__ void trsv_RT(const double* R, int ldr, int m, double* z, doubl
 }
 
 // Solve R d = z (in place), back substitution, blocked.
+template <int NT = NTHR>
 static __device__ void trsv_R(const double* R, int ldr, int m, double* z, double* tile) {
   const int nblk = (m + 31) / 32;
   for (int bb = nblk - 1; bb >= 0; --bb) {
     const int kb = bb * 32;
     const int nbk = min(32, m - kb);
     // z_B -= R[B, > B] d_{>B}: one warp per row, lanes over the row
-    for (int k = wpx(); k < nbk; k += NWARP) {
+    for (int k = wpx(); k < nbk; k += NT / 32) {
       double acc = 0.0;
       const double* row = R + (size_t)(kb + k) * ldr;
       int j = kb + nbk + lnx();
@@ -61,7 +63,7 @@ static __device__ void trsv_R(const double* R, int ldr, int m, double* z, double
       acc = warp_sum(acc);
       if (lnx() == 0) z[kb + k] = z[kb + k] - acc;
     }
-    for (int t = tix(); t < 32 * 32; t += NTHR) {
+    for (int t = tix(); t < 32 * 32; t += NT) {
       const int i = t >> 5, j = t & 31;
       tile[t] = (i < nbk && j < nbk) ? R[(size_t)(kb + i) * ldr + kb + j] : 0.0;
     }
@@ -84,6 +86,7 @@ static __device__ void trsv_R(const double* R, int ldr, int m, double* z, double
 // LINPACK rank-1 update of the (mt x mt) trailing block read from (src row
 // offset so, col offset so) and written shifted to (do, do); w consumed
 // (_fastkernels.pyx:46-59 semantics).
+template <int NT = NTHR>
 static __device__ void chol_update_shift(double* R, int ldr, int so, int dof, int mt, double* w, double* sc) {
   for (int p = 0; p < mt; ++p) {
     if (tix() == 0) {
@@ -95,7 +98,7 @@ static __device__ void chol_update_shift(double* R, int ldr, int so, int dof, in
     }
     __syncthreads();
     const double c = sc[0], s = sc[1];
-    for (int j = p + tix(); j < mt; j += NTHR) {
+    for (int j = p + tix(); j < mt; j += NT) {
       double row;
       if (j == p) row = sc[2];
       else {
@@ -110,6 +113,7 @@ static __device__ void chol_update_shift(double* R, int ldr, int so, int dof, in
 
 // dense Cholesky (upper, R^T R = G) of the m x m matrix in G (row-major), into R.
 // Returns false when not positive definite (numpy.linalg.cholesky LinAlgError).
+template <int NT = NTHR>
 static __device__ bool dense_chol(const double* G, double* R, int ldr, int m, double* sc) {
   for (int k = 0; k < m; ++k) {
     // R[k][j] = (G[k][j] - sum_{i<k} R[i][k] R[i][j]) / R[k][k]
@@ -121,7 +125,7 @@ static __device__ bool dense_chol(const double* G, double* R, int ldr, int m, do
     __syncthreads();
     if (!(sc[0] > 0.0)) return false;
     const double rkk = sqrt(sc[0]);
-    for (int j = k + tix(); j < m; j += NTHR) {
+    for (int j = k + tix(); j < m; j += NT) {
       if (j == k) { R[(size_t)k * ldr + k] = rkk; continue; }
       double s = G[(size_t)k * ldr + j];
       for (int i = 0; i < k; ++i) s -= R[(size_t)i * ldr + k] * R[(size_t)i * ldr + j];
