@@ -324,6 +324,34 @@ def leg_cfg4(torch, dev, ws, rank, iters=8, reps=2):
     return out
 
 
+_PEAKS = {}
+
+
+def gemm_peaks(torch, dev):
+    """Measured cuBLAS DGEMM / SGEMM throughput on this GPU (8192^3, best of 3):
+    the denominators of the batched solvers' tensor-pipe roofline (only bf16 is
+    in MEASURED_PEAKS.json)."""
+    if _PEAKS:
+        return _PEAKS
+    for name, dt in (("dgemm_tflops", torch.float64), ("sgemm_tflops", torch.float32)):
+        a = torch.randn(8192, 8192, device=dev, dtype=dt)
+        b = torch.randn(8192, 8192, device=dev, dtype=dt)
+        torch.matmul(a, b)
+        torch.cuda.synchronize()
+        best = 0.0
+        for _ in range(3):
+            s, e = _events(torch)
+            s.record()
+            torch.matmul(a, b)
+            e.record()
+            torch.cuda.synchronize()
+            best = max(best, 2 * 8192 ** 3 / (s.elapsed_time(e) / 1e3) / 1e12)
+        _PEAKS[name] = best
+        del a, b
+    torch.cuda.empty_cache()
+    return _PEAKS
+
+
 def _lib_mode():
     from paper_1007_3753_b200 import _lib
     return int(_lib.lib().ell1_blas_fp32_mode())
@@ -350,8 +378,13 @@ def leg_cfg3(torch, dev, queries=1024):
     torch.cuda.synchronize()
     t = s.elapsed_time(e) / 1e3
     its = res.iterations.astype(np.int64)
+    tfl = float(its.sum()) * 5 * 2.0 * 1024 * 1216 / t / 1e12
+    pk = gemm_peaks(torch, dev)["sgemm_tflops"]
     return {"workload": "cfg3: CAB [A I] 1024 x 2240, %d queries, batched DALM fp32 storage, "
                         "tol 1e-4, min-class-residual labels" % queries,
+            "roofline": {"bound": "fp32 GEMMs", "achieved": tfl, "peak": pk, "unit": "TFLOP/s",
+                         "frac": tfl / pk, "peak_source": "cuBLAS SGEMM 8192^3 measured in this run",
+                         "algorithmic": "5 dictionary passes x 2 d n_A flops per query-iteration"},
             "queries_per_sec": queries / t, "ms_per_batch": 1e3 * t,
             "mean_iterations": float(its.mean()), "max_iterations": int(its.max()),
             "accuracy_vs_truth": float(np.mean(labels == truth)),
@@ -410,8 +443,17 @@ def leg_cfg5(torch, dev, ws=1, B=1024, cpu_sample=8):
         t = float(t.item())
         its = res.iterations.astype(np.int64)
         unit = "breakpoints_per_sec" if name == "homotopy" else "iterations_per_sec"
+        # GEMM-form work per instance-iteration: dictionary passes x 2 d n flops
+        passes = {"fista": 2, "dalm": 5, "homotopy": 2}[name]
+        tfl = float(its.sum()) * passes * 2.0 * d * n / t / 1e12
+        pk = gemm_peaks(torch, dev)["dgemm_tflops"]
         out[name] = {"solves_per_sec": B / t, "ms_per_batch": 1e3 * t, unit: float(its.sum()) / t,
-                     "mean_iterations": float(its.mean()), "converged": int(res.converged.sum())}
+                     "mean_iterations": float(its.mean()), "converged": int(res.converged.sum()),
+                     "roofline": {"bound": "tensor (fp64 DMMA GEMMs)", "achieved": tfl,
+                                  "peak": pk, "unit": "TFLOP/s", "frac": tfl / pk,
+                                  "peak_source": "cuBLAS DGEMM 8192^3 measured in this run",
+                                  "algorithmic": "%d dictionary passes x 2 d n flops per instance-iteration"
+                                                 % passes}}
     if ws == 1 and cpu_sample > 0:
         # CPU reference port on a bounded sample of the same instances (all host cores)
         import oracle
@@ -544,9 +586,33 @@ def leg_solvers_cfg2(torch, P, reps=3):
             torch.cuda.synchronize()
             ms = s.elapsed_time(e) / reps
             out[name] = {"ms_per_solve": round(ms, 3), "iterations": int(r.iterations),
-                         "converged": bool(r.converged)}
+                         "converged": bool(r.converged),
+                         "us_per_iteration": round(1e3 * ms / max(int(r.iterations), 1), 2)}
         except Exception as exc:  # pragma: no cover - report, do not abort the bench
             out[name] = {"error": str(exc)[:160]}
+    # CPU port: the same solvers for a bounded number of iterations (per-iteration rate)
+    import oracle
+    cap = 40
+    cpu = {"fista": lambda: oracle.fista(P.A, P.b, tol=1e-6, max_iter=cap),
+           "ist": lambda: oracle.ist(P.A, P.b, lam=lam, tol=1e-6, max_iter=cap),
+           "palm": lambda: oracle.palm(P.A, P.b, tol=1e-6, max_iter=cap),
+           "dalm": lambda: oracle.dalm(P.A, P.b, tol=1e-6, max_iter=cap),
+           "gpsr": lambda: oracle.gpsr(P.A, P.b, lam=lam, tol=1e-6, max_iter=cap),
+           "tnipm": lambda: oracle.tnipm(P.A, P.b, lam=lam, tol=1e-6, max_iter=8),
+           "homotopy": lambda: oracle.homotopy(P.A, P.b, lam, max_iter=cap)[0],
+           "pdipa": lambda: oracle.pdipa(P.A, P.b, tol=1e-6, max_iter=8)}
+    for name, fn in cpu.items():
+        try:
+            t0 = time.perf_counter()
+            r = fn()
+            el = time.perf_counter() - t0
+            if name in out and isinstance(out[name], dict):
+                out[name]["cpu_port_us_per_iteration"] = round(1e6 * el / max(int(r.iterations), 1), 1)
+        except Exception as exc:  # pragma: no cover
+            if name in out and isinstance(out[name], dict):
+                out[name]["cpu_port_error"] = str(exc)[:120]
+    out["cpu_note"] = ("cpu_port_us_per_iteration: oracle port (numpy/OpenBLAS, %d host cores) run for "
+                       "a bounded number of iterations on the same instance" % os.cpu_count())
     return out
 
 

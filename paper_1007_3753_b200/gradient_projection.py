@@ -87,7 +87,8 @@ def gpsr_step_size(g, A):
     if gg == 0.0:
         raise ValueError("g must be nonzero")
     n = g.shape[0] // 2
-    Av = A @ (g[:n] - g[n:])
+    from paper_1007_3753_b200.operators import apply_any
+    Av = apply_any(A, g[:n] - g[n:])
     curvature = float(Av @ Av)
     if curvature <= _CURV_FLOOR * gg:
         return _ALPHA_CAP

@@ -34,12 +34,16 @@ class PathState:
 
 
 def breakpoint_gammas(state, d, A):
-    """Step lengths to the next add / remove event (homotopy.py:78-115),
-    evaluated on host arrays (utility for callers of the reference API)."""
-    A = np.asarray(A.A if hasattr(A, "A") and not isinstance(A, np.ndarray) else A, dtype=np.float64)
+    """Step lengths to the next add / remove event (homotopy.py:78-115); the
+    products v = A_I d_I and w = A^T v run on the device."""
+    from paper_1007_3753_b200.operators import adjoint_any, apply_any
+    if hasattr(A, "A") and isinstance(getattr(A, "A"), np.ndarray) and not hasattr(A, "device_extension"):
+        A = A.A
     sup = list(state.support)
-    v = A[:, sup] @ d[sup]
-    w = A.T @ v
+    dfull = np.zeros(np.asarray(state.x).shape[0])
+    dfull[sup] = np.asarray(d, dtype=np.float64)[sup]
+    v = apply_any(A, dfull)
+    w = adjoint_any(A, v)
     mask = np.zeros(state.c.shape[0], dtype=bool)
     mask[sup] = True
     return _gammas(state.lam, state.c, state.x, d, w, mask)
@@ -74,11 +78,11 @@ def _gammas(lam, c, x, d, w, support_mask):
 
 
 def update_direction(state, A):
-    """Full-length path direction from the state's factor (homotopy.py:67-75)."""
-    from scipy.linalg import solve_triangular
+    """Full-length path direction from the state's factor (homotopy.py:67-75);
+    the two triangular solves run on the device (CholFactor.solve)."""
+    from paper_1007_3753_b200.numerics import CholFactor
     sgn = np.sign(state.c[state.support])
-    R = state.chol.R
-    d_I = solve_triangular(R, solve_triangular(R, sgn, trans="T", lower=False), lower=False)
+    d_I = CholFactor(state.chol.R).solve(sgn)
     d = np.zeros(state.x.shape[0])
     d[state.support] = d_I
     return d

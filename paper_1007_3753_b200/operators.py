@@ -149,3 +149,34 @@ class DenseDictionary:
     def gram_dd(self):
         """D D^T (operators.py:57-58)."""
         return self._gram(None)
+
+
+def _device_op(A):
+    """A device operator for whatever a caller passed as a dictionary, or None
+    for a user-supplied host operator (which then keeps its own arithmetic)."""
+    if isinstance(A, DenseDictionary):
+        return A
+    if isinstance(A, device.DeviceDictionary):
+        return DenseDictionary(A)
+    if hasattr(A, "device_extension"):          # robust.ExtendedDictionary
+        return A
+    if isinstance(A, np.ndarray):
+        return DenseDictionary(A)
+    return None
+
+
+def apply_any(A, x):
+    """A @ x with the product on the device when A is a dense / device /
+    extended dictionary (the helper functions of the reference API use it)."""
+    op = _device_op(A)
+    if op is None:
+        return A @ x
+    return op.apply(np.asarray(x, dtype=np.float64))
+
+
+def adjoint_any(A, r):
+    """A^T @ r, on the device like apply_any."""
+    op = _device_op(A)
+    if op is None:
+        return A.T @ r
+    return op.adjoint(np.asarray(r, dtype=np.float64))

@@ -39,10 +39,9 @@ class ExtendedDictionary:
     """Implicit stack [A, s I] of width n + d (robust.py:57-155).
 
     Solvers of this package read it through ``device_extension()`` (the
-    device copy of A plus the scale).  The host-side operator methods
-    (apply / adjoint / column protocol / Gram hooks) are kept for callers
-    and tests of the reference API; ``norm_sq`` runs the device power
-    iteration.
+    device copy of A plus the scale).  The operator methods of the reference
+    API (apply / adjoint / column protocol / Gram hooks / norm_sq) run their
+    dictionary products on the device as well.
     """
 
     mode = "cab"
@@ -69,13 +68,13 @@ class ExtendedDictionary:
             self._dev = device.DeviceDictionary(self.A, dtype=self._dtype, device=self._ordinal)
         return self._dev, self.scale
 
-    def _host(self):
-        if self.A is None:
-            D = self._dev
-            self.A = D.storage.view(D.n, D.ld)[:, : D.d].double().T.contiguous().cpu().numpy()
-        return self.A
+    def _op(self):
+        from paper_1007_3753_b200.operators import DenseDictionary
+        if getattr(self, "_dd", None) is None:
+            self._dd = DenseDictionary(self.device_extension()[0])
+        return self._dd
 
-    # -- operator protocol (host utilities) --------------------------------
+    # -- operator protocol (products on the device; the identity block is O(d))
     @property
     def shape(self):
         if self.A is not None:
@@ -92,55 +91,54 @@ class ExtendedDictionary:
         return self.apply(np.asarray(w, dtype=np.float64))
 
     def apply(self, w):
-        A = self._host()
-        n = A.shape[1]
-        return A @ w[:n] + self.scale * w[n:]
+        w = np.asarray(w, dtype=np.float64)
+        n = self.shape[1] - self.shape[0]
+        return self._op().apply(w[:n]) + self.scale * w[n:]
 
     def adjoint(self, r):
-        A = self._host()
-        return np.concatenate([A.T @ r, self.scale * r])
+        r = np.asarray(r, dtype=np.float64)
+        return np.concatenate([self._op().adjoint(r), self.scale * r])
 
     def column(self, j):
-        A = self._host()
-        d, n = A.shape
+        d, N = self.shape
+        n = N - d
         if j < n:
-            return A[:, j].copy()
+            return self._op().column(j)
         out = np.zeros(d)
         out[j - n] = self.scale
         return out
 
     def apply_columns(self, idx, coeffs):
-        A = self._host()
-        d, n = A.shape
+        d, N = self.shape
+        n = N - d
         idx = np.asarray(idx, dtype=np.intp)
         coeffs = np.asarray(coeffs, dtype=np.float64)
         out = np.zeros(d)
         lo = idx < n
         if np.any(lo):
-            out += A[:, idx[lo]] @ coeffs[lo]
+            out += self._op().apply_columns(idx[lo], coeffs[lo])
         if np.any(~lo):
             out[idx[~lo] - n] += self.scale * coeffs[~lo]
         return out
 
     def columns_dot(self, idx, v):
-        A = self._host()
-        n = A.shape[1]
+        d, N = self.shape
+        n = N - d
         idx = np.asarray(idx, dtype=np.intp)
         out = np.empty(idx.shape[0])
         lo = idx < n
         if np.any(lo):
-            out[lo] = A[:, idx[lo]].T @ v
+            out[lo] = self._op().columns_dot(idx[lo], v)
         if np.any(~lo):
-            out[~lo] = self.scale * v[idx[~lo] - n]
+            out[~lo] = self.scale * np.asarray(v, dtype=np.float64)[idx[~lo] - n]
         return out
 
     def gram_column(self, idx, j):
         return self.columns_dot(idx, self.column(j))
 
     def column_norms_sq(self):
-        A = self._host()
-        d = A.shape[0]
-        return np.concatenate([np.sum(A * A, axis=0), np.full(d, self.scale ** 2)])
+        d = self.shape[0]
+        return np.concatenate([self._op().column_norms_sq(), np.full(d, self.scale ** 2)])
 
     def norm_sq(self):
         """||A||^2 + s^2 (robust.py:139-143), power iteration on the device."""
@@ -150,16 +148,16 @@ class ExtendedDictionary:
         return self._norm_sq
 
     def weighted_gram_dd(self, w):
-        A = self._host()
-        d, n = A.shape
-        M = (A * w[:n]) @ A.T
+        w = np.asarray(w, dtype=np.float64)
+        d, N = self.shape
+        n = N - d
+        M = self._op().weighted_gram_dd(w[:n])
         M[np.diag_indices(d)] += self.scale ** 2 * w[n:]
         return M
 
     def gram_dd(self):
-        A = self._host()
-        d = A.shape[0]
-        M = A @ A.T
+        d = self.shape[0]
+        M = self._op().gram_dd()
         M[np.diag_indices(d)] += self.scale ** 2
         return M
 

@@ -245,3 +245,63 @@ def test_solve_named_dispatch():
         assert r.x_star.shape == (60,)
     with pytest.raises(ValueError):
         solve_named("nope", P, cfg)
+
+
+# ------------------------------------------------------------ reference-API helpers on the device
+def test_extended_dictionary_operator_methods():
+    from paper_1007_3753_b200.robust import ExtendedDictionary
+    rng = np.random.default_rng(12)
+    A = rng.standard_normal((30, 50))
+    s = 0.7
+    E = ExtendedDictionary(A, s)
+    B = np.hstack([A, s * np.eye(30)])
+    w = rng.standard_normal(80)
+    r = rng.standard_normal(30)
+    idx = np.array([1, 49, 50, 79])
+    c = rng.standard_normal(4)
+    np.testing.assert_allclose(E.apply(w), B @ w, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(E @ w, B @ w, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(E.adjoint(r), B.T @ r, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(E.T @ r, B.T @ r, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(E.apply_columns(idx, c), B[:, idx] @ c, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(E.columns_dot(idx, r), B[:, idx].T @ r, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(E.column(60), B[:, 60])
+    np.testing.assert_allclose(E.gram_column(idx, 3), B[:, idx].T @ B[:, 3], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(E.column_norms_sq(), np.sum(B * B, axis=0), rtol=1e-12)
+    ww = rng.uniform(0.1, 1.0, 80)
+    np.testing.assert_allclose(E.weighted_gram_dd(ww), (B * ww) @ B.T, rtol=1e-11, atol=1e-11)
+    np.testing.assert_allclose(E.gram_dd(), B @ B.T, rtol=1e-11, atol=1e-11)
+    assert abs(E.norm_sq() - (O.power_norm_sq(A) + s * s)) <= 1e-9 * E.norm_sq()
+
+
+def test_model_and_solver_helpers_on_device():
+    from paper_1007_3753_b200 import model
+    from paper_1007_3753_b200.gradient_projection import gpsr_step_size
+    from paper_1007_3753_b200.homotopy import PathState, breakpoint_gammas, update_direction
+    from paper_1007_3753_b200.numerics import chol_factor
+    rng = np.random.default_rng(13)
+    A = rng.standard_normal((25, 60))
+    b = rng.standard_normal(25)
+    x = np.zeros(60)
+    x[[2, 9]] = [0.5, -1.0]
+    P = model.ProblemInstance(A, b)
+    r = b - A @ x
+    assert abs(model.objective(x, P, 0.1) - (0.5 * r @ r + 0.1 * np.abs(x).sum())) <= 1e-12
+    assert abs(model.kkt_residual(x, P, 0.1) - O.kkt_of(x, A.T @ r, 0.1)) <= 1e-12
+    assert abs(model.default_lambda(P) - 1e-2 * np.max(np.abs(A.T @ b))) <= 1e-14
+    g = rng.standard_normal(120)
+    Av = A @ (g[:60] - g[60:])
+    assert abs(gpsr_step_size(g, A) - (g @ g) / (Av @ Av)) <= 1e-12 * (g @ g) / (Av @ Av)
+    sup = [2, 9]
+    c = A.T @ r
+    st = PathState(x, sup, 1.5, c, chol_factor(A[:, sup].T @ A[:, sup]))
+    d = update_direction(st, A)
+    ref_dI = np.linalg.solve(A[:, sup].T @ A[:, sup], np.sign(c[sup]))
+    np.testing.assert_allclose(d[sup], ref_dI, rtol=1e-10)
+    mask = np.zeros(60, bool)
+    mask[sup] = True
+    w = A.T @ (A[:, sup] @ d[sup])
+    got = breakpoint_gammas(st, d, A)
+    ref = O.step_lengths(1.5, c, x, d, w, mask)
+    assert got[1] == ref[1] and got[3] == ref[3]
+    np.testing.assert_allclose([got[0], got[2]], [ref[0], ref[2]], rtol=1e-10)
