@@ -2,14 +2,13 @@
 // (element j equals shrinkage.fista_solve on (A, b_j), shrinkage.py:231-298).
 //
 // One host round = one backtracking trial of every active instance:
-//   bf_prox   momentum point (new iteration) or the stored one (retry),
-//             soft-threshold, backtracking reductions
+//   bf_step   accepted last round: KKT, support, trace, stopping rules,
+//             continuation of that iteration, then the next momentum point;
+//             retrying: undo the global ring rotation for this instance
+//             (copies); then soft-threshold + backtracking reductions
 //   GEMM      A X_next
 //   bf_resid  r_next, F, Q: accept, or grow L and mark the instance for a retry
 //   GEMM      A^T R_next  (speculative for instances that will retry)
-//   bf_finish accepted: KKT, support, trace, stopping rules, continuation;
-//             retrying: copy its columns so the global ring rotation leaves
-//             its state unchanged
 // Instances run their own backtracking independently, so the host never
 // waits for a retry decision: it reads one device counter every few rounds
 // (termination / compaction of finished instances).
@@ -94,16 +93,93 @@ __global__ void __launch_bounds__(BT) bf_init(const BFArgs a, const double* CT, 
   }
 }
 
-__global__ void __launch_bounds__(BT) bf_prox(const BFArgs a) {
+// One kernel per round before the GEMMs, run AFTER the host rotated the
+// rings (x_prev <- x <- x_next, r likewise, g_x <-> g slot):
+//   accepted last round -> finalise that iteration (KKT with the g_next the
+//     previous A^T R GEMM produced, trace, stopping, continuation), then start
+//     the next one (momentum point, prox trial)
+//   rejected last round -> undo the rotation for this instance (copies), then
+//     a new prox trial from the stored momentum point with the grown L
+//   first round         -> first prox trial
+__global__ void __launch_bounds__(BT) bf_step(const BFArgs a) {
   const int j = blockIdx.x;
   __shared__ double sh[BW * 7 + 7];
   __shared__ double sc[4];
-  __shared__ int fresh;
+  __shared__ int mode;                  // 0 first trial of a new iteration, 1 retry, 2 stop
   BI& I = a.inst[j];
   if (!I.active) return;
+  const int64_t o = (int64_t)j * a.ldx;
+  const int64_t orr = (int64_t)j * a.ld;
+  if (I.retry) {
+    for (int64_t k = threadIdx.x; k < a.N; k += BT) {
+      a.X[a.ix][o + k] = a.X[a.ixp][o + k];
+      a.X[a.ixp][o + k] = a.X[a.ixn][o + k];
+      a.G[a.igx][o + k] = a.G[a.igxp][o + k];
+    }
+    for (int64_t i = threadIdx.x; i < a.ld; i += BT) {
+      a.R[a.irx][orr + i] = a.R[a.irxp][orr + i];
+      a.R[a.irxp][orr + i] = a.R[a.irn][orr + i];
+    }
+    if (threadIdx.x == 0) mode = 1;
+  } else if (I.accepted) {
+    // ---- finish the accepted iteration (shrinkage.py:283-297)
+    const double* xc = a.X[a.ix] + o;
+    double* gc = a.G[a.igx] + o;
+    const double* rc = a.R[a.irx] + orr;
+    const double cut = 1e-10 * pymax(I.S[3], 1.0);   // model.py:232
+    const double lam = I.lam;
+    double k5[5] = {0, 0, 0, 0, 0};
+    for (int64_t k = threadIdx.x; k < a.N; k += BT) {
+      double g;
+      if (k < a.n) g = a.f32 ? (double)a.G32[(int64_t)j * a.n + k] : gc[k];
+      else g = a.s * rc[k - a.n];
+      gc[k] = g;
+      const double xk = xc[k];
+      const double c = -g;
+      if (xk != 0.0) { k5[0] = nmax(k5[0], fabs(c - lam * sgn(xk))); k5[2] = 1.0; }
+      else { k5[1] = nmax(k5[1], fabs(c)); k5[3] = 1.0; }
+      if (fabs(xk) > cut) k5[4] += 1.0;
+    }
+    cta_reduce<5>(k5, 0xFu, sh);
+    if (threadIdx.x == 0) {
+      double kkt = k5[2] > 0.0 ? k5[0] : 0.0;
+      if (k5[3] > 0.0) kkt = pymax(pymax(kkt, k5[1] - lam), 0.0);
+      I.tp = I.tc; I.tc = I.tn;
+      if (a.trace) {
+        double* tr = a.trace + ((int64_t)I.orig * a.C.max_iter + (I.it - 1)) * 4;
+        tr[0] = (double)I.it; tr[1] = I.Fn; tr[2] = sqrt(I.rr); tr[3] = k5[4];
+      }
+      I.hist = I.hist < 2 ? I.hist + 1 : 2;
+      int done = 0;
+      if (lam == I.lam_bar && kkt <= a.C.tol * I.lam_bar) done = 1;   // shrinkage.py:291-293
+      else if (stop_fires(a.C.stop_kind, a.C.stop_thr, I.hist, I.Fn, I.Fprev, I.S[4], I.S[5], I.S[6],
+                          a.C.gt_norm, kkt))
+        done = 1;
+      I.Fprev = I.Fn;
+      if (done) I.conv = 1;
+      else {
+        I.lam = pymax(a.O.beta * I.lam, I.lam_bar);         // shrinkage.py:297
+        I.fy = I.fy_next;
+        if (I.it >= a.C.max_iter) done = 2;
+      }
+      if (done) {
+        I.active = 0;
+        a.it_out[I.orig] = I.it; a.conv_out[I.orig] = I.conv; a.status_out[I.orig] = ELL1_OK;
+        atomicSub(a.counters + 1, 1);
+      }
+      mode = done ? 2 : 0;
+    }
+    __syncthreads();
+    if (mode == 2) {
+      double* xo = a.x_out + (int64_t)I.orig * a.N;
+      for (int64_t k = threadIdx.x; k < a.N; k += BT) xo[k] = xc[k];
+      return;
+    }
+  } else if (threadIdx.x == 0) {
+    mode = 0;                                              // very first trial
+  }
   if (threadIdx.x == 0) {
-    fresh = !I.retry;
-    if (fresh) {                                            // a new iteration
+    if (mode == 0) {                                       // a new iteration
       I.it++;
       I.bt = 0;
       I.m = (I.tp - 1.0) / I.tc;
@@ -115,8 +191,7 @@ __global__ void __launch_bounds__(BT) bf_prox(const BFArgs a) {
   }
   __syncthreads();
   const double m = sc[0], L = sc[1], thr = sc[2];
-  const bool fr = fresh;
-  const int64_t o = (int64_t)j * a.ldx;
+  const bool fr = mode == 0;
   const double* x = a.X[a.ix] + o;
   const double* xp = a.X[a.ixp] + o;
   double* xn = a.X[a.ixn] + o;
@@ -201,84 +276,6 @@ __global__ void __launch_bounds__(BT) bf_resid(const BFArgs a) {
         atomicSub(a.counters + 1, 1);
       }
     }
-  }
-}
-
-__global__ void __launch_bounds__(BT) bf_finish(const BFArgs a, int gslot) {
-  const int j = blockIdx.x;
-  __shared__ double sh[BW * 5 + 5];
-  BI& I = a.inst[j];
-  if (!I.active) return;
-  const int64_t o = (int64_t)j * a.ldx;
-  if (I.retry) {
-    // rejected trial: after the global rotation (x_prev <- x <- x_next,
-    // r likewise, g_x <-> g slot) this instance must see its current state
-    // again, so place it where the rotation will look for it
-    const int64_t orr = (int64_t)j * a.ld;
-    for (int64_t k = threadIdx.x; k < a.N; k += BT) {
-      a.X[a.ixn][o + k] = a.X[a.ix][o + k];
-      a.X[a.ix][o + k] = a.X[a.ixp][o + k];
-      a.G[gslot][o + k] = a.G[a.igx][o + k];
-    }
-    for (int64_t i = threadIdx.x; i < a.ld; i += BT) {
-      a.R[a.irn][orr + i] = a.R[a.irx][orr + i];
-      a.R[a.irx][orr + i] = a.R[a.irxp][orr + i];
-    }
-    return;
-  }
-  const double* xn = a.X[a.ixn] + o;               // the new x
-  double* gn = a.G[gslot] + o;                     // the new g_x
-  const double* rn = a.R[a.irn] + (int64_t)j * a.ld;
-  const double cut = 1e-10 * pymax(I.S[3], 1.0);   // model.py:232
-  const double lam = I.lam;
-  double k5[5] = {0, 0, 0, 0, 0};
-  for (int64_t k = threadIdx.x; k < a.N; k += BT) {
-    double g;
-    if (k < a.n) g = a.f32 ? (double)a.G32[(int64_t)j * a.n + k] : gn[k];
-    else g = a.s * rn[k - a.n];
-    gn[k] = g;
-    const double xk = xn[k];
-    const double c = -g;
-    if (xk != 0.0) { k5[0] = nmax(k5[0], fabs(c - lam * sgn(xk))); k5[2] = 1.0; }
-    else { k5[1] = nmax(k5[1], fabs(c)); k5[3] = 1.0; }
-    if (fabs(xk) > cut) k5[4] += 1.0;
-  }
-  cta_reduce<5>(k5, 0xFu, sh);
-  __shared__ int fin;
-  if (threadIdx.x == 0) {
-    double kkt = k5[2] > 0.0 ? k5[0] : 0.0;
-    if (k5[3] > 0.0) kkt = pymax(pymax(kkt, k5[1] - lam), 0.0);
-    I.tp = I.tc; I.tc = I.tn;
-    if (a.trace) {
-      double* tr = a.trace + ((int64_t)I.orig * a.C.max_iter + (I.it - 1)) * 4;
-      tr[0] = (double)I.it; tr[1] = I.Fn; tr[2] = sqrt(I.rr); tr[3] = k5[4];
-    }
-    I.hist = I.hist < 2 ? I.hist + 1 : 2;
-    int done = 0;
-    if (lam == I.lam_bar && kkt <= a.C.tol * I.lam_bar) done = 1;   // shrinkage.py:291-293
-    else {
-      const double gtn = a.C.gt_norm;
-      if (stop_fires(a.C.stop_kind, a.C.stop_thr, I.hist, I.Fn, I.Fprev, I.S[4], I.S[5], I.S[6], gtn, kkt))
-        done = 1;
-    }
-    I.Fprev = I.Fn;
-    if (done) I.conv = 1;
-    else {
-      I.lam = pymax(a.O.beta * I.lam, I.lam_bar);           // shrinkage.py:297
-      I.fy = I.fy_next;
-      if (I.it >= a.C.max_iter) done = 2;
-    }
-    if (done) {
-      I.active = 0;
-      a.it_out[I.orig] = I.it; a.conv_out[I.orig] = I.conv; a.status_out[I.orig] = ELL1_OK;
-      atomicSub(a.counters + 1, 1);
-    }
-    fin = done;
-  }
-  __syncthreads();
-  if (fin) {
-    double* xo = a.x_out + (int64_t)I.orig * a.N;
-    for (int64_t k = threadIdx.x; k < a.N; k += BT) xo[k] = xn[k];
   }
 }
 
@@ -423,6 +420,12 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
         perm_mat(a.GY, N, ldx);
         for (int k = 0; k < 3; ++k) perm_mat(a.R[k], ld, ld);
         perm_mat(Bm, ld, ld);
+        if (a.f32) {                  // g_next of the last round (fp32 GEMM output) is still pending
+          float* fs = reinterpret_cast<float*>(scratch);
+          dim3 g((unsigned)((D->n + 255) / 256 < 64 ? (D->n + 255) / 256 : 64), (unsigned)nact);
+          gather_cols<float><<<g, 256, 0, s>>>(a.G32, fs, D->n, D->n, perm, nact);
+          cudaMemcpyAsync(a.G32, fs, D->n * nact * 4, cudaMemcpyDeviceToDevice, s);
+        }
         {
           const int64_t words = (int64_t)sizeof(BI) / 4;
           dim3 g(1, (unsigned)nact);
@@ -432,8 +435,8 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
         Bcur = nact;
       }
     }
-    // ---- one backtracking trial for each of the Bcur leading instances
-    bf_prox<<<Bcur, BT, 0, s>>>(a);
+    // ---- finish last round's accepted iterations, then one backtracking trial each
+    bf_step<<<Bcur, BT, 0, s>>>(a);
     if (!gemm_AX(h, D, a.f32 ? (const void*)a.X32 : (const void*)a.X[a.ixn], ldx,
                  a.f32 ? (void*)a.AX32 : (void*)a.AX, ld, Bcur, spp))
       return ELL1_ERR_CUDA;
@@ -442,8 +445,7 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
     if (!gemm_AtR(h, D, a.f32 ? (const void*)a.R32 : (const void*)a.R[a.irn], ld,
                   a.f32 ? (void*)a.G32 : (void*)a.G[a.igxp], a.f32 ? D->n : ldx, Bcur, spp))
       return ELL1_ERR_CUDA;
-    bf_finish<<<Bcur, BT, 0, s>>>(a, a.igxp);
-    // rotate the rings (shrinkage.py:283-284); retrying instances pre-compensated
+    // rotate the rings (shrinkage.py:283-284); bf_step undoes it for retrying instances
     { int t = a.ixp; a.ixp = a.ix; a.ix = a.ixn; a.ixn = t; }
     { int t = a.irxp; a.irxp = a.irx; a.irx = a.irn; a.irn = t; }
     { int t = a.igxp; a.igxp = a.igx; a.igx = t; }
