@@ -78,13 +78,44 @@ def _gammas(lam, c, x, d, w, support_mask):
 
 
 def update_direction(state, A):
-    """Full-length path direction from the state's factor (homotopy.py:67-75);
-    the two triangular solves run on the device (CholFactor.solve)."""
-    from paper_1007_3753_b200.numerics import CholFactor
-    sgn = np.sign(state.c[state.support])
+    """Full-length path direction from the state's factor (homotopy.py:67-75,
+    _solve_direction :40-64): the triangular solves and the Gram check
+    (A_I^T A_I d_I against the signs) run on the device; a drifted factor is
+    replaced by a fresh device Cholesky of the support Gram, and a Gram that
+    stays singular raises DegenerateSupportError."""
+    from paper_1007_3753_b200.exceptions import DegenerateSupportError, NotPositiveDefiniteError
+    from paper_1007_3753_b200.numerics import CholFactor, chol_factor
+    from paper_1007_3753_b200.operators import adjoint_any, apply_any
+    if hasattr(A, "A") and isinstance(getattr(A, "A"), np.ndarray) and not hasattr(A, "device_extension"):
+        A = A.A
+    sup = list(state.support)
+    n = np.asarray(state.x).shape[0]
+    d = np.zeros(n)
+    if not sup:
+        return d
+    sgn = np.sign(state.c[sup])
+
+    def gram_times(dI):
+        full = np.zeros(n)
+        full[sup] = dI
+        return adjoint_any(A, apply_any(A, full))[sup]
+
     d_I = CholFactor(state.chol.R).solve(sgn)
-    d = np.zeros(state.x.shape[0])
-    d[state.support] = d_I
+    tol = 1e-6 * max(1.0, float(np.linalg.norm(sgn)))
+    if np.linalg.norm(gram_times(d_I) - sgn) > tol:
+        G = np.empty((len(sup), len(sup)))
+        for col in range(len(sup)):
+            e = np.zeros(len(sup))
+            e[col] = 1.0
+            G[:, col] = gram_times(e)
+        try:
+            fresh = chol_factor(G)
+        except NotPositiveDefiniteError as exc:
+            raise DegenerateSupportError("active-set Gram is singular") from exc
+        d_I = fresh.solve(sgn)
+        if np.linalg.norm(gram_times(d_I) - sgn) > tol:
+            raise DegenerateSupportError("active-set Gram solve failed")
+    d[sup] = d_I
     return d
 
 

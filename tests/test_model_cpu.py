@@ -103,3 +103,17 @@ def test_no_cpu_fallback():
         fista_solve(ProblemInstance(np.eye(2), np.ones(2)), SolverConfig(tol=1e-6))
     with pytest.raises(DeviceError):
         model.objective(np.zeros(2), ProblemInstance(np.eye(2), np.ones(2)), 0.1)
+
+
+def test_alm_state_validation():
+    from paper_1007_3753_b200.alm import AlmState, DalmState
+    AlmState(np.zeros(2), np.zeros(1), 1.0, 2.0, 3.0)
+    with pytest.raises(ValueError):
+        AlmState(np.zeros(2), np.zeros(1), 0.0, 2.0, 3.0)
+    with pytest.raises(ValueError):
+        AlmState(np.zeros(2), np.zeros(1), 1.0, 1.0, 3.0)
+    DalmState(np.zeros(2), np.zeros(1), np.array([1.0, -1.0]), 1.0, None)
+    with pytest.raises(ValueError):
+        DalmState(np.zeros(2), np.zeros(1), np.array([1.1, 0.0]), 1.0, None)
+    with pytest.raises(ValueError):
+        DalmState(np.zeros(2), np.zeros(1), np.zeros(2), 0.0, None)
