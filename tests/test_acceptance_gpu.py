@@ -26,7 +26,7 @@ def test_criterion_1_exact_recovery_agreement():
     from paper_1007_3753_b200.pdipa import pdipa_solve
     cfg = SolverConfig(tol=1e-8, max_iter=2000)
     wins = {"pdipa": 0, "homotopy": 0, "palm": 0, "dalm": 0}
-    trials = 40
+    trials = 100
     for t in range(trials):
         P = _instance(200, 100, 10, oracle.trial_seed(1000, t))
         nrm = np.linalg.norm(P.ground_truth)
@@ -45,7 +45,7 @@ def test_criterion_2_matched_weight_cross_agreement():
     from paper_1007_3753_b200.model import SolverConfig, kkt_residual, objective
     from paper_1007_3753_b200.shrinkage import fista_solve, ist_solve
     worst_obj = worst_kkt = 0.0
-    for t in range(10):
+    for t in range(20):
         P = _instance(200, 100, 10, oracle.trial_seed(3000, t))
         lam = 1e-2 * float(np.max(np.abs(P.A.T @ P.b)))
         cfg = SolverConfig(lam=lam, tol=1e-6, max_iter=20000)
@@ -65,7 +65,7 @@ def test_criterion_3_momentum_convergence_bound():
     from paper_1007_3753_b200.shrinkage import fista_solve
     opts = {"continuation": False, "exact_L": True}
     worst = np.inf
-    for t in range(4):
+    for t in range(10):
         P = _instance(100, 50, 8, oracle.trial_seed(4000, t))
         lam = 1e-2 * float(np.max(np.abs(P.A.T @ P.b)))
         L = spectral_norm_sq(P.A)

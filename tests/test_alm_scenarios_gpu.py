@@ -106,7 +106,7 @@ def test_dalm_honors_stopping_rule():
 
 def test_palm_and_dalm_agree_on_the_l1_value():
     from paper_1007_3753_b200.alm import dalm_solve, palm_solve
-    for seed in range(2600, 2620):
+    for seed in range(2600, 2700):
         P = _gen(100, 50, 1 + seed % 4, seed)
         rp = palm_solve(P, _cfg(tol=1e-7, max_iter=20000))
         rd = dalm_solve(P, _cfg(tol=1e-7, max_iter=20000, options={"beta": 0.2}))

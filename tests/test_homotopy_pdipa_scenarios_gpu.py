@@ -146,7 +146,7 @@ def test_homotopy_recovery_and_budget():
 
 def test_homotopy_support_recovery_rate():
     from paper_1007_3753_b200.homotopy import homotopy_solve
-    n, hits, trials = 256, 0, 40
+    n, hits, trials = 256, 0, 100
     for trial in range(trials):
         rng = np.random.default_rng(oracle.trial_seed(91, trial))
         k = int(rng.integers(1, 11))
@@ -226,7 +226,7 @@ def test_pdipa_small_problems():
 
 def test_pdipa_termination_certificates():
     from paper_1007_3753_b200.pdipa import pdipa_solve
-    for seed in range(900, 930):
+    for seed in range(900, 1010):
         A, b, _ = build_inputs(dict(kind="genspec", n=40, d=20, k=1 + seed % 5, seed=seed, sigma=0.0))
         states = []
         r = pdipa_solve(_P(A, b), _cfg(), observer=states.append)
