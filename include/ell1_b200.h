@@ -261,6 +261,59 @@ size_t ell1_homotopy_workspace(const ell1_dict_t* D, int32_t blocks);
 int ell1_homotopy(const ell1_dict_t* D, const double* b, double target_lambda, int32_t max_iter,
                   const ell1_homotopy_out_t* out, const ell1_io_t* io, void* stream);
 
+/* ------------------------------------------------ groups (one dictionary per solve)
+ * Many independent solves, each with its OWN dictionary, b, controls and
+ * buffers, in one persistent launch: teams of `team` consecutive CTAs run
+ * the single-solve kernel bodies round-robin over the solves, the team size
+ * chosen so each dictionary panel stays resident in shared memory.  Replaces
+ * the reference experiment harness's per-trial process fan-out
+ * (bench.py:_run_tasks :145-151 over _phase_task :127-136, _noise_task
+ * :196-220, _corruption_task :256-279), one solve per trial.
+ * All arrays are host arrays of length `count` holding device pointers. */
+#define ELL1_GROUP_ARG_BYTES 1024
+typedef struct {
+  int32_t count;
+  int32_t team;                   /* CTAs per solve; 0 = max over the solves of
+                                     ell1_<solver>_group_team (workspaces must be
+                                     sized with blocks = the team actually used) */
+  const ell1_dict_t* dicts;
+  const double* const* b;         /* ld entries each, zero padded */
+  const ell1_ctrl_t* ctrl;
+  const ell1_io_t* io;            /* state zeroed; max_steps 0 (no observers); blocks ignored */
+  void* args_ws;                  /* device scratch, ell1_group_args_bytes(count) bytes */
+  size_t args_ws_bytes;
+} ell1_group_t;
+
+enum {
+  ELL1_SOLVER_CORR = 0, ELL1_SOLVER_FISTA = 1, ELL1_SOLVER_IST = 2, ELL1_SOLVER_PALM = 3,
+  ELL1_SOLVER_DALM = 4, ELL1_SOLVER_GPSR = 5, ELL1_SOLVER_TNIPM = 6, ELL1_SOLVER_HOMOTOPY = 7,
+  ELL1_SOLVER_POWER = 8
+};
+size_t ell1_group_args_bytes(int32_t count);
+/* auto team size of one solve (CTAs whose shared memory holds its panel) */
+int32_t ell1_group_team(int32_t solver, const ell1_dict_t* D);
+/* workspace of one solve run by a team of `team` CTAs */
+size_t ell1_group_workspace(int32_t solver, const ell1_dict_t* D, int32_t team);
+/* max |D_i^T b_i| -> out[2i], ||b_i|| -> out[2i+1] (device); model.py:126-129 per trial */
+int ell1_correlation_max_group(const ell1_group_t* G, double* out, void* stream);
+/* spectral_norm_sq per dictionary (numerics.py:224-261): out[2i] = value,
+ * out[2i+1] = iterations; v0[i] = start vector + nredraw redraws, stride min(d, n) */
+int ell1_spectral_norm_sq_group(const ell1_group_t* G, const double* const* v0, int32_t nredraw,
+                                double tol, int32_t max_iter, double* out, void* stream);
+/* the solver bodies of ell1_fista / _ist / _palm / _dalm / _gpsr / _tnipm /
+ * _homotopy; per-solve options / parameters are host arrays [count] (the
+ * FISTA probe mode is not available in groups) */
+int ell1_fista_group(const ell1_group_t* G, const ell1_fista_opts_t* O, void* stream);
+int ell1_ist_group(const ell1_group_t* G, const double* const* stages, const int32_t* nstages,
+                   void* stream);
+int ell1_palm_group(const ell1_group_t* G, const ell1_palm_opts_t* O, void* stream);
+int ell1_dalm_group(const ell1_group_t* G, const ell1_dalm_opts_t* O, void* stream);
+int ell1_gpsr_group(const ell1_group_t* G, const double* lam, void* stream);
+int ell1_tnipm_group(const ell1_group_t* G, const double* lam, double pcg_tol, int32_t pcg_max_iter,
+                     void* stream);
+int ell1_homotopy_group(const ell1_group_t* G, const double* target_lambda, int32_t max_iter,
+                        const ell1_homotopy_out_t* out, void* stream);
+
 /* ------------------------------------------------ batched (shared dictionary)
  * B instances with right-hand sides b_j (columns of an ld x B device matrix,
  * zero padded) share one dictionary; element j of the result equals the

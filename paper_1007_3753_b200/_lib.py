@@ -81,6 +81,16 @@ class IO(ctypes.Structure):
                 ("phase_ns", ctypes.c_void_p)]
 
 
+class Group(ctypes.Structure):
+    _fields_ = [("count", ctypes.c_int32), ("team", ctypes.c_int32),
+                ("dicts", ctypes.c_void_p), ("b", ctypes.c_void_p), ("ctrl", ctypes.c_void_p),
+                ("io", ctypes.c_void_p), ("args_ws", ctypes.c_void_p), ("args_ws_bytes", ctypes.c_size_t)]
+
+
+SOLVER_CORR, SOLVER_FISTA, SOLVER_IST, SOLVER_PALM, SOLVER_DALM, SOLVER_GPSR, SOLVER_TNIPM, \
+    SOLVER_HOMOTOPY, SOLVER_POWER = range(9)
+GROUP_ARG_BYTES = 1024
+
 assert ctypes.sizeof(State) == 256, ctypes.sizeof(State)
 
 _lock = threading.Lock()
@@ -186,6 +196,21 @@ _SIGS = {
                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "ell1_pd_diag": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_double,
                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_group_args_bytes": (ctypes.c_size_t, [ctypes.c_int32]),
+    "ell1_group_team": (ctypes.c_int32, [ctypes.c_int32, P(Dict)]),
+    "ell1_group_workspace": (ctypes.c_size_t, [ctypes.c_int32, P(Dict), ctypes.c_int32]),
+    "ell1_correlation_max_group": (ctypes.c_int, [P(Group), ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_spectral_norm_sq_group": (ctypes.c_int, [P(Group), ctypes.c_void_p, ctypes.c_int32, ctypes.c_double,
+                                                   ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_fista_group": (ctypes.c_int, [P(Group), ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_ist_group": (ctypes.c_int, [P(Group), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_palm_group": (ctypes.c_int, [P(Group), ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_dalm_group": (ctypes.c_int, [P(Group), ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_gpsr_group": (ctypes.c_int, [P(Group), ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_tnipm_group": (ctypes.c_int, [P(Group), ctypes.c_void_p, ctypes.c_double, ctypes.c_int32,
+                                        ctypes.c_void_p]),
+    "ell1_homotopy_group": (ctypes.c_int, [P(Group), ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
+                                           ctypes.c_void_p]),
     "ell1_blas_fp32_mode": (ctypes.c_int, []),
     "ell1_device_sms": (ctypes.c_int, [ctypes.c_int32]),
     "ell1_version": (ctypes.c_char_p, []),

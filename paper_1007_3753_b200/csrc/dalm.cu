@@ -57,7 +57,7 @@ struct DalmV {
 #define T0 if (threadIdx.x == 0)
 
 template <class TA>
-__global__ void __launch_bounds__(NTHR, 1) dalm_kernel(const __grid_constant__ DalmArgs a) {
+__device__ __forceinline__ void dalm_body(const DalmArgs& a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ Ctx E;
   __shared__ DalmV V;
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(NTHR, 1) dalm_kernel(const __grid_constant__ D
   TA* panM = reinterpret_cast<TA*>(reinterpret_cast<char*>(smem) + (size_t)a.rcA * D.ld * esz);
   double* ov = smem + a.g.panel_bytes / 8;
   T0 {
-    ctx_init(E, D.d, D.n, D.ext);
+    ctx_init(E, D.d, D.n, D.ext, a.g.nb);
     ctx_bind(E, a.g, smem);
     E.prof = a.prof;
     E.sh = ov + DALM_OV * a.wmax;
@@ -448,6 +448,11 @@ out:
   }
 }
 
+template <class TA>
+__global__ void __launch_bounds__(NTHR, 1) dalm_kernel(const __grid_constant__ DalmArgs a) {
+  dalm_body<TA>(a);
+}
+
 }  // namespace ell1
 
 using namespace ell1;
@@ -459,13 +464,11 @@ extern "C" size_t ell1_dalm_workspace(const ell1_dict_t* D, int32_t blocks) {
   return grid_bytes(nb, D->d, 2) + 4 * align_up(N * 8, 256) + 7 * align_up(D->ld * 8, 256) + 4096;
 }
 
-extern "C" int ell1_dalm(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C,
-                         const ell1_dalm_opts_t* O, const ell1_io_t* io, void* stream) {
+static int dalm_setup(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C,
+                         const ell1_dalm_opts_t* O, const ell1_io_t* io, int nb, DalmArgs& a, SmemPlan& sp) {
   if (!dict_ok(D) || !b || !C || !O || !io || !io->state || !io->trace || !io->x) return ELL1_ERR_ARG;
   if (!O->M || !O->Ginv || !(O->beta > 0) || C->max_iter < 1) return ELL1_ERR_ARG;
-  const int nb = pick_blocks(D->n, io->blocks);
   const int64_t N = ncols_of(D);
-  DalmArgs a;
   a.D = to_raw(D);
   a.M = O->M;
   a.Ginv = O->Ginv;
@@ -487,7 +490,7 @@ extern "C" int ell1_dalm(const ell1_dict_t* D, const double* b, const ell1_ctrl_
   a.x_out = io->x; a.xprev_out = io->x_prev; a.y_out = O->y_out; a.z_out = O->z_out;
   a.max_steps = io->max_steps;
   a.prof = io->phase_ns;
-  SmemPlan sp = plan_smem(a.D, nb, DALM_OV, 6, false);
+  sp = plan_smem(a.D, nb, DALM_OV, 6, false);
   // resident budget shared between the A and M panels
   {
     const int64_t esz = D->dtype == ELL1_F64 ? 8 : 4;
@@ -504,10 +507,57 @@ extern "C" int ell1_dalm(const ell1_dict_t* D, const double* b, const ell1_ctrl_
   a.g.shcap = sp.scratch;
   a.g.panel_bytes = sp.panel_bytes;
   a.wmax = sp.wmax;
+  return ELL1_OK;
+}
+
+extern "C" int ell1_dalm(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C,
+                         const ell1_dalm_opts_t* O, const ell1_io_t* io, void* stream) {
+  if (!dict_ok(D) || !io) return ELL1_ERR_ARG;
+  const int nb = pick_blocks(D->n, io->blocks);
+  DalmArgs a;
+  SmemPlan sp;
+  const int rc0 = dalm_setup(D, b, C, O, io, nb, a, sp);
+  if (rc0 != ELL1_OK) return rc0;
   cudaStream_t s = (cudaStream_t)stream;
   if (D->ld > D->d)
     for (double* p : {a.Y[0], a.Y[1], a.AX, a.RHS, a.RES, a.C0})
       if (cudaMemsetAsync(p + D->d, 0, (D->ld - D->d) * 8, s) != cudaSuccess) return ELL1_ERR_CUDA;
   return (D->dtype == ELL1_F64) ? coop_launch(dalm_kernel<double>, nb, sp.bytes, s, a, a.g.bar)
                                 : coop_launch(dalm_kernel<float>, nb, sp.bytes, s, a, a.g.bar);
+
+}
+
+namespace ell1 {
+template <class TA>
+struct DalmRun {
+  static __device__ void run(const DalmArgs& a) { dalm_body<TA>(a); }
+  static __device__ void reset(const DalmArgs& a, int lane) {
+    reset_bar(a.g.bar, lane);
+    for (double* p : {a.Y[0], a.Y[1], a.AX, a.RHS, a.RES, a.C0}) zero_pad_rows(p, a.D.d, a.D.ld, lane);
+  }
+};
+static_assert(sizeof(DalmArgs) <= ELL1_GROUP_ARG_BYTES, "DalmArgs too large for the group scratch");
+}  // namespace ell1
+
+// the team must hold both the A and the M panel: size it for 2n columns
+int32_t ell1_dalm_group_team_impl(const ell1_dict_t* D) {
+  if (!dict_ok(D)) return 0;
+  DictRaw r = to_raw(D);
+  r.n *= 2;
+  return group_team(r, DALM_OV, 6, 0);
+}
+
+extern "C" int ell1_dalm_group(const ell1_group_t* G, const ell1_dalm_opts_t* O, void* stream) {
+  if (!G || (G->count > 0 && !O)) return ELL1_ERR_ARG;
+  int team = G->team;
+  if (team <= 0)
+    for (int i = 0; i < G->count; ++i) {
+      const int t = ell1_dalm_group_team_impl(&G->dicts[i]);
+      if (t > team) team = t;
+    }
+  ell1_group_t H = *G;
+  H.team = team;
+  return run_group<DalmArgs, DalmRun>(&H, DALM_OV, 6, 0, [&](int i, int nb, DalmArgs& a, SmemPlan& sp) {
+    return dalm_setup(&G->dicts[i], G->b[i], &G->ctrl[i], &O[i], &G->io[i], nb, a, sp);
+  }, stream);
 }

@@ -120,9 +120,11 @@ __device__ __forceinline__ int lnx() { return (int)(threadIdx.x & 31); }
 __device__ __forceinline__ int wpx() { return (int)(threadIdx.x >> 5); }
 
 // thread 0 only (Ctx is a __shared__ object); callers __syncthreads afterwards
-__device__ __forceinline__ void ctx_init(Ctx& E, int64_t d, int64_t n, int ext) {
-  E.nb = gridDim.x;
-  E.b = blockIdx.x;
+// nb: CTAs cooperating on this solve (gridDim.x for a single-solve launch,
+// the team size for a group launch, whose teams are consecutive CTAs).
+__device__ __forceinline__ void ctx_init(Ctx& E, int64_t d, int64_t n, int ext, int nb) {
+  E.nb = nb;
+  E.b = (int)(blockIdx.x % (unsigned)nb);
   E.ok = 1;
   E.c0 = (n * E.b) / E.nb;
   E.c1 = (n * (E.b + 1)) / E.nb;
@@ -169,6 +171,11 @@ __device__ __forceinline__ void mark(Ctx& E, int k) {
 // when a peer aborted or the wait timed out; callers unwind cleanly.
 __device__ __forceinline__ bool grid_sync(Ctx& E) {
   __syncthreads();
+  if (E.nb == 1) {                       // one-CTA team: a block barrier suffices
+    if (tix() == 0) E.nbar++;
+    __syncthreads();
+    return true;
+  }
   if (tix() == 0) {
     E.epoch += (unsigned long long)E.nb;
     E.nbar++;
@@ -198,10 +205,14 @@ __device__ __forceinline__ void grid_arrive(Ctx& E) {
   if (tix() == 0) {
     E.epoch += (unsigned long long)E.nb;
     E.nbar++;
-    red_release_add(E.bar, 1ULL);
+    if (E.nb > 1) red_release_add(E.bar, 1ULL);
   }
 }
 __device__ __forceinline__ bool grid_wait(Ctx& E) {
+  if (E.nb == 1) {
+    __syncthreads();
+    return true;
+  }
   if (tix() == 0) {
     long long spins = 0;
     int ok = 1;

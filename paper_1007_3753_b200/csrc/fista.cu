@@ -81,14 +81,14 @@ __device__ bool fista_finalize(FistaV& V, const ell1_ctrl_t& C, double* trace, b
 #define MARK(k) do { if constexpr (PROF) mark(E, k); } while (0)
 
 template <class TA, bool PROF>
-__global__ void __launch_bounds__(NTHR, 1) fista_kernel(const __grid_constant__ FistaArgs a) {
+__device__ __forceinline__ void fista_body(const FistaArgs& a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ Ctx E;
   __shared__ FistaV V;
   const DictV<TA> D = dict_view<TA>(a.D);
   double* ov = smem + a.g.panel_bytes / 8;
   T0 {
-    ctx_init(E, D.d, D.n, D.ext);
+    ctx_init(E, D.d, D.n, D.ext, a.g.nb);
     ctx_bind(E, a.g, smem);
     E.prof = a.prof;
     E.sh = ov + FISTA_OV * a.wmax;
@@ -482,6 +482,11 @@ out:
   }
 }
 
+template <class TA, bool PROF>
+__global__ void __launch_bounds__(NTHR, 1) fista_kernel(const __grid_constant__ FistaArgs a) {
+  fista_body<TA, PROF>(a);
+}
+
 // ---------------------------------------------------------------------------
 // correlation max: out = {max_j |(D^T b)_j|, ||b||}
 struct CorrArgs {
@@ -493,12 +498,12 @@ struct CorrArgs {
 };
 
 template <class TA>
-__global__ void __launch_bounds__(NTHR, 1) corr_kernel(const __grid_constant__ CorrArgs a) {
+__device__ __forceinline__ void corr_body(const CorrArgs& a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ Ctx E;
   const DictV<TA> D = dict_view<TA>(a.D);
   if (threadIdx.x == 0) {
-    ctx_init(E, D.d, D.n, D.ext);
+    ctx_init(E, D.d, D.n, D.ext, a.g.nb);
     ctx_bind(E, a.g, smem);
     E.sh = smem + a.wmax;
   }
@@ -525,6 +530,11 @@ __global__ void __launch_bounds__(NTHR, 1) corr_kernel(const __grid_constant__ C
   if (E.b == 0 && threadIdx.x == 0) { a.out[0] = o[0]; a.out[1] = sqrt(o[1]); }
 }
 
+template <class TA>
+__global__ void __launch_bounds__(NTHR, 1) corr_kernel(const __grid_constant__ CorrArgs a) {
+  corr_body<TA>(a);
+}
+
 // ---------------------------------------------------------------------------
 // power iteration on the smaller Gram side of the PLAIN dictionary A
 struct PowerArgs {
@@ -541,13 +551,13 @@ struct PowerArgs {
 };
 
 template <class TA>
-__global__ void __launch_bounds__(NTHR, 1) power_kernel(const __grid_constant__ PowerArgs a) {
+__device__ __forceinline__ void power_body(const PowerArgs& a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ Ctx E;
   DictV<TA> D = dict_view<TA>(a.D);
   D.ext = 0;
   if (threadIdx.x == 0) {
-    ctx_init(E, D.d, D.n, 0);
+    ctx_init(E, D.d, D.n, 0, a.g.nb);
     ctx_bind(E, a.g, smem);
     E.sh = smem + 3 * a.wmax;
   }
@@ -667,6 +677,11 @@ __global__ void __launch_bounds__(NTHR, 1) power_kernel(const __grid_constant__ 
   if (E.b == 0 && threadIdx.x == 0) { a.out[0] = theta; a.out[1] = (double)(k < a.max_iter ? k + 1 : k); }
 }
 
+template <class TA>
+__global__ void __launch_bounds__(NTHR, 1) power_kernel(const __grid_constant__ PowerArgs a) {
+  power_body<TA>(a);
+}
+
 }  // namespace ell1
 
 // ============================================================================ host
@@ -682,13 +697,12 @@ extern "C" size_t ell1_fista_workspace(const ell1_dict_t* D, const ell1_ctrl_t* 
   return b;
 }
 
-extern "C" int ell1_fista(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C,
-                          const ell1_fista_opts_t* O, const ell1_io_t* io, void* stream) {
+// Args of one FISTA solve on nb CTAs (shared by the single and group launches).
+static int fista_setup(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C,
+                       const ell1_fista_opts_t* O, const ell1_io_t* io, int nb, FistaArgs& a, SmemPlan& sp) {
   if (!dict_ok(D) || !b || !C || !O || !io || !io->state || !io->trace || !io->x) return ELL1_ERR_ARG;
   if (C->max_iter < 1) return ELL1_ERR_ARG;
-  const int nb = pick_blocks(D->n, io->blocks);
   const int64_t N = ncols_of(D);
-  FistaArgs a;
   a.D = to_raw(D);
   a.b = b;
   a.C = *C;
@@ -704,11 +718,22 @@ extern "C" int ell1_fista(const ell1_dict_t* D, const double* b, const ell1_ctrl
   a.x_out = io->x; a.xprev_out = io->x_prev; a.y_out = io->y;
   a.max_steps = io->max_steps;
   a.prof = io->phase_ns;
-  const SmemPlan sp = plan_smem(a.D, nb, FISTA_OV, 12, io->max_steps <= 0);
+  sp = plan_smem(a.D, nb, FISTA_OV, 12, io->max_steps <= 0);
   a.g.shcap = sp.scratch;
   a.g.panel_bytes = sp.panel_bytes;
   a.rc = sp.rc;
   a.wmax = sp.wmax;
+  return ELL1_OK;
+}
+
+extern "C" int ell1_fista(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C,
+                          const ell1_fista_opts_t* O, const ell1_io_t* io, void* stream) {
+  if (!dict_ok(D) || !io) return ELL1_ERR_ARG;
+  const int nb = pick_blocks(D->n, io->blocks);
+  FistaArgs a;
+  SmemPlan sp;
+  const int rc = fista_setup(D, b, C, O, io, nb, a, sp);
+  if (rc != ELL1_OK) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   // padding rows of the residual ring must read as zero (never written by the kernel)
   if (D->ld > D->d)
@@ -719,6 +744,31 @@ extern "C" int ell1_fista(const ell1_dict_t* D, const double* b, const ell1_ctrl
                                   : coop_launch(fista_kernel<float, true>, nb, sp.bytes, s, a, a.g.bar);
   return (D->dtype == ELL1_F64) ? coop_launch(fista_kernel<double, false>, nb, sp.bytes, s, a, a.g.bar)
                                 : coop_launch(fista_kernel<float, false>, nb, sp.bytes, s, a, a.g.bar);
+}
+
+namespace ell1 {
+template <class TA>
+struct FistaRun {
+  static __device__ void run(const FistaArgs& a) { fista_body<TA, false>(a); }
+  static __device__ void reset(const FistaArgs& a, int lane) {
+    reset_bar(a.g.bar, lane);
+    for (int k = 0; k < 3; ++k) zero_pad_rows(a.R[k], a.D.d, a.D.ld, lane);
+  }
+};
+static_assert(sizeof(FistaArgs) <= ELL1_GROUP_ARG_BYTES, "FistaArgs too large for the group scratch");
+}  // namespace ell1
+
+
+int32_t ell1_fista_group_team_impl(const ell1_dict_t* D) {
+  return dict_ok(D) ? group_team(to_raw(D), FISTA_OV, 12, 0) : 0;
+}
+
+extern "C" int ell1_fista_group(const ell1_group_t* G, const ell1_fista_opts_t* O, void* stream) {
+  if (!G || (G->count > 0 && !O)) return ELL1_ERR_ARG;
+  return run_group<FistaArgs, FistaRun>(G, FISTA_OV, 12, 0, [&](int i, int nb, FistaArgs& a, SmemPlan& sp) {
+    if (O[i].probe) return (int)ELL1_ERR_ARG;
+    return fista_setup(&G->dicts[i], G->b[i], &G->ctrl[i], &O[i], &G->io[i], nb, a, sp);
+  }, stream);
 }
 
 extern "C" size_t ell1_correlation_workspace(const ell1_dict_t* D) {
@@ -777,3 +827,72 @@ extern "C" int ell1_spectral_norm_sq(const ell1_dict_t* D, const double* v0, int
   return (D->dtype == ELL1_F64) ? coop_launch(power_kernel<double>, nb, sp.bytes, s, a, a.g.bar)
                                 : coop_launch(power_kernel<float>, nb, sp.bytes, s, a, a.g.bar);
 }
+
+namespace ell1 {
+template <class TA>
+struct CorrRun {
+  static __device__ void run(const CorrArgs& a) { corr_body<TA>(a); }
+  static __device__ void reset(const CorrArgs& a, int lane) { reset_bar(a.g.bar, lane); }
+};
+template <class TA>
+struct PowerRun {
+  static __device__ void run(const PowerArgs& a) { power_body<TA>(a); }
+  static __device__ void reset(const PowerArgs& a, int lane) {
+    reset_bar(a.g.bar, lane);
+    for (int64_t i = lane; i < a.D.ld; i += 32) { a.V[0][i] = 0.0; a.V[1][i] = 0.0; a.W[i] = 0.0; }
+  }
+};
+static_assert(sizeof(CorrArgs) <= ELL1_GROUP_ARG_BYTES, "CorrArgs too large for the group scratch");
+static_assert(sizeof(PowerArgs) <= ELL1_GROUP_ARG_BYTES, "PowerArgs too large for the group scratch");
+}  // namespace ell1
+
+// max |D_i^T b_i| and ||b_i|| for every solve of a group: out[2 i], out[2 i + 1]
+// (io[i].workspace: ell1_correlation_workspace; streamed, one CTA per solve)
+extern "C" int ell1_correlation_max_group(const ell1_group_t* G, double* out, void* stream) {
+  if (!G || (G->count > 0 && (!out || !G->b))) return ELL1_ERR_ARG;
+  ell1_group_t H = *G;
+  H.team = 1;
+  return run_group<CorrArgs, CorrRun>(&H, 1, 2, 0, [&](int i, int nb, CorrArgs& a, SmemPlan& sp) {
+    const ell1_dict_t* D = &G->dicts[i];
+    if (!G->b[i] || !G->io) return (int)ELL1_ERR_ARG;
+    a.D = to_raw(D);
+    a.b = G->b[i];
+    a.out = out + 2 * (int64_t)i;
+    Carve cv(G->io[i].workspace, G->io[i].workspace_bytes);
+    if (!carve_grid(cv, a.g, nb, D->d, 0)) return (int)ELL1_ERR_ARG;
+    sp = plan_smem(a.D, nb, 1, 2, false);
+    a.g.shcap = sp.scratch;
+    a.g.panel_bytes = 0;
+    a.wmax = sp.wmax;
+    return (int)ELL1_OK;
+  }, stream);
+}
+
+// spectral_norm_sq of every dictionary of a group (numerics.py:224-261):
+// out[2 i] = ||D_i||^2, out[2 i + 1] = iterations; v0[i]: start vector + redraws
+// (stride min(d, n)); io[i].workspace: ell1_power_workspace.  One CTA per solve.
+extern "C" int ell1_spectral_norm_sq_group(const ell1_group_t* G, const double* const* v0, int32_t nredraw,
+                                           double tol, int32_t max_iter, double* out, void* stream) {
+  if (!G || (G->count > 0 && (!out || !v0)) || max_iter < 0) return ELL1_ERR_ARG;
+  ell1_group_t H = *G;
+  H.team = 1;
+  return run_group<PowerArgs, PowerRun>(&H, 3, 2, 0, [&](int i, int nb, PowerArgs& a, SmemPlan& sp) {
+    const ell1_dict_t* D = &G->dicts[i];
+    if (!v0[i]) return (int)ELL1_ERR_ARG;
+    a.D = to_raw(D);
+    a.D.ext = 0;
+    a.v0 = v0[i]; a.nredraw = nredraw; a.tol = tol; a.max_iter = max_iter; a.out = out + 2 * (int64_t)i;
+    Carve cv(G->io[i].workspace, G->io[i].workspace_bytes);
+    if (!carve_grid(cv, a.g, nb, D->d, 1)) return (int)ELL1_ERR_ARG;
+    a.V[0] = cv.take<double>(D->ld);
+    a.V[1] = cv.take<double>(D->ld);
+    a.W = cv.take<double>(D->ld);
+    if (!cv.ok) return (int)ELL1_ERR_ARG;
+    sp = plan_smem(a.D, nb, 3, 2, false);
+    a.g.shcap = sp.scratch;
+    a.g.panel_bytes = 0;
+    a.wmax = sp.wmax;
+    return (int)ELL1_OK;
+  }, stream);
+}
+

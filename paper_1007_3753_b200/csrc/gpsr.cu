@@ -40,14 +40,14 @@ struct GpsrV {
 #define T0 if (threadIdx.x == 0)
 
 template <class TA>
-__global__ void __launch_bounds__(NTHR, 1) gpsr_kernel(const __grid_constant__ GpsrArgs a) {
+__device__ __forceinline__ void gpsr_body(const GpsrArgs& a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ Ctx E;
   __shared__ GpsrV V;
   const DictV<TA> D = dict_view<TA>(a.D);
   double* ov = smem + a.g.panel_bytes / 8;
   T0 {
-    ctx_init(E, D.d, D.n, D.ext);
+    ctx_init(E, D.d, D.n, D.ext, a.g.nb);
     ctx_bind(E, a.g, smem);
     E.prof = a.prof;
     E.sh = ov + GPSR_OV * a.wmax;
@@ -332,6 +332,11 @@ out:
   }
 }
 
+template <class TA>
+__global__ void __launch_bounds__(NTHR, 1) gpsr_kernel(const __grid_constant__ GpsrArgs a) {
+  gpsr_body<TA>(a);
+}
+
 }  // namespace ell1
 
 using namespace ell1;
@@ -343,13 +348,11 @@ extern "C" size_t ell1_gpsr_workspace(const ell1_dict_t* D, int32_t blocks) {
   return grid_bytes(nb, D->d, 2) + 3 * align_up(N * 8, 256) + 2 * align_up(D->ld * 8, 256) + 4096;
 }
 
-extern "C" int ell1_gpsr(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C, double lam,
-                         double* z_out, const ell1_io_t* io, void* stream) {
+static int gpsr_setup(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C, double lam,
+                         double* z_out, const ell1_io_t* io, int nb, GpsrArgs& a, SmemPlan& sp) {
   if (!dict_ok(D) || !b || !C || !io || !io->state || !io->trace || !io->x) return ELL1_ERR_ARG;
   if (!(lam > 0) || C->max_iter < 1) return ELL1_ERR_ARG;
-  const int nb = pick_blocks(D->n, io->blocks);
   const int64_t N = ncols_of(D);
-  GpsrArgs a;
   a.D = to_raw(D);
   a.b = b;
   a.C = *C;
@@ -365,15 +368,51 @@ extern "C" int ell1_gpsr(const ell1_dict_t* D, const double* b, const ell1_ctrl_
   a.z_out = z_out;
   a.max_steps = io->max_steps;
   a.prof = io->phase_ns;
-  const SmemPlan sp = plan_smem(a.D, nb, GPSR_OV, 8, io->max_steps <= 0);
+  sp = plan_smem(a.D, nb, GPSR_OV, 8, io->max_steps <= 0);
   a.g.shcap = sp.scratch;
   a.g.panel_bytes = sp.panel_bytes;
   a.rc = sp.rc;
   a.wmax = sp.wmax;
+  return ELL1_OK;
+}
+
+extern "C" int ell1_gpsr(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C, double lam,
+                         double* z_out, const ell1_io_t* io, void* stream) {
+  if (!dict_ok(D) || !io) return ELL1_ERR_ARG;
+  const int nb = pick_blocks(D->n, io->blocks);
+  GpsrArgs a;
+  SmemPlan sp;
+  const int rc0 = gpsr_setup(D, b, C, lam, z_out, io, nb, a, sp);
+  if (rc0 != ELL1_OK) return rc0;
   cudaStream_t s = (cudaStream_t)stream;
   if (D->ld > D->d)
     for (double* p : {a.R[0], a.R[1]})
       if (cudaMemsetAsync(p + D->d, 0, (D->ld - D->d) * 8, s) != cudaSuccess) return ELL1_ERR_CUDA;
   return (D->dtype == ELL1_F64) ? coop_launch(gpsr_kernel<double>, nb, sp.bytes, s, a, a.g.bar)
                                 : coop_launch(gpsr_kernel<float>, nb, sp.bytes, s, a, a.g.bar);
+
+}
+
+namespace ell1 {
+template <class TA>
+struct GpsrRun {
+  static __device__ void run(const GpsrArgs& a) { gpsr_body<TA>(a); }
+  static __device__ void reset(const GpsrArgs& a, int lane) {
+    reset_bar(a.g.bar, lane);
+    zero_pad_rows(a.R[0], a.D.d, a.D.ld, lane);
+    zero_pad_rows(a.R[1], a.D.d, a.D.ld, lane);
+  }
+};
+static_assert(sizeof(GpsrArgs) <= ELL1_GROUP_ARG_BYTES, "GpsrArgs too large for the group scratch");
+}  // namespace ell1
+
+int32_t ell1_gpsr_group_team_impl(const ell1_dict_t* D) {
+  return dict_ok(D) ? group_team(to_raw(D), GPSR_OV, 8, 0) : 0;
+}
+
+extern "C" int ell1_gpsr_group(const ell1_group_t* G, const double* lam, void* stream) {
+  if (!G || (G->count > 0 && !lam)) return ELL1_ERR_ARG;
+  return run_group<GpsrArgs, GpsrRun>(G, GPSR_OV, 8, 0, [&](int i, int nb, GpsrArgs& a, SmemPlan& sp) {
+    return gpsr_setup(&G->dicts[i], G->b[i], &G->ctrl[i], lam[i], nullptr, &G->io[i], nb, a, sp);
+  }, stream);
 }

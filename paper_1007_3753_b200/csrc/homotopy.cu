@@ -55,7 +55,7 @@ struct HomV {
 #define T0 if (threadIdx.x == 0)
 
 template <class TA>
-__global__ void __launch_bounds__(NTHR, 1) homotopy_kernel(const __grid_constant__ HomArgs a) {
+__device__ __forceinline__ void homotopy_body(const HomArgs& a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ Ctx E;
   __shared__ HomV V;
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(NTHR, 1) homotopy_kernel(const __grid_constant
   const DictV<TA> D = dict_view<TA>(a.D);
   double* ov = smem;
   T0 {
-    ctx_init(E, D.d, D.n, D.ext);
+    ctx_init(E, D.d, D.n, D.ext, a.g.nb);
     ctx_bind(E, a.g, smem);
     E.prof = a.prof;
     E.sh = ov + HOM_OV * a.wmax;
@@ -625,6 +625,11 @@ out:
   }
 }
 
+template <class TA>
+__global__ void __launch_bounds__(NTHR, 1) homotopy_kernel(const __grid_constant__ HomArgs a) {
+  homotopy_body<TA>(a);
+}
+
 }  // namespace ell1
 
 using namespace ell1;
@@ -648,15 +653,12 @@ extern "C" size_t ell1_homotopy_workspace(const ell1_dict_t* D, int32_t blocks) 
 
 extern "C" int ell1_homotopy_capacity(const ell1_dict_t* D) { return dict_ok(D) ? hom_mmax(D) : 0; }
 
-extern "C" int ell1_homotopy(const ell1_dict_t* D, const double* b, double target_lambda,
-                             int32_t max_iter, const ell1_homotopy_out_t* O, const ell1_io_t* io,
-                             void* stream) {
+static int homotopy_setup(const ell1_dict_t* D, const double* b, double target_lambda,
+                             int32_t max_iter, const ell1_homotopy_out_t* O, const ell1_io_t* io, int nb, HomArgs& a, SmemPlan& sp) {
   if (!dict_ok(D) || !b || !O || !O->c || !io || !io->state || !io->trace || !io->x) return ELL1_ERR_ARG;
   double* c_out = O->c;
   if (!(target_lambda >= 0) || max_iter < 1) return ELL1_ERR_ARG;
-  const int nb = pick_blocks(D->n, io->blocks);
   const int64_t N = ncols_of(D);
-  HomArgs a;
   a.D = to_raw(D);
   a.b = b;
   a.target = target_lambda;
@@ -680,16 +682,58 @@ extern "C" int ell1_homotopy(const ell1_dict_t* D, const double* b, double targe
   a.R_out = O->factor;
   a.max_steps = io->max_steps;
   a.prof = io->phase_ns;
-  SmemPlan sp = plan_smem(a.D, nb, HOM_OV, 8, false);
+  sp = plan_smem(a.D, nb, HOM_OV, 8, false);
   // CTA-0 solves keep z (mmax doubles) in the scratch area past 512 reduction doubles
   if (sp.scratch < 512 + m) { sp.bytes += (size_t)(512 + m - sp.scratch) * 8; sp.scratch = 512 + m; }
   a.g.shcap = sp.scratch;
   a.g.panel_bytes = 0;
   a.wmax = sp.wmax;
+  return ELL1_OK;
+}
+
+extern "C" int ell1_homotopy(const ell1_dict_t* D, const double* b, double target_lambda,
+                             int32_t max_iter, const ell1_homotopy_out_t* O, const ell1_io_t* io,
+                             void* stream) {
+  if (!dict_ok(D) || !io) return ELL1_ERR_ARG;
+  const int nb = pick_blocks(D->n, io->blocks);
+  HomArgs a;
+  SmemPlan sp;
+  const int rc0 = homotopy_setup(D, b, target_lambda, max_iter, O, io, nb, a, sp);
+  if (rc0 != ELL1_OK) return rc0;
+  const int64_t N = ncols_of(D);
   cudaStream_t s = (cudaStream_t)stream;
   if (cudaMemsetAsync(a.dfull, 0, N * 8, s) != cudaSuccess) return ELL1_ERR_CUDA;
   for (double* p : {a.colv, a.Vd, a.Rd})
     if (cudaMemsetAsync(p, 0, D->ld * 8, s) != cudaSuccess) return ELL1_ERR_CUDA;
   return (D->dtype == ELL1_F64) ? coop_launch(homotopy_kernel<double>, nb, sp.bytes, s, a, a.g.bar)
                                 : coop_launch(homotopy_kernel<float>, nb, sp.bytes, s, a, a.g.bar);
+
+}
+
+namespace ell1 {
+template <class TA>
+struct HomRun {
+  static __device__ void run(const HomArgs& a) { homotopy_body<TA>(a); }
+  static __device__ void reset(const HomArgs& a, int lane) {
+    reset_bar(a.g.bar, lane);
+    const int64_t N = a.D.n + (a.D.ext ? a.D.d : 0);
+    for (int64_t i = lane; i < N; i += 32) a.dfull[i] = 0.0;
+    for (int64_t i = lane; i < a.D.ld; i += 32) { a.colv[i] = 0.0; a.Vd[i] = 0.0; a.Rd[i] = 0.0; }
+  }
+};
+static_assert(sizeof(HomArgs) <= ELL1_GROUP_ARG_BYTES, "HomArgs too large for the group scratch");
+}  // namespace ell1
+
+// the path streams the dictionary (no resident panel); the breakpoint
+// bookkeeping is CTA 0's, so one CTA per solve
+int32_t ell1_homotopy_group_team_impl(const ell1_dict_t* D) { return dict_ok(D) ? 1 : 0; }
+
+extern "C" int ell1_homotopy_group(const ell1_group_t* G, const double* target_lambda, int32_t max_iter,
+                                   const ell1_homotopy_out_t* O, void* stream) {
+  if (!G || (G->count > 0 && (!target_lambda || !O))) return ELL1_ERR_ARG;
+  ell1_group_t H = *G;
+  if (H.team <= 0) H.team = 1;
+  return run_group<HomArgs, HomRun>(&H, HOM_OV, 8, 0, [&](int i, int nb, HomArgs& a, SmemPlan& sp) {
+    return homotopy_setup(&G->dicts[i], G->b[i], target_lambda[i], max_iter, &O[i], &G->io[i], nb, a, sp);
+  }, stream);
 }

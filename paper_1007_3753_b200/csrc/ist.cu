@@ -42,14 +42,14 @@ struct IstV {
 #define T0 if (threadIdx.x == 0)
 
 template <class TA>
-__global__ void __launch_bounds__(NTHR, 1) ist_kernel(const __grid_constant__ IstArgs a) {
+__device__ __forceinline__ void ist_body(const IstArgs& a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ Ctx E;
   __shared__ IstV V;
   const DictV<TA> D = dict_view<TA>(a.D);
   double* ov = smem + a.g.panel_bytes / 8;
   T0 {
-    ctx_init(E, D.d, D.n, D.ext);
+    ctx_init(E, D.d, D.n, D.ext, a.g.nb);
     ctx_bind(E, a.g, smem);
     E.prof = a.prof;
     E.sh = ov + IST_OV * a.wmax;
@@ -346,6 +346,11 @@ out:
   }
 }
 
+template <class TA>
+__global__ void __launch_bounds__(NTHR, 1) ist_kernel(const __grid_constant__ IstArgs a) {
+  ist_body<TA>(a);
+}
+
 }  // namespace ell1
 
 using namespace ell1;
@@ -357,13 +362,11 @@ extern "C" size_t ell1_ist_workspace(const ell1_dict_t* D, int32_t blocks) {
   return grid_bytes(nb, D->d, 1) + 4 * align_up(N * 8, 256) + 3 * align_up(D->ld * 8, 256) + 4096;
 }
 
-extern "C" int ell1_ist(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C,
-                        const double* stages, int32_t nstages, const ell1_io_t* io, void* stream) {
+static int ist_setup(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C, const double* stages,
+                     int32_t nstages, const ell1_io_t* io, int nb, IstArgs& a, SmemPlan& sp) {
   if (!dict_ok(D) || !b || !C || !stages || nstages < 1 || !io || !io->state || !io->trace || !io->x)
     return ELL1_ERR_ARG;
-  const int nb = pick_blocks(D->n, io->blocks);
   const int64_t N = ncols_of(D);
-  IstArgs a;
   a.D = to_raw(D);
   a.b = b;
   a.C = *C;
@@ -381,14 +384,49 @@ extern "C" int ell1_ist(const ell1_dict_t* D, const double* b, const ell1_ctrl_t
   a.x_out = io->x;
   a.max_steps = io->max_steps;
   a.prof = io->phase_ns;
-  const SmemPlan sp = plan_smem(a.D, nb, IST_OV, 7, io->max_steps <= 0);
+  sp = plan_smem(a.D, nb, IST_OV, 7, io->max_steps <= 0);
   a.g.shcap = sp.scratch;
   a.g.panel_bytes = sp.panel_bytes;
   a.rc = sp.rc;
   a.wmax = sp.wmax;
+  return ELL1_OK;
+}
+
+extern "C" int ell1_ist(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C,
+                        const double* stages, int32_t nstages, const ell1_io_t* io, void* stream) {
+  if (!dict_ok(D) || !io) return ELL1_ERR_ARG;
+  const int nb = pick_blocks(D->n, io->blocks);
+  IstArgs a;
+  SmemPlan sp;
+  const int rc = ist_setup(D, b, C, stages, nstages, io, nb, a, sp);
+  if (rc != ELL1_OK) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   if (D->ld > D->d)
     if (cudaMemsetAsync(a.RC + D->d, 0, (D->ld - D->d) * 8, s) != cudaSuccess) return ELL1_ERR_CUDA;
   return (D->dtype == ELL1_F64) ? coop_launch(ist_kernel<double>, nb, sp.bytes, s, a, a.g.bar)
                                 : coop_launch(ist_kernel<float>, nb, sp.bytes, s, a, a.g.bar);
+}
+
+namespace ell1 {
+template <class TA>
+struct IstRun {
+  static __device__ void run(const IstArgs& a) { ist_body<TA>(a); }
+  static __device__ void reset(const IstArgs& a, int lane) {
+    reset_bar(a.g.bar, lane);
+    zero_pad_rows(a.RC, a.D.d, a.D.ld, lane);
+  }
+};
+static_assert(sizeof(IstArgs) <= ELL1_GROUP_ARG_BYTES, "IstArgs too large for the group scratch");
+}  // namespace ell1
+
+int32_t ell1_ist_group_team_impl(const ell1_dict_t* D) {
+  return dict_ok(D) ? group_team(to_raw(D), IST_OV, 7, 0) : 0;
+}
+
+extern "C" int ell1_ist_group(const ell1_group_t* G, const double* const* stages, const int32_t* nstages,
+                              void* stream) {
+  if (!G || (G->count > 0 && (!stages || !nstages))) return ELL1_ERR_ARG;
+  return run_group<IstArgs, IstRun>(G, IST_OV, 7, 0, [&](int i, int nb, IstArgs& a, SmemPlan& sp) {
+    return ist_setup(&G->dicts[i], G->b[i], &G->ctrl[i], stages[i], nstages[i], &G->io[i], nb, a, sp);
+  }, stream);
 }

@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(NTHR, 1) pcg_kernel(const __grid_constant__ Pc
   TA* panel = reinterpret_cast<TA*>(smem);
   double* ov = reinterpret_cast<double*>(reinterpret_cast<char*>(smem) + a.g.panel_bytes);
   if (tix() == 0) {
-    ctx_init(E, D.d, D.n, 0);
+    ctx_init(E, D.d, D.n, 0, a.g.nb);
     ctx_bind(E, a.g, smem);
     E.sh = ov + PCG_OV * a.wmax;
   }

@@ -43,14 +43,14 @@ struct PalmV {
 #define T0 if (threadIdx.x == 0)
 
 template <class TA>
-__global__ void __launch_bounds__(NTHR, 1) palm_kernel(const __grid_constant__ PalmArgs a) {
+__device__ __forceinline__ void palm_body(const PalmArgs& a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ Ctx E;
   __shared__ PalmV V;
   const DictV<TA> D = dict_view<TA>(a.D);
   double* ov = smem + a.g.panel_bytes / 8;
   T0 {
-    ctx_init(E, D.d, D.n, D.ext);
+    ctx_init(E, D.d, D.n, D.ext, a.g.nb);
     ctx_bind(E, a.g, smem);
     E.prof = a.prof;
     E.sh = ov + PALM_OV * a.wmax;
@@ -286,6 +286,11 @@ out:
   }
 }
 
+template <class TA>
+__global__ void __launch_bounds__(NTHR, 1) palm_kernel(const __grid_constant__ PalmArgs a) {
+  palm_body<TA>(a);
+}
+
 }  // namespace ell1
 
 using namespace ell1;
@@ -297,13 +302,11 @@ extern "C" size_t ell1_palm_workspace(const ell1_dict_t* D, int32_t blocks) {
   return grid_bytes(nb, D->d, 1) + 2 * align_up(N * 8, 256) + 2 * align_up(D->ld * 8, 256) + 4096;
 }
 
-extern "C" int ell1_palm(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C,
-                         const ell1_palm_opts_t* O, const ell1_io_t* io, void* stream) {
+static int palm_setup(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C,
+                         const ell1_palm_opts_t* O, const ell1_io_t* io, int nb, PalmArgs& a, SmemPlan& sp) {
   if (!dict_ok(D) || !b || !C || !O || !io || !io->state || !io->trace || !io->x) return ELL1_ERR_ARG;
   if (!(O->mu0 > 0) || !(O->rho > 1) || !(O->tau > 0) || C->max_iter < 1) return ELL1_ERR_ARG;
-  const int nb = pick_blocks(D->n, io->blocks);
   const int64_t N = ncols_of(D);
-  PalmArgs a;
   a.D = to_raw(D);
   a.b = b;
   a.C = *C;
@@ -321,15 +324,51 @@ extern "C" int ell1_palm(const ell1_dict_t* D, const double* b, const ell1_ctrl_
   a.y_out = O->y_out;
   a.max_steps = io->max_steps;
   a.prof = io->phase_ns;
-  const SmemPlan sp = plan_smem(a.D, nb, PALM_OV, 5, io->max_steps <= 0);
+  sp = plan_smem(a.D, nb, PALM_OV, 5, io->max_steps <= 0);
   a.g.shcap = sp.scratch;
   a.g.panel_bytes = sp.panel_bytes;
   a.rc = sp.rc;
   a.wmax = sp.wmax;
+  return ELL1_OK;
+}
+
+extern "C" int ell1_palm(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C,
+                         const ell1_palm_opts_t* O, const ell1_io_t* io, void* stream) {
+  if (!dict_ok(D) || !io) return ELL1_ERR_ARG;
+  const int nb = pick_blocks(D->n, io->blocks);
+  PalmArgs a;
+  SmemPlan sp;
+  const int rc0 = palm_setup(D, b, C, O, io, nb, a, sp);
+  if (rc0 != ELL1_OK) return rc0;
   cudaStream_t s = (cudaStream_t)stream;
   if (D->ld > D->d)
     for (double* p : {a.Yd, a.RIN})
       if (cudaMemsetAsync(p + D->d, 0, (D->ld - D->d) * 8, s) != cudaSuccess) return ELL1_ERR_CUDA;
   return (D->dtype == ELL1_F64) ? coop_launch(palm_kernel<double>, nb, sp.bytes, s, a, a.g.bar)
                                 : coop_launch(palm_kernel<float>, nb, sp.bytes, s, a, a.g.bar);
+
+}
+
+namespace ell1 {
+template <class TA>
+struct PalmRun {
+  static __device__ void run(const PalmArgs& a) { palm_body<TA>(a); }
+  static __device__ void reset(const PalmArgs& a, int lane) {
+    reset_bar(a.g.bar, lane);
+    zero_pad_rows(a.Yd, a.D.d, a.D.ld, lane);
+    zero_pad_rows(a.RIN, a.D.d, a.D.ld, lane);
+  }
+};
+static_assert(sizeof(PalmArgs) <= ELL1_GROUP_ARG_BYTES, "PalmArgs too large for the group scratch");
+}  // namespace ell1
+
+int32_t ell1_palm_group_team_impl(const ell1_dict_t* D) {
+  return dict_ok(D) ? group_team(to_raw(D), PALM_OV, 5, 0) : 0;
+}
+
+extern "C" int ell1_palm_group(const ell1_group_t* G, const ell1_palm_opts_t* O, void* stream) {
+  if (!G || (G->count > 0 && !O)) return ELL1_ERR_ARG;
+  return run_group<PalmArgs, PalmRun>(G, PALM_OV, 5, 0, [&](int i, int nb, PalmArgs& a, SmemPlan& sp) {
+    return palm_setup(&G->dicts[i], G->b[i], &G->ctrl[i], &O[i], &G->io[i], nb, a, sp);
+  }, stream);
 }

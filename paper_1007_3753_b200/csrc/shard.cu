@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(NTHR, 1) gemv_partial_kernel(const __grid_cons
   DictV<TA> D = dict_view<TA>(a.D);
   D.ext = 0;
   if (threadIdx.x == 0) {
-    ctx_init(E, D.d, D.n, 0);
+    ctx_init(E, D.d, D.n, 0, a.g.nb);
     ctx_bind(E, a.g, smem);
   }
   __syncthreads();
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(NTHR, 1) gemv_t_kernel(const __grid_constant__
   DictV<TA> D = dict_view<TA>(a.D);
   D.ext = 0;
   if (threadIdx.x == 0) {
-    ctx_init(E, D.d, D.n, 0);
+    ctx_init(E, D.d, D.n, 0, a.g.nb);
     ctx_bind(E, a.g, smem);
   }
   __syncthreads();

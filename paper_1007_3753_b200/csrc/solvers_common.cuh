@@ -23,6 +23,7 @@ struct GridBufs {
   int* abort;
   int64_t shcap;              // shared-memory scratch doubles per CTA
   size_t panel_bytes;         // resident dictionary panel bytes (0: streamed)
+  int nb;                     // CTAs cooperating on the solve
 };
 
 template <class TA>
@@ -69,10 +70,49 @@ __device__ __forceinline__ bool stop_fires(int kind, double thr, int hist, doubl
   }
 }
 
+
+// ---------------------------------------------------------------- groups
+// A group launch runs `count` independent solves — each with its own Args
+// (dictionary, b, controls, workspace, outputs) — on teams of `nb`
+// consecutive CTAs of one persistent launch; team t takes solves t,
+// t + nteams, ...  Run::run(a) is the solver body (the same code as the
+// single-solve kernel), Run::reset(a, lane) prepares one solve's workspace
+// (barrier counter, padding rows) with one warp.
+template <class Args, class Run>
+__global__ void __launch_bounds__(NTHR, 1) group_kernel(const Args* __restrict__ argv, int count, int nb) {
+  __shared__ __align__(16) Args sa;
+  const int team = (int)(blockIdx.x / (unsigned)nb);
+  const int nteams = (int)(gridDim.x / (unsigned)nb);
+  static_assert(sizeof(Args) % 4 == 0, "Args must be a whole number of words");
+  for (int g = team; g < count; g += nteams) {
+    __syncthreads();
+    const unsigned* src = reinterpret_cast<const unsigned*>(argv + g);
+    unsigned* dst = reinterpret_cast<unsigned*>(&sa);
+    for (int i = (int)threadIdx.x; i < (int)(sizeof(Args) / 4); i += NTHR) dst[i] = src[i];
+    __syncthreads();
+    Run::run(sa);
+  }
+}
+
+template <class Args, class Run>
+__global__ void group_reset_kernel(const Args* __restrict__ argv, int count) {
+  const int g = (int)(blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32);
+  if (g < count) Run::reset(argv[g], (int)(threadIdx.x & 31));
+}
+
+// zero the 4-word barrier block and the rows [d, ld) of k vectors (one warp)
+__device__ __forceinline__ void reset_bar(unsigned long long* bar, int lane) {
+  if (lane < 4) bar[lane] = 0ULL;
+}
+__device__ __forceinline__ void zero_pad_rows(double* v, int64_t d, int64_t ld, int lane) {
+  for (int64_t i = d + lane; i < ld; i += 32) v[i] = 0.0;
+}
+
 }  // namespace ell1
 
 // ---------------------------------------------------------------- host side
 #include <cstdio>
+#include <vector>
 namespace ell1 {
 
 inline int sm_count(int dev) {
@@ -121,6 +161,7 @@ inline size_t grid_bytes(int nb, int64_t d, int nv) {
 }
 
 inline bool carve_grid(Carve& cv, GridBufs& g, int nb, int64_t d, int nv) {
+  g.nb = nb;
   g.rp = rpad(d, nb);
   g.pvec = (int64_t)nb * nb * g.rp;
   g.part = cv.take<double>((size_t)(nv > 0 ? nv : 1) * g.pvec);
@@ -197,6 +238,56 @@ inline SmemPlan plan_smem(const DictRaw& D, int nb, int nov, int kmax, bool allo
   return p;
 }
 
+
+// Team size for a group launch: the fewest CTAs (<= 32, >= 16 columns each)
+// whose shared memory holds the whole dictionary panel; 0 when even 32 do not.
+inline int group_team_for(const DictRaw& D, int nov, int kmax, int64_t min_scratch = 0) {
+  const int64_t wcols_1 = D.n;
+  for (int nb = 1; nb <= 32; ++nb) {
+    if (nb > 1 && (wcols_1 + nb - 1) / nb < 16) break;
+    const SmemPlan p = plan_smem(D, nb, nov, kmax, true, min_scratch);
+    if ((int64_t)p.rc >= (D.n + nb - 1) / nb) return nb;
+  }
+  return 0;
+}
+
+// Launch a group: copy the per-solve Args to the device (args_ws), reset
+// each solve's workspace, then one persistent launch of teams of nb CTAs
+// (cooperative when nb > 1, so every team's CTAs are co-resident).
+template <class Args, class Run>
+inline int group_launch(const std::vector<Args>& av, int nb, size_t smem, void* args_ws, size_t args_bytes,
+                        cudaStream_t s) {
+  const int count = (int)av.size();
+  if (count == 0) return ELL1_OK;
+  if (nb < 1) return ELL1_ERR_ARG;
+  const size_t bytes = av.size() * sizeof(Args);
+  if (!args_ws || args_bytes < bytes) return ELL1_ERR_ARG;
+  if (cudaMemcpyAsync(args_ws, av.data(), bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) return ELL1_ERR_CUDA;
+  const Args* dargs = reinterpret_cast<const Args*>(args_ws);
+  group_reset_kernel<Args, Run><<<(count + 7) / 8, 256, 0, s>>>(dargs, count);
+  if (cudaGetLastError() != cudaSuccess) return ELL1_ERR_CUDA;
+  auto kernel = group_kernel<Args, Run>;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return ELL1_ERR_CUDA;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, NTHR, smem) != cudaSuccess) return ELL1_ERR_CUDA;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int teams = per_sm * sm_count(dev) / nb;
+  if (teams < 1) return ELL1_ERR_NOCOOP;
+  if (teams > count) teams = count;
+  int cnt = count, team = nb;
+  void* kargs[] = {(void*)&dargs, (void*)&cnt, (void*)&team};
+  cudaError_t e = nb > 1 ? cudaLaunchCooperativeKernel((const void*)kernel, dim3(teams * nb), dim3(NTHR), kargs, smem, s)
+                         : cudaLaunchKernel((const void*)kernel, dim3(teams * nb), dim3(NTHR), kargs, smem, s);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "ell1_b200: group launch failed: %s\n", cudaGetErrorString(e));
+    return ELL1_ERR_CUDA;
+  }
+  return ELL1_OK;
+}
+
+
 inline DictRaw to_raw(const ell1_dict_t* D) {
   DictRaw r;
   r.A = D->A; r.dtype = D->dtype; r.ext = D->ext; r.d = D->d; r.n = D->n; r.ld = D->ld;
@@ -210,5 +301,50 @@ inline bool dict_ok(const ell1_dict_t* D) {
 }
 
 inline int64_t ncols_of(const ell1_dict_t* D) { return D->n + (D->ext ? D->d : 0); }
+
+// Auto team size: group_team_for, or (dictionary too large for 32 CTAs'
+// shared memory) the streamed single-solve grid capped at 32.
+inline int group_team(const DictRaw& D, int nov, int kmax, int64_t min_scratch) {
+  const int t = group_team_for(D, nov, kmax, min_scratch);
+  return t > 0 ? t : pick_blocks(D.n, 32);
+}
+
+// Shared group driver: per-solve setup at the team size, then one launch
+// per storage dtype present (a group normally holds one dtype).
+template <class Args, template <class> class Run, class Setup>
+inline int run_group(const ell1_group_t* G, int nov, int kmax, int64_t min_scratch, Setup setup, void* stream) {
+  if (!G || G->count < 0 || (G->count > 0 && (!G->dicts || !G->io))) return ELL1_ERR_ARG;
+  if (G->count == 0) return ELL1_OK;
+  int nb = G->team;
+  for (int i = 0; i < G->count; ++i)
+    if (!dict_ok(&G->dicts[i])) return ELL1_ERR_ARG;
+  if (nb <= 0) {
+    nb = 1;
+    for (int i = 0; i < G->count; ++i) {
+      const int t = group_team(to_raw(&G->dicts[i]), nov, kmax, min_scratch);
+      if (t > nb) nb = t;
+    }
+  }
+  std::vector<Args> av64, av32;
+  size_t smem64 = 0, smem32 = 0;
+  for (int i = 0; i < G->count; ++i) {
+    if (G->io[i].max_steps > 0) return ELL1_ERR_ARG;
+    Args a;
+    SmemPlan sp;
+    const int rc = setup(i, nb, a, sp);
+    if (rc != ELL1_OK) return rc;
+    if (G->dicts[i].dtype == ELL1_F64) { av64.push_back(a); if (sp.bytes > smem64) smem64 = sp.bytes; }
+    else { av32.push_back(a); if (sp.bytes > smem32) smem32 = sp.bytes; }
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  char* ws = (char*)G->args_ws;
+  size_t wsb = G->args_ws_bytes;
+  int rc = group_launch<Args, Run<double>>(av64, nb, smem64, ws, wsb, s);
+  if (rc != ELL1_OK) return rc;
+  const size_t used = align_up((int64_t)(av64.size() * sizeof(Args)), 256);
+  if (av32.empty()) return ELL1_OK;
+  if (wsb < used) return ELL1_ERR_ARG;
+  return group_launch<Args, Run<float>>(av32, nb, smem32, ws + used, wsb - used, s);
+}
 
 }  // namespace ell1

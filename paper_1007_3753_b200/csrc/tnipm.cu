@@ -43,14 +43,14 @@ struct TnV {
 #define T0 if (threadIdx.x == 0)
 
 template <class TA>
-__global__ void __launch_bounds__(NTHR, 1) tnipm_kernel(const __grid_constant__ TnipmArgs a) {
+__device__ __forceinline__ void tnipm_body(const TnipmArgs& a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ Ctx E;
   __shared__ TnV V;
   const DictV<TA> D = dict_view<TA>(a.D);
   double* ov = smem + a.g.panel_bytes / 8;
   T0 {
-    ctx_init(E, D.d, D.n, D.ext);
+    ctx_init(E, D.d, D.n, D.ext, a.g.nb);
     ctx_bind(E, a.g, smem);
     E.prof = a.prof;
     E.sh = ov + TN_OV * a.wmax;
@@ -527,6 +527,11 @@ out:
   }
 }
 
+template <class TA>
+__global__ void __launch_bounds__(NTHR, 1) tnipm_kernel(const __grid_constant__ TnipmArgs a) {
+  tnipm_body<TA>(a);
+}
+
 }  // namespace ell1
 
 using namespace ell1;
@@ -538,14 +543,11 @@ extern "C" size_t ell1_tnipm_workspace(const ell1_dict_t* D, int32_t blocks) {
   return grid_bytes(nb, D->d, 1) + 2 * align_up(N * 8, 256) + 3 * align_up(D->ld * 8, 256) + 4096;
 }
 
-extern "C" int ell1_tnipm(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C, double lam,
-                          double pcg_tol, int32_t pcg_max_iter, double* u_out, const ell1_io_t* io,
-                          void* stream) {
+static int tnipm_setup(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C, double lam,
+                          double pcg_tol, int32_t pcg_max_iter, double* u_out, const ell1_io_t* io, int nb, TnipmArgs& a, SmemPlan& sp) {
   if (!dict_ok(D) || !b || !C || !io || !io->state || !io->trace || !io->x) return ELL1_ERR_ARG;
   if (!(lam > 0) || C->max_iter < 1) return ELL1_ERR_ARG;
-  const int nb = pick_blocks(D->n, io->blocks);
   const int64_t N = ncols_of(D);
-  TnipmArgs a;
   a.D = to_raw(D);
   a.b = b;
   a.C = *C;
@@ -563,16 +565,58 @@ extern "C" int ell1_tnipm(const ell1_dict_t* D, const double* b, const ell1_ctrl
   a.u_out = u_out;
   a.max_steps = io->max_steps;
   a.prof = io->phase_ns;
-  const SmemPlan sp = plan_smem(a.D, nb, TN_OV, 8, io->max_steps <= 0);
+  sp = plan_smem(a.D, nb, TN_OV, 8, io->max_steps <= 0);
   if (sp.bytes > (size_t)max_smem_optin()) return ELL1_ERR_ARG;   // owned vectors must fit
   a.g.shcap = sp.scratch;
   a.g.panel_bytes = sp.panel_bytes;
   a.rc = sp.rc;
   a.wmax = sp.wmax;
+  return ELL1_OK;
+}
+
+extern "C" int ell1_tnipm(const ell1_dict_t* D, const double* b, const ell1_ctrl_t* C, double lam,
+                          double pcg_tol, int32_t pcg_max_iter, double* u_out, const ell1_io_t* io,
+                          void* stream) {
+  if (!dict_ok(D) || !io) return ELL1_ERR_ARG;
+  const int nb = pick_blocks(D->n, io->blocks);
+  TnipmArgs a;
+  SmemPlan sp;
+  const int rc0 = tnipm_setup(D, b, C, lam, pcg_tol, pcg_max_iter, u_out, io, nb, a, sp);
+  if (rc0 != ELL1_OK) return rc0;
   cudaStream_t s = (cudaStream_t)stream;
   if (D->ld > D->d)
     for (double* p : {a.Rv, a.APd, a.ADX})
       if (cudaMemsetAsync(p + D->d, 0, (D->ld - D->d) * 8, s) != cudaSuccess) return ELL1_ERR_CUDA;
   return (D->dtype == ELL1_F64) ? coop_launch(tnipm_kernel<double>, nb, sp.bytes, s, a, a.g.bar)
                                 : coop_launch(tnipm_kernel<float>, nb, sp.bytes, s, a, a.g.bar);
+
+}
+
+namespace ell1 {
+template <class TA>
+struct TnipmRun {
+  static __device__ void run(const TnipmArgs& a) { tnipm_body<TA>(a); }
+  static __device__ void reset(const TnipmArgs& a, int lane) {
+    reset_bar(a.g.bar, lane);
+    zero_pad_rows(a.Rv, a.D.d, a.D.ld, lane);
+    zero_pad_rows(a.APd, a.D.d, a.D.ld, lane);
+    zero_pad_rows(a.ADX, a.D.d, a.D.ld, lane);
+  }
+};
+static_assert(sizeof(TnipmArgs) <= ELL1_GROUP_ARG_BYTES, "TnipmArgs too large for the group scratch");
+}  // namespace ell1
+
+int32_t ell1_tnipm_group_team_impl(const ell1_dict_t* D) {
+  return dict_ok(D) ? group_team(to_raw(D), TN_OV, 8, 0) : 0;
+}
+
+extern "C" int ell1_tnipm_group(const ell1_group_t* G, const double* lam, double pcg_tol, int32_t pcg_max_iter,
+                                void* stream) {
+  if (!G || (G->count > 0 && !lam)) return ELL1_ERR_ARG;
+  return run_group<TnipmArgs, TnipmRun>(G, TN_OV, 8, 0, [&](int i, int nb, TnipmArgs& a, SmemPlan& sp) {
+    const int rc = tnipm_setup(&G->dicts[i], G->b[i], &G->ctrl[i], lam[i], pcg_tol, pcg_max_iter, nullptr,
+                               &G->io[i], nb, a, sp);
+    if (rc == ELL1_OK && sp.bytes > (size_t)max_smem_optin()) return (int)ELL1_ERR_ARG;
+    return rc;
+  }, stream);
 }

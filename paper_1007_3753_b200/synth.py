@@ -135,3 +135,92 @@ def cab_queries(A, labels, count, fraction=0.2, seed=0):
         out[q], _ = corrupt_entries(b, fraction, 0.0, 1.0, trial_seed(seed, q))
         truth[q] = c
     return out, truth
+
+
+# ---------------------------------------------------------------- experiment recipes
+# The reference harness's generators (synth.py:18-37 GenSpec, :56-67 unit-norm
+# sparse signal, :70-77 noise, :102-132 bouquet dictionary, :135-142
+# make_instance), restated so harness trials see the reference's instances.
+
+RNG_NAME = "numpy PCG64 (default_rng, SeedSequence sub-streams)"
+
+
+@dataclass(frozen=True)
+class GenSpec:
+    """Recipe for one synthetic instance (synth.py:18-37)."""
+
+    n: int
+    d: int
+    k: int
+    seed: int
+    noise_sigma: float = 0.0
+    corruption_fraction: float = 0.0
+
+    def __post_init__(self):
+        if self.d < 1:
+            raise ValueError("d must be at least 1")
+        if not 1 <= self.k <= self.n:
+            raise ValueError("need 1 <= k <= n")
+        if self.noise_sigma < 0:
+            raise ValueError("noise_sigma must be nonnegative")
+        if not 0 <= self.corruption_fraction <= 1:
+            raise ValueError("corruption_fraction must lie in [0, 1]")
+
+
+def gen_sparse_signal(n, k, seed):
+    """Unit-l2 k-sparse vector on a uniform support (synth.py:56-67)."""
+    if not 1 <= k <= n:
+        raise ValueError("need 1 <= k <= n")
+    g = _stream(seed, 1)
+    where = g.choice(n, size=k, replace=False)
+    vals = g.standard_normal(k)
+    while np.any(vals == 0.0):
+        vals[vals == 0.0] = g.standard_normal(int(np.sum(vals == 0.0)))
+    x = np.zeros(n)
+    x[where] = vals / np.linalg.norm(vals)
+    return x
+
+
+def add_noise(b, sigma, seed):
+    """b + N(0, sigma^2) i.i.d. (synth.py:70-77); sigma = 0 returns a copy."""
+    if sigma < 0:
+        raise ValueError("sigma must be nonnegative")
+    b = np.asarray(b, dtype=np.float64)
+    if sigma == 0.0:
+        return b.copy()
+    return b + sigma * _stream(seed, 2).standard_normal(b.shape[0])
+
+
+def gen_bouquet_dict(d, n, groups, coherence, seed):
+    """Clustered unit-column dictionary and its group labels (synth.py:102-132):
+    columns = coherence * shared mean + residual split 30/70 between a group
+    direction and column noise."""
+    if not 0 < coherence < 1:
+        raise ValueError("coherence must lie in (0, 1)")
+    if not 1 <= groups <= n:
+        raise ValueError("need 1 <= groups <= n")
+    g = _stream(seed, 4)
+    mean = g.standard_normal(d)
+    mean /= np.linalg.norm(mean)
+    gdir = g.standard_normal((groups, d))
+    gdir /= np.linalg.norm(gdir, axis=1)[:, None]
+    sizes = np.full(groups, n // groups)
+    sizes[: n % groups] += 1
+    labels = np.repeat(np.arange(groups), sizes)
+    share = 0.3
+    rest = np.sqrt(1.0 - coherence ** 2)
+    noise = g.standard_normal((d, n))
+    cols = (coherence * mean[:, None] + rest * np.sqrt(share) * gdir[labels].T
+            + rest * np.sqrt(1.0 - share) * noise / np.sqrt(d))
+    cols /= np.linalg.norm(cols, axis=0)
+    return cols, labels
+
+
+def make_instance(spec):
+    """ProblemInstance of a GenSpec (synth.py:135-142)."""
+    A = gen_gaussian_dict(spec.d, spec.n, spec.seed)
+    x0 = gen_sparse_signal(spec.n, spec.k, spec.seed)
+    b = A @ x0
+    if spec.noise_sigma > 0:
+        b = add_noise(b, spec.noise_sigma, spec.seed)
+    return ProblemInstance(A, b, ground_truth=x0, noise_sigma=spec.noise_sigma)
