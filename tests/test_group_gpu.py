@@ -93,7 +93,7 @@ def test_group_multi_cta_teams_and_norms():
     assert team > 1
     ns = grp.norm_sq()
     for P, v in zip(probs, ns):
-        assert abs(v - oracle.power_norm_sq(P.A)[0]) <= 1e-12 * v
+        assert abs(v - oracle.power_norm_sq(P.A)) <= 1e-12 * v
     res = grp.solve("fista", _cfg(tol=1e-6, max_iter=3000))
     for P, r in zip(probs, res):
         ref = oracle.fista(P.A, P.b, tol=1e-6, max_iter=3000)

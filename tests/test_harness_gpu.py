@@ -1,0 +1,68 @@
+"""Experiment harness on the B200 against the REAL reference's outputs
+(tests/golden/make_harness_golden.py): identical success rates and
+iteration means, relative-error means within the parity tolerance,
+byte-identical phase-grid CSV, and run-to-run determinism."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.join(os.path.dirname(__file__), "golden")
+GOLD = np.load(os.path.join(HERE, "harness_ref.npz"))
+META = json.load(open(os.path.join(HERE, "harness_ref.json")))
+
+
+def _run(cid):
+    from paper_1007_3753_b200 import harness
+    c = META["cases"][cid]
+    if c["kind"] == "phase":
+        return harness.run_phase_grid(c["solver"], c["n"], c["rho"], c["delta"], c["trials"], base_seed=c["seed"])
+    if c["kind"] == "noise":
+        return harness.run_noise_sweep(c["solvers"], c["mode"], c["spec"], c["trials"], base_seed=c["seed"])
+    return harness.run_corruption_sweep(c["dict_spec"], c["levels"], c["solvers"], c["trials"], base_seed=c["seed"])
+
+
+@pytest.mark.parametrize("cid", ["phase_homotopy", "phase_fista", "phase_dalm"])
+def test_phase_grid_matches_reference(cid, tmp_path):
+    from paper_1007_3753_b200 import harness
+    g = _run(cid)
+    np.testing.assert_array_equal(g.success_rate, GOLD[cid + "__success_rate"])
+    path = harness.phase_grid_to_csv(g, str(tmp_path / "g.csv"))
+    assert open(path).read() == META["csv"][cid]          # byte-identical to the reference's CSV
+
+
+@pytest.mark.parametrize("cid", ["noise_vary_d", "noise_vary_k_clean"])
+def test_noise_sweep_matches_reference(cid):
+    s = _run(cid)
+    np.testing.assert_array_equal(s.mean_iterations, GOLD[cid + "__mean_iterations"])
+    ref = GOLD[cid + "__mean_rel_error"]
+    np.testing.assert_allclose(s.mean_rel_error, ref, rtol=0, atol=1e-6 * (1.0 + np.abs(ref)).max())
+    assert np.all(s.mean_time > 0)
+
+
+def test_corruption_sweep_matches_reference():
+    s = _run("corruption")
+    np.testing.assert_array_equal(s.success_rate, GOLD["corruption__success_rate"])
+
+
+def test_harness_is_deterministic(tmp_path):
+    from paper_1007_3753_b200 import harness
+    a = harness.run_noise_sweep(["fista", "homotopy"], "vary-d", {"n": 50, "k": 3, "d_values": [20, 30]}, 3)
+    b = harness.run_noise_sweep(["fista", "homotopy"], "vary-d", {"n": 50, "k": 3, "d_values": [20, 30]}, 3)
+    np.testing.assert_array_equal(a.mean_rel_error, b.mean_rel_error)
+    np.testing.assert_array_equal(a.mean_iterations, b.mean_iterations)
+    g1 = harness.run_phase_grid("homotopy", 40, [0.1, 0.2], [0.5, 0.8], 3, base_seed=42)
+    g2 = harness.run_phase_grid("homotopy", 40, [0.1, 0.2], [0.5, 0.8], 3, base_seed=42)
+    p1 = harness.phase_grid_to_csv(g1, str(tmp_path / "a.csv"))
+    p2 = harness.phase_grid_to_csv(g2, str(tmp_path / "b.csv"))
+    assert open(p1, "rb").read() == open(p2, "rb").read()
+
+
+def test_pdipa_trials_run_one_at_a_time():
+    from paper_1007_3753_b200 import harness
+    g = harness.run_phase_grid("pdipa", 30, [0.1], [0.6], 2, base_seed=5)
+    assert g.success_rate.shape == (1, 1)
