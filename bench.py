@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--no-secondary", action="store_true",
                     help="skip the config 1/3/4/5 and all-solver legs")
     ap.add_argument("--cfg5-sweep", action="store_true", help="add the config-5 batch-size sweep leg")
+    ap.add_argument("--only-leg", default=None, help="run one secondary leg alone (diagnostics)")
     return ap.parse_args()
 
 
@@ -549,6 +550,81 @@ def leg_cfg5_sweep(torch, dev, sizes=(1, 16, 256, 1024, 8192)):
     return {"workload": "cfg5 sweep: shared A 512 x 2048, k~U[16,256], lambda 1e-3", "rows": rows}
 
 
+def leg_harness(torch, n=200, grid=10, trials=10, cpu_sample=6):
+    """the experiment harness on the GPU.  A phase grid
+    (bench.run_phase_grid: rho x delta = grid x grid cells, `trials` fresh
+    instances each, one dictionary per trial, tol 1e-8, max_iter 20000,
+    lambda 1e-4 ||A^T b||_inf) solved in group launches, plus the reference
+    acceptance suite's noise sweep (criterion 5).  Timed: device solve of
+    all trials (dictionaries already uploaded) and the whole harness call
+    (host instances in, success rates out)."""
+    from paper_1007_3753_b200 import harness
+    from paper_1007_3753_b200.group import TrialGroup
+    from paper_1007_3753_b200.model import SolverConfig
+    from paper_1007_3753_b200.synth import GenSpec, make_instance, trial_seed
+    rhos = [round(0.02 + 0.38 * i / (grid - 1), 4) for i in range(grid)]
+    deltas = [round(0.1 + 0.9 * j / (grid - 1), 4) for j in range(grid)]
+    probs = []
+    for i, rho in enumerate(rhos):
+        for j, delta in enumerate(deltas):
+            k, d = max(1, int(round(rho * n))), max(1, int(round(delta * n)))
+            for t in range(trials):
+                probs.append(make_instance(GenSpec(n=n, d=d, k=k, seed=trial_seed(0, i, j, t))))
+    out = {"workload": "phase grid n=%d, %dx%d cells (rho %.2f..%.2f, delta %.2f..%.2f), %d trials/cell = %d "
+                       "trials, one Gaussian dictionary per trial, tol 1e-8, lambda 1e-4||A^T b||_inf"
+                       % (n, grid, grid, rhos[0], rhos[-1], deltas[0], deltas[-1], trials, len(probs))}
+    cfg = SolverConfig(tol=1e-8, max_iter=20000)
+    for name in ("fista", "homotopy", "dalm"):
+        grp = TrialGroup(probs)
+        lams = 1e-4 * grp.correlation_max()
+        grp.solve(name, SolverConfig(tol=1e-8, max_iter=5), lams=lams)        # warm-up (module load)
+        torch.cuda.synchronize()
+        s, e = _events(torch)
+        s.record()
+        res = grp.solve(name, cfg, lams=lams)
+        e.record()
+        torch.cuda.synchronize()
+        sec = s.elapsed_time(e) / 1e3
+        its = np.array([r.iterations for r in res])
+        ok = np.mean([np.linalg.norm(r.x_star - P.ground_truth) <= 1e-3 * np.linalg.norm(P.ground_truth)
+                      for r, P in zip(res, probs)])
+        t0 = time.perf_counter()
+        harness.run_phase_grid(name, n, rhos, deltas, trials)
+        whole = time.perf_counter() - t0
+        out[name] = {"trials_per_sec": len(probs) / sec, "device_seconds": sec,
+                     "harness_call_seconds": whole, "mean_iterations": float(its.mean()),
+                     "max_iterations": int(its.max()), "success_fraction": float(ok)}
+    # CPU port (the reference's per-trial solve, one process) on the first trials of the same grid
+    import oracle
+    cpu = {}
+    sample = probs[:: max(1, len(probs) // cpu_sample)][:cpu_sample]
+    for name in ("fista", "homotopy", "dalm"):
+        t0 = time.perf_counter()
+        for P in sample:
+            lam = 1e-4 * float(np.max(np.abs(P.A.T @ P.b)))
+            if name == "fista":
+                oracle.fista(P.A, P.b, lam=lam, tol=1e-8, max_iter=20000)
+            elif name == "homotopy":
+                oracle.homotopy(P.A, P.b, lam, max_iter=20000)
+            else:
+                oracle.dalm(P.A, P.b, tol=1e-8, max_iter=20000)
+        cpu[name + "_trials_per_sec"] = len(sample) / (time.perf_counter() - t0)
+    cpu.update({"cores": 1, "kind": "port", "sample": "%d trials spread over the grid, one process "
+                "(the reference fans trials over processes, one trial per process)" % len(sample)})
+    out["cpu_baseline"] = cpu
+    # acceptance criterion 5 noise sweep (test_acceptance.py:128-160), jobs ignored
+    t0 = time.perf_counter()
+    sw = harness.run_noise_sweep(("homotopy", "gpsr", "tnipm", "ist", "fista"), "vary-d",
+                                 {"n": 400, "k": 40, "d_values": [160, 200, 240, 280, 320, 360, 380],
+                                  "noise_sigma": 0.01}, trials=20, base_seed=0)
+    out["noise_sweep_criterion5"] = {"seconds": time.perf_counter() - t0,
+                                     "final_rel_error": {s: float(sw.mean_rel_error[q, -1])
+                                                         for q, s in enumerate(sw.solvers)},
+                                     "reference_bound_seconds": 300.0,
+                                     "note": "7 d values x 20 trials x 5 solvers, one call"}
+    return out
+
+
 def leg_solvers_cfg2(torch, P, reps=3):
     """Every single-instance solver on the cfg2 instance (ms per solve)."""
     from paper_1007_3753_b200 import device as dv
@@ -625,6 +701,12 @@ def run_b200(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local if ws > 1 else 0)
     torch.cuda.set_device(dev)
+    if args.only_leg:
+        legs = {"harness": lambda: leg_harness(torch), "cfg1": lambda: leg_cfg1(torch),
+                "cfg3": lambda: leg_cfg3(torch, dev), "cfg5": lambda: leg_cfg5(torch, dev, ws),
+                "cfg5_sweep": lambda: leg_cfg5_sweep(torch, dev)}
+        print(json.dumps({args.only_leg: legs[args.only_leg]()}), flush=True)
+        return
 
     from paper_1007_3753_b200 import device as dv
     from paper_1007_3753_b200.model import ProblemInstance
@@ -755,7 +837,8 @@ def run_b200(args):
                 legs2.append(("cfg5_sweep", lambda: leg_cfg5_sweep(torch, dev)))
             legs2 += [("solvers_cfg2", lambda: leg_solvers_cfg2(torch, P)),
                       ("cfg3", lambda: leg_cfg3(torch, dev)),
-                      ("cfg5", lambda: leg_cfg5(torch, dev, ws))]
+                      ("cfg5", lambda: leg_cfg5(torch, dev, ws)),
+                      ("harness", lambda: leg_harness(torch))]
             for name, fn in legs2:
                 try:
                     sec[name] = fn()

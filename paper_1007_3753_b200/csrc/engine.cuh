@@ -763,6 +763,16 @@ __device__ void panel_gemv(const Ctx& E, const DictV<TA>& D, const Panel<TA>& P,
 // (before the decision that needs them is known): thread q's slice of r and
 // the first streamed (non-resident) panel column.  Issuing these loads early
 // overlaps their L2 latency with other work.
+// Short-column GEMV^T thread map: a column is covered by wg = ceil(nvec / 32)
+// warps; the CTA's warps form NWARP / wg column groups, each walking its own
+// column chunks.  Returns this thread's row vector (-1: idle warp).
+__device__ __forceinline__ int64_t gt_row(int64_t nvec) {
+  const int wg = (int)((nvec + 31) >> 5);
+  const int grp = wpx() / wg;
+  if (grp >= NWARP / wg) return -1;
+  return (int64_t)(wpx() - grp * wg) * 32 + lnx();
+}
+
 template <class TA, int NV>
 struct GtPre {
   double rq[NV][VecOf<TA>::VW];
@@ -775,8 +785,8 @@ __device__ __forceinline__ void gemv_t_prefetch(const DictV<TA>& D, const Panel<
   constexpr int VW = VecOf<TA>::VW;
   const int64_t nvec = D.ld / VW;
   if (nvec > NTHR) return;                          // long columns stage r themselves
-  const int64_t q = tix();
-  const bool act = q < nvec;
+  const int64_t q = gt_row(nvec);
+  const bool act = q >= 0 && q < nvec;
 #pragma unroll
   for (int v = 0; v < NV; ++v)
 #pragma unroll
@@ -811,14 +821,23 @@ __device__ void panel_gemv_t_pre(const Ctx& E, const DictV<TA>& D, const Panel<T
   double* red = shmem(E.sh);                        // [NWARP][CW] per v pass
   __syncthreads();
   if (nvec <= NTHR) {
-    const int64_t q = tix();
-    const bool act = q < nvec;
-    const unsigned sbase = (unsigned)__cvta_generic_to_shared(P.sm + q * VW);
+    // column groups of wg warps (gt_row); per chunk of CW columns each warp
+    // transpose-reduces its rows, then (wg > 1) the group's warps are summed
+    // in warp order through shared memory — the same order, and so the same
+    // bits, as one group spanning the whole CTA.
+    const int wg = (int)((nvec + 31) >> 5);
+    const int G = NWARP / wg;
+    const int grp = wpx() / wg;
+    const int64_t q = gt_row(nvec);
+    const bool act = q >= 0 && q < nvec;
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(P.sm + (act ? q : 0) * VW);
     const unsigned cst = (unsigned)(D.ld * sizeof(TA));
     constexpr int CW = 16;                          // columns per transpose-reduce chunk
-    int cb = 0;                                     // staging buffer (double-buffered: one sync per chunk)
-    for (int j0 = 0; j0 < w; j0 += CW) {
-      const int cnt = (w - j0) < CW ? (w - j0) : CW;
+    const int nchunk = (w + CW - 1) / CW;
+    int cb = 0;                                     // staging buffer (double-buffered: one sync per round)
+    for (int r0 = 0; r0 < nchunk; r0 += G) {
+      const int j0 = (r0 + grp) * CW;
+      const int cnt = (grp < G && j0 < w) ? ((w - j0) < CW ? (w - j0) : CW) : 0;
 #pragma unroll
       for (int v = 0; v < NV; ++v, cb ^= 1) {
         double* rb = red + cb * (NWARP * CW);
@@ -854,16 +873,21 @@ __device__ void panel_gemv_t_pre(const Ctx& E, const DictV<TA>& D, const Panel<T
           }
         }
         p[0] += __shfl_xor_sync(0xffffffffu, p[0], 16);
-        if (lnx() < CW) rb[wpx() * CW + lnx()] = p[0];
-        __syncthreads();
-        if (tix() < cnt) {
-          double t[NWARP];
-#pragma unroll
-          for (int ww = 0; ww < NWARP; ++ww) t[ww] = rb[ww * CW + tix()];
-          double s = t[0];
-#pragma unroll
-          for (int ww = 1; ww < NWARP; ++ww) s += t[ww];
-          outs[v][j0 + tix()] = s;
+        if (wg == 1) {
+          if (lnx() < cnt) outs[v][j0 + lnx()] = p[0];
+        } else {
+          if (lnx() < CW) rb[wpx() * CW + lnx()] = p[0];
+          __syncthreads();
+          const int g2 = tix() / CW, c = tix() - (tix() / CW) * CW;
+          if (g2 < G) {
+            const int jj = (r0 + g2) * CW + c;
+            if (jj < w && c < CW) {
+              const double* t = rb + (g2 * wg) * CW + c;
+              double s2 = t[0];
+              for (int ww = 1; ww < wg; ++ww) s2 += t[ww * CW];
+              outs[v][jj] = s2;
+            }
+          }
         }
       }
     }

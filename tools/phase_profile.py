@@ -24,8 +24,10 @@ def main():
     ap.add_argument("--dtype", default="float64")
     ap.add_argument("--d", type=int, default=1024)
     ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--blocks", type=int, default=0, help="persistent grid size (0: one CTA per SM)")
     args = ap.parse_args()
     P = synth.make_problem(synth.Workload("p", args.d, args.n, max(1, args.n // 32), 0, 0.01))
+
     D = dv.DeviceDictionary(P.A, dtype=args.dtype)
     Pd = ProblemInstance.__new__(ProblemInstance)
     Pd.A, Pd.b, Pd.ground_truth = D, P.b, None
@@ -34,7 +36,7 @@ def main():
     plan.launch()
     torch.cuda.synchronize()
     prof = torch.zeros(148 * 16, dtype=torch.int64, device=D.device)
-    io = plan.bufs.io(0)
+    io = plan.bufs.io(0, blocks=args.blocks)
     io.phase_ns = prof.data_ptr()
     plan.bufs.state.zero_()
     from paper_1007_3753_b200 import _lib
