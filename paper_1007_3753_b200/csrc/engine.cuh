@@ -651,6 +651,93 @@ __device__ void panel_gemv(const Ctx& E, const DictV<TA>& D, const Panel<TA>& P,
   double* out = E.part + (size_t)slot0 * E.pvec + (size_t)E.b * E.rp;
   const int64_t reg = (int64_t)E.nb * E.rp;      // region stride (one owner)
   __syncthreads();
+  {
+    // Short panels with many columns (small problems, group launches): KG
+    // column groups of wgr warps each cover all rows; group g sums its column
+    // range, the KG partials are added in group order through E.sh (first
+    // NWARP * 32 doubles only).
+    const int wgr = (int)((nvec + 31) >> 5);
+    int KG = NWARP / wgr;
+    const int64_t per = (int64_t)wgr * 32 * VW * NV;          // doubles per group partial
+    while (KG > 1 && KG * per > NWARP * 32) --KG;
+    if (KG > 1 && w >= 8 * KG) {
+      const int grp = wpx() / wgr;
+      const int64_t q = (int64_t)(wpx() - grp * wgr) * 32 + lnx();
+      const bool act = grp < KG && q < nvec;
+      double acc[NV][VW];
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int e = 0; e < VW; ++e) acc[v][e] = 0.0;
+      if (act) {
+        const int ja = (int)(((int64_t)w * grp) / KG), jb = (int)(((int64_t)w * (grp + 1)) / KG);
+        const unsigned p = (unsigned)__cvta_generic_to_shared(P.sm + q * VW);
+        const unsigned cst = (unsigned)(D.ld * sizeof(TA));
+        const TA* pg = P.gl + q * VW;
+        int j = ja;
+        for (; j + 4 <= jb; j += 4) {
+          TA a[4][VW];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (j + u < rc) ld16_sa<TA>(p + (unsigned)(j + u) * cst, a[u]);
+            else ld16_g<TA>(pg + (int64_t)(j + u) * D.ld, a[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+              const double xv = xs[v][j + u];
+#pragma unroll
+              for (int e = 0; e < VW; ++e) acc[v][e] = fma((double)a[u][e], xv, acc[v][e]);
+            }
+        }
+        for (; j < jb; ++j) {
+          TA a[VW];
+          if (j < rc) ld16_sa<TA>(p + (unsigned)j * cst, a);
+          else ld16_g<TA>(pg + (int64_t)j * D.ld, a);
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const double xv = xs[v][j];
+#pragma unroll
+            for (int e = 0; e < VW; ++e) acc[v][e] = fma((double)a[e], xv, acc[v][e]);
+          }
+        }
+      }
+      double* st = shmem(E.sh);                                 // [KG][NV][rows]
+      const int64_t rows = (int64_t)wgr * 32 * VW;
+      if (act && grp > 0)
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+          for (int e = 0; e < VW; ++e) st[(grp * NV + v) * rows + q * VW + e] = acc[v][e];
+      __syncthreads();
+      if (act && grp == 0) {
+        for (int g = 1; g < KG; ++g)
+#pragma unroll
+          for (int v = 0; v < NV; ++v)
+#pragma unroll
+            for (int e = 0; e < VW; ++e) acc[v][e] += st[(g * NV + v) * rows + q * VW + e];
+        const int64_t i0 = q * VW;
+        int64_t ow = i0 < D.d ? slice_owner(D.d, E.nb, i0) : 0;
+        int64_t r0 = slice_r0(D.d, E.nb, ow), r1 = slice_r0(D.d, E.nb, ow + 1);
+#pragma unroll
+        for (int e = 0; e < VW; ++e) {
+          const int64_t i = i0 + e;
+          if (i < D.d) {
+            while (i >= r1) { ++ow; r0 = r1; r1 = slice_r0(D.d, E.nb, ow + 1); }
+            double* o = out + ow * reg + (i - r0);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+              double* ov = o + (size_t)v * E.pvec;
+              *ov = accumulate ? *ov + acc[v][e] : acc[v][e];
+            }
+          }
+        }
+      }
+      __syncthreads();                                          // E.sh free again for the caller
+      return;
+    }
+  }
   for (int64_t q = tix(); q < nvec; q += NTHR) {
     double acc[NV][VW];
 #pragma unroll
