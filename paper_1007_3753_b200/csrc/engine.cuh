@@ -566,6 +566,8 @@ struct Panel {
   const TA* gl;    // global column c0
   int rc;
   int w;
+  int oqv;         // 1: oq holds this thread's slice-major output offsets (ld / VW <= NTHR)
+  int oq[VecOf<TA>::VW];   // offset of row tix() * VW + e in the partial slot (-1: padding row)
 };
 
 template <class TA>
@@ -601,6 +603,7 @@ __device__ Panel<TA> setup_panel_at(const TA* Abase, int64_t ld, int64_t c0, int
   P.w = w;
   P.rc = rc < w ? rc : w;
   P.sm = dst;
+  P.oqv = 0;
   const int64_t n4 = (int64_t)P.rc * ld * (int64_t)sizeof(TA) / 16;
   const int4* src = reinterpret_cast<const int4*>(P.gl);
   int4* d4 = reinterpret_cast<int4*>(dst);
@@ -608,6 +611,9 @@ __device__ Panel<TA> setup_panel_at(const TA* Abase, int64_t ld, int64_t c0, int
   __syncthreads();
   return P;
 }
+
+template <class TA>
+__device__ __forceinline__ void panel_offsets_impl(const Ctx& E, const DictV<TA>& D, Panel<TA>& P);
 
 // Copy the first rc panel columns (contiguous in the column-major layout)
 // into shared memory.
@@ -618,6 +624,7 @@ __device__ Panel<TA> setup_panel(const Ctx& E, const DictV<TA>& D, TA* dst, int 
   P.w = E.w;
   P.rc = rc < E.w ? rc : E.w;
   P.sm = dst;
+  panel_offsets_impl<TA>(E, D, P);
   const int64_t n4 = (int64_t)P.rc * D.ld * (int64_t)sizeof(TA) / 16;
   const int4* src = reinterpret_cast<const int4*>(P.gl);
   int4* d4 = reinterpret_cast<int4*>(dst);
@@ -641,6 +648,27 @@ __device__ __forceinline__ int64_t slice_owner(int64_t d, int nb, int64_t i) {
   if (d * nb < 0xFFFFFFFFLL) return (int64_t)((((unsigned)i + 1u) * (unsigned)nb - 1u) / (unsigned)d);
   return ((i + 1) * nb - 1) / d;
 }
+// this thread's output offsets for its row vector (rows tix() * VW + e)
+template <class TA>
+__device__ __forceinline__ void panel_offsets_impl(const Ctx& E, const DictV<TA>& D, Panel<TA>& P) {
+  constexpr int VW = VecOf<TA>::VW;
+  const int64_t nvec = D.ld / VW;
+  P.oqv = nvec <= NTHR ? 1 : 0;
+  const int64_t reg = (int64_t)E.nb * E.rp;
+  const int64_t i0 = (int64_t)tix() * VW;
+  int64_t ow = i0 < D.d ? slice_owner(D.d, E.nb, i0) : 0;
+  int64_t r0 = slice_r0(D.d, E.nb, ow), r1 = slice_r0(D.d, E.nb, ow + 1);
+#pragma unroll
+  for (int e = 0; e < VW; ++e) {
+    const int64_t i = i0 + e;
+    P.oq[e] = -1;
+    if (i < D.d) {
+      while (i >= r1) { ++ow; r0 = r1; r1 = slice_r0(D.d, E.nb, ow + 1); }
+      P.oq[e] = (int)(ow * reg + (i - r0));
+    }
+  }
+}
+
 template <class TA, int NV>
 __device__ void panel_gemv(const Ctx& E, const DictV<TA>& D, const Panel<TA>& P,
                            const double* const (&xs)[NV], bool accumulate = false, int slot0 = 0) {
@@ -816,7 +844,18 @@ __device__ void panel_gemv(const Ctx& E, const DictV<TA>& D, const Panel<TA>& P,
         for (int e = 0; e < VW; ++e) acc[v][e] = fma((double)a[e], xv, acc[v][e]);
       }
     }
-    {
+    if (P.oqv) {                                  // q == tix(): offsets precomputed
+#pragma unroll
+      for (int e = 0; e < VW; ++e)
+        if (P.oq[e] >= 0) {
+          double* o = out + P.oq[e];
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            double* ov = o + (size_t)v * E.pvec;
+            *ov = accumulate ? *ov + acc[v][e] : acc[v][e];
+          }
+        }
+    } else {
       const int64_t i0 = q * VW;
       int64_t ow = i0 < D.d ? slice_owner(D.d, E.nb, i0) : 0;
       int64_t r0 = slice_r0(D.d, E.nb, ow), r1 = slice_r0(D.d, E.nb, ow + 1);
