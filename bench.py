@@ -704,7 +704,8 @@ def run_b200(args):
     if args.only_leg:
         legs = {"harness": lambda: leg_harness(torch), "cfg1": lambda: leg_cfg1(torch),
                 "cfg3": lambda: leg_cfg3(torch, dev), "cfg5": lambda: leg_cfg5(torch, dev, ws),
-                "cfg5_sweep": lambda: leg_cfg5_sweep(torch, dev)}
+                "cfg5_sweep": lambda: leg_cfg5_sweep(torch, dev),
+                "solvers_cfg2": lambda: leg_solvers_cfg2(torch, make_instance(rank))}
         print(json.dumps({args.only_leg: legs[args.only_leg]()}), flush=True)
         return
 

@@ -13,9 +13,11 @@ static __device__ void trsv_RT(const double* R, int ldr, int m, double* z, doubl
   for (int kb = 0; kb < m; kb += 32) {
     const int nbk = min(32, m - kb);
     // stage the 32 x 32 diagonal block
+    // diagonal staged as reciprocals: the serial chain multiplies instead of dividing
     for (int t = tix(); t < 32 * 32; t += NT) {
       const int i = t >> 5, j = t & 31;
-      tile[t] = (i < nbk && j < nbk) ? R[(size_t)(kb + i) * ldr + kb + j] : 0.0;
+      const double r = (i < nbk && j < nbk) ? R[(size_t)(kb + i) * ldr + kb + j] : 0.0;
+      tile[t] = (i == j && i < nbk) ? 1.0 / r : r;
     }
     __syncthreads();
     if (wpx() == 0) {
@@ -23,7 +25,7 @@ static __device__ void trsv_RT(const double* R, int ldr, int m, double* z, doubl
       double zj = j < nbk ? z[kb + j] : 0.0;
       for (int k = 0; k < nbk; ++k) {
         double zk = __shfl_sync(0xffffffffu, zj, k);
-        zk = zk / tile[k * 32 + k];
+        zk = zk * tile[k * 32 + k];
         if (j == k) zj = zk;
         if (j > k && j < nbk) zj = zj - tile[k * 32 + j] * zk;
       }
@@ -65,7 +67,8 @@ static __device__ void trsv_R(const double* R, int ldr, int m, double* z, double
     }
     for (int t = tix(); t < 32 * 32; t += NT) {
       const int i = t >> 5, j = t & 31;
-      tile[t] = (i < nbk && j < nbk) ? R[(size_t)(kb + i) * ldr + kb + j] : 0.0;
+      const double r = (i < nbk && j < nbk) ? R[(size_t)(kb + i) * ldr + kb + j] : 0.0;
+      tile[t] = (i == j && i < nbk) ? 1.0 / r : r;
     }
     __syncthreads();
     if (wpx() == 0) {
@@ -73,7 +76,7 @@ static __device__ void trsv_R(const double* R, int ldr, int m, double* z, double
       double zi = i < nbk ? z[kb + i] : 0.0;
       for (int k = nbk - 1; k >= 0; --k) {
         double dk = __shfl_sync(0xffffffffu, zi, k);
-        dk = dk / tile[k * 32 + k];
+        dk = dk * tile[k * 32 + k];
         if (i == k) zi = dk;
         if (i < k) zi = zi - tile[i * 32 + k] * dk;
       }

@@ -290,17 +290,30 @@ __device__ __forceinline__ void homotopy_body(const HomArgs& a) {
           gather<8>(E, G8, 0xFCu);
           // CTAs whose block min != global min must not contribute their index: recheck
           // by publishing again (cheap, scalars only)
-          double fix[3];
-          {
-            for (int t = 0; t < 3; ++t) {
-              double best = -INFINITY;
-              for (int q = lnx(); q < E.nb; q += 32) {
-                const double val = ldcg(published(E, 8, q, 2 + t));
-                const double idx = ldcg(published(E, 8, q, 5 + t));
-                if (val == G8[2 + t]) best = nmax(best, idx);
+          double fix[3] = {-INFINITY, -INFINITY, -INFINITY};
+          if (wpx() == 0) {
+            // warp 0 only (thread 0 consumes it); every load of a round is in flight at once
+            constexpr int QU = 4;
+            double best[3] = {-INFINITY, -INFINITY, -INFINITY};
+            for (int q0 = 0; q0 < E.nb; q0 += 32 * QU) {
+              double val[QU][3], idx[QU][3];
+#pragma unroll
+              for (int u = 0; u < QU; ++u) {
+                const int q = q0 + 32 * u + lnx();
+#pragma unroll
+                for (int t = 0; t < 3; ++t) {
+                  val[u][t] = q < E.nb ? ldcg(published(E, 8, q, 2 + t)) : NAN;
+                  idx[u][t] = q < E.nb ? ldcg(published(E, 8, q, 5 + t)) : -INFINITY;
+                }
               }
-              fix[t] = warp_max(best);
+#pragma unroll
+              for (int u = 0; u < QU; ++u)
+#pragma unroll
+                for (int t = 0; t < 3; ++t)
+                  if (val[u][t] == G8[2 + t]) best[t] = nmax(best[t], idx[u][t]);
             }
+#pragma unroll
+            for (int t = 0; t < 3; ++t) fix[t] = warp_max(best[t]);
           }
           T0 {
             V.drift = sqrt(G8[0]);

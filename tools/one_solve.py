@@ -38,6 +38,15 @@ def main():
     elif args.solver == "gpsr":
         from paper_1007_3753_b200.gradient_projection import gpsr_solve as fn
         run = lambda: fn(Pd, lam, cfg)
+    elif args.solver == "homotopy":
+        from paper_1007_3753_b200.homotopy import homotopy_solve as fn
+        run = lambda: fn(Pd, lam, SolverConfig())
+    elif args.solver == "ist":
+        from paper_1007_3753_b200.shrinkage import ist_solve as fn
+        run = lambda: fn(Pd, None, cfg)
+    elif args.solver == "tnipm":
+        from paper_1007_3753_b200.gradient_projection import tnipm_solve as fn
+        run = lambda: fn(Pd, lam, cfg)
     else:
         raise SystemExit("unknown solver")
     for _ in range(args.reps):
