@@ -1,8 +1,12 @@
 // homotopy.cu — LASSO solution path (homotopy.solve_path, homotopy.py:128-244)
 // as one persistent cooperative launch.
 //
-// Per breakpoint: the direction d_I = (A_I^T A_I)^{-1} sgn(c_I) from the
-// maintained upper Cholesky factor R (CTA 0: blocked triangular solves),
+// Per breakpoint: the direction d_I = (A_I^T A_I)^{-1} sgn(c_I) = W W^T sgn
+// from the maintained upper Cholesky factor R AND its inverse W = R^{-1}
+// (CTA 0: two parallel triangular matvecs instead of two serial
+// substitutions; appends extend W by one column, deletes rotate W's columns
+// with the same Givens sequence that re-triangularises R, refactorisations
+// rebuild W column-parallel over the whole grid),
 // v = A_I d_I (support-sparse panel GEMV: only support columns are read),
 // w = A^T v (panel GEMV^T), the drift check ||w_I - sgn|| (w_I == A_I^T v),
 // the step lengths gamma+/gamma- as grid-wide (value, lowest index) argmins,
@@ -23,7 +27,9 @@ struct HomArgs {
   int mmax;                 // factor capacity
   GridBufs g;
   double* R;                // mmax x mmax row-major upper factor
-  double* G;                // mmax x mmax scratch (dense refactor)
+  double* W;                // mmax x mmax row-major upper inverse W = R^{-1}
+  double* Wt;               // its transpose (row-major lower), so W^T v is a row-wise matvec too
+  double* G;                // mmax x mmax scratch (dense refactor, shifts)
   int* sup;                 // support list (reference order)
   int* posof;               // column -> support position or -1 (N)
   double* sgn;              // mmax
@@ -54,13 +60,104 @@ struct HomV {
 
 #define T0 if (threadIdx.x == 0)
 
+// Triangular matvec out = M v over rows of a row-major m x m triangle (ldr):
+// LOWER: row j uses columns [0, j]; else row i uses [i, m).  A warp takes 4
+// rows at a time and issues every load of a 128-column segment of all 4 rows
+// before the FMAs (one L2 round trip per 128-column segment, not per row).
+template <bool LOWER>
+static __device__ void tri_mv(const double* M, int ldr, int m, const double* v, double* out) {
+  constexpr int RW = 4, CH = 4;
+  for (int r0 = wpx() * RW; r0 < m; r0 += NWARP * RW) {
+    double acc[RW];
+#pragma unroll
+    for (int k = 0; k < RW; ++k) acc[k] = 0.0;
+    const int lo = LOWER ? 0 : r0;                   // union of the 4 rows' column ranges
+    const int hi = LOWER ? (r0 + RW - 1 < m - 1 ? r0 + RW - 1 : m - 1) + 1 : m;
+    for (int c0 = lo; c0 < hi; c0 += 32 * CH) {
+      double a[RW][CH];
+#pragma unroll
+      for (int k = 0; k < RW; ++k) {
+        const int r = r0 + k;
+        const double* row = M + (size_t)r * ldr;
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+          const int c = c0 + q * 32 + lnx();
+          const bool in = r < m && c < hi && (LOWER ? c <= r : c >= r);
+          a[k][q] = in ? row[c] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const int c = c0 + q * 32 + lnx();
+        const double x = c < hi ? v[c] : 0.0;
+#pragma unroll
+        for (int k = 0; k < RW; ++k) acc[k] = fma(a[k][q], x, acc[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < RW; ++k) {
+      const double t = warp_sum(acc[k]);
+      if (lnx() == 0 && r0 + k < m) out[r0 + k] = t;
+    }
+  }
+  __syncthreads();
+}
+
+// u = W^T s through the stored transpose (lower), d = W u
+static __device__ __forceinline__ void wt_mv(const double* Wt, int ldr, int m, const double* s, double* u) {
+  tri_mv<true>(Wt, ldr, m, s, u);
+}
+static __device__ __forceinline__ void w_mv(const double* W, int ldr, int m, const double* u, double* d) {
+  tri_mv<false>(W, ldr, m, u, d);
+}
+
+// chol_delete's LINPACK rank-1 update of the trailing block (factor.cuh
+// chol_update_shift) fused with the same Givens sequence on the inverse: step
+// p rotates W's column so + p with the extra column X (the deleted row's
+// column of W), W <- W G_p^T.  Whole CTA.
+static __device__ void chol_update_shift_w(double* R, double* W, double* Wt, int ldr, int so, int dof, int mt,
+                                           double* w, double* X, double* sc) {
+  for (int p = 0; p < mt; ++p) {
+    if (tix() == 0) {
+      const double rkk = R[(size_t)(so + p) * ldr + so + p];
+      const double r = hypot(rkk, w[p]);
+      sc[0] = r / rkk;
+      sc[1] = w[p] / rkk;
+      sc[2] = r;
+      sc[3] = rkk / r;
+      sc[4] = w[p] / r;
+    }
+    __syncthreads();
+    const double c = sc[0], s = sc[1];
+    for (int j = p + tix(); j < mt; j += NTHR) {
+      double row;
+      if (j == p) row = sc[2];
+      else {
+        row = (R[(size_t)(so + p) * ldr + so + j] + s * w[j]) / c;
+        w[j] = c * w[j] - s * row;
+      }
+      R[(size_t)(dof + p) * ldr + dof + j] = row;
+    }
+    const double cg = sc[3], sg = sc[4];
+    const int col = so + p;
+    for (int i = tix(); i <= col; i += NTHR) {
+      const double wa = Wt[(size_t)col * ldr + i], xb = X[i];
+      const double v = cg * wa + sg * xb;
+      W[(size_t)i * ldr + col] = v;
+      Wt[(size_t)col * ldr + i] = v;
+      X[i] = -sg * wa + cg * xb;
+    }
+    __syncthreads();
+  }
+}
+
 template <class TA>
 __device__ __forceinline__ void homotopy_body(const HomArgs& a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ Ctx E;
   __shared__ HomV V;
   __shared__ double tile[32 * 32];
-  __shared__ double sc[4];
+  __shared__ double sc[8];
   const DictV<TA> D = dict_view<TA>(a.D);
   double* ov = smem;
   T0 {
@@ -91,6 +188,7 @@ __device__ __forceinline__ void homotopy_body(const HomArgs& a) {
   double* T = ov + 4 * Wm;     // scratch (d_I on owned support / x_I)
   const int64_t N = D.n + (D.ext ? D.d : 0);
   double* zs = E.sh + 512;     // CTA-0 solves: z vector (mmax doubles) past the reduction scratch
+  double* us = zs + ldr;       // second CTA-0 vector (mmax doubles)
 
   // dot of the owned column k with a replicated d-vector (A column or s e_i)
   auto col_dot = [&](int k, const double* vec) -> double {
@@ -100,6 +198,21 @@ __device__ __forceinline__ void homotopy_body(const HomArgs& a) {
     double acc = 0.0;
     for (int64_t i = lnx(); i < D.ld; i += 32) acc = fma((double)col[i], ldcg(vec + i), acc);
     return warp_sum(acc);
+  };
+
+  // W = R^{-1} rebuilt column-parallel over the grid (after a dense
+  // refactorisation): CTA b solves R[0:j+1, 0:j+1] w = e_j for j = b, b + nb, ...
+  auto rebuild_w = [&](int m) {
+    for (int j = E.b; j < m; j += E.nb) {
+      for (int p = tix(); p <= j; p += NTHR) zs[p] = (p == j) ? 1.0 : 0.0;
+      __syncthreads();
+      trsv_R(a.R, ldr, j + 1, zs, tile);
+      for (int p = tix(); p <= j; p += NTHR) {
+        a.W[(size_t)p * ldr + j] = zs[p];
+        a.Wt[(size_t)j * ldr + p] = zs[p];
+      }
+      __syncthreads();
+    }
   };
 
   if (V.phase == 0) {
@@ -175,6 +288,8 @@ __device__ __forceinline__ void homotopy_body(const HomArgs& a) {
       T0 {
         if (!(q[0] > 0.0)) { V.status = ELL1_NOT_PD; }
         a.R[0] = sqrt(q[0]);
+        a.W[0] = 1.0 / a.R[0];
+        a.Wt[0] = a.W[0];
         a.sup[0] = V.ip;
         a.posof[V.ip] = 0;
         V.m = 1;
@@ -193,6 +308,8 @@ __device__ __forceinline__ void homotopy_body(const HomArgs& a) {
   }
 
   while (true) {
+    mark(E, 7);
+    mark(E, -1);
     T0 V.quit = V.it >= a.max_iter || (a.max_steps > 0 && V.steps >= a.max_steps);
     __syncthreads();
     if (V.quit) break;
@@ -205,6 +322,7 @@ __device__ __forceinline__ void homotopy_body(const HomArgs& a) {
       }
     });
     if (!grid_sync(E)) { T0 V.status = ELL1_ERR_TIMEOUT; goto out; }
+    mark(E, 0);
     {
       bool retry = true;
       while (retry) {
@@ -213,14 +331,15 @@ __device__ __forceinline__ void homotopy_body(const HomArgs& a) {
           const int m = V.m;
           for (int p = tix(); p < m; p += NTHR) zs[p] = ldcg(a.sgn + p);
           __syncthreads();
-          trsv_RT(a.R, ldr, m, zs, tile);
-          trsv_R(a.R, ldr, m, zs, tile);
+          wt_mv(a.Wt, ldr, m, zs, us);                       // u = W^T sgn = R^{-T} sgn
+          w_mv(a.W, ldr, m, us, zs);                         // d = W u
           for (int p = tix(); p < m; p += NTHR) {
             a.dI[p] = zs[p];
             a.dfull[a.sup[p]] = zs[p];
           }
         }
         if (!grid_sync(E)) { T0 V.status = ELL1_ERR_TIMEOUT; goto out; }
+        mark(E, 1);
         // v = A_I d_I (support-sparse panel GEMV)
         for_owned(E, [&](int k) { T[k] = (MK[k] != 0.0) ? ldcg(a.dfull + gcol(E, D.n, k)) : 0.0; });
         __syncthreads();
@@ -235,6 +354,7 @@ __device__ __forceinline__ void homotopy_body(const HomArgs& a) {
           a.Vd[i] = v;
         });
         if (!grid_sync(E)) { T0 V.status = ELL1_ERR_TIMEOUT; goto out; }
+        mark(E, 2);
         // w = A^T v; drift ||w_I - sgn||, ||sgn||; step lengths (homotopy.py:78-105)
         {
           const double* rs[1] = {a.Vd};
@@ -376,12 +496,15 @@ __device__ __forceinline__ void homotopy_body(const HomArgs& a) {
           }
           if (!grid_sync(E)) { T0 V.status = ELL1_ERR_TIMEOUT; goto out; }
           T0 { V.ridge = ((volatile int*)a.st->rot)[6]; V.fail = 0; }
+          rebuild_w(m);
           if (!grid_sync(E)) { T0 V.status = ELL1_ERR_TIMEOUT; goto out; }
           if (V.status != ELL1_OK) goto out;
+          T0 if (E.b == 0) a.st->rot[7] = a.st->rot[7] + 1;  // refactorisation count (diagnostics)
           retry = true;
         }
       }
     }
+    mark(E, 3);
     // ---- event (homotopy.py:192-223)
     T0 {
       const double ge = fmin(V.gp, V.gm);
@@ -407,29 +530,49 @@ __device__ __forceinline__ void homotopy_body(const HomArgs& a) {
       }
     }
     __syncthreads();
+    mark(E, 4);
     if (!V.finish) {
       if (V.remove) {
         // chol_delete(pos) on CTA 0 (numerics.py:140-158)
         if (E.b == 0) {
           const int m = V.m;
           const int pos = a.posof[V.im];
-          T0 sc[3] = (double)pos;
-          __syncthreads();
-          // top rows: columns > pos shift left
-          for (int i = 0; i < pos; ++i) {
-            double vals[4];
-            int cnt = 0;
-            for (int j = pos + 1 + tix(); j < m && cnt < 4; j += NTHR) vals[cnt++] = a.R[(size_t)i * ldr + j];
-            __syncthreads();
-            cnt = 0;
-            for (int j = pos + 1 + tix(); j < m && cnt < 4; j += NTHR) a.R[(size_t)i * ldr + j - 1] = vals[cnt++];
-            __syncthreads();
+          const int mt = m - pos - 1;
+          // X = W[:, pos] (rows <= pos): the column the rotations fold away
+          for (int i = tix(); i < m; i += NTHR) us[i] = i <= pos ? a.Wt[(size_t)pos * ldr + i] : 0.0;
+          // top rows of R: columns > pos shift left (two parallel passes through G)
+          for (int t = tix(); t < pos * mt; t += NTHR) {
+            const int i = t / mt, j = pos + 1 + (t - i * mt);
+            a.G[(size_t)i * ldr + j - 1] = a.R[(size_t)i * ldr + j];
           }
-          if (pos < m - 1) {
-            const int mt = m - pos - 1;
+          __syncthreads();
+          for (int t = tix(); t < pos * mt; t += NTHR) {
+            const int i = t / mt, j = pos + (t - i * mt);
+            a.R[(size_t)i * ldr + j] = a.G[(size_t)i * ldr + j];
+          }
+          __syncthreads();
+          if (mt > 0) {
             for (int j = tix(); j < mt; j += NTHR) zs[j] = a.R[(size_t)pos * ldr + pos + 1 + j];
             __syncthreads();
-            chol_update_shift(a.R, ldr, pos + 1, pos, mt, zs, sc);
+            chol_update_shift_w(a.R, a.W, a.Wt, ldr, pos + 1, pos, mt, zs, us, sc);
+          }
+          // W' = (W G^T) without row pos and column pos (entries with j' >= pos change)
+          {
+            const int m1 = m - 1, wc = m1 - pos;          // new columns pos .. m-2
+            for (int t = tix(); t < m1 * wc; t += NTHR) {
+              const int i = t / wc, j = pos + (t - i * wc);
+              if (j >= i) a.G[(size_t)i * ldr + j] = a.W[(size_t)(i + (i >= pos ? 1 : 0)) * ldr + j + 1];
+            }
+            __syncthreads();
+            for (int t = tix(); t < m1 * wc; t += NTHR) {
+              const int i = t / wc, j = pos + (t - i * wc);
+              if (j >= i) {
+                const double v = a.G[(size_t)i * ldr + j];
+                a.W[(size_t)i * ldr + j] = v;
+                a.Wt[(size_t)j * ldr + i] = v;             // rows pos.. of Wt (row j, col i)
+              }
+            }
+            __syncthreads();
           }
           // support list / positions
           T0 {
@@ -443,6 +586,7 @@ __device__ __forceinline__ void homotopy_body(const HomArgs& a) {
           }
         }
         T0 V.m = V.m - 1;
+        mark(E, 5);
       } else {
         // chol_append (numerics.py:115-137): gcol = A_I^T a_ip, diag = a_ip . a_ip
         const int64_t ip = V.ip;
@@ -468,14 +612,23 @@ __device__ __forceinline__ void homotopy_body(const HomArgs& a) {
           double q[1] = {0.0};
           for (int64_t i = tix(); i < D.ld; i += NTHR) { const double c = ldcg(a.colv + i); q[0] += c * c; }
           block_reduce<1>(E, q, 0u);
-          for (int p = tix(); p < m; p += NTHR) zs[p] = ldcg(a.gcol + p);
+          for (int p = tix(); p < m; p += NTHR) us[p] = ldcg(a.gcol + p);
           __syncthreads();
-          trsv_RT(a.R, ldr, m, zs, tile);
+          wt_mv(a.Wt, ldr, m, us, zs);                      // r = R^{-T} g = W^T g
           double uu[1] = {0.0};
           for (int p = tix(); p < m; p += NTHR) uu[0] += zs[p] * zs[p];
           block_reduce<1>(E, uu, 0u);
           const double d2 = q[0] - uu[0];
           if (d2 > 0.0 && m < ldr) {
+            // inverse column: W[:m, m] = -(W r) / rho, W[m, m] = 1 / rho
+            w_mv(a.W, ldr, m, zs, us);
+            const double rho = sqrt(d2);
+            for (int p = tix(); p < m; p += NTHR) {
+              const double v = -us[p] / rho;
+              a.W[(size_t)p * ldr + m] = v;
+              a.Wt[(size_t)m * ldr + p] = v;
+            }
+            T0 { a.W[(size_t)m * ldr + m] = 1.0 / rho; a.Wt[(size_t)m * ldr + m] = 1.0 / rho; }
             for (int p = tix(); p < m; p += NTHR) a.R[(size_t)p * ldr + m] = zs[p];
             T0 {
               a.R[(size_t)m * ldr + m] = sqrt(d2);
@@ -535,8 +688,11 @@ __device__ __forceinline__ void homotopy_body(const HomArgs& a) {
             const bool ok2 = dense_chol(a.G, a.R, ldr, m, sc);
             T0 { if (!ok2) V.status = ELL1_NOT_PD; V.note = 1; }
           }
+          if (!grid_sync(E)) { T0 V.status = ELL1_ERR_TIMEOUT; goto out; }
+          rebuild_w(m);
           T0 V.ridge = 0;
         }
+        mark(E, 6);
       }
     }
     // ---- fresh residual and correlations (homotopy.py:224-234)
@@ -659,7 +815,7 @@ extern "C" size_t ell1_homotopy_workspace(const ell1_dict_t* D, int32_t blocks) 
   const int nb = pick_blocks(D->n, blocks);
   const int64_t N = ncols_of(D);
   const int64_t m = hom_mmax(D);
-  return grid_bytes(nb, D->d, 1) + 2 * align_up(m * m * 8, 256) + 2 * align_up(m * 4, 256) +
+  return grid_bytes(nb, D->d, 1) + 4 * align_up(m * m * 8, 256) + 2 * align_up(m * 4, 256) +
          align_up(N * 4, 256) + 3 * align_up(m * 8, 256) + align_up(N * 8, 256) +
          3 * align_up(D->ld * 8, 256) + 4096;
 }
@@ -680,7 +836,8 @@ static int homotopy_setup(const ell1_dict_t* D, const double* b, double target_l
   const int64_t m = a.mmax;
   Carve cv(io->workspace, io->workspace_bytes);
   if (!carve_grid(cv, a.g, nb, D->d, 1)) return ELL1_ERR_ARG;
-  a.R = cv.take<double>(m * m); a.G = cv.take<double>(m * m);
+  a.R = cv.take<double>(m * m); a.W = cv.take<double>(m * m); a.Wt = cv.take<double>(m * m);
+  a.G = cv.take<double>(m * m);
   a.sup = cv.take<int>(m); a.posof = cv.take<int>(N);
   a.sgn = cv.take<double>(m); a.dI = cv.take<double>(m); a.gcol = cv.take<double>(m);
   a.dfull = cv.take<double>(N);
@@ -696,8 +853,8 @@ static int homotopy_setup(const ell1_dict_t* D, const double* b, double target_l
   a.max_steps = io->max_steps;
   a.prof = io->phase_ns;
   sp = plan_smem(a.D, nb, HOM_OV, 8, false);
-  // CTA-0 solves keep z (mmax doubles) in the scratch area past 512 reduction doubles
-  if (sp.scratch < 512 + m) { sp.bytes += (size_t)(512 + m - sp.scratch) * 8; sp.scratch = 512 + m; }
+  // CTA-0 solves keep z and u (2 x mmax doubles) in the scratch area past 512 reduction doubles
+  if (sp.scratch < 512 + 2 * m) { sp.bytes += (size_t)(512 + 2 * m - sp.scratch) * 8; sp.scratch = 512 + 2 * m; }
   a.g.shcap = sp.scratch;
   a.g.panel_bytes = 0;
   a.wmax = sp.wmax;

@@ -109,3 +109,37 @@ def test_matches_oracle_random(hom, model):
         res = hom.homotopy_solve(model.ProblemInstance(A, b), target, model.SolverConfig())
         assert res.iterations == ref.iterations, trial
         assert rel_err(res.x_star, ref.x) <= 1e-8
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_maintained_inverse_needs_no_refactorisation(seed):
+    """homotopy.cu keeps W = R^{-1} next to R (appends extend it, deletes rotate
+    it with R's Givens sequence).  If W drifted from R^{-1}, the drift check
+    would trigger dense refactorisations (counted in state.rot[7]); a clean
+    path — including remove events — must need none (the reference's
+    test_no_fresh_factorization_on_clean_path, homotopy.py:53-64)."""
+    import torch
+    from paper_1007_3753_b200 import _lib, device as dv
+    from paper_1007_3753_b200._runner import Buffers, Prepared, byref
+    from paper_1007_3753_b200.model import ProblemInstance, SolverConfig
+    rng = np.random.default_rng(40 + seed)
+    d, n = 120, 400
+    A = rng.standard_normal((d, n))
+    A /= np.linalg.norm(A, axis=0)
+    b = A @ oracle.sparse_signal(n, 30, 40 + seed) + 0.02 * rng.standard_normal(d)
+    cfg = SolverConfig(lam=None, tol=1.0, max_iter=2000)
+    prep = Prepared(ProblemInstance(A, b), cfg)
+    L = _lib.lib()
+    bufs = Buffers(prep, L.ell1_homotopy_workspace(byref(prep.view), 0), cfg.max_iter + 2)
+    out = _lib.HomOut()
+    cb = torch.zeros(prep.n, dtype=torch.float64, device=prep.dev)
+    out.c = cb.data_ptr()
+    lam = 1e-3 * float(np.max(np.abs(A.T @ b)))
+    _lib.check(L.ell1_homotopy(byref(prep.view), dv.ptr(prep.b), lam, cfg.max_iter, byref(out),
+                               byref(bufs.io(0)), prep.stream), "homotopy")
+    st = bufs.read_all()
+    ref, _ = oracle.homotopy(A, b, lam, max_iter=2000)
+    removes = sum(1 for a0, a1 in zip(ref.trace, ref.trace[1:]) if a1[3] < a0[3])
+    assert st.iterations == ref.iterations and removes > 0
+    assert st.rot[7] == 0
+    np.testing.assert_allclose(bufs.x_host(), ref.x, atol=1e-8 * max(1.0, np.abs(ref.x).max()))
