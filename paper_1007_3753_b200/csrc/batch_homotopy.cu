@@ -418,12 +418,19 @@ __global__ void __launch_bounds__(HBT) hb_step(HB a, int nact) {
     const int im = dec[3];
     const int p0 = pos[im];
     T0 X[im] = 0.0;
-    for (int i = 0; i < p0; ++i) {                         // rows above: shift columns > p0 left
-      for (int jj = p0 + 1 + tix(); jj < m; jj += HBT) row[jj] = R[(size_t)i * ldr + jj];
-      __syncthreads();
-      for (int jj = p0 + 1 + tix(); jj < m; jj += HBT) R[(size_t)i * ldr + jj - 1] = row[jj];
-      __syncthreads();
+    // rows above: shift columns > p0 left — a warp per row, each 32-column
+    // chunk read before any lane writes (row-local, so rows run in parallel)
+    for (int i = wpx(); i < p0; i += HBW) {
+      double* Ri = R + (size_t)i * ldr;
+      for (int j0 = p0 + 1; j0 < m; j0 += 32) {
+        const int jj = j0 + lnx();
+        const double v = jj < m ? Ri[jj] : 0.0;
+        __syncwarp();
+        if (jj < m) Ri[jj - 1] = v;
+        __syncwarp();
+      }
     }
+    __syncthreads();
     if (p0 < m - 1) {
       const int mt = m - p0 - 1;
       for (int jj = tix(); jj < mt; jj += HBT) zs[jj] = R[(size_t)p0 * ldr + p0 + 1 + jj];
