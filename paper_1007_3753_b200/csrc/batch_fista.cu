@@ -131,9 +131,13 @@ __global__ void __launch_bounds__(BT) bf_step(const BFArgs a) {
     double k5[5] = {0, 0, 0, 0, 0};
     for (int64_t k = threadIdx.x; k < a.N; k += BT) {
       double g;
-      if (k < a.n) g = a.f32 ? (double)a.G32[(int64_t)j * a.n + k] : gc[k];
-      else g = a.s * rc[k - a.n];
-      gc[k] = g;
+      if (k < a.n) {
+        if (a.f32) { g = (double)a.G32[(int64_t)j * a.n + k]; gc[k] = g; }
+        else g = gc[k];                                    // the GEMM wrote it in place
+      } else {
+        g = a.s * rc[k - a.n];
+        gc[k] = g;
+      }
       const double xk = xc[k];
       const double c = -g;
       if (xk != 0.0) { k5[0] = nmax(k5[0], fabs(c - lam * sgn(xk))); k5[2] = 1.0; }

@@ -49,6 +49,7 @@ def to_device_vec(v, length, dev):
     v = np.ascontiguousarray(v, dtype=np.float64)
     out = torch.zeros(length, dtype=torch.float64, device=dev)
     if v.shape[0]:
+        # stream-ordered: from pinned memory the copy overlaps the host work that follows
         out[: v.shape[0]].copy_(torch.from_numpy(v), non_blocking=False)
     return out
 
@@ -67,7 +68,7 @@ class DeviceDictionary:
     (operators.py:53-56, cached spectral_norm_sq).
     """
 
-    def __init__(self, A, dtype="float64", device=None):
+    def __init__(self, A, dtype="float64", device=None, _overlap=False):
         torch = _torch()
         L = _lib.lib()
         self.device = current_device(device)
@@ -79,7 +80,12 @@ class DeviceDictionary:
             host = np.ascontiguousarray(A, dtype=np.float64)
             if host.ndim != 2:
                 raise ValueError("dictionary must be a matrix")
-            src = torch.from_numpy(host).to(self.device, non_blocking=False)
+            # _overlap (solver-internal uploads only): the H2D is left in flight so it
+            # overlaps the host-side setup of the solve; safe because the caller's
+            # array is used in place (no temporary), stays referenced by the
+            # problem, and the solve synchronises before it returns.  Stream
+            # order puts ell1_dict_build below after the copy.
+            src = torch.from_numpy(host).to(self.device, non_blocking=bool(_overlap and host is A))
         if src.ndim != 2:
             raise ValueError("dictionary must be a matrix")
         self.d, self.n = int(src.shape[0]), int(src.shape[1])
@@ -175,7 +181,7 @@ def as_device_dictionary(A, config=None):
     if config is not None:
         dtype = config.opt("dtype", "float64")
         dev = config.opt("device", None)
-    return DeviceDictionary(A, dtype=dtype, device=dev), True
+    return DeviceDictionary(A, dtype=dtype, device=dev, _overlap=True), True
 
 
 def correlation_max(A, b, device=None):
