@@ -24,6 +24,7 @@ struct DI {
 struct BDArgs {
   int64_t d, n, N, ld, ldx;
   int ext, f32, cg;
+  int fuse_ext;              // fp32 [A, sI]: [M | Ginv] V as one tensor-core GEMM (no GEXT)
   double s, beta, ytol;
   const double* Bm;         // ld x B
   const double* C0;         // ld x B  (Ginv b)
@@ -104,7 +105,8 @@ __global__ void __launch_bounds__(BT) bd_z(const BDArgs a) {
     a.Z[o + k] = z;
     const double vv = k < a.n ? z - xb : a.s * (z - xb);
     a.V[o + k] = vv;
-    if (a.f32 && k < a.n) { a.V32[o + k] = (float)vv; a.Z32[o + k] = (float)z; }
+    if (a.f32 && (k < a.n || a.fuse_ext)) a.V32[o + k] = (float)vv;
+    if (a.f32 && k < a.n) a.Z32[o + k] = (float)z;
   }
 }
 
@@ -121,7 +123,7 @@ __global__ void __launch_bounds__(BT) bd_y(const BDArgs a) {
   double q[2] = {0.0, 0.0};
   for (int64_t i = threadIdx.x; i < a.d; i += BT) {
     double mv = bd_rd(a, a.P1, a.P1f, oj + i);
-    if (a.ext) mv = mv + a.GEXT[oj + i];
+    if (a.ext && !a.fuse_ext) mv = mv + a.GEXT[oj + i];
     const double yi = mv + a.C0[oj + i] / a.beta;
     double az = bd_rd(a, a.P2, a.P2f, oj + i);
     if (a.ext) az = az + a.s * zx[i];
@@ -262,6 +264,30 @@ __global__ void __launch_bounds__(BT) bd_refine(const BDArgs a, const double* de
   if (threadIdx.x == 0) I.by = q[0];
 }
 
+// row-major 3xTF32 split of [M | Ginv] (ld x N, pitch pr): the y-step's two
+// products M v_A + Ginv (s v_ext) as one K = n + d GEMM
+__global__ void bd_mext_split(const float* __restrict__ M, const double* __restrict__ Ginv, int64_t ld, int64_t n,
+                              int64_t d, int64_t pr, float* __restrict__ hi, float* __restrict__ lo) {
+  __shared__ float t[32][33];
+  const int64_t k0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t k = k0 + r, i = i0 + threadIdx.x;
+    float x = 0.f;
+    if (i < ld) x = k < n ? M[k * ld + i] : (k < n + d ? (float)Ginv[(k - n) * ld + i] : 0.f);
+    t[r][threadIdx.x] = x;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t i = i0 + r, k = k0 + threadIdx.x;
+    if (i < ld && k < pr) {
+      const float x = t[threadIdx.x][r];
+      const float h = tf32_rna(x);
+      hi[i * pr + k] = h;
+      lo[i * pr + k] = tf32_rna(x - h);
+    }
+  }
+}
+
 __global__ void bd_scan(DI* inst, int B, int* perm, int* newB) {
   __shared__ int base;
   __shared__ int wsum[32];
@@ -316,7 +342,8 @@ extern "C" size_t ell1_batch_dalm_workspace(const ell1_dict_t* D, int32_t B) {
        align_up(ld * 2 * B * 4, 256);
   s += 2 * align_up((int64_t)sizeof(DI) * B, 256) + align_up(B * 4, 256) + align_up(ldx * B * 8, 256);
   if (D->dtype == ELL1_F32)                                  // splits of A and M + operand scratch
-    s += (size_t)(f32split_floats(D, (ldx > ld ? ldx : ld) * 2 * B) + 2 * align_up(D->n * D->ld, 64)) * 4 + 2048;
+    s += (size_t)(f32split_floats(D, (ldx > ld ? ldx : ld) * 2 * B) + f32split_dict_floats(D) +
+                  2 * align_up(ld * ldx, 64)) * 4 + 2048;
   return s + 8192;
 }
 
@@ -332,7 +359,7 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   const int64_t N = ncols_of(D), ldx = r4(N), ld = D->ld, d = D->d;
   BDArgs a;
   a.d = d; a.n = D->n; a.N = N; a.ld = ld; a.ldx = ldx;
-  a.ext = D->ext; a.f32 = D->dtype == ELL1_F32; a.cg = O->y_cg_step;
+  a.ext = D->ext; a.f32 = D->dtype == ELL1_F32; a.cg = O->y_cg_step; a.fuse_ext = 0;
   a.s = D->ext_scale; a.beta = O->beta; a.ytol = O->y_tol;
   a.C = *C;
   if (a.cg) return ELL1_ERR_ARG;   // batched CG y-step: not provided (use the single-instance solver)
@@ -359,18 +386,23 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   int* ctr = cv.take<int>(8);
   if (!cv.ok) return ELL1_ERR_ARG;
   (void)xscr; (void)T32;
-  F32Split spA, spM;
+  F32Split spA, spM, spX;
   const F32Split* pA = nullptr;
   const F32Split* pM = nullptr;
   if (a.f32) {
     if (!f32split_setup(spA, cv, D, (ldx > ld ? ldx : ld) * 2 * B, s)) return ELL1_ERR_ARG;
-    ell1_dict_t MDs = *D;
-    MDs.A = O->M;
-    float* mh = cv.take<float>(D->n * D->ld);
-    float* ml = cv.take<float>(D->n * D->ld);
-    if (!cv.ok || !split_tf32((const float*)O->M, mh, ml, D->n * D->ld, s)) return ELL1_ERR_ARG;
     spM = spA;                                               // shares the operand scratch
-    spM.Ahi = mh; spM.Alo = ml;
+    if (!f32split_dict(spM, cv, D, (const float*)O->M, s)) return ELL1_ERR_ARG;
+    if (a.ext && fp32_mode_select() == 3) {
+      float* xh = cv.take<float>(ld * ldx);
+      float* xl = cv.take<float>(ld * ldx);
+      if (!cv.ok) return ELL1_ERR_ARG;
+      dim3 g((unsigned)((ldx + 31) / 32), (unsigned)((ld + 31) / 32));
+      bd_mext_split<<<g, dim3(32, 8), 0, s>>>((const float*)O->M, O->Ginv, ld, D->n, d, ldx, xh, xl);
+      spX = spM;
+      spX.Arhi = xh; spX.Arlo = xl; spX.pr = ldx;
+      a.fuse_ext = 1;
+    }
     pA = &spA; pM = &spM;
   }
   a.Bm = Bm; a.C0 = C0;
@@ -423,9 +455,15 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
     {
       const void* Vop = a.f32 ? (const void*)a.V32 : (const void*)a.V;
       const void* Zop = a.f32 ? (const void*)a.Z32 : (const void*)a.Z;
-      if (!gemm_AX(h, &MD, Vop, ldx, a.f32 ? (void*)a.P1f : (void*)a.P1, ld, Bcur, pM)) return ELL1_ERR_CUDA;
+      if (a.fuse_ext) {
+        // P1 = [M | Ginv] V over K = n + d (V's identity block already carries s)
+        if (!sgemm_split(h, CUBLAS_OP_N, (int)ld, Bcur, (int)N, nullptr, 0, &spX, a.V32, ldx, a.P1f, ld, N))
+          return ELL1_ERR_CUDA;
+      } else if (!gemm_AX(h, &MD, Vop, ldx, a.f32 ? (void*)a.P1f : (void*)a.P1, ld, Bcur, pM)) {
+        return ELL1_ERR_CUDA;
+      }
       if (!gemm_AX(h, D, Zop, ldx, a.f32 ? (void*)a.P2f : (void*)a.P2, ld, Bcur, pA)) return ELL1_ERR_CUDA;
-      if (a.ext) {
+      if (a.ext && !a.fuse_ext) {
         // identity block of M: s Ginv v_ext (s folded into v_ext by bd_z)
         if (cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)ld, Bcur, (int)d, &one, O->Ginv, (int)ld,
                         a.V + D->n, (int)ldx, &zero, a.GEXT, (int)ld) != CUBLAS_STATUS_SUCCESS)

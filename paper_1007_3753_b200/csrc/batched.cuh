@@ -14,6 +14,7 @@
 #include <cublas_v2.h>
 #include <cstdlib>
 #include "solvers_common.cuh"
+#include "tc_gemm.cuh"
 
 namespace ell1 {
 
@@ -50,7 +51,8 @@ struct Blas {
   int dev = -1;
 };
 
-// fp32 GEMM path of the batched solvers: 2 = 3xTF32 split on the tensor pipe,
+// fp32 GEMM path of the batched solvers: 3 = 3xTF32 tcgen05 kernel (tc_gemm.cu,
+// default), 2 = 3xTF32 split over three cuBLAS TF32 GEMMs (ELL1_FP32_GEMM=tf32x3),
 // 0 = SIMT SGEMM (ELL1_FP32_GEMM=simt), -1 = not used yet.
 inline int& fp32_gemm_mode() {
   static int mode = -1;
@@ -71,19 +73,22 @@ inline cublasHandle_t blas_handle(cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------- 3xTF32 fp32 GEMMs
-// fp32 products of the batched solvers run on the tensor pipe as three TF32
-// GEMMs with split operands (a = a_hi + a_lo, both TF32-representable):
+// fp32 products of the batched solvers run on the tensor pipe as 3xTF32: both
+// operands are split a = a_hi + a_lo (both TF32-representable) and
 //   A X ~= A_lo X_hi + A_hi X_lo + A_hi X_hi     (fp32 accumulation)
-// which keeps fp32-level accuracy (the dropped A_lo X_lo term is ~2^-22
-// relative) at TF32 tensor-core throughput.  The dictionary split is made
-// once per solve; the right operand is split per product into caller
-// workspace.  Opt-in (ELL1_FP32_GEMM=tf32x3): measured on B200 at config 3
-// the three launches per product (skinny n x B GEMMs, B <= 1024) cost more
-// than one SIMT SGEMM and the DALM certificate refines more often, so SIMT
-// SGEMM stays the default.
+// keeps fp32-level accuracy (the dropped A_lo X_lo term is ~2^-22 relative).
+// Default: one tcgen05 kernel accumulates the three products in TMEM
+// (tc_gemm.cu).  The dictionary split is made once per solve, in both
+// orientations (column-major for A^T R, row-major for A X: the kernel reads
+// K-major operands); the right operand is split per product into caller
+// workspace.  ELL1_FP32_GEMM=tf32x3 runs the split as three cuBLAS TF32 GEMMs,
+// ELL1_FP32_GEMM=simt uses cuBLAS SIMT SGEMM.
 struct F32Split {
-  const float* Ahi;         // split dictionary, same layout as D->A
+  const float* Ahi;         // split dictionary, same layout as D->A (column-major, ld)
   const float* Alo;
+  const float* Arhi;        // split dictionary, row-major (ld rows of pr floats)
+  const float* Arlo;
+  int64_t pr;
   float* Xhi;               // right-operand scratch (xcap floats each)
   float* Xlo;
   int64_t xcap;
@@ -105,6 +110,27 @@ static __global__ void split_tf32_kernel(const float* __restrict__ src, float* _
   }
 }
 
+// row-major split of a column-major (ld x n) dictionary: hi/lo[i * pr + k] from src[k * ld + i]
+static __global__ void split_tf32_t_kernel(const float* __restrict__ src, float* __restrict__ hi,
+                                           float* __restrict__ lo, int64_t ld, int64_t n, int64_t pr) {
+  __shared__ float t[32][33];
+  const int64_t k0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t k = k0 + r, i = i0 + threadIdx.x;
+    t[r][threadIdx.x] = (k < n && i < ld) ? src[k * ld + i] : 0.f;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t i = i0 + r, k = k0 + threadIdx.x;
+    if (i < ld && k < pr) {
+      const float x = t[threadIdx.x][r];
+      const float h = tf32_rna(x);
+      hi[i * pr + k] = h;
+      lo[i * pr + k] = tf32_rna(x - h);
+    }
+  }
+}
+
 inline bool split_tf32(const float* src, float* hi, float* lo, int64_t n, cudaStream_t s) {
   if (n <= 0) return true;
   int64_t g = (n + 255) / 256;
@@ -113,14 +139,16 @@ inline bool split_tf32(const float* src, float* hi, float* lo, int64_t n, cudaSt
   return cudaGetLastError() == cudaSuccess;
 }
 
-inline bool use_tf32x3() {
+inline int fp32_mode_select() {
   static int v = -1;
   if (v < 0) {
     const char* env = getenv("ELL1_FP32_GEMM");
-    v = (env && (env[0] == 't' || env[0] == 'T')) ? 1 : 0;   // opt-in: ELL1_FP32_GEMM=tf32x3
-    fp32_gemm_mode() = v ? 2 : 0;
+    if (env && (env[0] == 's' || env[0] == 'S')) v = 0;
+    else if (env && (env[0] == 't' || env[0] == 'T')) v = 2;
+    else v = tc3_available() == 1 ? 3 : 0;
+    fp32_gemm_mode() = v;
   }
-  return v == 1;
+  return v;
 }
 
 // Y (m x B) = op(A) X with fp32 operands through the 3xTF32 split (sp) or SIMT SGEMM
@@ -128,14 +156,24 @@ inline bool sgemm_split(cublasHandle_t h, cublasOperation_t opA, int m, int B, i
                         int lda, const F32Split* sp, const float* X, int64_t ldx, float* Y, int64_t ldy,
                         int64_t xrows) {
   const float one = 1.0f, zero = 0.0f;
-  if (!sp || !use_tf32x3()) {
+  const int mode = fp32_mode_select();
+  if (!sp || mode == 0) {
+    return cublasSgemm(h, opA, CUBLAS_OP_N, m, B, k, &one, A, lda, X, (int)ldx, &zero, Y, (int)ldy) ==
+           CUBLAS_STATUS_SUCCESS;
+  }
+  cudaStream_t s;
+  cublasGetStream(h, &s);
+  if (mode == 3) {
+    // the kernel splits the right operand tile by tile in shared memory
+    const bool ok = opA == CUBLAS_OP_N ? tc3_gemm(m, B, k, sp->Arhi, sp->Arlo, sp->pr, X, ldx, Y, ldy, s)
+                                       : tc3_gemm(m, B, k, sp->Ahi, sp->Alo, lda, X, ldx, Y, ldy, s);
+    if (ok) return true;
+    if (!A) return false;
     return cublasSgemm(h, opA, CUBLAS_OP_N, m, B, k, &one, A, lda, X, (int)ldx, &zero, Y, (int)ldy) ==
            CUBLAS_STATUS_SUCCESS;
   }
   const int64_t xn = ldx * (int64_t)(B - 1) + xrows;
   if (xn > sp->xcap) return false;
-  cudaStream_t s;
-  cublasGetStream(h, &s);
   if (!split_tf32(X, sp->Xhi, sp->Xlo, xn, s)) return false;
   const cublasComputeType_t ct = CUBLAS_COMPUTE_32F_FAST_TF32;
   const void* terms[3][2] = {{sp->Alo, sp->Xhi}, {sp->Ahi, sp->Xlo}, {sp->Ahi, sp->Xhi}};
@@ -176,20 +214,37 @@ inline bool gemm_AtR(cublasHandle_t h, const ell1_dict_t* D, const void* R, int6
                      (const float*)R, ldr, (float*)G, ldg, D->ld);
 }
 
+// workspace floats for one dictionary split (both orientations)
+inline int64_t f32split_dict_floats(const ell1_dict_t* D) {
+  return 2 * align_up(D->n * D->ld, 64) + 2 * align_up(D->ld * align_up(D->n, 4), 64);
+}
+
 // workspace floats for the dictionary split + the right-operand scratch
 inline int64_t f32split_floats(const ell1_dict_t* D, int64_t xcap) {
-  return 2 * align_up(D->n * D->ld, 64) + 2 * align_up(xcap, 64);
+  return f32split_dict_floats(D) + 2 * align_up(xcap, 64);
+}
+
+// split a column-major (ld x n) fp32 dictionary A into sp's four arrays
+inline bool f32split_dict(F32Split& sp, Carve& cv, const ell1_dict_t* D, const float* A, cudaStream_t s) {
+  float* hi = cv.take<float>(D->n * D->ld);
+  float* lo = cv.take<float>(D->n * D->ld);
+  const int64_t pr = align_up(D->n, 4);
+  float* rhi = cv.take<float>(D->ld * pr);
+  float* rlo = cv.take<float>(D->ld * pr);
+  if (!cv.ok) return false;
+  sp.Ahi = hi; sp.Alo = lo; sp.Arhi = rhi; sp.Arlo = rlo; sp.pr = pr;
+  if (!split_tf32(A, hi, lo, D->n * D->ld, s)) return false;
+  dim3 g((unsigned)((pr + 31) / 32), (unsigned)((D->ld + 31) / 32));
+  split_tf32_t_kernel<<<g, dim3(32, 8), 0, s>>>(A, rhi, rlo, D->ld, D->n, pr);
+  return cudaGetLastError() == cudaSuccess;
 }
 
 inline bool f32split_setup(F32Split& sp, Carve& cv, const ell1_dict_t* D, int64_t xcap, cudaStream_t s) {
-  float* hi = cv.take<float>(D->n * D->ld);
-  float* lo = cv.take<float>(D->n * D->ld);
+  if (!f32split_dict(sp, cv, D, (const float*)D->A, s)) return false;
   sp.Xhi = cv.take<float>(xcap);
   sp.Xlo = cv.take<float>(xcap);
   sp.xcap = xcap;
-  sp.Ahi = hi; sp.Alo = lo;
-  if (!cv.ok) return false;
-  return split_tf32((const float*)D->A, hi, lo, D->n * D->ld, s);
+  return cv.ok;
 }
 
 }  // namespace ell1
