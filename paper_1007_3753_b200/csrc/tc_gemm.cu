@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 
 #include "tc_gemm.cuh"
@@ -85,6 +86,18 @@ __device__ __forceinline__ float tf32_rna_dev(float x) {
   return __uint_as_float(r);
 }
 
+#ifdef TC3_TIMING
+__device__ unsigned long long g_tc3_dbg[16];
+#define TW(slot, cond, stmt)                                        \
+  {                                                                 \
+    const long long _t = clock64();                                 \
+    stmt;                                                           \
+    if (cond) atomicAdd(&g_tc3_dbg[slot], (unsigned long long)(clock64() - _t)); \
+  }
+#else
+#define TW(slot, cond, stmt) stmt;
+#endif
+
 template <int BN, int ST>
 struct Smem {
   static constexpr int A_BYTES = TM * TK * 4;         // 16 KB
@@ -94,19 +107,27 @@ struct Smem {
   static constexpr int TOTAL = ST * STAGE + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-// Warp roles (192 threads): warp 0 lane 0 = TMA producer, warp 1 lane 0 = MMA
-// issuer, warps 2-5 = split + drain.  Per k-block the drain warps split the
-// raw B tile in place (hi) and into the lo tile, and — one k-block behind the
-// tensor core — add the block's TMEM partial product into fp32 registers:
-// the tensor pipe's accumulation spans only 32 products, the running sum is
-// IEEE fp32 (keeps the SIMT SGEMM's accuracy).  TMEM holds two BN-column
-// partial buffers (MMA fills one while the other drains).
-template <int BN, int ST>
-__global__ void __launch_bounds__(192, 1)
+// Warp roles (320 threads): warp 0 lane 0 = TMA producer, warp 1 lane 0 = MMA
+// issuer, warps 2-5 = drain, warps 6-9 = split.  Per k-block the split warps
+// split the raw B tile in place (hi) and into the lo tile; every KC k-blocks
+// the drain warps add the tensor pipe's TMEM partial product into fp32 registers (the tensor
+// core's own accumulation spans only KC*32 products, the running sum is IEEE
+// fp32: keeps the SIMT SGEMM's accuracy).  TMEM holds two BN-column partial
+// buffers (the MMA fills one while the other drains).
+// SK = 2 splits K over a 2-CTA cluster (small GEMMs: bigger tiles, same CTA
+// count); rank 1 hands its fp32 sums to rank 0 through distributed shared
+// memory and rank 0 adds them in a fixed order (deterministic) and writes C.
+template <int BN, int ST, int KC, int SK>
+__global__ void __launch_bounds__(320, 1)
     tc3_gemm_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                     const __grid_constant__ CUtensorMap mB, int M, int N, int K, float* __restrict__ C,
                     int64_t ldc) {
   using S = Smem<BN, ST>;
+  static_assert(BN % 32 == 0 && BN <= 128, "BN");
+  static_assert(SK == 1 || ST * S::STAGE >= BN * TM * 4, "partial exchange buffer");
+#ifdef TC3_TIMING
+  const long long t_start = clock64();
+#endif
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + ST * S::STAGE);
@@ -117,7 +138,12 @@ __global__ void __launch_bounds__(192, 1)
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * TM, n0 = blockIdx.y * BN;
-  const int nkb = (K + TK - 1) / TK;
+  const int nkb_all = (K + TK - 1) / TK;
+  const int kz = SK == 1 ? 0 : (int)blockIdx.z;            // == cluster rank (cluster dims 1 x 1 x SK)
+  const int kh = (nkb_all + SK - 1) / SK;
+  const int kb0 = kz * kh;
+  const int nkb = (nkb_all - kb0 < kh ? nkb_all - kb0 : kh);   // >= 1 when K > TK * (SK - 1)
+  constexpr uint32_t TCOLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 256;
 
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&mAh) : "memory");
@@ -136,35 +162,40 @@ __global__ void __launch_bounds__(192, 1)
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(2 * BN));
+                 "n"(TCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  float acc[BN];
+#pragma unroll
+  for (int j = 0; j < BN; ++j) acc[j] = 0.f;
+  const int q = warp & 3;                                    // TMEM lane quarter of a drain warp
 
   if (warp == 0) {
     if (lane == 0) {
       // ---- TMA producer
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % ST, u = kb / ST;
-        if (u > 0) mbar_wait(empty + s, (u - 1) & 1);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % ST, u = i / ST, kc = (kb0 + i) * TK;
+        if (u > 0) TW(0, true, mbar_wait(empty + s, (u - 1) & 1));
         uint8_t* st = smem + s * S::STAGE;
         mbar_expect_tx(full + s, S::TX);
-        tma_load_2d(st, &mAh, kb * TK, m0, full + s);
-        tma_load_2d(st + S::A_BYTES, &mAl, kb * TK, m0, full + s);
-        tma_load_2d(st + 2 * S::A_BYTES, &mB, kb * TK, n0, full + s);
+        tma_load_2d(st, &mAh, kc, m0, full + s);
+        tma_load_2d(st + S::A_BYTES, &mAl, kc, m0, full + s);
+        tma_load_2d(st + 2 * S::A_BYTES, &mB, kc, n0, full + s);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---- MMA issuer: one fresh partial per k-block, lo*hi + hi*lo + hi*hi
+      // ---- MMA issuer: one fresh partial per KC k-blocks, lo*hi + hi*lo + hi*hi
       constexpr uint32_t idesc = instr_desc<BN>();
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % ST, u = kb / ST, buf = kb & 1, ub = kb >> 1;
-        if (ub > 0) mbar_wait(tempty + buf, (ub - 1) & 1);
-        mbar_wait(conv + s, u & 1);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % ST, u = i / ST, p = i / KC, buf = p & 1, ub = p >> 1;
+        const bool first = i % KC == 0, last = i % KC == KC - 1 || i == nkb - 1;
+        if (first && ub > 0) TW(1, true, mbar_wait(tempty + buf, (ub - 1) & 1));
+        TW(2, true, mbar_wait(conv + s, u & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         uint8_t* st = smem + s * S::STAGE;
         const uint64_t ah = smem_desc(st), al = smem_desc(st + S::A_BYTES);
@@ -173,31 +204,26 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
         for (int k = 0; k < TK / UK; ++k) {
           const uint64_t dk = (uint64_t)((k * UK * 4) >> 4);      // +32 bytes along K inside the swizzle row
-          umma_tf32(td, al + dk, bh + dk, idesc, k != 0);
+          umma_tf32(td, al + dk, bh + dk, idesc, (k != 0 || !first) ? 1u : 0u);
           umma_tf32(td, ah + dk, bl + dk, idesc, 1u);
           umma_tf32(td, ah + dk, bh + dk, idesc, 1u);
         }
         umma_commit(empty + s);
-        umma_commit(tfull + buf);
+        if (last) umma_commit(tfull + buf);
       }
     }
-  } else {
-    // ---- split + drain warps (2..5); TMEM lane quarter = warp % 4
-    const int et = threadIdx.x - 64;                         // 0..127
-    const int q = warp & 3;
+  } else if (warp < 6) {
+    // ---- drain warps (2..5): TMEM partials -> fp32 registers
     const uint32_t tlane = tmem + ((uint32_t)(q * 32) << 16);
-    float acc[BN];
-#pragma unroll
-    for (int j = 0; j < BN; ++j) acc[j] = 0.f;
-    auto drain = [&](int kb) {
-      const int buf = kb & 1;
-      mbar_wait(tfull + buf, (kb >> 1) & 1);
+    for (int p = 0; p < (nkb + KC - 1) / KC; ++p) {
+      const int buf = p & 1;
+      TW(3, threadIdx.x == 64, mbar_wait(tfull + buf, (p >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 64) {
-        uint32_t r[64];
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
 #pragma unroll
-        for (int c = 0; c < 64; c += 16) {
+        for (int c = 0; c < 32; c += 16) {
           asm volatile(
               "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
               "[%16];"
@@ -208,38 +234,63 @@ __global__ void __launch_bounds__(192, 1)
         }
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int j = 0; j < 64; ++j) acc[c0 + j] += __uint_as_float(r[j]);
+        for (int j = 0; j < 32; ++j) acc[c0 + j] += __uint_as_float(r[j]);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(tempty + buf);
-    };
-    // split the raw B tile of k-block kb's stage: hi in place, lo into the next tile
-    auto split = [&](int kb) {
-      const int s = kb % ST, u = kb / ST;
-      mbar_wait(full + s, u & 1);
+    }
+  } else {
+    // ---- split warps (6..9): raw B tile -> hi in place, lo into the next tile
+    const int et = threadIdx.x - 192;                        // 0..127
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % ST, u = i / ST;
+      TW(4, threadIdx.x == 192, mbar_wait(full + s, u & 1));
       const uint32_t bh = smem_u32(smem + s * S::STAGE + 2 * S::A_BYTES);
       const uint32_t bl = bh + S::B_BYTES;
 #pragma unroll
-      for (int i = et * 16; i < S::B_BYTES; i += 128 * 16) {
+      for (int o = et * 16; o < S::B_BYTES; o += 128 * 16) {
         float x0, x1, x2, x3;
-        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x0), "=f"(x1), "=f"(x2), "=f"(x3) : "r"(bh + i));
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x0), "=f"(x1), "=f"(x2), "=f"(x3) : "r"(bh + o));
         const float h0 = tf32_rna_dev(x0), h1 = tf32_rna_dev(x1), h2 = tf32_rna_dev(x2), h3 = tf32_rna_dev(x3);
-        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(bh + i), "f"(h0), "f"(h1), "f"(h2), "f"(h3)
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(bh + o), "f"(h0), "f"(h1), "f"(h2), "f"(h3)
                      : "memory");
-        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(bl + i), "f"(tf32_rna_dev(x0 - h0)),
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(bl + o), "f"(tf32_rna_dev(x0 - h0)),
                      "f"(tf32_rna_dev(x1 - h1)), "f"(tf32_rna_dev(x2 - h2)), "f"(tf32_rna_dev(x3 - h3))
                      : "memory");
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(conv + s);
-    };
-    // split one k-block ahead of the drain so the tensor pipe never waits on it
-    split(0);
-    for (int kb = 0; kb < nkb; ++kb) {
-      if (kb + 1 < nkb) split(kb + 1);
-      drain(kb);
     }
-    const int row = m0 + q * 32 + lane;
+  }
+  const bool drainw = warp >= 2 && warp < 6;
+  const int row_l = q * 32 + lane;                           // tile row of a drain thread
+  if constexpr (SK == 2) {
+    // rank 1 -> rank 0 partial sums through DSMEM (the operand ring is idle now)
+    const uint32_t xbuf = smem_u32(smem);
+    // both CTAs are past their main loops before rank 1 writes into rank 0's ring
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (kz == 1 && drainw) {
+      uint32_t rbuf;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rbuf) : "r"(xbuf));
+#pragma unroll
+      for (int j = 0; j < BN; ++j)
+        asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(rbuf + (uint32_t)((j * TM + row_l) * 4)), "f"(acc[j])
+                     : "memory");
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (kz == 0 && drainw) {
+#pragma unroll
+      for (int j = 0; j < BN; ++j) {
+        float v;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(xbuf + (uint32_t)((j * TM + row_l) * 4)));
+        acc[j] += v;
+      }
+    }
+  }
+  if (drainw && kz == 0) {
+    const int row = m0 + row_l;
     if (row < M) {
 #pragma unroll
       for (int j = 0; j < BN; ++j) {
@@ -250,7 +301,13 @@ __global__ void __launch_bounds__(192, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN));
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS));
+#ifdef TC3_TIMING
+  if (threadIdx.x == 0) {
+    atomicAdd(&g_tc3_dbg[5], (unsigned long long)(clock64() - t_start));
+    atomicAdd(&g_tc3_dbg[6], 1ull);
+  }
+#endif
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -280,26 +337,51 @@ bool make_map(CUtensorMap* m, const float* p, int K, int rows, int64_t ld, int b
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, int ST>
+template <int BN, int ST, int SK, int KC>
 bool launch(int M, int N, int K, const float* ah, const float* al, int64_t lda, const float* b, int64_t ldb,
             float* C, int64_t ldc, cudaStream_t s) {
   CUtensorMap mAh, mAl, mB;
   if (!make_map(&mAh, ah, K, M, lda, TM) || !make_map(&mAl, al, K, M, lda, TM) || !make_map(&mB, b, K, N, ldb, BN))
     return false;
   constexpr int smem = Smem<BN, ST>::TOTAL;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(tc3_gemm_kernel<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-        cudaSuccess)
-      return false;
-    attr = true;
+  auto kern = tc3_gemm_kernel<BN, ST, KC, SK>;
+  static unsigned attr = 0;                                  // per-device bit
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr >> (dev & 31) & 1u)) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
+    attr |= 1u << (dev & 31);
   }
-  dim3 grid((unsigned)((M + TM - 1) / TM), (unsigned)((N + BN - 1) / BN));
-  tc3_gemm_kernel<BN, ST><<<grid, 192, smem, s>>>(mAh, mAl, mB, M, N, K, C, ldc);
-  return cudaGetLastError() == cudaSuccess;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((M + TM - 1) / TM), (unsigned)((N + BN - 1) / BN), (unsigned)SK);
+  cfg.blockDim = dim3(320, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = SK;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, mAh, mAl, mB, M, N, K, C, ldc) == cudaSuccess;
 }
 
+// SMEM bytes moved per k-block (TMA fill + in-smem split + three MMA operand reads),
+// the resource that bounds these tiles
+constexpr double kb_cost(int bn) { return 80.0 * 1024 + 7.0 * bn * 128; }
+
 }  // namespace
+
+#ifdef TC3_TIMING
+void tc3_debug(unsigned long long* out, bool reset) {
+  cudaMemcpyFromSymbol(out, g_tc3_dbg, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_tc3_dbg, z, sizeof(z));
+  }
+}
+#endif
 
 int tc3_available() {
   std::call_once(g_once, init_once);
@@ -311,10 +393,45 @@ bool tc3_gemm(int M, int N, int K, const float* a_hi, const float* a_lo, int64_t
   if (M <= 0 || N <= 0) return true;
   if (K <= 0 || tc3_available() != 1) return false;
   if ((lda & 3) || (ldb & 3) || (((uintptr_t)a_hi | (uintptr_t)a_lo | (uintptr_t)b) & 15)) return false;
-  // fill the 148 SMs: 128 x 128 tiles when they already give >= one wave, else 128 x 64
-  const int tiles128 = ((M + TM - 1) / TM) * ((N + 127) / 128);
-  if (tiles128 >= 148) return launch<128, 3>(M, N, K, a_hi, a_lo, lda, b, ldb, C, ldc, s);
-  return launch<64, 4>(M, N, K, a_hi, a_lo, lda, b, ldb, C, ldc, s);
+  // pick the tile (BN) and K split (SK) with the least per-SM smem traffic on
+  // the critical path: waves x k-blocks per CTA x bytes per k-block (+ fixed costs)
+  const int mt = (M + TM - 1) / TM, nkb = (K + TK - 1) / TK;
+  struct Opt { int bn, sk; } opts[] = {{64, 1}, {96, 1}, {128, 1}, {64, 2}, {96, 2}, {128, 2}};
+  double best = 1e300;
+  Opt pick = {64, 1};
+  for (const Opt& o : opts) {
+    if (o.sk == 2 && nkb < 4) continue;
+    const long ctas = (long)mt * ((N + o.bn - 1) / o.bn) * o.sk;
+    const long waves = (ctas + 147) / 148;
+    const double kbs = (double)((nkb + o.sk - 1) / o.sk);
+    const double t = waves * (kbs * kb_cost(o.bn) + 24.0 * 1024 + (o.sk == 2 ? 24.0 * 1024 : 0.0));
+    if (t < best) { best = t; pick = o; }
+  }
+  static int force = -1;
+  if (force < 0) {
+    const char* e = getenv("ELL1_TC3_FORCE");             // diagnostics: "<bn><sk>", e.g. 1282
+    force = e ? atoi(e) : 0;
+  }
+  static int kc = -1;
+  if (kc < 0) {
+    const char* e = getenv("ELL1_TC3_KC");                // diagnostics: k-blocks per TMEM partial
+    kc = e && atoi(e) == 2 ? 2 : 1;
+  }
+  const int code = force ? force : pick.bn * 10 + pick.sk;
+#define TC3_CASE(BN_, ST_, SK_)                                                              \
+  case BN_ * 10 + SK_:                                                                       \
+    return kc == 2 ? launch<BN_, ST_, SK_, 2>(M, N, K, a_hi, a_lo, lda, b, ldb, C, ldc, s)   \
+                   : launch<BN_, ST_, SK_, 1>(M, N, K, a_hi, a_lo, lda, b, ldb, C, ldc, s);
+  switch (code) {
+    TC3_CASE(64, 4, 1)
+    TC3_CASE(96, 3, 1)
+    TC3_CASE(128, 3, 1)
+    TC3_CASE(64, 4, 2)
+    TC3_CASE(96, 3, 2)
+    default:
+    TC3_CASE(128, 3, 2)
+  }
+#undef TC3_CASE
 }
 
 }  // namespace ell1

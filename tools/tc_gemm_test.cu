@@ -9,6 +9,9 @@
 #include <cstdlib>
 #include <vector>
 #include "tc_gemm.cuh"
+#ifdef TC3_TIMING
+namespace ell1 { void tc3_debug(unsigned long long* out, bool reset); }
+#endif
 
 static float rna(float x) {  // host tf32 round-to-nearest-away
   unsigned u;
@@ -52,6 +55,22 @@ int main(int argc, char** argv) {
     cudaMemcpy(dBh, Bh.data(), B.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(dBl, Bl.data(), B.size() * 4, cudaMemcpyHostToDevice);
     cudaMemset(dC, 0xFF, (size_t)ldc * N * 4);
+#ifdef TC3_TIMING
+    {
+      unsigned long long dbg[16];
+      ell1::tc3_gemm(M, N, K, dAh, dAl, lda, dB, ldb, dC, ldc, 0);
+      cudaDeviceSynchronize();
+      ell1::tc3_debug(dbg, true);
+      for (int r = 0; r < 5; ++r) ell1::tc3_gemm(M, N, K, dAh, dAl, lda, dB, ldb, dC, ldc, 0);
+      cudaDeviceSynchronize();
+      ell1::tc3_debug(dbg, true);
+      const double ctas = (double)dbg[6], nkb = (K + 31) / 32;
+      printf("timing per CTA per k-block (cycles): prod-wait-empty %.0f mma-wait-tempty %.0f mma-wait-conv %.0f "
+             "drain-wait-tfull %.0f split-wait-full %.0f | CTA total %.0f cyc (%.0f per kb)\n",
+             dbg[0] / ctas / nkb, dbg[1] / ctas / nkb, dbg[2] / ctas / nkb, dbg[3] / ctas / nkb, dbg[4] / ctas / nkb,
+             dbg[5] / ctas, dbg[5] / ctas / nkb);
+    }
+#endif
     bool ok = ell1::tc3_gemm(M, N, K, dAh, dAl, lda, dB, ldb, dC, ldc, 0);
     cudaError_t e = cudaDeviceSynchronize();
     if (!ok || e != cudaSuccess) {
