@@ -413,9 +413,21 @@ int ell1_pd_update(int64_t N2, int64_t d, double* x, const double* dx, double ap
 /* M[i][i] += alpha v[i] (v NULL: none), *trace = sum_i M[i][i]  (jitter, robust.py:148) */
 int ell1_pd_diag(int64_t d, int64_t ldm, double* M, double alpha, const double* v, double* trace, void* stream);
 
-/* fp32 GEMM path of the batched solvers (2: 3xTF32 split GEMMs on the tensor
- * pipe, opt-in with ELL1_FP32_GEMM=tf32x3; 0: SIMT SGEMM; -1: not used yet). */
+/* fp32 GEMM path of the batched solvers (3: 3xTF32 tcgen05 kernel, the default;
+ * 2: 3xTF32 split over cuBLAS TF32 GEMMs, ELL1_FP32_GEMM=tf32x3; 0: SIMT SGEMM,
+ * ELL1_FP32_GEMM=simt; -1: not used yet). */
 int ell1_blas_fp32_mode(void);
+
+/* The batched solvers' fp32 dictionary product on its own (new; the
+ * reference's equivalent is the numpy `A @ X` / `A.T @ R` of its solvers,
+ * e.g. alm.py:179, 239, shrinkage.py:271-272, looped over instances):
+ *   trans = 0: C (M x N) = A (M x K, column-major, lda >= M) * B (K x N, ldb)
+ *   trans = 1: C (M x N) = A^T (A is K x M, column-major, lda >= K) * B
+ * fp32-accurate (3xTF32 on tcgen05, per-k-block fp32 accumulation).  B, C
+ * column-major; lda, ldb multiples of 4; workspace holds the split A. */
+size_t ell1_gemm_f32_workspace(int32_t trans, int64_t M, int64_t K);
+int ell1_gemm_f32(int32_t trans, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
+                  int64_t ldb, float* C, int64_t ldc, void* ws, size_t wsb, void* stream);
 
 /* library / device info */
 int ell1_device_sms(int32_t device);

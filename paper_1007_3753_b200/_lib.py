@@ -212,6 +212,11 @@ _SIGS = {
     "ell1_homotopy_group": (ctypes.c_int, [P(Group), ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
                                            ctypes.c_void_p]),
     "ell1_blas_fp32_mode": (ctypes.c_int, []),
+    "ell1_gemm_f32_workspace": (ctypes.c_size_t, [ctypes.c_int32, ctypes.c_int64, ctypes.c_int64]),
+    "ell1_gemm_f32": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                     ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
+                                     ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t,
+                                     ctypes.c_void_p]),
     "ell1_device_sms": (ctypes.c_int, [ctypes.c_int32]),
     "ell1_version": (ctypes.c_char_p, []),
 }

@@ -110,19 +110,20 @@ static __global__ void split_tf32_kernel(const float* __restrict__ src, float* _
   }
 }
 
-// row-major split of a column-major (ld x n) dictionary: hi/lo[i * pr + k] from src[k * ld + i]
+// row-major split of a column-major (rows x n, stride ld) matrix: hi/lo[i * pr + k] from src[k * ld + i]
 static __global__ void split_tf32_t_kernel(const float* __restrict__ src, float* __restrict__ hi,
-                                           float* __restrict__ lo, int64_t ld, int64_t n, int64_t pr) {
+                                           float* __restrict__ lo, int64_t rows, int64_t ld, int64_t n,
+                                           int64_t pr) {
   __shared__ float t[32][33];
   const int64_t k0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     const int64_t k = k0 + r, i = i0 + threadIdx.x;
-    t[r][threadIdx.x] = (k < n && i < ld) ? src[k * ld + i] : 0.f;
+    t[r][threadIdx.x] = (k < n && i < rows) ? src[k * ld + i] : 0.f;
   }
   __syncthreads();
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     const int64_t i = i0 + r, k = k0 + threadIdx.x;
-    if (i < ld && k < pr) {
+    if (i < rows && k < pr) {
       const float x = t[threadIdx.x][r];
       const float h = tf32_rna(x);
       hi[i * pr + k] = h;
@@ -235,7 +236,7 @@ inline bool f32split_dict(F32Split& sp, Carve& cv, const ell1_dict_t* D, const f
   sp.Ahi = hi; sp.Alo = lo; sp.Arhi = rhi; sp.Arlo = rlo; sp.pr = pr;
   if (!split_tf32(A, hi, lo, D->n * D->ld, s)) return false;
   dim3 g((unsigned)((pr + 31) / 32), (unsigned)((D->ld + 31) / 32));
-  split_tf32_t_kernel<<<g, dim3(32, 8), 0, s>>>(A, rhi, rlo, D->ld, D->n, pr);
+  split_tf32_t_kernel<<<g, dim3(32, 8), 0, s>>>(A, rhi, rlo, D->ld, D->ld, D->n, pr);
   return cudaGetLastError() == cudaSuccess;
 }
 
