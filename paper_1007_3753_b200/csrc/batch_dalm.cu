@@ -424,7 +424,8 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   int Bcur = B;
   // hc = {refine flags, active instances}: read once here, then together with
   // every certificate round's refine count (one device->host sync per iteration)
-  int hc[2] = {0, 0};
+  int* hc = host_mailbox();
+  hc[0] = hc[1] = 0;
   if (cudaMemcpyAsync(hc, ctr, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
   if (cudaStreamSynchronize(s) != cudaSuccess) return ELL1_ERR_CUDA;
   while (true) {

@@ -402,7 +402,8 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
     bf_init<<<B, BT, 0, s>>>(a, (const double*)CT, (const float*)CT, B);
   }
   int Bcur = B;
-  int h_ctr[2] = {0, 0};
+  int* h_ctr = host_mailbox();
+  h_ctr[0] = h_ctr[1] = 0;
   constexpr int SYNC_EVERY = 8;          // rounds between reads of the active count
   for (int64_t round = 0;; ++round) {
     if (round % SYNC_EVERY == 0) {

@@ -665,9 +665,10 @@ extern "C" int ell1_batch_homotopy(const ell1_dict_t* D, const double* Bmat, int
     hb_dir<<<nact, HBT, smem, s>>>(a, nact);
     // drop finished instances from the GEMM operands
     hb_scan<<<1, 1024, 0, s>>>(a.st, act, nact, perm, ctr);
-    int nn = 0;
-    if (cudaMemcpyAsync(&nn, ctr, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
+    int* box = host_mailbox();
+    if (cudaMemcpyAsync(box, ctr, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
     if (cudaStreamSynchronize(s) != cudaSuccess) return ELL1_ERR_CUDA;
+    const int nn = box[0];
     if (nn == 0) break;
     if (nn < nact) {
       dim3 g((unsigned)std::min<int64_t>((ld + 255) / 256, 8), (unsigned)nn);

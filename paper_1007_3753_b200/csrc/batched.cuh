@@ -59,6 +59,20 @@ inline int& fp32_gemm_mode() {
   return mode;
 }
 
+// Pinned host mailbox (per thread, 16 ints) for the per-round device counter
+// read-backs of the batched host loops: a pageable 8-byte D2H is a staged
+// copy (~7 us on the B200 box), a pinned one is a direct DMA.
+inline int* host_mailbox() {
+  static thread_local int* box = nullptr;
+  static thread_local int fallback[16];
+  if (!box) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, 64) == cudaSuccess) box = (int*)p;
+    else box = fallback;
+  }
+  return box;
+}
+
 inline cublasHandle_t blas_handle(cudaStream_t s) {
   static thread_local Blas B[16];
   int dev = 0;

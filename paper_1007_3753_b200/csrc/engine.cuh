@@ -19,6 +19,10 @@
 #include <stdint.h>
 #include "../../include/ell1_b200.h"
 
+#ifndef ELL1_GT_QU32
+#define ELL1_GT_QU32 1    // fp32 long-column GEMV^T: row steps per lane in flight
+#endif
+
 namespace ell1 {
 
 constexpr int NTHR = 512;
@@ -1026,7 +1030,7 @@ __device__ void panel_gemv_t_pre(const Ctx& E, const DictV<TA>& D, const Panel<T
     // per chunk.  The CPW columns of a warp are walked together, so each lane
     // keeps CPW independent 16-byte loads of A in flight.
     constexpr int CPW = sizeof(TA) == 8 ? 2 : 4;        // columns per warp
-    constexpr int QU = sizeof(TA) == 8 ? 2 : 1;         // row steps per lane in flight
+    constexpr int QU = sizeof(TA) == 8 ? 2 : ELL1_GT_QU32;  // row steps per lane in flight
     constexpr int SPT = 4;                              // staged doubles per thread per chunk
     int64_t rch = (int64_t)NTHR * SPT / (VW * NV);      // row vectors per chunk
     while (rch * VW * NV * 2 > E.shcap && rch > 32) rch /= 2;
