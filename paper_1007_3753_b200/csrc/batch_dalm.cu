@@ -39,6 +39,8 @@ struct BDArgs {
   double* P1; double* P2;   // GEMM outputs ld x B / ld x 2B (fp64)
   double* GEXT;             // ld x B (Ginv v_ext)
   float* V32; float* Z32; float* UX32; float* Y32; float* P1f; float* P2f; float* P3f;
+  float* UT32;               // fp32 storage: U = A^T y (n x B, pitch n), the GEMM output itself;
+                             // the fp64 copies of U and x_new in UX are then not kept
   DI* inst;
   ell1_ctrl_t C;
   int* counters;            // [0] refine, [1] active
@@ -69,6 +71,8 @@ __global__ void __launch_bounds__(BT) bd_init(const BDArgs a) {
     a.X[1][(int64_t)j * a.ldx + k] = 0.0;
     a.UX[(int64_t)j * a.ldx + k] = 0.0;            // A^T y_0 = 0
   }
+  if (a.f32)
+    for (int64_t k = threadIdx.x; k < a.n; k += BT) a.UT32[(int64_t)j * a.n + k] = 0.f;
   cta_reduce<1>(v, 0u, sh);
   if (threadIdx.x == 0) {
     I.orig = j; I.it = 0; I.hist = 0; I.conv = 0; I.status = ELL1_OK; I.l1_prev = 0.0; I.refine = 0;
@@ -98,13 +102,18 @@ __global__ void __launch_bounds__(BT) bd_z(const BDArgs a) {
   const int64_t o = (int64_t)j * a.ldx;
   const double* x = a.X[a.ix] + o;
   const double* u = a.UX + o;
+  const float* u32 = a.UT32 + (int64_t)j * a.n;
+  const double* ycur = a.Y[a.iy] + (int64_t)j * a.ld;
+  const bool keep_v = !a.f32 || (a.ext && !a.fuse_ext);    // fp64 v feeds a GEMM only then
   for (int64_t k = threadIdx.x; k < a.N; k += BT) {
     const double xb = x[k] / a.beta;
-    const double t = u[k] + xb;
+    // U = A^T y of the current y: fp32 storage reads the GEMM output (+ s y for [A, sI])
+    const double uk = !a.f32 ? u[k] : (k < a.n ? (double)u32[k] : a.s * ycur[k - a.n]);
+    const double t = uk + xb;
     const double z = t > 1.0 ? 1.0 : (t < -1.0 ? -1.0 : t);
     a.Z[o + k] = z;
     const double vv = k < a.n ? z - xb : a.s * (z - xb);
-    a.V[o + k] = vv;
+    if (keep_v) a.V[o + k] = vv;
     if (a.f32 && (k < a.n || a.fuse_ext)) a.V32[o + k] = (float)vv;
     if (a.f32 && k < a.n) a.Z32[o + k] = (float)z;
   }
@@ -155,10 +164,9 @@ __global__ void __launch_bounds__(BT) bd_x(const BDArgs a, const double* Ut, con
     double uk;
     if (k < a.n) uk = a.f32 ? (double)Ut32[(int64_t)j * a.n + k] : Ut[(int64_t)j * a.n + k];
     else uk = a.s * y[k - a.n];                           // robust.py:96
-    u[k] = uk;
     const double xo = x[k];
     const double xv = xo - a.beta * (a.Z[o + k] - uk);
-    xn[k] = xv;
+    if (!a.f32) { u[k] = uk; xn[k] = xv; }                // fp64 GEMM operand [U | x_new]
     a.X[a.ix ^ 1][o + k] = xv;
     if (a.f32 && k < a.n) {
       a.UX32[o + k] = (float)uk;
@@ -185,13 +193,15 @@ __global__ void __launch_bounds__(BT) bd_c(const BDArgs a, int refine_only) {
   const int64_t oj = (int64_t)j * a.ld;
   const double* b = a.Bm + oj;
   const double* u = a.UX + (int64_t)j * a.ldx;
-  const double* xn = a.UX + ((int64_t)B + j) * a.ldx;
+  // x_new: fp32 storage keeps it only in X (the UX copy is the fp64 GEMM operand)
+  const double* xn = a.f32 ? a.X[a.ix ^ 1] + (int64_t)j * a.ldx : a.UX + ((int64_t)B + j) * a.ldx;
+  const double* ynew = a.Y[a.iy ^ 1] + oj;
   const double cut = 1e-10 * pymax(I.S[2], 1.0);
   double q[3] = {0.0, 0.0, 0.0};
   for (int64_t i = threadIdx.x; i < a.d; i += BT) {
     double aau = bd_rd(a, a.P2, a.P2f, ((int64_t)j) * a.ld + i);
     double ax = bd_rd(a, a.P2, a.P2f, ((int64_t)B + j) * a.ld + i);
-    if (a.ext) { aau = aau + a.s * u[a.n + i]; ax = ax + a.s * xn[a.n + i]; }
+    if (a.ext) { aau = aau + a.s * (a.f32 ? a.s * ynew[i] : u[a.n + i]); ax = ax + a.s * xn[a.n + i]; }
     const double resid = a.RHS[oj + i] - aau;
     a.RES[oj + i] = resid;
     a.AX[oj + i] = ax;
@@ -385,7 +395,8 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   double* scratch = cv.take<double>(ldx * B);
   int* ctr = cv.take<int>(8);
   if (!cv.ok) return ELL1_ERR_ARG;
-  (void)xscr; (void)T32;
+  (void)xscr;
+  a.UT32 = T32;
   F32Split spA, spM, spX;
   const F32Split* pA = nullptr;
   const F32Split* pM = nullptr;
@@ -439,7 +450,13 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
         cudaMemcpyAsync(M, scratch, ldm * nact * 8, cudaMemcpyDeviceToDevice, s);
       };
       pm(a.X[a.ix], N, ldx);
-      pm(a.UX, N, ldx);                                     // A^T y of the current y
+      if (a.f32) {                                          // A^T y of the current y
+        dim3 g((unsigned)((D->n + 255) / 256 < 64 ? (D->n + 255) / 256 : 64), (unsigned)nact);
+        bd_gather<float><<<g, 256, 0, s>>>(T32, (float*)scratch, D->n, D->n, perm, nact);
+        cudaMemcpyAsync(T32, scratch, D->n * nact * 4, cudaMemcpyDeviceToDevice, s);
+      } else {
+        pm(a.UX, N, ldx);
+      }
       pm(a.Y[a.iy], ld, ld);
       pm(a.AX, ld, ld);
       pm(C0, ld, ld);
