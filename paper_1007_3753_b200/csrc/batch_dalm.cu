@@ -100,22 +100,30 @@ __global__ void __launch_bounds__(BT) bd_z(const BDArgs a) {
   if (!I.active) return;
   if (threadIdx.x == 0) { I.it++; I.refine = 0; }
   const int64_t o = (int64_t)j * a.ldx;
-  const double* x = a.X[a.ix] + o;
-  const double* u = a.UX + o;
-  const float* u32 = a.UT32 + (int64_t)j * a.n;
-  const double* ycur = a.Y[a.iy] + (int64_t)j * a.ld;
+  const double* __restrict__ x = a.X[a.ix] + o;
+  const double* __restrict__ u = a.UX + o;
+  const float* __restrict__ u32 = a.UT32 + (int64_t)j * a.n;
+  const double* __restrict__ ycur = a.Y[a.iy] + (int64_t)j * a.ld;
+  double* __restrict__ zo = a.Z + o;
+  double* __restrict__ vo = a.V + o;
+  float* __restrict__ v32 = a.V32 + o;
+  float* __restrict__ z32 = a.Z32 + o;
   const bool keep_v = !a.f32 || (a.ext && !a.fuse_ext);    // fp64 v feeds a GEMM only then
+  const bool f32 = a.f32, fuse = a.fuse_ext;
+  const int64_t n = a.n;
+  const double beta = a.beta, sc = a.s;
+#pragma unroll 4
   for (int64_t k = threadIdx.x; k < a.N; k += BT) {
-    const double xb = x[k] / a.beta;
+    const double xb = x[k] / beta;
     // U = A^T y of the current y: fp32 storage reads the GEMM output (+ s y for [A, sI])
-    const double uk = !a.f32 ? u[k] : (k < a.n ? (double)u32[k] : a.s * ycur[k - a.n]);
+    const double uk = !f32 ? u[k] : (k < n ? (double)u32[k] : sc * ycur[k - n]);
     const double t = uk + xb;
     const double z = t > 1.0 ? 1.0 : (t < -1.0 ? -1.0 : t);
-    a.Z[o + k] = z;
-    const double vv = k < a.n ? z - xb : a.s * (z - xb);
-    if (keep_v) a.V[o + k] = vv;
-    if (a.f32 && (k < a.n || a.fuse_ext)) a.V32[o + k] = (float)vv;
-    if (a.f32 && k < a.n) a.Z32[o + k] = (float)z;
+    zo[k] = z;
+    const double vv = k < n ? z - xb : sc * (z - xb);
+    if (keep_v) vo[k] = vv;
+    if (f32 && (k < n || fuse)) v32[k] = (float)vv;
+    if (f32 && k < n) z32[k] = (float)z;
   }
 }
 
@@ -126,22 +134,37 @@ __global__ void __launch_bounds__(BT) bd_y(const BDArgs a) {
   DI& I = a.inst[j];
   if (!I.active) return;
   const int64_t oj = (int64_t)j * a.ld;
-  const double* b = a.Bm + oj;
-  double* y = a.Y[a.iy ^ 1] + oj;
-  const double* zx = a.Z + (int64_t)j * a.ldx + a.n;
+  // restrict-qualified views: the four row loads of a thread are independent of
+  // its stores, so the unrolled loop keeps them all in flight
+  const double* __restrict__ b = a.Bm + oj;
+  double* __restrict__ y = a.Y[a.iy ^ 1] + oj;
+  const double* __restrict__ zx = a.Z + (int64_t)j * a.ldx + a.n;
+  const double* __restrict__ c0 = a.C0 + oj;
+  const double* __restrict__ ax = a.AX + oj;
+  const double* __restrict__ gx = a.GEXT + oj;
+  const float* __restrict__ p1f = a.P1f + oj;
+  const float* __restrict__ p2f = a.P2f + oj;
+  const double* __restrict__ p1 = a.P1 + oj;
+  const double* __restrict__ p2 = a.P2 + oj;
+  float* __restrict__ y32 = a.Y32 + oj;
+  double* __restrict__ rh = a.RHS + oj;
+  const bool f32 = a.f32, addg = a.ext && !a.fuse_ext, ext = a.ext;
+  const double beta = a.beta, sc = a.s;
   double q[2] = {0.0, 0.0};
+#pragma unroll 4
   for (int64_t i = threadIdx.x; i < a.d; i += BT) {
-    double mv = bd_rd(a, a.P1, a.P1f, oj + i);
-    if (a.ext && !a.fuse_ext) mv = mv + a.GEXT[oj + i];
-    const double yi = mv + a.C0[oj + i] / a.beta;
-    double az = bd_rd(a, a.P2, a.P2f, oj + i);
-    if (a.ext) az = az + a.s * zx[i];
-    const double rhs = az - (a.AX[oj + i] - b[i]) / a.beta;
+    double mv = f32 ? (double)p1f[i] : p1[i];
+    if (addg) mv = mv + gx[i];
+    const double yi = mv + c0[i] / beta;
+    double az = f32 ? (double)p2f[i] : p2[i];
+    if (ext) az = az + sc * zx[i];
+    const double bi = b[i];
+    const double rhs = az - (ax[i] - bi) / beta;
     y[i] = yi;
-    if (a.f32) a.Y32[oj + i] = (float)yi;
-    a.RHS[oj + i] = rhs;
+    if (f32) y32[i] = (float)yi;
+    rh[i] = rhs;
     q[0] += rhs * rhs;
-    q[1] += b[i] * yi;
+    q[1] += bi * yi;
   }
   cta_reduce<2>(q, 0u, sh);
   if (threadIdx.x == 0) { I.rhs2 = q[0]; I.by = q[1]; }
@@ -154,23 +177,33 @@ __global__ void __launch_bounds__(BT) bd_x(const BDArgs a, const double* Ut, con
   DI& I = a.inst[j];
   if (!I.active || (refine_only && !I.refine)) return;
   const int64_t o = (int64_t)j * a.ldx;
-  const double* x = a.X[a.ix] + o;
-  double* u = a.UX + o;                                   // [A^T y | x_new] block j
-  double* xn = a.UX + ((int64_t)gridDim.x + j) * a.ldx;   // second half of UX
-  const double* y = a.Y[a.iy ^ 1] + (int64_t)j * a.ld;
+  const double* __restrict__ x = a.X[a.ix] + o;
+  double* __restrict__ u = a.UX + o;                                   // [A^T y | x_new] block j
+  double* __restrict__ xn = a.UX + ((int64_t)gridDim.x + j) * a.ldx;   // second half of UX
+  const double* __restrict__ y = a.Y[a.iy ^ 1] + (int64_t)j * a.ld;
+  const double* __restrict__ zz = a.Z + o;
+  double* __restrict__ xw = a.X[a.ix ^ 1] + o;
+  float* __restrict__ ux32 = a.UX32 + o;
+  float* __restrict__ xn32 = a.UX32 + ((int64_t)gridDim.x + j) * a.ldx;
+  const double* __restrict__ ut = Ut + (int64_t)j * a.n;
+  const float* __restrict__ ut32 = Ut32 + (int64_t)j * a.n;
   const bool relest = a.C.stop_kind == ELL1_STOP_REL_ESTIMATE;
+  const bool f32 = a.f32;
+  const int64_t n = a.n;
+  const double beta = a.beta, sc = a.s;
   double s[6] = {0, 0, 0, 0, 0, 0};                       // l1, max|Aty|, max|x|, dx2, xp2, -
+#pragma unroll 4
   for (int64_t k = threadIdx.x; k < a.N; k += BT) {
     double uk;
-    if (k < a.n) uk = a.f32 ? (double)Ut32[(int64_t)j * a.n + k] : Ut[(int64_t)j * a.n + k];
-    else uk = a.s * y[k - a.n];                           // robust.py:96
+    if (k < n) uk = f32 ? (double)ut32[k] : ut[k];
+    else uk = sc * y[k - n];                              // robust.py:96
     const double xo = x[k];
-    const double xv = xo - a.beta * (a.Z[o + k] - uk);
-    if (!a.f32) { u[k] = uk; xn[k] = xv; }                // fp64 GEMM operand [U | x_new]
-    a.X[a.ix ^ 1][o + k] = xv;
-    if (a.f32 && k < a.n) {
-      a.UX32[o + k] = (float)uk;
-      a.UX32[((int64_t)gridDim.x + j) * a.ldx + k] = (float)xv;
+    const double xv = xo - beta * (zz[k] - uk);
+    if (!f32) { u[k] = uk; xn[k] = xv; }                  // fp64 GEMM operand [U | x_new]
+    xw[k] = xv;
+    if (f32 && k < n) {
+      ux32[k] = (float)uk;
+      xn32[k] = (float)xv;
     }
     s[0] += fabs(xv);
     s[1] = nmax(s[1], fabs(uk));
@@ -198,18 +231,36 @@ __global__ void __launch_bounds__(BT) bd_c(const BDArgs a, int refine_only) {
   const double* ynew = a.Y[a.iy ^ 1] + oj;
   const double cut = 1e-10 * pymax(I.S[2], 1.0);
   double q[3] = {0.0, 0.0, 0.0};
-  for (int64_t i = threadIdx.x; i < a.d; i += BT) {
-    double aau = bd_rd(a, a.P2, a.P2f, ((int64_t)j) * a.ld + i);
-    double ax = bd_rd(a, a.P2, a.P2f, ((int64_t)B + j) * a.ld + i);
-    if (a.ext) { aau = aau + a.s * (a.f32 ? a.s * ynew[i] : u[a.n + i]); ax = ax + a.s * xn[a.n + i]; }
-    const double resid = a.RHS[oj + i] - aau;
-    a.RES[oj + i] = resid;
-    a.AX[oj + i] = ax;
-    const double r = b[i] - ax;
-    q[0] += resid * resid;
-    q[1] += r * r;
+  {
+    const float* __restrict__ pu = a.P2f + (int64_t)j * a.ld;
+    const float* __restrict__ px = a.P2f + ((int64_t)B + j) * a.ld;
+    const double* __restrict__ pu64 = a.P2 + (int64_t)j * a.ld;
+    const double* __restrict__ px64 = a.P2 + ((int64_t)B + j) * a.ld;
+    const double* __restrict__ rh = a.RHS + oj;
+    const double* __restrict__ bb = b;
+    const double* __restrict__ yn = ynew;
+    const double* __restrict__ ue = u + a.n;
+    const double* __restrict__ xe = xn + a.n;
+    double* __restrict__ res = a.RES + oj;
+    double* __restrict__ axo = a.AX + oj;
+    const bool f32 = a.f32, ext = a.ext;
+    const double sc = a.s;
+#pragma unroll 4
+    for (int64_t i = threadIdx.x; i < a.d; i += BT) {
+      double aau = f32 ? (double)pu[i] : pu64[i];
+      double ax = f32 ? (double)px[i] : px64[i];
+      if (ext) { aau = aau + sc * (f32 ? sc * yn[i] : ue[i]); ax = ax + sc * xe[i]; }
+      const double resid = rh[i] - aau;
+      res[i] = resid;
+      axo[i] = ax;
+      const double r = bb[i] - ax;
+      q[0] += resid * resid;
+      q[1] += r * r;
+    }
+    const double* __restrict__ xs = xn;
+#pragma unroll 4
+    for (int64_t k = threadIdx.x; k < a.N; k += BT) if (fabs(xs[k]) > cut) q[2] += 1.0;
   }
-  for (int64_t k = threadIdx.x; k < a.N; k += BT) if (fabs(xn[k]) > cut) q[2] += 1.0;
   cta_reduce<3>(q, 0u, sh);
   if (threadIdx.x == 0) {
     int done = 0;
