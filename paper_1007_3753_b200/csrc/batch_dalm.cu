@@ -11,6 +11,7 @@
 //   GEMM      : A [A^T y | x_new]   (one GEMM over 2B columns)
 //   c-kernel  : certificate, residual, gap, trace, stopping rules
 //   [refinement for instances failing the certificate: Ginv resid GEMM]
+#include <cstdio>
 #include "batched.cuh"
 
 namespace ell1 {
@@ -349,6 +350,47 @@ __global__ void bd_mext_split(const float* __restrict__ M, const double* __restr
   }
 }
 
+// delta[:, j] = Ginv resid[:, j] for the instances flagged for refinement
+// (graph driver: cuBLAS may record nodes a conditional body cannot hold).
+// grid (row blocks of 256, instances); Ginv column-major ld x d (symmetric)
+__global__ void __launch_bounds__(256) bd_refine_gemv(const BDArgs a, const double* __restrict__ Ginv,
+                                                      double* __restrict__ delta) {
+  const int j = blockIdx.y;
+  const DI& I = a.inst[j];
+  if (!I.active || !I.refine) return;
+  __shared__ double r[1024];
+  const double* __restrict__ res = a.RES + (int64_t)j * a.ld;
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  double acc = 0.0;
+  for (int64_t k0 = 0; k0 < a.d; k0 += 1024) {
+    const int64_t kn = a.d - k0 < 1024 ? a.d - k0 : 1024;
+    __syncthreads();
+    for (int64_t t = threadIdx.x; t < kn; t += 256) r[t] = res[k0 + t];
+    __syncthreads();
+    if (i < a.ld) {
+#pragma unroll 8
+      for (int64_t k = 0; k < kn; ++k) acc = fma(Ginv[(k0 + k) * a.ld + i], r[k], acc);
+    }
+  }
+  if (i < a.ld) delta[(int64_t)j * a.ld + i] = acc;
+}
+
+// graph driver: IF condition = refinement flagged by this certificate round
+__global__ void bd_if(const int* ctr, cudaGraphConditionalHandle h) {
+  if (threadIdx.x == 0) cudaGraphSetConditional(h, ctr[0] > 0 ? 1u : 0u);
+}
+
+// graph driver: keep iterating while no compaction is due (same rule as the
+// host loop) and the pass budget of one launch lasts; ctr[4] counts passes
+__global__ void bd_loop(int* ctr, cudaGraphConditionalHandle h, int Bcur) {
+  if (threadIdx.x == 0) {
+    const int nact = ctr[1];
+    const int passes = ++ctr[4];
+    const bool compact = nact < Bcur * 3 / 4 || (nact < Bcur && nact <= 64);
+    cudaGraphSetConditional(h, (nact > 0 && !compact && passes < 4096) ? 1u : 0u);
+  }
+}
+
 __global__ void bd_scan(DI* inst, int B, int* perm, int* newB) {
   __shared__ int base;
   __shared__ int wsum[32];
@@ -490,6 +532,136 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   hc[0] = hc[1] = 0;
   if (cudaMemcpyAsync(hc, ctr, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
   if (cudaStreamSynchronize(s) != cudaSuccess) return ELL1_ERR_CUDA;
+
+  cudaStream_t ks = s;                                   // launch stream (a capture stream while recording)
+  // U = A^T y_new (n x B), x_new, A [U | x_new], certificate (refine_only: flagged instances)
+  auto tail_part = [&](const BDArgs& aa, int Bc, int refine_only) -> bool {
+    void* Ut = aa.f32 ? (void*)T32 : (void*)scratch;
+    if (!gemm_AtR(h, D, aa.f32 ? (const void*)aa.Y32 : (const void*)aa.Y[aa.iy ^ 1], ld, Ut, D->n, Bc, pA))
+      return false;
+    // [U | x_new] for the Bc instances: the x_new block starts at column Bc
+    bd_x<<<Bc, BT, 0, ks>>>(aa, (const double*)Ut, (const float*)Ut, refine_only);
+    if (aa.f32) {
+      if (!gemm_AX(h, D, aa.UX32, ldx, aa.P2f, ld, 2 * Bc, pA)) return false;
+    } else {
+      if (!gemm_AX(h, D, aa.UX, ldx, aa.P2, ld, 2 * Bc)) return false;
+    }
+    if (cudaMemsetAsync(ctr, 0, 4, ks) != cudaSuccess) return false;
+    bd_c<<<Bc, BT, 0, ks>>>(aa, refine_only);
+    return cudaGetLastError() == cudaSuccess;
+  };
+  // one iteration up to the certificate (bd_c raises ctr[0] refine flags)
+  auto main_part = [&](const BDArgs& aa, int Bc) -> bool {
+    bd_z<<<Bc, BT, 0, ks>>>(aa);
+    const void* Vop = aa.f32 ? (const void*)aa.V32 : (const void*)aa.V;
+    const void* Zop = aa.f32 ? (const void*)aa.Z32 : (const void*)aa.Z;
+    if (aa.fuse_ext) {
+      // P1 = [M | Ginv] V over K = n + d (V's identity block already carries s)
+      if (!sgemm_split(h, CUBLAS_OP_N, (int)ld, Bc, (int)N, nullptr, 0, &spX, aa.V32, ldx, aa.P1f, ld, N))
+        return false;
+    } else if (!gemm_AX(h, &MD, Vop, ldx, aa.f32 ? (void*)aa.P1f : (void*)aa.P1, ld, Bc, pM)) {
+      return false;
+    }
+    if (!gemm_AX(h, D, Zop, ldx, aa.f32 ? (void*)aa.P2f : (void*)aa.P2, ld, Bc, pA)) return false;
+    if (aa.ext && !aa.fuse_ext) {
+      // identity block of M: s Ginv v_ext (s folded into v_ext by bd_z)
+      if (cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)ld, Bc, (int)d, &one, O->Ginv, (int)ld,
+                      aa.V + D->n, (int)ldx, &zero, aa.GEXT, (int)ld) != CUBLAS_STATUS_SUCCESS)
+        return false;
+    }
+    bd_y<<<Bc, BT, 0, ks>>>(aa);
+    return tail_part(aa, Bc, 0);
+  };
+  // y += Ginv resid for the flagged instances (alm.py:184), then their certificate again
+  auto refine_part = [&](const BDArgs& aa, int Bc, bool own_gemv) -> bool {
+    if (own_gemv) {
+      bd_refine_gemv<<<dim3((unsigned)((ld + 255) / 256), (unsigned)Bc), 256, 0, ks>>>(aa, O->Ginv, aa.GEXT);
+    } else if (cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)ld, Bc, (int)d, &one, O->Ginv, (int)ld, aa.RES,
+                           (int)ld, &zero, aa.GEXT, (int)ld) != CUBLAS_STATUS_SUCCESS) {
+      return false;
+    }
+    bd_refine<<<Bc, BT, 0, ks>>>(aa, aa.GEXT);
+    return tail_part(aa, Bc, 1);
+  };
+
+  // CUDA-graph driver (fp32 storage on the tensor-core GEMM path): two
+  // iterations (both buffer parities) per WHILE-body pass, each followed by
+  // an IF node running the refinement when bd_c raised a flag; the WHILE
+  // condition (bd_loop) drops when compaction is due or everything finished.
+  bool use_graph = a.f32 && fp32_mode_select() == 3;
+  if (const char* e = getenv("ELL1_BATCH_GRAPH")) use_graph = use_graph && e[0] != '0';
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  int gB = -1, gpar = -1, gfail = 0;
+  auto build_graph = [&]() -> bool {
+    gfail = 0;
+#define GSTEP(expr)          \
+  do {                       \
+    ++gfail;                 \
+    if (!(expr)) return false; \
+  } while (0)
+    GSTEP(cudaGraphCreate(&graph, 0) == cudaSuccess);
+    cudaGraphConditionalHandle hloop, hif[2];
+    GSTEP(cudaGraphConditionalHandleCreate(&hloop, graph, 1, cudaGraphCondAssignDefault) == cudaSuccess);
+    for (int q = 0; q < 2; ++q)
+      GSTEP(cudaGraphConditionalHandleCreate(&hif[q], graph, 0, cudaGraphCondAssignDefault) == cudaSuccess);
+    cudaGraphNodeParams wp = {};
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = hloop;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    GSTEP(cudaGraphAddNode(&wnode, graph, nullptr, 0, &wp) == cudaSuccess);
+    cudaGraph_t body = wp.conditional.phGraph_out[0];
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    cudaGraphNode_t last = nullptr;
+    BDArgs aa = a;
+    // record on a private stream (the caller's may be the legacy default
+    // stream, which cannot capture); the graph is launched on the caller's
+    cudaStream_t cs = nullptr;
+    GSTEP(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess);
+    struct Restore {
+      cudaStream_t& ks; cudaStream_t s; cublasHandle_t h; cudaStream_t cs;
+      ~Restore() { ks = s; cublasSetStream(h, s); cudaStreamDestroy(cs); }
+    } restore{ks, s, h, cs};
+    ks = cs;
+    cublasSetStream(h, cs);
+    for (int q = 0; q < 2; ++q) {
+      aa.ix = aa.iy = a.ix ^ q;
+      GSTEP(cudaStreamBeginCaptureToGraph(cs, body, last ? &last : nullptr, nullptr, last ? 1 : 0,
+                                          cudaStreamCaptureModeRelaxed) == cudaSuccess);
+      bool ok = main_part(aa, Bcur);
+      if (ok) bd_if<<<1, 32, 0, cs>>>(ctr, hif[q]);
+      cudaStreamCaptureStatus cst;
+      ok = ok && cudaStreamGetCaptureInfo(cs, &cst, nullptr, nullptr, &deps, &ndeps) == cudaSuccess && ndeps == 1;
+      cudaGraphNode_t tailn = ok ? deps[0] : nullptr;
+      cudaGraph_t tmp;
+      GSTEP(cudaStreamEndCapture(cs, &tmp) == cudaSuccess);
+      GSTEP(ok);
+      cudaGraphNodeParams ip = {};
+      ip.type = cudaGraphNodeTypeConditional;
+      ip.conditional.handle = hif[q];
+      ip.conditional.type = cudaGraphCondTypeIf;
+      ip.conditional.size = 1;
+      cudaGraphNode_t inode;
+      GSTEP(cudaGraphAddNode(&inode, body, &tailn, 1, &ip) == cudaSuccess);
+      GSTEP(cudaStreamBeginCaptureToGraph(cs, ip.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeRelaxed) == cudaSuccess);
+      ok = refine_part(aa, Bcur, true);
+      GSTEP(cudaStreamEndCapture(cs, &tmp) == cudaSuccess);
+      GSTEP(ok);
+      last = inode;
+    }
+    GSTEP(cudaStreamBeginCaptureToGraph(cs, body, &last, nullptr, 1, cudaStreamCaptureModeRelaxed) == cudaSuccess);
+    bd_loop<<<1, 32, 0, cs>>>(ctr, hloop, Bcur);
+    cudaGraph_t tmp;
+    GSTEP(cudaStreamEndCapture(cs, &tmp) == cudaSuccess);
+    ++gfail;
+    return cudaGraphInstantiate(&gexec, graph, 0) == cudaSuccess;
+#undef GSTEP
+  };
+
   while (true) {
     const int nact = hc[1];
     if (nact <= 0) break;
@@ -519,55 +691,46 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
       }
       Bcur = nact;
     }
-    // ---- one DALM iteration over Bcur instances
-    bd_z<<<Bcur, BT, 0, s>>>(a);
-    {
-      const void* Vop = a.f32 ? (const void*)a.V32 : (const void*)a.V;
-      const void* Zop = a.f32 ? (const void*)a.Z32 : (const void*)a.Z;
-      if (a.fuse_ext) {
-        // P1 = [M | Ginv] V over K = n + d (V's identity block already carries s)
-        if (!sgemm_split(h, CUBLAS_OP_N, (int)ld, Bcur, (int)N, nullptr, 0, &spX, a.V32, ldx, a.P1f, ld, N))
-          return ELL1_ERR_CUDA;
-      } else if (!gemm_AX(h, &MD, Vop, ldx, a.f32 ? (void*)a.P1f : (void*)a.P1, ld, Bcur, pM)) {
-        return ELL1_ERR_CUDA;
+    // ---- DALM iterations over Bcur instances
+    if (use_graph && Bcur >= 32) {
+      // device-driven: whole iterations (and the rare certificate refinement)
+      // inside one CUDA graph whose WHILE node runs until an instance
+      // finishes often enough to warrant compaction
+      if (!gexec || gB != Bcur || gpar != a.ix) {
+        if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
+        if (graph) { cudaGraphDestroy(graph); graph = nullptr; }
+        if (!build_graph()) {
+          if (getenv("ELL1_DEBUG"))
+            fprintf(stderr, "ell1_batch_dalm: graph build (B=%d) failed at step %d (%s)\n", Bcur, gfail,
+                    cudaGetErrorString(cudaGetLastError()));
+          use_graph = false;                                 // fall back to host-driven iterations
+          if (graph) { cudaGraphDestroy(graph); graph = nullptr; }
+          cudaGetLastError();
+          continue;
+        }
+        gB = Bcur;
+        gpar = a.ix;
       }
-      if (!gemm_AX(h, D, Zop, ldx, a.f32 ? (void*)a.P2f : (void*)a.P2, ld, Bcur, pA)) return ELL1_ERR_CUDA;
-      if (a.ext && !a.fuse_ext) {
-        // identity block of M: s Ginv v_ext (s folded into v_ext by bd_z)
-        if (cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)ld, Bcur, (int)d, &one, O->Ginv, (int)ld,
-                        a.V + D->n, (int)ldx, &zero, a.GEXT, (int)ld) != CUBLAS_STATUS_SUCCESS)
-          return ELL1_ERR_CUDA;
-      }
-    }
-    bd_y<<<Bcur, BT, 0, s>>>(a);
-    int refine_only = 0;
-    while (true) {
-      // U = A^T y_new (n x B), then x_new, then A [U | x_new]
-      void* Ut = a.f32 ? (void*)T32 : (void*)scratch;
-      if (!gemm_AtR(h, D, a.f32 ? (const void*)a.Y32 : (const void*)a.Y[a.iy ^ 1], ld, Ut, D->n, Bcur, pA))
-        return ELL1_ERR_CUDA;
-      // UX holds [U | x_new] for the Bcur instances: x_new block starts at column Bcur
-      bd_x<<<Bcur, BT, 0, s>>>(a, (const double*)Ut, (const float*)Ut, refine_only);
-      if (a.f32) {
-        // UX32 layout: [U | x_new] with Bcur columns each
-        if (!gemm_AX(h, D, a.UX32, ldx, a.P2f, ld, 2 * Bcur, pA)) return ELL1_ERR_CUDA;
-      } else {
-        if (!gemm_AX(h, D, a.UX, ldx, a.P2, ld, 2 * Bcur)) return ELL1_ERR_CUDA;
-      }
-      if (cudaMemsetAsync(ctr, 0, 4, s) != cudaSuccess) return ELL1_ERR_CUDA;
-      bd_c<<<Bcur, BT, 0, s>>>(a, refine_only);
+      if (cudaMemsetAsync(ctr + 4, 0, 4, s) != cudaSuccess) return ELL1_ERR_CUDA;
+      if (cudaGraphLaunch(gexec, s) != cudaSuccess) return ELL1_ERR_CUDA;
       if (cudaMemcpyAsync(hc, ctr, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
       if (cudaStreamSynchronize(s) != cudaSuccess) return ELL1_ERR_CUDA;
-      if (hc[0] == 0) break;
-      // y += Ginv resid for the flagged instances (alm.py:184)
-      if (cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)ld, Bcur, (int)d, &one, O->Ginv, (int)ld, a.RES,
-                      (int)ld, &zero, a.GEXT, (int)ld) != CUBLAS_STATUS_SUCCESS)
-        return ELL1_ERR_CUDA;
-      bd_refine<<<Bcur, BT, 0, s>>>(a, a.GEXT);
-      refine_only = 1;
+      continue;                                              // parity unchanged (even iteration count)
+    }
+    if (!main_part(a, Bcur)) return ELL1_ERR_CUDA;
+    if (cudaMemcpyAsync(hc, ctr, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return ELL1_ERR_CUDA;
+    if (hc[0] != 0) {
+      // one refinement round; instances failing it again end ill-conditioned
+      // inside bd_c, so no further refine flags can be raised
+      if (!refine_part(a, Bcur, false)) return ELL1_ERR_CUDA;
+      if (cudaMemcpyAsync(hc, ctr, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
+      if (cudaStreamSynchronize(s) != cudaSuccess) return ELL1_ERR_CUDA;
     }
     a.ix ^= 1;
     a.iy ^= 1;
   }
+  if (gexec) cudaGraphExecDestroy(gexec);
+  if (graph) cudaGraphDestroy(graph);
   return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
 }
