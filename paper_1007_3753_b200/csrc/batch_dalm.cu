@@ -584,7 +584,8 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
     return tail_part(aa, Bc, 1);
   };
 
-  // CUDA-graph driver (fp32 storage on the tensor-core GEMM path): two
+  // CUDA-graph driver (fp32 storage on the tensor-core GEMM path; the fp64
+  // path's cuBLAS DGEMMs record nodes a conditional body cannot hold): two
   // iterations (both buffer parities) per WHILE-body pass, each followed by
   // an IF node running the refinement when bd_c raised a flag; the WHILE
   // condition (bd_loop) drops when compaction is due or everything finished.
