@@ -594,6 +594,10 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
   int gB = -1, gpar = -1, gfail = 0;
+  bool use_plain = true;
+  if (const char* e = getenv("ELL1_BATCH_GRAPH")) use_plain = e[0] != '0';
+  cudaGraphExec_t pexec[2] = {nullptr, nullptr};
+  int pB = -1;
   auto build_graph = [&]() -> bool {
     gfail = 0;
 #define GSTEP(expr)          \
@@ -718,7 +722,42 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
       if (cudaStreamSynchronize(s) != cudaSuccess) return ELL1_ERR_CUDA;
       continue;                                              // parity unchanged (even iteration count)
     }
-    if (!main_part(a, Bcur)) return ELL1_ERR_CUDA;
+    // host-driven iteration; its launches are replayed from a per-(B, parity)
+    // graph when one could be recorded (one API call instead of ~10 library calls)
+    if (use_plain && (pB != Bcur)) {
+      for (int q = 0; q < 2; ++q)
+        if (pexec[q]) { cudaGraphExecDestroy(pexec[q]); pexec[q] = nullptr; }
+      pB = Bcur;
+    }
+    if (use_plain && !pexec[a.ix]) {
+      cudaStream_t cs = nullptr;
+      cudaGraph_t pg = nullptr;
+      bool ok = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess;
+      if (ok) {
+        ks = cs;
+        cublasSetStream(h, cs);
+        ok = cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+        if (ok) {
+          ok = main_part(a, Bcur);
+          ok = cudaStreamEndCapture(cs, &pg) == cudaSuccess && ok;
+        }
+        ks = s;
+        cublasSetStream(h, s);
+        cudaStreamDestroy(cs);
+      }
+      ok = ok && cudaGraphInstantiate(&pexec[a.ix], pg, 0) == cudaSuccess;
+      if (pg) cudaGraphDestroy(pg);
+      if (!ok) {
+        pexec[a.ix] = nullptr;
+        use_plain = false;
+        cudaGetLastError();
+      }
+    }
+    if (use_plain && pexec[a.ix]) {
+      if (cudaGraphLaunch(pexec[a.ix], s) != cudaSuccess) return ELL1_ERR_CUDA;
+    } else if (!main_part(a, Bcur)) {
+      return ELL1_ERR_CUDA;
+    }
     if (cudaMemcpyAsync(hc, ctr, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
     if (cudaStreamSynchronize(s) != cudaSuccess) return ELL1_ERR_CUDA;
     if (hc[0] != 0) {
@@ -733,5 +772,7 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   }
   if (gexec) cudaGraphExecDestroy(gexec);
   if (graph) cudaGraphDestroy(graph);
+  for (int q = 0; q < 2; ++q)
+    if (pexec[q]) cudaGraphExecDestroy(pexec[q]);
   return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
 }
