@@ -404,57 +404,102 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
   int Bcur = B;
   int* h_ctr = host_mailbox();
   h_ctr[0] = h_ctr[1] = 0;
-  constexpr int SYNC_EVERY = 8;          // rounds between reads of the active count
-  for (int64_t round = 0;; ++round) {
-    if (round % SYNC_EVERY == 0) {
-      if (cudaMemcpyAsync(h_ctr, ctr, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
-      if (cudaStreamSynchronize(s) != cudaSuccess) return ELL1_ERR_CUDA;
-      const int nact = h_ctr[1];
-      if (nact <= 0) break;
-      if (nact < Bcur * 3 / 4 || (nact < Bcur && nact <= 64)) {
-        // compact the active instances to the front of every state matrix
-        bf_scan<<<1, 1024, 0, s>>>(a.inst, Bcur, perm, ctr + 2);
-        auto perm_mat = [&](double* M, int64_t rows, int64_t ldm) {
-          dim3 g((unsigned)((rows + 255) / 256 < 64 ? (rows + 255) / 256 : 64), (unsigned)nact);
-          gather_cols<double><<<g, 256, 0, s>>>(M, scratch, rows, ldm, perm, nact);
-          cudaMemcpyAsync(M, scratch, ldm * nact * 8, cudaMemcpyDeviceToDevice, s);
-        };
-        for (int k = 0; k < 3; ++k) perm_mat(a.X[k], N, ldx);
-        for (int k = 0; k < 2; ++k) perm_mat(a.G[k], N, ldx);
-        perm_mat(a.Y, N, ldx);
-        perm_mat(a.GY, N, ldx);
-        for (int k = 0; k < 3; ++k) perm_mat(a.R[k], ld, ld);
-        perm_mat(Bm, ld, ld);
-        if (a.f32) {                  // g_next of the last round (fp32 GEMM output) is still pending
-          float* fs = reinterpret_cast<float*>(scratch);
-          dim3 g((unsigned)((D->n + 255) / 256 < 64 ? (D->n + 255) / 256 : 64), (unsigned)nact);
-          gather_cols<float><<<g, 256, 0, s>>>(a.G32, fs, D->n, D->n, perm, nact);
-          cudaMemcpyAsync(a.G32, fs, D->n * nact * 4, cudaMemcpyDeviceToDevice, s);
+  // rounds between reads of the active count: a multiple of 6 (the period of
+  // the x / r / g ring rotations), so R rounds leave the ring indices as they
+  // were and one recorded graph per batch size replays them
+  constexpr int R = 12;
+  cudaStream_t ks = s;
+  auto one_round = [&](BFArgs& aa) -> bool {
+    // ---- finish last round's accepted iterations, then one backtracking trial each
+    bf_step<<<Bcur, BT, 0, ks>>>(aa);
+    if (!gemm_AX(h, D, aa.f32 ? (const void*)aa.X32 : (const void*)aa.X[aa.ixn], ldx,
+                 aa.f32 ? (void*)aa.AX32 : (void*)aa.AX, ld, Bcur, spp))
+      return false;
+    bf_resid<<<Bcur, BT, 0, ks>>>(aa);
+    // g_next = A^T r_next into the g ring's free slot (speculative for retries)
+    if (!gemm_AtR(h, D, aa.f32 ? (const void*)aa.R32 : (const void*)aa.R[aa.irn], ld,
+                  aa.f32 ? (void*)aa.G32 : (void*)aa.G[aa.igxp], aa.f32 ? D->n : ldx, Bcur, spp))
+      return false;
+    // rotate the rings (shrinkage.py:283-284); bf_step undoes it for retrying instances
+    { int t = aa.ixp; aa.ixp = aa.ix; aa.ix = aa.ixn; aa.ixn = t; }
+    { int t = aa.irxp; aa.irxp = aa.irx; aa.irx = aa.irn; aa.irn = t; }
+    { int t = aa.igxp; aa.igxp = aa.igx; aa.igx = t; }
+    return cudaGetLastError() == cudaSuccess;
+  };
+  bool use_graph = true;
+  if (const char* e = getenv("ELL1_BATCH_GRAPH")) use_graph = e[0] != '0';
+  cudaGraphExec_t gexec = nullptr;
+  int gB = -1;
+  for (;;) {
+    if (cudaMemcpyAsync(h_ctr, ctr, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return ELL1_ERR_CUDA;
+    const int nact = h_ctr[1];
+    if (nact <= 0) break;
+    if (nact < Bcur * 3 / 4 || (nact < Bcur && nact <= 64)) {
+      // compact the active instances to the front of every state matrix
+      bf_scan<<<1, 1024, 0, s>>>(a.inst, Bcur, perm, ctr + 2);
+      auto perm_mat = [&](double* M, int64_t rows, int64_t ldm) {
+        dim3 g((unsigned)((rows + 255) / 256 < 64 ? (rows + 255) / 256 : 64), (unsigned)nact);
+        gather_cols<double><<<g, 256, 0, s>>>(M, scratch, rows, ldm, perm, nact);
+        cudaMemcpyAsync(M, scratch, ldm * nact * 8, cudaMemcpyDeviceToDevice, s);
+      };
+      for (int k = 0; k < 3; ++k) perm_mat(a.X[k], N, ldx);
+      for (int k = 0; k < 2; ++k) perm_mat(a.G[k], N, ldx);
+      perm_mat(a.Y, N, ldx);
+      perm_mat(a.GY, N, ldx);
+      for (int k = 0; k < 3; ++k) perm_mat(a.R[k], ld, ld);
+      perm_mat(Bm, ld, ld);
+      if (a.f32) {                  // g_next of the last round (fp32 GEMM output) is still pending
+        float* fs = reinterpret_cast<float*>(scratch);
+        dim3 g((unsigned)((D->n + 255) / 256 < 64 ? (D->n + 255) / 256 : 64), (unsigned)nact);
+        gather_cols<float><<<g, 256, 0, s>>>(a.G32, fs, D->n, D->n, perm, nact);
+        cudaMemcpyAsync(a.G32, fs, D->n * nact * 4, cudaMemcpyDeviceToDevice, s);
+      }
+      {
+        const int64_t words = (int64_t)sizeof(BI) / 4;
+        dim3 g(1, (unsigned)nact);
+        gather_cols<int><<<g, 64, 0, s>>>((const int*)a.inst, (int*)inst2, words, words, perm, nact);
+        cudaMemcpyAsync(a.inst, inst2, sizeof(BI) * nact, cudaMemcpyDeviceToDevice, s);
+      }
+      Bcur = nact;
+    }
+    if (use_graph && gB != Bcur) {
+      if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
+      cudaStream_t cs = nullptr;
+      cudaGraph_t g = nullptr;
+      bool ok = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess;
+      if (ok) {
+        ks = cs;
+        cublasSetStream(h, cs);
+        ok = cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+        if (ok) {
+          BFArgs aa = a;
+          for (int r = 0; r < R && ok; ++r) ok = one_round(aa);
+          ok = cudaStreamEndCapture(cs, &g) == cudaSuccess && ok;
         }
-        {
-          const int64_t words = (int64_t)sizeof(BI) / 4;
-          dim3 g(1, (unsigned)nact);
-          gather_cols<int><<<g, 64, 0, s>>>((const int*)a.inst, (int*)inst2, words, words, perm, nact);
-          cudaMemcpyAsync(a.inst, inst2, sizeof(BI) * nact, cudaMemcpyDeviceToDevice, s);
-        }
-        Bcur = nact;
+        ks = s;
+        cublasSetStream(h, s);
+        cudaStreamDestroy(cs);
+      }
+      ok = ok && cudaGraphInstantiate(&gexec, g, 0) == cudaSuccess;
+      if (g) cudaGraphDestroy(g);
+      if (ok) {
+        gB = Bcur;
+      } else {
+        gexec = nullptr;
+        use_graph = false;
+        cudaGetLastError();
       }
     }
-    // ---- finish last round's accepted iterations, then one backtracking trial each
-    bf_step<<<Bcur, BT, 0, s>>>(a);
-    if (!gemm_AX(h, D, a.f32 ? (const void*)a.X32 : (const void*)a.X[a.ixn], ldx,
-                 a.f32 ? (void*)a.AX32 : (void*)a.AX, ld, Bcur, spp))
-      return ELL1_ERR_CUDA;
-    bf_resid<<<Bcur, BT, 0, s>>>(a);
-    // g_next = A^T r_next into the g ring's free slot (speculative for retries)
-    if (!gemm_AtR(h, D, a.f32 ? (const void*)a.R32 : (const void*)a.R[a.irn], ld,
-                  a.f32 ? (void*)a.G32 : (void*)a.G[a.igxp], a.f32 ? D->n : ldx, Bcur, spp))
-      return ELL1_ERR_CUDA;
-    // rotate the rings (shrinkage.py:283-284); bf_step undoes it for retrying instances
-    { int t = a.ixp; a.ixp = a.ix; a.ix = a.ixn; a.ixn = t; }
-    { int t = a.irxp; a.irxp = a.irx; a.irx = a.irn; a.irn = t; }
-    { int t = a.igxp; a.igxp = a.igx; a.igx = t; }
+    if (use_graph) {
+      if (cudaGraphLaunch(gexec, s) != cudaSuccess) return ELL1_ERR_CUDA;
+    } else {
+      BFArgs aa = a;
+      for (int r = 0; r < R; ++r)
+        if (!one_round(aa)) return ELL1_ERR_CUDA;
+    }
   }
+  if (gexec) cudaGraphExecDestroy(gexec);
   return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
 }
 
