@@ -117,11 +117,11 @@ struct Smem {
 // SK = 2 splits K over a 2-CTA cluster (small GEMMs: bigger tiles, same CTA
 // count); rank 1 hands its fp32 sums to rank 0 through distributed shared
 // memory and rank 0 adds them in a fixed order (deterministic) and writes C.
-template <int BN, int ST, int KC, int SK>
+template <int BN, int ST, int KC, int SK, bool PRE>
 __global__ void __launch_bounds__(320, 1)
     tc3_gemm_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
-                    const __grid_constant__ CUtensorMap mB, int M, int N, int K, float* __restrict__ C,
-                    int64_t ldc) {
+                    const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mBl, int M, int N,
+                    int K, float* __restrict__ C, int64_t ldc) {
   using S = Smem<BN, ST>;
   static_assert(BN % 32 == 0 && BN <= 128, "BN");
   static_assert(SK == 1 || ST * S::STAGE >= BN * TM * 4, "partial exchange buffer");
@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(320, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&mAh) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&mAl) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&mB) : "memory");
+    if (PRE) asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&mBl) : "memory");
     for (int s = 0; s < ST; ++s) {
       mbar_init(full + s, 1);
       mbar_init(conv + s, 128);
@@ -181,10 +182,11 @@ __global__ void __launch_bounds__(320, 1)
         const int s = i % ST, u = i / ST, kc = (kb0 + i) * TK;
         if (u > 0) TW(0, true, mbar_wait(empty + s, (u - 1) & 1));
         uint8_t* st = smem + s * S::STAGE;
-        mbar_expect_tx(full + s, S::TX);
+        mbar_expect_tx(full + s, PRE ? S::STAGE : S::TX);
         tma_load_2d(st, &mAh, kc, m0, full + s);
         tma_load_2d(st + S::A_BYTES, &mAl, kc, m0, full + s);
         tma_load_2d(st + 2 * S::A_BYTES, &mB, kc, n0, full + s);
+        if (PRE) tma_load_2d(st + 2 * S::A_BYTES + S::B_BYTES, &mBl, kc, n0, full + s);
       }
     }
   } else if (warp == 1) {
@@ -195,7 +197,7 @@ __global__ void __launch_bounds__(320, 1)
         const int s = i % ST, u = i / ST, p = i / KC, buf = p & 1, ub = p >> 1;
         const bool first = i % KC == 0, last = i % KC == KC - 1 || i == nkb - 1;
         if (first && ub > 0) TW(1, true, mbar_wait(tempty + buf, (ub - 1) & 1));
-        TW(2, true, mbar_wait(conv + s, u & 1));
+        TW(2, true, mbar_wait((PRE ? full : conv) + s, u & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         uint8_t* st = smem + s * S::STAGE;
         const uint64_t ah = smem_desc(st), al = smem_desc(st + S::A_BYTES);
@@ -242,7 +244,7 @@ __global__ void __launch_bounds__(320, 1)
   } else {
     // ---- split warps (6..9): raw B tile -> hi in place, lo into the next tile
     const int et = threadIdx.x - 192;                        // 0..127
-    for (int i = 0; i < nkb; ++i) {
+    for (int i = 0; i < (PRE ? 0 : nkb); ++i) {
       const int s = i % ST, u = i / ST;
       TW(4, threadIdx.x == 192, mbar_wait(full + s, u & 1));
       const uint32_t bh = smem_u32(smem + s * S::STAGE + 2 * S::A_BYTES);
@@ -337,14 +339,16 @@ bool make_map(CUtensorMap* m, const float* p, int K, int rows, int64_t ld, int b
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, int ST, int SK, int KC>
-bool launch(int M, int N, int K, const float* ah, const float* al, int64_t lda, const float* b, int64_t ldb,
-            float* C, int64_t ldc, cudaStream_t s) {
-  CUtensorMap mAh, mAl, mB;
+template <int BN, int ST, int SK, int KC, bool PRE>
+bool launch(int M, int N, int K, const float* ah, const float* al, int64_t lda, const float* b, const float* bl,
+            int64_t ldb, float* C, int64_t ldc, cudaStream_t s) {
+  CUtensorMap mAh, mAl, mB, mBl;
   if (!make_map(&mAh, ah, K, M, lda, TM) || !make_map(&mAl, al, K, M, lda, TM) || !make_map(&mB, b, K, N, ldb, BN))
     return false;
+  if (PRE ? !make_map(&mBl, bl, K, N, ldb, BN) : false) return false;
+  if (!PRE) mBl = mB;
   constexpr int smem = Smem<BN, ST>::TOTAL;
-  auto kern = tc3_gemm_kernel<BN, ST, KC, SK>;
+  auto kern = tc3_gemm_kernel<BN, ST, KC, SK, PRE>;
   static unsigned attr = 0;                                  // per-device bit
   int dev = 0;
   cudaGetDevice(&dev);
@@ -364,12 +368,14 @@ bool launch(int M, int N, int K, const float* ah, const float* al, int64_t lda, 
   at[0].val.clusterDim.z = SK;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, mAh, mAl, mB, M, N, K, C, ldc) == cudaSuccess;
+  return cudaLaunchKernelEx(&cfg, kern, mAh, mAl, mB, mBl, M, N, K, C, ldc) == cudaSuccess;
 }
 
 // SMEM bytes moved per k-block (TMA fill + in-smem split + three MMA operand reads),
 // the resource that bounds these tiles
-constexpr double kb_cost(int bn) { return 80.0 * 1024 + 7.0 * bn * 128; }
+constexpr double kb_cost(int bn, bool pre = false) {
+  return pre ? 80.0 * 1024 + 5.0 * bn * 128 : 80.0 * 1024 + 7.0 * bn * 128;
+}
 
 }  // namespace
 
@@ -389,10 +395,11 @@ int tc3_available() {
 }
 
 bool tc3_gemm(int M, int N, int K, const float* a_hi, const float* a_lo, int64_t lda, const float* b, int64_t ldb,
-              float* C, int64_t ldc, cudaStream_t s) {
+              float* C, int64_t ldc, cudaStream_t s, const float* b_lo) {
   if (M <= 0 || N <= 0) return true;
   if (K <= 0 || tc3_available() != 1) return false;
-  if ((lda & 3) || (ldb & 3) || (((uintptr_t)a_hi | (uintptr_t)a_lo | (uintptr_t)b) & 15)) return false;
+  if ((lda & 3) || (ldb & 3) || (((uintptr_t)a_hi | (uintptr_t)a_lo | (uintptr_t)b | (uintptr_t)b_lo) & 15))
+    return false;
   // pick the tile (BN) and K split (SK) with the least per-SM smem traffic on
   // the critical path: waves x k-blocks per CTA x bytes per k-block (+ fixed costs)
   const int mt = (M + TM - 1) / TM, nkb = (K + TK - 1) / TK;
@@ -404,7 +411,7 @@ bool tc3_gemm(int M, int N, int K, const float* a_hi, const float* a_lo, int64_t
     const long ctas = (long)mt * ((N + o.bn - 1) / o.bn) * o.sk;
     const long waves = (ctas + 147) / 148;
     const double kbs = (double)((nkb + o.sk - 1) / o.sk);
-    const double t = waves * (kbs * kb_cost(o.bn) + 24.0 * 1024 + (o.sk == 2 ? 24.0 * 1024 : 0.0));
+    const double t = waves * (kbs * kb_cost(o.bn, b_lo != nullptr) + 24.0 * 1024 + (o.sk == 2 ? 24.0 * 1024 : 0.0));
     if (t < best) { best = t; pick = o; }
   }
   static int force = -1;
@@ -418,10 +425,11 @@ bool tc3_gemm(int M, int N, int K, const float* a_hi, const float* a_lo, int64_t
     kc = e && atoi(e) == 2 ? 2 : 1;
   }
   const int code = force ? force : pick.bn * 10 + pick.sk;
-#define TC3_CASE(BN_, ST_, SK_)                                                              \
-  case BN_ * 10 + SK_:                                                                       \
-    return kc == 2 ? launch<BN_, ST_, SK_, 2>(M, N, K, a_hi, a_lo, lda, b, ldb, C, ldc, s)   \
-                   : launch<BN_, ST_, SK_, 1>(M, N, K, a_hi, a_lo, lda, b, ldb, C, ldc, s);
+#define TC3_CASE(BN_, ST_, SK_)                                                                         \
+  case BN_ * 10 + SK_:                                                                                  \
+    if (b_lo) return launch<BN_, ST_, SK_, 1, true>(M, N, K, a_hi, a_lo, lda, b, b_lo, ldb, C, ldc, s); \
+    return kc == 2 ? launch<BN_, ST_, SK_, 2, false>(M, N, K, a_hi, a_lo, lda, b, b, ldb, C, ldc, s)    \
+                   : launch<BN_, ST_, SK_, 1, false>(M, N, K, a_hi, a_lo, lda, b, b, ldb, C, ldc, s);
   switch (code) {
     TC3_CASE(64, 4, 1)
     TC3_CASE(96, 3, 1)

@@ -30,8 +30,10 @@ namespace ell1 {
 //   the kernel splits each staged tile itself).
 // lda, ldb multiples of 4 floats, pointers 16-byte aligned.  Returns false if
 // the tensor-core path cannot take the call (the caller then uses SIMT SGEMM).
+// b_lo (optional): B already split by its producer — b holds rna_tf32(B) and
+// b_lo rna_tf32(B - b); both arrive by TMA and the in-kernel split is skipped.
 bool tc3_gemm(int M, int N, int K, const float* a_hi, const float* a_lo, int64_t lda, const float* b, int64_t ldb,
-              float* C, int64_t ldc, cudaStream_t s);
+              float* C, int64_t ldc, cudaStream_t s, const float* b_lo = nullptr);
 
 // 0 = not tried yet, 1 = available, -1 = unavailable (no driver entry point)
 int tc3_available();

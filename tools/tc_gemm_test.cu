@@ -85,6 +85,8 @@ int main(int argc, char** argv) {
     cudaDeviceSynchronize();
     std::vector<float> Cs((size_t)ldc * N);
     cudaMemcpy(Cs.data(), dC2, Cs.size() * 4, cudaMemcpyDeviceToHost);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
     double etc = 0, esimt = 0;
     const int samples = (M * (int64_t)N <= 200000) ? M * N : 4000;
     for (int t = 0; t < samples; ++t) {
@@ -100,8 +102,6 @@ int main(int argc, char** argv) {
       esimt = fmax(esimt, fabs(Cs[(size_t)j * ldc + i] - s) / sa);
     }
     // timings
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0); cudaEventCreate(&e1);
     const int reps = M >= 8192 ? 5 : 50;
     cudaEventRecord(e0);
     for (int r = 0; r < reps; ++r) ell1::tc3_gemm(M, N, K, dAh, dAl, lda, dB, ldb, dC, ldc, 0);
@@ -112,6 +112,20 @@ int main(int argc, char** argv) {
       cublasSgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, M, N, K, &one, dA, (int)lda, dB, (int)ldb, &zero, dC2, (int)ldc);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= reps;
+    // producer-split B (b = hi, b_lo = lo): must give the same bits as the in-kernel split
+    std::vector<float> Cp((size_t)ldc * N);
+    ell1::tc3_gemm(M, N, K, dAh, dAl, lda, dBh, ldb, dC2, ldc, 0, dBl);
+    cudaDeviceSynchronize();
+    cudaMemcpy(Cp.data(), dC2, Cp.size() * 4, cudaMemcpyDeviceToHost);
+    size_t ndiff = 0;
+    for (int j = 0; j < N; ++j)
+      for (int i = 0; i < M; ++i) ndiff += Cp[(size_t)j * ldc + i] != Cg[(size_t)j * ldc + i];
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) ell1::tc3_gemm(M, N, K, dAh, dAl, lda, dBh, ldb, dC2, ldc, 0, dBl);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float mp; cudaEventElapsedTime(&mp, e0, e1); mp /= reps;
+    printf("        pre-split B: %8.4f ms %6.1f TF/s, %zu entries differ from the in-kernel split\n", mp,
+           2.0 * M * N * K / mp / 1e9, ndiff);
     const bool pass = etc < 5e-7;
     bad += !pass;
     printf("%5dx%5dx%5d  tc3 %8.4f ms %6.1f TF/s err %.2e | simt %8.4f ms %6.1f TF/s err %.2e  %s\n", M, N, K, mt,
