@@ -578,6 +578,39 @@ def leg_cfg5_sweep(torch, dev, sizes=(1, 16, 256, 1024, 8192)):
     return {"workload": "cfg5 sweep: shared A 512 x 2048, k~U[16,256], lambda 1e-3", "rows": rows}
 
 
+def leg_align(torch, count=4096, d=1024, m=11, cpu_sample=24):
+    """PALM alignment (robust.py:470-515) batched across
+    images — `count` images of d pixels, m parameters, 20% grossly corrupted
+    rows — vs the numpy restatement (oracle.align_palm) on host cores."""
+    from paper_1007_3753_b200 import robust
+    from paper_1007_3753_b200.model import SolverConfig
+    from tests.golden.align_cases import align_instance
+    insts = [align_instance(seed=1000 + j, d=d, m=m, frac=0.2) for j in range(count)]
+    Bs = np.stack([B for B, _ in insts])
+    bs = np.stack([b for _, b in insts])
+    cfg = SolverConfig(tol=1e-8, max_iter=5000)
+    robust.align_palm_solve_batch(Bs[:64], bs[:64], cfg)       # warm-up
+    torch.cuda.synchronize()
+    s, e = _events(torch)
+    s.record()
+    W, E = robust.align_palm_solve_batch(Bs, bs, cfg)
+    e.record()
+    torch.cuda.synchronize()
+    t = s.elapsed_time(e) / 1e3
+    from oracle.l1_oracle import align_palm
+    t0 = time.perf_counter()
+    worst = 0.0
+    for j in range(cpu_sample):
+        w_ref, e_ref = align_palm(Bs[j], bs[j], tol=1e-8, max_iter=5000)
+        worst = max(worst, float(np.linalg.norm(W[j] - w_ref) / np.linalg.norm(w_ref)))
+    tc = time.perf_counter() - t0
+    return {"workload": "PALM alignment, %d images, d=%d pixels, m=%d parameters, 20%% corrupted rows, "
+                        "tol 1e-8 (public call: host images in, host w/e out)" % (count, d, m),
+            "images_per_sec": count / t, "ms_per_batch": 1e3 * t,
+            "cpu_port_images_per_sec": cpu_sample / tc, "cpu_sample": "%d images, 1 process" % cpu_sample,
+            "max_rel_err_w_vs_port": worst}
+
+
 def leg_harness(torch, n=200, grid=10, trials=10, cpu_sample=6):
     """the experiment harness on the GPU.  A phase grid
     (bench.run_phase_grid: rho x delta = grid x grid cells, `trials` fresh
@@ -731,6 +764,7 @@ def run_b200(args):
     torch.cuda.set_device(dev)
     if args.only_leg:
         legs = {"harness": lambda: leg_harness(torch), "cfg1": lambda: leg_cfg1(torch),
+                "align": lambda: leg_align(torch),
                 "cfg3": lambda: leg_cfg3(torch, dev), "cfg5": lambda: leg_cfg5(torch, dev, ws),
                 "cfg5_sweep": lambda: leg_cfg5_sweep(torch, dev),
                 "solvers_cfg2": lambda: leg_solvers_cfg2(torch, make_instance(rank))}
@@ -867,7 +901,8 @@ def run_b200(args):
             legs2 += [("solvers_cfg2", lambda: leg_solvers_cfg2(torch, P)),
                       ("cfg3", lambda: leg_cfg3(torch, dev)),
                       ("cfg5", lambda: leg_cfg5(torch, dev, ws)),
-                      ("harness", lambda: leg_harness(torch))]
+                      ("harness", lambda: leg_harness(torch)),
+                      ("align", lambda: leg_align(torch))]
             for name, fn in legs2:
                 try:
                     sec[name] = fn()

@@ -413,6 +413,32 @@ int ell1_pd_update(int64_t N2, int64_t d, double* x, const double* dx, double ap
 /* M[i][i] += alpha v[i] (v NULL: none), *trace = sum_i M[i][i]  (jitter, robust.py:148) */
 int ell1_pd_diag(int64_t d, int64_t ldm, double* M, double alpha, const double* v, double* trace, void* stream);
 
+/* Alignment solvers batched across images (robust.py:223-515).
+ * Image j: B_j (d x m, row-major with row pitch ldb >= m — numpy's layout —
+ * images b_stride apart), b_j (d, images ld_rhs apart); outputs w (count x m),
+ * e (count x d).
+ * d <= 2048, m <= 32, d > m.  status[j]: ELL1_OK or ELL1_NOT_PD (B_j lacks full
+ * column rank -> IllConditionedError, robust.py:254-258). */
+typedef struct {
+  int32_t count, d, m, max_iter;
+  const double* B;
+  int64_t ldb, b_stride;
+  const double* rhs;
+  int64_t ld_rhs;
+  double tol;
+  double mu0, rho;      /* PALM (robust.py:487-490) */
+  double lam;           /* IST: <= 0 -> 1e-2 * peak least-squares residual (robust.py:270-273) */
+  const double* v0;     /* IST: 4 normalised power-iteration start vectors (4 x m) */
+  double* w;
+  double* e;
+  int32_t* status;
+  int32_t* iterations;  /* optional */
+} ell1_align_t;
+/* align_palm_solve per image (robust.py:470-515) */
+int ell1_align_palm_batch(const ell1_align_t* A, void* stream);
+/* align_ist_solve per image (robust.py:427-467) */
+int ell1_align_ist_batch(const ell1_align_t* A, void* stream);
+
 /* fp32 GEMM path of the batched solvers (3: 3xTF32 tcgen05 kernel, the default;
  * 2: 3xTF32 split over cuBLAS TF32 GEMMs, ELL1_FP32_GEMM=tf32x3; 0: SIMT SGEMM,
  * ELL1_FP32_GEMM=simt; -1: not used yet). */

@@ -1349,3 +1349,36 @@ def trial_seed(base, *idx):
     """synth.py:145-148."""
     ss = np.random.SeedSequence((int(base),) + tuple(int(i) for i in idx))
     return int(ss.generate_state(1, np.uint64)[0])
+
+
+# ---------------------------------------------------------------- alignment
+def align_palm(B, b, tol=1e-8, max_iter=5000, mu0=1.0, rho=2.0):
+    """robust.py:470-515 (align_palm_solve): exact-fit multiplier method for
+    min ||e||_1 s.t. b = B w + e.  Returns (w, e)."""
+    B = np.asarray(B, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    R = chol_upper(B.T @ B)
+    mu = float(mu0)
+    bn = float(np.linalg.norm(b))
+    w = chol_solve(R, B.T @ b)
+    e = np.zeros(B.shape[0])
+    y = np.zeros(B.shape[0])
+    if bn == 0.0:
+        return w, e
+    it = 0
+    while it < max_iter:
+        for _ in range(min(100, max_iter - it)):
+            it += 1
+            w = chol_solve(R, B.T @ (b - e + y / mu))
+            e_new = soft(b - B @ w + y / mu, 1.0 / mu)
+            change = float(np.linalg.norm(e_new - e))
+            e = e_new
+            if change <= 1e-2 / mu * max(1.0, float(np.linalg.norm(e))):
+                break
+        r = b - B @ w - e
+        y = y + mu * r
+        if float(np.linalg.norm(r)) <= tol * bn:
+            break
+        mu *= rho
+    return w, e
+

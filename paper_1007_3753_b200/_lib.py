@@ -97,6 +97,15 @@ _lock = threading.Lock()
 _lib = None
 _load_error = None
 
+class Align(ctypes.Structure):
+    _fields_ = [("count", ctypes.c_int32), ("d", ctypes.c_int32), ("m", ctypes.c_int32),
+                ("max_iter", ctypes.c_int32), ("B", ctypes.c_void_p), ("ldb", ctypes.c_int64),
+                ("b_stride", ctypes.c_int64), ("rhs", ctypes.c_void_p), ("ld_rhs", ctypes.c_int64),
+                ("tol", ctypes.c_double), ("mu0", ctypes.c_double), ("rho", ctypes.c_double),
+                ("lam", ctypes.c_double), ("v0", ctypes.c_void_p), ("w", ctypes.c_void_p),
+                ("e", ctypes.c_void_p), ("status", ctypes.c_void_p), ("iterations", ctypes.c_void_p)]
+
+
 P = ctypes.POINTER
 _SIGS = {
     "ell1_dict_build": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
@@ -212,6 +221,8 @@ _SIGS = {
     "ell1_homotopy_group": (ctypes.c_int, [P(Group), ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
                                            ctypes.c_void_p]),
     "ell1_blas_fp32_mode": (ctypes.c_int, []),
+    "ell1_align_palm_batch": (ctypes.c_int, [P(Align), ctypes.c_void_p]),
+    "ell1_align_ist_batch": (ctypes.c_int, [P(Align), ctypes.c_void_p]),
     "ell1_gemm_f32_workspace": (ctypes.c_size_t, [ctypes.c_int32, ctypes.c_int64, ctypes.c_int64]),
     "ell1_gemm_f32": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                      ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,

@@ -1,0 +1,381 @@
+// align.cu — alignment solvers batched across images.
+//
+// Reference: robust.py:223-515.  Each instance is a tall regression
+// b ~ B w + e with sparse gross error e (B: d x m, m small — the
+// transformation parameters of one image alignment step).  The reference
+// solves one image per call with numpy; here a batch of images (each with
+// its own B) runs in one launch, one CTA per image:
+//   * B (row-major, numpy's layout) is staged in shared memory once as columns
+//     of d + 1 doubles (odd stride: conflict-free staging and column walks);
+//     the d-vectors (b, e, y / w-step residuals) live in registers, a fixed
+//     set of rows per thread (RPT rows, 256 threads apart);
+//   * the column Gram G = B^T B is formed by fixed-order block reductions and
+//     factored G = R^T R by warp 0 (not PD -> IllConditionedError, robust.py:254-258);
+//   * every B^T v is one m-wide block reduction (lanes -> xor tree -> warps,
+//     fixed order), every gram.solve two warp-parallel triangular solves.
+// Solvers: PALM (the paper's choice for alignment, robust.py:470-515) and
+// block IST (robust.py:427-467, step 1/alpha with alpha from the reference's
+// power iteration on B^T B).
+#include "ell1_b200.h"
+#include "engine.cuh"
+#include "solvers_common.cuh"
+
+namespace ell1 {
+namespace {
+
+constexpr int AT = 256;                 // threads per image
+constexpr int AW = AT / 32;
+constexpr int MAXM = 32;                // columns of B (parameters) supported
+constexpr int RPT = 8;                  // rows per thread kept in registers (d <= AT * RPT = 2048)
+
+struct AlignSh {
+  double red[AW][MAXM + 2];
+  double out[MAXM + 2];
+  double R[MAXM][MAXM];                 // upper Cholesky factor of B^T B
+  double w[MAXM];
+  double t[MAXM];
+  int flag;
+};
+
+// sum over the CTA of k per-thread values (fixed order); results in S.out[0..k)
+__device__ __forceinline__ void block_sum(AlignSh& S, double* v, int k) {
+  const int wi = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int c = 0; c < k; ++c) {
+    double s = v[c];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (l == 0) S.red[wi][c] = s;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < k) {
+    double s = S.red[0][threadIdx.x];
+    for (int ww = 1; ww < AW; ++ww) s += S.red[ww][threadIdx.x];
+    S.out[threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+// g = B^T v for the rows this thread holds; result in S.out[0..m)
+__device__ __forceinline__ void bt_times(AlignSh& S, const double* Bs, int d, int m, const double (&v)[RPT]) {
+  double p[MAXM];
+  for (int c = 0; c < m; ++c) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = threadIdx.x + q * AT;
+      if (i < d) s = fma(Bs[(int64_t)c * (d + 1) + i], v[q], s);
+    }
+    p[c] = s;
+  }
+  block_sum(S, p, m);
+}
+
+// S.w = G^{-1} S.out via R^T z = g, R w = z (warp 0; gram.solve, numerics.py:62-72)
+__device__ __forceinline__ void gram_solve(AlignSh& S, int m) {
+  if (threadIdx.x < 32) {
+    const int l = threadIdx.x;
+    double z = l < m ? S.out[l] : 0.0;
+    for (int i = 0; i < m; ++i) {                       // forward: R^T z = g
+      const double zi = __shfl_sync(0xffffffffu, z, i) / S.R[i][i];
+      if (l == i) z = zi;
+      if (l > i && l < m) z = fma(-S.R[i][l], zi, z);
+    }
+    for (int i = m - 1; i >= 0; --i) {                  // backward: R w = z
+      const double wi = __shfl_sync(0xffffffffu, z, i) / S.R[i][i];
+      if (l == i) z = wi;
+      if (l < i) z = fma(-S.R[l][i], wi, z);
+    }
+    if (l < m) S.w[l] = z;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double soft(double x, double a) {
+  return x > a ? x - a : (x < -a ? x + a : 0.0);          // _fastkernels.pyx:14-27
+}
+
+// stage B, form G = B^T B, factor; returns false (status set) when not PD
+__device__ bool setup(AlignSh& S, double* Bs, const ell1_align_t& a, int j, double (&b)[RPT]) {
+  const int d = a.d, m = a.m;
+  const double* Bj = a.B + (int64_t)j * a.b_stride;
+  for (int64_t t = threadIdx.x; t < (int64_t)d * m; t += AT) {   // row-major image, read coalesced
+    const int64_t i = t / m, c = t - i * m;
+    Bs[c * (d + 1) + i] = Bj[i * a.ldb + c];
+  }
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int i = threadIdx.x + q * AT;
+    b[q] = i < d ? a.rhs[(int64_t)j * a.ld_rhs + i] : 0.0;
+  }
+  __syncthreads();
+  for (int c = 0; c < m; ++c) {                          // row c of G (columns c..m-1)
+    double p[MAXM];
+    for (int k = c; k < m; ++k) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        const int i = threadIdx.x + q * AT;
+        if (i < d) s = fma(Bs[(int64_t)c * (d + 1) + i], Bs[(int64_t)k * (d + 1) + i], s);
+      }
+      p[k - c] = s;
+    }
+    block_sum(S, p, m - c);
+    if ((int)threadIdx.x < m - c) S.R[c][c + threadIdx.x] = S.out[threadIdx.x];
+    __syncthreads();
+  }
+  // upper Cholesky G = R^T R in place (warp 0, row-oriented)
+  if (threadIdx.x < 32) {
+    const int l = threadIdx.x;
+    int bad = 0;
+    for (int i = 0; i < m; ++i) {
+      double piv = S.R[i][i];
+      for (int k = 0; k < i; ++k) piv -= S.R[k][i] * S.R[k][i];
+      if (!(piv > 0.0)) { bad = 1; break; }
+      const double rii = sqrt(piv);
+      __syncwarp();
+      if (l > i && l < m) {
+        double v = S.R[i][l];
+        for (int k = 0; k < i; ++k) v -= S.R[k][i] * S.R[k][l];
+        S.R[i][l] = v / rii;
+      }
+      __syncwarp();
+      if (l == 0) S.R[i][i] = rii;
+      __syncwarp();
+    }
+    if (l == 0) S.flag = bad;
+  }
+  __syncthreads();
+  if (S.flag) {
+    if (threadIdx.x == 0) a.status[j] = ELL1_NOT_PD;
+    return false;
+  }
+  return true;
+}
+
+__device__ __forceinline__ void store_out(const ell1_align_t& a, int j, const AlignSh& S, const double (&e)[RPT]) {
+  if ((int)threadIdx.x < a.m) a.w[(int64_t)j * a.m + threadIdx.x] = S.w[threadIdx.x];
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int i = threadIdx.x + q * AT;
+    if (i < a.d) a.e[(int64_t)j * a.d + i] = e[q];
+  }
+}
+
+// ---------------------------------------------------------------- PALM
+// robust.py:470-515: w = G^{-1} B^T (b - e + y/mu); e = soft(b - Bw + y/mu, 1/mu)
+// (inner sweeps to 1e-2/mu relative change, <= 100 per mu), y += mu r, mu *= rho
+__global__ void __launch_bounds__(AT) align_palm_kernel(const ell1_align_t a) {
+  extern __shared__ double Bs[];
+  __shared__ AlignSh S;
+  const int d = a.d, m = a.m;
+  for (int j = blockIdx.x; j < a.count; j += gridDim.x) {
+    double b[RPT], e[RPT], y[RPT], bw[RPT], tv[RPT];
+    if (!setup(S, Bs, a, j, b)) continue;
+    double bb = 0.0;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) { e[q] = 0.0; y[q] = 0.0; bb = fma(b[q], b[q], bb); }
+    block_sum(S, &bb, 1);
+    const double bnorm = sqrt(S.out[0]);
+    bt_times(S, Bs, d, m, b);
+    gram_solve(S, m);                                    // w = gram.solve(B^T b)
+    int it = 0;
+    if (bnorm != 0.0) {
+      double mu = a.mu0;
+      while (it < a.max_iter) {
+        const int inner = a.max_iter - it < 100 ? a.max_iter - it : 100;
+        for (int s = 0; s < inner; ++s) {
+          ++it;
+#pragma unroll
+          for (int q = 0; q < RPT; ++q) tv[q] = b[q] - e[q] + y[q] / mu;
+          bt_times(S, Bs, d, m, tv);
+          gram_solve(S, m);
+          double nrm[2] = {0.0, 0.0};                    // ||e_new - e||^2, ||e_new||^2
+#pragma unroll
+          for (int q = 0; q < RPT; ++q) {
+            const int i = threadIdx.x + q * AT;
+            double s2 = 0.0;
+            if (i < d)
+              for (int c = 0; c < m; ++c) s2 = fma(Bs[(int64_t)c * (d + 1) + i], S.w[c], s2);
+            bw[q] = s2;
+            const double en = i < d ? soft(b[q] - s2 + y[q] / mu, 1.0 / mu) : 0.0;
+            const double df = en - e[q];
+            nrm[0] = fma(df, df, nrm[0]);
+            nrm[1] = fma(en, en, nrm[1]);
+            e[q] = en;
+          }
+          block_sum(S, nrm, 2);
+          const double change = sqrt(S.out[0]), en2 = sqrt(S.out[1]);
+          if (change <= 1e-2 / mu * (en2 > 1.0 ? en2 : 1.0)) break;
+        }
+        double rr = 0.0;
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+          const double r = b[q] - bw[q] - e[q];
+          y[q] = fma(mu, r, y[q]);
+          rr = fma(r, r, rr);
+        }
+        block_sum(S, &rr, 1);
+        if (sqrt(S.out[0]) <= a.tol * bnorm) break;
+        mu *= a.rho;
+      }
+    }
+    store_out(a, j, S, e);
+    if (threadIdx.x == 0) { a.status[j] = ELL1_OK; if (a.iterations) a.iterations[j] = it; }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- block IST
+// robust.py:427-467: w += B^T r / alpha, e = soft(e + r/alpha, lam/alpha); stop
+// when max|B^T r| <= tol and kkt(e, r, lam) <= tol lam.  alpha = 1.01 (||B||^2 + 1)
+// with ||B||^2 from the reference's power iteration (numerics.py:224-261) run on
+// B^T (B v) from the host-drawn start vectors.
+__global__ void __launch_bounds__(AT) align_ist_kernel(const ell1_align_t a) {
+  extern __shared__ double Bs[];
+  __shared__ AlignSh S;
+  __shared__ double v[MAXM];
+  const int d = a.d, m = a.m;
+  for (int j = blockIdx.x; j < a.count; j += gridDim.x) {
+    double b[RPT], e[RPT], r[RPT];
+    if (!setup(S, Bs, a, j, b)) continue;
+    // lambda: 1e-2 max|b - B w0|, w0 = gram.solve(B^T b) (robust.py:270-273)
+    double lam = a.lam;
+    if (!(lam > 0.0)) {
+      bt_times(S, Bs, d, m, b);
+      gram_solve(S, m);
+      double mx = 0.0;
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        const int i = threadIdx.x + q * AT;
+        if (i < d) {
+          double s2 = 0.0;
+          for (int c = 0; c < m; ++c) s2 = fma(Bs[(int64_t)c * (d + 1) + i], S.w[c], s2);
+          mx = nmax(mx, fabs(b[q] - s2));
+        }
+      }
+      mx = warp_max(mx);
+      if ((threadIdx.x & 31) == 0) S.red[threadIdx.x >> 5][0] = mx;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = S.red[0][0];
+        for (int ww = 1; ww < AW; ++ww) t = nmax(t, S.red[ww][0]);
+        S.out[0] = 1e-2 * t;
+      }
+      __syncthreads();
+      lam = S.out[0];
+    }
+    // power iteration on B^T B (spectral_norm_sq, dim = m < d)
+    int draw = 0;
+    if ((int)threadIdx.x < m) v[threadIdx.x] = a.v0[threadIdx.x];
+    __syncthreads();
+    double theta = 0.0;
+    for (int k = 0; k < 1000; ++k) {
+      double u[RPT];
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        const int i = threadIdx.x + q * AT;
+        double s2 = 0.0;
+        if (i < d)
+          for (int c = 0; c < m; ++c) s2 = fma(Bs[(int64_t)c * (d + 1) + i], v[c], s2);
+        u[q] = s2;
+      }
+      bt_times(S, Bs, d, m, u);                          // S.out = B^T (B v)
+      if (threadIdx.x == 0) {
+        double th = 0.0, res = 0.0, nw = 0.0;
+        for (int c = 0; c < m; ++c) th = fma(v[c], S.out[c], th);
+        for (int c = 0; c < m; ++c) { const double t = S.out[c] - th * v[c]; res = fma(t, t, res); }
+        for (int c = 0; c < m; ++c) nw = fma(S.out[c], S.out[c], nw);
+        S.t[0] = th;
+        S.t[1] = sqrt(res);
+        S.t[2] = sqrt(nw);
+      }
+      __syncthreads();
+      theta = S.t[0];
+      if (S.t[1] <= 1e-6 * (theta > 2.2250738585072014e-308 ? theta : 2.2250738585072014e-308)) break;
+      const double nw = S.t[2];
+      __syncthreads();
+      if (nw == 0.0) ++draw;                             // start vector in the nullspace: next draw
+      if ((int)threadIdx.x < m)
+        v[threadIdx.x] = nw == 0.0 ? a.v0[(draw % 4) * m + threadIdx.x] : S.out[threadIdx.x] / nw;
+      __syncthreads();
+    }
+    const double alpha = 1.01 * (theta + 1.0);
+    // iterate from w = 0, e = 0 (robust.py:457-466)
+    if ((int)threadIdx.x < m) S.w[threadIdx.x] = 0.0;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) { e[q] = 0.0; r[q] = b[q]; }
+    __syncthreads();
+    bt_times(S, Bs, d, m, r);                            // B^T r at (0, 0)
+    int it = 0;
+    for (; it < a.max_iter;) {
+      ++it;
+      if ((int)threadIdx.x < m) S.w[threadIdx.x] += S.out[threadIdx.x] / alpha;
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) e[q] = soft(e[q] + r[q] / alpha, lam / alpha);
+      __syncthreads();
+      double kk = 0.0;
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        const int i = threadIdx.x + q * AT;
+        double s2 = 0.0;
+        if (i < d)
+          for (int c = 0; c < m; ++c) s2 = fma(Bs[(int64_t)c * (d + 1) + i], S.w[c], s2);
+        r[q] = i < d ? b[q] - s2 - e[q] : 0.0;
+        if (i < d) {                                     // kkt_from_correlation(e, r, lam), model.py:160-173
+          const double viol = e[q] != 0.0 ? fabs(r[q] - lam * (e[q] > 0.0 ? 1.0 : -1.0))
+                                          : fabs(r[q]) - lam;
+          kk = nmax(kk, viol);
+        }
+      }
+      kk = warp_max(kk);
+      bt_times(S, Bs, d, m, r);                          // also the next step's gradient
+      if ((threadIdx.x & 31) == 0) S.red[threadIdx.x >> 5][MAXM + 1] = kk;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = S.red[0][MAXM + 1], g = 0.0;
+        for (int ww = 1; ww < AW; ++ww) t = nmax(t, S.red[ww][MAXM + 1]);
+        for (int c = 0; c < m; ++c) g = nmax(g, fabs(S.out[c]));
+        S.flag = g <= a.tol && nmax(t, 0.0) <= a.tol * lam;
+      }
+      __syncthreads();
+      if (S.flag) break;
+    }
+    store_out(a, j, S, e);
+    if (threadIdx.x == 0) { a.status[j] = ELL1_OK; if (a.iterations) a.iterations[j] = it; }
+    __syncthreads();
+  }
+}
+
+int launch_align(bool palm, const ell1_align_t* A, void* stream) {
+  if (!A || A->count < 0 || A->m < 1 || A->m > MAXM || A->d <= A->m || A->d > AT * RPT || !A->B || !A->rhs ||
+      !A->w || !A->e || !A->status || A->ldb < A->m || A->ld_rhs < A->d || A->b_stride < A->ldb * A->d)
+    return ELL1_ERR_ARG;
+  if (!palm && !A->v0) return ELL1_ERR_ARG;
+  if (A->count == 0) return ELL1_OK;
+  const size_t smem = (size_t)(A->d + 1) * A->m * 8;
+  const void* k = palm ? (const void*)align_palm_kernel : (const void*)align_ist_kernel;
+  if (smem > 48 * 1024 && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+                              cudaSuccess)
+    return ELL1_ERR_ARG;
+  int dev = 0, sms = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, AT, smem);
+  int grid = sms * (per > 0 ? per : 1);
+  if (grid > A->count) grid = A->count;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (palm) align_palm_kernel<<<grid, AT, smem, s>>>(*A);
+  else align_ist_kernel<<<grid, AT, smem, s>>>(*A);
+  return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
+}
+
+}  // namespace
+}  // namespace ell1
+
+extern "C" int ell1_align_palm_batch(const ell1_align_t* A, void* stream) {
+  return ell1::launch_align(true, A, stream);
+}
+
+extern "C" int ell1_align_ist_batch(const ell1_align_t* A, void* stream) {
+  return ell1::launch_align(false, A, stream);
+}

@@ -229,3 +229,127 @@ def cab_solve(A, b, solver, config):
         res = pdipa_solve(prob, config)
     w = res.x_star
     return w[:n], scale * w[n:], res
+
+
+# ---------------------------------------------------------------- alignment
+# the alignment solvers (robust.py:223-515), batched
+# across images on the device (csrc/align.cu, one CTA per image).
+
+_POWER_SEED = 218751     # numerics.py:224 (IST step size)
+
+
+class AlignmentProblem:
+    """Tall regression b ~ B w with sparse gross error e (robust.py:223-252)."""
+
+    def __init__(self, B, b, ground_truth_w=None, ground_truth_e=None):
+        self.B = np.ascontiguousarray(B, dtype=np.float64)
+        self.b = np.ascontiguousarray(b, dtype=np.float64)
+        self.ground_truth_w = ground_truth_w
+        self.ground_truth_e = ground_truth_e
+        if self.B.ndim != 2:
+            raise ValueError("B must be a matrix")
+        if self.B.shape[0] <= self.B.shape[1]:
+            raise ValueError("B must be tall: more rows than columns")
+        if self.b.shape != (self.B.shape[0],):
+            raise ValueError("b must have length d")
+
+    @property
+    def d(self):
+        return self.B.shape[0]
+
+    @property
+    def m(self):
+        return self.B.shape[1]
+
+
+def _align_batch(kind, Bs, bs, config, lam=None):
+    """Run one batched alignment launch.  Bs: (count, d, m), bs: (count, d).
+    Returns (W (count, m), E (count, d), iterations (count,))."""
+    import ctypes
+    from paper_1007_3753_b200 import _lib
+    from paper_1007_3753_b200._runner import raise_for
+    torch = device._torch()
+    L = _lib.lib()
+    Bs = np.asarray(Bs, dtype=np.float64)
+    bs = np.asarray(bs, dtype=np.float64)
+    if Bs.ndim != 3 or bs.ndim != 2 or bs.shape != Bs.shape[:2]:
+        raise ValueError("need B of shape (count, d, m) and b of shape (count, d)")
+    count, d, m = Bs.shape
+    if d <= m:
+        raise ValueError("B must be tall: more rows than columns")
+    if m > 32 or d > 2048:
+        raise ValueError("batched alignment supports m <= 32 parameters and d <= 2048 rows")
+    dev = device.current_device(config.opt("device", None))
+    Bd = torch.from_numpy(np.ascontiguousarray(Bs)).to(dev)      # row-major images, as given
+    bd = torch.from_numpy(np.ascontiguousarray(bs)).to(dev)
+    W = torch.empty((count, m), dtype=torch.float64, device=dev)
+    E = torch.empty((count, d), dtype=torch.float64, device=dev)
+    st = torch.full((count,), -1, dtype=torch.int32, device=dev)
+    its = torch.zeros((count,), dtype=torch.int32, device=dev)
+    a = _lib.Align()
+    a.count, a.d, a.m, a.max_iter = count, d, m, int(config.max_iter)
+    a.B, a.ldb, a.b_stride = Bd.data_ptr(), m, d * m
+    a.rhs, a.ld_rhs = bd.data_ptr(), d
+    a.tol = float(config.tol)
+    a.mu0 = float(config.opt("mu0", 1.0))
+    a.rho = float(config.opt("rho", 2.0))
+    a.lam = -1.0 if lam is None else float(lam)
+    v0 = None
+    if kind == "ist":
+        rng = np.random.default_rng(_POWER_SEED)      # spectral_norm_sq's start vector + redraws
+        draws = []
+        for _ in range(4):
+            v = rng.standard_normal(m)
+            draws.append(v / np.linalg.norm(v))
+        v0 = torch.from_numpy(np.concatenate(draws)).to(dev)
+        a.v0 = v0.data_ptr()
+    a.w, a.e, a.status, a.iterations = W.data_ptr(), E.data_ptr(), st.data_ptr(), its.data_ptr()
+    fn = L.ell1_align_palm_batch if kind == "palm" else L.ell1_align_ist_batch
+    _lib.check(fn(ctypes.byref(a), device.stream_ptr(dev)), "ell1_align_%s_batch" % kind)
+    status = st.cpu().numpy()
+    if np.any(status == _lib.NOT_PD):                 # robust.py:254-258
+        from paper_1007_3753_b200.exceptions import IllConditionedError
+        raise IllConditionedError("B must have full column rank")
+    for s in np.unique(status):
+        raise_for(int(s), {})
+    return W.cpu().numpy(), E.cpu().numpy(), its.cpu().numpy()
+
+
+def _palm_options(config):
+    mu = float(config.opt("mu0", 1.0))
+    rho = float(config.opt("rho", 2.0))
+    if not mu > 0 or not rho > 1:
+        raise ValueError("mu0 must be positive and rho must exceed 1")
+
+
+def align_palm_solve_batch(Bs, bs, config):
+    """align_palm_solve for a batch of images (element j == align_palm_solve
+    on (Bs[j], bs[j])).  Returns (W, E)."""
+    _palm_options(config)
+    W, E, _ = _align_batch("palm", Bs, bs, config)
+    return W, E
+
+
+def align_ist_solve_batch(Bs, bs, lam, config):
+    """align_ist_solve for a batch of images; lam=None: per-image default."""
+    if lam is not None and not lam > 0:
+        raise ValueError("lambda must be positive")
+    W, E, _ = _align_batch("ist", Bs, bs, config, lam)
+    return W, E
+
+
+def align_palm_solve(prob, config):
+    """Multiplier method for min ||e||_1 s.t. b = B w + e (robust.py:470-515);
+    options mu0 (1.0), rho (2.0).  Returns (w, e)."""
+    _palm_options(config)
+    W, E, _ = _align_batch("palm", prob.B[None], prob.b[None], config)
+    return W[0], E[0]
+
+
+def align_ist_solve(prob, lam, config):
+    """Block soft-thresholding on the alignment objective (robust.py:427-467).
+    Returns (w, e)."""
+    if lam is not None and not lam > 0:
+        raise ValueError("lambda must be positive")
+    W, E, _ = _align_batch("ist", prob.B[None], prob.b[None], config, lam)
+    return W[0], E[0]

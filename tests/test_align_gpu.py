@@ -1,0 +1,96 @@
+"""Alignment solvers batched across images (robust.py:223-515)
+against the reference's own outputs (tests/golden/make_align_golden.py), plus
+the reference's edge cases (test_robust.py: rank-deficient basis, zero data,
+option validation).  Batched element j must equal the single-image call."""
+
+import os
+
+import numpy as np
+import pytest
+
+from tests.golden.align_cases import CASES, align_instance
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "align_golden.npz")
+
+
+def _cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+
+
+def _rel(x, ref):
+    return float(np.linalg.norm(x - ref) / max(np.linalg.norm(ref), 1e-300))
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_align_matches_reference(name):
+    _cuda()
+    from paper_1007_3753_b200.model import SolverConfig
+    from paper_1007_3753_b200.robust import AlignmentProblem, align_ist_solve, align_palm_solve
+    c = CASES[name]
+    gold = np.load(GOLD)
+    B, b = align_instance(**c["recipe"])
+    prob = AlignmentProblem(B, b)
+    cfg = SolverConfig(tol=c["tol"], max_iter=c["max_iter"], options=c.get("options", {}))
+    if c["solver"] == "palm":
+        w, e = align_palm_solve(prob, cfg)
+    else:
+        w, e = align_ist_solve(prob, c.get("lam"), cfg)
+    assert _rel(w, gold[name + "_w"]) <= 1e-6
+    assert _rel(e, gold[name + "_e"]) <= 1e-6
+    top = np.max(np.abs(gold[name + "_e"]))
+    assert set(np.nonzero(np.abs(e) > 1e-3 * top)[0]) == set(np.nonzero(np.abs(gold[name + "_e"]) > 1e-3 * top)[0])
+
+
+@pytest.mark.parametrize("solver", ["palm", "ist"])
+def test_batch_equals_single_images(solver):
+    _cuda()
+    from paper_1007_3753_b200.model import SolverConfig
+    from paper_1007_3753_b200 import robust
+    insts = [align_instance(seed=100 + j, d=150, m=9) for j in range(12)]
+    Bs = np.stack([B for B, _ in insts])
+    bs = np.stack([b for _, b in insts])
+    cfg = SolverConfig(tol=1e-8, max_iter=5000)
+    if solver == "palm":
+        W, E = robust.align_palm_solve_batch(Bs, bs, cfg)
+    else:
+        W, E = robust.align_ist_solve_batch(Bs, bs, None, cfg)
+    for j, (B, b) in enumerate(insts):
+        prob = robust.AlignmentProblem(B, b)
+        if solver == "palm":
+            w, e = robust.align_palm_solve(prob, cfg)
+        else:
+            w, e = robust.align_ist_solve(prob, None, cfg)
+        assert np.array_equal(W[j], w) and np.array_equal(E[j], e)
+
+
+def test_rank_deficient_basis_raises():
+    _cuda()
+    from paper_1007_3753_b200.exceptions import IllConditionedError
+    from paper_1007_3753_b200.model import SolverConfig
+    from paper_1007_3753_b200.robust import AlignmentProblem, align_ist_solve, align_palm_solve
+    B, b = align_instance(seed=9, d=40, m=4)
+    B[:, 3] = 0.0                      # zero column: G has a zero pivot (the reference raises too)
+    prob = AlignmentProblem(B, b)
+    with pytest.raises(IllConditionedError):
+        align_palm_solve(prob, SolverConfig())
+    with pytest.raises(IllConditionedError):
+        align_ist_solve(prob, 0.1, SolverConfig())
+
+
+def test_zero_data_and_option_validation():
+    _cuda()
+    from paper_1007_3753_b200.model import SolverConfig
+    from paper_1007_3753_b200.robust import AlignmentProblem, align_ist_solve, align_palm_solve
+    B, _ = align_instance(seed=10, d=30, m=3)
+    w, e = align_palm_solve(AlignmentProblem(B, np.zeros(30)), SolverConfig())
+    assert np.all(w == 0.0) and np.all(e == 0.0)
+    prob = AlignmentProblem(B, B @ np.ones(3))
+    with pytest.raises(ValueError):
+        align_palm_solve(prob, SolverConfig(options={"mu0": 0.0}))
+    with pytest.raises(ValueError):
+        align_palm_solve(prob, SolverConfig(options={"rho": 1.0}))
+    with pytest.raises(ValueError):
+        align_ist_solve(prob, -1.0, SolverConfig())

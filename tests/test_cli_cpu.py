@@ -121,3 +121,13 @@ def test_result_payload_key_order_matches_reference():
                               e=np.zeros(2))
     assert list(ours.keys()) == list(ref.keys())
     assert list(ours["config_echo"].keys()) == list(ref["config_echo"].keys())
+
+
+def test_alignment_problem_validation():
+    from paper_1007_3753_b200.robust import AlignmentProblem
+    with pytest.raises(ValueError):
+        AlignmentProblem(np.ones((3, 5)), np.ones(3))      # wide
+    with pytest.raises(ValueError):
+        AlignmentProblem(np.ones((6, 2)), np.ones(5))      # length mismatch
+    p = AlignmentProblem(np.ones((6, 2)), np.ones(6))
+    assert (p.d, p.m) == (6, 2)
