@@ -10,9 +10,9 @@ formats and exit codes — with every solve running on the device:
 * exit codes: 0 success, 1 solver did not meet its convergence test
   (results still written) or broke down numerically, 2 usage error.
 
-Subcommands: solve, gen, cab, phase, noise-sweep (cli.py:137-302).  `align`
-(the alignment solvers, §8(f) rank 4) and SVG rendering (`report`, --svg)
-are not part of this backend and exit 2 with a diagnostic.
+Subcommands: solve, gen, cab, phase, noise-sweep, align (palm / ist)
+(cli.py:137-350).  SVG rendering (`report`, --svg) and `align --algo gp /
+homotopy` are not part of this backend and exit 2 with a diagnostic.
 
     python -m paper_1007_3753_b200.cli solve --algo fista --matrix A.csv --rhs b.csv --out r.json
 """
@@ -254,10 +254,53 @@ def cmd_noise_sweep(args):
     return 0
 
 
+def cmd_align(args):
+    """cli.py:298-350: tall regression with sparse gross errors (PALM / IST on
+    the device; iteration counts are not part of the alignment contract, so
+    convergence is certified after the fact as in the reference)."""
+    from paper_1007_3753_b200.robust import AlignmentProblem, align_ist_solve, align_palm_solve
+    import time
+    if args.algo not in ("palm", "ist"):
+        raise UsageError("align --algo %s is not provided by the B200 backend (palm, ist are)" % args.algo)
+    B = read_csv(args.basis, "basis")
+    b = read_vector(args.rhs, "rhs")
+    same_rows("basis", B.shape, "rhs", b.size)
+    try:
+        prob = AlignmentProblem(B, b)
+    except ValueError as exc:
+        raise UsageError(str(exc))
+    cfg = make_config(args, 1e-8, 5000)
+    t0 = time.perf_counter()
+    if args.algo == "palm":
+        w, e = align_palm_solve(prob, cfg)
+    else:
+        w, e = align_ist_solve(prob, args.lam, cfg)
+    wall = time.perf_counter() - t0
+    r = b - B @ w - e
+    if args.algo == "palm":
+        lam = None
+        obj = float(np.abs(e).sum())
+        kkt = float(np.abs(r).max())
+        converged = bool(np.linalg.norm(r) <= 10.0 * cfg.tol * max(1.0, np.linalg.norm(b)))
+    else:
+        lam = cfg.lam
+        if lam is None:                      # 1e-2 x the peak least-squares residual (robust.py:270-273)
+            w0 = np.linalg.solve(B.T @ B, B.T @ b)
+            lam = 1e-2 * float(np.abs(b - B @ w0).max())
+        obj = 0.5 * float(r @ r) + lam * float(np.abs(e).sum())
+        grad_w = float(np.abs(B.T @ r).max())
+        ke = kkt_from_correlation(e, r, lam)
+        kkt = max(grad_w, ke)
+        scale = max(1.0, float(np.abs(B.T @ b).max()))
+        converged = bool(grad_w <= 10.0 * cfg.tol * scale and ke <= 10.0 * cfg.tol * lam)
+    write_json(args.out, result_payload(args.algo, prob.m, prob.d, lam, None, converged, wall, w, obj, kkt,
+                                        cfg, args.seed, e=e))
+    return 0 if converged else 1
+
+
 def cmd_unsupported(args):
     raise UsageError("`%s` is not provided by the B200 backend (%s)" % (
-        args.subcommand, {"align": "alignment solvers: SURVEY §8(f) rank 4",
-                          "report": "SVG rendering"}[args.subcommand]))
+        args.subcommand, {"report": "SVG rendering"}[args.subcommand]))
 
 
 # ------------------------------------------------------------------ parser
@@ -335,10 +378,18 @@ def build_parser():
     p.add_argument("--out", required=True)
     p.set_defaults(func=cmd_cab)
 
-    for name in ("align", "report"):
-        p = sub.add_parser(name)
-        p.add_argument("rest", nargs=argparse.REMAINDER)
-        p.set_defaults(func=cmd_unsupported)
+    p = sub.add_parser("align")
+    p.add_argument("--algo", choices=("gp", "homotopy", "ist", "palm"), default="palm")
+    p.add_argument("--basis", required=True)
+    p.add_argument("--rhs", required=True)
+    _config_flags(p)
+    p.add_argument("--seed", type=int, default=None)
+    p.add_argument("--out", required=True)
+    p.set_defaults(func=cmd_align)
+
+    p = sub.add_parser("report")
+    p.add_argument("rest", nargs=argparse.REMAINDER)
+    p.set_defaults(func=cmd_unsupported)
     return top
 
 

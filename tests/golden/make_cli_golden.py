@@ -33,12 +33,26 @@ RUNS = [
 ]
 
 
+ALIGN_RUNS = [
+    ("align_palm", ["align", "--algo", "palm", "--basis", "B.csv", "--rhs", "balign.csv",
+                    "--out", "align_palm.json"]),
+    ("align_ist", ["align", "--algo", "ist", "--basis", "B.csv", "--rhs", "balign.csv", "--lambda", "0.05",
+                   "--tol", "1e-7", "--max-iter", "20000", "--out", "align_ist.json"]),
+]
+
+
 def main():
     from ell1 import cli
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from tests.golden.align_cases import align_instance
+    import numpy as np
     os.makedirs(OUT, exist_ok=True)
+    B, b = align_instance(seed=21, d=90, m=6)
+    np.savetxt(os.path.join(OUT, "B.csv"), B, fmt="%.17g", delimiter=",")
+    np.savetxt(os.path.join(OUT, "balign.csv"), b[:, None], fmt="%.17g", delimiter=",")
     os.environ["ELL1_OUT_DIR"] = OUT
     manifest = []
-    for name, argv in RUNS:
+    for name, argv in RUNS + ALIGN_RUNS:
         # inputs are read relative to the fixture directory
         argv = [os.path.join(OUT, a) if a.endswith(".csv") and name != "gen" else a for a in argv]
         rc = cli.run(argv)
