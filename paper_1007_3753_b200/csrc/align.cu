@@ -346,14 +346,130 @@ __global__ void __launch_bounds__(AT) align_ist_kernel(const ell1_align_t a) {
   }
 }
 
-int launch_align(bool palm, const ell1_align_t* A, void* stream) {
+// ---------------------------------------------------------------- homotopy
+// robust.py:374-424: walk the weight down from the peak least-squares
+// residual, moving the active error coordinates along their sign between
+// events, re-solving w from the normal equations after each step; then a
+// block-coordinate cleanup at the target weight.
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ void block_min2(AlignSh& S, double v0, double v1) {
+  v0 = warp_min(v0);
+  v1 = warp_min(v1);
+  if ((threadIdx.x & 31) == 0) { S.red[threadIdx.x >> 5][0] = v0; S.red[threadIdx.x >> 5][1] = v1; }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double t = S.red[0][threadIdx.x];
+    for (int ww = 1; ww < AW; ++ww) t = fmin(t, S.red[ww][threadIdx.x]);
+    S.out[threadIdx.x] = t;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(AT) align_homotopy_kernel(const ell1_align_t a) {
+  extern __shared__ double Bs[];
+  __shared__ AlignSh S;
+  const int d = a.d, m = a.m;
+  const double INF = __longlong_as_double(0x7ff0000000000000LL);
+  for (int j = blockIdx.x; j < a.count; j += gridDim.x) {
+    double b[RPT], e[RPT], c[RPT], tv[RPT], rb[RPT];
+    if (!setup(S, Bs, a, j, b)) continue;
+    // w = w_solve(e) (robust.py:386-387); rb = b - B w, c = rb - e
+    auto w_solve_c = [&]() {
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) tv[q] = b[q] - e[q];
+      bt_times(S, Bs, d, m, tv);
+      gram_solve(S, m);
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        const int i = threadIdx.x + q * AT;
+        double s2 = 0.0;
+        if (i < d)
+          for (int k = 0; k < m; ++k) s2 = fma(Bs[(int64_t)k * (d + 1) + i], S.w[k], s2);
+        rb[q] = i < d ? b[q] - s2 : 0.0;
+        c[q] = rb[q] - e[q];
+      }
+    };
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) e[q] = 0.0;
+    w_solve_c();
+    double mx = 0.0;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) mx = nmax(mx, fabs(c[q]));
+    block_min2(S, -mx, 0.0);
+    const double lam0 = -S.out[0];
+    const double target = a.lam > 0.0 ? a.lam : 1e-2 * lam0;
+    int it = 0;
+    if (!(lam0 <= target || lam0 == 0.0)) {
+      double lam = lam0;
+      for (; it < a.max_iter; ++it) {
+        if (lam <= target) break;
+        // gamma = min(lam - target, min_inactive(lam - |c|), min_closing(-e / dir))
+        double g_in = INF, g_cl = INF;
+        bool act[RPT];
+        double dir[RPT];
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+          const int i = threadIdx.x + q * AT;
+          const double ac = fabs(c[q]);
+          act[q] = i < d && (ac >= lam * (1.0 - 1e-9) || e[q] != 0.0);
+          dir[q] = ac > 0.0 ? (c[q] > 0.0 ? 1.0 : -1.0) : (e[q] > 0.0 ? 1.0 : (e[q] < 0.0 ? -1.0 : 0.0));
+          if (i < d && !act[q]) g_in = fmin(g_in, lam - ac);
+          if (act[q] && e[q] * dir[q] < 0.0) g_cl = fmin(g_cl, -e[q] / dir[q]);
+        }
+        block_min2(S, g_in, g_cl);
+        double gamma = lam - target;
+        gamma = fmin(gamma, S.out[0]);
+        gamma = fmin(gamma, S.out[1]);
+        gamma = nmax(gamma, 1e-12 * lam0);                 // anti-stall floor
+#pragma unroll
+        for (int q = 0; q < RPT; ++q)
+          if (act[q]) e[q] = e[q] + gamma * dir[q];
+        lam = lam - gamma;
+        w_solve_c();
+      }
+      // block-coordinate cleanup at the target weight
+      lam = target;
+      for (int k = 0; k < a.max_iter; ++k) {
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+          const int i = threadIdx.x + q * AT;
+          e[q] = i < d ? soft(rb[q], lam) : 0.0;
+        }
+        w_solve_c();
+        double kk = 0.0;
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+          const int i = threadIdx.x + q * AT;
+          if (i < d) {
+            const double viol = e[q] != 0.0 ? fabs(c[q] - lam * (e[q] > 0.0 ? 1.0 : -1.0)) : fabs(c[q]) - lam;
+            kk = nmax(kk, viol);
+          }
+        }
+        block_min2(S, -kk, 0.0);
+        if (nmax(-S.out[0], 0.0) <= a.tol * lam) break;
+      }
+    }
+    store_out(a, j, S, e);
+    if (threadIdx.x == 0) { a.status[j] = ELL1_OK; if (a.iterations) a.iterations[j] = it; }
+    __syncthreads();
+  }
+}
+
+int launch_align(int kind, const ell1_align_t* A, void* stream) {
   if (!A || A->count < 0 || A->m < 1 || A->m > MAXM || A->d <= A->m || A->d > AT * RPT || !A->B || !A->rhs ||
       !A->w || !A->e || !A->status || A->ldb < A->m || A->ld_rhs < A->d || A->b_stride < A->ldb * A->d)
     return ELL1_ERR_ARG;
-  if (!palm && !A->v0) return ELL1_ERR_ARG;
+  const bool palm = kind == 0;
+  if (kind == 1 && !A->v0) return ELL1_ERR_ARG;
   if (A->count == 0) return ELL1_OK;
   const size_t smem = (size_t)(A->d + 1) * A->m * 8;
-  const void* k = palm ? (const void*)align_palm_kernel : (const void*)align_ist_kernel;
+  const void* k = kind == 0 ? (const void*)align_palm_kernel
+                 : kind == 1 ? (const void*)align_ist_kernel : (const void*)align_homotopy_kernel;
   if (smem > 48 * 1024 && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
                               cudaSuccess)
     return ELL1_ERR_ARG;
@@ -365,7 +481,8 @@ int launch_align(bool palm, const ell1_align_t* A, void* stream) {
   if (grid > A->count) grid = A->count;
   cudaStream_t s = (cudaStream_t)stream;
   if (palm) align_palm_kernel<<<grid, AT, smem, s>>>(*A);
-  else align_ist_kernel<<<grid, AT, smem, s>>>(*A);
+  else if (kind == 1) align_ist_kernel<<<grid, AT, smem, s>>>(*A);
+  else align_homotopy_kernel<<<grid, AT, smem, s>>>(*A);
   return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
 }
 
@@ -373,9 +490,13 @@ int launch_align(bool palm, const ell1_align_t* A, void* stream) {
 }  // namespace ell1
 
 extern "C" int ell1_align_palm_batch(const ell1_align_t* A, void* stream) {
-  return ell1::launch_align(true, A, stream);
+  return ell1::launch_align(0, A, stream);
 }
 
 extern "C" int ell1_align_ist_batch(const ell1_align_t* A, void* stream) {
-  return ell1::launch_align(false, A, stream);
+  return ell1::launch_align(1, A, stream);
+}
+
+extern "C" int ell1_align_homotopy_batch(const ell1_align_t* A, void* stream) {
+  return ell1::launch_align(2, A, stream);
 }

@@ -304,7 +304,8 @@ def _align_batch(kind, Bs, bs, config, lam=None):
         v0 = torch.from_numpy(np.concatenate(draws)).to(dev)
         a.v0 = v0.data_ptr()
     a.w, a.e, a.status, a.iterations = W.data_ptr(), E.data_ptr(), st.data_ptr(), its.data_ptr()
-    fn = L.ell1_align_palm_batch if kind == "palm" else L.ell1_align_ist_batch
+    fn = {"palm": L.ell1_align_palm_batch, "ist": L.ell1_align_ist_batch,
+          "homotopy": L.ell1_align_homotopy_batch}[kind]
     _lib.check(fn(ctypes.byref(a), device.stream_ptr(dev)), "ell1_align_%s_batch" % kind)
     status = st.cpu().numpy()
     if np.any(status == _lib.NOT_PD):                 # robust.py:254-258
@@ -353,3 +354,19 @@ def align_ist_solve(prob, lam, config):
         raise ValueError("lambda must be positive")
     W, E, _ = _align_batch("ist", prob.B[None], prob.b[None], config, lam)
     return W[0], E[0]
+
+
+def align_homotopy_solve_batch(Bs, bs, config):
+    """align_homotopy_solve for a batch of images (target config.lam, default
+    1e-2 of each image's peak least-squares residual)."""
+    W, E, _ = _align_batch("homotopy", Bs, bs, config, config.lam)
+    return W, E
+
+
+def align_homotopy_solve(prob, config):
+    """Path-following in the error block with w re-solved at every step, then
+    a block-coordinate cleanup at the target weight (robust.py:374-424).
+    Returns (w, e)."""
+    W, E, _ = _align_batch("homotopy", prob.B[None], prob.b[None], config, config.lam)
+    return W[0], E[0]
+

@@ -25,6 +25,11 @@ CASES = {
                 "options": {"mu0": 0.5, "rho": 1.5}},
     "palm_budget": {"solver": "palm", "recipe": dict(seed=5, d=80, m=5), "tol": 1e-12, "max_iter": 37},
     "ist_60x7": {"solver": "ist", "recipe": dict(seed=6, d=60, m=7), "tol": 1e-9, "max_iter": 20000},
+    "hom_120x11": {"solver": "homotopy", "recipe": dict(seed=8, d=120, m=11), "tol": 1e-9, "max_iter": 5000},
+    "hom_60x7_lam": {"solver": "homotopy", "recipe": dict(seed=9, d=60, m=7), "tol": 1e-8, "max_iter": 5000,
+                     "lam": 0.02},
+    "hom_1024x11": {"solver": "homotopy", "recipe": dict(seed=10, d=1024, m=11, frac=0.2), "tol": 1e-8,
+                    "max_iter": 5000},
     "ist_120x11_lam": {"solver": "ist", "recipe": dict(seed=7, d=120, m=11), "tol": 1e-8, "max_iter": 20000,
                        "lam": 0.05},
 }

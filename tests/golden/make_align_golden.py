@@ -19,14 +19,17 @@ from tests.golden.align_cases import CASES, align_instance  # noqa: E402
 
 def main():
     from ell1.model import SolverConfig
-    from ell1.robust import AlignmentProblem, align_ist_solve, align_palm_solve
+    from ell1.robust import AlignmentProblem, align_homotopy_solve, align_ist_solve, align_palm_solve
     out = {}
     for name, c in CASES.items():
         B, b = align_instance(**c["recipe"])
         prob = AlignmentProblem(B, b)
-        cfg = SolverConfig(tol=c["tol"], max_iter=c["max_iter"], options=c.get("options", {}))
+        cfg = SolverConfig(tol=c["tol"], max_iter=c["max_iter"], options=c.get("options", {}),
+                           lam=c.get("lam") if c["solver"] == "homotopy" else None)
         if c["solver"] == "palm":
             w, e = align_palm_solve(prob, cfg)
+        elif c["solver"] == "homotopy":
+            w, e = align_homotopy_solve(prob, cfg)
         else:
             w, e = align_ist_solve(prob, c.get("lam"), cfg)
         out[name + "_w"] = w

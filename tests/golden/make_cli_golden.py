@@ -38,6 +38,8 @@ ALIGN_RUNS = [
                     "--out", "align_palm.json"]),
     ("align_ist", ["align", "--algo", "ist", "--basis", "B.csv", "--rhs", "balign.csv", "--lambda", "0.05",
                    "--tol", "1e-7", "--max-iter", "20000", "--out", "align_ist.json"]),
+    ("align_homotopy", ["align", "--algo", "homotopy", "--basis", "B.csv", "--rhs", "balign.csv",
+                        "--out", "align_homotopy.json"]),
 ]
 
 

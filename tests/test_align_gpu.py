@@ -28,14 +28,18 @@ def _rel(x, ref):
 def test_align_matches_reference(name):
     _cuda()
     from paper_1007_3753_b200.model import SolverConfig
-    from paper_1007_3753_b200.robust import AlignmentProblem, align_ist_solve, align_palm_solve
+    from paper_1007_3753_b200.robust import (AlignmentProblem, align_homotopy_solve, align_ist_solve,
+                                             align_palm_solve)
     c = CASES[name]
     gold = np.load(GOLD)
     B, b = align_instance(**c["recipe"])
     prob = AlignmentProblem(B, b)
-    cfg = SolverConfig(tol=c["tol"], max_iter=c["max_iter"], options=c.get("options", {}))
+    cfg = SolverConfig(tol=c["tol"], max_iter=c["max_iter"], options=c.get("options", {}),
+                       lam=c.get("lam") if c["solver"] == "homotopy" else None)
     if c["solver"] == "palm":
         w, e = align_palm_solve(prob, cfg)
+    elif c["solver"] == "homotopy":
+        w, e = align_homotopy_solve(prob, cfg)
     else:
         w, e = align_ist_solve(prob, c.get("lam"), cfg)
     assert _rel(w, gold[name + "_w"]) <= 1e-6
@@ -44,7 +48,7 @@ def test_align_matches_reference(name):
     assert set(np.nonzero(np.abs(e) > 1e-3 * top)[0]) == set(np.nonzero(np.abs(gold[name + "_e"]) > 1e-3 * top)[0])
 
 
-@pytest.mark.parametrize("solver", ["palm", "ist"])
+@pytest.mark.parametrize("solver", ["palm", "ist", "homotopy"])
 def test_batch_equals_single_images(solver):
     _cuda()
     from paper_1007_3753_b200.model import SolverConfig
@@ -55,12 +59,16 @@ def test_batch_equals_single_images(solver):
     cfg = SolverConfig(tol=1e-8, max_iter=5000)
     if solver == "palm":
         W, E = robust.align_palm_solve_batch(Bs, bs, cfg)
+    elif solver == "homotopy":
+        W, E = robust.align_homotopy_solve_batch(Bs, bs, cfg)
     else:
         W, E = robust.align_ist_solve_batch(Bs, bs, None, cfg)
     for j, (B, b) in enumerate(insts):
         prob = robust.AlignmentProblem(B, b)
         if solver == "palm":
             w, e = robust.align_palm_solve(prob, cfg)
+        elif solver == "homotopy":
+            w, e = robust.align_homotopy_solve(prob, cfg)
         else:
             w, e = robust.align_ist_solve(prob, None, cfg)
         assert np.array_equal(W[j], w) and np.array_equal(E[j], e)
