@@ -427,7 +427,7 @@ typedef struct {
   int64_t ld_rhs;
   double tol;
   double mu0, rho;      /* PALM (robust.py:487-490) */
-  double lam;           /* IST / homotopy: <= 0 -> 1e-2 * peak least-squares residual (robust.py:270-273, 391) */
+  double lam;           /* IST / homotopy / gp: <= 0 -> 1e-2 * peak least-squares residual (robust.py:270-273, 391) */
   const double* v0;     /* IST: 4 normalised power-iteration start vectors (4 x m) */
   double* w;
   double* e;
@@ -440,6 +440,9 @@ int ell1_align_palm_batch(const ell1_align_t* A, void* stream);
 int ell1_align_ist_batch(const ell1_align_t* A, void* stream);
 /* align_homotopy_solve per image (robust.py:374-424); lam = target weight (<= 0: 1e-2 peak residual) */
 int ell1_align_homotopy_batch(const ell1_align_t* A, void* stream);
+/* align_gp_solve per image (robust.py:276-371); status ELL1_ILL_CONDITIONED (reduced system not PD),
+ * ELL1_BREAKDOWN (line search exhausted), ELL1_LAMBDA_NONPOS */
+int ell1_align_gp_batch(const ell1_align_t* A, void* stream);
 
 /* fp32 GEMM path of the batched solvers (3: 3xTF32 tcgen05 kernel, the default;
  * 2: 3xTF32 split over cuBLAS TF32 GEMMs, ELL1_FP32_GEMM=tf32x3; 0: SIMT SGEMM,

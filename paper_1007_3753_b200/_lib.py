@@ -224,6 +224,7 @@ _SIGS = {
     "ell1_align_palm_batch": (ctypes.c_int, [P(Align), ctypes.c_void_p]),
     "ell1_align_ist_batch": (ctypes.c_int, [P(Align), ctypes.c_void_p]),
     "ell1_align_homotopy_batch": (ctypes.c_int, [P(Align), ctypes.c_void_p]),
+    "ell1_align_gp_batch": (ctypes.c_int, [P(Align), ctypes.c_void_p]),
     "ell1_gemm_f32_workspace": (ctypes.c_size_t, [ctypes.c_int32, ctypes.c_int64, ctypes.c_int64]),
     "ell1_gemm_f32": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                      ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,

@@ -10,9 +10,9 @@ formats and exit codes — with every solve running on the device:
 * exit codes: 0 success, 1 solver did not meet its convergence test
   (results still written) or broke down numerically, 2 usage error.
 
-Subcommands: solve, gen, cab, phase, noise-sweep, align (palm / ist /
-homotopy) (cli.py:137-350).  SVG rendering (`report`, --svg) and `align
---algo gp` are not part of this backend and exit 2 with a diagnostic.
+Subcommands: solve, gen, cab, phase, noise-sweep, align (cli.py:137-350).
+SVG rendering (`report`, --svg) is not part of this backend and exits 2
+with a diagnostic.
 
     python -m paper_1007_3753_b200.cli solve --algo fista --matrix A.csv --rhs b.csv --out r.json
 """
@@ -258,12 +258,9 @@ def cmd_align(args):
     """cli.py:298-350: tall regression with sparse gross errors (PALM / IST on
     the device; iteration counts are not part of the alignment contract, so
     convergence is certified after the fact as in the reference)."""
-    from paper_1007_3753_b200.robust import (AlignmentProblem, align_homotopy_solve, align_ist_solve,
-                                             align_palm_solve)
+    from paper_1007_3753_b200.robust import (AlignmentProblem, align_gp_solve, align_homotopy_solve,
+                                             align_ist_solve, align_palm_solve)
     import time
-    if args.algo not in ("palm", "ist", "homotopy"):
-        raise UsageError("align --algo %s is not provided by the B200 backend (palm, ist, homotopy are)"
-                         % args.algo)
     B = read_csv(args.basis, "basis")
     b = read_vector(args.rhs, "rhs")
     same_rows("basis", B.shape, "rhs", b.size)
@@ -277,6 +274,8 @@ def cmd_align(args):
         w, e = align_palm_solve(prob, cfg)
     elif args.algo == "homotopy":
         w, e = align_homotopy_solve(prob, cfg)
+    elif args.algo == "gp":
+        w, e = align_gp_solve(prob, args.lam, cfg)
     else:
         w, e = align_ist_solve(prob, args.lam, cfg)
     wall = time.perf_counter() - t0

@@ -460,6 +460,280 @@ __global__ void __launch_bounds__(AT) align_homotopy_kernel(const ell1_align_t a
   }
 }
 
+// ---------------------------------------------------------------- barrier Newton (gp)
+// robust.py:276-371: log-barrier walk of the central path in (w, e, u) with
+// -u <= e <= u; the bound and error blocks are eliminated so each Newton step
+// factors one m x m weighted Gram B^T diag(weight) B; Armijo backtracking
+// (<= 50 halvings, slope 0.01); t x 10 when the decrement^2 <= 1/4; exit
+// through the polished iterate (e truncated at 1e-7 max|e|, w re-solved).
+__device__ __forceinline__ double block_sum1(AlignSh& S, double v) {
+  block_sum(S, &v, 1);
+  return S.out[0];
+}
+
+// upper Cholesky of the weighted Gram B^T diag(wt) B into S.R; false if not PD
+__device__ bool weighted_gram_factor(AlignSh& S, const double* Bs, int d, int m, const double (&wt)[RPT]) {
+  for (int c = 0; c < m; ++c) {
+    double p[MAXM];
+    for (int k = c; k < m; ++k) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        const int i = threadIdx.x + q * AT;
+        if (i < d) s = fma(Bs[(int64_t)c * (d + 1) + i] * wt[q], Bs[(int64_t)k * (d + 1) + i], s);
+      }
+      p[k - c] = s;
+    }
+    block_sum(S, p, m - c);
+    if ((int)threadIdx.x < m - c) S.R[c][c + threadIdx.x] = S.out[threadIdx.x];
+    __syncthreads();
+  }
+  if (threadIdx.x < 32) {
+    const int l = threadIdx.x;
+    int bad = 0;
+    for (int i = 0; i < m; ++i) {
+      double piv = S.R[i][i];
+      for (int k = 0; k < i; ++k) piv -= S.R[k][i] * S.R[k][i];
+      if (!(piv > 0.0)) { bad = 1; break; }
+      const double rii = sqrt(piv);
+      __syncwarp();
+      if (l > i && l < m) {
+        double v = S.R[i][l];
+        for (int k = 0; k < i; ++k) v -= S.R[k][i] * S.R[k][l];
+        S.R[i][l] = v / rii;
+      }
+      __syncwarp();
+      if (l == 0) S.R[i][i] = rii;
+      __syncwarp();
+    }
+    if (l == 0) S.flag = bad;
+  }
+  __syncthreads();
+  return !S.flag;
+}
+
+__global__ void __launch_bounds__(AT) align_gp_kernel(const ell1_align_t a) {
+  extern __shared__ double Bs[];
+  __shared__ AlignSh S;
+  __shared__ double R0[MAXM][MAXM];        // factor of B^T B (the step factor reuses S.R)
+  __shared__ double wv[MAXM], dw[MAXM];
+  const int d = a.d, m = a.m;
+  for (int j = blockIdx.x; j < a.count; j += gridDim.x) {
+    double b[RPT], e[RPT], u[RPT], r[RPT];
+    if (!setup(S, Bs, a, j, b)) continue;
+    for (int t = threadIdx.x; t < MAXM * MAXM; t += AT) R0[t / MAXM][t % MAXM] = S.R[t / MAXM][t % MAXM];
+    __syncthreads();
+    auto use_gram = [&]() {
+      for (int t = threadIdx.x; t < MAXM * MAXM; t += AT) S.R[t / MAXM][t % MAXM] = R0[t / MAXM][t % MAXM];
+      __syncthreads();
+    };
+    // B w for this thread's rows from a shared m-vector
+    auto bmul = [&](const double* vec, double (&out)[RPT]) {
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        const int i = threadIdx.x + q * AT;
+        double s2 = 0.0;
+        if (i < d)
+          for (int k = 0; k < m; ++k) s2 = fma(Bs[(int64_t)k * (d + 1) + i], vec[k], s2);
+        out[q] = s2;
+      }
+    };
+    double tmp[RPT];
+    // lambda default: 1e-2 max|b - B w0| (robust.py:270-273)
+    bt_times(S, Bs, d, m, b);
+    gram_solve(S, m);
+    if ((int)threadIdx.x < m) wv[threadIdx.x] = S.w[threadIdx.x];
+    __syncthreads();
+    double lam = a.lam;
+    double bmax = 0.0;
+    {
+      bmul(wv, tmp);
+      double mx = 0.0;
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        const int i = threadIdx.x + q * AT;
+        if (i < d) { mx = nmax(mx, fabs(b[q] - tmp[q])); bmax = nmax(bmax, fabs(b[q])); }
+      }
+      block_min2(S, -mx, -bmax);
+      if (!(lam > 0.0)) lam = 1e-2 * (-S.out[0]);
+      bmax = -S.out[1];
+    }
+    int status = ELL1_OK, it = 0;
+    // polished(e): truncate |e| <= 1e-7 max|e|, w = gram.solve(B^T (b - e_t)); returns kkt <= tol lam
+    auto polish = [&](double (&et)[RPT]) -> bool {
+      double mx = 0.0;
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) mx = nmax(mx, fabs(e[q]));
+      block_min2(S, -mx, 0.0);
+      const double top = -S.out[0];
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        et[q] = (top > 0.0 && fabs(e[q]) <= 1e-7 * top) ? 0.0 : e[q];
+        tmp[q] = b[q] - et[q];
+      }
+      use_gram();
+      bt_times(S, Bs, d, m, tmp);
+      gram_solve(S, m);
+      double kk = 0.0;
+      bmul(S.w, tmp);
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        const int i = threadIdx.x + q * AT;
+        if (i < d) {
+          const double c = b[q] - tmp[q] - et[q];
+          const double viol = et[q] != 0.0 ? fabs(c - lam * (et[q] > 0.0 ? 1.0 : -1.0)) : fabs(c) - lam;
+          kk = nmax(kk, viol);
+        }
+      }
+      block_min2(S, -kk, 0.0);
+      return nmax(-S.out[0], 0.0) <= a.tol * lam;
+    };
+    double et[RPT];
+    bool done = false;
+    if (!(lam > 0.0)) {
+      status = ELL1_LAMBDA_NONPOS;
+    } else {
+      double t = 1.0 / lam;
+      const double u0 = bmax > 1.0 ? bmax : 1.0;
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) { e[q] = 0.0; u[q] = u0; }
+      for (; it < a.max_iter; ++it) {
+        bmul(wv, tmp);
+        double rr = 0.0, ae = 0.0;
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+          const int i = threadIdx.x + q * AT;
+          r[q] = i < d ? b[q] - tmp[q] - e[q] : 0.0;
+          rr = fma(r[q], r[q], rr);
+          ae += fabs(e[q]);
+        }
+        double v2[2] = {rr, ae};
+        block_sum(S, v2, 2);
+        const double rr_all = S.out[0];
+        const double obj = 0.5 * rr_all + lam * S.out[1];
+        if (2.0 * d / t <= a.tol * (1.0 + obj)) {
+          if (polish(et)) { done = true; break; }
+        }
+        // Newton system (robust.py:307-330)
+        double g_e[RPT], g_u[RPT], dsum[RPT], ddiff[RPT], rhs_e[RPT], den[RPT], wt[RPT], up[RPT], um[RPT];
+        double lsum = 0.0, usum = 0.0;
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+          const int i = threadIdx.x + q * AT;
+          if (i < d) {
+            up[q] = u[q] + e[q];
+            um[q] = u[q] - e[q];
+            const double p = 1.0 / up[q], qq_ = 1.0 / um[q];
+            g_e[q] = -t * r[q] + (qq_ - p);
+            g_u[q] = t * lam - p - qq_;
+            const double pp = p * p, qq = qq_ * qq_;
+            dsum[q] = pp + qq;
+            ddiff[q] = pp - qq;
+            const double dred = 4.0 * pp * qq / dsum[q];
+            rhs_e[q] = -g_e[q] + ddiff[q] * (g_u[q] / dsum[q]);
+            den[q] = t + dred;
+            wt[q] = t * dred / den[q];
+            lsum += log(up[q]) + log(um[q]);
+            usum += u[q];
+          } else {
+            up[q] = um[q] = 1.0; g_e[q] = g_u[q] = dsum[q] = ddiff[q] = rhs_e[q] = 0.0; den[q] = 1.0; wt[q] = 0.0;
+          }
+        }
+        // g_w = -t B^T r
+        bt_times(S, Bs, d, m, r);
+        double gw[MAXM];
+        for (int c = 0; c < m; ++c) gw[c] = -t * S.out[c];
+        // rhs_w = -g_w - t B^T (rhs_e / den)
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) tmp[q] = rhs_e[q] / den[q];
+        bt_times(S, Bs, d, m, tmp);
+        double rw[MAXM];
+        for (int c = 0; c < m; ++c) rw[c] = -gw[c] - t * S.out[c];
+        if (!weighted_gram_factor(S, Bs, d, m, wt)) { status = ELL1_ILL_CONDITIONED; break; }
+        if ((int)threadIdx.x < m) S.out[threadIdx.x] = rw[threadIdx.x];
+        __syncthreads();
+        gram_solve(S, m);                                  // dw = step_fac.solve(...)
+        if ((int)threadIdx.x < m) dw[threadIdx.x] = S.w[threadIdx.x];
+        __syncthreads();
+        double bdw[RPT], de[RPT], du[RPT];
+        bmul(dw, bdw);
+        double dec = 0.0, smin[2] = {1.0, 1.0};
+        // 0.99 min(up/-dup) over dup < 0, same for um (fraction to the boundary)
+        double f1 = __longlong_as_double(0x7ff0000000000000LL), f2 = f1;
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+          const int i = threadIdx.x + q * AT;
+          if (i < d) {
+            de[q] = (rhs_e[q] - t * bdw[q]) / den[q];
+            du[q] = -(g_u[q] + ddiff[q] * de[q]) / dsum[q];
+            dec += g_e[q] * de[q] + g_u[q] * du[q];
+            const double dup = du[q] + de[q], dum = du[q] - de[q];
+            if (dup < 0.0) f1 = fmin(f1, up[q] / -dup);
+            if (dum < 0.0) f2 = fmin(f2, um[q] / -dum);
+          } else {
+            de[q] = du[q] = 0.0;
+          }
+        }
+        (void)smin;
+        double v3[3] = {dec, lsum, usum};
+        block_sum(S, v3, 3);
+        double gwdw = 0.0;
+        for (int c = 0; c < m; ++c) gwdw = fma(gw[c], dw[c], gwdw);
+        const double decrement_sq = -(gwdw + S.out[0]);
+        const double F_t = t * (0.5 * rr_all + lam * S.out[2]) - S.out[1];
+        block_min2(S, f1, f2);
+        double sstep = 1.0;
+        if (S.out[0] < __longlong_as_double(0x7ff0000000000000LL)) sstep = fmin(sstep, 0.99 * S.out[0]);
+        if (S.out[1] < __longlong_as_double(0x7ff0000000000000LL)) sstep = fmin(sstep, 0.99 * S.out[1]);
+        // Armijo backtracking (<= 50 halvings, robust.py:346-366)
+        bool accepted = false;
+        double en[RPT], un[RPT];
+        for (int h = 0; h <= 50; ++h) {
+          double mn1 = __longlong_as_double(0x7ff0000000000000LL), mn2 = mn1;
+#pragma unroll
+          for (int q = 0; q < RPT; ++q) {
+            const int i = threadIdx.x + q * AT;
+            en[q] = e[q] + sstep * de[q];
+            un[q] = u[q] + sstep * du[q];
+            if (i < d) { mn1 = fmin(mn1, un[q] + en[q]); mn2 = fmin(mn2, un[q] - en[q]); }
+          }
+          block_min2(S, mn1, mn2);
+          if (S.out[0] > 0.0 && S.out[1] > 0.0) {
+            double rn2 = 0.0, us = 0.0, ls = 0.0;
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) {
+              const int i = threadIdx.x + q * AT;
+              if (i < d) {
+                const double rn = r[q] - sstep * bdw[q] - sstep * de[q];
+                rn2 = fma(rn, rn, rn2);
+                us += un[q];
+                ls += log(un[q] + en[q]) + log(un[q] - en[q]);
+              }
+            }
+            double v4[3] = {rn2, us, ls};
+            block_sum(S, v4, 3);
+            const double F_new = t * (0.5 * S.out[0] + lam * S.out[1]) - S.out[2];
+            if (F_new <= F_t - 0.01 * sstep * decrement_sq) { accepted = true; break; }
+          }
+          sstep *= 0.5;
+        }
+        if (!accepted) { status = ELL1_BREAKDOWN; break; }
+        if ((int)threadIdx.x < m) wv[threadIdx.x] += sstep * dw[threadIdx.x];
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) { e[q] = en[q]; u[q] = un[q]; }
+        __syncthreads();
+        if (decrement_sq <= 0.25) t *= 10.0;
+      }
+      if (status == ELL1_OK && !done) polish(et);           // budget exhausted: polished(e)
+    }
+    if (status == ELL1_OK) {
+      store_out(a, j, S, et);
+    }
+    if (threadIdx.x == 0) { a.status[j] = status; if (a.iterations) a.iterations[j] = it; }
+    __syncthreads();
+  }
+}
+
 int launch_align(int kind, const ell1_align_t* A, void* stream) {
   if (!A || A->count < 0 || A->m < 1 || A->m > MAXM || A->d <= A->m || A->d > AT * RPT || !A->B || !A->rhs ||
       !A->w || !A->e || !A->status || A->ldb < A->m || A->ld_rhs < A->d || A->b_stride < A->ldb * A->d)
@@ -468,10 +742,12 @@ int launch_align(int kind, const ell1_align_t* A, void* stream) {
   if (kind == 1 && !A->v0) return ELL1_ERR_ARG;
   if (A->count == 0) return ELL1_OK;
   const size_t smem = (size_t)(A->d + 1) * A->m * 8;
-  const void* k = kind == 0 ? (const void*)align_palm_kernel
-                 : kind == 1 ? (const void*)align_ist_kernel : (const void*)align_homotopy_kernel;
-  if (smem > 48 * 1024 && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-                              cudaSuccess)
+  const void* k = kind == 0   ? (const void*)align_palm_kernel
+                 : kind == 1 ? (const void*)align_ist_kernel
+                 : kind == 2 ? (const void*)align_homotopy_kernel
+                             : (const void*)align_gp_kernel;
+  // static + dynamic shared memory may pass 48 KB even when the dynamic part does not: always opt in
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return ELL1_ERR_ARG;
   int dev = 0, sms = 148, per = 1;
   cudaGetDevice(&dev);
@@ -482,7 +758,8 @@ int launch_align(int kind, const ell1_align_t* A, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (palm) align_palm_kernel<<<grid, AT, smem, s>>>(*A);
   else if (kind == 1) align_ist_kernel<<<grid, AT, smem, s>>>(*A);
-  else align_homotopy_kernel<<<grid, AT, smem, s>>>(*A);
+  else if (kind == 2) align_homotopy_kernel<<<grid, AT, smem, s>>>(*A);
+  else align_gp_kernel<<<grid, AT, smem, s>>>(*A);
   return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
 }
 
@@ -499,4 +776,8 @@ extern "C" int ell1_align_ist_batch(const ell1_align_t* A, void* stream) {
 
 extern "C" int ell1_align_homotopy_batch(const ell1_align_t* A, void* stream) {
   return ell1::launch_align(2, A, stream);
+}
+
+extern "C" int ell1_align_gp_batch(const ell1_align_t* A, void* stream) {
+  return ell1::launch_align(3, A, stream);
 }

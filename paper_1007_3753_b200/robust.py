@@ -305,14 +305,16 @@ def _align_batch(kind, Bs, bs, config, lam=None):
         a.v0 = v0.data_ptr()
     a.w, a.e, a.status, a.iterations = W.data_ptr(), E.data_ptr(), st.data_ptr(), its.data_ptr()
     fn = {"palm": L.ell1_align_palm_batch, "ist": L.ell1_align_ist_batch,
-          "homotopy": L.ell1_align_homotopy_batch}[kind]
+          "homotopy": L.ell1_align_homotopy_batch, "gp": L.ell1_align_gp_batch}[kind]
     _lib.check(fn(ctypes.byref(a), device.stream_ptr(dev)), "ell1_align_%s_batch" % kind)
     status = st.cpu().numpy()
     if np.any(status == _lib.NOT_PD):                 # robust.py:254-258
         from paper_1007_3753_b200.exceptions import IllConditionedError
         raise IllConditionedError("B must have full column rank")
     for s in np.unique(status):
-        raise_for(int(s), {})
+        raise_for(int(s), {_lib.ILL_CONDITIONED: "reduced alignment system lost definiteness",
+                           _lib.BREAKDOWN: "alignment barrier line search exhausted",
+                           _lib.LAMBDA_NONPOS: "lambda must be positive"})
     return W.cpu().numpy(), E.cpu().numpy(), its.cpu().numpy()
 
 
@@ -368,5 +370,23 @@ def align_homotopy_solve(prob, config):
     a block-coordinate cleanup at the target weight (robust.py:374-424).
     Returns (w, e)."""
     W, E, _ = _align_batch("homotopy", prob.B[None], prob.b[None], config, config.lam)
+    return W[0], E[0]
+
+
+def align_gp_solve_batch(Bs, bs, lam, config):
+    """align_gp_solve for a batch of images; lam=None: per-image default."""
+    if lam is not None and not lam > 0:
+        raise ValueError("lambda must be positive")
+    W, E, _ = _align_batch("gp", Bs, bs, config, lam)
+    return W, E
+
+
+def align_gp_solve(prob, lam, config):
+    """Log-barrier Newton solve of the alignment objective (robust.py:276-371):
+    central path in (w, e, u) with -u <= e <= u, one m x m factorisation per
+    Newton step, polished exit.  Returns (w, e)."""
+    if lam is not None and not lam > 0:
+        raise ValueError("lambda must be positive")
+    W, E, _ = _align_batch("gp", prob.B[None], prob.b[None], config, lam)
     return W[0], E[0]
 

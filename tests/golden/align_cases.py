@@ -30,6 +30,9 @@ CASES = {
                      "lam": 0.02},
     "hom_1024x11": {"solver": "homotopy", "recipe": dict(seed=10, d=1024, m=11, frac=0.2), "tol": 1e-8,
                     "max_iter": 5000},
+    "gp_120x11": {"solver": "gp", "recipe": dict(seed=11, d=120, m=11), "tol": 1e-8, "max_iter": 200},
+    "gp_60x7_lam": {"solver": "gp", "recipe": dict(seed=12, d=60, m=7), "tol": 1e-9, "max_iter": 200, "lam": 0.1},
+    "gp_512x8": {"solver": "gp", "recipe": dict(seed=13, d=512, m=8, frac=0.15), "tol": 1e-8, "max_iter": 200},
     "ist_120x11_lam": {"solver": "ist", "recipe": dict(seed=7, d=120, m=11), "tol": 1e-8, "max_iter": 20000,
                        "lam": 0.05},
 }

@@ -19,7 +19,8 @@ from tests.golden.align_cases import CASES, align_instance  # noqa: E402
 
 def main():
     from ell1.model import SolverConfig
-    from ell1.robust import AlignmentProblem, align_homotopy_solve, align_ist_solve, align_palm_solve
+    from ell1.robust import (AlignmentProblem, align_gp_solve, align_homotopy_solve, align_ist_solve,
+                             align_palm_solve)
     out = {}
     for name, c in CASES.items():
         B, b = align_instance(**c["recipe"])
@@ -30,6 +31,8 @@ def main():
             w, e = align_palm_solve(prob, cfg)
         elif c["solver"] == "homotopy":
             w, e = align_homotopy_solve(prob, cfg)
+        elif c["solver"] == "gp":
+            w, e = align_gp_solve(prob, c.get("lam"), cfg)
         else:
             w, e = align_ist_solve(prob, c.get("lam"), cfg)
         out[name + "_w"] = w

@@ -40,6 +40,8 @@ ALIGN_RUNS = [
                    "--tol", "1e-7", "--max-iter", "20000", "--out", "align_ist.json"]),
     ("align_homotopy", ["align", "--algo", "homotopy", "--basis", "B.csv", "--rhs", "balign.csv",
                         "--out", "align_homotopy.json"]),
+    ("align_gp", ["align", "--algo", "gp", "--basis", "B.csv", "--rhs", "balign.csv", "--max-iter", "200",
+                  "--out", "align_gp.json"]),
 ]
 
 

@@ -28,8 +28,8 @@ def _rel(x, ref):
 def test_align_matches_reference(name):
     _cuda()
     from paper_1007_3753_b200.model import SolverConfig
-    from paper_1007_3753_b200.robust import (AlignmentProblem, align_homotopy_solve, align_ist_solve,
-                                             align_palm_solve)
+    from paper_1007_3753_b200.robust import (AlignmentProblem, align_gp_solve, align_homotopy_solve,
+                                             align_ist_solve, align_palm_solve)
     c = CASES[name]
     gold = np.load(GOLD)
     B, b = align_instance(**c["recipe"])
@@ -40,6 +40,8 @@ def test_align_matches_reference(name):
         w, e = align_palm_solve(prob, cfg)
     elif c["solver"] == "homotopy":
         w, e = align_homotopy_solve(prob, cfg)
+    elif c["solver"] == "gp":
+        w, e = align_gp_solve(prob, c.get("lam"), cfg)
     else:
         w, e = align_ist_solve(prob, c.get("lam"), cfg)
     assert _rel(w, gold[name + "_w"]) <= 1e-6
@@ -48,7 +50,7 @@ def test_align_matches_reference(name):
     assert set(np.nonzero(np.abs(e) > 1e-3 * top)[0]) == set(np.nonzero(np.abs(gold[name + "_e"]) > 1e-3 * top)[0])
 
 
-@pytest.mark.parametrize("solver", ["palm", "ist", "homotopy"])
+@pytest.mark.parametrize("solver", ["palm", "ist", "homotopy", "gp"])
 def test_batch_equals_single_images(solver):
     _cuda()
     from paper_1007_3753_b200.model import SolverConfig
@@ -61,6 +63,8 @@ def test_batch_equals_single_images(solver):
         W, E = robust.align_palm_solve_batch(Bs, bs, cfg)
     elif solver == "homotopy":
         W, E = robust.align_homotopy_solve_batch(Bs, bs, cfg)
+    elif solver == "gp":
+        W, E = robust.align_gp_solve_batch(Bs, bs, None, cfg)
     else:
         W, E = robust.align_ist_solve_batch(Bs, bs, None, cfg)
     for j, (B, b) in enumerate(insts):
@@ -69,6 +73,8 @@ def test_batch_equals_single_images(solver):
             w, e = robust.align_palm_solve(prob, cfg)
         elif solver == "homotopy":
             w, e = robust.align_homotopy_solve(prob, cfg)
+        elif solver == "gp":
+            w, e = robust.align_gp_solve(prob, None, cfg)
         else:
             w, e = robust.align_ist_solve(prob, None, cfg)
         assert np.array_equal(W[j], w) and np.array_equal(E[j], e)
@@ -86,6 +92,9 @@ def test_rank_deficient_basis_raises():
         align_palm_solve(prob, SolverConfig())
     with pytest.raises(IllConditionedError):
         align_ist_solve(prob, 0.1, SolverConfig())
+    from paper_1007_3753_b200.robust import align_gp_solve
+    with pytest.raises(IllConditionedError):
+        align_gp_solve(prob, 0.1, SolverConfig())
 
 
 def test_zero_data_and_option_validation():
