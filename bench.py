@@ -597,6 +597,18 @@ def leg_align(torch, count=4096, d=1024, m=11, cpu_sample=24):
     e.record()
     torch.cuda.synchronize()
     t = s.elapsed_time(e) / 1e3
+    # the same batch with the images already resident (device throughput of the kernel)
+    Bd = torch.from_numpy(Bs).cuda()
+    bd = torch.from_numpy(bs).cuda()
+    robust.align_batch_device("palm", Bd[:64], bd[:64], cfg)
+    torch.cuda.synchronize()
+    s2, e2 = _events(torch)
+    s2.record()
+    W2, _, its = robust.align_batch_device("palm", Bd, bd, cfg)
+    e2.record()
+    torch.cuda.synchronize()
+    td = s2.elapsed_time(e2) / 1e3
+    its = its.cpu().numpy()
     from oracle.l1_oracle import align_palm
     t0 = time.perf_counter()
     worst = 0.0
@@ -607,6 +619,9 @@ def leg_align(torch, count=4096, d=1024, m=11, cpu_sample=24):
     return {"workload": "PALM alignment, %d images, d=%d pixels, m=%d parameters, 20%% corrupted rows, "
                         "tol 1e-8 (public call: host images in, host w/e out)" % (count, d, m),
             "images_per_sec": count / t, "ms_per_batch": 1e3 * t,
+            "device_images_per_sec": count / td, "device_ms_per_batch": 1e3 * td,
+            "mean_palm_steps": float(its.mean()),
+            "bitwise_equal_resident_vs_host_call": bool(np.array_equal(W2.cpu().numpy(), W)),
             "cpu_port_images_per_sec": cpu_sample / tc, "cpu_sample": "%d images, 1 process" % cpu_sample,
             "max_rel_err_w_vs_port": worst}
 

@@ -262,26 +262,27 @@ class AlignmentProblem:
         return self.B.shape[1]
 
 
-def _align_batch(kind, Bs, bs, config, lam=None):
-    """Run one batched alignment launch.  Bs: (count, d, m), bs: (count, d).
-    Returns (W (count, m), E (count, d), iterations (count,))."""
+def align_batch_device(kind, Bd, bd, config, lam=None, v0=None):
+    """Batched alignment on device-resident images (new; e.g. images coming
+    from a GPU pipeline).  Bd: CUDA float64 (count, d, m) row-major images,
+    bd: (count, d).  kind: "palm" | "ist" | "homotopy" | "gp".  Returns device
+    tensors (W (count, m), E (count, d), iterations (count,)) without syncing;
+    raises on a failed image after reading the statuses back."""
     import ctypes
     from paper_1007_3753_b200 import _lib
     from paper_1007_3753_b200._runner import raise_for
     torch = device._torch()
     L = _lib.lib()
-    Bs = np.asarray(Bs, dtype=np.float64)
-    bs = np.asarray(bs, dtype=np.float64)
-    if Bs.ndim != 3 or bs.ndim != 2 or bs.shape != Bs.shape[:2]:
+    if Bd.ndim != 3 or bd.ndim != 2 or tuple(bd.shape) != tuple(Bd.shape[:2]):
         raise ValueError("need B of shape (count, d, m) and b of shape (count, d)")
-    count, d, m = Bs.shape
+    count, d, m = (int(x) for x in Bd.shape)
     if d <= m:
         raise ValueError("B must be tall: more rows than columns")
     if m > 32 or d > 2048:
         raise ValueError("batched alignment supports m <= 32 parameters and d <= 2048 rows")
-    dev = device.current_device(config.opt("device", None))
-    Bd = torch.from_numpy(np.ascontiguousarray(Bs)).to(dev)      # row-major images, as given
-    bd = torch.from_numpy(np.ascontiguousarray(bs)).to(dev)
+    dev = Bd.device
+    Bd = Bd.to(torch.float64).contiguous()
+    bd = bd.to(device=dev, dtype=torch.float64).contiguous()
     W = torch.empty((count, m), dtype=torch.float64, device=dev)
     E = torch.empty((count, d), dtype=torch.float64, device=dev)
     st = torch.full((count,), -1, dtype=torch.int32, device=dev)
@@ -294,19 +295,27 @@ def _align_batch(kind, Bs, bs, config, lam=None):
     a.mu0 = float(config.opt("mu0", 1.0))
     a.rho = float(config.opt("rho", 2.0))
     a.lam = -1.0 if lam is None else float(lam)
-    v0 = None
     if kind == "ist":
-        rng = np.random.default_rng(_POWER_SEED)      # spectral_norm_sq's start vector + redraws
-        draws = []
-        for _ in range(4):
-            v = rng.standard_normal(m)
-            draws.append(v / np.linalg.norm(v))
-        v0 = torch.from_numpy(np.concatenate(draws)).to(dev)
+        if v0 is None:
+            rng = np.random.default_rng(_POWER_SEED)      # spectral_norm_sq's start vector + redraws
+            draws = []
+            for _ in range(4):
+                v = rng.standard_normal(m)
+                draws.append(v / np.linalg.norm(v))
+            v0 = torch.from_numpy(np.concatenate(draws)).to(dev)
         a.v0 = v0.data_ptr()
     a.w, a.e, a.status, a.iterations = W.data_ptr(), E.data_ptr(), st.data_ptr(), its.data_ptr()
     fn = {"palm": L.ell1_align_palm_batch, "ist": L.ell1_align_ist_batch,
           "homotopy": L.ell1_align_homotopy_batch, "gp": L.ell1_align_gp_batch}[kind]
     _lib.check(fn(ctypes.byref(a), device.stream_ptr(dev)), "ell1_align_%s_batch" % kind)
+    W._ell1_keep = (Bd, bd, v0, st)                       # operands live until the caller syncs
+    W._ell1_status = st
+    return W, E, its
+
+
+def _check_align_status(st):
+    from paper_1007_3753_b200 import _lib
+    from paper_1007_3753_b200._runner import raise_for
     status = st.cpu().numpy()
     if np.any(status == _lib.NOT_PD):                 # robust.py:254-258
         from paper_1007_3753_b200.exceptions import IllConditionedError
@@ -315,6 +324,21 @@ def _align_batch(kind, Bs, bs, config, lam=None):
         raise_for(int(s), {_lib.ILL_CONDITIONED: "reduced alignment system lost definiteness",
                            _lib.BREAKDOWN: "alignment barrier line search exhausted",
                            _lib.LAMBDA_NONPOS: "lambda must be positive"})
+
+
+def _align_batch(kind, Bs, bs, config, lam=None):
+    """One batched alignment from host arrays.  Bs: (count, d, m), bs: (count, d).
+    Returns host (W (count, m), E (count, d), iterations (count,))."""
+    torch = device._torch()
+    Bs = np.asarray(Bs, dtype=np.float64)
+    bs = np.asarray(bs, dtype=np.float64)
+    if Bs.ndim != 3 or bs.ndim != 2 or bs.shape != Bs.shape[:2]:
+        raise ValueError("need B of shape (count, d, m) and b of shape (count, d)")
+    dev = device.current_device(config.opt("device", None))
+    Bd = torch.from_numpy(np.ascontiguousarray(Bs)).to(dev)      # row-major images, as given
+    bd = torch.from_numpy(np.ascontiguousarray(bs)).to(dev)
+    W, E, its = align_batch_device(kind, Bd, bd, config, lam)
+    _check_align_status(W._ell1_status)
     return W.cpu().numpy(), E.cpu().numpy(), its.cpu().numpy()
 
 
