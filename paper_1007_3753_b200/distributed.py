@@ -102,3 +102,22 @@ def src_classify_sharded(classify, A, class_labels, Bmat, config, group=None, de
     lab = _gather_rows(np.asarray(labels, np.int64), B, world, group, device)
     res = _gather_rows(np.asarray(resid, np.float64), B, world, group, device)
     return lab.astype(np.int32), res
+
+
+def align_batch_sharded(solve, Bs, bs, config, group=None, device=None, **kw):
+    """Alignment images split across ranks (SURVEY §8(f) rank 4 on §8(e)'s
+    batch sharding): ``solve`` is robust.align_*_solve_batch, Bs (count, d, m),
+    bs (count, d); every rank gets (W, E) for all images in the original order."""
+    Bs = np.asarray(Bs, dtype=np.float64)
+    bs = np.asarray(bs, dtype=np.float64)
+    count = Bs.shape[0]
+    world, rank = _world(group)
+    idx = shard_indices(count, rank, world)
+    W, E = solve(np.ascontiguousarray(Bs[idx]), np.ascontiguousarray(bs[idx]), config, **kw)
+    if world == 1:
+        return W, E
+    if device is None:
+        import torch
+        device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else "cpu"
+    return (_gather_rows(np.asarray(W), count, world, group, device),
+            _gather_rows(np.asarray(E), count, world, group, device))

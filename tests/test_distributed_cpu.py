@@ -36,6 +36,24 @@ def _oracle_classify(A, labels, Bsub, config):
     return lab, res, None
 
 
+def _oracle_align(Bs, bs, config):
+    """Test stand-in for robust.align_palm_solve_batch on one rank's images."""
+    from oracle.l1_oracle import align_palm
+    ws, es = [], []
+    for B, b in zip(Bs, bs):
+        w, e = align_palm(B, b, tol=config["tol"])
+        ws.append(w)
+        es.append(e)
+    m, d = Bs.shape[2], Bs.shape[1]
+    return (np.stack(ws) if ws else np.zeros((0, m))), (np.stack(es) if es else np.zeros((0, d)))
+
+
+def _align_problem():
+    from tests.golden.align_cases import align_instance
+    insts = [align_instance(seed=50 + j, d=30, m=3) for j in range(7)]
+    return np.stack([B for B, _ in insts]), np.stack([b for _, b in insts])
+
+
 def _problem():
     A = oracle.gaussian_dict(30, 60, 3)
     rng = np.random.default_rng(4)
@@ -53,7 +71,7 @@ def _free_port():
 
 def _worker(rank, world, port, out_dir):
     import torch.distributed as dist
-    from paper_1007_3753_b200.distributed import solve_batch_sharded, src_classify_sharded
+    from paper_1007_3753_b200.distributed import align_batch_sharded, solve_batch_sharded, src_classify_sharded
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -61,8 +79,10 @@ def _worker(rank, world, port, out_dir):
         A, Bm = _problem()
         res = solve_batch_sharded(_oracle_batch, A, Bm, {"lam": 1e-3}, device="cpu")
         lab, cres = src_classify_sharded(_oracle_classify, A, None, Bm, None, device="cpu")
+        Bs, bs = _align_problem()
+        W, E = align_batch_sharded(_oracle_align, Bs, bs, {"tol": 1e-8}, device="cpu")
         np.savez(os.path.join(out_dir, "r%d.npz" % rank), x=res.x, it=res.iterations, conv=res.converged,
-                 lam=res.lam, lab=lab, cres=cres)
+                 lam=res.lam, lab=lab, cres=cres, W=W, E=E)
     finally:
         dist.destroy_process_group()
 
@@ -83,6 +103,7 @@ def test_sharded_batch_gathers_in_order(world):
     A, Bm = _problem()
     full = _oracle_batch(A, Bm, {"lam": 1e-3})
     lab_ref, _, _ = _oracle_classify(A, None, Bm, None)
+    W_ref, E_ref = _oracle_align(*_align_problem(), {"tol": 1e-8})
     with tempfile.TemporaryDirectory() as tmp:
         mp.spawn(_worker, args=(world, _free_port(), tmp), nprocs=world, join=True)
         outs = [dict(np.load(os.path.join(tmp, "r%d.npz" % r))) for r in range(world)]
@@ -91,6 +112,8 @@ def test_sharded_batch_gathers_in_order(world):
         np.testing.assert_array_equal(o["it"], full.iterations)
         np.testing.assert_array_equal(o["conv"], full.converged)
         np.testing.assert_array_equal(o["lab"], lab_ref)
+        np.testing.assert_array_equal(o["W"], W_ref)
+        np.testing.assert_array_equal(o["E"], E_ref)
         # per-rank local indices were gathered back to their global slots
         from paper_1007_3753_b200.distributed import shard_indices
         for r in range(world):
