@@ -10,6 +10,7 @@
 //   ell1_shard_kkt   KKT / support partials of the local columns (model.py:160-173, 227-233)
 // All reductions are deterministic (fixed order); scalar partials are
 // returned per rank for the host driver to combine across ranks.
+#include <cstdlib>
 #include "solvers_common.cuh"
 
 namespace ell1 {
@@ -73,6 +74,160 @@ __global__ void __launch_bounds__(NTHR, 1) gemv_t_kernel(const __grid_constant__
   const double* rs[1] = {a.x};
   double* os[1] = {a.y + E.c0};
   panel_gemv_t<TA, 1>(E, D, PN, rs, os);
+}
+
+// ---- GEMV^T for long fp32 columns (config 4 panels: d = 65536 rows per column)
+// A bulk-copy pipeline instead of register-staged loads: one producer lane
+// streams, per stage, the next RC-row chunk of CB columns (CB bulk copies of
+// RC x 4 bytes) and the matching RC doubles of r into an ST-deep shared-memory
+// ring (mbarrier complete_tx); 16 consumer warps accumulate the CB column dots
+// in fp64 registers (row pairs strided over the consumers) and release the slot.  Each
+// column block ends in one fixed-order block reduction, so the result is
+// deterministic.  3 stages x (16 columns x 1024 rows) = 192 KB of A in flight
+// per SM keeps HBM busy: 7.1 TB/s at d = 65536 (the register-staged engine
+// path holds ~32 KB per SM and reached 4.8 TB/s; 8-column x 4-stage 5.9,
+// 16 x 512-row stages 4.2 — measured with tools/gemv_bench.py).
+namespace gts {
+#ifndef ELL1_GTS_CB
+#define ELL1_GTS_CB 16
+#endif
+#ifndef ELL1_GTS_RC
+#define ELL1_GTS_RC 1024
+#endif
+constexpr int CB = ELL1_GTS_CB;           // columns per block
+constexpr int RC = ELL1_GTS_RC;           // rows per chunk (2 per consumer thread)
+#ifndef ELL1_GTS_ST
+#define ELL1_GTS_ST 3
+#endif
+constexpr int ST = ELL1_GTS_ST;           // ring depth
+constexpr int CW = 16;                    // consumer warps
+constexpr int THREADS = (CW + 1) * 32;    // + producer warp
+constexpr int A_BYTES = CB * RC * 4;
+constexpr int R_BYTES = RC * 8;
+constexpr int STAGE = A_BYTES + R_BYTES;
+constexpr int SMEM = ST * STAGE + 2 * ST * 8 + CW * CB * 8 + 64;
+}  // namespace gts
+
+__device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__global__ void __launch_bounds__(gts::THREADS, 1)
+    gemv_t_stream_kernel(const float* __restrict__ A, int64_t ld, int64_t d, int64_t n, const double* __restrict__ r,
+                         double* __restrict__ g) {
+  using namespace gts;
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* full = (uint64_t*)(sm + ST * STAGE);
+  uint64_t* empty = full + ST;
+  double* red = (double*)(empty + ST);                  // [CW][CB]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // balanced contiguous column ranges per CTA, in blocks of CB
+  const int64_t nblk = (n + CB - 1) / CB;
+  const int64_t b0 = nblk * blockIdx.x / gridDim.x, b1 = nblk * (blockIdx.x + 1) / gridDim.x;
+  const int nch = (int)((d + RC - 1) / RC);
+  const int64_t total = (b1 - b0) * nch;                  // (block, chunk) steps of this CTA
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(full + s)), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(empty + s)), "r"(CW));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto wait = [](uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
+        "@!p bra W_%=;\n\t}" ::"r"(su32(bar)),
+        "r"(parity)
+        : "memory");
+  };
+  if (warp == CW) {
+    if (lane == 0) {
+      // ---- producer
+      for (int64_t t = 0; t < total; ++t) {
+        const int s = (int)(t % ST);
+        const int64_t u = t / ST;
+        if (u > 0) wait(empty + s, (unsigned)((u - 1) & 1));
+        const int64_t blk = b0 + t / nch;
+        const int ch = (int)(t % nch);
+        const int64_t row0 = (int64_t)ch * RC;
+        const int rows = (int)((d - row0) < RC ? (d - row0) : RC);
+        const int64_t c0 = blk * CB;
+        const int cols = (int)((n - c0) < CB ? (n - c0) : CB);
+        unsigned char* st = sm + (size_t)s * STAGE;
+        const unsigned bytes = (unsigned)(cols * rows * 4 + rows * 8);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full + s)), "r"(bytes)
+                     : "memory");
+        for (int c = 0; c < cols; ++c)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  su32(st + (size_t)c * RC * 4)),
+              "l"(A + (c0 + c) * ld + row0), "r"(rows * 4), "r"(su32(full + s))
+              : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         su32(st + A_BYTES)),
+                     "l"(r + row0), "r"(rows * 8), "r"(su32(full + s))
+                     : "memory");
+      }
+    }
+    return;
+  }
+  // ---- consumers: thread t owns rows 2t, 2t+1 of every chunk
+  const int tc = threadIdx.x;                           // 0 .. CW*32-1
+  double acc[CB];
+  for (int64_t t = 0; t < total; ++t) {
+    const int s = (int)(t % ST);
+    const int64_t u = t / ST;
+    const int ch = (int)(t % nch);
+    const int64_t blk = b0 + t / nch;
+    const int64_t row0 = (int64_t)ch * RC;
+    const int rows = (int)((d - row0) < RC ? (d - row0) : RC);
+    const int64_t c0 = blk * CB;
+    const int cols = (int)((n - c0) < CB ? (n - c0) : CB);
+    if (ch == 0)
+#pragma unroll
+      for (int c = 0; c < CB; ++c) acc[c] = 0.0;
+    wait(full + s, (unsigned)(u & 1));
+    const unsigned char* st = sm + (size_t)s * STAGE;
+    for (int i = 2 * tc; i < rows; i += 2 * CW * 32) {
+      const double2 rv = *reinterpret_cast<const double2*>(st + A_BYTES + (size_t)i * 8);
+#pragma unroll
+      for (int c = 0; c < CB; ++c) {
+        if (c < cols) {
+          const float2 av = *reinterpret_cast<const float2*>(st + ((size_t)c * RC + i) * 4);
+          acc[c] = fma((double)av.x, rv.x, acc[c]);
+          acc[c] = fma((double)av.y, rv.y, acc[c]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(empty + s)) : "memory");
+    if (ch == nch - 1) {
+      // column block done: fixed-order reduction (lanes -> xor tree, then warps in order)
+#pragma unroll
+      for (int c = 0; c < CB; ++c) {
+        double v = acc[c];
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[warp * CB + c] = v;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(CW * 32) : "memory");
+      if (tc < cols) {
+        double v = red[tc];
+        for (int w = 1; w < CW; ++w) v += red[w * CB + tc];
+        g[c0 + tc] = v;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(CW * 32) : "memory");
+    }
+  }
+}
+
+static bool gemv_t_stream_ok(const ell1_dict_t* D) {
+  static int off = -1;
+  if (off < 0) {
+    const char* e = getenv("ELL1_GEMVT_STREAM");
+    off = e && e[0] == '0';
+  }
+  return !off && D->dtype == ELL1_F32 && !D->ext && D->d >= 4096 && D->d % 32 == 0 && D->ld % 4 == 0;
 }
 
 // ---- elementwise + partial-sum kernels (grid-stride, CTA partials, then one CTA folds)
@@ -194,6 +349,21 @@ extern "C" int ell1_gemv(const ell1_dict_t* D, const double* x, double* y, void*
 
 extern "C" int ell1_gemv_t(const ell1_dict_t* D, const double* r, double* g, void* ws, size_t wsb, void* stream) {
   if (!dict_ok(D) || !r || !g) return ELL1_ERR_ARG;
+  if (gemv_t_stream_ok(D)) {
+    cudaStream_t s = (cudaStream_t)stream;
+    static bool attr = false;
+    if (!attr) {
+      if (cudaFuncSetAttribute(gemv_t_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gts::SMEM) !=
+          cudaSuccess)
+        return ELL1_ERR_CUDA;
+      attr = true;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    gemv_t_stream_kernel<<<sms, gts::THREADS, gts::SMEM, s>>>((const float*)D->A, D->ld, D->d, D->n, r, g);
+    return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
+  }
   const int nb = pick_blocks(D->n, 0);
   GvArgs a;
   a.D = to_raw(D);
