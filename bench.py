@@ -779,7 +779,7 @@ def run_b200(args):
     torch.cuda.set_device(dev)
     if args.only_leg:
         legs = {"harness": lambda: leg_harness(torch), "cfg1": lambda: leg_cfg1(torch),
-                "align": lambda: leg_align(torch),
+                "align": lambda: leg_align(torch), "cfg4": lambda: leg_cfg4(torch, dev, ws, rank),
                 "cfg3": lambda: leg_cfg3(torch, dev), "cfg5": lambda: leg_cfg5(torch, dev, ws),
                 "cfg5_sweep": lambda: leg_cfg5_sweep(torch, dev),
                 "solvers_cfg2": lambda: leg_solvers_cfg2(torch, make_instance(rank))}

@@ -13,6 +13,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--lib", default=None)
+    ap.add_argument("--full", action="store_true", help="only the config-4 single-GPU shape (64 GiB fp32)")
     args = ap.parse_args()
     from paper_1007_3753_b200 import _lib
     import torch
@@ -25,11 +26,16 @@ def main():
     else:
         L = _lib.lib()
     dev = torch.device("cuda", 0)
-    for (d, n, dt) in [(65536, 32768, torch.float32), (16384, 65536, torch.float32), (4096, 131072, torch.float32),
-                       (1024, 262144, torch.float32), (16384, 32768, torch.float64)]:
+    shapes = [(65536, 32768, torch.float32), (16384, 65536, torch.float32), (4096, 131072, torch.float32),
+              (1024, 262144, torch.float32), (16384, 32768, torch.float64)]
+    if args.full:
+        shapes = [(65536, 262144, torch.float32)]
+    for (d, n, dt) in shapes:
         g = torch.Generator(device=dev)
         g.manual_seed(1)
-        st = torch.randn(n, d, generator=g, device=dev, dtype=dt)
+        st = torch.empty(n, d, device=dev, dtype=dt)
+        for c0 in range(0, n, 8192):                    # chunked: no 2x-size temporaries at 64 GiB
+            st[c0:c0 + 8192].normal_(generator=g)
         D = dv.DeviceDictionary.wrap(st, d)
         v = D.view()
         wsb = L.ell1_gemv_workspace(ctypes.byref(v))
