@@ -351,15 +351,15 @@ extern "C" int ell1_gemv_t(const ell1_dict_t* D, const double* r, double* g, voi
   if (!dict_ok(D) || !r || !g) return ELL1_ERR_ARG;
   if (gemv_t_stream_ok(D)) {
     cudaStream_t s = (cudaStream_t)stream;
-    static bool attr = false;
-    if (!attr) {
+    static unsigned attr = 0;                              // per-device bit
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    if (!(attr >> (dev & 31) & 1u)) {
       if (cudaFuncSetAttribute(gemv_t_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gts::SMEM) !=
           cudaSuccess)
         return ELL1_ERR_CUDA;
-      attr = true;
+      attr |= 1u << (dev & 31);
     }
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     gemv_t_stream_kernel<<<sms, gts::THREADS, gts::SMEM, s>>>((const float*)D->A, D->ld, D->d, D->n, r, g);
     return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
