@@ -149,7 +149,12 @@ __global__ void __launch_bounds__(NTHR, 1) pcg_kernel(const __grid_constant__ Pc
   }
   __syncthreads();
   while (!V.done) {
-    if (V.k >= a.max_iter) {                         // budget: best iterate, not converged
+    // every thread reads the budget before thread 0 advances V.k (a warp that
+    // read the incremented count would leave the loop alone and write the
+    // current iterate for its columns while the others go on)
+    const bool over = V.k >= a.max_iter;
+    __syncthreads();
+    if (over) {                                      // budget: best iterate, not converged
       T0 { V.done = 1; V.use_best = 1; V.res = V.best; V.k = a.max_iter; }
       __syncthreads();
       break;
