@@ -57,6 +57,8 @@ def _gemm(torch, A, B, trans):
     (1024, 700, 2240, True),       # config 3: [M | Ginv] V after compaction
     (512, 1024, 2048, False),      # config 5
     (2048, 300, 512, False),
+    (300, 1, 1001, False),         # single instance left after compaction, odd K
+    (517, 5, 1001, True),          # ragged M, tiny N, odd K
 ])
 def test_tc_gemm_matches_fp64(trans, M, N, K, nonneg):
     torch = pytest.importorskip("torch")
