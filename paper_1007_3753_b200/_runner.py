@@ -77,7 +77,7 @@ class Buffers:
     finished solve is read back with a single device->host copy
     (``read_all``) instead of one synchronising copy per field."""
 
-    SNAP_ROWS = 4096           # trace rows included in the single read-back
+    SNAP_ROWS = 512            # trace rows included in the single read-back (longer traces: one more copy)
 
     def __init__(self, prep, ws_bytes, trace_rows, want_prev=False, want_y=False):
         torch = device._torch()
