@@ -362,27 +362,70 @@ int ell1_src_classify(const ell1_dict_t* D, const double* Bmat, int32_t B, const
                       int64_t ldw, const int32_t* class_offsets, int32_t nclasses, int32_t* labels,
                       double* class_resid, void* stream);
 
-/* ----------------------------------------- column-sharded primitives (config 4)
- * Device building blocks of the multi-GPU FISTA (one rank per GPU, one NCCL
- * allreduce of the d-length partial A x per iteration).  The
- * shard-level scalar partials (out8, 8 doubles) are combined across ranks by
- * the host driver (paper_1007_3753_b200/sharded.py). */
+/* ----------------------------------------- column-sharded FISTA (config 4)
+ * One huge instance, A = [A_0 | ... | A_{G-1}] by columns, one rank per GPU
+ * (SURVEY §8(e)).  Replaces shrinkage.fista_solve (shrinkage.py:231-298) with
+ * its backtracking (_backtrack :199-213), momentum (fista_t_next :184-196),
+ * continuation, KKT (model.kkt_from_correlation, model.py:160-173) and stop
+ * rules (model.check_stop, model.py:176-224), for a dictionary no single
+ * process can hold.
+ *
+ * Control stays on the device.  A solve is a sequence of identical ROUNDS,
+ * each one backtracking trial:
+ *     ell1_sfista_pre   prox x_n = soft(y - g_y/L, lam/L) on the local columns
+ *                       + the rank's scalar partials into its slot of xchg,
+ *                       then xchg[0:d) = A_r x_n (skipped once finished)
+ *     <allreduce(sum) of xchg: ld + 16*world doubles, the ONLY collective>
+ *     ell1_sfista_post  r_n = xchg - b, the rank-ordered fold of every rank's
+ *                       slots, the acceptance / stop / continuation decisions
+ *                       in ctl, then (if accepted) g_n = A_r^T r_n, the
+ *                       iterate rotation and the KKT partials of the new
+ *                       iterate (they ride on the NEXT round's allreduce; the
+ *                       trace row's support count and the KKT exit are
+ *                       finalised one round late).
+ * Every rank holds bit-identical ctl (same allreduced inputs, fixed-order
+ * folds), so all ranks run the same number of rounds; the host only polls
+ * ctl->state every few rounds.  Rounds after FINISHED are no-ops.
+ * xchg layout: [0, ld) partial A x | slot r (16 doubles): 8 prox partials
+ * {sum|xn|, g_y.dl, dl.dl, max|xn|, ||xn-x||^2, ||x||^2, ||xn-gt||^2, 0},
+ * 8 KKT partials {max_on, max_off, any_on, any_off, count, 0, 0, 0}. */
+enum { ELL1_SF_RUNNING = 0, ELL1_SF_FINAL = 1, ELL1_SF_FINISHED = 2 };
+typedef struct {
+  /* constants (set by the host before the first round) */
+  double lam_bar, tol, stop_thr, gt_norm, eta, beta;
+  int64_t max_iter;
+  int32_t stop_kind, exact, world, rank;
+  /* state (device-owned after begin) */
+  double L, lam_k, lam_used, tp, tc, m, mn, f_y, F_prev, cut;
+  int64_t it, passes, trials;
+  int32_t hist, growths, state, converged, status, run_trial, adv, pending;
+} ell1_shard_ctl_t;
 size_t ell1_gemv_workspace(const ell1_dict_t* D);
 /* y (ld) = D x (n), fixed-order reduction  (DenseDictionary.apply, operators.py:27-28) */
 int ell1_gemv(const ell1_dict_t* D, const double* x, double* y, void* ws, size_t ws_bytes, void* stream);
 /* g (n) = D^T r (ld)  (DenseDictionary.adjoint, operators.py:30-31) */
 int ell1_gemv_t(const ell1_dict_t* D, const double* r, double* g, void* ws, size_t ws_bytes, void* stream);
-/* x_next = soft(y - g_y/L, lam/L) on a shard; out8 = {sum|xn|, g_y.dl, dl.dl, max|xn|,
- * ||xn - x||^2, ||x||^2, ||xn - gt||^2, 0} (shrinkage.py:199-213); ws >= 296*8*8 bytes */
-int ell1_shard_prox(int64_t n, const double* x, const double* xp, const double* gx, const double* gxp,
-                    double* xn, double m, double L, double lam, const double* gt, double* out8,
-                    void* ws, void* stream);
 /* KKT / support partials of a shard: out8 = {max_on, max_off, any_on, any_off, count, ...} */
 int ell1_shard_kkt(int64_t n, const double* x, const double* g, double lam, double cut, double* out8,
                    void* ws, void* stream);
 /* r_next = ax - b, out8 = {||r_next||^2, ||(1+mn) r_next - mn r_x||^2, ...} */
 int ell1_shard_resid(int64_t d, const double* ax, const double* b, const double* rx, double mn, double* rn,
                      double* out8, void* ws, void* stream);
+/* Vectors of one rank: V[0..5] = x, x_prev, x_next, g, g_prev, g_next (n_local
+ * each), V[6..7] = r, r_next (ld each), gt (n_local or NULL), b (ld); trace
+ * (max_iter x 4 doubles: it, F, ||r||, support). ws >= ell1_sfista_workspace(). */
+typedef struct {
+  double *x, *xp, *xn, *g, *gp, *gn, *r, *rn;
+  const double* gt;
+  const double* b;
+  double* xchg;
+  double* trace;
+} ell1_sfista_bufs_t;
+size_t ell1_sfista_workspace(const ell1_dict_t* D);
+int ell1_sfista_pre(const ell1_dict_t* D, ell1_shard_ctl_t* ctl, const ell1_sfista_bufs_t* V, void* ws,
+                    size_t ws_bytes, void* stream);
+int ell1_sfista_post(const ell1_dict_t* D, ell1_shard_ctl_t* ctl, const ell1_sfista_bufs_t* V, void* ws,
+                     size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------- PDIPA vector kernels (pdipa.cu)
  * Primal-dual interior point on the split LP min 1'v, [A, -A] v = b, v >= 0

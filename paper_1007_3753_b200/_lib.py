@@ -50,6 +50,26 @@ class FistaOpts(ctypes.Structure):
                 ("probe", ctypes.c_int32), ("_pad", ctypes.c_int32)]
 
 
+class ShardCtl(ctypes.Structure):
+    """ell1_shard_ctl_t: device-side control of the column-sharded FISTA."""
+    _fields_ = ([(f, ctypes.c_double) for f in ("lam_bar", "tol", "stop_thr", "gt_norm", "eta", "beta")]
+                + [("max_iter", ctypes.c_int64)]
+                + [(f, ctypes.c_int32) for f in ("stop_kind", "exact", "world", "rank")]
+                + [(f, ctypes.c_double) for f in ("L", "lam_k", "lam_used", "tp", "tc", "m", "mn", "f_y",
+                                                   "F_prev", "cut")]
+                + [(f, ctypes.c_int64) for f in ("it", "passes", "trials")]
+                + [(f, ctypes.c_int32) for f in ("hist", "growths", "state", "converged", "status",
+                                                  "run_trial", "adv", "pending")])
+
+
+SF_RUNNING, SF_FINAL, SF_FINISHED = 0, 1, 2
+
+
+class SfBufs(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_void_p) for f in ("x", "xp", "xn", "g", "gp", "gn", "r", "rn", "gt", "b",
+                                               "xchg", "trace")]
+
+
 class DalmOpts(ctypes.Structure):
     _fields_ = [("beta", ctypes.c_double), ("y_tol", ctypes.c_double),
                 ("y_cg_step", ctypes.c_int32), ("_pad", ctypes.c_int32),
@@ -185,8 +205,11 @@ _SIGS = {
                                  ctypes.c_size_t, ctypes.c_void_p]),
     "ell1_gemv_t": (ctypes.c_int, [P(Dict), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                    ctypes.c_size_t, ctypes.c_void_p]),
-    "ell1_shard_prox": (ctypes.c_int, [ctypes.c_int64] + [ctypes.c_void_p] * 5 +
-                        [ctypes.c_double] * 3 + [ctypes.c_void_p] * 4),
+    "ell1_sfista_workspace": (ctypes.c_size_t, [P(Dict)]),
+    "ell1_sfista_pre": (ctypes.c_int, [P(Dict), ctypes.c_void_p, P(SfBufs), ctypes.c_void_p, ctypes.c_size_t,
+                                       ctypes.c_void_p]),
+    "ell1_sfista_post": (ctypes.c_int, [P(Dict), ctypes.c_void_p, P(SfBufs), ctypes.c_void_p, ctypes.c_size_t,
+                                        ctypes.c_void_p]),
     "ell1_shard_kkt": (ctypes.c_int, [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
                                       ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "ell1_shard_resid": (ctypes.c_int, [ctypes.c_int64] + [ctypes.c_void_p] * 3 + [ctypes.c_double] +

@@ -4,12 +4,13 @@
 //
 //   ell1_gemv        y = A x          (panel partials + fixed-order row reduction)
 //   ell1_gemv_t      g = A^T r        (panel GEMV^T, local to each column)
-//   ell1_shard_prox  x_next = soft(y - g_y/L, lam/L) over the local columns with
-//                    the backtracking / stopping partial sums (shrinkage.py:199-213)
-//   ell1_shard_resid r_next = (A x_next) - b, ||r||^2, ||r_y'||^2 (replicated d side)
-//   ell1_shard_kkt   KKT / support partials of the local columns (model.py:160-173, 227-233)
-// All reductions are deterministic (fixed order); scalar partials are
-// returned per rank for the host driver to combine across ranks.
+//   ell1_sfista_pre  one backtracking trial up to the collective: prox on the
+//                    local columns + the rank's scalar slot, then A_r x_next
+//   ell1_sfista_post after the allreduce: residual, the FISTA decisions on the
+//                    device, A_r^T r_next, rotation, KKT partials (next slot)
+//   ell1_shard_resid / ell1_shard_kkt  set-up helpers (r = -b, max|A^T b|)
+// All reductions are deterministic (fixed order), so every rank folds the
+// allreduced slots to bit-identical control decisions.
 #include <cstdlib>
 #include "solvers_common.cuh"
 
@@ -20,12 +21,18 @@ struct GvArgs {
   const double* x;
   double* y;
   GridBufs g;
+  const int* gate;            // NULL, or run only while *gate != 0 (device-side control)
 };
+
+__device__ __forceinline__ bool gated_off(const int* gate) {
+  return gate != nullptr && *(const volatile int*)gate == 0;
+}
 
 template <class TA>
 __global__ void __launch_bounds__(NTHR, 1) gemv_partial_kernel(const __grid_constant__ GvArgs a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ Ctx E;
+  if (gated_off(a.gate)) return;
   DictV<TA> D = dict_view<TA>(a.D);
   D.ext = 0;
   if (threadIdx.x == 0) {
@@ -41,7 +48,8 @@ __global__ void __launch_bounds__(NTHR, 1) gemv_partial_kernel(const __grid_cons
 // y[r0(o) + j] = sum_c part[o][c][j] in fixed order (block o reduces the
 // region of row slice o; 16-byte loads, consecutive threads -> consecutive rows)
 __global__ void __launch_bounds__(NTHR) gemv_reduce_kernel(const double* part, int rp, int nb, int64_t d,
-                                                           double* y) {
+                                                           double* y, const int* gate) {
+  if (gated_off(gate)) return;
   const int o = blockIdx.x;
   const int64_t r0 = (d * o) / nb, r1 = (d * (o + 1)) / nb;
   const int rows = (int)(r1 - r0);
@@ -63,6 +71,7 @@ template <class TA>
 __global__ void __launch_bounds__(NTHR, 1) gemv_t_kernel(const __grid_constant__ GvArgs a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ Ctx E;
+  if (gated_off(a.gate)) return;
   DictV<TA> D = dict_view<TA>(a.D);
   D.ext = 0;
   if (threadIdx.x == 0) {
@@ -112,8 +121,9 @@ __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvt
 
 __global__ void __launch_bounds__(gts::THREADS, 1)
     gemv_t_stream_kernel(const float* __restrict__ A, int64_t ld, int64_t d, int64_t n, const double* __restrict__ r,
-                         double* __restrict__ g) {
+                         double* __restrict__ g, const int* gate) {
   using namespace gts;
+  if (gated_off(gate)) return;
   extern __shared__ __align__(128) unsigned char sm[];
   uint64_t* full = (uint64_t*)(sm + ST * STAGE);
   uint64_t* empty = full + ST;
@@ -222,45 +232,11 @@ __global__ void __launch_bounds__(gts::THREADS, 1)
 }
 
 static bool gemv_t_stream_ok(const ell1_dict_t* D) {
-  static int off = -1;
-  if (off < 0) {
-    const char* e = getenv("ELL1_GEMVT_STREAM");
-    off = e && e[0] == '0';
-  }
-  return !off && D->dtype == ELL1_F32 && !D->ext && D->d >= 4096 && D->d % 32 == 0 && D->ld % 4 == 0;
+  return D->dtype == ELL1_F32 && !D->ext && D->d >= 4096 && D->d % 32 == 0 && D->ld % 4 == 0;
 }
 
 // ---- elementwise + partial-sum kernels (grid-stride, CTA partials, then one CTA folds)
 constexpr int SP = 8;
-
-__global__ void __launch_bounds__(NTHR) shard_prox_kernel(int64_t n, const double* x, const double* xp,
-                                                          const double* gx, const double* gxp, double* xn,
-                                                          double m, double L, double thr, const double* gt,
-                                                          double* part) {
-  __shared__ double sh[NWARP * SP + SP];
-  __shared__ Ctx E;
-  if (threadIdx.x == 0) E.sh = sh;
-  __syncthreads();
-  double s[SP] = {0, 0, 0, 0, 0, 0, 0, 0};   // |xn|, gy.dl, dl.dl, max|xn|, (xn-x)^2, x^2, (xn-gt)^2, -
-  for (int64_t k = (int64_t)blockIdx.x * NTHR + threadIdx.x; k < n; k += (int64_t)gridDim.x * NTHR) {
-    const double xk = x[k];
-    const double yk = xk + m * (xk - xp[k]);
-    const double gk = (1.0 + m) * gx[k] - m * gxp[k];
-    const double u = soft1(yk - gk / L, thr);
-    xn[k] = u;
-    const double dl = u - yk;
-    s[0] += fabs(u);
-    s[1] += gk * dl;
-    s[2] += dl * dl;
-    s[3] = nmax(s[3], fabs(u));
-    const double dd = u - xk;
-    s[4] += dd * dd;
-    s[5] += xk * xk;
-    if (gt) { const double e = u - gt[k]; s[6] += e * e; }
-  }
-  block_reduce<SP>(E, s, 1u << 3);
-  if (threadIdx.x < SP) part[(int64_t)blockIdx.x * SP + threadIdx.x] = s[threadIdx.x];
-}
 
 __global__ void __launch_bounds__(NTHR) shard_kkt_kernel(int64_t n, const double* x, const double* g, double lam,
                                                          double cut, double* part) {
@@ -313,29 +289,257 @@ __global__ void fold_kernel(const double* part, int nblk, unsigned maxmask, doub
 
 constexpr int EW_BLOCKS = 148 * 2;
 
+// ---------------------------------------------------------------------------
+// Device-controlled column-sharded FISTA rounds (ell1_sfista_pre / _post).
+// Each kernel reduces its per-CTA partials with the "last CTA folds" pattern
+// (ticket counter, fixed CTA order), so a round is 6 launches + 1 collective
+// and nothing leaves the device.  Scalar arithmetic follows shrinkage.py
+// (:199-213 backtracking, :184-196 t-sequence, :259-297 continuation, stop
+// rules model.py:176-224, KKT model.py:160-173) with the same expressions as
+// the single-GPU fista_kernel; the file is built with -fmad=false.
+constexpr int SLOT = 16;                       // doubles per rank in xchg
+
+struct SfWs {
+  double* part;                                // [EW_BLOCKS][SP]
+  unsigned* ticket;                            // [NTICKET]
+};
+
+__device__ __forceinline__ bool last_cta(unsigned* ticket) {
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
+// thread k < SP of the last CTA: fixed-order fold of the CTA partials
+__device__ __forceinline__ double fold_parts(const double* part, int nblk, int k, bool mx) {
+  double s = mx ? -INFINITY : 0.0;
+  for (int c = 0; c < nblk; ++c) {
+    const double t = ((const volatile double*)part)[(int64_t)c * SP + k];
+    s = mx ? nmax(s, t) : s + t;
+  }
+  return s;
+}
+
+// K1: prox step on the local columns (shrinkage.py:204-207 with y, g_y as
+// exact linear combinations of the cached iterates) + the rank's 8 partials.
+__global__ void __launch_bounds__(NTHR) sf_prox_kernel(const ell1_shard_ctl_t* __restrict__ ctl, int64_t n,
+                                                       ell1_sfista_bufs_t V, SfWs w) {
+  __shared__ double sh[NWARP * SP + SP];
+  __shared__ Ctx E;
+  const int world = ctl->world, rank = ctl->rank;
+  double* slots = V.xchg + 0;                  // caller passes xchg + ld as V.xchg here
+  if (blockIdx.x == 0)
+    for (int i = (int)threadIdx.x; i < world * SLOT; i += NTHR)
+      if (i / SLOT != rank) slots[i] = 0.0;
+  if (ctl->state != ELL1_SF_RUNNING) return;
+  if (threadIdx.x == 0) E.sh = sh;
+  __syncthreads();
+  const double m = ctl->m, L = ctl->L, thr = ctl->lam_k / ctl->L;
+  double s[SP] = {0, 0, 0, 0, 0, 0, 0, 0};   // |xn|, gy.dl, dl.dl, max|xn|, (xn-x)^2, x^2, (xn-gt)^2, -
+  for (int64_t k = (int64_t)blockIdx.x * NTHR + threadIdx.x; k < n; k += (int64_t)gridDim.x * NTHR) {
+    const double xk = V.x[k];
+    const double yk = xk + m * (xk - V.xp[k]);
+    const double gk = (1.0 + m) * V.g[k] - m * V.gp[k];
+    const double u = soft1(yk - gk / L, thr);
+    V.xn[k] = u;
+    const double dl = u - yk;
+    s[0] += fabs(u);
+    s[1] += gk * dl;
+    s[2] += dl * dl;
+    s[3] = nmax(s[3], fabs(u));
+    const double dd = u - xk;
+    s[4] += dd * dd;
+    s[5] += xk * xk;
+    if (V.gt) { const double e = u - V.gt[k]; s[6] += e * e; }
+  }
+  block_reduce<SP>(E, s, 1u << 3);
+  if (threadIdx.x < SP) w.part[(int64_t)blockIdx.x * SP + threadIdx.x] = s[threadIdx.x];
+  if (last_cta(w.ticket + 0)) {
+    if (threadIdx.x < SP) slots[rank * SLOT + threadIdx.x] = fold_parts(w.part, gridDim.x, threadIdx.x, threadIdx.x == 3);
+    if (threadIdx.x == 0) w.ticket[0] = 0u;
+  }
+}
+
+// K4: replicated residual r_n = A x_n - b (+ ||r_n||^2, ||r_y'||^2), then the
+// decisions (one thread of the last CTA).
+__global__ void __launch_bounds__(NTHR) sf_decide_kernel(ell1_shard_ctl_t* __restrict__ ctl, int64_t d,
+                                                         int64_t ld, ell1_sfista_bufs_t V, SfWs w) {
+  __shared__ double sh[NWARP * SP + SP];
+  __shared__ Ctx E;
+  const int st = ctl->state;
+  if (st == ELL1_SF_FINISHED) return;
+  if (threadIdx.x == 0) E.sh = sh;
+  __syncthreads();
+  double s[2] = {0.0, 0.0};
+  if (ctl->run_trial) {
+    const double mn = ctl->mn;
+    for (int64_t i = (int64_t)blockIdx.x * NTHR + threadIdx.x; i < d; i += (int64_t)gridDim.x * NTHR) {
+      const double r = V.xchg[i] - V.b[i];
+      V.rn[i] = r;
+      s[0] += r * r;
+      const double ry = (1.0 + mn) * r - mn * V.r[i];
+      s[1] += ry * ry;
+    }
+  }
+  block_reduce<2>(E, s, 0u);
+  if (threadIdx.x < 2) w.part[(int64_t)blockIdx.x * SP + threadIdx.x] = s[threadIdx.x];
+  if (!last_cta(w.ticket + 1)) return;
+  __shared__ double rs[2];
+  if (threadIdx.x < 2) rs[threadIdx.x] = fold_parts(w.part, gridDim.x, threadIdx.x, false);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  w.ticket[1] = 0u;
+  ell1_shard_ctl_t& C = *ctl;
+  const int world = C.world;
+  const double* slots = V.xchg + ld;
+  C.adv = 0;
+  // (1) the previous accepted iteration's KKT (rode on this round's allreduce)
+  if (C.pending) {
+    double max_on = -INFINITY, max_off = -INFINITY, cnt = 0.0;
+    bool any_on = false, any_off = false;
+    for (int r = 0; r < world; ++r) {
+      const double* q = slots + r * SLOT + SP;
+      max_on = pymax(max_on, q[0]);
+      max_off = pymax(max_off, q[1]);
+      any_on = any_on || q[2] > 0.0;
+      any_off = any_off || q[3] > 0.0;
+      cnt += q[4];
+    }
+    double kk = 0.0;
+    if (any_on) kk = max_on;
+    if (any_off) kk = pymax(pymax(kk, max_off - C.lam_used), 0.0);
+    V.trace[(C.it - 1) * 4 + 3] = rint(cnt);
+    C.pending = 0;
+    const bool conv = C.lam_used == C.lam_bar && kk <= C.tol * C.lam_bar;
+    const bool kfire = C.stop_kind == ELL1_STOP_KKT && kk <= C.stop_thr;
+    if (conv || kfire) C.converged = 1;
+    if (conv || kfire || st == ELL1_SF_FINAL) {
+      if (C.run_trial) C.passes += 1;          // the speculative trial's A x pass ran
+      C.state = ELL1_SF_FINISHED;
+      C.run_trial = 0;
+      return;
+    }
+  }
+  if (st != ELL1_SF_RUNNING) {                  // FINAL without a pending row: nothing left
+    C.state = ELL1_SF_FINISHED;
+    C.run_trial = 0;
+    return;
+  }
+  // (2) this round's trial (shrinkage.py:199-213)
+  double p[SP];
+  for (int k = 0; k < SP; ++k) p[k] = 0.0;
+  double mx = -INFINITY;
+  for (int r = 0; r < world; ++r) {
+    const double* q = slots + r * SLOT;
+    p[0] = p[0] + q[0]; p[1] = p[1] + q[1]; p[2] = p[2] + q[2];
+    p[4] = p[4] + q[4]; p[5] = p[5] + q[5]; p[6] = p[6] + q[6];
+    mx = pymax(mx, q[3]);
+  }
+  p[3] = mx;
+  C.trials += 1;
+  C.passes += 1;
+  const double l1 = p[0];
+  const double Fn = 0.5 * rs[0] + C.lam_k * l1;
+  if (!C.exact) {
+    const double Q = C.f_y + p[1] + 0.5 * C.L * p[2] + C.lam_k * l1;
+    if (!(Fn <= Q + 1e-12 * pymax(1.0, fabs(Q)))) {
+      C.L *= C.eta;
+      C.growths += 1;
+      if (C.growths >= 101) {                   // shrinkage.py:24,203
+        C.status = ELL1_BREAKDOWN;
+        C.state = ELL1_SF_FINISHED;
+        C.run_trial = 0;
+      }
+      return;
+    }
+  }
+  // accepted: iteration it+1 done; rotation + A^T r_n + KKT partials follow (adv)
+  C.growths = 0;
+  C.it += 1;
+  C.passes += 1;
+  C.adv = 1;
+  V.trace[(C.it - 1) * 4 + 0] = (double)C.it;
+  V.trace[(C.it - 1) * 4 + 1] = Fn;
+  V.trace[(C.it - 1) * 4 + 2] = sqrt(rs[0]);
+  V.trace[(C.it - 1) * 4 + 3] = 0.0;
+  C.pending = 1;
+  C.lam_used = C.lam_k;
+  C.cut = 1e-10 * pymax(p[3], 1.0);
+  C.hist = C.hist + 1 < 2 ? C.hist + 1 : 2;
+  const bool fires = C.stop_kind != ELL1_STOP_KKT &&
+                     stop_fires(C.stop_kind, C.stop_thr, C.hist, Fn, C.F_prev, p[4], p[5], p[6], C.gt_norm, 0.0);
+  const double t_new = fista_t_next(C.tc);     // the t computed at the top of this iteration
+  C.tp = C.tc;
+  C.tc = t_new;
+  C.f_y = 0.5 * rs[1];
+  C.F_prev = Fn;
+  if (fires) C.converged = 1;
+  if (fires || C.it >= C.max_iter) {
+    C.state = ELL1_SF_FINAL;                   // one more round carries the KKT count
+    C.run_trial = 0;
+    return;
+  }
+  C.lam_k = pymax(C.beta * C.lam_k, C.lam_bar);
+  // momentum of the next iteration and of its residual (shrinkage.py:266-272)
+  C.m = (C.tp - 1.0) / C.tc;
+  C.mn = (C.tc - 1.0) / fista_t_next(C.tc);
+}
+
+// K6: rotate (x_prev <- x <- x_n, g likewise, r <- r_n) and the KKT partials
+// of the accepted iterate into the rank's slot (model.py:160-173, support
+// cut 1e-10 max(max|x|, 1), model.py:227-233).
+__global__ void __launch_bounds__(NTHR) sf_advance_kernel(const ell1_shard_ctl_t* __restrict__ ctl, int64_t n,
+                                                          int64_t d, int64_t ld, ell1_sfista_bufs_t V, SfWs w) {
+  __shared__ double sh[NWARP * SP + SP];
+  __shared__ Ctx E;
+  if (!ctl->adv) return;
+  if (threadIdx.x == 0) E.sh = sh;
+  __syncthreads();
+  const double lam = ctl->lam_used, cut = ctl->cut;
+  double s[SP] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int64_t k = (int64_t)blockIdx.x * NTHR + threadIdx.x; k < n; k += (int64_t)gridDim.x * NTHR) {
+    const double xk = V.xn[k], gk = V.gn[k];
+    V.xp[k] = V.x[k];
+    V.x[k] = xk;
+    V.gp[k] = V.g[k];
+    V.g[k] = gk;
+    const double c = -gk;
+    if (xk != 0.0) { s[0] = nmax(s[0], fabs(c - lam * sgn(xk))); s[2] = 1.0; }
+    else { s[1] = nmax(s[1], fabs(c)); s[3] = 1.0; }
+    if (fabs(xk) > cut) s[4] += 1.0;
+  }
+  for (int64_t i = (int64_t)blockIdx.x * NTHR + threadIdx.x; i < d; i += (int64_t)gridDim.x * NTHR) V.r[i] = V.rn[i];
+  block_reduce<SP>(E, s, 0xFu);
+  if (threadIdx.x < SP) w.part[(int64_t)blockIdx.x * SP + threadIdx.x] = s[threadIdx.x];
+  if (last_cta(w.ticket + 2)) {
+    double* slots = V.xchg + ld;
+    if (threadIdx.x < SP)
+      slots[ctl->rank * SLOT + SP + threadIdx.x] = fold_parts(w.part, gridDim.x, threadIdx.x, threadIdx.x < 4);
+    if (threadIdx.x == 0) w.ticket[2] = 0u;
+  }
+}
+
 }  // namespace ell1
 
 using namespace ell1;
 
-extern "C" size_t ell1_gemv_workspace(const ell1_dict_t* D) {
-  if (!dict_ok(D)) return 0;
-  const int nb = pick_blocks(D->n, 0);
-  return grid_bytes(nb, D->d, 1) + (size_t)EW_BLOCKS * SP * 8 + 4096;
-}
-
-extern "C" int ell1_gemv(const ell1_dict_t* D, const double* x, double* y, void* ws, size_t wsb, void* stream) {
-  if (!dict_ok(D) || !x || !y) return ELL1_ERR_ARG;
+static int launch_gemv(const ell1_dict_t* D, const double* x, double* y, void* ws, size_t wsb, cudaStream_t s,
+                       const int* gate) {
   const int nb = pick_blocks(D->n, 0);
   GvArgs a;
   a.D = to_raw(D);
   a.D.ext = 0;
   a.x = x; a.y = y;
+  a.gate = gate;
   Carve cv(ws, wsb);
   if (!carve_grid(cv, a.g, nb, D->d, 1)) return ELL1_ERR_ARG;
   const SmemPlan sp = plan_smem(a.D, nb, 0, 2, false);
   a.g.shcap = sp.scratch;
   a.g.panel_bytes = 0;
-  cudaStream_t s = (cudaStream_t)stream;
   if (D->dtype == ELL1_F64) {
     cudaFuncSetAttribute(gemv_partial_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.bytes);
     gemv_partial_kernel<double><<<nb, NTHR, sp.bytes, s>>>(a);
@@ -343,14 +547,13 @@ extern "C" int ell1_gemv(const ell1_dict_t* D, const double* x, double* y, void*
     cudaFuncSetAttribute(gemv_partial_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.bytes);
     gemv_partial_kernel<float><<<nb, NTHR, sp.bytes, s>>>(a);
   }
-  gemv_reduce_kernel<<<nb, NTHR, 0, s>>>(a.g.part, a.g.rp, nb, D->d, y);
+  gemv_reduce_kernel<<<nb, NTHR, 0, s>>>(a.g.part, a.g.rp, nb, D->d, y, gate);
   return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
 }
 
-extern "C" int ell1_gemv_t(const ell1_dict_t* D, const double* r, double* g, void* ws, size_t wsb, void* stream) {
-  if (!dict_ok(D) || !r || !g) return ELL1_ERR_ARG;
+static int launch_gemv_t(const ell1_dict_t* D, const double* r, double* g, void* ws, size_t wsb, cudaStream_t s,
+                         const int* gate) {
   if (gemv_t_stream_ok(D)) {
-    cudaStream_t s = (cudaStream_t)stream;
     static unsigned attr = 0;                              // per-device bit
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -361,7 +564,7 @@ extern "C" int ell1_gemv_t(const ell1_dict_t* D, const double* r, double* g, voi
       attr |= 1u << (dev & 31);
     }
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    gemv_t_stream_kernel<<<sms, gts::THREADS, gts::SMEM, s>>>((const float*)D->A, D->ld, D->d, D->n, r, g);
+    gemv_t_stream_kernel<<<sms, gts::THREADS, gts::SMEM, s>>>((const float*)D->A, D->ld, D->d, D->n, r, g, gate);
     return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
   }
   const int nb = pick_blocks(D->n, 0);
@@ -369,12 +572,12 @@ extern "C" int ell1_gemv_t(const ell1_dict_t* D, const double* r, double* g, voi
   a.D = to_raw(D);
   a.D.ext = 0;
   a.x = r; a.y = g;
+  a.gate = gate;
   Carve cv(ws, wsb);
   if (!carve_grid(cv, a.g, nb, D->d, 1)) return ELL1_ERR_ARG;
   const SmemPlan sp = plan_smem(a.D, nb, 0, 2, false);
   a.g.shcap = sp.scratch;
   a.g.panel_bytes = 0;
-  cudaStream_t s = (cudaStream_t)stream;
   if (D->dtype == ELL1_F64) {
     cudaFuncSetAttribute(gemv_t_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.bytes);
     gemv_t_kernel<double><<<nb, NTHR, sp.bytes, s>>>(a);
@@ -385,22 +588,26 @@ extern "C" int ell1_gemv_t(const ell1_dict_t* D, const double* r, double* g, voi
   return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
 }
 
+extern "C" size_t ell1_gemv_workspace(const ell1_dict_t* D) {
+  if (!dict_ok(D)) return 0;
+  const int nb = pick_blocks(D->n, 0);
+  return grid_bytes(nb, D->d, 1) + (size_t)EW_BLOCKS * SP * 8 + 4096;
+}
+
+extern "C" int ell1_gemv(const ell1_dict_t* D, const double* x, double* y, void* ws, size_t wsb, void* stream) {
+  if (!dict_ok(D) || !x || !y) return ELL1_ERR_ARG;
+  return launch_gemv(D, x, y, ws, wsb, (cudaStream_t)stream, nullptr);
+}
+
+extern "C" int ell1_gemv_t(const ell1_dict_t* D, const double* r, double* g, void* ws, size_t wsb, void* stream) {
+  if (!dict_ok(D) || !r || !g) return ELL1_ERR_ARG;
+  return launch_gemv_t(D, r, g, ws, wsb, (cudaStream_t)stream, nullptr);
+}
+
 static int ew_blocks(int64_t n) {
   int64_t b = (n + NTHR - 1) / NTHR;
   if (b > EW_BLOCKS) b = EW_BLOCKS;
   return b < 1 ? 1 : (int)b;
-}
-
-extern "C" int ell1_shard_prox(int64_t n, const double* x, const double* xp, const double* gx,
-                               const double* gxp, double* xn, double m, double L, double lam,
-                               const double* gt, double* out8, void* ws, void* stream) {
-  if (n < 0 || !out8 || !ws || !(L > 0)) return ELL1_ERR_ARG;
-  cudaStream_t s = (cudaStream_t)stream;
-  const int nb = ew_blocks(n);
-  double* part = (double*)ws;
-  shard_prox_kernel<<<nb, NTHR, 0, s>>>(n, x, xp, gx, gxp, xn, m, L, lam / L, gt, part);
-  fold_kernel<<<1, 32, 0, s>>>(part, nb, 1u << 3, out8);
-  return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
 }
 
 extern "C" int ell1_shard_kkt(int64_t n, const double* x, const double* g, double lam, double cut,
@@ -422,5 +629,51 @@ extern "C" int ell1_shard_resid(int64_t d, const double* ax, const double* b, co
   double* part = (double*)ws;
   shard_resid_kernel<<<nb, NTHR, 0, s>>>(d, ax, b, rx, mn, rn, part);
   fold_kernel<<<1, 32, 0, s>>>(part, nb, 0u, out8);
+  return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
+}
+
+// ---- device-controlled rounds
+// workspace: [gemv grid scratch | EW_BLOCKS x SP partials | NTICKET tickets]
+extern "C" size_t ell1_sfista_workspace(const ell1_dict_t* D) {
+  if (!dict_ok(D)) return 0;
+  return ell1_gemv_workspace(D) + (size_t)EW_BLOCKS * SP * 8 + 256;
+}
+
+static bool sf_carve(const ell1_dict_t* D, void* ws, size_t wsb, SfWs& w, size_t& gws) {
+  gws = ell1_gemv_workspace(D);
+  if (!ws || wsb < ell1_sfista_workspace(D)) return false;
+  w.part = (double*)((char*)ws + gws);
+  w.ticket = (unsigned*)((char*)ws + gws + (size_t)EW_BLOCKS * SP * 8);
+  return true;
+}
+
+static bool sf_bufs_ok(const ell1_sfista_bufs_t* V) {
+  return V && V->x && V->xp && V->xn && V->g && V->gp && V->gn && V->r && V->rn && V->b && V->xchg && V->trace;
+}
+
+extern "C" int ell1_sfista_pre(const ell1_dict_t* D, ell1_shard_ctl_t* ctl, const ell1_sfista_bufs_t* V,
+                               void* ws, size_t wsb, void* stream) {
+  SfWs w;
+  size_t gws;
+  if (!dict_ok(D) || D->ext || !ctl || !sf_bufs_ok(V) || !sf_carve(D, ws, wsb, w, gws)) return ELL1_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  ell1_sfista_bufs_t P = *V;
+  P.xchg = V->xchg + D->ld;                    // the prox kernel addresses the slot region
+  sf_prox_kernel<<<ew_blocks(D->n), NTHR, 0, s>>>(ctl, D->n, P, w);
+  if (cudaGetLastError() != cudaSuccess) return ELL1_ERR_CUDA;
+  return launch_gemv(D, V->xn, V->xchg, ws, gws, s, &ctl->run_trial);
+}
+
+extern "C" int ell1_sfista_post(const ell1_dict_t* D, ell1_shard_ctl_t* ctl, const ell1_sfista_bufs_t* V,
+                                void* ws, size_t wsb, void* stream) {
+  SfWs w;
+  size_t gws;
+  if (!dict_ok(D) || D->ext || !ctl || !sf_bufs_ok(V) || !sf_carve(D, ws, wsb, w, gws)) return ELL1_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  sf_decide_kernel<<<ew_blocks(D->d), NTHR, 0, s>>>(ctl, D->d, D->ld, *V, w);
+  if (cudaGetLastError() != cudaSuccess) return ELL1_ERR_CUDA;
+  const int rc = launch_gemv_t(D, V->rn, V->gn, ws, gws, s, &ctl->adv);
+  if (rc != ELL1_OK) return rc;
+  sf_advance_kernel<<<ew_blocks(D->n > D->d ? D->n : D->d), NTHR, 0, s>>>(ctl, D->n, D->d, D->ld, *V, w);
   return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
 }

@@ -2,29 +2,35 @@
 
 A = [A_0 | A_1 | ... | A_{G-1}] split by columns, one rank (process) per GPU,
 x / gradient sharded the same way, the d-side vectors (b, residuals)
-replicated.  Per iteration the only bulk exchange is ONE allreduce(sum) of the
-d-length partial A_r x_r (NCCL over NVLink); the backtracking / stopping
-scalars travel as an all_gather of 8 doubles per rank and are folded on the
-host in rank order, so every rank takes identical control decisions.
-
-The iteration is the reference FISTA (shrinkage.py:231-298, oracle/l1_oracle.py
-``fista``) restated on shards:
+replicated.  The iteration is the reference FISTA (shrinkage.py:231-298,
+oracle/l1_oracle.py ``fista``) restated on shards:
 
     y      = x + m (x - x_prev)                        m = (t_prev - 1) / t
-    r_y    = (1 + m) r_x - m r_xprev                   (linear combination, no pass)
-    g_y    = (1 + m) g_x - m g_xprev
-    repeat (shrinkage.py:199-213):
-        x_n = soft(y - g_y / L, lam_k / L)             ell1_shard_prox   (local)
-        A x_n = allreduce_r(A_r x_n,r)                 ell1_gemv + NCCL  (1 pass)
-        r_n = A x_n - b, F_n, Q                        ell1_shard_resid  (replicated)
+    g_y    = (1 + m) g_x - m g_xprev                   (linear combination, no pass)
+    repeat (shrinkage.py:199-213):                     one ROUND per trial
+        x_n = soft(y - g_y / L, lam_k / L)             local
+        A x_n = allreduce_r(A_r x_n,r)                 1 pass + THE collective
+        r_n = A x_n - b, F_n, Q                        replicated
         accept if F_n <= Q + 1e-12 max(1, |Q|) else L *= eta
-    g_n = A_r^T r_n                                    ell1_gemv_t       (local, 1 pass)
-    KKT / support partials                             ell1_shard_kkt
+    g_n = A_r^T r_n                                    local, 1 pass
+    KKT / support partials                             ride on the next round's allreduce
 
-so a non-backtracking iteration streams each shard twice.  The device work
-is libell1b200.so (csrc/shard.cu); this module is the host control loop and
-the collectives.  The same loop runs over any ``ops`` object with the
-ShardOps interface, which is how the tests drive it with gloo on CPU.
+Control lives on the device (csrc/shard.cu ``ell1_sfista_pre`` /
+``ell1_sfista_post``): the d-length partial A_r x_n and every rank's scalar
+partials (8 prox sums + 8 KKT partials, one 16-double slot per rank, the
+other ranks' slots zero) travel in ONE allreduce(sum) per round, so each
+rank folds the slots in rank order and takes bit-identical decisions without
+any host round trip.  The host only enqueues rounds and polls the device
+state word every ``ROUNDS_PER_POLL`` rounds (asynchronously, one batch
+behind, so the GPU queue never drains).  The trace row's support count and
+the KKT exit test of iteration k are finalised in round k+1 (their partials
+need the global max|x| first); a solve therefore ends with one extra round.
+
+The driver runs over any ``ops`` object with this interface
+(``setup / begin / round / poll_async / poll_wait / result`` plus the
+``gemv / gemv_t / allreduce_`` primitives of the exact-L power iteration);
+``DeviceShardOps`` is the product, tests/shard_numpy_ops.py restates it in
+numpy for the gloo (CPU) tests.
 """
 
 import ctypes
@@ -35,10 +41,11 @@ from dataclasses import dataclass
 import numpy as np
 
 from paper_1007_3753_b200 import _lib, device
-from paper_1007_3753_b200.exceptions import NumericalBreakdownError
+from paper_1007_3753_b200.exceptions import DeviceError, NumericalBreakdownError
 from paper_1007_3753_b200.model import SolverResult, TraceEntry
 
 _POWER_SEED = 218751   # numerics.py:224
+SLOT = 16              # doubles per rank in the exchange buffer
 
 
 def column_range(n, rank, world):
@@ -101,119 +108,30 @@ class ShardedInstance:
 
 
 # ----------------------------------------------------------------------------
-# device ops (libell1b200.so + torch.distributed)
+# collectives
 # ----------------------------------------------------------------------------
 
-class DeviceShardOps:
-    """ShardOps over libell1b200.so; collectives through torch.distributed
-    (NCCL on GPUs).  Vectors are float64 torch tensors on the rank's GPU."""
+class TorchCollective:
+    """torch.distributed (NCCL on GPUs) over ``group``; a no-op at world 1."""
 
-    def __init__(self, shard):
-        torch = device._torch()
-        self.torch = torch
-        self.L = _lib.lib()
-        D = shard.local
-        self.D = D
-        self.view = D.view()
-        self.dev = D.device
-        self.stream = device.stream_ptr(self.dev)
-        self.d, self.nl, self.ld = D.d, D.n, D.ld
-        self.group = shard.group
-        self.world, self.rank = _world(shard.group)
-        self.gws_bytes = int(self.L.ell1_gemv_workspace(ctypes.byref(self.view)))
-        self.gws = device.alloc_bytes(self.gws_bytes, self.dev)
-        self.ews = device.alloc_bytes(296 * 8 * 8, self.dev)
-        # [world x 8 prox partials | 8 replicated residual sums]
-        self.scal = torch.zeros(self.world * 8 + 8, dtype=torch.float64, device=self.dev)
-        self.kscal = torch.zeros(self.world * 8, dtype=torch.float64, device=self.dev)
-        self.mine = torch.zeros(8, dtype=torch.float64, device=self.dev)
+    def __init__(self, group=None):
+        self.group = group
+        self.world, self.rank = _world(group)
 
-    # vectors
-    def zeros_d(self):
-        return self.torch.zeros(self.ld, dtype=self.torch.float64, device=self.dev)
-
-    def zeros_n(self):
-        return self.torch.zeros(max(self.nl, 1), dtype=self.torch.float64, device=self.dev)
-
-    def from_host_d(self, v):
-        return device.to_device_vec(v, self.ld, self.dev)
-
-    def from_host_n(self, v):
-        return device.to_device_vec(v, max(self.nl, 1), self.dev)
-
-    def to_host_n(self, v):
-        return v[: self.nl].cpu().numpy().copy()
-
-    def to_host_d(self, v):
-        return v[: self.d].cpu().numpy().copy()
-
-    # kernels
-    def gemv(self, x, out):
-        _lib.check(self.L.ell1_gemv(ctypes.byref(self.view), device.ptr(x), device.ptr(out),
-                                    device.ptr(self.gws), self.gws_bytes, self.stream), "ell1_gemv")
-
-    def gemv_t(self, r, out):
-        _lib.check(self.L.ell1_gemv_t(ctypes.byref(self.view), device.ptr(r), device.ptr(out),
-                                      device.ptr(self.gws), self.gws_bytes, self.stream),
-                   "ell1_gemv_t")
-
-    def prox(self, x, xp, gx, gxp, xn, m, L, lam, gt):
-        _lib.check(self.L.ell1_shard_prox(self.nl, device.ptr(x), device.ptr(xp), device.ptr(gx),
-                                          device.ptr(gxp), device.ptr(xn), float(m), float(L),
-                                          float(lam), device.ptr(gt), device.ptr(self.mine),
-                                          device.ptr(self.ews), self.stream), "ell1_shard_prox")
-
-    def resid(self, ax, b, rx, mn, rn):
-        out = self.scal[self.world * 8:]
-        _lib.check(self.L.ell1_shard_resid(self.d, device.ptr(ax), device.ptr(b), device.ptr(rx),
-                                           float(mn), device.ptr(rn), device.ptr(out),
-                                           device.ptr(self.ews), self.stream), "ell1_shard_resid")
-
-    def kkt(self, x, g, lam, cut):
-        _lib.check(self.L.ell1_shard_kkt(self.nl, device.ptr(x), device.ptr(g), float(lam),
-                                         float(cut), device.ptr(self.mine), device.ptr(self.ews),
-                                         self.stream), "ell1_shard_kkt")
-
-    # collectives + read-back
-    def allreduce_(self, v):
+    def allreduce_(self, t):
         if self.world > 1:
             import torch.distributed as dist
-            dist.all_reduce(v, op=dist.ReduceOp.SUM, group=self.group)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
 
-    def _gather_mine(self, dst):
-        if self.world > 1:
-            import torch.distributed as dist
-            dist.all_gather_into_tensor(dst, self.mine, group=self.group)
-        else:
-            dst.copy_(self.mine)
-
-    def trial_scalars(self):
-        """-> (prox partials (world x 8), residual sums (8,)) on the host."""
-        self._gather_mine(self.scal[: self.world * 8])
-        h = self.scal.cpu().numpy()
-        return h[: self.world * 8].reshape(self.world, 8), h[self.world * 8:]
-
-    def kkt_scalars(self):
-        self._gather_mine(self.kscal)
-        return self.kscal.cpu().numpy().reshape(self.world, 8)
-
-    def gather_n(self, v, n_global):
-        """Full-length x on every rank (result assembly)."""
-        torch = self.torch
+    def all_gather(self, t):
+        """-> tensor of world * len(t) (rank-major)."""
         if self.world == 1:
-            return self.to_host_n(v)
+            return t.clone()
+        import torch
         import torch.distributed as dist
-        sizes = [column_range(n_global, r, self.world) for r in range(self.world)]
-        cap = max(c1 - c0 for c0, c1 in sizes)
-        buf = torch.zeros(cap, dtype=torch.float64, device=self.dev)
-        buf[: self.nl] = v[: self.nl]
-        out = torch.zeros(cap * self.world, dtype=torch.float64, device=self.dev)
-        dist.all_gather_into_tensor(out, buf, group=self.group)
-        h = out.cpu().numpy().reshape(self.world, cap)
-        return np.concatenate([h[r, : c1 - c0] for r, (c0, c1) in enumerate(sizes)])
-
-    def sync(self):
-        self.torch.cuda.synchronize(self.dev)
+        out = torch.empty(t.numel() * self.world, dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(out, t, group=self.group)
+        return out
 
 
 def _world(group):
@@ -227,55 +145,162 @@ def _world(group):
 
 
 # ----------------------------------------------------------------------------
-# host control loop (identical on every rank)
+# device ops (libell1b200.so + one collective per round)
 # ----------------------------------------------------------------------------
 
-def _fold_prox(parts):
-    """Rank-order fold of the per-rank prox partials
-    {sum|xn|, g_y.dl, dl.dl, max|xn|, ||xn-x||^2, ||x||^2, ||xn-gt||^2}."""
-    s = np.zeros(8)
-    mx = -math.inf
-    for r in range(parts.shape[0]):
-        for k in (0, 1, 2, 4, 5, 6):
-            s[k] = s[k] + parts[r, k]
-        mx = max(mx, float(parts[r, 3]))
-    s[3] = mx
-    return s
+class DeviceShardOps:
+    """The rank's device state of a column-sharded FISTA solve.  Vectors are
+    float64 torch tensors on the rank's GPU; the control block
+    (ell1_shard_ctl_t) lives in device memory."""
+
+    def __init__(self, shard, coll=None):
+        torch = device._torch()
+        self.torch = torch
+        self.L = _lib.lib()
+        D = shard.local
+        self.D = D
+        self.view = D.view()
+        self.dev = D.device
+        self.stream = device.stream_ptr(self.dev)
+        self.d, self.nl, self.ld = D.d, D.n, D.ld
+        self.n_global = shard.n
+        self.coll = coll if coll is not None else TorchCollective(shard.group)
+        self.world, self.rank = self.coll.world, self.coll.rank
+        c0, c1 = column_range(shard.n, self.rank, self.world)
+        if (shard.c0, shard.c1) != (c0, c1):
+            raise ValueError("shard columns [%d, %d) differ from column_range(n, %d, %d) = [%d, %d)"
+                             % (shard.c0, shard.c1, self.rank, self.world, c0, c1))
+        self.gws_bytes = int(self.L.ell1_gemv_workspace(ctypes.byref(self.view)))
+        self.ws_bytes = int(self.L.ell1_sfista_workspace(ctypes.byref(self.view)))
+        self.ws = torch.zeros(self.ws_bytes, dtype=torch.uint8, device=self.dev)  # tickets start at 0
+        self.ews = device.alloc_bytes(296 * 8 * 8, self.dev)
+        f64 = dict(dtype=torch.float64, device=self.dev)
+        nl = max(self.nl, 1)
+        self.vec = torch.zeros(6 * nl, **f64)          # x, xp, xn, g, gp, gn
+        self.x, self.xp, self.xn, self.g, self.gp, self.gn = self.vec.split(nl)
+        self.dvec = torch.zeros(2 * self.ld, **f64)    # r, rn
+        self.r, self.rn = self.dvec.split(self.ld)
+        self.xchg = torch.zeros(self.ld + SLOT * self.world, **f64)
+        self.out8 = torch.zeros(8, **f64)
+        self.ctl = torch.zeros(ctypes.sizeof(_lib.ShardCtl), dtype=torch.uint8, device=self.dev)
+        self._state_word = _lib.ShardCtl.state.offset // 4
+        self._pin = torch.zeros(2, dtype=torch.int32).pin_memory()
+        self._polls = 0
+        self.b = None
+        self.gt = None
+        self.trace = None
+        self.bufs = None
+
+    # -- primitives (set-up, power iteration) --------------------------------
+    def zeros_d(self):
+        return self.torch.zeros(self.ld, dtype=self.torch.float64, device=self.dev)
+
+    def zeros_n(self):
+        return self.torch.zeros(max(self.nl, 1), dtype=self.torch.float64, device=self.dev)
+
+    def from_host_d(self, v):
+        return device.to_device_vec(v, self.ld, self.dev)
+
+    def to_host_d(self, v):
+        return v[: self.d].cpu().numpy().copy()
+
+    def gemv(self, x, out):
+        _lib.check(self.L.ell1_gemv(ctypes.byref(self.view), device.ptr(x), device.ptr(out),
+                                    device.ptr(self.ws), self.gws_bytes, self.stream), "ell1_gemv")
+
+    def gemv_t(self, r, out):
+        _lib.check(self.L.ell1_gemv_t(ctypes.byref(self.view), device.ptr(r), device.ptr(out),
+                                      device.ptr(self.ws), self.gws_bytes, self.stream), "ell1_gemv_t")
+
+    def allreduce_(self, v):
+        self.coll.allreduce_(v)
+
+    # -- the solve --------------------------------------------------------------
+    def setup(self, b, gt_local=None):
+        """r = -b, g = A_r^T r, and the global max|A^T b| (one slot allreduce).
+        Returns c0."""
+        self.vec.zero_()
+        self.dvec.zero_()
+        self.b = self.from_host_d(b)
+        self.gt = device.to_device_vec(gt_local, max(self.nl, 1), self.dev) if gt_local is not None else None
+        _lib.check(self.L.ell1_shard_resid(self.d, device.ptr(self.rn), device.ptr(self.b), device.ptr(self.r),
+                                           0.0, device.ptr(self.r), device.ptr(self.out8),
+                                           device.ptr(self.ews), self.stream), "ell1_shard_resid")
+        self.gemv_t(self.r, self.g)
+        _lib.check(self.L.ell1_shard_kkt(self.nl, device.ptr(self.x), device.ptr(self.g), 0.0, 1.0,
+                                         device.ptr(self.out8), device.ptr(self.ews), self.stream),
+                   "ell1_shard_kkt")
+        slots = self.xchg[self.ld:].view(self.world, SLOT)
+        slots.zero_()
+        slots[self.rank, 8:] = self.out8
+        self.coll.allreduce_(self.xchg[self.ld:])
+        return float(slots[:, 9].max().item())
+
+    def begin(self, ctl):
+        """Upload the control block (an _lib.ShardCtl) and size the trace."""
+        torch = self.torch
+        ctl.world, ctl.rank = self.world, self.rank
+        self.trace = torch.zeros(max(int(ctl.max_iter), 1) * 4, dtype=torch.float64, device=self.dev)
+        raw = torch.frombuffer(bytearray(bytes(ctl)), dtype=torch.uint8)
+        self.ctl.copy_(raw)
+        B = _lib.SfBufs()
+        for f in ("x", "xp", "xn", "g", "gp", "gn", "r", "rn", "b", "xchg", "trace"):
+            setattr(B, f, getattr(self, f).data_ptr())
+        B.gt = self.gt.data_ptr() if self.gt is not None else None
+        self.bufs = B
+        self._polls = 0
+
+    def round(self):
+        """One backtracking trial: pre (prox, A_r x_n) -> allreduce -> post."""
+        V = ctypes.byref(self.bufs)
+        cp = ctypes.c_void_p(self.ctl.data_ptr())
+        _lib.check(self.L.ell1_sfista_pre(ctypes.byref(self.view), cp, V, device.ptr(self.ws), self.ws_bytes,
+                                          self.stream), "ell1_sfista_pre")
+        self.coll.allreduce_(self.xchg)
+        _lib.check(self.L.ell1_sfista_post(ctypes.byref(self.view), cp, V, device.ptr(self.ws), self.ws_bytes,
+                                           self.stream), "ell1_sfista_post")
+
+    def poll_async(self):
+        """Queue a read of ctl->state into pinned memory; returns a handle."""
+        k = self._polls & 1
+        self._polls += 1
+        self._pin[k:k + 1].copy_(self.ctl.view(self.torch.int32)[self._state_word:self._state_word + 1],
+                                 non_blocking=True)
+        ev = self.torch.cuda.Event()
+        ev.record(self.torch.cuda.current_stream(self.dev))
+        return (k, ev)
+
+    def poll_wait(self, h):
+        k, ev = h
+        ev.synchronize()
+        return int(self._pin[k])
+
+    def result(self):
+        """-> (ShardCtl, trace rows (it x 4), full x) on every rank."""
+        ctl = _lib.ShardCtl.from_buffer_copy(bytes(self.ctl.cpu().numpy().tobytes()))
+        it = int(ctl.it)
+        tr = self.trace[: 4 * it].cpu().numpy().reshape(-1, 4) if it else np.zeros((0, 4))
+        sizes = [column_range(self.n_global, r, self.world) for r in range(self.world)]
+        cap = max(c1 - c0 for c0, c1 in sizes)
+        buf = self.torch.zeros(cap, dtype=self.torch.float64, device=self.dev)
+        buf[: self.nl] = self.x[: self.nl]
+        h = self.coll.all_gather(buf).cpu().numpy().reshape(self.world, cap)
+        x = np.concatenate([h[r, : c1 - c0] for r, (c0, c1) in enumerate(sizes)])
+        return ctl, tr, x
+
+    def sync(self):
+        self.torch.cuda.synchronize(self.dev)
 
 
-def _fold_kkt(parts, lam):
-    """model.py:160-173 from {max_on, max_off, any_on, any_off, count} partials."""
-    max_on = max(float(p) for p in parts[:, 0])
-    max_off = max(float(p) for p in parts[:, 1])
-    any_on = bool(np.any(parts[:, 2] > 0))
-    any_off = bool(np.any(parts[:, 3] > 0))
-    count = int(round(float(np.sum(parts[:, 4]))))
-    worst = 0.0
-    if any_on:
-        worst = max_on
-    if any_off:
-        worst = max(worst, max_off - lam, 0.0)
-    return worst, count
-
-
-def _stop_fires(kind, thr, hist, F, F_prev, dx2, xp2, gt2, gtn, kk):
-    """model.py:176-224 on reduced quantities."""
-    if kind is None:
-        return False
-    if kind == "relative-objective":
-        return hist >= 2 and abs(F - F_prev) <= thr * abs(F_prev)
-    if kind == "relative-estimate":
-        return hist >= 2 and math.sqrt(dx2) <= thr * math.sqrt(xp2)
-    if kind == "ground-truth-distance":
-        return math.sqrt(gt2) <= thr * gtn
-    return kk <= thr
-
+# ----------------------------------------------------------------------------
+# host driver (identical on every rank)
+# ----------------------------------------------------------------------------
 
 def sharded_power_norm_sq(ops, tol=1e-6, max_iter=1000):
     """Largest eigenvalue of A^T A over the shards (numerics.py:227-261) for
     d <= n: v -> A (A^T v) with one allreduce per step; the d-length power
     vector is kept on the host so the start vector and redraws follow the
-    reference generator exactly."""
+    reference generator exactly (exact_L option only)."""
     gen = np.random.default_rng(_POWER_SEED)
     d = ops.d
     v = gen.standard_normal(d)
@@ -301,126 +326,78 @@ def sharded_power_norm_sq(ops, tol=1e-6, max_iter=1000):
 
 
 class ShardedFista:
-    """Host driver of the column-sharded FISTA.  ``ops`` implements the
-    ShardOps interface (DeviceShardOps in production)."""
+    """Host driver of the column-sharded FISTA: set-up, then rounds until the
+    device reports FINISHED.  ``ops`` implements the ShardOps interface."""
+
+    ROUNDS_PER_POLL = 8
 
     def __init__(self, ops, b, n_global, config, gt_local=None, gt_norm=0.0):
         self.ops = ops
         self.config = config
         self.b_host = np.asarray(b, dtype=np.float64)
         self.n = int(n_global)
-        o = ops
-        self.b = o.from_host_d(self.b_host)
-        self.gt = o.from_host_n(gt_local) if gt_local is not None else None
+        self.gt_local = gt_local
         self.gt_norm = float(gt_norm)
         self.passes = 0        # panel passes (A x or A^T r) of the last solve
         self.trials = 0
-        self._reset()
-
-    def _reset(self):
-        o = self.ops
-        # iterate buffers (swapped, never copied)
-        self.x, self.xp, self.xn = o.zeros_n(), o.zeros_n(), o.zeros_n()
-        self.gx, self.gxp, self.gn = o.zeros_n(), o.zeros_n(), o.zeros_n()
-        self.rx, self.rn, self.ax = o.zeros_d(), o.zeros_d(), o.zeros_d()
-
-    def _kkt(self, x, g, lam, cut):
-        self.ops.kkt(x, g, lam, cut)
-        return _fold_kkt(self.ops.kkt_scalars(), lam)
+        self.rounds = 0
 
     def solve(self):
         cfg, o = self.config, self.ops
         t0 = time.perf_counter()
         stop = cfg.stopping
         kind = stop.kind if stop is not None else None
-        thr = float(stop.threshold) if stop is not None else 0.0
-        if kind == "ground-truth-distance" and self.gt is None:
+        if kind == "ground-truth-distance" and self.gt_local is None:
             raise ValueError("ground-truth-distance rule needs a ground truth")
-        eta = float(cfg.opt("eta", 1.5))
-        L = float(cfg.opt("L0", 1.0))
-        beta = float(cfg.opt("beta", 0.5))
-        exact = bool(cfg.opt("exact_L", False))
         bn2 = float(self.b_host @ self.b_host)
-        if self.passes:
-            self._reset()
-        self.passes = 0
-        self.trials = 0
-        # r_x = A 0 - b = -b ; g_x = A^T r_x = -A^T b ; c0 = max|A^T b|
-        o.resid(self.ax, self.b, self.rx, 0.0, self.rx)          # ax == 0 -> rx = -b
-        o.gemv_t(self.rx, self.gx)
-        self.passes += 1
-        o.kkt(self.x, self.gx, 0.0, 1.0)
-        c0 = max(float(p) for p in o.kkt_scalars()[:, 1])
+        c0 = o.setup(self.b_host, self.gt_local)
         lam_bar = float(cfg.lam) if cfg.lam is not None else 1e-2 * c0
-        if c0 == 0.0:
-            x = np.zeros(self.n)
-            return SolverResult(x, 0, time.perf_counter() - t0, True,
+        if c0 == 0.0:                                   # shrinkage.py:245-247
+            self.passes, self.trials, self.rounds = 1, 0, 0
+            return SolverResult(np.zeros(self.n), 0, time.perf_counter() - t0, True,
                                 [TraceEntry(0, 0.0, math.sqrt(bn2), 0)])
         if not lam_bar > 0:
             raise ValueError("lambda must be positive")
+        exact = bool(cfg.opt("exact_L", False))
+        L = float(cfg.opt("L0", 1.0))
         if exact:
             L = sharded_power_norm_sq(o) * (1.0 + 1e-9)
-        lam_k = max(0.9 * c0, lam_bar) if cfg.opt("continuation", True) else lam_bar
-        tp = tc = 1.0
-        trace = []
-        hist = 0
-        F_prev = 0.0
-        f_y = 0.5 * bn2                 # r_y = r_x = -b at the first iteration
-        done = False
-        it = 0
-        while it < cfg.max_iter:
-            it += 1
-            m = (tp - 1.0) / tc
-            t_new = _t_next(tc)
-            mn = (tc - 1.0) / t_new     # momentum of the NEXT iteration
-            accepted = False
-            for _ in range(1 if exact else 101):
-                o.prox(self.x, self.xp, self.gx, self.gxp, self.xn, m, L, lam_k, self.gt)
-                o.gemv(self.xn, self.ax)
-                self.passes += 1
-                self.trials += 1
-                o.allreduce_(self.ax)
-                o.resid(self.ax, self.b, self.rx, mn, self.rn)
-                parts, rs = o.trial_scalars()
-                s = _fold_prox(parts)
-                l1 = s[0]
-                Fn = 0.5 * float(rs[0]) + lam_k * l1
-                if exact:
-                    accepted = True
-                    break
-                Q = f_y + float(s[1]) + 0.5 * L * float(s[2]) + lam_k * l1
-                if Fn <= Q + 1e-12 * max(1.0, abs(Q)):
-                    accepted = True
-                    break
-                L *= eta
-            if not accepted:
-                raise NumericalBreakdownError("backtracking exceeded 100 growth steps")
-            # rotate: x_prev <- x, x <- x_n ; r, g likewise
-            self.xp, self.x, self.xn = self.x, self.xn, self.xp
-            self.rx, self.rn = self.rn, self.rx
-            self.gxp, self.gx, self.gn = self.gx, self.gn, self.gxp
-            o.gemv_t(self.rx, self.gx)
-            self.passes += 1
-            tp, tc = tc, t_new
-            f_next = 0.5 * float(rs[1])
-            cut = 1e-10 * max(float(s[3]), 1.0)
-            kk, count = self._kkt(self.x, self.gx, lam_k, cut)
-            trace.append(TraceEntry(it, Fn, math.sqrt(float(rs[0])), count))
-            hist = min(hist + 1, 2)
-            fires = _stop_fires(kind, thr, hist, Fn, F_prev, float(s[4]), float(s[5]),
-                                float(s[6]), self.gt_norm, kk)
-            F_prev = Fn
-            f_y = f_next
-            if lam_k == lam_bar and kk <= cfg.tol * lam_bar:
-                done = True
+        C = _lib.ShardCtl()
+        C.lam_bar, C.tol = lam_bar, float(cfg.tol)
+        C.stop_kind = _lib.STOP_CODES[kind]
+        C.stop_thr = float(stop.threshold) if stop is not None else 0.0
+        C.gt_norm = self.gt_norm
+        C.eta, C.beta = float(cfg.opt("eta", 1.5)), float(cfg.opt("beta", 0.5))
+        C.max_iter, C.exact = int(cfg.max_iter), int(exact)
+        C.L = L
+        C.lam_k = max(0.9 * c0, lam_bar) if cfg.opt("continuation", True) else lam_bar
+        C.tp = C.tc = 1.0
+        C.m, C.mn = 0.0, 0.0               # (t_prev - 1) / t and (t - 1) / t_next at t = 1
+        C.f_y = 0.5 * bn2                  # r_y = r_x = -b at the first iteration
+        C.state, C.run_trial = _lib.SF_RUNNING, 1
+        o.begin(C)
+        # every trial is one round; each iteration adds <= 101 trials, the
+        # solve one finalising round, the poll lag one batch
+        limit = (int(cfg.max_iter) + 1) * 102 + 4 * self.ROUNDS_PER_POLL
+        rounds, prev = 0, None
+        while True:
+            for _ in range(self.ROUNDS_PER_POLL):
+                o.round()
+            rounds += self.ROUNDS_PER_POLL
+            h = o.poll_async()
+            if prev is not None and o.poll_wait(prev) == _lib.SF_FINISHED:
                 break
-            if fires:
-                done = True
-                break
-            lam_k = max(beta * lam_k, lam_bar)
-        self.L = L
-        x = o.gather_n(self.x, self.n)
-        return SolverResult(x, it, time.perf_counter() - t0, done, trace)
+            prev = h
+            if rounds > limit:
+                raise DeviceError("sharded FISTA did not finish within %d rounds" % limit)
+        ctl, tr, x = o.result()
+        self.rounds = rounds
+        self.passes = 1 + int(ctl.passes)
+        self.trials = int(ctl.trials)
+        if ctl.status == _lib.BREAKDOWN:
+            raise NumericalBreakdownError("backtracking exceeded 100 growth steps")
+        trace = [TraceEntry(int(r[0]), float(r[1]), float(r[2]), int(r[3])) for r in tr]
+        return SolverResult(x, int(ctl.it), time.perf_counter() - t0, bool(ctl.converged), trace)
 
 
 def sharded_fista_solve(P, config, ops=None):
@@ -448,3 +425,81 @@ def sharded_fista_solve(P, config, ops=None):
         gt_local = gt[shard.c0: shard.c1]
     drv = ShardedFista(ops, P.b, shard.n, config, gt_local, gtn)
     return drv.solve()
+
+
+# ----------------------------------------------------------------------------
+# BASELINE config 4 on the device
+# ----------------------------------------------------------------------------
+
+CFG4 = dict(d=65536, n=262144, k=2048, chunk=2048, dict_seed=7000003, x_seed=44, noise_rel=1e-3)
+
+
+def make_cfg4_shard(rank=0, world=1, dev=None, coll=None, d=CFG4["d"], n=CFG4["n"], k=CFG4["k"],
+                    dtype="float32"):
+    """This rank's column panel of the config-4 instance, generated on the
+    device: A = unit-norm N(0,1) columns drawn per 2048-column global chunk
+    from a seeded Philox stream (the same matrix for every world size), x0 =
+    k N(0,1) values on a uniform support (numpy PCG64), b = A x0 + 1e-3
+    relative Gaussian noise (one allreduce of the partial A_r x0_r).
+    Returns (ShardedDictionary, b (host, d), x0 (host, n), ops)."""
+    torch = device._torch()
+    dev = dev if dev is not None else device.current_device()
+    c0, c1 = column_range(n, rank, world)
+    nl = c1 - c0
+    ld = (d + 31) // 32 * 32
+    tdt = torch.float32 if dtype == "float32" else torch.float64
+    storage = torch.zeros(nl, ld, dtype=tdt, device=dev)
+    CH = CFG4["chunk"]
+    g = torch.Generator(device=dev)
+    for j0 in range(c0 // CH * CH, c1, CH):
+        g.manual_seed(CFG4["dict_seed"] + j0 // CH)
+        blk = torch.randn(CH, d, generator=g, device=dev, dtype=torch.float32)
+        blk /= torch.linalg.vector_norm(blk, dim=1, keepdim=True)
+        a, e = max(j0, c0), min(j0 + CH, c1)
+        storage[a - c0:e - c0, :d] = blk[a - j0:e - j0]
+        del blk
+    torch.cuda.empty_cache()
+    D = device.DeviceDictionary.wrap(storage, d)
+    shard = ShardedDictionary(D, c0, n, None if coll is None else getattr(coll, "group", None))
+    ops = DeviceShardOps(shard, coll)
+    rng = np.random.default_rng(CFG4["x_seed"])
+    x0 = np.zeros(n)
+    x0[rng.choice(n, k, replace=False)] = rng.standard_normal(k)
+    xl = device.to_device_vec(x0[c0:c1], max(nl, 1), dev)
+    bd = ops.zeros_d()
+    ops.gemv(xl, bd)
+    ops.allreduce_(bd)
+    b = ops.to_host_d(bd)
+    sigma = CFG4["noise_rel"] * float(np.linalg.norm(b)) / np.sqrt(d)
+    b = b + sigma * rng.standard_normal(d)
+    return shard, b, x0, ops
+
+
+def kkt_certificate(ops, x_local, b, lam):
+    """Independent fp64 optimality certificate of a sharded solution:
+    c = A^T (b - A x) by fresh GEMV / GEMV^T passes (fp64 accumulation) and
+    model.kkt_from_correlation (model.py:160-173) folded over the ranks.
+    Returns (kkt, objective)."""
+    torch = ops.torch
+    xl = device.to_device_vec(x_local, max(ops.nl, 1), ops.dev)
+    ax = ops.zeros_d()
+    ops.gemv(xl, ax)
+    ops.allreduce_(ax)
+    r = ops.from_host_d(b) - ax
+    r[ops.d:] = 0.0
+    c = ops.zeros_n()
+    ops.gemv_t(r, c)
+    x = xl[: ops.nl]
+    c = c[: ops.nl]
+    on = x != 0
+    part = torch.zeros(4, dtype=torch.float64, device=ops.dev)
+    if bool(on.any()):
+        part[0] = (c[on] - lam * torch.sign(x[on])).abs().max()
+    if bool((~on).any()):
+        part[1] = (c[~on].abs() - lam).clamp_min(0.0).max()
+    part[2] = x.abs().sum()
+    part[3] = 0.0
+    g = ops.coll.all_gather(part).view(-1, 4)
+    kk = float(torch.maximum(g[:, 0].max(), g[:, 1].max()).item())
+    rr = float((r[: ops.d] ** 2).sum().item())
+    return kk, 0.5 * rr + lam * float(g[:, 2].sum().item())

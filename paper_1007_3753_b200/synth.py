@@ -98,6 +98,20 @@ def make_problem(w, A=None):
     return ProblemInstance(A, b, ground_truth=x0, noise_sigma=sigma)
 
 
+def cfg5_batch(B, d=512, n=2048, dict_seed=5, seed=55):
+    """Config-5 batch: shared A (d x n, unit columns) and B noiseless
+    instances b_j = A x0_j, k_j ~ U{16..256} N(0,1) values on a uniform
+    support.  Instance j depends only on the draws of instances < j, so any
+    batch is a prefix of a larger one.  Returns (A, X0 (n x B), Bmat (d x B))."""
+    A = gen_gaussian_dict(d, n, dict_seed)
+    rng = np.random.default_rng(seed)
+    X = np.zeros((n, B))
+    for j in range(B):
+        kk = int(rng.integers(16, 257))
+        X[rng.choice(n, kk, replace=False), j] = rng.standard_normal(kk)
+    return A, X, A @ X
+
+
 def cab_dictionary(d=1024, classes=38, per_class=32, subspace=9, seed=0):
     """Face-recognition-style class dictionary for config 3.
 

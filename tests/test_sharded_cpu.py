@@ -26,7 +26,7 @@ def _solve(cid, rank, world):
     c0, c1 = column_range(A.shape[1], rank, world)
     shard = SimpleNamespace(c0=c0, c1=c1, d=A.shape[0], n=A.shape[1])
     P = SimpleNamespace(A=shard, b=b, ground_truth=gt)
-    return sharded_fista_solve(P, cfg, ops=NumpyShardOps(A[:, c0:c1])), gold
+    return sharded_fista_solve(P, cfg, ops=NumpyShardOps(A[:, c0:c1], A.shape[1])), gold
 
 
 @pytest.mark.parametrize("cid", CASES)
