@@ -1,21 +1,30 @@
 #!/usr/bin/env python
-"""Benchmark: l1-min solves/sec on BASELINE config 2 (d=1024, n=4096, k=128,
-1% noise, fp64, default lambda, relative-estimate 1e-6) with the B200 FISTA
-kernel; one step = one complete solve.
+"""Benchmark: BASELINE config 4 — one d=65536 x n=262144 compressed-sensing
+instance (fp32 storage, 64 GiB), FISTA with default lambda and relative
+change in x < 1e-6, column-sharded over the ranks with ONE allreduce per
+backtracking trial and all control on the device.  One step = one complete
+solve; the metric is solver iterations/s of the whole job (config 4 is one
+instance: total work fixed, strong scaling).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference]
 
-N>1 (torchrun): "replicas only" — config 2 is a single instance, so each rank
-solves its own seeded instance (weak scaling, no data-path collective);
-timing is the max over ranks of the CUDA-event totals.
+--gpus N without torchrun re-launches itself under torch.distributed.run
+(one rank per GPU, NCCL).  --impl reference times the reference algorithm's
+CPU implementation (the numpy/OpenBLAS port of shrinkage.fista_solve, all
+host cores) on a scaled proxy of the same instance (d=8192, n=32768, fp64 —
+the reference is fp64-only and a 64 GiB dictionary does not fit its host
+path) and extrapolates by dictionary bytes (x64).  --dry-run drives the
+launcher, the gloo rendezvous and the sharded control protocol on CPU
+(numpy shard ops, small proxy) — no GPU, no timing claim.
 
---impl reference times the reference algorithm's CPU implementation (the
-numpy/OpenBLAS oracle port, all host cores) on the same workload.
+Secondary legs (N=1): configs 1, 2 (all solvers), 3, 5, the HBM streaming
+roofline, the experiment harness and the alignment solvers.
 """
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -27,23 +36,29 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "l1-min solves/sec"
-UNIT = "solves/s"
-WORKLOAD = ("cfg2: single noisy BPDN instance d=1024 n=4096 k=128 sigma=0.01||Ax0||/sqrt(d), "
-            "FISTA, lambda=1e-2||A^T b||_inf, stop relative-estimate 1e-6")
+METRIC = "l1-min solver iterations/sec (config 4: one 65536 x 262144 instance, FISTA)"
+UNIT = "iterations/s"
+WORKLOAD = ("cfg4: single compressed-sensing instance d=65536 n=262144 (A fp32 storage, 64 GiB, unit-norm "
+            "Gaussian columns), k=2048 N(0,1), b = A x0 + 1e-3 relative noise; FISTA, lambda = "
+            "1e-2||A^T b||_inf, stop relative-estimate 1e-6 (max_iter 2000); column-sharded, one NCCL "
+            "allreduce of [A_r x_r | scalar slots] per backtracking trial")
+PROXY = dict(d=8192, n=32768, k=256, seed=4, noise_rel=1e-3)      # = tests/golden cfg4_proxy_fista
+PROXY_SCALE = (65536 * 262144) / (8192 * 32768)                  # dictionary-bytes ratio (64)
+CFG2_WORKLOAD = ("cfg2: single noisy BPDN instance d=1024 n=4096 k=128 sigma=0.01||Ax0||/sqrt(d), "
+                 "FISTA, lambda=1e-2||A^T b||_inf, stop relative-estimate 1e-6")
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--dtype", default="float64", choices=["float64", "float32"])
+    ap.add_argument("--dry-run", action="store_true", help="CPU/gloo dry run of the launcher + protocol")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-stream", action="store_true", help="skip the HBM streaming roofline leg")
     ap.add_argument("--no-secondary", action="store_true",
-                    help="skip the config 1/3/4/5 and all-solver legs")
+                    help="skip the config 1/2/3/5 and all-solver legs")
     ap.add_argument("--cfg5-sweep", action="store_true", help="add the config-5 batch-size sweep leg")
     ap.add_argument("--only-leg", default=None, help="run one secondary leg alone (diagnostics)")
     return ap.parse_args()
@@ -56,6 +71,27 @@ def dist_env():
     return ws, rank, local
 
 
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_launch(args):
+    """--gpus N > 1 outside torchrun: re-run this script under
+    torch.distributed.run with N ranks on this node (rendezvous on
+    127.0.0.1); NCCL's init lines (rings, NVLS) go to stderr."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    env = dict(os.environ)
+    if not args.dry_run and "NCCL_DEBUG" not in env:
+        env.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT,NVLS", NCCL_DEBUG_FILE="/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node=%d" % args.gpus, "--master-addr=127.0.0.1",
+           "--master-port=%d" % _free_port(), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def make_instance(rank):
     from paper_1007_3753_b200 import synth
     w = synth.Workload("cfg2", 1024, 4096, 128, seed=rank, noise_rel=0.01)
@@ -66,6 +102,12 @@ def config(dtype="float64"):
     from paper_1007_3753_b200.model import SolverConfig, StoppingRule
     return SolverConfig(lam=None, tol=1e-6, stopping=StoppingRule("relative-estimate", 1e-6),
                         options={"dtype": dtype})
+
+
+def cfg4_config(max_iter=2000):
+    from paper_1007_3753_b200.model import SolverConfig, StoppingRule
+    return SolverConfig(lam=None, tol=1e-6, max_iter=max_iter,
+                        stopping=StoppingRule("relative-estimate", 1e-6))
 
 
 # ----------------------------------------------------------------- clocks
@@ -137,7 +179,7 @@ def cpu_solve_once(P):
     return oracle.fista(P.A, P.b, lam=None, tol=1e-6, stop=("relative-estimate", 1e-6))
 
 
-def cpu_baseline(P, budget_s=10.0):
+def cpu_baseline_cfg2(P, budget_s=10.0):
     n = 0
     t0 = time.perf_counter()
     its = 0
@@ -148,33 +190,69 @@ def cpu_baseline(P, budget_s=10.0):
         el = time.perf_counter() - t0
         if el >= budget_s and n >= 2:
             break
-    return {"value": n / el, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+    return {"value": n / el, "unit": "solves/s", "cores": os.cpu_count(), "kind": "port",
             "sample": "%d full cfg2 FISTA solves (numpy/OpenBLAS oracle port of "
                       "shrinkage.fista_solve, %d iterations total) in %.1f s" % (n, its, el),
             "iterations_per_sec": its / el}
+
+
+def proxy_problem():
+    from paper_1007_3753_b200 import synth
+    w = synth.Workload("cfg4p", PROXY["d"], PROXY["n"], PROXY["k"], PROXY["seed"], PROXY["noise_rel"])
+    return synth.make_problem(w)
+
+
+def cpu_cfg4_sample(P, iters):
+    """`iters` FISTA iterations of the oracle port (shrinkage.fista_solve
+    restated, numpy/OpenBLAS on all host cores) on the config-4 proxy;
+    returns (seconds, iterations, passes-equivalent)."""
+    import oracle  # CPU baseline / reference arm only
+    t0 = time.perf_counter()
+    r = oracle.fista(P.A, P.b, lam=None, tol=1e-6, max_iter=iters, stop=("relative-estimate", 1e-6))
+    return time.perf_counter() - t0, int(r.iterations)
+
+
+def cpu_baseline_cfg4(budget_s=15.0):
+    P = proxy_problem()
+    cpu_cfg4_sample(P, 2)                      # warm (BLAS threads, page-in)
+    t, its, n = 0.0, 0, 0
+    while t < budget_s or n < 1:
+        dt, k = cpu_cfg4_sample(P, 8)
+        t += dt
+        its += k
+        n += 1
+    v = its / t / PROXY_SCALE
+    return {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": "%d x 8 FISTA iterations (oracle port of shrinkage.fista_solve, numpy/OpenBLAS, "
+                      "fp64) on the d=8192 n=32768 proxy of config 4 in %.1f s; iterations/s divided by "
+                      "the dictionary-bytes ratio %d (streaming-bound on the host)" % (n, t, PROXY_SCALE),
+            "proxy_iterations_per_sec": its / t}
 
 
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    P = make_instance(0)
+    P = proxy_problem()
+    per_step = 4
     for _ in range(args.warmup):
-        cpu_solve_once(P)
-    t0 = time.perf_counter()
-    its = 0
+        cpu_cfg4_sample(P, per_step)
+    t, its = 0.0, 0
     for _ in range(args.steps):
-        its += cpu_solve_once(P).iterations
-    el = time.perf_counter() - t0
-    v = args.steps / el
+        dt, k = cpu_cfg4_sample(P, per_step)
+        t += dt
+        its += k
+    v = its / t / PROXY_SCALE
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic (seeded numpy PCG64, reference generator recipe)",
-           "config": {"workload": WORKLOAD, "parallelism": "host cores (OpenBLAS threads)"},
-           "iterations_per_sec": its / el,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded numpy PCG64 proxy of config 4, reference generator recipe)",
+           "config": {"workload": WORKLOAD, "parallelism": "host cores (OpenBLAS threads)",
+                      "proxy": "d=8192 n=32768 k=256 fp64 (2 GiB), %d FISTA iterations per step, "
+                               "extrapolated x%d by dictionary bytes" % (per_step, PROXY_SCALE)},
            "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                            "sample": "%d full cfg2 FISTA solves" % args.steps},
+                            "sample": "%d steps x %d FISTA iterations on the config-4 proxy"
+                                      % (args.steps, per_step)},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -232,95 +310,121 @@ def _events(torch):
     return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
 
-def leg_cfg4(torch, dev, ws, rank, iters=8, reps=2):
-    """BASELINE config 4: one d=65536 x n=262144 fp32 instance (64 GiB),
-    columns sharded over the ranks, FISTA with one NCCL allreduce of the
-    d-length partial A x per iteration (strong scaling: total work fixed).
-    Dictionary generated on the device (seeded Philox per 2048-column global
-    chunk, so A is the same matrix for every world size); A >> L2, so every
-    panel pass streams from HBM."""
-    from paper_1007_3753_b200 import device as dv
-    from paper_1007_3753_b200.model import SolverConfig
-    from paper_1007_3753_b200.sharded import (DeviceShardOps, ShardedDictionary, ShardedFista,
-                                              column_range)
-    d, n, k = 65536, 262144, 2048
-    c0, c1 = column_range(n, rank, ws)
-    nl = c1 - c0
-    storage = torch.empty(nl, d, dtype=torch.float32, device=dev)
-    CH = 2048
-    g = torch.Generator(device=dev)
-    for j0 in range(c0 // CH * CH, c1, CH):
-        g.manual_seed(7000003 + j0 // CH)
-        blk = torch.randn(CH, d, generator=g, device=dev, dtype=torch.float32)
-        blk /= torch.linalg.vector_norm(blk, dim=1, keepdim=True)
-        a, e = max(j0, c0), min(j0 + CH, c1)
-        storage[a - c0:e - c0] = blk[a - j0:e - j0]
-        del blk
+def _proxy_parity(torch, dev):
+    """The config-4 proxy (d=8192, n=32768) through the same sharded path
+    against the real reference's output (tests/golden/cfg4_proxy_fista.npz)."""
+    from paper_1007_3753_b200 import synth
+    from paper_1007_3753_b200.sharded import ShardedDictionary, ShardedInstance, sharded_fista_solve
+    g = np.load(os.path.join(ROOT, "tests", "golden", "cfg4_proxy_fista.npz"))
+    rc = json.loads(str(g["recipe"]))
+    A = synth.gen_gaussian_dict(rc["d"], rc["n"], rc["seed"])
+    out = {}
+    for dt in ("float64", "float32"):
+        cfg = cfg4_config(5000)
+        cfg.options["dtype"] = dt
+        shard = ShardedDictionary.from_dense(A, 0, 1, dtype=dt, device_ordinal=dev.index)
+        r = sharded_fista_solve(ShardedInstance(shard, g["b"]), cfg)
+        ref = g["x"]
+        out[dt] = {"rel_err_vs_reference": float(np.linalg.norm(r.x_star - ref) / np.linalg.norm(ref)),
+                   "iterations": int(r.iterations), "iterations_reference": int(g["iterations"])}
+        del shard
     torch.cuda.empty_cache()
-    D = dv.DeviceDictionary.wrap(storage, d)
-    shard = ShardedDictionary(D, c0, n, None)
-    ops = DeviceShardOps(shard)
-    rng = np.random.default_rng(44)
-    x0 = np.zeros(n)
-    x0[rng.choice(n, k, replace=False)] = rng.standard_normal(k)
-    xl = ops.from_host_n(x0[c0:c1])
-    bd = ops.zeros_d()
-    ops.gemv(xl, bd)
-    ops.allreduce_(bd)
-    b = ops.to_host_d(bd)
-    sigma = 1e-3 * float(np.linalg.norm(b)) / np.sqrt(d)
-    b = b + sigma * rng.standard_normal(d)
-    # kernel roofline: the two panel passes alone
-    gt_ev, g_ev = _events(torch), _events(torch)
-    r = ops.from_host_d(b)
-    gl = ops.zeros_n()
-    for _ in range(2):
-        ops.gemv(xl, bd)
-        ops.gemv_t(r, gl)
+    return out
+
+
+def headline_cfg4(torch, dev, ws, rank, args):
+    from paper_1007_3753_b200 import device as dv
+    from paper_1007_3753_b200.sharded import (ShardedFista, ShardedInstance, TorchCollective,
+                                              kkt_certificate, make_cfg4_shard, sharded_fista_solve)
+    coll = TorchCollective()
+    t0 = time.perf_counter()
+    shard, b, x0, ops = make_cfg4_shard(rank, ws, dev, coll)
     torch.cuda.synchronize()
-    K = 5
-    g_ev[0].record()
-    for _ in range(K):
-        ops.gemv(xl, bd)
-    g_ev[1].record()
-    gt_ev[0].record()
-    for _ in range(K):
-        ops.gemv_t(r, gl)
-    gt_ev[1].record()
+    gen_s = time.perf_counter() - t0
+    cfg = cfg4_config()
+    b_dev = ops.from_host_d(b)
+    drv = ShardedFista(ops, b, shard.n, cfg, b_device=b_dev)
+    for _ in range(max(args.warmup, 3)):
+        res = drv.solve()
     torch.cuda.synchronize()
-    shard_bytes = nl * d * 4
-    t_gemv = g_ev[0].elapsed_time(g_ev[1]) / 1e3 / K
-    t_gemvt = gt_ev[0].elapsed_time(gt_ev[1]) / 1e3 / K
-    cfg = SolverConfig(lam=None, tol=1e-6, max_iter=iters)
-    drv = ShardedFista(ops, b, n, cfg)
-    drv.solve()                                   # warm-up
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    clocks.wait_ready()
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    s, e = _events(torch)
-    s.record()
-    passes = 0
-    its = 0
-    for _ in range(reps):
+    spans, its, passes, rounds, trials = [], 0, 0, 0, 0
+    ops.timing = []
+    for _ in range(args.steps):
+        ev = _events(torch)
+        drv.span_events = ev
         res = drv.solve()
-        passes += drv.passes
+        spans.append(ev)
         its += res.iterations
-    e.record()
+        passes += drv.passes
+        rounds += drv.rounds
+        trials += drv.trials
     torch.cuda.synchronize()
-    t = torch.tensor([s.elapsed_time(e) / 1e3], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.barrier()
+    drv.span_events = None
+    timing, ops.timing = ops.timing, None
+    tot = sum(s.elapsed_time(e) for s, e in spans) / 1e3
+    t_pre = sum(e[0].elapsed_time(e[1]) for e in timing) / 1e3
+    t_coll = sum(e[1].elapsed_time(e[2]) for e in timing) / 1e3
+    t_post = sum(e[2].elapsed_time(e[3]) for e in timing) / 1e3
+    t = torch.tensor([tot, t_pre + t_post], dtype=torch.float64, device=dev)
     if ws > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    tmax = float(t.item())
-    out = {"workload": "cfg4: d=65536 n=262144 fp32 storage (64 GiB) k=2048, 1e-3 relative noise, "
-                       "FISTA, default lambda, %d iterations per solve" % iters,
-           "n_gpus": ws, "scaling": "strong", "parallelism": "column-sharded, NCCL allreduce of "
-           "A_r x_r per backtracking trial" if ws > 1 else "single GPU (whole dictionary)",
-           "iterations_per_sec": its / tmax, "ms_per_iteration": 1e3 * tmax / its,
-           "passes_per_iteration": passes / its,
-           "achieved_gbs_per_gpu": passes * shard_bytes / tmax / 1e9,
-           "gemv_gbs": shard_bytes / t_gemv / 1e9, "gemv_t_gbs": shard_bytes / t_gemvt / 1e9,
-           "l2": "none needed (64 GiB dictionary >> 126 MB L2)"}
-    del drv, ops, shard, D, storage
+    tmax, tkern = float(t[0].item()), float(t[1].item())
+    value = its / tmax
+    # end to end through the public API: host b in (pinned), host x + trace out
+    e2e_steps = max(1, min(args.steps, 5))
+    b_pin = torch.from_numpy(b).pin_memory().numpy()
+    sharded_fista_solve(ShardedInstance(shard, b_pin), cfg, ops=ops)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    es, ee = _events(torch)
+    e_its = 0
+    es.record()
+    for _ in range(e2e_steps):
+        r2 = sharded_fista_solve(ShardedInstance(shard, b_pin), cfg, ops=ops)
+        e_its += r2.iterations
+    ee.record()
+    torch.cuda.synchronize()
+    ck = clocks.stop()
+    te = torch.tensor([es.elapsed_time(ee) / 1e3], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+    e2e_val = e_its / float(te.item())
+    # certificate of the last solution (fp64 recomputation of c = A^T (b - A x))
+    lam = 1e-2 * ops.setup(b)
+    kk, F = kkt_certificate(ops, res.x_star[shard.c0:shard.c1], b, lam)
+    shard_bytes = shard.local.n * shard.d * 4
+    alg = passes * shard_bytes
+    out = {"value": value, "ms_per_step": 1e3 * tmax / args.steps, "iterations": its,
+           "solves_per_sec": args.steps / tmax, "iterations_per_solve": its / args.steps,
+           "passes_per_iteration": passes / its, "trials_per_iteration": trials / its,
+           "rounds_per_solve": rounds / args.steps, "gen_seconds": gen_s,
+           "gpu_launches": args.steps * 5 + 6 * rounds,
+           "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(b.nbytes),
+                   "d2h_bytes_per_step": int(shard.n * 8 + 32 * res.iterations + 160),
+                   "api": "paper_1007_3753_b200.sharded.sharded_fista_solve(ShardedInstance(shard, b), config): "
+                          "pinned host b in, host x (n) + trace out; dictionary resident (64 GiB)"},
+           "kernel_seconds": {"pre (prox + A_r x)": t_pre, "allreduce": t_coll,
+                              "post (decide + A_r^T r + rotate/KKT)": t_post, "step_total": tot},
+           "achieved_gbs": alg / tkern / 1e9, "step_gbs": alg / tmax / 1e9,
+           "shard_bytes": shard_bytes,
+           "certificate": {"kkt_fp64": kk, "lambda": lam, "kkt_over_lambda": kk / lam,
+                           "objective": F, "objective_trace": res.trace[-1].objective,
+                           "converged": bool(res.converged),
+                           "x0_large_entries_recovered": bool(np.all(res.x_star[np.abs(x0) > 4 * lam] != 0))},
+           "clocks": ck}
+    if ws > 1:
+        import torch.distributed as dist
+        out["nccl"] = {"backend": dist.get_backend(), "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))}
+    del drv, ops, shard, b_dev
     torch.cuda.empty_cache()
     return out
 
@@ -768,6 +872,70 @@ def leg_solvers_cfg2(torch, P, reps=3):
     return out
 
 
+def leg_cfg2(torch, dev, steps=20, warmup=3, dtype="float64"):
+    """BASELINE config 2 (configs[1]): one complete FISTA solve per step on the
+    resident 32 MiB dictionary (SMEM/L2-resident after the first pass: the
+    single persistent kernel is latency-bound, reported against HBM for
+    reference only), plus its end-to-end public call and the CPU port."""
+    from paper_1007_3753_b200 import device as dv
+    from paper_1007_3753_b200.model import ProblemInstance
+    from paper_1007_3753_b200.shrinkage import FistaPlan, fista_solve
+    import oracle  # checker: parity of the timed solve
+    P = make_instance(0)
+    cfg = config(dtype)
+    D = dv.DeviceDictionary(P.A, dtype=dtype, device=dev.index)
+    Pd = ProblemInstance.__new__(ProblemInstance)
+    Pd.A, Pd.b, Pd.ground_truth, Pd.noise_sigma = D, P.b, P.ground_truth, P.noise_sigma
+    plan = FistaPlan(Pd, cfg)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # 512 MiB > L2
+    for _ in range(max(warmup, 3)):
+        plan.launch()
+    torch.cuda.synchronize()
+    res = plan.result()
+    iters = res.iterations
+    passes = plan.passes()
+    ev = [_events(torch) for _ in range(steps)]
+    torch.cuda.synchronize()
+    for s, e in ev:
+        flush.zero_()                      # evict A from L2 between timed steps
+        s.record()
+        plan.launch()
+        e.record()
+    torch.cuda.synchronize()
+    tot = sum(s.elapsed_time(e) for s, e in ev) / 1e3
+    e2e_steps = 5
+    pin_A = torch.from_numpy(P.A).pin_memory()
+    pin_b = torch.from_numpy(P.b).pin_memory()
+    Ph = ProblemInstance(pin_A.numpy(), pin_b.numpy(), ground_truth=P.ground_truth)
+    fista_solve(Ph, cfg)
+    torch.cuda.synchronize()
+    es, ee = _events(torch)
+    es.record()
+    for _ in range(e2e_steps):
+        r = fista_solve(Ph, cfg)
+    ee.record()
+    torch.cuda.synchronize()
+    e2e_val = e2e_steps / (es.elapsed_time(ee) / 1e3)
+    ref = cpu_solve_once(P)
+    err = float(np.linalg.norm(res.x_star - ref.x) / np.linalg.norm(ref.x))
+    sz = 8 if dtype == "float64" else 4
+    alg = passes * P.d * P.n * sz
+    t1 = tot / steps
+    del flush, plan, D
+    torch.cuda.empty_cache()
+    return {"workload": CFG2_WORKLOAD, "solves_per_sec": steps / tot, "ms_per_solve": 1e3 * t1,
+            "iterations_per_solve": iters, "us_per_iteration": 1e6 * t1 / iters,
+            "parity": {"rel_err_vs_oracle": err, "iterations_oracle": ref.iterations, "iterations_b200": iters},
+            "e2e": {"value": e2e_val, "unit": "solves/s", "h2d_bytes_per_step": int(P.A.nbytes + P.b.nbytes),
+                    "d2h_bytes_per_step": int(P.n * 8 + 32 * r.iterations + 256),
+                    "api": "shrinkage.fista_solve(P, config), pinned host A/b"},
+            "roofline_l2": {"bound": "latency (A 32 MiB is SMEM/L2-resident after the first pass)",
+                            "dictionary_bytes_per_second": alg / t1 / 1e9, "unit": "GB/s",
+                            "passes_per_solve": passes,
+                            "note": "2 grid barriers + region reductions per iteration; see profiles/"},
+            "cpu_baseline": cpu_baseline_cfg2(P)}
+
+
 def run_b200(args):
     import torch
     ws, rank, local = dist_env()
@@ -779,127 +947,65 @@ def run_b200(args):
     torch.cuda.set_device(dev)
     if args.only_leg:
         legs = {"harness": lambda: leg_harness(torch), "cfg1": lambda: leg_cfg1(torch),
-                "align": lambda: leg_align(torch), "cfg4": lambda: leg_cfg4(torch, dev, ws, rank),
+                "align": lambda: leg_align(torch), "cfg2": lambda: leg_cfg2(torch, dev),
                 "cfg3": lambda: leg_cfg3(torch, dev), "cfg5": lambda: leg_cfg5(torch, dev, ws),
                 "cfg5_sweep": lambda: leg_cfg5_sweep(torch, dev),
-                "solvers_cfg2": lambda: leg_solvers_cfg2(torch, make_instance(rank))}
-        print(json.dumps({args.only_leg: legs[args.only_leg]()}), flush=True)
+                "solvers_cfg2": lambda: leg_solvers_cfg2(torch, make_instance(rank)),
+                "cfg4": lambda: headline_cfg4(torch, dev, ws, rank, args),
+                "proxy": lambda: _proxy_parity(torch, dev)}
+        r = legs[args.only_leg]()
+        if rank == 0:
+            print(json.dumps({args.only_leg: r}), flush=True)
         return
 
-    from paper_1007_3753_b200 import device as dv
-    from paper_1007_3753_b200.model import ProblemInstance
-    from paper_1007_3753_b200.shrinkage import FistaPlan, fista_solve
-
-    P = make_instance(rank)
-    cfg = config(args.dtype)
-    D = dv.DeviceDictionary(P.A, dtype=args.dtype, device=dev.index)
-    Pd = ProblemInstance.__new__(ProblemInstance)
-    Pd.A, Pd.b, Pd.ground_truth, Pd.noise_sigma = D, P.b, P.ground_truth, P.noise_sigma
-    plan = FistaPlan(Pd, cfg)
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # 512 MiB > L2
-
-    for _ in range(max(args.warmup, 3)):
-        plan.launch()
-    torch.cuda.synchronize()
-    res = plan.result()
-    iters = res.iterations
-    passes = plan.passes()
-
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    clocks = ClockSampler(dev.index)
-    clocks.start()
-    clocks.wait_ready()
-    if ws > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    for s, e in ev:
-        flush.zero_()                      # evict A from L2 between timed steps
-        s.record()
-        plan.launch()
-        e.record()
-    torch.cuda.synchronize()
-    if ws > 1:
-        torch.distributed.barrier()
-    tot = sum(s.elapsed_time(e) for s, e in ev) / 1e3
-    t = torch.tensor([tot], dtype=torch.float64, device=dev)
-    if ws > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    tmax = float(t.item())
-    value = ws * args.steps / tmax
-    ms = 1e3 * tmax / args.steps
-
-    # end to end through the public API: pinned host A, b -> solve -> host x
-    e2e_steps = max(1, min(args.steps, 5))
-    pin_A = torch.from_numpy(P.A).pin_memory()
-    pin_b = torch.from_numpy(P.b).pin_memory()
-    Ph = ProblemInstance(pin_A.numpy(), pin_b.numpy(), ground_truth=P.ground_truth)
-    fista_solve(Ph, cfg)
-    torch.cuda.synchronize()
-    if ws > 1:
-        torch.distributed.barrier()
-    es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    es.record()
-    for _ in range(e2e_steps):
-        r = fista_solve(Ph, cfg)
-    ee.record()
-    torch.cuda.synchronize()
-    # the sampler ran across the timed region and the e2e leg (>= 100 ms of load)
-    ck = clocks.stop()
-    if ck is not None:
-        ck["window"] = "timed steps + e2e leg"
-    te = torch.tensor([es.elapsed_time(ee) / 1e3], dtype=torch.float64, device=dev)
-    if ws > 1:
-        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-    e2e_val = ws * e2e_steps / float(te.item())
-    h2d = P.A.nbytes + P.b.nbytes
-    d2h = P.n * 8 + 4 * 8 * r.iterations + 256
-
+    h = headline_cfg4(torch, dev, ws, rank, args)
     out = None
     if rank == 0:
-        import oracle  # checker: parity of the timed solve
-        ref = cpu_solve_once(P)
-        err = float(np.linalg.norm(res.x_star - ref.x) / np.linalg.norm(ref.x))
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
-            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+        peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        peaks = json.load(open(peaks_path)) if os.path.exists(peaks_path) else {}
         peak = float(peaks.get("hbm_gbs", 6650.0))
-        peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-        sz = 8 if args.dtype == "float64" else 4
-        alg_bytes = passes * P.d * P.n * sz
-        achieved = alg_bytes / (tmax / args.steps) / 1e9
         traffic = None
-        prof = os.path.join(ROOT, "profiles", "r01_ncu_fista_cfg2.json")
-        if os.path.exists(prof) and args.dtype == "float64":
+        prof = os.path.join(ROOT, "profiles", "r02_ncu_cfg4_kernels.json")
+        if os.path.exists(prof):
             try:
-                traffic = json.load(open(prof))["kernels"][0].get("dram_traffic_bytes")
-            except (ValueError, KeyError, IndexError):
+                traffic = json.load(open(prof)).get("dram_bytes_per_pass")
+            except ValueError:
                 traffic = None
-        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
-               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-               "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-               "dtype": "f64" if args.dtype == "float64" else "f32 storage / f64 accumulate",
-               "data": "synthetic (seeded numpy PCG64, reference generator recipe)",
-               "config": {"workload": WORKLOAD, "solver": "fista", "parallelism":
-                          "replicas only (one independent instance per rank)" if ws > 1 else "single GPU",
-                          "l2": "512 MiB buffer written between timed steps (A is 32 MiB)"},
-               "iterations_per_solve": iters,
-               "iterations_per_sec": value * iters,
-               "parity": {"rel_err_vs_oracle": err, "iterations_oracle": ref.iterations,
-                          "iterations_b200": iters},
-               "gpu_launches": args.steps,
-               "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                       "d2h_bytes_per_step": int(d2h),
-                       "api": "paper_1007_3753_b200.shrinkage.fista_solve(P, config), pinned host A/b"},
-               "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                            "frac": achieved / peak, "traffic": traffic,
-                            "kernel": "fista_kernel<%s> (whole solve = 1 launch)" % (
-                                "double" if sz == 8 else "float"),
-                            "algorithmic_bytes_per_launch": alg_bytes,
-                            "passes_per_launch": passes,
-                            "peak_source": peak_src,
-                            "note": "A (32 MiB) is L2-resident after the first pass of a solve; "
-                                    "see roofline_stream for the HBM-streaming case"},
-               "clocks": ck}
+        out = {"metric": METRIC, "value": h["value"], "unit": UNIT, "n_gpus": ws,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": h["ms_per_step"],
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+               "dtype": "f32 storage / f64 accumulate",
+               "data": "synthetic (device Philox dictionary per 2048-column chunk, numpy PCG64 x0/noise)",
+               "config": {"workload": WORKLOAD, "solver": "fista",
+                          "parallelism": "column-sharded over %d GPU(s), one NCCL allreduce per trial" % ws
+                          if ws > 1 else "single GPU (whole 64 GiB dictionary)",
+                          "l2": "inputs larger than L2 (64 GiB dictionary >> 126 MB L2); no flush needed"},
+               "solves_per_sec": h["solves_per_sec"], "iterations_per_solve": h["iterations_per_solve"],
+               "gpu_launches": h["gpu_launches"],
+               "e2e": h["e2e"],
+               "roofline": {"bound": "hbm", "achieved": h["achieved_gbs"], "peak": peak, "unit": "GB/s",
+                            "frac": h["achieved_gbs"] / peak, "traffic": traffic,
+                            "kernel": "the two dictionary passes: gemv_partial_kernel<float> (A_r x) and "
+                                      "gemv_t_stream_kernel (A_r^T r), with the elementwise round kernels",
+                            "algorithmic": "d * n_local * 4 bytes per pass (%d bytes); passes = 1 A_r x per "
+                                           "trial + 1 A_r^T r per accepted iteration; time = CUDA events "
+                                           "around ell1_sfista_pre + ell1_sfista_post of every timed round "
+                                           "(collective excluded)" % h["shard_bytes"],
+                            "step_gbs": h["step_gbs"],
+                            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"
+                            if "hbm_gbs" in peaks else "fallback"},
+               "headline_detail": {k: h[k] for k in ("iterations", "passes_per_iteration", "trials_per_iteration",
+                                                      "rounds_per_solve", "kernel_seconds", "gen_seconds",
+                                                      "certificate") if k in h},
+               "clocks": h["clocks"]}
+        if "nccl" in h:
+            out["nccl"] = h["nccl"]
+        if ws == 1:
+            try:
+                out["parity"] = {"cfg4_proxy_vs_reference": _proxy_parity(torch, dev),
+                                 "cfg4_full_scale_certificate": h["certificate"]}
+            except Exception as exc:  # pragma: no cover - report, do not abort the bench
+                out["parity"] = {"error": str(exc)[:200]}
         if not args.no_stream and ws == 1:
             try:
                 rs = stream_roofline(torch, dev)
@@ -910,10 +1016,10 @@ def run_b200(args):
                 out["roofline_stream"] = {"error": str(exc)[:200]}
         if not args.no_secondary and ws == 1:
             sec = {}
-            legs2 = [("cfg1", lambda: leg_cfg1(torch))]
+            legs2 = [("cfg2", lambda: leg_cfg2(torch, dev)), ("cfg1", lambda: leg_cfg1(torch))]
             if args.cfg5_sweep:
                 legs2.append(("cfg5_sweep", lambda: leg_cfg5_sweep(torch, dev)))
-            legs2 += [("solvers_cfg2", lambda: leg_solvers_cfg2(torch, P)),
+            legs2 += [("solvers_cfg2", lambda: leg_solvers_cfg2(torch, make_instance(0))),
                       ("cfg3", lambda: leg_cfg3(torch, dev)),
                       ("cfg5", lambda: leg_cfg5(torch, dev, ws)),
                       ("harness", lambda: leg_harness(torch)),
@@ -925,15 +1031,7 @@ def run_b200(args):
                     sec[name] = {"error": str(exc)[:200]}
             out["secondary"] = sec
         if ws == 1 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline(P)
-    if not args.no_secondary:
-        # config 4 runs on every rank (column-sharded, collective)
-        try:
-            c4 = leg_cfg4(torch, dev, ws, rank)
-        except Exception as exc:  # pragma: no cover - best effort leg
-            c4 = {"error": str(exc)[:200]}
-        if out is not None:
-            out.setdefault("secondary", {})["cfg4"] = c4
+            out["cpu_baseline"] = cpu_baseline_cfg4()
     if ws > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
@@ -941,9 +1039,43 @@ def run_b200(args):
         print(json.dumps(out), flush=True)
 
 
+def run_dry(args):
+    """CPU dry run (no GPU): the launcher, a gloo rendezvous and the sharded
+    control protocol (numpy restatement of the device rounds, one allreduce
+    per round) on the config-1-sized proxy; prints the bench line shape with
+    n_gpus = world size.  Not a measurement."""
+    import torch.distributed as dist
+    ws, rank, _ = dist_env()
+    if ws > 1:
+        dist.init_process_group("gloo")
+    from paper_1007_3753_b200 import synth
+    from paper_1007_3753_b200.sharded import ShardedFista, column_range
+    from tests.shard_numpy_ops import NumpyShardOps
+    P = synth.make_problem(synth.Workload("dry", 500, 1000, 50, seed=0, noise_rel=1e-3))
+    c0, c1 = column_range(P.n, rank, ws)
+    drv = ShardedFista(NumpyShardOps(P.A[:, c0:c1], P.n), P.b, P.n, cfg4_config())
+    t0 = time.perf_counter()
+    res = drv.solve()
+    el = time.perf_counter() - t0
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": ws, "dry_run": True,
+                          "backend": "gloo" if ws > 1 else "none", "iterations": res.iterations,
+                          "rounds": drv.rounds, "converged": bool(res.converged), "seconds": el,
+                          "note": "CPU dry run of the launcher and the one-allreduce-per-round protocol "
+                                  "(d=500 n=1000 proxy, numpy shard ops); no timing claim"}), flush=True)
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
+    rc = maybe_launch(args)
+    if rc is not None:
+        sys.exit(rc)
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_b200(args)

@@ -190,6 +190,7 @@ class DeviceShardOps:
         self.gt = None
         self.trace = None
         self.bufs = None
+        self.timing = None      # list -> per-round events (pre | collective | post), bench only
 
     # -- primitives (set-up, power iteration) --------------------------------
     def zeros_d(self):
@@ -218,10 +219,11 @@ class DeviceShardOps:
     # -- the solve --------------------------------------------------------------
     def setup(self, b, gt_local=None):
         """r = -b, g = A_r^T r, and the global max|A^T b| (one slot allreduce).
+        ``b`` is a host vector or a device tensor of ld entries (resident).
         Returns c0."""
         self.vec.zero_()
         self.dvec.zero_()
-        self.b = self.from_host_d(b)
+        self.b = b if isinstance(b, self.torch.Tensor) else self.from_host_d(b)
         self.gt = device.to_device_vec(gt_local, max(self.nl, 1), self.dev) if gt_local is not None else None
         _lib.check(self.L.ell1_shard_resid(self.d, device.ptr(self.rn), device.ptr(self.b), device.ptr(self.r),
                                            0.0, device.ptr(self.r), device.ptr(self.out8),
@@ -254,11 +256,22 @@ class DeviceShardOps:
         """One backtracking trial: pre (prox, A_r x_n) -> allreduce -> post."""
         V = ctypes.byref(self.bufs)
         cp = ctypes.c_void_p(self.ctl.data_ptr())
+        ev = None
+        if self.timing is not None:
+            ev = [self.torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev[0].record()
         _lib.check(self.L.ell1_sfista_pre(ctypes.byref(self.view), cp, V, device.ptr(self.ws), self.ws_bytes,
                                           self.stream), "ell1_sfista_pre")
+        if ev:
+            ev[1].record()
         self.coll.allreduce_(self.xchg)
+        if ev:
+            ev[2].record()
         _lib.check(self.L.ell1_sfista_post(ctypes.byref(self.view), cp, V, device.ptr(self.ws), self.ws_bytes,
                                            self.stream), "ell1_sfista_post")
+        if ev:
+            ev[3].record()
+            self.timing.append(ev)
 
     def poll_async(self):
         """Queue a read of ctl->state into pinned memory; returns a handle."""
@@ -331,10 +344,12 @@ class ShardedFista:
 
     ROUNDS_PER_POLL = 8
 
-    def __init__(self, ops, b, n_global, config, gt_local=None, gt_norm=0.0):
+    def __init__(self, ops, b, n_global, config, gt_local=None, gt_norm=0.0, b_device=None):
         self.ops = ops
         self.config = config
         self.b_host = np.asarray(b, dtype=np.float64)
+        self.b_device = b_device     # optional resident copy of b (skips the H2D)
+        self.span_events = None      # optional (start, end) CUDA events around the device work
         self.n = int(n_global)
         self.gt_local = gt_local
         self.gt_norm = float(gt_norm)
@@ -350,7 +365,9 @@ class ShardedFista:
         if kind == "ground-truth-distance" and self.gt_local is None:
             raise ValueError("ground-truth-distance rule needs a ground truth")
         bn2 = float(self.b_host @ self.b_host)
-        c0 = o.setup(self.b_host, self.gt_local)
+        if self.span_events:
+            self.span_events[0].record()
+        c0 = o.setup(self.b_host if self.b_device is None else self.b_device, self.gt_local)
         lam_bar = float(cfg.lam) if cfg.lam is not None else 1e-2 * c0
         if c0 == 0.0:                                   # shrinkage.py:245-247
             self.passes, self.trials, self.rounds = 1, 0, 0
@@ -390,6 +407,8 @@ class ShardedFista:
             prev = h
             if rounds > limit:
                 raise DeviceError("sharded FISTA did not finish within %d rounds" % limit)
+        if self.span_events:
+            self.span_events[1].record()
         ctl, tr, x = o.result()
         self.rounds = rounds
         self.passes = 1 + int(ctl.passes)
