@@ -968,8 +968,9 @@ def run_b200(args):
         prof = os.path.join(ROOT, "profiles", "r02_ncu_cfg4_kernels.json")
         if os.path.exists(prof):
             try:
-                traffic = json.load(open(prof)).get("dram_bytes_per_pass")
-            except ValueError:
+                # ncu dram read+write per pass, measured on the 8 GiB shard, scaled to this run's shard
+                traffic = json.load(open(prof))["traffic_over_algorithmic"] * h["shard_bytes"]
+            except (ValueError, KeyError):
                 traffic = None
         out = {"metric": METRIC, "value": h["value"], "unit": UNIT, "n_gpus": ws,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": h["ms_per_step"],
@@ -992,6 +993,9 @@ def run_b200(args):
                                            "around ell1_sfista_pre + ell1_sfista_post of every timed round "
                                            "(collective excluded)" % h["shard_bytes"],
                             "step_gbs": h["step_gbs"],
+                            "traffic_source": "profiles/r02_ncu_cfg4_kernels.json: dram__bytes_read.sum + "
+                                              "dram__bytes_write.sum per pass (mean of the two passes) / "
+                                              "algorithmic bytes, x this run's bytes per pass",
                             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"
                             if "hbm_gbs" in peaks else "fallback"},
                "headline_detail": {k: h[k] for k in ("iterations", "passes_per_iteration", "trials_per_iteration",

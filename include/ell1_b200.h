@@ -476,7 +476,11 @@ typedef struct {
   double* e;
   int32_t* status;
   int32_t* iterations;  /* optional */
+  double* Bstage;       /* global staging of B when (d+1) m doubles exceed the SM's
+                           shared memory: ell1_align_stage_bytes() bytes, else NULL */
 } ell1_align_t;
+/* bytes of global B staging a launch of this shape needs (0: B fits in shared memory) */
+size_t ell1_align_stage_bytes(int32_t kind, int32_t count, int32_t d, int32_t m);
 /* align_palm_solve per image (robust.py:470-515) */
 int ell1_align_palm_batch(const ell1_align_t* A, void* stream);
 /* align_ist_solve per image (robust.py:427-467) */
@@ -502,6 +506,19 @@ int ell1_blas_fp32_mode(void);
 size_t ell1_gemm_f32_workspace(int32_t trans, int64_t M, int64_t K);
 int ell1_gemm_f32(int32_t trans, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
                   int64_t ldb, float* C, int64_t ldc, void* ws, size_t wsb, void* stream);
+/* fp64 product on the DMMA tensor path (dmma_gemm.cu): C (M x N, column-major,
+ * ldc) = op(A) op(B), transA: A is K x M (else M x K), transB: B is N x K (else
+ * K x N); not both transposed.  The batched solvers' float64 dictionary
+ * products (the reference's A @ X / A.T @ R, shrinkage.py:271-272, alm.py:179-181,
+ * 239-249, and pdipa.py:150-153's weighted Gram) all go through it. */
+int ell1_gemm_f64(int32_t transA, int32_t transB, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                  const double* B, int64_t ldb, double* C, int64_t ldc, void* stream);
+/* the same with a fixed tile variant (0: 64x64x4 stages, 1: 64x64x3, 2: 128x64,
+ * 3: 64x128, 4: 128x128) and K split (1/2/4/8 CTAs of a cluster, -1 auto); tuning */
+int ell1_gemm_f64_variant(int32_t variant, int32_t split, int32_t transA, int32_t transB, int64_t M, int64_t N,
+                          int64_t K, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                          int64_t ldc, void* stream);
+
 
 /* library / device info */
 int ell1_device_sms(int32_t device);

@@ -123,7 +123,8 @@ class Align(ctypes.Structure):
                 ("b_stride", ctypes.c_int64), ("rhs", ctypes.c_void_p), ("ld_rhs", ctypes.c_int64),
                 ("tol", ctypes.c_double), ("mu0", ctypes.c_double), ("rho", ctypes.c_double),
                 ("lam", ctypes.c_double), ("v0", ctypes.c_void_p), ("w", ctypes.c_void_p),
-                ("e", ctypes.c_void_p), ("status", ctypes.c_void_p), ("iterations", ctypes.c_void_p)]
+                ("e", ctypes.c_void_p), ("status", ctypes.c_void_p), ("iterations", ctypes.c_void_p),
+                ("Bstage", ctypes.c_void_p)]
 
 
 P = ctypes.POINTER
@@ -244,6 +245,7 @@ _SIGS = {
     "ell1_homotopy_group": (ctypes.c_int, [P(Group), ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
                                            ctypes.c_void_p]),
     "ell1_blas_fp32_mode": (ctypes.c_int, []),
+    "ell1_align_stage_bytes": (ctypes.c_size_t, [ctypes.c_int32] * 4),
     "ell1_align_palm_batch": (ctypes.c_int, [P(Align), ctypes.c_void_p]),
     "ell1_align_ist_batch": (ctypes.c_int, [P(Align), ctypes.c_void_p]),
     "ell1_align_homotopy_batch": (ctypes.c_int, [P(Align), ctypes.c_void_p]),
@@ -253,6 +255,12 @@ _SIGS = {
                                      ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
                                      ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t,
                                      ctypes.c_void_p]),
+    "ell1_gemm_f64": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
+                                     ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                     ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]),
+    "ell1_gemm_f64_variant": (ctypes.c_int, [ctypes.c_int32] * 4 + [ctypes.c_int64] * 3 +
+                              [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
+                               ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]),
     "ell1_device_sms": (ctypes.c_int, [ctypes.c_int32]),
     "ell1_version": (ctypes.c_char_p, []),
 }

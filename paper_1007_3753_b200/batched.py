@@ -33,33 +33,34 @@ class BatchResult:
     lam: np.ndarray = None     # homotopy: lambda reached per instance
     notes: np.ndarray = None   # homotopy: ridge flag per instance
 
+    def result(self, j):
+        """SolverResult of instance j (reference record type)."""
+        st = int(self.status[j])
+        raise_for(st, {_lib.BREAKDOWN: "backtracking exceeded 100 growth steps",
+                       _lib.ILL_CONDITIONED: "dual least-squares step failed its residual contract",
+                       _lib.NOT_PD: "active-set Gram is singular",
+                       _lib.DEGENERATE: "active-set Gram is singular"})
+        it = int(self.iterations[j])
+        tr = []
+        if self.trace is not None:
+            if st == _lib.ZERO_DATA:
+                rows = 1
+            else:
+                rows = it + 1 if self.kind == "dalm" else it
+            tr = [TraceEntry(int(r[0]), float(r[1]), float(r[2]), int(r[3]))
+                  for r in self.trace[j, :rows]]
+        notes = ()
+        if self.kind == "dalm" and not self.converged[j] and it >= self.max_iter:
+            notes = ("iteration budget exhausted",)
+        if self.kind == "homotopy" and self.notes is not None and self.notes[j]:
+            notes = ("ridge-regularized gram",)
+        B = self.x.shape[1]
+        return SolverResult(self.x[:, j].copy(), it, self.wall_time_seconds / B,
+                            bool(self.converged[j]), tr, notes)
+
     def results(self):
         """Per-instance SolverResult records (reference record type)."""
-        out = []
-        B = self.x.shape[1]
-        for j in range(B):
-            st = int(self.status[j])
-            raise_for(st, {_lib.BREAKDOWN: "backtracking exceeded 100 growth steps",
-                           _lib.ILL_CONDITIONED: "dual least-squares step failed its residual contract",
-                           _lib.NOT_PD: "active-set Gram is singular",
-                           _lib.DEGENERATE: "active-set Gram is singular"})
-            it = int(self.iterations[j])
-            tr = []
-            if self.trace is not None:
-                if st == _lib.ZERO_DATA:
-                    rows = 1
-                else:
-                    rows = it + 1 if self.kind == "dalm" else it
-                tr = [TraceEntry(int(r[0]), float(r[1]), float(r[2]), int(r[3]))
-                      for r in self.trace[j, :rows]]
-            notes = ()
-            if self.kind == "dalm" and not self.converged[j] and it >= self.max_iter:
-                notes = ("iteration budget exhausted",)
-            if self.kind == "homotopy" and self.notes is not None and self.notes[j]:
-                notes = ("ridge-regularized gram",)
-            out.append(SolverResult(self.x[:, j].copy(), it, self.wall_time_seconds / B,
-                                    bool(self.converged[j]), tr, notes))
-        return out
+        return [self.result(j) for j in range(self.x.shape[1])]
 
 
 def _dict_view(A, config):
@@ -130,6 +131,31 @@ def _collect(bufs, t0, dev, trace_offset=0):
 SMALL_B = 4     # below this, one persistent single-instance launch per column wins
 
 
+def _empty(kind, A, Bmat, config):
+    """The result of a batch with no instances (e.g. a rank's empty share)."""
+    if hasattr(A, "device_extension"):
+        D, _ = A.device_extension()
+        N = D.n + D.d
+    else:
+        N = int(np.shape(A)[1]) if not hasattr(A, "n") else int(A.n)
+    res = BatchResult(np.zeros((N, 0)), np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0, np.int32),
+                      0.0, None, kind, config.max_iter)
+    if kind == "homotopy":
+        res.lam = np.zeros(0)
+        res.notes = np.zeros(0, np.int32)
+    return res
+
+
+def _status_of(exc):
+    """Per-instance status code of a single-instance solver exception."""
+    from paper_1007_3753_b200 import exceptions as ex
+    for cls, code in ((ex.NumericalBreakdownError, _lib.BREAKDOWN), (ex.IllConditionedError, _lib.ILL_CONDITIONED),
+                      (ex.NotPositiveDefiniteError, _lib.NOT_PD), (ex.DegenerateSupportError, _lib.DEGENERATE)):
+        if isinstance(exc, cls):
+            return code
+    return None
+
+
 def _ncols(Bmat):
     shape = getattr(Bmat, "shape", None)
     if shape is None:
@@ -156,13 +182,28 @@ def _small_batch(kind, A, Bmat, config, with_trace, target=None):
         P = ProblemInstance.__new__(ProblemInstance)
         P.A, P.b, P.ground_truth, P.noise_sigma = A if hasattr(A, "device_extension") else D, \
             np.ascontiguousarray(Bmat[:, j]), None, None
-        if kind == "fista":
-            r = fista_solve(P, config)
-        elif kind == "dalm":
-            r = dalm_solve(P, config)
-        else:
-            r, lam = hom.solve_path(P.A, P.b, target, config)
-            lams.append(lam)
+        try:
+            if kind == "fista":
+                r = fista_solve(P, config)
+            elif kind == "dalm":
+                r = dalm_solve(P, config)
+            else:
+                r, lam = hom.solve_path(P.A, P.b, target, config)
+                lams.append(lam)
+        except Exception as exc:  # noqa: BLE001 - numerical failures become per-instance status
+            code = _status_of(exc)
+            if code is None:
+                raise
+            # same as the batched path: status recorded, raised by BatchResult.result(j)
+            xs.append(np.zeros(N))
+            its.append(0)
+            conv.append(0)
+            stat.append(code)
+            notes.append(0)
+            traces.append(np.zeros((0, 4)))
+            if kind == "homotopy":
+                lams.append(float("nan"))
+            continue
         xs.append(r.x_star)
         its.append(r.iterations)
         conv.append(int(r.converged))
@@ -198,6 +239,9 @@ def src_classify(A, class_labels, Bmat, config):
     ext = A if hasattr(A, "device_extension") else ExtendedDictionary(
         A, 1.0 / e_weight, dtype=config.opt("dtype", "float64"), device_ordinal=config.opt("device", None))
     res = dalm_solve_batch(ext, Bmat, config)
+    lab = np.asarray(class_labels)
+    if res.x.shape[1] == 0:
+        return np.zeros(0, np.int32), np.zeros((0, int(lab.max()) + 1)), res
     D, s = ext.device_extension()
     view = D.view(ext=True, scale=s)
     lab = np.asarray(class_labels)
@@ -223,6 +267,10 @@ def dalm_solve_batch(A, Bmat, config, with_trace=False):
     """Dual ALM for every column of Bmat (d x B) against the shared A (or a
     robust.ExtendedDictionary for CAB batches).  Element j equals
     alm.dalm_solve on (A, b_j); option beta as in the reference."""
+    if config.opt("y_cg_step", False):
+        raise NotImplementedError("y_cg_step is single-instance only")
+    if _ncols(Bmat) == 0:
+        return _empty("dalm", A, Bmat, config)
     if (_ncols(Bmat) or SMALL_B) < SMALL_B:
         return _small_batch("dalm", A, Bmat, config, with_trace)
     t0 = time.perf_counter()
@@ -259,6 +307,8 @@ def dalm_solve_batch(A, Bmat, config, with_trace=False):
 def fista_solve_batch(A, Bmat, config, with_trace=False):
     """FISTA for every column of Bmat (d x B) against the shared A.
     Returns a BatchResult; ``.results()`` gives per-instance SolverResults."""
+    if _ncols(Bmat) == 0:
+        return _empty("fista", A, Bmat, config)
     if (_ncols(Bmat) or SMALL_B) < SMALL_B:
         return _small_batch("fista", A, Bmat, config, with_trace)
     torch = device._torch()
@@ -311,6 +361,8 @@ def homotopy_solve_batch(A, Bmat, target_lambda, config, with_trace=False):
         raise ValueError("target lambda must be nonnegative")
     if hasattr(A, "device_extension"):
         raise NotImplementedError("batched Homotopy runs on plain dictionaries")
+    if _ncols(Bmat) == 0:
+        return _empty("homotopy", A, Bmat, config)
     if (_ncols(Bmat) or SMALL_B) < SMALL_B:
         return _small_batch("homotopy", A, Bmat, config, with_trace, target=float(target_lambda))
     t0 = time.perf_counter()

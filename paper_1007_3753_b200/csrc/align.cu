@@ -90,6 +90,13 @@ __device__ __forceinline__ void gram_solve(AlignSh& S, int m) {
   __syncthreads();
 }
 
+// B's staging area of this CTA: shared memory, or (images whose (d+1) m
+// doubles exceed the SM's shared memory) this CTA's slice of a.Bstage —
+// the same column layout, read through L1/L2.
+__device__ __forceinline__ double* stage_ptr(const ell1_align_t& a, double* sm) {
+  return a.Bstage ? a.Bstage + (size_t)blockIdx.x * a.m * (a.d + 1) : sm;
+}
+
 __device__ __forceinline__ double soft(double x, double a) {
   return x > a ? x - a : (x < -a ? x + a : 0.0);          // _fastkernels.pyx:14-27
 }
@@ -165,7 +172,8 @@ __device__ __forceinline__ void store_out(const ell1_align_t& a, int j, const Al
 // robust.py:470-515: w = G^{-1} B^T (b - e + y/mu); e = soft(b - Bw + y/mu, 1/mu)
 // (inner sweeps to 1e-2/mu relative change, <= 100 per mu), y += mu r, mu *= rho
 __global__ void __launch_bounds__(AT) align_palm_kernel(const ell1_align_t a) {
-  extern __shared__ double Bs[];
+  extern __shared__ double Bsm[];
+  double* const Bs = stage_ptr(a, Bsm);
   __shared__ AlignSh S;
   const int d = a.d, m = a.m;
   for (int j = blockIdx.x; j < a.count; j += gridDim.x) {
@@ -231,7 +239,8 @@ __global__ void __launch_bounds__(AT) align_palm_kernel(const ell1_align_t a) {
 // with ||B||^2 from the reference's power iteration (numerics.py:224-261) run on
 // B^T (B v) from the host-drawn start vectors.
 __global__ void __launch_bounds__(AT) align_ist_kernel(const ell1_align_t a) {
-  extern __shared__ double Bs[];
+  extern __shared__ double Bsm[];
+  double* const Bs = stage_ptr(a, Bsm);
   __shared__ AlignSh S;
   __shared__ double v[MAXM];
   const int d = a.d, m = a.m;
@@ -371,7 +380,8 @@ __device__ __forceinline__ void block_min2(AlignSh& S, double v0, double v1) {
 }
 
 __global__ void __launch_bounds__(AT) align_homotopy_kernel(const ell1_align_t a) {
-  extern __shared__ double Bs[];
+  extern __shared__ double Bsm[];
+  double* const Bs = stage_ptr(a, Bsm);
   __shared__ AlignSh S;
   const int d = a.d, m = a.m;
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
@@ -513,7 +523,8 @@ __device__ bool weighted_gram_factor(AlignSh& S, const double* Bs, int d, int m,
 }
 
 __global__ void __launch_bounds__(AT) align_gp_kernel(const ell1_align_t a) {
-  extern __shared__ double Bs[];
+  extern __shared__ double Bsm[];
+  double* const Bs = stage_ptr(a, Bsm);
   __shared__ AlignSh S;
   __shared__ double R0[MAXM][MAXM];        // factor of B^T B (the step factor reuses S.R)
   __shared__ double wv[MAXM], dw[MAXM];
@@ -734,37 +745,69 @@ __global__ void __launch_bounds__(AT) align_gp_kernel(const ell1_align_t a) {
   }
 }
 
+const void* align_kernel(int kind) {
+  return kind == 0   ? (const void*)align_palm_kernel
+         : kind == 1 ? (const void*)align_ist_kernel
+         : kind == 2 ? (const void*)align_homotopy_kernel
+                     : (const void*)align_gp_kernel;
+}
+
+// launch geometry: shared-memory staging when it fits next to the kernel's
+// static shared memory, else global staging (grid CTAs x (d+1) m doubles)
+struct AlignPlan {
+  size_t smem;        // dynamic shared memory of the launch
+  int grid;
+  size_t stage;       // bytes of global staging (0: shared)
+};
+
+bool align_plan(int kind, int count, int d, int m, AlignPlan& P) {
+  const void* k = align_kernel(kind);
+  int dev = 0, sms = 148, optin = 0, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) return false;
+  const size_t need = (size_t)(d + 1) * m * 8;
+  const bool shared = need + fa.sharedSizeBytes <= (size_t)optin;
+  P.smem = shared ? need : 0;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem) != cudaSuccess)
+    return false;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, AT, P.smem);
+  P.grid = sms * (per > 0 ? per : 1);
+  if (P.grid > count) P.grid = count;
+  P.stage = shared ? 0 : need * (size_t)P.grid;
+  return true;
+}
+
 int launch_align(int kind, const ell1_align_t* A, void* stream) {
   if (!A || A->count < 0 || A->m < 1 || A->m > MAXM || A->d <= A->m || A->d > AT * RPT || !A->B || !A->rhs ||
       !A->w || !A->e || !A->status || A->ldb < A->m || A->ld_rhs < A->d || A->b_stride < A->ldb * A->d)
     return ELL1_ERR_ARG;
-  const bool palm = kind == 0;
   if (kind == 1 && !A->v0) return ELL1_ERR_ARG;
   if (A->count == 0) return ELL1_OK;
-  const size_t smem = (size_t)(A->d + 1) * A->m * 8;
-  const void* k = kind == 0   ? (const void*)align_palm_kernel
-                 : kind == 1 ? (const void*)align_ist_kernel
-                 : kind == 2 ? (const void*)align_homotopy_kernel
-                             : (const void*)align_gp_kernel;
-  // static + dynamic shared memory may pass 48 KB even when the dynamic part does not: always opt in
-  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return ELL1_ERR_ARG;
-  int dev = 0, sms = 148, per = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, AT, smem);
-  int grid = sms * (per > 0 ? per : 1);
-  if (grid > A->count) grid = A->count;
+  AlignPlan P;
+  if (!align_plan(kind, A->count, A->d, A->m, P)) return ELL1_ERR_CUDA;
+  ell1_align_t a = *A;
+  if (P.stage == 0) a.Bstage = nullptr;
+  else if (!A->Bstage) return ELL1_ERR_ARG;            // caller must provide ell1_align_stage_bytes()
   cudaStream_t s = (cudaStream_t)stream;
-  if (palm) align_palm_kernel<<<grid, AT, smem, s>>>(*A);
-  else if (kind == 1) align_ist_kernel<<<grid, AT, smem, s>>>(*A);
-  else if (kind == 2) align_homotopy_kernel<<<grid, AT, smem, s>>>(*A);
-  else align_gp_kernel<<<grid, AT, smem, s>>>(*A);
+  if (kind == 0) align_palm_kernel<<<P.grid, AT, P.smem, s>>>(a);
+  else if (kind == 1) align_ist_kernel<<<P.grid, AT, P.smem, s>>>(a);
+  else if (kind == 2) align_homotopy_kernel<<<P.grid, AT, P.smem, s>>>(a);
+  else align_gp_kernel<<<P.grid, AT, P.smem, s>>>(a);
   return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
 }
 
 }  // namespace
 }  // namespace ell1
+
+extern "C" size_t ell1_align_stage_bytes(int32_t kind, int32_t count, int32_t d, int32_t m) {
+  if (kind < 0 || kind > 3 || count <= 0 || m < 1 || m > ell1::MAXM || d <= m || d > ell1::AT * ell1::RPT) return 0;
+  ell1::AlignPlan P;
+  if (!ell1::align_plan(kind, count, d, m, P)) return 0;
+  return P.stage;
+}
 
 extern "C" int ell1_align_palm_batch(const ell1_align_t* A, void* stream) {
   return ell1::launch_align(0, A, stream);

@@ -51,6 +51,32 @@ def _gather_rows(arr, B, world, group, device):
     return full
 
 
+def _collective_call(fn, world, group, device):
+    """Run the rank-local ``fn()``; before any result collective, all ranks
+    agree (MAX all-reduce of a failure flag) on whether some rank failed, so a
+    failure on one rank raises on every rank instead of leaving the others
+    blocked in the gather."""
+    if world == 1:
+        return fn()
+    import torch
+    import torch.distributed as dist
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else "cpu"
+    out, err = None, None
+    try:
+        out = fn()
+    except Exception as exc:  # noqa: BLE001 - re-raised after the agreement below
+        err = exc
+    flag = torch.tensor([1 if err is not None else 0], dtype=torch.int32, device=device)
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+    if err is not None:
+        raise err
+    if int(flag.item()):
+        from paper_1007_3753_b200.exceptions import DeviceError
+        raise DeviceError("the batched solve failed on another rank")
+    return out
+
+
 def solve_batch_sharded(solve, A, Bmat, config, group=None, device=None, **kw):
     """Run ``solve(A, Bmat_share, config, **kw)`` (a batched entry point such as
     batched.fista_solve_batch / dalm_solve_batch / homotopy_solve_batch) on
@@ -63,7 +89,8 @@ def solve_batch_sharded(solve, A, Bmat, config, group=None, device=None, **kw):
     B = Bmat.shape[1]
     world, rank = _world(group)
     idx = shard_indices(B, rank, world)
-    res = solve(A, np.ascontiguousarray(Bmat[:, idx]), config, **kw)
+    res = _collective_call(lambda: solve(A, np.ascontiguousarray(Bmat[:, idx]), config, **kw),
+                           world, group, device)
     if world == 1:
         return res
     if device is None:
@@ -93,7 +120,8 @@ def src_classify_sharded(classify, A, class_labels, Bmat, config, group=None, de
     B = Bmat.shape[1]
     world, rank = _world(group)
     idx = shard_indices(B, rank, world)
-    labels, resid, _ = classify(A, class_labels, np.ascontiguousarray(Bmat[:, idx]), config)
+    labels, resid, _ = _collective_call(
+        lambda: classify(A, class_labels, np.ascontiguousarray(Bmat[:, idx]), config), world, group, device)
     if world == 1:
         return np.asarray(labels), np.asarray(resid)
     if device is None:
@@ -113,7 +141,8 @@ def align_batch_sharded(solve, Bs, bs, config, group=None, device=None, **kw):
     count = Bs.shape[0]
     world, rank = _world(group)
     idx = shard_indices(count, rank, world)
-    W, E = solve(np.ascontiguousarray(Bs[idx]), np.ascontiguousarray(bs[idx]), config, **kw)
+    W, E = _collective_call(lambda: solve(np.ascontiguousarray(Bs[idx]), np.ascontiguousarray(bs[idx]),
+                                          config, **kw), world, group, device)
     if world == 1:
         return W, E
     if device is None:

@@ -305,10 +305,16 @@ def align_batch_device(kind, Bd, bd, config, lam=None, v0=None):
             v0 = torch.from_numpy(np.concatenate(draws)).to(dev)
         a.v0 = v0.data_ptr()
     a.w, a.e, a.status, a.iterations = W.data_ptr(), E.data_ptr(), st.data_ptr(), its.data_ptr()
+    kid = {"palm": 0, "ist": 1, "homotopy": 2, "gp": 3}[kind]
+    stage = None
+    sb = int(L.ell1_align_stage_bytes(kid, count, d, m)) if count else 0
+    if sb:                          # B does not fit in shared memory: stage it in global memory
+        stage = torch.empty(sb // 8, dtype=torch.float64, device=dev)
+        a.Bstage = stage.data_ptr()
     fn = {"palm": L.ell1_align_palm_batch, "ist": L.ell1_align_ist_batch,
           "homotopy": L.ell1_align_homotopy_batch, "gp": L.ell1_align_gp_batch}[kind]
     _lib.check(fn(ctypes.byref(a), device.stream_ptr(dev)), "ell1_align_%s_batch" % kind)
-    W._ell1_keep = (Bd, bd, v0, st)                       # operands live until the caller syncs
+    W._ell1_keep = (Bd, bd, v0, st, stage)                       # operands live until the caller syncs
     W._ell1_status = st
     return W, E, its
 

@@ -13,7 +13,20 @@ import torch  # noqa: E402
 
 from paper_1007_3753_b200.sharded import make_cfg4_shard  # noqa: E402
 
-shard, b, x0, ops = make_cfg4_shard(rank=0, world=int(os.environ.get("SHARDS", "8")))
+class _Solo:
+    """rank 0 of an S-way split, no peers (the collective is not profiled)."""
+    world = int(os.environ.get("SHARDS", "8"))
+    rank = 0
+    group = None
+
+    def allreduce_(self, t):
+        pass
+
+    def all_gather(self, t):
+        return t.repeat(self.world)
+
+
+shard, b, x0, ops = make_cfg4_shard(rank=0, world=_Solo.world, coll=_Solo())
 x = ops.zeros_n()
 x.normal_()
 r = ops.from_host_d(b)
