@@ -477,11 +477,6 @@ def gemm_peaks(torch, dev):
     return _PEAKS
 
 
-def _lib_mode():
-    from paper_1007_3753_b200 import _lib
-    return int(_lib.lib().ell1_blas_fp32_mode())
-
-
 def leg_cfg3(torch, dev, queries=1024):
     """BASELINE config 3: CAB [A I] (d=1024, 38 classes x 32 columns), 1024
     corrupted queries, batched dual ALM in fp32 storage + SRC labels."""
@@ -506,7 +501,6 @@ def leg_cfg3(torch, dev, queries=1024):
     tfl = float(its.sum()) * 5 * 2.0 * 1024 * 1216 / t / 1e12
     peaks = gemm_peaks(torch, dev)
     pk = peaks["sgemm_tflops"]
-    mode = _lib_mode()
     return {"workload": "cfg3: CAB [A I] 1024 x 2240, %d queries, batched DALM fp32 storage, "
                         "tol 1e-4, min-class-residual labels" % queries,
             "roofline": {"bound": "fp32 GEMMs", "achieved": tfl, "peak": pk, "unit": "TFLOP/s",
@@ -515,14 +509,13 @@ def leg_cfg3(torch, dev, queries=1024):
             "queries_per_sec": queries / t, "ms_per_batch": 1e3 * t,
             "mean_iterations": float(its.mean()), "max_iterations": int(its.max()),
             "accuracy_vs_truth": float(np.mean(labels == truth)),
-            "fp32_gemm": {3: "3xTF32 tcgen05 kernel (tc_gemm.cu)", 2: "3xTF32 split cuBLAS GEMMs",
-                          0: "cuBLAS SIMT SGEMM"}.get(mode, "unknown"),
+            "fp32_gemm": "3xTF32 tcgen05 kernel (tc_gemm.cu)",
             "tensor_pipe": ({"mma_tflops": 3 * tfl, "peak": peaks["tf32_tflops"], "unit": "TFLOP/s",
                              "frac": 3 * tfl / peaks["tf32_tflops"],
                              "peak_source": "cuBLAS TF32 8192^3 measured in this run",
                              "note": "3 TF32 MMAs per fp32-accurate product; algorithmic flops only "
                                      "(the y-step's identity block and certificate products not counted)"}
-                            if mode in (2, 3) else None),
+                            ),
             "note": "timed through the public call (host queries in, labels out)"}
 
 

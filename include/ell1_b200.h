@@ -427,6 +427,15 @@ int ell1_sfista_pre(const ell1_dict_t* D, ell1_shard_ctl_t* ctl, const ell1_sfis
 int ell1_sfista_post(const ell1_dict_t* D, ell1_shard_ctl_t* ctl, const ell1_sfista_bufs_t* V, void* ws,
                      size_t ws_bytes, void* stream);
 
+/* Dense Cholesky of PDIPA's weighted normal matrix (pdipa.py:43-52
+ * _factor_with_jitter -> numerics.chol_factor; chol.cu): L (lower, ldl) of
+ * M + jitter I (M column-major, ldm); *status (device int) = 0, or k + 1 when
+ * the k-th pivot is not positive (LAPACK's potrf convention). */
+int ell1_chol_factor_dense(int64_t d, const double* M, int64_t ldm, double jitter, double* L, int64_t ldl,
+                           int* status, void* stream);
+/* x = (L L^T)^-1 rhs (factor.solve, numerics.py:62-72); d <= 25600 */
+int ell1_chol_solve_dense(int64_t d, const double* L, int64_t ldl, const double* rhs, double* x, void* stream);
+
 /* ---------------------------------------------- PDIPA vector kernels (pdipa.cu)
  * Primal-dual interior point on the split LP min 1'v, [A, -A] v = b, v >= 0
  * (pdipa.py:97-185; split = 1: vectors of length 2n against n columns; split = 0:
@@ -481,6 +490,10 @@ typedef struct {
 } ell1_align_t;
 /* bytes of global B staging a launch of this shape needs (0: B fits in shared memory) */
 size_t ell1_align_stage_bytes(int32_t kind, int32_t count, int32_t d, int32_t m);
+/* robust.ist_block_step (robust.py:433-445): one block soft-threshold sweep on one
+ * image, B row-major d x m (ldb), m <= 32; w_next (m), e_next (d) device outputs */
+int ell1_align_ist_step(int32_t d, int32_t m, const double* B, int64_t ldb, const double* b, const double* w,
+                        const double* e, double lam, double alpha, double* w_next, double* e_next, void* stream);
 /* align_palm_solve per image (robust.py:470-515) */
 int ell1_align_palm_batch(const ell1_align_t* A, void* stream);
 /* align_ist_solve per image (robust.py:427-467) */
@@ -490,11 +503,6 @@ int ell1_align_homotopy_batch(const ell1_align_t* A, void* stream);
 /* align_gp_solve per image (robust.py:276-371); status ELL1_ILL_CONDITIONED (reduced system not PD),
  * ELL1_BREAKDOWN (line search exhausted), ELL1_LAMBDA_NONPOS */
 int ell1_align_gp_batch(const ell1_align_t* A, void* stream);
-
-/* fp32 GEMM path of the batched solvers (3: 3xTF32 tcgen05 kernel, the default;
- * 2: 3xTF32 split over cuBLAS TF32 GEMMs, ELL1_FP32_GEMM=tf32x3; 0: SIMT SGEMM,
- * ELL1_FP32_GEMM=simt; -1: not used yet). */
-int ell1_blas_fp32_mode(void);
 
 /* The batched solvers' fp32 dictionary product on its own (new; the
  * reference's equivalent is the numpy `A @ X` / `A.T @ R` of its solvers,
@@ -513,8 +521,9 @@ int ell1_gemm_f32(int32_t trans, int64_t M, int64_t N, int64_t K, const float* A
  * 239-249, and pdipa.py:150-153's weighted Gram) all go through it. */
 int ell1_gemm_f64(int32_t transA, int32_t transB, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                   const double* B, int64_t ldb, double* C, int64_t ldc, void* stream);
-/* the same with a fixed tile variant (0: 64x64x4 stages, 1: 64x64x3, 2: 128x64,
- * 3: 64x128, 4: 128x128) and K split (1/2/4/8 CTAs of a cluster, -1 auto); tuning */
+/* the same with a fixed tile variant (0: 64x64, 4 stages of k16; 1: 64x64, 3 x k16
+ * (default); 2: 128x64, 3 x k16; 3: 64x64, 3 x k32; 4: 128x64, 2 x k32) and K split
+ * (1/2/4/8 CTAs of a cluster, -1 auto); tuning */
 int ell1_gemm_f64_variant(int32_t variant, int32_t split, int32_t transA, int32_t transB, int64_t M, int64_t N,
                           int64_t K, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                           int64_t ldc, void* stream);

@@ -215,6 +215,10 @@ _SIGS = {
                                       ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "ell1_shard_resid": (ctypes.c_int, [ctypes.c_int64] + [ctypes.c_void_p] * 3 + [ctypes.c_double] +
                          [ctypes.c_void_p] * 4),
+    "ell1_chol_factor_dense": (ctypes.c_int, [ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_double,
+                                              ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_chol_solve_dense": (ctypes.c_int, [ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                             ctypes.c_void_p, ctypes.c_void_p]),
     "ell1_pd_workspace": (ctypes.c_size_t, []),
     "ell1_pd_split": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32] + [ctypes.c_void_p] * 5),
     "ell1_pd_resid": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32] + [ctypes.c_void_p] * 12),
@@ -244,7 +248,8 @@ _SIGS = {
                                         ctypes.c_void_p]),
     "ell1_homotopy_group": (ctypes.c_int, [P(Group), ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
                                            ctypes.c_void_p]),
-    "ell1_blas_fp32_mode": (ctypes.c_int, []),
+    "ell1_align_ist_step": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64] +
+                            [ctypes.c_void_p] * 3 + [ctypes.c_double] * 2 + [ctypes.c_void_p] * 3),
     "ell1_align_stage_bytes": (ctypes.c_size_t, [ctypes.c_int32] * 4),
     "ell1_align_palm_batch": (ctypes.c_int, [P(Align), ctypes.c_void_p]),
     "ell1_align_ist_batch": (ctypes.c_int, [P(Align), ctypes.c_void_p]),

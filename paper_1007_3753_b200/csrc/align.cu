@@ -745,6 +745,30 @@ __global__ void __launch_bounds__(AT) align_gp_kernel(const ell1_align_t a) {
   }
 }
 
+// robust.ist_block_step (robust.py:433-445): one block soft-threshold sweep,
+// r = b - B w - e, w' = w + B^T r / alpha, e' = soft(e + r / alpha, lam / alpha);
+// one CTA, any d (rows strided over the threads), fixed-order reductions.
+__global__ void __launch_bounds__(AT) align_ist_step_kernel(int d, int m, const double* __restrict__ B, int64_t ldb,
+                                                            const double* __restrict__ b, const double* __restrict__ w,
+                                                            const double* __restrict__ e, double lam, double alpha,
+                                                            double* __restrict__ w_next, double* __restrict__ e_next) {
+  __shared__ AlignSh S;
+  if (threadIdx.x < MAXM) S.w[threadIdx.x] = threadIdx.x < (unsigned)m ? w[threadIdx.x] : 0.0;
+  __syncthreads();
+  double p[MAXM];
+  for (int c = 0; c < MAXM; ++c) p[c] = 0.0;
+  for (int i = threadIdx.x; i < d; i += AT) {
+    const double* Bi = B + (int64_t)i * ldb;
+    double bw = 0.0;
+    for (int c = 0; c < m; ++c) bw = fma(Bi[c], S.w[c], bw);
+    const double r = b[i] - bw - e[i];
+    e_next[i] = soft(e[i] + r / alpha, lam / alpha);
+    for (int c = 0; c < m; ++c) p[c] = fma(Bi[c], r, p[c]);
+  }
+  block_sum(S, p, m);
+  if ((int)threadIdx.x < m) w_next[threadIdx.x] = S.w[threadIdx.x] + S.out[threadIdx.x] / alpha;
+}
+
 const void* align_kernel(int kind) {
   return kind == 0   ? (const void*)align_palm_kernel
          : kind == 1 ? (const void*)align_ist_kernel
@@ -807,6 +831,16 @@ extern "C" size_t ell1_align_stage_bytes(int32_t kind, int32_t count, int32_t d,
   ell1::AlignPlan P;
   if (!ell1::align_plan(kind, count, d, m, P)) return 0;
   return P.stage;
+}
+
+extern "C" int ell1_align_ist_step(int32_t d, int32_t m, const double* B, int64_t ldb, const double* b,
+                                   const double* w, const double* e, double lam, double alpha, double* w_next,
+                                   double* e_next, void* stream) {
+  if (d < 1 || m < 1 || m > ell1::MAXM || ldb < m || !B || !b || !w || !e || !w_next || !e_next || !(alpha > 0))
+    return ELL1_ERR_ARG;
+  ell1::align_ist_step_kernel<<<1, ell1::AT, 0, (cudaStream_t)stream>>>(d, m, B, ldb, b, w, e, lam, alpha, w_next,
+                                                                        e_next);
+  return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
 }
 
 extern "C" int ell1_align_palm_batch(const ell1_align_t* A, void* stream) {

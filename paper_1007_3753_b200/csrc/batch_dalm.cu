@@ -457,8 +457,6 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
       !out->x || !out->iterations || !out->converged || !out->status)
     return ELL1_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  cublasHandle_t h = blas_handle(s);
-  if (!h) return ELL1_ERR_CUDA;
   const int64_t N = ncols_of(D), ldx = r4(N), ld = D->ld, d = D->d;
   BDArgs a;
   a.d = d; a.n = D->n; a.N = N; a.ld = ld; a.ldx = ldx;
@@ -497,7 +495,7 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
     if (!f32split_setup(spA, cv, D, (ldx > ld ? ldx : ld) * 2 * B, s)) return ELL1_ERR_ARG;
     spM = spA;                                               // shares the operand scratch
     if (!f32split_dict(spM, cv, D, (const float*)O->M, s)) return ELL1_ERR_ARG;
-    if (a.ext && fp32_mode_select() == 3) {
+    if (a.ext) {
       float* xh = cv.take<float>(ld * ldx);
       float* xl = cv.take<float>(ld * ldx);
       if (!cv.ok) return ELL1_ERR_ARG;
@@ -517,11 +515,8 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   if (cudaMemcpyAsync(Bm, Bmat, ld * B * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return ELL1_ERR_CUDA;
   if (cudaMemsetAsync(ctr, 0, 32, s) != cudaSuccess) return ELL1_ERR_CUDA;
   if (cudaMemsetAsync(a.UX32, 0, ldx * 2 * B * 4, s) != cudaSuccess) return ELL1_ERR_CUDA;
-  const double one = 1.0, zero = 0.0;
   // C0 = Ginv B (Ginv column-major ld x d, float64)
-  if (cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)ld, B, (int)d, &one, O->Ginv, (int)ld, Bm, (int)ld,
-                  &zero, C0, (int)ld) != CUBLAS_STATUS_SUCCESS)
-    return ELL1_ERR_CUDA;
+  if (!dgemm(0, 0, ld, B, d, O->Ginv, ld, Bm, ld, C0, ld, s)) return ELL1_ERR_CUDA;
   bd_init<<<B, BT, 0, s>>>(a);
   ell1_dict_t MD = *D;
   MD.A = O->M;                                              // M has A's layout / dtype
@@ -537,14 +532,14 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   // U = A^T y_new (n x B), x_new, A [U | x_new], certificate (refine_only: flagged instances)
   auto tail_part = [&](const BDArgs& aa, int Bc, int refine_only) -> bool {
     void* Ut = aa.f32 ? (void*)T32 : (void*)scratch;
-    if (!gemm_AtR(h, D, aa.f32 ? (const void*)aa.Y32 : (const void*)aa.Y[aa.iy ^ 1], ld, Ut, D->n, Bc, pA))
+    if (!gemm_AtR(ks, D, aa.f32 ? (const void*)aa.Y32 : (const void*)aa.Y[aa.iy ^ 1], ld, Ut, D->n, Bc, pA))
       return false;
     // [U | x_new] for the Bc instances: the x_new block starts at column Bc
     bd_x<<<Bc, BT, 0, ks>>>(aa, (const double*)Ut, (const float*)Ut, refine_only);
     if (aa.f32) {
-      if (!gemm_AX(h, D, aa.UX32, ldx, aa.P2f, ld, 2 * Bc, pA)) return false;
+      if (!gemm_AX(ks, D, aa.UX32, ldx, aa.P2f, ld, 2 * Bc, pA)) return false;
     } else {
-      if (!gemm_AX(h, D, aa.UX, ldx, aa.P2, ld, 2 * Bc)) return false;
+      if (!gemm_AX(ks, D, aa.UX, ldx, aa.P2, ld, 2 * Bc)) return false;
     }
     if (cudaMemsetAsync(ctr, 0, 4, ks) != cudaSuccess) return false;
     bd_c<<<Bc, BT, 0, ks>>>(aa, refine_only);
@@ -557,17 +552,15 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
     const void* Zop = aa.f32 ? (const void*)aa.Z32 : (const void*)aa.Z;
     if (aa.fuse_ext) {
       // P1 = [M | Ginv] V over K = n + d (V's identity block already carries s)
-      if (!sgemm_split(h, CUBLAS_OP_N, (int)ld, Bc, (int)N, nullptr, 0, &spX, aa.V32, ldx, aa.P1f, ld, N))
+      if (!sgemm_split(ks, 0, (int)ld, Bc, (int)N, &spX, aa.V32, ldx, aa.P1f, ld))
         return false;
-    } else if (!gemm_AX(h, &MD, Vop, ldx, aa.f32 ? (void*)aa.P1f : (void*)aa.P1, ld, Bc, pM)) {
+    } else if (!gemm_AX(ks, &MD, Vop, ldx, aa.f32 ? (void*)aa.P1f : (void*)aa.P1, ld, Bc, pM)) {
       return false;
     }
-    if (!gemm_AX(h, D, Zop, ldx, aa.f32 ? (void*)aa.P2f : (void*)aa.P2, ld, Bc, pA)) return false;
+    if (!gemm_AX(ks, D, Zop, ldx, aa.f32 ? (void*)aa.P2f : (void*)aa.P2, ld, Bc, pA)) return false;
     if (aa.ext && !aa.fuse_ext) {
       // identity block of M: s Ginv v_ext (s folded into v_ext by bd_z)
-      if (cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)ld, Bc, (int)d, &one, O->Ginv, (int)ld,
-                      aa.V + D->n, (int)ldx, &zero, aa.GEXT, (int)ld) != CUBLAS_STATUS_SUCCESS)
-        return false;
+      if (!dgemm(0, 0, ld, Bc, d, O->Ginv, ld, aa.V + D->n, ldx, aa.GEXT, ld, ks)) return false;
     }
     bd_y<<<Bc, BT, 0, ks>>>(aa);
     return tail_part(aa, Bc, 0);
@@ -576,8 +569,7 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   auto refine_part = [&](const BDArgs& aa, int Bc, bool own_gemv) -> bool {
     if (own_gemv) {
       bd_refine_gemv<<<dim3((unsigned)((ld + 255) / 256), (unsigned)Bc), 256, 0, ks>>>(aa, O->Ginv, aa.GEXT);
-    } else if (cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)ld, Bc, (int)d, &one, O->Ginv, (int)ld, aa.RES,
-                           (int)ld, &zero, aa.GEXT, (int)ld) != CUBLAS_STATUS_SUCCESS) {
+    } else if (!dgemm(0, 0, ld, Bc, d, O->Ginv, ld, aa.RES, ld, aa.GEXT, ld, ks)) {
       return false;
     }
     bd_refine<<<Bc, BT, 0, ks>>>(aa, aa.GEXT);
@@ -589,7 +581,7 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   // iterations (both buffer parities) per WHILE-body pass, each followed by
   // an IF node running the refinement when bd_c raised a flag; the WHILE
   // condition (bd_loop) drops when compaction is due or everything finished.
-  bool use_graph = a.f32 && fp32_mode_select() == 3;
+  bool use_graph = true;
   if (const char* e = getenv("ELL1_BATCH_GRAPH")) use_graph = use_graph && e[0] != '0';
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
@@ -627,11 +619,10 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
     cudaStream_t cs = nullptr;
     GSTEP(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess);
     struct Restore {
-      cudaStream_t& ks; cudaStream_t s; cublasHandle_t h; cudaStream_t cs;
-      ~Restore() { ks = s; cublasSetStream(h, s); cudaStreamDestroy(cs); }
-    } restore{ks, s, h, cs};
+      cudaStream_t& ks; cudaStream_t s; cudaStream_t cs;
+      ~Restore() { ks = s; cudaStreamDestroy(cs); }
+    } restore{ks, s, cs};
     ks = cs;
-    cublasSetStream(h, cs);
     for (int q = 0; q < 2; ++q) {
       aa.ix = aa.iy = a.ix ^ q;
       GSTEP(cudaStreamBeginCaptureToGraph(cs, body, last ? &last : nullptr, nullptr, last ? 1 : 0,
@@ -735,14 +726,12 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
       bool ok = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess;
       if (ok) {
         ks = cs;
-        cublasSetStream(h, cs);
         ok = cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed) == cudaSuccess;
         if (ok) {
           ok = main_part(a, Bcur);
           ok = cudaStreamEndCapture(cs, &pg) == cudaSuccess && ok;
         }
         ks = s;
-        cublasSetStream(h, s);
         cudaStreamDestroy(cs);
       }
       ok = ok && cudaGraphInstantiate(&pexec[a.ix], pg, 0) == cudaSuccess;

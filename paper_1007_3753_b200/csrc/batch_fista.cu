@@ -350,8 +350,6 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
       !out->converged || !out->status)
     return ELL1_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  cublasHandle_t h = blas_handle(s);
-  if (!h) return ELL1_ERR_CUDA;
   const int64_t N = ncols_of(D), ldx = round4(N), ld = D->ld;
   BFArgs a;
   a.d = D->d; a.n = D->n; a.N = N; a.ld = ld; a.ldx = ldx;
@@ -398,7 +396,7 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
       Bop = B32;
     }
     void* CT = a.f32 ? (void*)a.G32 : (void*)scratch;      // n x B
-    if (!gemm_AtR(h, D, Bop, ld, CT, D->n, B, spp)) return ELL1_ERR_CUDA;
+    if (!gemm_AtR(s, D, Bop, ld, CT, D->n, B, spp)) return ELL1_ERR_CUDA;
     bf_init<<<B, BT, 0, s>>>(a, (const double*)CT, (const float*)CT, B);
   }
   int Bcur = B;
@@ -412,12 +410,12 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
   auto one_round = [&](BFArgs& aa) -> bool {
     // ---- finish last round's accepted iterations, then one backtracking trial each
     bf_step<<<Bcur, BT, 0, ks>>>(aa);
-    if (!gemm_AX(h, D, aa.f32 ? (const void*)aa.X32 : (const void*)aa.X[aa.ixn], ldx,
+    if (!gemm_AX(ks, D, aa.f32 ? (const void*)aa.X32 : (const void*)aa.X[aa.ixn], ldx,
                  aa.f32 ? (void*)aa.AX32 : (void*)aa.AX, ld, Bcur, spp))
       return false;
     bf_resid<<<Bcur, BT, 0, ks>>>(aa);
     // g_next = A^T r_next into the g ring's free slot (speculative for retries)
-    if (!gemm_AtR(h, D, aa.f32 ? (const void*)aa.R32 : (const void*)aa.R[aa.irn], ld,
+    if (!gemm_AtR(ks, D, aa.f32 ? (const void*)aa.R32 : (const void*)aa.R[aa.irn], ld,
                   aa.f32 ? (void*)aa.G32 : (void*)aa.G[aa.igxp], aa.f32 ? D->n : ldx, Bcur, spp))
       return false;
     // rotate the rings (shrinkage.py:283-284); bf_step undoes it for retrying instances
@@ -470,7 +468,6 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
       bool ok = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess;
       if (ok) {
         ks = cs;
-        cublasSetStream(h, cs);
         ok = cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed) == cudaSuccess;
         if (ok) {
           BFArgs aa = a;
@@ -478,7 +475,6 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
           ok = cudaStreamEndCapture(cs, &g) == cudaSuccess && ok;
         }
         ks = s;
-        cublasSetStream(h, s);
         cudaStreamDestroy(cs);
       }
       ok = ok && cudaGraphInstantiate(&gexec, g, 0) == cudaSuccess;

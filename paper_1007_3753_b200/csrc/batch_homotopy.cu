@@ -558,12 +558,10 @@ __global__ void widen_kernel(const float* src, double* dst, int64_t n) {
     dst[i] = (double)src[i];
 }
 
-inline bool dgemm_AtX(cublasHandle_t h, const HB& a, const double* X, double* Y, int B) {
+inline bool dgemm_AtX(cudaStream_t st, const HB& a, const double* X, double* Y, int B) {
   if (B <= 0) return true;
-  const double one = 1.0, zero = 0.0;
-  // Y (n x B) = A^T (n x d) X (d x B)
-  return cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)a.n, B, (int)a.d, &one, a.A, (int)a.ld, X, (int)a.ld,
-                     &zero, Y, (int)a.n) == CUBLAS_STATUS_SUCCESS;
+  // Y (n x B) = A^T (n x d) X (d x B) on the DMMA path (dmma_gemm.cu)
+  return dgemm(1, 0, a.n, B, a.d, a.A, a.ld, X, a.ld, Y, a.n, st);
 }
 
 }  // namespace ell1
@@ -601,8 +599,6 @@ extern "C" int ell1_batch_homotopy(const ell1_dict_t* D, const double* Bmat, int
       !out->status || max_iter < 0 || !(target >= 0.0))
     return ELL1_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  cublasHandle_t h = blas_handle(s);
-  if (!h) return ELL1_ERR_CUDA;
   const int64_t n = D->n, ld = D->ld;
   HB a;
   a.d = D->d; a.n = n; a.ld = ld; a.mmax = hb_mmax(D); a.target = target; a.max_iter = max_iter;
@@ -640,7 +636,7 @@ extern "C" int ell1_batch_homotopy(const ell1_dict_t* D, const double* Bmat, int
   a.V = V1;
   if (cudaMemcpyAsync(Bm, Bmat, ld * B * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return ELL1_ERR_CUDA;
   // c = A^T b for every instance, then lambda0 / first atom
-  if (!dgemm_AtX(h, a, Bm, a.C, B)) return ELL1_ERR_CUDA;
+  if (!dgemm_AtX(s, a, Bm, a.C, B)) return ELL1_ERR_CUDA;
   hb_init<<<B, HBT, 0, s>>>(a, B);
   // identity active list
   {
@@ -679,9 +675,9 @@ extern "C" int ell1_batch_homotopy(const ell1_dict_t* D, const double* Bmat, int
       a.act = act;
       a.V = Vcur;
     }
-    if (!dgemm_AtX(h, a, a.V, a.W, nact)) return ELL1_ERR_CUDA;
+    if (!dgemm_AtX(s, a, a.V, a.W, nact)) return ELL1_ERR_CUDA;
     hb_step<<<nact, HBT, smem, s>>>(a, nact);
-    if (!dgemm_AtX(h, a, a.Rr, a.C, nact)) return ELL1_ERR_CUDA;
+    if (!dgemm_AtX(s, a, a.Rr, a.C, nact)) return ELL1_ERR_CUDA;
   }
   hb_out<<<B, 256, 0, s>>>(a, B, out->x, out->iterations, out->converged, out->status, notes);
   return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;

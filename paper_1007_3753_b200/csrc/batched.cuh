@@ -3,7 +3,8 @@
 // B instances share one dictionary D (d x N, N = n or n + d for [A, sI]).  The
 // instance vectors are stored column-major as matrices (N x B for x-like,
 // ld x B for r-like), so every dictionary product of an iteration is one
-// GEMM over all active instances (cuBLAS D/SGEMM on the B200), and the solver
+// GEMM over all active instances (the library's own tensor-core GEMMs: DMMA
+// for float64 storage, dmma_gemm.cu; tcgen05 3xTF32 for float32, tc_gemm.cu), and the solver
 // arithmetic in between runs in per-instance epilogue kernels (one CTA per
 // instance, fixed-order block reductions) that reproduce the single-instance
 // control flow of the reference (backtracking, continuation, stopping rules)
@@ -11,8 +12,8 @@
 // launches, reads one device counter per backtracking round, and compacts the
 // active instances to the front of every matrix as they converge.
 #pragma once
-#include <cublas_v2.h>
 #include <cstdlib>
+#include "dmma_gemm.cuh"
 #include "solvers_common.cuh"
 #include "tc_gemm.cuh"
 
@@ -46,19 +47,6 @@ __device__ __forceinline__ void cta_reduce(double (&v)[K], unsigned maxmask, dou
 }
 
 // --------------------------------------------------------------- host helpers
-struct Blas {
-  cublasHandle_t h = nullptr;
-  int dev = -1;
-};
-
-// fp32 GEMM path of the batched solvers: 3 = 3xTF32 tcgen05 kernel (tc_gemm.cu,
-// default), 2 = 3xTF32 split over three cuBLAS TF32 GEMMs (ELL1_FP32_GEMM=tf32x3),
-// 0 = SIMT SGEMM (ELL1_FP32_GEMM=simt), -1 = not used yet.
-inline int& fp32_gemm_mode() {
-  static int mode = -1;
-  return mode;
-}
-
 // Pinned host mailbox (per thread, 16 ints) for the per-round device counter
 // read-backs of the batched host loops: a pageable 8-byte D2H is a staged
 // copy (~7 us on the B200 box), a pinned one is a direct DMA.
@@ -73,39 +61,23 @@ inline int* host_mailbox() {
   return box;
 }
 
-inline cublasHandle_t blas_handle(cudaStream_t s) {
-  static thread_local Blas B[16];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  Blas& b = B[dev & 15];
-  if (!b.h) {
-    if (cublasCreate(&b.h) != CUBLAS_STATUS_SUCCESS) return nullptr;
-    b.dev = dev;
-  }
-  cublasSetStream(b.h, s);
-  return b.h;
-}
-
 // ---------------------------------------------------------------- 3xTF32 fp32 GEMMs
 // fp32 products of the batched solvers run on the tensor pipe as 3xTF32: both
 // operands are split a = a_hi + a_lo (both TF32-representable) and
 //   A X ~= A_lo X_hi + A_hi X_lo + A_hi X_hi     (fp32 accumulation)
 // keeps fp32-level accuracy (the dropped A_lo X_lo term is ~2^-22 relative).
-// Default: one tcgen05 kernel accumulates the three products in TMEM
-// (tc_gemm.cu).  The dictionary split is made once per solve, in both
-// orientations (column-major for A^T R, row-major for A X: the kernel reads
-// K-major operands); the right operand is split per product into caller
-// workspace.  ELL1_FP32_GEMM=tf32x3 runs the split as three cuBLAS TF32 GEMMs,
-// ELL1_FP32_GEMM=simt uses cuBLAS SIMT SGEMM.
+// One tcgen05 kernel accumulates the three products in TMEM (tc_gemm.cu).
+// The dictionary split is made once per solve, in both orientations
+// (column-major for A^T R, row-major for A X: the kernel reads K-major
+// operands); the right operand is split tile by tile inside the kernel.
+// There is no other fp32 path: a call the kernel cannot take is an error.
 struct F32Split {
   const float* Ahi;         // split dictionary, same layout as D->A (column-major, ld)
   const float* Alo;
   const float* Arhi;        // split dictionary, row-major (ld rows of pr floats)
   const float* Arlo;
   int64_t pr;
-  float* Xhi;               // right-operand scratch (xcap floats each)
-  float* Xlo;
-  int64_t xcap;
+  int64_t pc;               // column stride of Ahi / Alo (the dictionary's ld)
 };
 
 __device__ __forceinline__ float tf32_rna(float x) {
@@ -154,79 +126,30 @@ inline bool split_tf32(const float* src, float* hi, float* lo, int64_t n, cudaSt
   return cudaGetLastError() == cudaSuccess;
 }
 
-inline int fp32_mode_select() {
-  static int v = -1;
-  if (v < 0) {
-    const char* env = getenv("ELL1_FP32_GEMM");
-    if (env && (env[0] == 's' || env[0] == 'S')) v = 0;
-    else if (env && (env[0] == 't' || env[0] == 'T')) v = 2;
-    else v = tc3_available() == 1 ? 3 : 0;
-    fp32_gemm_mode() = v;
-  }
-  return v;
-}
-
-// Y (m x B) = op(A) X with fp32 operands through the 3xTF32 split (sp) or SIMT SGEMM
-inline bool sgemm_split(cublasHandle_t h, cublasOperation_t opA, int m, int B, int k, const float* A,
-                        int lda, const F32Split* sp, const float* X, int64_t ldx, float* Y, int64_t ldy,
-                        int64_t xrows) {
-  const float one = 1.0f, zero = 0.0f;
-  const int mode = fp32_mode_select();
-  if (!sp || mode == 0) {
-    return cublasSgemm(h, opA, CUBLAS_OP_N, m, B, k, &one, A, lda, X, (int)ldx, &zero, Y, (int)ldy) ==
-           CUBLAS_STATUS_SUCCESS;
-  }
-  cudaStream_t s;
-  cublasGetStream(h, &s);
-  if (mode == 3) {
-    // the kernel splits the right operand tile by tile in shared memory
-    const bool ok = opA == CUBLAS_OP_N ? tc3_gemm(m, B, k, sp->Arhi, sp->Arlo, sp->pr, X, ldx, Y, ldy, s)
-                                       : tc3_gemm(m, B, k, sp->Ahi, sp->Alo, lda, X, ldx, Y, ldy, s);
-    if (ok) return true;
-    if (!A) return false;
-    return cublasSgemm(h, opA, CUBLAS_OP_N, m, B, k, &one, A, lda, X, (int)ldx, &zero, Y, (int)ldy) ==
-           CUBLAS_STATUS_SUCCESS;
-  }
-  const int64_t xn = ldx * (int64_t)(B - 1) + xrows;
-  if (xn > sp->xcap) return false;
-  if (!split_tf32(X, sp->Xhi, sp->Xlo, xn, s)) return false;
-  const cublasComputeType_t ct = CUBLAS_COMPUTE_32F_FAST_TF32;
-  const void* terms[3][2] = {{sp->Alo, sp->Xhi}, {sp->Ahi, sp->Xlo}, {sp->Ahi, sp->Xhi}};
-  for (int t = 0; t < 3; ++t) {
-    const float* beta = t == 0 ? &zero : &one;
-    if (cublasGemmEx(h, opA, CUBLAS_OP_N, m, B, k, &one, terms[t][0], CUDA_R_32F, lda, terms[t][1], CUDA_R_32F,
-                     (int)ldx, beta, Y, CUDA_R_32F, (int)ldy, ct, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
-      return false;
-  }
-  return true;
+// Y (m x B) = op(A) X with fp32 operands through the 3xTF32 split of A (sp)
+inline bool sgemm_split(cudaStream_t st, int transA, int m, int B, int k, const F32Split* sp, const float* X,
+                        int64_t ldx, float* Y, int64_t ldy) {
+  if (!sp) return false;
+  return transA ? tc3_gemm(m, B, k, sp->Ahi, sp->Alo, sp->pc, X, ldx, Y, ldy, st)
+                : tc3_gemm(m, B, k, sp->Arhi, sp->Arlo, sp->pr, X, ldx, Y, ldy, st);
 }
 
 // Y(ld x B) = A(ld x n, column-major) X(n x B, ldx)      (A columns only)
-inline bool gemm_AX(cublasHandle_t h, const ell1_dict_t* D, const void* X, int64_t ldx, void* Y,
-                    int64_t ldy, int B, const F32Split* sp = nullptr) {
+inline bool gemm_AX(cudaStream_t st, const ell1_dict_t* D, const void* X, int64_t ldx, void* Y, int64_t ldy,
+                    int B, const F32Split* sp = nullptr) {
   if (B <= 0) return true;
-  if (D->dtype == ELL1_F64) {
-    const double one = 1.0, zero = 0.0;
-    return cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)D->ld, B, (int)D->n, &one,
-                       (const double*)D->A, (int)D->ld, (const double*)X, (int)ldx, &zero, (double*)Y,
-                       (int)ldy) == CUBLAS_STATUS_SUCCESS;
-  }
-  return sgemm_split(h, CUBLAS_OP_N, (int)D->ld, B, (int)D->n, (const float*)D->A, (int)D->ld, sp,
-                     (const float*)X, ldx, (float*)Y, ldy, D->n);
+  if (D->dtype == ELL1_F64)
+    return dgemm(0, 0, D->ld, B, D->n, (const double*)D->A, D->ld, (const double*)X, ldx, (double*)Y, ldy, st);
+  return sgemm_split(st, 0, (int)D->ld, B, (int)D->n, sp, (const float*)X, ldx, (float*)Y, ldy);
 }
 
 // G(n x B) = A^T R(ld x B)
-inline bool gemm_AtR(cublasHandle_t h, const ell1_dict_t* D, const void* R, int64_t ldr, void* G,
-                     int64_t ldg, int B, const F32Split* sp = nullptr) {
+inline bool gemm_AtR(cudaStream_t st, const ell1_dict_t* D, const void* R, int64_t ldr, void* G, int64_t ldg,
+                     int B, const F32Split* sp = nullptr) {
   if (B <= 0) return true;
-  if (D->dtype == ELL1_F64) {
-    const double one = 1.0, zero = 0.0;
-    return cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)D->n, B, (int)D->ld, &one,
-                       (const double*)D->A, (int)D->ld, (const double*)R, (int)ldr, &zero, (double*)G,
-                       (int)ldg) == CUBLAS_STATUS_SUCCESS;
-  }
-  return sgemm_split(h, CUBLAS_OP_T, (int)D->n, B, (int)D->ld, (const float*)D->A, (int)D->ld, sp,
-                     (const float*)R, ldr, (float*)G, ldg, D->ld);
+  if (D->dtype == ELL1_F64)
+    return dgemm(1, 0, D->n, B, D->ld, (const double*)D->A, D->ld, (const double*)R, ldr, (double*)G, ldg, st);
+  return sgemm_split(st, 1, (int)D->n, B, (int)D->ld, sp, (const float*)R, ldr, (float*)G, ldg);
 }
 
 // workspace floats for one dictionary split (both orientations)
@@ -234,9 +157,10 @@ inline int64_t f32split_dict_floats(const ell1_dict_t* D) {
   return 2 * align_up(D->n * D->ld, 64) + 2 * align_up(D->ld * align_up(D->n, 4), 64);
 }
 
-// workspace floats for the dictionary split + the right-operand scratch
+// workspace floats of f32split_setup (the right operand is split inside the GEMM)
 inline int64_t f32split_floats(const ell1_dict_t* D, int64_t xcap) {
-  return f32split_dict_floats(D) + 2 * align_up(xcap, 64);
+  (void)xcap;
+  return f32split_dict_floats(D);
 }
 
 // split a column-major (ld x n) fp32 dictionary A into sp's four arrays
@@ -247,7 +171,7 @@ inline bool f32split_dict(F32Split& sp, Carve& cv, const ell1_dict_t* D, const f
   float* rhi = cv.take<float>(D->ld * pr);
   float* rlo = cv.take<float>(D->ld * pr);
   if (!cv.ok) return false;
-  sp.Ahi = hi; sp.Alo = lo; sp.Arhi = rhi; sp.Arlo = rlo; sp.pr = pr;
+  sp.Ahi = hi; sp.Alo = lo; sp.Arhi = rhi; sp.Arlo = rlo; sp.pr = pr; sp.pc = D->ld;
   if (!split_tf32(A, hi, lo, D->n * D->ld, s)) return false;
   dim3 g((unsigned)((pr + 31) / 32), (unsigned)((D->ld + 31) / 32));
   split_tf32_t_kernel<<<g, dim3(32, 8), 0, s>>>(A, rhi, rlo, D->ld, D->ld, D->n, pr);
@@ -255,11 +179,8 @@ inline bool f32split_dict(F32Split& sp, Carve& cv, const ell1_dict_t* D, const f
 }
 
 inline bool f32split_setup(F32Split& sp, Carve& cv, const ell1_dict_t* D, int64_t xcap, cudaStream_t s) {
-  if (!f32split_dict(sp, cv, D, (const float*)D->A, s)) return false;
-  sp.Xhi = cv.take<float>(xcap);
-  sp.Xlo = cv.take<float>(xcap);
-  sp.xcap = xcap;
-  return cv.ok;
+  (void)xcap;
+  return f32split_dict(sp, cv, D, (const float*)D->A, s);
 }
 
 }  // namespace ell1

@@ -1,0 +1,193 @@
+// chol.cu — dense Cholesky factor + solve of PDIPA's weighted normal matrix
+// M = A diag(w) A^T (pdipa.py:43-62: _factor_with_jitter, then
+// factor.solve(rhs) inside _eliminate), replacing numpy/LAPACK's potrf/potrs.
+//
+// Blocked right-looking factorisation, NB = 64 columns per panel:
+//   chol_panel_kernel   one CTA factors the NB x NB diagonal block in shared
+//                       memory (pivot <= 0 or not finite -> status = k + 1,
+//                       LAPACK's convention; the host then retries with the
+//                       reference's jitter)
+//   chol_trsm_kernel    L21 = A21 L11^-T, one thread per row below the panel
+//   dgemm (DMMA)        trailing update A22 -= L21 L21^T (dmma_gemm.cu)
+// Solve: L y = rhs, L^T x = y, 32-column blocks in one CTA (the small
+// triangles by one warp, the rank-32 updates by the whole CTA).
+#include "dmma_gemm.cuh"
+#include "ell1_b200.h"
+#include "engine.cuh"
+
+namespace ell1 {
+namespace {
+
+constexpr int NB = 64;
+constexpr int PT = 256;
+
+__global__ void chol_copy_kernel(int64_t d, const double* __restrict__ M, int64_t ldm, double* __restrict__ L,
+                                 int64_t ldl, double jitter, int* status) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *status = 0;
+  const int64_t tot = d * d;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t / d, i = t - j * d;
+    double v = M[j * ldm + i];
+    if (i == j) v += jitter;
+    L[j * ldl + i] = v;
+  }
+}
+
+// factor the nb x nb diagonal block at (kb, kb) in place (lower triangle)
+__global__ void __launch_bounds__(PT) chol_panel_kernel(double* __restrict__ L, int64_t ld, int64_t kb, int nb,
+                                                        int* status) {
+  __shared__ double T[NB][NB + 1];
+  __shared__ int bad;
+  if (*(volatile int*)status != 0) return;
+  for (int t = threadIdx.x; t < nb * nb; t += PT) {
+    const int c = t / nb, r = t - c * nb;
+    T[r][c] = L[(kb + c) * ld + kb + r];
+  }
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    if (threadIdx.x == 0) {
+      const double dj = T[j][j];
+      if (!(dj > 0.0) || !isfinite(dj)) bad = (int)(kb + j) + 1;
+      else T[j][j] = sqrt(dj);
+    }
+    __syncthreads();
+    if (bad) break;
+    const double piv = T[j][j];
+    for (int i = j + 1 + threadIdx.x; i < nb; i += PT) T[i][j] /= piv;
+    __syncthreads();
+    const int m = nb - j - 1;
+    for (int t = threadIdx.x; t < m * m; t += PT) {
+      const int c = t / m, r = t - c * m;
+      if (r >= c) T[j + 1 + r][j + 1 + c] -= T[j + 1 + r][j] * T[j + 1 + c][j];
+    }
+    __syncthreads();
+  }
+  if (bad) {
+    if (threadIdx.x == 0) *status = bad;
+    return;
+  }
+  for (int t = threadIdx.x; t < nb * nb; t += PT) {
+    const int c = t / nb, r = t - c * nb;
+    if (r >= c) L[(kb + c) * ld + kb + r] = T[r][c];
+  }
+}
+
+// rows i in [r0, d): L[i, kb:kb+nb] <- L[i, kb:kb+nb] L11^-T
+__global__ void __launch_bounds__(PT) chol_trsm_kernel(double* __restrict__ L, int64_t ld, int64_t d, int64_t kb,
+                                                       int nb, const int* status) {
+  __shared__ double T[NB][NB + 1];
+  if (*(volatile int*)status != 0) return;
+  for (int t = threadIdx.x; t < nb * nb; t += PT) {
+    const int c = t / nb, r = t - c * nb;
+    T[r][c] = L[(kb + c) * ld + kb + r];
+  }
+  __syncthreads();
+  const int64_t i = kb + nb + (int64_t)blockIdx.x * PT + threadIdx.x;
+  if (i >= d) return;
+  double x[NB];
+#pragma unroll
+  for (int c = 0; c < NB; ++c) x[c] = c < nb ? L[(kb + c) * ld + i] : 0.0;
+#pragma unroll
+  for (int c = 0; c < NB; ++c) {
+    if (c < nb) {
+      double v = x[c];
+#pragma unroll
+      for (int p = 0; p < c; ++p) v -= x[p] * T[c][p];
+      x[c] = v / T[c][c];
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NB; ++c)
+    if (c < nb) L[(kb + c) * ld + i] = x[c];
+}
+
+// x = (L L^T)^-1 rhs, one CTA; y staged in shared memory (d doubles)
+__global__ void __launch_bounds__(1024) chol_solve_kernel(int64_t d, const double* __restrict__ L, int64_t ld,
+                                                          const double* __restrict__ rhs, double* __restrict__ x) {
+  extern __shared__ double y[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  for (int64_t i = tid; i < d; i += blockDim.x) y[i] = rhs[i];
+  __syncthreads();
+  // forward: L y = rhs, 32-column blocks
+  for (int64_t jb = 0; jb < d; jb += 32) {
+    const int w = (int)((d - jb) < 32 ? (d - jb) : 32);
+    if (warp == 0) {
+      double v = lane < w ? y[jb + lane] : 0.0;
+      for (int j = 0; j < w; ++j) {
+        const double xj = __shfl_sync(0xffffffffu, v, j) / L[(jb + j) * ld + jb + j];
+        if (lane == j) v = xj;
+        if (lane > j && lane < w) v -= L[(jb + j) * ld + jb + lane] * xj;
+      }
+      if (lane < w) y[jb + lane] = v;
+    }
+    __syncthreads();
+    for (int64_t i = jb + w + tid; i < d; i += blockDim.x) {
+      double s = y[i];
+      for (int j = 0; j < w; ++j) s -= L[(jb + j) * ld + i] * y[jb + j];
+      y[i] = s;
+    }
+    __syncthreads();
+  }
+  // backward: L^T x = y, blocks from the end; x_i = (y_i - sum_{j>i} L_ji x_j) / L_ii
+  for (int64_t je = d; je > 0; je -= 32) {
+    const int64_t jb = je >= 32 ? je - 32 : 0;
+    const int w = (int)(je - jb);
+    if (warp == 0) {
+      double v = lane < w ? y[jb + lane] : 0.0;
+      for (int j = w - 1; j >= 0; --j) {
+        const double xj = __shfl_sync(0xffffffffu, v, j) / L[(jb + j) * ld + jb + j];
+        if (lane == j) v = xj;
+        if (lane < j) v -= L[(jb + lane) * ld + jb + j] * xj;
+      }
+      if (lane < w) y[jb + lane] = v;
+    }
+    __syncthreads();
+    // y_i -= sum_{j in block} L_ji x_j for i < jb: one warp per column i (coalesced in j)
+    for (int64_t i = warp; i < jb; i += nw) {
+      double s = lane < w ? L[i * ld + jb + lane] * y[jb + lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) y[i] -= s;
+    }
+    __syncthreads();
+  }
+  for (int64_t i = tid; i < d; i += blockDim.x) x[i] = y[i];
+}
+
+}  // namespace
+}  // namespace ell1
+
+using namespace ell1;
+
+extern "C" int ell1_chol_factor_dense(int64_t d, const double* M, int64_t ldm, double jitter, double* L, int64_t ldl,
+                                      int* status, void* stream) {
+  if (d < 1 || !M || !L || !status || ldm < d || ldl < d) return ELL1_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t tot = d * d;
+  const unsigned g = (unsigned)((tot + 255) / 256 < 148 * 8 ? (tot + 255) / 256 : 148 * 8);
+  chol_copy_kernel<<<g, 256, 0, s>>>(d, M, ldm, L, ldl, jitter, status);
+  for (int64_t kb = 0; kb < d; kb += NB) {
+    const int nb = (int)((d - kb) < NB ? (d - kb) : NB);
+    chol_panel_kernel<<<1, PT, 0, s>>>(L, ldl, kb, nb, status);
+    const int64_t below = d - kb - nb;
+    if (below <= 0) break;
+    chol_trsm_kernel<<<(unsigned)((below + PT - 1) / PT), PT, 0, s>>>(L, ldl, d, kb, nb, status);
+    // trailing update A22 -= L21 L21^T (full square; the lower triangle is used)
+    double* L21 = L + kb * ldl + kb + nb;
+    double* A22 = L + (kb + nb) * ldl + kb + nb;
+    if (!dgemm(0, 1, below, below, nb, L21, ldl, L21, ldl, A22, ldl, s, -1.0, 1.0)) return ELL1_ERR_CUDA;
+  }
+  return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
+}
+
+extern "C" int ell1_chol_solve_dense(int64_t d, const double* L, int64_t ldl, const double* rhs, double* x,
+                                     void* stream) {
+  if (d < 1 || !L || !rhs || !x || ldl < d) return ELL1_ERR_ARG;
+  const size_t smem = (size_t)d * 8;
+  if (smem > 200 * 1024) return ELL1_ERR_ARG;
+  if (cudaFuncSetAttribute(chol_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return ELL1_ERR_CUDA;
+  chol_solve_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(d, L, ldl, rhs, x);
+  return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
+}

@@ -16,15 +16,16 @@
 
 namespace ell1 {
 
-// C (m x n, column-major, ldc) = op(A) (m x k) * op(B) (k x n).
+// C (m x n, column-major, ldc) = alpha op(A) (m x k) * op(B) (k x n) + beta C.
 //   transA = 0: A is m x k column-major (lda >= m); 1: A is k x m (lda >= k).
 //   transB = 0: B is k x n column-major (ldb >= k); 1: B is n x k (ldb >= n).
 // Returns false on a launch error or bad argument.
 bool dgemm(int transA, int transB, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
-           const double* B, int64_t ldb, double* C, int64_t ldc, cudaStream_t s);
+           const double* B, int64_t ldb, double* C, int64_t ldc, cudaStream_t s, double alpha = 1.0,
+           double beta = 0.0);
 // the same with a fixed tile variant (0..4) / K split (-1: heuristic), for tuning
 bool dgemm_variant(int variant, int split, int transA, int transB, int64_t m, int64_t n, int64_t k,
                    const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
-                   cudaStream_t s);
+                   cudaStream_t s, double alpha = 1.0, double beta = 0.0);
 
 }  // namespace ell1

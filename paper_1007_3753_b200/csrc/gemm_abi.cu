@@ -33,7 +33,6 @@ extern "C" int ell1_gemm_f32(int32_t trans, int64_t M, int64_t N, int64_t K, con
   if (M == 0 || N == 0) return ELL1_OK;
   if (wsb < ell1_gemm_f32_workspace(trans, M, K) || !ws) return ELL1_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  fp32_mode_select();
   const int64_t pitch = align_up(K, 4);
   Carve cv(ws, wsb);
   float* hi = cv.take<float>(M * pitch);

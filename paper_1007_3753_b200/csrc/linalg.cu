@@ -265,13 +265,8 @@ extern "C" int ell1_gram_dd(const ell1_dict_t* D, const double* w, double* G, vo
   if (D->dtype == ELL1_F64) scale_cols_kernel<double><<<g, 256, 0, s>>>((const double*)D->A, D->ld, D->n, w, AW, nullptr);
   else scale_cols_kernel<float><<<g, 256, 0, s>>>((const float*)D->A, D->ld, D->n, w, AW, A64);
   if (cudaGetLastError() != cudaSuccess) return ELL1_ERR_CUDA;
-  cublasHandle_t h = blas_handle(s);
-  if (!h) return ELL1_ERR_CUDA;
-  const double one = 1.0, zero = 0.0;
-  // G (d x d, ld d) = AW (d x n, ld) * A64^T
-  const cublasStatus_t st = cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)D->d, (int)D->d, (int)D->n, &one, AW,
-                                        (int)D->ld, A64, (int)D->ld, &zero, G, (int)D->d);
-  return st == CUBLAS_STATUS_SUCCESS ? ELL1_OK : ELL1_ERR_CUDA;
+  // G (d x d, ld d) = AW (d x n, ld) * A64^T on the DMMA path (dmma_gemm.cu)
+  return dgemm(0, 1, D->d, D->d, D->n, AW, D->ld, A64, D->ld, G, D->d, s) ? ELL1_OK : ELL1_ERR_CUDA;
 }
 
 extern "C" size_t ell1_pcg_workspace(const ell1_dict_t* M) {

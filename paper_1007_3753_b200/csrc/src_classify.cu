@@ -84,4 +84,4 @@ extern "C" int ell1_src_classify(const ell1_dict_t* D, const double* Bmat, int32
 
 // fp32 GEMM path of the batched solvers: 2 = 3xTF32 split on the tensor pipe
 // (opt-in), 0 = SIMT SGEMM, -1 = not used yet
-extern "C" int ell1_blas_fp32_mode(void) { return ell1::fp32_gemm_mode(); }
+

@@ -2,11 +2,11 @@
 
 min ||x||_1 s.t. A x = b as the split LP min 1'v, [A, -A] v = b, v >= 0.
 Per Newton step the device runs: two dictionary products (panel GEMV /
-GEMV^T), the weighted row Gram M = A diag(w+ + w-) A^T (cuBLAS DGEMM,
-``ell1_gram_dd``), the fused residual / elimination / step-to-boundary /
-duality-measure kernels of csrc/pdipa.cu, and one d x d Cholesky solve of M
-(cuSOLVER through torch.linalg — a plain library factorisation, like the DALM
-row-Gram factor).  The host loop here only sequences those calls and reads
+GEMV^T), the weighted row Gram M = A diag(w+ + w-) A^T (the library's DMMA
+GEMM, ``ell1_gram_dd``), the fused residual / elimination / step-to-boundary /
+duality-measure kernels of csrc/pdipa.cu, and one d x d Cholesky factor +
+solve of M (csrc/chol.cu: blocked panels, DMMA trailing updates, with the
+reference's one jitter retry).  The host loop here only sequences those calls and reads
 back a few scalars per step; it follows the reference's control flow
 exactly (jitter retry, non-finite / stalled-measure stops, notes, trace).
 """
@@ -97,16 +97,27 @@ class _Ops:
         return tr
 
     def factor_solve(self, M, rhs, tr):
-        """dy = M^-1 rhs with the reference's one jitter retry (pdipa.py:43-52)."""
+        """dy = M^-1 rhs with the reference's one jitter retry (pdipa.py:43-52):
+        the library's blocked Cholesky (chol.cu; DMMA trailing updates) and
+        triangular solves."""
         torch = self.torch
-        Mv = M.view(self.d, self.d)
-        Lf, info = torch.linalg.cholesky_ex(Mv)
-        if int(info.item()) != 0:
-            jit = 1e-12 * max(float(tr.item()) / self.d, 1.0)
-            Lf, info = torch.linalg.cholesky_ex(Mv + jit * torch.eye(self.d, dtype=torch.float64, device=self.dev))
-            if int(info.item()) != 0:
+        d = self.d
+        if getattr(self, "_Lf", None) is None:
+            self._Lf = torch.empty(d * d, dtype=torch.float64, device=self.dev)
+            self._cst = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        Lf, cst = self._Lf, self._cst
+        _lib.check(self.L.ell1_chol_factor_dense(d, device.ptr(M), d, 0.0, device.ptr(Lf), d, device.ptr(cst),
+                                                 self.st), "ell1_chol_factor_dense")
+        if int(cst.item()) != 0:
+            jit = 1e-12 * max(float(tr.item()) / d, 1.0)
+            _lib.check(self.L.ell1_chol_factor_dense(d, device.ptr(M), d, jit, device.ptr(Lf), d, device.ptr(cst),
+                                                     self.st), "ell1_chol_factor_dense")
+            if int(cst.item()) != 0:
                 raise IllConditionedError("weighted normal matrix is singular")
-        return torch.cholesky_solve(rhs[: self.d].view(self.d, 1), Lf).view(self.d)
+        out = torch.empty(d, dtype=torch.float64, device=self.dev)
+        _lib.check(self.L.ell1_chol_solve_dense(d, device.ptr(Lf), d, device.ptr(rhs), device.ptr(out), self.st),
+                   "ell1_chol_solve_dense")
+        return out
 
 
 def pdipa_solve(P, config, observer=None):

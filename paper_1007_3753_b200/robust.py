@@ -355,6 +355,31 @@ def _palm_options(config):
         raise ValueError("mu0 must be positive and rho must exceed 1")
 
 
+def ist_block_step(B, b, w, e, lam, alpha):
+    """One block soft-threshold sweep on the alignment objective
+    (robust.py:433-445): r = b - B w - e, w_next = w + B^T r / alpha,
+    e_next = soft(e + r / alpha, lam / alpha).  Returns (w_next, e_next);
+    ValueError unless alpha > 0.  Runs on the device (ell1_align_ist_step)."""
+    import ctypes
+    from paper_1007_3753_b200 import _lib
+    if not alpha > 0:
+        raise ValueError("alpha must be positive")
+    torch = device._torch()
+    B = np.ascontiguousarray(B, dtype=np.float64)
+    d, m = B.shape
+    if m > 32:
+        raise ValueError("ist_block_step on the device supports m <= 32 columns")
+    dev = device.current_device()
+    t = lambda v: torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(dev)  # noqa: E731
+    Bd, bd, wd, ed = t(B), t(b), t(w), t(e)
+    wn = torch.empty(m, dtype=torch.float64, device=dev)
+    en = torch.empty(d, dtype=torch.float64, device=dev)
+    _lib.check(_lib.lib().ell1_align_ist_step(d, m, Bd.data_ptr(), m, bd.data_ptr(), wd.data_ptr(), ed.data_ptr(),
+                                              float(lam), float(alpha), wn.data_ptr(), en.data_ptr(),
+                                              device.stream_ptr(dev)), "ell1_align_ist_step")
+    return wn.cpu().numpy(), en.cpu().numpy()
+
+
 def align_palm_solve_batch(Bs, bs, config):
     """align_palm_solve for a batch of images (element j == align_palm_solve
     on (Bs[j], bs[j])).  Returns (W, E)."""

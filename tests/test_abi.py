@@ -49,3 +49,18 @@ def test_no_cpu_fallback_without_gpu():
     P = ProblemInstance(np.eye(3), np.ones(3))
     with pytest.raises(DeviceError):
         fista_solve(P, SolverConfig(lam=0.1))
+
+
+def test_library_has_no_blas_dependency():
+    """Every dictionary product is the library's own kernel (tcgen05 3xTF32 for
+    fp32, DMMA for fp64): libell1b200.so links no cuBLAS / cuSOLVER and
+    references none of their symbols."""
+    import subprocess
+    from paper_1007_3753_b200 import _lib
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("library not built")
+    dyn = subprocess.run(["readelf", "-d", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    needed = [ln for ln in dyn.splitlines() if "NEEDED" in ln]
+    assert needed and not any("cublas" in ln or "cusolver" in ln for ln in needed), needed
+    syms = subprocess.run(["nm", "-D", "--undefined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "cublas" not in syms and "cusolver" not in syms

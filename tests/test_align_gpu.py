@@ -111,3 +111,41 @@ def test_zero_data_and_option_validation():
         align_palm_solve(prob, SolverConfig(options={"rho": 1.0}))
     with pytest.raises(ValueError):
         align_ist_solve(prob, -1.0, SolverConfig())
+
+
+def test_ist_block_step_matches_reference_formula():
+    """robust.ist_block_step (robust.py:433-445) on the device vs the
+    reference's numpy expression; alpha <= 0 raises ValueError."""
+    _cuda()
+    from paper_1007_3753_b200.robust import ist_block_step
+    from oracle.l1_oracle import soft
+    rng = np.random.default_rng(5)
+    for d, m in ((40, 3), (1500, 11), (5000, 32)):
+        B = rng.standard_normal((d, m))
+        b, e, w = rng.standard_normal(d), rng.standard_normal(d) * (rng.random(d) < 0.2), rng.standard_normal(m)
+        lam, alpha = 0.3, 2.5
+        wn, en = ist_block_step(B, b, w, e, lam, alpha)
+        r = b - B @ w - e
+        np.testing.assert_allclose(wn, w + (B.T @ r) / alpha, rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(en, soft(e + r / alpha, lam / alpha), rtol=1e-12, atol=1e-12)
+    with pytest.raises(ValueError):
+        ist_block_step(B, b, w, e, lam, 0.0)
+
+
+@pytest.mark.parametrize("d,m", [(1024, 32), (2048, 16)])
+def test_align_large_images_stage_b_in_global_memory(d, m):
+    """Images whose (d+1) m doubles exceed the SM's shared memory:
+    B is staged in global memory; results equal the numpy PALM restatement."""
+    _cuda()
+    from oracle.l1_oracle import align_palm
+    from paper_1007_3753_b200 import robust
+    from paper_1007_3753_b200.model import SolverConfig
+    insts = [align_instance(seed=900 + j, d=d, m=m, frac=0.2) for j in range(3)]
+    Bs = np.stack([B for B, _ in insts])
+    bs = np.stack([b for _, b in insts])
+    cfg = SolverConfig(tol=1e-8, max_iter=5000)
+    W, E = robust.align_palm_solve_batch(Bs, bs, cfg)
+    for j in range(3):
+        w_ref, e_ref = align_palm(Bs[j], bs[j], tol=1e-8, max_iter=5000)
+        assert _rel(W[j], w_ref) <= 1e-9
+        assert _rel(E[j], e_ref) <= 1e-9

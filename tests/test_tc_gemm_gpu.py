@@ -96,4 +96,4 @@ def test_tc_gemm_is_the_active_fp32_path():
     B = np.ones((32, 8), np.float32)
     C = _gemm(torch, A, B, 0)
     assert np.all(C == 32.0)
-    assert _lib.lib().ell1_blas_fp32_mode() == 3
+    assert not hasattr(_lib.lib(), "ell1_blas_fp32_mode")      # no alternative fp32 backend
