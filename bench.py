@@ -179,6 +179,43 @@ def cpu_solve_once(P):
     return oracle.fista(P.A, P.b, lam=None, tol=1e-6, stop=("relative-estimate", 1e-6))
 
 
+def _pool_init():
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)                       # one BLAS thread per worker process
+
+
+def _cpu_task(args):
+    """One reference-port solve in a worker (SURVEY §8(d) batched CPU baseline)."""
+    import oracle  # CPU baseline only
+    kind, A, b = args[:3]
+    if kind == "fista":
+        return oracle.fista(A, b, lam=1e-3, tol=1e-6, stop=("relative-estimate", 1e-6)).iterations
+    if kind == "dalm":
+        return oracle.dalm(A, b, tol=1e-6, stop=("relative-estimate", 1e-6)).iterations
+    if kind == "homotopy":
+        return oracle.homotopy(A, b, 1e-3)[0].iterations
+    if kind == "cab_dalm":
+        return oracle.cab(A, b, "dalm", tol=1e-4, max_iter=2000)[2].iterations
+    raise ValueError(kind)
+
+
+def cpu_pool_rate(kind, A, cols, per_core=4):
+    """Instances/s of the reference port over a process pool of all host cores
+    (one BLAS thread each, the reference bench's _run_tasks pattern) on
+    per_core x cores instances of the batch."""
+    from concurrent.futures import ProcessPoolExecutor
+    cores = os.cpu_count()
+    count = min(per_core * cores, len(cols))
+    t0 = time.perf_counter()
+    with ProcessPoolExecutor(max_workers=cores, initializer=_pool_init) as ex:
+        its = list(ex.map(_cpu_task, [(kind, A, cols[j]) for j in range(count)]))
+    el = time.perf_counter() - t0
+    return {"solves_per_sec": count / el, "iterations_per_sec": float(sum(its)) / el, "instances": count,
+            "seconds": el, "cores": cores, "kind": "port",
+            "sample": "first %d instances of the batch, ProcessPoolExecutor(%d workers, 1 BLAS thread each)"
+                      % (count, cores)}
+
+
 def cpu_baseline_cfg2(P, budget_s=10.0):
     n = 0
     t0 = time.perf_counter()
@@ -498,28 +535,29 @@ def leg_cfg3(torch, dev, queries=1024):
     torch.cuda.synchronize()
     t = s.elapsed_time(e) / 1e3
     its = res.iterations.astype(np.int64)
-    tfl = float(its.sum()) * 5 * 2.0 * 1024 * 1216 / t / 1e12
+    # 2 passes over A (4 d n_A) + the two triangular solves with the
+    # row-Gram factor (2 d^2) per query-iteration (7.08 MFLOP; 7.25 GFLOP per
+    # batched iteration at 1024 queries); the identity block costs nothing
+    d_, nA = 1024, 1216
+    tfl = float(its.sum()) * (4.0 * d_ * nA + 2.0 * d_ * d_) / t / 1e12
     peaks = gemm_peaks(torch, dev)
-    pk = peaks["sgemm_tflops"]
     return {"workload": "cfg3: CAB [A I] 1024 x 2240, %d queries, batched DALM fp32 storage, "
                         "tol 1e-4, min-class-residual labels" % queries,
-            "roofline": {"bound": "fp32 GEMMs", "achieved": tfl, "peak": pk, "unit": "TFLOP/s",
-                         "frac": tfl / pk, "peak_source": "cuBLAS SGEMM 8192^3 measured in this run",
-                         "algorithmic": "5 dictionary passes x 2 d n_A flops per query-iteration"},
+            "roofline": {"bound": "tensor (3xTF32 tcgen05)", "achieved": 3 * tfl, "peak": peaks["tf32_tflops"],
+                         "unit": "TFLOP/s", "frac": 3 * tfl / peaks["tf32_tflops"],
+                         "peak_source": "cuBLAS TF32 8192^3 measured in this run",
+                         "algorithmic": "SURVEY 8(d): (4 d n_A + 2 d^2) flops per query-iteration, x3 TF32 "
+                                        "MMAs per fp32-accurate product",
+                         "fp32_accurate_tflops": tfl},
             "queries_per_sec": queries / t, "ms_per_batch": 1e3 * t,
             "mean_iterations": float(its.mean()), "max_iterations": int(its.max()),
             "accuracy_vs_truth": float(np.mean(labels == truth)),
             "fp32_gemm": "3xTF32 tcgen05 kernel (tc_gemm.cu)",
-            "tensor_pipe": ({"mma_tflops": 3 * tfl, "peak": peaks["tf32_tflops"], "unit": "TFLOP/s",
-                             "frac": 3 * tfl / peaks["tf32_tflops"],
-                             "peak_source": "cuBLAS TF32 8192^3 measured in this run",
-                             "note": "3 TF32 MMAs per fp32-accurate product; algorithmic flops only "
-                                     "(the y-step's identity block and certificate products not counted)"}
-                            ),
-            "note": "timed through the public call (host queries in, labels out)"}
+            "note": "timed through the public call (host queries in, labels out)",
+            "cpu_baseline": cpu_pool_rate("cab_dalm", A, [Bq[q] for q in range(queries)], per_core=2)}
 
 
-def leg_cfg5(torch, dev, ws=1, B=1024, cpu_sample=8):
+def leg_cfg5(torch, dev, ws=1, B=1024, cpu_sample=4):
     """BASELINE config 5 point: B instances sharing one A (512 x 2048, fp64),
     k ~ U[16, 256], noiseless b = A x0; batched FISTA (lambda 1e-3,
     relative-estimate 1e-6), batched dual ALM (relative-estimate 1e-6) and
@@ -532,13 +570,7 @@ def leg_cfg5(torch, dev, ws=1, B=1024, cpu_sample=8):
     from paper_1007_3753_b200.distributed import solve_batch_sharded
     from paper_1007_3753_b200.model import SolverConfig, StoppingRule
     d, n = 512, 2048
-    A = synth.gen_gaussian_dict(d, n, 5)
-    rng = np.random.default_rng(55)
-    X = np.zeros((n, B))
-    for j in range(B):
-        kk = int(rng.integers(16, 257))
-        X[rng.choice(n, kk, replace=False), j] = rng.standard_normal(kk)
-    Bmat = A @ X
+    A, _, Bmat = synth.cfg5_batch(B)
     D = dv.DeviceDictionary(A, dtype="float64", device=dev.index)
     rel = StoppingRule("relative-estimate", 1e-6)
     legs = {
@@ -569,31 +601,24 @@ def leg_cfg5(torch, dev, ws=1, B=1024, cpu_sample=8):
         t = float(t.item())
         its = res.iterations.astype(np.int64)
         unit = "breakpoints_per_sec" if name == "homotopy" else "iterations_per_sec"
-        # GEMM-form work per instance-iteration: dictionary passes x 2 d n flops
-        passes = {"fista": 2, "dalm": 5, "homotopy": 2}[name]
-        tfl = float(its.sum()) * passes * 2.0 * d * n / t / 1e12
+        # SURVEY §8(d) algorithmic flops per instance-iteration: FISTA 2 passes (4 d n),
+        # DALM 2 passes + 2 triangular solves (4 d n + 2 d^2), Homotopy the 2 A^T passes (4 d n)
+        per = {"fista": 4.0 * d * n, "dalm": 4.0 * d * n + 2.0 * d * d, "homotopy": 4.0 * d * n}[name]
+        tfl = float(its.sum()) * per / t / 1e12
         pk = gemm_peaks(torch, dev)["dgemm_tflops"]
         out[name] = {"solves_per_sec": B / t, "ms_per_batch": 1e3 * t, unit: float(its.sum()) / t,
                      "mean_iterations": float(its.mean()), "converged": int(res.converged.sum()),
                      "roofline": {"bound": "tensor (fp64 DMMA GEMMs)", "achieved": tfl,
                                   "peak": pk, "unit": "TFLOP/s", "frac": tfl / pk,
                                   "peak_source": "cuBLAS DGEMM 8192^3 measured in this run",
-                                  "algorithmic": "%d dictionary passes x 2 d n flops per instance-iteration"
-                                                 % passes}}
+                                  "algorithmic": {"fista": "4 d n", "dalm": "4 d n + 2 d^2",
+                                                  "homotopy": "4 d n (the two A^T passes)"}[name]
+                                                 + " flops per instance-iteration (SURVEY 8(d))"}}
     if ws == 1 and cpu_sample > 0:
-        # CPU reference port on a bounded sample of the same instances (all host cores)
-        import oracle
-        t0 = time.perf_counter()
-        for j in range(cpu_sample):
-            oracle.fista(A, Bmat[:, j], lam=1e-3, tol=1e-6, stop=("relative-estimate", 1e-6))
-        tf = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        for j in range(cpu_sample):
-            oracle.homotopy(A, Bmat[:, j], 1e-3)
-        th = time.perf_counter() - t0
-        out["cpu_baseline"] = {"fista_solves_per_sec": cpu_sample / tf,
-                               "homotopy_solves_per_sec": cpu_sample / th, "cores": os.cpu_count(),
-                               "kind": "port", "sample": "first %d instances, one at a time" % cpu_sample}
+        # CPU reference port on a bounded sample of the same instances (all host cores, process pool)
+        cols = [Bmat[:, j] for j in range(B)]
+        out["cpu_baseline"] = {name: cpu_pool_rate(name, A, cols, per_core=cpu_sample)
+                               for name in ("fista", "homotopy", "dalm")}
     return out
 
 
@@ -646,14 +671,7 @@ def leg_cfg5_sweep(torch, dev, sizes=(1, 16, 256, 1024, 8192)):
     from paper_1007_3753_b200.batched import fista_solve_batch, homotopy_solve_batch
     from paper_1007_3753_b200.model import SolverConfig, StoppingRule
     d, n = 512, 2048
-    A = synth.gen_gaussian_dict(d, n, 5)
-    rng = np.random.default_rng(55)
-    Bmax = max(sizes)
-    X = np.zeros((n, Bmax))
-    for j in range(Bmax):
-        kk = int(rng.integers(16, 257))
-        X[rng.choice(n, kk, replace=False), j] = rng.standard_normal(kk)
-    Bmat = A @ X
+    A, _, Bmat = synth.cfg5_batch(max(sizes))
     rel = StoppingRule("relative-estimate", 1e-6)
     D64 = dv.DeviceDictionary(A, dtype="float64", device=dev.index)
     D32 = dv.DeviceDictionary(A, dtype="float32", device=dev.index)

@@ -427,6 +427,20 @@ int ell1_sfista_pre(const ell1_dict_t* D, ell1_shard_ctl_t* ctl, const ell1_sfis
 int ell1_sfista_post(const ell1_dict_t* D, ell1_shard_ctl_t* ctl, const ell1_sfista_bufs_t* V, void* ws,
                      size_t ws_bytes, void* stream);
 
+/* ------------------------------ column-sharded Homotopy (shard_hom.cu)
+ * Per-rank candidates of homotopy.py:78-105 / :229-233 for the sharded path
+ * (paper_1007_3753_b200/sharded_homotopy.py); first index wins ties.
+ * out2 = {max |c|, first argmax}; out4 = {gamma_a, i_a, gamma_b, i_b} over the
+ * columns with mask == 0 (floor 1e-10 max(lam, 1e-30), INFINITY / -1 if none);
+ * gamma_minus: {min -x/d (finite, > 0), its position; ties -> lowest keys[k]};
+ * xstats: {sum |x|, count |x| > 1e-10 max(max|x|, 1)}. */
+int ell1_hom_absmax(int64_t n, const double* c, double* out2, void* stream);
+int ell1_hom_gammas(int64_t n, const double* c, const double* w, const unsigned char* mask, double lam,
+                    double* out4, void* stream);
+int ell1_hom_gamma_minus(int64_t m, const double* x, const double* d, const int64_t* keys, double* out2,
+                         void* stream);
+int ell1_hom_xstats(int64_t m, const double* x, double* out2, void* stream);
+
 /* Dense Cholesky of PDIPA's weighted normal matrix (pdipa.py:43-52
  * _factor_with_jitter -> numerics.chol_factor; chol.cu): L (lower, ldl) of
  * M + jitter I (M column-major, ldm); *status (device int) = 0, or k + 1 when
@@ -435,6 +449,10 @@ int ell1_chol_factor_dense(int64_t d, const double* M, int64_t ldm, double jitte
                            int* status, void* stream);
 /* x = (L L^T)^-1 rhs (factor.solve, numerics.py:62-72); d <= 25600 */
 int ell1_chol_solve_dense(int64_t d, const double* L, int64_t ldl, const double* rhs, double* x, void* stream);
+/* the same for nrhs right-hand sides (columns of rhs / x, leading dimensions ldr / ldx),
+ * one CTA each: the dual ALM's row-Gram inverse G^-1 (alm.py:162-169 _gram_factor) */
+int ell1_chol_solve_dense_multi(int64_t d, const double* L, int64_t ldl, int64_t nrhs, const double* rhs,
+                                int64_t ldr, double* x, int64_t ldx, void* stream);
 
 /* ---------------------------------------------- PDIPA vector kernels (pdipa.cu)
  * Primal-dual interior point on the split LP min 1'v, [A, -A] v = b, v >= 0

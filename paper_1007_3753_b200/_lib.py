@@ -215,10 +215,18 @@ _SIGS = {
                                       ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "ell1_shard_resid": (ctypes.c_int, [ctypes.c_int64] + [ctypes.c_void_p] * 3 + [ctypes.c_double] +
                          [ctypes.c_void_p] * 4),
+    "ell1_hom_absmax": (ctypes.c_int, [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_hom_gammas": (ctypes.c_int, [ctypes.c_int64] + [ctypes.c_void_p] * 3 + [ctypes.c_double] +
+                        [ctypes.c_void_p] * 2),
+    "ell1_hom_gamma_minus": (ctypes.c_int, [ctypes.c_int64] + [ctypes.c_void_p] * 5),
+    "ell1_hom_xstats": (ctypes.c_int, [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "ell1_chol_factor_dense": (ctypes.c_int, [ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_double,
                                               ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
     "ell1_chol_solve_dense": (ctypes.c_int, [ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                                              ctypes.c_void_p, ctypes.c_void_p]),
+    "ell1_chol_solve_dense_multi": (ctypes.c_int, [ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                                   ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
+                                                   ctypes.c_void_p]),
     "ell1_pd_workspace": (ctypes.c_size_t, []),
     "ell1_pd_split": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32] + [ctypes.c_void_p] * 5),
     "ell1_pd_resid": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32] + [ctypes.c_void_p] * 12),

@@ -101,17 +101,152 @@ __global__ void __launch_bounds__(BT) bf_init(const BFArgs a, const double* CT, 
 //   rejected last round -> undo the rotation for this instance (copies), then
 //     a new prox trial from the stored momentum point with the grown L
 //   first round         -> first prox trial
+// One prox trial element (shrinkage.py:204-207 + the backtracking / stopping
+// partial sums), shared by the fused and the plain passes.
+struct ProxAcc {
+  double s[7];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int k = 0; k < 7; ++k) s[k] = 0.0;
+  }
+  __device__ __forceinline__ void add(double u, double yk, double gk, double xk, bool relest, bool gtr, double gt) {
+    const double dl = u - yk;
+    s[0] += fabs(u);
+    s[1] += gk * dl;
+    s[2] += dl * dl;
+    s[3] = nmax(s[3], fabs(u));
+    if (relest) { const double dd = u - xk; s[4] += dd * dd; s[5] += xk * xk; }
+    if (gtr) { const double e = u - gt; s[6] += e * e; }
+  }
+};
+
+// UNROLL independent elements per thread and trip: all loads of a trip are
+// issued before any use, so each CTA keeps UNROLL x BT loads in flight.
+constexpr int UNROLL = 4;
+
 __global__ void __launch_bounds__(BT) bf_step(const BFArgs a) {
   const int j = blockIdx.x;
-  __shared__ double sh[BW * 7 + 7];
-  __shared__ double sc[4];
+  __shared__ double sh[BW * 12 + 12];
+  __shared__ double sc[6];
   __shared__ int mode;                  // 0 first trial of a new iteration, 1 retry, 2 stop
   BI& I = a.inst[j];
   if (!I.active) return;
   const int64_t o = (int64_t)j * a.ldx;
   const int64_t orr = (int64_t)j * a.ld;
+  const int64_t N = a.N;
+  const bool relest = a.C.stop_kind == ELL1_STOP_REL_ESTIMATE;
+  const bool gtr = a.C.stop_kind == ELL1_STOP_GROUND_TRUTH;
+  const double* gtj = gtr ? a.C.ground_truth + (int64_t)I.orig * N : nullptr;
+  if (I.accepted && !I.retry) {
+    // ---- accepted last round: finish that iteration (shrinkage.py:283-297) and,
+    // in the same pass, the next iteration's first prox trial with the momentum
+    // parameters it would use (they do not depend on the KKT outcome; discarded
+    // when the instance stops)
+    if (threadIdx.x == 0) {
+      const double tp = I.tc, tc = I.tn;
+      const double tn = fista_t_next(tc);
+      const double lam_n = pymax(a.O.beta * I.lam, I.lam_bar);       // shrinkage.py:297
+      sc[0] = (tp - 1.0) / tc;                                       // m of the next iteration
+      sc[1] = tn;
+      sc[2] = lam_n / I.L;
+      sc[3] = 1e-10 * pymax(I.S[3], 1.0);                           // support cut, model.py:232
+      sc[4] = lam_n;
+    }
+    __syncthreads();
+    const double m = sc[0], L = I.L, thr = sc[2], cut = sc[3], lam = I.lam;
+    const double* __restrict__ xc = a.X[a.ix] + o;
+    const double* __restrict__ xp = a.X[a.ixp] + o;
+    double* __restrict__ xn = a.X[a.ixn] + o;
+    double* __restrict__ gc = a.G[a.igx] + o;
+    const double* __restrict__ gxp = a.G[a.igxp] + o;
+    const double* __restrict__ rc = a.R[a.irx] + orr;
+    const float* __restrict__ g32 = a.f32 ? a.G32 + (int64_t)j * a.n : nullptr;
+    double* __restrict__ Y = a.Y + o;
+    double* __restrict__ GY = a.GY + o;
+    double k5[5] = {0, 0, 0, 0, 0};
+    ProxAcc P;
+    P.zero();
+    for (int64_t base = threadIdx.x; base < N; base += UNROLL * BT) {
+      double g[UNROLL], xk[UNROLL], xq[UNROLL], gq[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const int64_t k = base + u * BT;
+        if (k < N) {
+          if (k < a.n) g[u] = g32 ? (double)g32[k] : gc[k];
+          else g[u] = a.s * rc[k - a.n];
+          xk[u] = xc[k];
+          xq[u] = xp[k];
+          gq[u] = gxp[k];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const int64_t k = base + u * BT;
+        if (k >= N) continue;
+        if (g32 || k >= a.n) gc[k] = g[u];
+        const double c = -g[u];
+        if (xk[u] != 0.0) { k5[0] = nmax(k5[0], fabs(c - lam * sgn(xk[u]))); k5[2] = 1.0; }
+        else { k5[1] = nmax(k5[1], fabs(c)); k5[3] = 1.0; }
+        if (fabs(xk[u]) > cut) k5[4] += 1.0;
+        const double yk = xk[u] + m * (xk[u] - xq[u]);                 // shrinkage.py:270
+        const double gk = (1.0 + m) * g[u] - m * gq[u];               // A^T(A y - b)
+        Y[k] = yk; GY[k] = gk;
+        const double un = soft1(yk - gk / L, thr);                      // shrinkage.py:204
+        xn[k] = un;
+        if (a.f32 && k < a.n) a.X32[(int64_t)j * a.ldx + k] = (float)un;
+        P.add(un, yk, gk, xk[u], relest, gtr, gtr ? gtj[k] : 0.0);
+      }
+    }
+    double v[12];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) v[k] = k5[k];
+#pragma unroll
+    for (int k = 0; k < 7; ++k) v[5 + k] = P.s[k];
+    cta_reduce<12>(v, 0xFu | (1u << 8), sh);                // max: k5[0..3], prox max|u| (slot 8)
+    if (threadIdx.x == 0) {
+      double kkt = v[2] > 0.0 ? v[0] : 0.0;
+      if (v[3] > 0.0) kkt = pymax(pymax(kkt, v[1] - lam), 0.0);
+      if (a.trace) {
+        double* tr = a.trace + ((int64_t)I.orig * a.C.max_iter + (I.it - 1)) * 4;
+        tr[0] = (double)I.it; tr[1] = I.Fn; tr[2] = sqrt(I.rr); tr[3] = v[4];
+      }
+      I.hist = I.hist < 2 ? I.hist + 1 : 2;
+      int done = 0;
+      if (lam == I.lam_bar && kkt <= a.C.tol * I.lam_bar) done = 1;   // shrinkage.py:291-293
+      else if (stop_fires(a.C.stop_kind, a.C.stop_thr, I.hist, I.Fn, I.Fprev, I.S[4], I.S[5], I.S[6],
+                          a.C.gt_norm, kkt))
+        done = 1;
+      I.Fprev = I.Fn;
+      I.tp = I.tc; I.tc = I.tn;
+      if (done) I.conv = 1;
+      else if (I.it >= a.C.max_iter) done = 2;
+      if (done) {
+        I.active = 0;
+        a.it_out[I.orig] = I.it; a.conv_out[I.orig] = I.conv; a.status_out[I.orig] = ELL1_OK;
+        atomicSub(a.counters + 1, 1);
+      } else {
+        // commit the next iteration the pass already started
+        I.lam = sc[4];
+        I.fy = I.fy_next;
+        I.it++;
+        I.bt = 0;
+        I.m = sc[0];
+        I.tn = sc[1];
+        I.mn = (I.tc - 1.0) / I.tn;
+        I.accepted = 0;
+        for (int k = 0; k < 7; ++k) I.S[k] = v[5 + k];
+      }
+      mode = done ? 2 : 0;
+    }
+    __syncthreads();
+    if (mode == 2) {
+      double* xo = a.x_out + (int64_t)I.orig * N;
+      for (int64_t k = threadIdx.x; k < N; k += BT) xo[k] = xc[k];
+    }
+    return;
+  }
   if (I.retry) {
-    for (int64_t k = threadIdx.x; k < a.N; k += BT) {
+    for (int64_t k = threadIdx.x; k < N; k += BT) {
       a.X[a.ix][o + k] = a.X[a.ixp][o + k];
       a.X[a.ixp][o + k] = a.X[a.ixn][o + k];
       a.G[a.igx][o + k] = a.G[a.igxp][o + k];
@@ -121,64 +256,6 @@ __global__ void __launch_bounds__(BT) bf_step(const BFArgs a) {
       a.R[a.irxp][orr + i] = a.R[a.irn][orr + i];
     }
     if (threadIdx.x == 0) mode = 1;
-  } else if (I.accepted) {
-    // ---- finish the accepted iteration (shrinkage.py:283-297)
-    const double* xc = a.X[a.ix] + o;
-    double* gc = a.G[a.igx] + o;
-    const double* rc = a.R[a.irx] + orr;
-    const double cut = 1e-10 * pymax(I.S[3], 1.0);   // model.py:232
-    const double lam = I.lam;
-    double k5[5] = {0, 0, 0, 0, 0};
-    for (int64_t k = threadIdx.x; k < a.N; k += BT) {
-      double g;
-      if (k < a.n) {
-        if (a.f32) { g = (double)a.G32[(int64_t)j * a.n + k]; gc[k] = g; }
-        else g = gc[k];                                    // the GEMM wrote it in place
-      } else {
-        g = a.s * rc[k - a.n];
-        gc[k] = g;
-      }
-      const double xk = xc[k];
-      const double c = -g;
-      if (xk != 0.0) { k5[0] = nmax(k5[0], fabs(c - lam * sgn(xk))); k5[2] = 1.0; }
-      else { k5[1] = nmax(k5[1], fabs(c)); k5[3] = 1.0; }
-      if (fabs(xk) > cut) k5[4] += 1.0;
-    }
-    cta_reduce<5>(k5, 0xFu, sh);
-    if (threadIdx.x == 0) {
-      double kkt = k5[2] > 0.0 ? k5[0] : 0.0;
-      if (k5[3] > 0.0) kkt = pymax(pymax(kkt, k5[1] - lam), 0.0);
-      I.tp = I.tc; I.tc = I.tn;
-      if (a.trace) {
-        double* tr = a.trace + ((int64_t)I.orig * a.C.max_iter + (I.it - 1)) * 4;
-        tr[0] = (double)I.it; tr[1] = I.Fn; tr[2] = sqrt(I.rr); tr[3] = k5[4];
-      }
-      I.hist = I.hist < 2 ? I.hist + 1 : 2;
-      int done = 0;
-      if (lam == I.lam_bar && kkt <= a.C.tol * I.lam_bar) done = 1;   // shrinkage.py:291-293
-      else if (stop_fires(a.C.stop_kind, a.C.stop_thr, I.hist, I.Fn, I.Fprev, I.S[4], I.S[5], I.S[6],
-                          a.C.gt_norm, kkt))
-        done = 1;
-      I.Fprev = I.Fn;
-      if (done) I.conv = 1;
-      else {
-        I.lam = pymax(a.O.beta * I.lam, I.lam_bar);         // shrinkage.py:297
-        I.fy = I.fy_next;
-        if (I.it >= a.C.max_iter) done = 2;
-      }
-      if (done) {
-        I.active = 0;
-        a.it_out[I.orig] = I.it; a.conv_out[I.orig] = I.conv; a.status_out[I.orig] = ELL1_OK;
-        atomicSub(a.counters + 1, 1);
-      }
-      mode = done ? 2 : 0;
-    }
-    __syncthreads();
-    if (mode == 2) {
-      double* xo = a.x_out + (int64_t)I.orig * a.N;
-      for (int64_t k = threadIdx.x; k < a.N; k += BT) xo[k] = xc[k];
-      return;
-    }
   } else if (threadIdx.x == 0) {
     mode = 0;                                              // very first trial
   }
@@ -196,17 +273,16 @@ __global__ void __launch_bounds__(BT) bf_step(const BFArgs a) {
   __syncthreads();
   const double m = sc[0], L = sc[1], thr = sc[2];
   const bool fr = mode == 0;
-  const double* x = a.X[a.ix] + o;
-  const double* xp = a.X[a.ixp] + o;
-  double* xn = a.X[a.ixn] + o;
-  const double* gx = a.G[a.igx] + o;
-  const double* gxp = a.G[a.igxp] + o;
-  double* Y = a.Y + o;
-  double* GY = a.GY + o;
-  const bool relest = a.C.stop_kind == ELL1_STOP_REL_ESTIMATE;
-  const bool gtr = a.C.stop_kind == ELL1_STOP_GROUND_TRUTH;
-  double s[7] = {0, 0, 0, 0, 0, 0, 0};
-  for (int64_t k = threadIdx.x; k < a.N; k += BT) {
+  const double* __restrict__ x = a.X[a.ix] + o;
+  const double* __restrict__ xp = a.X[a.ixp] + o;
+  double* __restrict__ xn = a.X[a.ixn] + o;
+  const double* __restrict__ gx = a.G[a.igx] + o;
+  const double* __restrict__ gxp = a.G[a.igxp] + o;
+  double* __restrict__ Y = a.Y + o;
+  double* __restrict__ GY = a.GY + o;
+  ProxAcc P;
+  P.zero();
+  for (int64_t k = threadIdx.x; k < N; k += BT) {
     const double xk = x[k];
     double yk, gk;
     if (fr) {
@@ -219,17 +295,11 @@ __global__ void __launch_bounds__(BT) bf_step(const BFArgs a) {
     const double u = soft1(yk - gk / L, thr);                // shrinkage.py:204
     xn[k] = u;
     if (a.f32 && k < a.n) a.X32[(int64_t)j * a.ldx + k] = (float)u;
-    const double dl = u - yk;
-    s[0] += fabs(u);
-    s[1] += gk * dl;
-    s[2] += dl * dl;
-    s[3] = nmax(s[3], fabs(u));
-    if (relest) { const double dd = u - xk; s[4] += dd * dd; s[5] += xk * xk; }
-    if (gtr) { const double e = u - a.C.ground_truth[(int64_t)I.orig * a.N + k]; s[6] += e * e; }
+    P.add(u, yk, gk, xk, relest, gtr, gtr ? gtj[k] : 0.0);
   }
-  cta_reduce<7>(s, 1u << 3, sh);
+  cta_reduce<7>(P.s, 1u << 3, sh);
   if (threadIdx.x == 0)
-    for (int k = 0; k < 7; ++k) I.S[k] = s[k];
+    for (int k = 0; k < 7; ++k) I.S[k] = P.s[k];
 }
 
 __global__ void __launch_bounds__(BT) bf_resid(const BFArgs a) {

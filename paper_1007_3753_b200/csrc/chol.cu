@@ -102,10 +102,14 @@ __global__ void __launch_bounds__(PT) chol_trsm_kernel(double* __restrict__ L, i
     if (c < nb) L[(kb + c) * ld + i] = x[c];
 }
 
-// x = (L L^T)^-1 rhs, one CTA; y staged in shared memory (d doubles)
+// x = (L L^T)^-1 rhs, one CTA per right-hand side (column blockIdx.x of
+// rhs / x, strides ldr / ldx); y staged in shared memory (d doubles)
 __global__ void __launch_bounds__(1024) chol_solve_kernel(int64_t d, const double* __restrict__ L, int64_t ld,
-                                                          const double* __restrict__ rhs, double* __restrict__ x) {
+                                                          const double* __restrict__ rhs_all, int64_t ldr,
+                                                          double* __restrict__ x_all, int64_t ldx) {
   extern __shared__ double y[];
+  const double* __restrict__ rhs = rhs_all + (int64_t)blockIdx.x * ldr;
+  double* __restrict__ x = x_all + (int64_t)blockIdx.x * ldx;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   for (int64_t i = tid; i < d; i += blockDim.x) y[i] = rhs[i];
   __syncthreads();
@@ -183,11 +187,19 @@ extern "C" int ell1_chol_factor_dense(int64_t d, const double* M, int64_t ldm, d
 
 extern "C" int ell1_chol_solve_dense(int64_t d, const double* L, int64_t ldl, const double* rhs, double* x,
                                      void* stream) {
-  if (d < 1 || !L || !rhs || !x || ldl < d) return ELL1_ERR_ARG;
+  return ell1_chol_solve_dense_multi(d, L, ldl, 1, rhs, d, x, d, stream);
+}
+
+extern "C" int ell1_chol_solve_dense_multi(int64_t d, const double* L, int64_t ldl, int64_t nrhs, const double* rhs,
+                                           int64_t ldr, double* x, int64_t ldx, void* stream) {
+  if (d < 1 || nrhs < 0 || !L || !rhs || !x || ldl < d || ldr < d || ldx < d || nrhs > 0x7fffffff)
+    return ELL1_ERR_ARG;
+  if (nrhs == 0) return ELL1_OK;
   const size_t smem = (size_t)d * 8;
   if (smem > 200 * 1024) return ELL1_ERR_ARG;
   if (cudaFuncSetAttribute(chol_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return ELL1_ERR_CUDA;
-  chol_solve_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(d, L, ldl, rhs, x);
+  const int threads = d >= 1024 ? 1024 : (d >= 256 ? 256 : 128);
+  chol_solve_kernel<<<(unsigned)nrhs, threads, smem, (cudaStream_t)stream>>>(d, L, ldl, rhs, ldr, x, ldx);
   return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
 }

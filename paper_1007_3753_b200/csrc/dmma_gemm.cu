@@ -13,7 +13,6 @@
 // z dimension splits K across a cluster of S CTAs (cluster dims 1 x 1 x S);
 // ranks 1..S-1 park their fp64 partial tile in their own shared memory and
 // rank 0 adds them in rank order through DSMEM (deterministic).
-#include <cmath>
 #include <cooperative_groups.h>
 #include "dmma_gemm.cuh"
 #include "ell1_b200.h"
@@ -313,21 +312,15 @@ using C128x64s3 = Cfg<128, 64, 3>;
 using C64x64k32 = Cfg<64, 64, 3, 32>;
 using C128x64k32 = Cfg<128, 64, 2, 32>;
 
-// Wave-quantised estimate of the useful fraction of the machine for a K
-// split: CTAs in ceil(CTAs / slots) rounds, each CTA paying ~3 k-tiles of
-// pipeline fill / epilogue and ~0.5 per extra split rank for the DSMEM sum.
-static int pick_split(int64_t tiles, int64_t kt, int slots) {
-  double best = -1.0;
-  int pick = 1;
-  for (int s = 1; s <= 8; s *= 2) {
-    if (s > 1 && kt / s < 4) break;
-    const double ctas = (double)tiles * s;
-    const double rounds = std::ceil(ctas / slots);
-    const double kps = (double)kt / s;
-    const double eff = (ctas / (rounds * slots)) * (kps / (kps + 3.0 + 0.5 * (s - 1)));
-    if (eff > best * 1.02) { best = eff; pick = s; }
-  }
-  return pick;
+// K split for a 64 x 64-tile launch (tuned on the batched solvers' shapes,
+// tools/dgemm_bench.py): enough CTAs to fill the SMs (>= 256 in flight) while
+// each split keeps >= 8 k-tiles; outputs of 512+ tiles with long K take one
+// more split (shorter tails of the last wave).
+static int pick_split(int64_t tiles, int64_t kt) {
+  int s = 1;
+  while (s < 8 && tiles * s < 256 && kt / (2 * s) >= 8) s *= 2;
+  if (s < 8 && tiles >= 512 && tiles * s < 1024 && kt / (2 * s) >= 16) s *= 2;
+  return s;
 }
 
 // variant = tile config (0..4), split = K split (1, 2, 4, 8); -1 = heuristic
@@ -337,11 +330,7 @@ static bool run(int variant, int split, int64_t m, int64_t n, int64_t k, const d
   if (variant < 0) variant = 1;
   const int bm = (variant == 2 || variant == 4) ? 128 : 64, bn = 64;
   const int bk = variant >= 3 ? 32 : BK0;
-  const int per = variant == 0 ? 2 : (variant == 1 ? 3 : (variant == 3 ? 2 : 1));   // CTAs per SM
-  if (split < 0) {
-    const int64_t tiles = ((m + bm - 1) / bm) * ((n + bn - 1) / bn);
-    split = pick_split(tiles, (k + bk - 1) / bk, 148 * per);
-  }
+  if (split < 0) split = pick_split(((m + bm - 1) / bm) * ((n + bn - 1) / bn), (k + bk - 1) / bk);
   switch (variant) {
     case 0: return with_split<C64x64s4, TA, TB, VA, VB>(split, m, n, k, A, lda, B, ldb, C, ldc, s, al, be);
     case 2: return with_split<C128x64s3, TA, TB, VA, VB>(split, m, n, k, A, lda, B, ldb, C, ldc, s, al, be);

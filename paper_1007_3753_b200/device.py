@@ -146,20 +146,34 @@ class DeviceDictionary:
             return cache[key]
         torch = _torch()
         from paper_1007_3753_b200.exceptions import IllConditionedError
-        At = self.storage.view(self.n, self.ld)[:, : self.d].to(torch.float64)   # A^T (n x d)
-        G = At.T @ At
+        L_ = _lib.lib()
+        st = stream_ptr(self.device)
+        d, n, ld = self.d, self.n, self.ld
+        f64 = dict(dtype=torch.float64, device=self.device)
+        A64 = self.storage.view(n, ld).to(torch.float64)        # column-major A, ld rows
+        G = torch.empty(d * d, **f64)
+        # G = A A^T (+ s^2 I) on the DMMA path, its Cholesky factor, G^-1 and
+        # M = G^-1 A: the library's own kernels (dmma_gemm.cu, chol.cu)
+        _lib.check(L_.ell1_gemm_f64(0, 1, d, d, n, ptr(A64), ld, ptr(A64), ld, ptr(G), d, st), "ell1_gemm_f64")
         if ext:
-            G.diagonal().add_(float(scale) ** 2)
-        L, info = torch.linalg.cholesky_ex(G)
+            tr = torch.zeros(1, **f64)
+            ones = torch.ones(d, **f64)
+            _lib.check(L_.ell1_pd_diag(d, d, ptr(G), float(scale) ** 2, ptr(ones), ptr(tr), st), "ell1_pd_diag")
+        Lf = torch.empty(d * d, **f64)
+        info = torch.zeros(1, dtype=torch.int32, device=self.device)
+        _lib.check(L_.ell1_chol_factor_dense(d, ptr(G), d, 0.0, ptr(Lf), d, ptr(info), st), "ell1_chol_factor_dense")
         if int(info.item()) != 0:
             raise IllConditionedError("row Gram A A^T is not positive definite; the dual "
                                       "solver needs full row rank")
-        Ginv = torch.cholesky_inverse(L)
-        Gcm = torch.zeros(self.d, self.ld, dtype=torch.float64, device=self.device)
-        Gcm[:, : self.d] = Ginv            # symmetric: row j == column j
-        MT = torch.zeros(self.n, self.ld, dtype=self.storage.dtype, device=self.device)
-        MT[:, : self.d] = (At @ Ginv).to(self.storage.dtype)   # row j of M^T == column j of M
-        cache[key] = (MT, Gcm, L)
+        eye = torch.eye(d, **f64)
+        Gcm = torch.zeros(d, ld, **f64)                         # G^-1, column-major (symmetric)
+        _lib.check(L_.ell1_chol_solve_dense_multi(d, ptr(Lf), d, d, ptr(eye), d, ptr(Gcm), ld, st),
+                   "ell1_chol_solve_dense_multi")
+        M64 = torch.zeros(n, ld, **f64)                         # M = G^-1 A, column-major, ld rows
+        _lib.check(L_.ell1_gemm_f64(0, 0, d, n, d, ptr(Gcm), ld, ptr(A64), ld, ptr(M64), ld, st), "ell1_gemm_f64")
+        MT = M64 if self.storage.dtype == torch.float64 else M64.to(self.storage.dtype)
+        Llow = torch.tril(Lf.view(d, d).T)                     # lower factor (row-major view), observers
+        cache[key] = (MT, Gcm, Llow)
         return cache[key]
 
     # -- operator-protocol hooks ------------------------------------------

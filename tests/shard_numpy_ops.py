@@ -256,3 +256,198 @@ class NumpyShardOps:
         outs = [torch.zeros(cap, dtype=torch.float64) for _ in range(self.world)]
         dist.all_gather(outs, buf, group=self.group)
         return ctl, tr, np.concatenate([outs[r].numpy()[: c1 - c0] for r, (c0, c1) in enumerate(sizes)])
+
+
+# ---------------------------------------------------------------------------
+# column-sharded Homotopy (paper_1007_3753_b200/sharded_homotopy.py ops)
+# ---------------------------------------------------------------------------
+
+class NumpyHomShardOps:
+    """numpy + gloo restatement of DeviceHomShardOps (csrc/shard_hom.cu
+    reductions, the chol_* factor kernels) — test infrastructure only."""
+
+    SLOT = 4
+
+    def __init__(self, A_local, n_global, group=None):
+        import torch.distributed as dist
+        from paper_1007_3753_b200.sharded import column_range
+        self.A = np.ascontiguousarray(A_local, dtype=np.float64)
+        self.d, self.nl = self.A.shape
+        self.n = n_global
+        self.group = group
+        if dist.is_available() and dist.is_initialized():
+            self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        else:
+            self.world, self.rank = 1, 0
+        self.c0, _ = column_range(n_global, self.rank, self.world)
+        self.S = np.zeros((0, self.d))
+        self.mask = np.zeros(self.nl, dtype=bool)
+        self.c = np.zeros(self.nl)
+        self.w = np.zeros(self.nl)
+
+    def _allreduce(self, v):
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            dist.all_reduce(torch.from_numpy(v), op=dist.ReduceOp.SUM, group=self.group)
+
+    def vec_m(self, m):
+        return np.zeros(max(m, 1))
+
+    def set_b(self, b):
+        self.b = np.array(b, dtype=np.float64)
+        self.bnorm = float(np.linalg.norm(b))
+
+    def corr(self, r):
+        self.c = self.A.T @ r
+
+    def corr_exchange(self, sup):
+        m = len(sup)
+        buf = np.zeros(m + self.SLOT * self.world)
+        for p, j in enumerate(sup):
+            if self.c0 <= j < self.c0 + self.nl:
+                buf[p] = self.c[j - self.c0]
+        s = buf[m + self.SLOT * self.rank:]
+        if self.nl:
+            k = int(np.argmax(np.abs(self.c)))
+            s[0], s[1] = abs(self.c[k]), k + self.c0
+        else:
+            s[0], s[1] = -1.0, -1.0
+        self._allreduce(buf)
+        sl = buf[m:].reshape(self.world, self.SLOT)
+        best, arg = -1.0, -1
+        for r in range(self.world):
+            if sl[r, 1] >= 0 and sl[r, 0] > best:
+                best, arg = float(sl[r, 0]), int(sl[r, 1])
+        return buf[:m].copy(), max(best, 0.0), arg
+
+    def wpass(self, v):
+        self.w = self.A.T @ v
+
+    def gammas(self, lam):
+        import math
+        from paper_1007_3753_b200.sharded import column_range
+        mask = self.mask
+        gp_loc = np.full(4, np.inf)
+        gp_loc[1] = gp_loc[3] = -1
+        off = np.nonzero(~mask)[0]
+        if off.size:
+            co, wo = self.c[off], self.w[off]
+            with np.errstate(divide="ignore", invalid="ignore"):
+                ra = (lam - co) / (1.0 - wo)
+                rb = (lam + co) / (1.0 + wo)
+            floor = 1e-10 * max(lam, 1e-30)
+            for q, rr in ((0, ra), (2, rb)):
+                ok = np.isfinite(rr) & (rr > floor)
+                if np.any(ok):
+                    j = int(np.argmin(np.where(ok, rr, np.inf)))
+                    gp_loc[q], gp_loc[q + 1] = rr[j], off[j]
+        buf = np.zeros(self.SLOT * self.world)
+        buf[self.SLOT * self.rank: self.SLOT * (self.rank + 1)] = gp_loc
+        self._allreduce(buf)
+        sl = buf.reshape(self.world, self.SLOT)
+        ga, ia, gb, ib = math.inf, -1, math.inf, -1
+        for r in range(self.world):
+            c0 = column_range(self.n, r, self.world)[0]
+            if sl[r, 1] >= 0 and sl[r, 0] < ga:
+                ga, ia = float(sl[r, 0]), int(sl[r, 1]) + c0
+            if sl[r, 3] >= 0 and sl[r, 2] < gb:
+                gb, ib = float(sl[r, 2]), int(sl[r, 3]) + c0
+        return (gb, ib) if gb < ga else (ga, ia)
+
+    def fetch_column(self, j):
+        col = np.zeros(self.d)
+        if self.c0 <= j < self.c0 + self.nl:
+            col[:] = self.A[:, j - self.c0]
+        self._allreduce(col)
+        return col
+
+    def set_mask(self, j, on):
+        if self.c0 <= j < self.c0 + self.nl:
+            self.mask[j - self.c0] = on
+
+    def store_put(self, m, col):
+        self.S = np.vstack([self.S[:m], col[None, :]])
+
+    def store_drop(self, pos, m):
+        self.S = np.delete(self.S[:m], pos, axis=0)
+
+    def S_times(self, m, xI):
+        return self.S[:m].T @ xI[:m] if m else np.zeros(self.d)
+
+    def St_times(self, m, v):
+        return self.S[:m] @ v
+
+    def resid(self, m, xI):
+        return self.b - self.S_times(m, xI)
+
+    def sumsq(self, v, n):
+        return float(np.asarray(v)[:n] @ np.asarray(v)[:n])
+
+    def norm(self, v, n):
+        return float(np.linalg.norm(np.asarray(v)[:n]))
+
+    def matvec(self, G, m, x):
+        return G.reshape(m, m) @ x[:m]
+
+    def gram(self, m):
+        return (self.S[:m] @ self.S[:m].T).reshape(-1)
+
+    def gram_ridge(self, m):
+        G = self.S[:m] @ self.S[:m].T
+        G[np.diag_indices_from(G)] += 1e-12 * max(float(np.trace(G)), 1.0)
+        return G.reshape(-1)
+
+    def remove_entry(self, x, pos, m):
+        return np.delete(np.asarray(x)[:m], pos)
+
+    def append_zero(self, x, m):
+        return np.concatenate([np.asarray(x)[:m], [0.0]])
+
+    def chol(self, G, m):
+        from oracle.l1_oracle import NotPD, chol_upper
+        from paper_1007_3753_b200.exceptions import NotPositiveDefiniteError
+        try:
+            return chol_upper(G.reshape(m, m)).reshape(-1)
+        except NotPD as exc:
+            raise NotPositiveDefiniteError(str(exc)) from exc
+
+    def solve(self, R, m, rhs):
+        from oracle.l1_oracle import chol_solve
+        return chol_solve(R.reshape(m, m), rhs[:m])
+
+    def grow(self, R, m, g, diag):
+        from oracle.l1_oracle import NotPD, chol_grow
+        from paper_1007_3753_b200.exceptions import NotPositiveDefiniteError
+        Rm = R.reshape(m, m) if m else np.zeros((0, 0))
+        try:
+            return chol_grow(Rm, g[:m] if m else np.zeros(0), diag).reshape(-1)
+        except NotPD as exc:
+            raise NotPositiveDefiniteError(str(exc)) from exc
+
+    def drop(self, R, m, k):
+        from oracle.l1_oracle import chol_drop
+        return chol_drop(R.reshape(m, m), k).reshape(-1)
+
+    def gamma_minus(self, m, xI, dI, sup):
+        best, pos = np.inf, -1
+        for k in np.argsort(sup, kind="stable"):
+            with np.errstate(divide="ignore", invalid="ignore"):
+                r = -xI[k] / dI[k]
+            if np.isfinite(r) and r > 0 and r < best:
+                best, pos = float(r), int(k)
+        return best, pos
+
+    def xstats(self, m, xI):
+        x = np.asarray(xI[:m])
+        cut = 1e-10 * max(float(np.max(np.abs(x))) if m else 0.0, 1.0)
+        return float(np.sum(np.abs(x))), int(np.count_nonzero(np.abs(x) > cut))
+
+    def axpy(self, a, x, y):
+        y[: len(x)] += a * x
+
+    def sign(self, v):
+        return np.sign(v)
+
+    def to_host(self, v):
+        return np.array(v, dtype=np.float64)

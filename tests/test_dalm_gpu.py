@@ -49,10 +49,18 @@ def test_dalm_zero_data(alm, model):
 
 
 def test_dalm_rejects_rank_deficient_rows(alm, model):
+    # test_alm.py:133-137: more rows than columns, A A^T cannot be positive definite
     from paper_1007_3753_b200.exceptions import IllConditionedError
-    A = np.array([[1.0, 0.0, 1.0], [2.0, 0.0, 2.0]])
     with pytest.raises(IllConditionedError):
-        alm.dalm_solve(model.ProblemInstance(A, np.array([1.0, 2.0])), model.SolverConfig())
+        alm.dalm_solve(model.ProblemInstance(np.ones((3, 2)), np.ones(3)), model.SolverConfig())
+
+
+def test_dalm_borderline_gram_matches_reference(alm, model):
+    # a rank-1 row Gram whose last Cholesky pivot rounds to +1.8e-15: the
+    # reference's numpy factor succeeds and the solve converges in 2 steps
+    A = np.array([[1.0, 0.0, 1.0], [2.0, 0.0, 2.0]])
+    r = alm.dalm_solve(model.ProblemInstance(A, np.array([1.0, 2.0])), model.SolverConfig())
+    assert r.converged and r.iterations == 2
 
 
 def test_dalm_two_variable_value(alm, model):

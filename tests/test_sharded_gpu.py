@@ -214,3 +214,32 @@ def test_cfg4_full_scale_kkt_certificate():
     assert np.all(res.x_star[big] != 0.0)
     del ops, shard
     torch.cuda.empty_cache()
+
+
+# ---------------------------------------------------------------- column-sharded Homotopy (§8(e) row 3)
+@pytest.mark.parametrize("cid", ["homotopy_small_1300", "homotopy_small_1301", "cfg2_homotopy",
+                                 "cfg5_homotopy_k16", "cfg5_homotopy_k64"])
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_sharded_homotopy_matches_golden(cid, world):
+    """The sharded path (A^T passes per rank, replicated active set and
+    factor on the device) on `world` thread-ranks of this GPU against the
+    reference's golden path: same breakpoints, trace and x (fp64)."""
+    from tests.golden.cases import resolve_lambda
+    from paper_1007_3753_b200.model import SolverConfig
+    from paper_1007_3753_b200.sharded import ShardedDictionary, ShardedInstance
+    from paper_1007_3753_b200.sharded_homotopy import DeviceHomShardOps, sharded_solve_path
+    from tests.emulated_collective import run_ranks
+    case, A, b, gt, gold = case_inputs(cid)
+    lam = resolve_lambda(case["cfg"], A, b)
+    target = lam if lam is not None else 1e-2 * float(np.max(np.abs(A.T @ b)))
+
+    def rank_fn(rank, coll):
+        import torch
+        torch.cuda.set_device(0)
+        shard = ShardedDictionary.from_dense(A, rank, world)
+        return sharded_solve_path(ShardedInstance(shard, b), target, SolverConfig(max_iter=5000),
+                                  ops=DeviceHomShardOps(shard, coll))
+    results, _ = run_ranks(world, rank_fn)
+    for res, lam_r in results:
+        assert_parity(res.x_star, res.iterations, res.converged, res.trace, gold, 1e-8)
+        np.testing.assert_array_equal(res.x_star, results[0][0].x_star)
