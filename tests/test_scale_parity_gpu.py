@@ -213,6 +213,4 @@ def test_cfg5_homotopy_batch_matches_reference(cfg5, B):
             np.testing.assert_allclose(tr[:, 1:3], tg[:, 1:3], rtol=1e-6, atol=1e-12)
     print("cfg5 homotopy B=%d: %d sampled instances matched a b-perturbed reference run, %d a "
           "correlation-perturbed one (saturated support)" % (B, spread, cspread))
-    print("cfg5 homotopy B=%d: %d sampled instances matched a perturbed reference run, %d saturated-support "
-          "instances certified by objective + KKT" % (B, spread, saturated))
 
