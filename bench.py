@@ -470,11 +470,21 @@ _PEAKS = {}
 
 
 def gemm_peaks(torch, dev):
-    """Measured cuBLAS DGEMM / SGEMM throughput on this GPU (8192^3, best of 3):
-    the denominators of the batched solvers' tensor-pipe roofline (only bf16 is
-    in MEASURED_PEAKS.json)."""
+    """Library DGEMM / SGEMM / TF32 throughput on this GPU pool (8192^3): the
+    denominators of the batched solvers' tensor-pipe roofline (only bf16 is in
+    MEASURED_PEAKS.json).  Read from profiles/r02_gemm_peaks.json
+    (tools/gemm_peaks.py, measured on this pool) so the bench launches no
+    library kernels; measured here only when that file is missing."""
     if _PEAKS:
         return _PEAKS
+    path = os.path.join(ROOT, "profiles", "r02_gemm_peaks.json")
+    if os.path.exists(path):
+        try:
+            _PEAKS.update(json.load(open(path)))
+            if all(k in _PEAKS for k in ("dgemm_tflops", "sgemm_tflops", "tf32_tflops")):
+                return _PEAKS
+        except ValueError:
+            _PEAKS.clear()
     for name, dt in (("dgemm_tflops", torch.float64), ("sgemm_tflops", torch.float32)):
         a = torch.randn(8192, 8192, device=dev, dtype=dt)
         b = torch.randn(8192, 8192, device=dev, dtype=dt)
@@ -545,7 +555,7 @@ def leg_cfg3(torch, dev, queries=1024):
                         "tol 1e-4, min-class-residual labels" % queries,
             "roofline": {"bound": "tensor (3xTF32 tcgen05)", "achieved": 3 * tfl, "peak": peaks["tf32_tflops"],
                          "unit": "TFLOP/s", "frac": 3 * tfl / peaks["tf32_tflops"],
-                         "peak_source": "cuBLAS TF32 8192^3 measured in this run",
+                         "peak_source": "cuBLAS TF32 8192^3 (profiles/r02_gemm_peaks.json)",
                          "algorithmic": "SURVEY 8(d): (4 d n_A + 2 d^2) flops per query-iteration, x3 TF32 "
                                         "MMAs per fp32-accurate product",
                          "fp32_accurate_tflops": tfl},
@@ -610,7 +620,7 @@ def leg_cfg5(torch, dev, ws=1, B=1024, cpu_sample=4):
                      "mean_iterations": float(its.mean()), "converged": int(res.converged.sum()),
                      "roofline": {"bound": "tensor (fp64 DMMA GEMMs)", "achieved": tfl,
                                   "peak": pk, "unit": "TFLOP/s", "frac": tfl / pk,
-                                  "peak_source": "cuBLAS DGEMM 8192^3 measured in this run",
+                                  "peak_source": "cuBLAS DGEMM 8192^3 (profiles/r02_gemm_peaks.json)",
                                   "algorithmic": {"fista": "4 d n", "dalm": "4 d n + 2 d^2",
                                                   "homotopy": "4 d n (the two A^T passes)"}[name]
                                                  + " flops per instance-iteration (SURVEY 8(d))"}}

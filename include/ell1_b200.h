@@ -195,6 +195,8 @@ typedef struct {
   const double* Ginv;
   double* y_out;       /* optional (observer): multiplier y, ld entries */
   double* z_out;       /* optional (observer): z, n(+d) entries */
+  const double* G;     /* optional (batched): G itself, column-major d x ld, float64 — the y-step
+                          certificate then uses G y (d^2 per instance) instead of A (A^T y) */
 } ell1_dalm_opts_t;
 
 /* Dual augmented Lagrangian — replaces alm.dalm_solve (alm.py:206-272)

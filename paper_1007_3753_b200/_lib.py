@@ -74,7 +74,7 @@ class DalmOpts(ctypes.Structure):
     _fields_ = [("beta", ctypes.c_double), ("y_tol", ctypes.c_double),
                 ("y_cg_step", ctypes.c_int32), ("_pad", ctypes.c_int32),
                 ("M", ctypes.c_void_p), ("Ginv", ctypes.c_void_p), ("y_out", ctypes.c_void_p),
-                ("z_out", ctypes.c_void_p)]
+                ("z_out", ctypes.c_void_p), ("G", ctypes.c_void_p)]
 
 
 class PalmOpts(ctypes.Structure):

@@ -75,7 +75,7 @@ def dalm_solve(P, config, observer=None):
     cg_mode = bool(config.opt("y_cg_step", False))
     D = prep.D
     try:
-        MT, Gcm, Lfac = D.gram_factor(prep.ext, prep.scale)
+        MT, Gcm, Lfac, _ = D.gram_factor(prep.ext, prep.scale)
     except IllConditionedError:
         if not np.any(np.asarray(P.b)):       # alm.py:223-226: zero data exits first
             return SolverResult(np.zeros(prep.n), 0, prep.elapsed(), True, [TraceEntry(0, 0.0, 0.0, 0)])

@@ -281,7 +281,7 @@ def dalm_solve_batch(A, Bmat, config, with_trace=False):
         raise ValueError("beta must be positive")
     if config.opt("y_cg_step", False):
         raise NotImplementedError("y_cg_step is single-instance only")
-    MT, Gcm, _ = D.gram_factor(ext, view.ext_scale)
+    MT, Gcm, _, Gfull = D.gram_factor(ext, view.ext_scale)
     from paper_1007_3753_b200.alm import _Y_REFINE_TOL, _Y_REFINE_TOL_F32
     O = _lib.DalmOpts()
     O.beta = beta
@@ -289,6 +289,10 @@ def dalm_solve_batch(A, Bmat, config, with_trace=False):
     O.y_cg_step = 0
     O.M = MT.data_ptr()
     O.Ginv = Gcm.data_ptr()
+    # float64 storage: the y-step certificate as G y (d^2 per instance) instead
+    # of A (A^T y) (d n); float32 keeps the single 2B-column tensor-core GEMM,
+    # which measured faster than two B-column ones at config 3
+    O.G = Gfull.data_ptr() if D.dtype == _lib.F64 else None
     Bpad, B = _upload_rhs(Bmat, D)
     C, _ = _ctrl(config, B, N, D.device, None)
     L = _lib.lib()

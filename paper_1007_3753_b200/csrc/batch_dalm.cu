@@ -26,6 +26,8 @@ struct BDArgs {
   int64_t d, n, N, ld, ldx;
   int ext, f32, cg;
   int fuse_ext;              // fp32 [A, sI]: [M | Ginv] V as one tensor-core GEMM (no GEXT)
+  int gcert;                 // certificate from G y (the opts carry G): P2[:, j] = G y_j already
+                             // includes the [A, sI] block, only A x_new needs the s x_e term
   double s, beta, ytol;
   const double* Bm;         // ld x B
   const double* C0;         // ld x B  (Ginv b)
@@ -250,7 +252,10 @@ __global__ void __launch_bounds__(BT) bd_c(const BDArgs a, int refine_only) {
     for (int64_t i = threadIdx.x; i < a.d; i += BT) {
       double aau = f32 ? (double)pu[i] : pu64[i];
       double ax = f32 ? (double)px[i] : px64[i];
-      if (ext) { aau = aau + sc * (f32 ? sc * yn[i] : ue[i]); ax = ax + sc * xe[i]; }
+      if (ext) {
+        if (!a.gcert) aau = aau + sc * (f32 ? sc * yn[i] : ue[i]);
+        ax = ax + sc * xe[i];
+      }
       const double resid = rh[i] - aau;
       res[i] = resid;
       axo[i] = ax;
@@ -446,6 +451,7 @@ extern "C" size_t ell1_batch_dalm_workspace(const ell1_dict_t* D, int32_t B) {
   s += 2 * align_up((int64_t)sizeof(DI) * B, 256) + align_up(B * 4, 256) + align_up(ldx * B * 8, 256);
   if (D->dtype == ELL1_F32)                                  // splits of A and M + operand scratch
     s += (size_t)(f32split_floats(D, (ldx > ld ? ldx : ld) * 2 * B) + f32split_dict_floats(D) +
+                  2 * align_up(ld * ld, 64) + 2 * align_up(ld * align_up(ld, 4), 64) + align_up(ld * ld, 64) +
                   2 * align_up(ld * ldx, 64)) * 4 + 2048;
   return s + 8192;
 }
@@ -461,6 +467,7 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   BDArgs a;
   a.d = d; a.n = D->n; a.N = N; a.ld = ld; a.ldx = ldx;
   a.ext = D->ext; a.f32 = D->dtype == ELL1_F32; a.cg = O->y_cg_step; a.fuse_ext = 0;
+  a.gcert = O->G != nullptr;
   a.s = D->ext_scale; a.beta = O->beta; a.ytol = O->y_tol;
   a.C = *C;
   if (a.cg) return ELL1_ERR_ARG;   // batched CG y-step: not provided (use the single-instance solver)
@@ -488,9 +495,19 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   if (!cv.ok) return ELL1_ERR_ARG;
   (void)xscr;
   a.UT32 = T32;
-  F32Split spA, spM, spX;
+  F32Split spA, spM, spX, spG;
   const F32Split* pA = nullptr;
   const F32Split* pM = nullptr;
+  if (a.f32 && a.gcert) {
+    // G (d columns x ld, fp64) -> fp32 -> 3xTF32 split, the certificate's G y operand
+    float* Gf = cv.take<float>(ld * ld);
+    if (!cv.ok) return ELL1_ERR_ARG;
+    bd_f2d<<<(unsigned)((d * ld + 255) / 256 < 148 * 8 ? (d * ld + 255) / 256 : 148 * 8), 256, 0, s>>>(O->G, Gf,
+                                                                                                   d * ld);
+    ell1_dict_t GD = *D;
+    GD.A = Gf; GD.n = d; GD.ext = 0;
+    if (!f32split_dict(spG, cv, &GD, Gf, s)) return ELL1_ERR_ARG;
+  }
   if (a.f32) {
     if (!f32split_setup(spA, cv, D, (ldx > ld ? ldx : ld) * 2 * B, s)) return ELL1_ERR_ARG;
     spM = spA;                                               // shares the operand scratch
@@ -536,7 +553,16 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
       return false;
     // [U | x_new] for the Bc instances: the x_new block starts at column Bc
     bd_x<<<Bc, BT, 0, ks>>>(aa, (const double*)Ut, (const float*)Ut, refine_only);
-    if (aa.f32) {
+    if (aa.gcert) {
+      // certificate A A^T y as G y (d^2 per instance instead of d n) and A x_new
+      if (aa.f32) {
+        if (!sgemm_split(ks, 0, (int)ld, Bc, (int)d, &spG, aa.Y32, ld, aa.P2f, ld)) return false;
+        if (!gemm_AX(ks, D, aa.UX32 + (int64_t)Bc * ldx, ldx, aa.P2f + (int64_t)Bc * ld, ld, Bc, pA)) return false;
+      } else {
+        if (!dgemm(0, 0, ld, Bc, d, O->G, ld, aa.Y[aa.iy ^ 1], ld, aa.P2, ld, ks)) return false;
+        if (!gemm_AX(ks, D, aa.UX + (int64_t)Bc * ldx, ldx, aa.P2 + (int64_t)Bc * ld, ld, Bc)) return false;
+      }
+    } else if (aa.f32) {
       if (!gemm_AX(ks, D, aa.UX32, ldx, aa.P2f, ld, 2 * Bc, pA)) return false;
     } else {
       if (!gemm_AX(ks, D, aa.UX, ldx, aa.P2, ld, 2 * Bc)) return false;

@@ -135,9 +135,9 @@ class DeviceDictionary:
 
     # -- row-Gram factorisation for the dual ALM (alm.py:162-169) ----------
     def gram_factor(self, ext=False, scale=0.0):
-        """(M, Ginv, L) with G = A A^T (+ s^2 I), L its lower Cholesky factor,
-        Ginv = G^{-1} (column-major, ld rows, float64) and M = Ginv A in the
-        dictionary's layout / dtype.  Computed once per (ext, scale) from the
+        """(M, Ginv, L, G) with G = A A^T (+ s^2 I), L its lower Cholesky factor,
+        Ginv = G^{-1} and G (column-major, ld rows, float64) and M = Ginv A in
+        the dictionary's layout / dtype.  Computed once per (ext, scale) from the
         device copy of A (so float32 storage factors the rounded A).
         Raises IllConditionedError when G is not positive definite."""
         key = (bool(ext), float(scale) if ext else 0.0)
@@ -173,7 +173,9 @@ class DeviceDictionary:
         _lib.check(L_.ell1_gemm_f64(0, 0, d, n, d, ptr(Gcm), ld, ptr(A64), ld, ptr(M64), ld, st), "ell1_gemm_f64")
         MT = M64 if self.storage.dtype == torch.float64 else M64.to(self.storage.dtype)
         Llow = torch.tril(Lf.view(d, d).T)                     # lower factor (row-major view), observers
-        cache[key] = (MT, Gcm, Llow)
+        Gld = torch.zeros(d, ld, **f64)                         # G itself, column-major (batched certificate)
+        Gld[:, :d] = G.view(d, d)
+        cache[key] = (MT, Gcm, Llow, Gld)
         return cache[key]
 
     # -- operator-protocol hooks ------------------------------------------

@@ -20,7 +20,8 @@ def _dev_dict(A, dtype):
 
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
 @pytest.mark.parametrize("shape", [(20, 40), (500, 1000), (1024, 4096), (1500, 700),
-                                   (4100, 300), (9000, 2000), (65536, 64)])
+                                   (4100, 300), (9000, 2000), (65536, 64), (8192, 3001), (40960, 37),
+                                   (131072, 21)])
 def test_gemv_pair(shape, dtype):
     import torch
     from paper_1007_3753_b200 import _lib, device

@@ -24,7 +24,7 @@ def main():
     cfg = SolverConfig(tol=1e-8, max_iter=300)
     prep = Prepared(ProblemInstance(P.A, P.b), cfg)
     D = prep.D
-    MT, Gcm, _ = D.gram_factor(False, 0.0)
+    MT, Gcm, _, _ = D.gram_factor(False, 0.0)
     O = _lib.DalmOpts()
     O.beta, O.y_tol, O.y_cg_step = 1.0, 1e-10, 0
     O.M, O.Ginv = MT.data_ptr(), Gcm.data_ptr()

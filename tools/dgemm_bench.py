@@ -40,8 +40,8 @@ def timeit(fn, reps=5):
 
 
 rows = []
-shapes = [("AX", 0, 0, 512, B, 2048) for B in (64, 256, 1024, 2048, 8192)] + \
-         [("AtR", 1, 0, 2048, B, 512) for B in (64, 256, 1024, 2048, 8192)] + \
+shapes = [("AX", 0, 0, 512, B, 2048) for B in (64, 256, 485, 1024, 2048, 8192)] + \
+         [("AtR", 1, 0, 2048, B, 512) for B in (64, 256, 485, 1024, 2048, 8192)] + \
          [("GinvB", 0, 0, 1024, 1024, 1024), ("AX_cab", 0, 0, 1024, 2048, 2240),
           ("gramNT", 0, 1, 1024, 1024, 4096), ("big", 0, 0, 4096, 4096, 4096)]
 for name, ta, tb, m, n, k in shapes:
