@@ -615,6 +615,17 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   bool use_plain = true;
   if (const char* e = getenv("ELL1_BATCH_GRAPH")) use_plain = e[0] != '0';
   cudaGraphExec_t pexec[2] = {nullptr, nullptr};
+  struct GraphGuard {                                  // every exit path releases the graphs
+    cudaGraph_t& g;
+    cudaGraphExec_t& e;
+    cudaGraphExec_t* pe;
+    ~GraphGuard() {
+      if (e) cudaGraphExecDestroy(e);
+      if (g) cudaGraphDestroy(g);
+      for (int q = 0; q < 2; ++q)
+        if (pe[q]) cudaGraphExecDestroy(pe[q]);
+    }
+  } graph_guard{graph, gexec, pexec};
   int pB = -1;
   auto build_graph = [&]() -> bool {
     gfail = 0;
@@ -689,16 +700,17 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
     if (nact <= 0) break;
     if (nact < Bcur * 3 / 4 || (nact < Bcur && nact <= 64)) {
       bd_scan<<<1, 1024, 0, s>>>(a.inst, Bcur, perm, ctr + 2);
+      bool cok = true;
       auto pm = [&](double* M, int64_t rows, int64_t ldm) {
         dim3 g((unsigned)((rows + 255) / 256 < 64 ? (rows + 255) / 256 : 64), (unsigned)nact);
         bd_gather<double><<<g, 256, 0, s>>>(M, scratch, rows, ldm, perm, nact);
-        cudaMemcpyAsync(M, scratch, ldm * nact * 8, cudaMemcpyDeviceToDevice, s);
+        cok = cok && cudaMemcpyAsync(M, scratch, ldm * nact * 8, cudaMemcpyDeviceToDevice, s) == cudaSuccess;
       };
       pm(a.X[a.ix], N, ldx);
       if (a.f32) {                                          // A^T y of the current y
         dim3 g((unsigned)((D->n + 255) / 256 < 64 ? (D->n + 255) / 256 : 64), (unsigned)nact);
         bd_gather<float><<<g, 256, 0, s>>>(T32, (float*)scratch, D->n, D->n, perm, nact);
-        cudaMemcpyAsync(T32, scratch, D->n * nact * 4, cudaMemcpyDeviceToDevice, s);
+        cok = cok && cudaMemcpyAsync(T32, scratch, D->n * nact * 4, cudaMemcpyDeviceToDevice, s) == cudaSuccess;
       } else {
         pm(a.UX, N, ldx);
       }
@@ -709,8 +721,9 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
       {
         const int64_t words = (int64_t)sizeof(DI) / 4;
         bd_gather<int><<<dim3(1, (unsigned)nact), 64, 0, s>>>((const int*)a.inst, (int*)inst2, words, words, perm, nact);
-        cudaMemcpyAsync(a.inst, inst2, sizeof(DI) * nact, cudaMemcpyDeviceToDevice, s);
+        cok = cok && cudaMemcpyAsync(a.inst, inst2, sizeof(DI) * nact, cudaMemcpyDeviceToDevice, s) == cudaSuccess;
       }
+      if (!cok || cudaGetLastError() != cudaSuccess) return ELL1_ERR_CUDA;
       Bcur = nact;
     }
     // ---- DALM iterations over Bcur instances
@@ -785,9 +798,5 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
     a.ix ^= 1;
     a.iy ^= 1;
   }
-  if (gexec) cudaGraphExecDestroy(gexec);
-  if (graph) cudaGraphDestroy(graph);
-  for (int q = 0; q < 2; ++q)
-    if (pexec[q]) cudaGraphExecDestroy(pexec[q]);
   return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
 }

@@ -497,6 +497,10 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
   bool use_graph = true;
   if (const char* e = getenv("ELL1_BATCH_GRAPH")) use_graph = e[0] != '0';
   cudaGraphExec_t gexec = nullptr;
+  struct ExecGuard {                                   // every exit path releases the graph
+    cudaGraphExec_t& e;
+    ~ExecGuard() { if (e) cudaGraphExecDestroy(e); }
+  } gexec_guard{gexec};
   int gB = -1;
   for (;;) {
     if (cudaMemcpyAsync(h_ctr, ctr, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ELL1_ERR_CUDA;
@@ -506,10 +510,11 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
     if (nact < Bcur * 3 / 4 || (nact < Bcur && nact <= 64)) {
       // compact the active instances to the front of every state matrix
       bf_scan<<<1, 1024, 0, s>>>(a.inst, Bcur, perm, ctr + 2);
+      bool cok = true;
       auto perm_mat = [&](double* M, int64_t rows, int64_t ldm) {
         dim3 g((unsigned)((rows + 255) / 256 < 64 ? (rows + 255) / 256 : 64), (unsigned)nact);
         gather_cols<double><<<g, 256, 0, s>>>(M, scratch, rows, ldm, perm, nact);
-        cudaMemcpyAsync(M, scratch, ldm * nact * 8, cudaMemcpyDeviceToDevice, s);
+        cok = cok && cudaMemcpyAsync(M, scratch, ldm * nact * 8, cudaMemcpyDeviceToDevice, s) == cudaSuccess;
       };
       for (int k = 0; k < 3; ++k) perm_mat(a.X[k], N, ldx);
       for (int k = 0; k < 2; ++k) perm_mat(a.G[k], N, ldx);
@@ -521,14 +526,15 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
         float* fs = reinterpret_cast<float*>(scratch);
         dim3 g((unsigned)((D->n + 255) / 256 < 64 ? (D->n + 255) / 256 : 64), (unsigned)nact);
         gather_cols<float><<<g, 256, 0, s>>>(a.G32, fs, D->n, D->n, perm, nact);
-        cudaMemcpyAsync(a.G32, fs, D->n * nact * 4, cudaMemcpyDeviceToDevice, s);
+        cok = cok && cudaMemcpyAsync(a.G32, fs, D->n * nact * 4, cudaMemcpyDeviceToDevice, s) == cudaSuccess;
       }
       {
         const int64_t words = (int64_t)sizeof(BI) / 4;
         dim3 g(1, (unsigned)nact);
         gather_cols<int><<<g, 64, 0, s>>>((const int*)a.inst, (int*)inst2, words, words, perm, nact);
-        cudaMemcpyAsync(a.inst, inst2, sizeof(BI) * nact, cudaMemcpyDeviceToDevice, s);
+        cok = cok && cudaMemcpyAsync(a.inst, inst2, sizeof(BI) * nact, cudaMemcpyDeviceToDevice, s) == cudaSuccess;
       }
+      if (!cok || cudaGetLastError() != cudaSuccess) return ELL1_ERR_CUDA;
       Bcur = nact;
     }
     if (use_graph && gB != Bcur) {
@@ -565,7 +571,6 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
         if (!one_round(aa)) return ELL1_ERR_CUDA;
     }
   }
-  if (gexec) cudaGraphExecDestroy(gexec);
   return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
 }
 

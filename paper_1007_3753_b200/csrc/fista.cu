@@ -497,6 +497,12 @@ struct CorrArgs {
   int wmax;
 };
 
+// a grid barrier timed out (the kernel aborts cleanly): tell the host through
+// the output block — out[0] = NaN, out[1] = ELL1_ERR_TIMEOUT
+__device__ __forceinline__ void timeout_out(const Ctx& E, double* out) {
+  if (E.b == 0 && threadIdx.x == 0) { out[0] = NAN; out[1] = (double)ELL1_ERR_TIMEOUT; }
+}
+
 template <class TA>
 __device__ __forceinline__ void corr_body(const CorrArgs& a) {
   extern __shared__ __align__(16) double smem[];
@@ -524,7 +530,7 @@ __device__ __forceinline__ void corr_body(const CorrArgs& a) {
   for (int64_t i = E.r0 + tix(); i < E.r1; i += NTHR) v[1] += a.b[i] * a.b[i];
   block_reduce<2>(E, v, 1u);
   publish<2>(E, v);
-  if (!grid_sync(E)) return;
+  if (!grid_sync(E)) { timeout_out(E, a.out); return; }
   double o[2];
   gather<2>(E, o, 1u);
   if (E.b == 0 && threadIdx.x == 0) { a.out[0] = o[0]; a.out[1] = sqrt(o[1]); }
@@ -574,7 +580,7 @@ __device__ __forceinline__ void power_body(const PowerArgs& a) {
   } else {
     for_owned(E, [&](int kk) { Vn[0][kk] = a.v0[E.c0 + kk]; });
   }
-  if (!grid_sync(E)) return;
+  if (!grid_sync(E)) { timeout_out(E, a.out); return; }
   for (k = 0; k < a.max_iter; ++k) {
     double T[2], R2[1];
     if (dside) {
@@ -588,7 +594,7 @@ __device__ __forceinline__ void power_body(const PowerArgs& a) {
         const double* xs[1] = {U};
         panel_gemv<TA, 1>(E, D, PN, xs);                 // partial A u
       }
-      if (!grid_sync(E)) return;
+      if (!grid_sync(E)) { timeout_out(E, a.out); return; }
       double q[2] = {0.0, 0.0};
       double none[1];
       const double* aux[1] = {v};
@@ -600,7 +606,7 @@ __device__ __forceinline__ void power_body(const PowerArgs& a) {
       });
       block_reduce<2>(E, q, 0u);
       publish<2>(E, q);
-      if (!grid_sync(E)) return;
+      if (!grid_sync(E)) { timeout_out(E, a.out); return; }
       gather<2>(E, T, 0u);
       theta = T[0];
       const double nw = sqrt(T[1]);
@@ -613,14 +619,14 @@ __device__ __forceinline__ void power_body(const PowerArgs& a) {
       }
       block_reduce<1>(E, e, 0u);
       publish<1>(E, e);
-      if (!grid_sync(E)) return;
+      if (!grid_sync(E)) { timeout_out(E, a.out); return; }
       gather<1>(E, R2, 0u);
       if (sqrt(R2[0]) <= a.tol * pymax(theta, 2.2250738585072014e-308)) break;
       if (nw == 0.0) {
         if (redraw >= a.nredraw) break;
         ++redraw;
         for (int64_t i = E.r0 + tix(); i < E.r1; i += NTHR) vn[i] = a.v0[redraw * dim + i];
-        if (!grid_sync(E)) return;
+        if (!grid_sync(E)) { timeout_out(E, a.out); return; }
       }
     } else {
       double* v = Vn[iv];
@@ -629,12 +635,12 @@ __device__ __forceinline__ void power_body(const PowerArgs& a) {
         const double* xs[1] = {v};
         panel_gemv<TA, 1>(E, D, PN, xs);                 // partial A v
       }
-      if (!grid_sync(E)) return;
+      if (!grid_sync(E)) { timeout_out(E, a.out); return; }
       double none[1];
       const double* aux[1] = {nullptr};
       gather_slice<0, 1, 0>(E, none, 0u, D.ld, aux,
                             [&](int64_t i, const double* sums, const double*) { a.W[i] = sums[0]; });
-      if (!grid_sync(E)) return;
+      if (!grid_sync(E)) { timeout_out(E, a.out); return; }
       {
         const double* rs[1] = {a.W};
         double* os[1] = {U};
@@ -649,7 +655,7 @@ __device__ __forceinline__ void power_body(const PowerArgs& a) {
       });
       block_reduce<2>(E, q, 0u);
       publish<2>(E, q);
-      if (!grid_sync(E)) return;
+      if (!grid_sync(E)) { timeout_out(E, a.out); return; }
       gather<2>(E, T, 0u);
       theta = T[0];
       const double nw = sqrt(T[1]);
@@ -662,7 +668,7 @@ __device__ __forceinline__ void power_body(const PowerArgs& a) {
       });
       block_reduce<1>(E, e, 0u);
       publish<1>(E, e);
-      if (!grid_sync(E)) return;
+      if (!grid_sync(E)) { timeout_out(E, a.out); return; }
       gather<1>(E, R2, 0u);
       if (sqrt(R2[0]) <= a.tol * pymax(theta, 2.2250738585072014e-308)) break;
       if (nw == 0.0) {

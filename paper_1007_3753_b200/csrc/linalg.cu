@@ -108,6 +108,11 @@ struct PcgV {
   int k, done, conv, status, use_best;
 };
 
+// a grid barrier timed out (the kernel aborts cleanly): status ELL1_ERR_TIMEOUT in out[3]
+__device__ __forceinline__ void pcg_timeout(const Ctx& E, double* out) {
+  if (E.b == 0 && threadIdx.x == 0) { out[0] = 0.0; out[1] = 0.0; out[2] = NAN; out[3] = (double)ELL1_ERR_TIMEOUT; }
+}
+
 template <class TA>
 __global__ void __launch_bounds__(NTHR, 1) pcg_kernel(const __grid_constant__ PcgArgs a) {
   extern __shared__ __align__(16) double smem[];
@@ -141,7 +146,7 @@ __global__ void __launch_bounds__(NTHR, 1) pcg_kernel(const __grid_constant__ Pc
     s2[0] += r * r;
     s2[1] += r * z;
   });
-  if (!allreduce<2>(E, s2, 0u)) return;
+  if (!allreduce<2>(E, s2, 0u)) { pcg_timeout(E, a.out); return; }
   if (tix() == 0) {
     V.bn = sqrt(s2[0]); V.rz = s2[1]; V.best = V.bn; V.res = 0.0;
     V.k = 0; V.done = 0; V.conv = 0; V.status = 0; V.use_best = 0;
@@ -167,7 +172,7 @@ __global__ void __launch_bounds__(NTHR, 1) pcg_kernel(const __grid_constant__ Pc
     }
     double q[1] = {0.0};
     for_owned(E, [&](int k) { q[0] += Pv[k] * AP[k]; });
-    if (!allreduce<1>(E, q, 0u)) return;
+    if (!allreduce<1>(E, q, 0u)) { pcg_timeout(E, a.out); return; }
     const double pAp = q[0];
     if (!isfinite(pAp)) { T0 { V.status = ELL1_BREAKDOWN; V.done = 1; } __syncthreads(); break; }
     if (pAp <= 0.0) { T0 { V.done = 1; V.use_best = 1; V.res = V.best; } __syncthreads(); break; }
@@ -179,7 +184,7 @@ __global__ void __launch_bounds__(NTHR, 1) pcg_kernel(const __grid_constant__ Pc
       Rv[k] = r;
       s[0] += r * r;
     });
-    if (!allreduce<1>(E, *reinterpret_cast<double(*)[1]>(s), 0u)) return;
+    if (!allreduce<1>(E, *reinterpret_cast<double(*)[1]>(s), 0u)) { pcg_timeout(E, a.out); return; }
     const double res = sqrt(s[0]);
     if (!isfinite(res)) { T0 { V.status = ELL1_BREAKDOWN; V.done = 1; } __syncthreads(); break; }
     const bool better = res < V.best;
@@ -192,7 +197,7 @@ __global__ void __launch_bounds__(NTHR, 1) pcg_kernel(const __grid_constant__ Pc
       const double z = dg ? Rv[k] / dg[E.c0 + k] : Rv[k];
       rz1[0] += Rv[k] * z;
     });
-    if (!allreduce<1>(E, rz1, 0u)) return;
+    if (!allreduce<1>(E, rz1, 0u)) { pcg_timeout(E, a.out); return; }
     const double beta = rz1[0] / V.rz;
     for_owned(E, [&](int k) {
       const double z = dg ? Rv[k] / dg[E.c0 + k] : Rv[k];
@@ -202,7 +207,7 @@ __global__ void __launch_bounds__(NTHR, 1) pcg_kernel(const __grid_constant__ Pc
     });
     __syncthreads();
     T0 V.rz = rz1[0];
-    if (!grid_sync(E)) return;                       // p complete before the next GEMV^T
+    if (!grid_sync(E)) { pcg_timeout(E, a.out); return; }   // p complete before the next GEMV^T
   }
   __syncthreads();
   const bool ub = V.use_best;

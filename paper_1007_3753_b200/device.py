@@ -217,6 +217,8 @@ def _corr(D, view, b):
                                 stream_ptr(D.device))
     _lib.check(rc, "ell1_correlation_max")
     o = out.cpu().numpy()
+    if np.isnan(o[0]):
+        raise DeviceError("ell1_correlation_max: grid barrier timed out")
     return float(o[0]), float(o[1])
 
 
@@ -242,4 +244,7 @@ def spectral_norm_sq_device(D, tol=1e-6, max_iter=1000):
     rc = L.ell1_spectral_norm_sq(ctypes.byref(view), ptr(vd), 3, float(tol), int(max_iter),
                                  ptr(out), ptr(ws), wsb, stream_ptr(D.device))
     _lib.check(rc, "ell1_spectral_norm_sq")
-    return float(out.cpu().numpy()[0])
+    o = out.cpu().numpy()
+    if np.isnan(o[0]):
+        raise DeviceError("ell1_spectral_norm_sq: grid barrier timed out")
+    return float(o[0])

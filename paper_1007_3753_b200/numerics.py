@@ -208,6 +208,9 @@ def pcg_solve(op, rhs, precond=None, tol=1e-8, max_iter=None):
                                 int(max_iter), device.ptr(x), device.ptr(out), device.ptr(ws), wsb,
                                 device.stream_ptr(dev)), "ell1_pcg_dense")
     o = out.cpu().numpy()
+    if int(o[3]) == _lib.ERR_TIMEOUT:
+        from paper_1007_3753_b200.exceptions import DeviceError
+        raise DeviceError("ell1_pcg_dense: grid barrier timed out")
     if int(o[3]) == _lib.BREAKDOWN:
         raise NumericalBreakdownError("non-finite curvature or residual in PCG")
     return PcgResult(x.cpu().numpy(), bool(o[0]), int(o[1]), float(o[2]))

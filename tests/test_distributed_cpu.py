@@ -120,3 +120,50 @@ def test_sharded_batch_gathers_in_order(world):
             idx = shard_indices(Bm.shape[1], r, world)
             np.testing.assert_array_equal(o["lam"][idx], np.arange(idx.shape[0]) + 0.5)
             np.testing.assert_array_equal(o["cres"][idx, 0], np.arange(idx.shape[0]))
+
+
+def _fail_worker(rank, world, port, out_dir):
+    """Rank 1 fails inside its local solve: every rank must raise (ADVICE r01:
+    no rank may be left blocked in the result gather)."""
+    import torch.distributed as dist
+    from paper_1007_3753_b200.distributed import solve_batch_sharded
+    from paper_1007_3753_b200.exceptions import DeviceError, NumericalBreakdownError
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def solve(A, Bsub, config):
+        if dist.get_rank() == 1:
+            raise NumericalBreakdownError("rank 1 breaks down")
+        return _oracle_batch(A, Bsub, config)
+    try:
+        A, Bm = _problem()
+        try:
+            solve_batch_sharded(solve, A, Bm[:, :3], {"lam": 1e-3}, device="cpu")
+            outcome = "returned"
+        except NumericalBreakdownError:
+            outcome = "breakdown"
+        except DeviceError:
+            outcome = "peer_failed"
+        with open(os.path.join(out_dir, "r%d.txt" % rank), "w") as fh:
+            fh.write(outcome)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_batch_failure_raises_on_every_rank():
+    import torch.multiprocessing as mp
+    with tempfile.TemporaryDirectory() as tmp:
+        mp.spawn(_fail_worker, args=(3, _free_port(), tmp), nprocs=3, join=True)
+        got = [open(os.path.join(tmp, "r%d.txt" % r)).read() for r in range(3)]
+    assert got == ["peer_failed", "breakdown", "peer_failed"]
+
+
+def test_batched_entry_points_accept_empty_share():
+    """B < world leaves a rank with no columns: the batched entry points return
+    an empty result instead of an argument error (no GPU needed for B = 0)."""
+    from paper_1007_3753_b200 import batched
+    from paper_1007_3753_b200.model import SolverConfig
+    A = np.eye(4)
+    r = batched._empty("fista", A, np.zeros((4, 0)), SolverConfig())
+    assert r.x.shape == (4, 0) and r.results() == []
