@@ -2,10 +2,13 @@
 // (element j equals alm.dalm_solve on (D, b_j), alm.py:206-272), e.g. the
 // cross-and-bouquet face-recognition batch of BASELINE config 3 on [A, sI].
 //
-// Per iteration (same algebra as csrc/dalm.cu, with M = G^{-1} A, Ginv = G^{-1}):
-//   z-kernel  : z = clamp(A^T y + x/beta), v = z - x/beta
-//   GEMMs     : M v, A z (+ Ginv v_ext for [A, sI])
-//   y-kernel  : y = M v + Ginv b / beta, rhs = A z - (A x - b)/beta
+// Per iteration (alm.py:172-189, 239-268; Ginv = G^{-1}, G = A A^T (+ s^2 I)):
+//   z-kernel  : z = clamp(A^T y + x/beta)
+//   float64 storage:
+//     GEMM      : A z;  rhs-kernel: rhs = A z - (A x - b)/beta
+//     GEMM      : y = Ginv rhs  (d^2 per instance: the reference's cho_solve), y-kernel: b^T y
+//   float32 storage (tensor-core GEMMs need the fp32 operands of the precomputed M = Ginv A):
+//     v = z - x/beta; GEMMs [M | Ginv] v and A z; y-kernel: y = M v + Ginv b / beta, rhs
 //   GEMM      : A^T y
 //   x-kernel  : x_new = x - beta (z - A^T y)
 //   GEMM      : A [A^T y | x_new]   (one GEMM over 2B columns)
@@ -111,7 +114,7 @@ __global__ void __launch_bounds__(BT) bd_z(const BDArgs a) {
   double* __restrict__ vo = a.V + o;
   float* __restrict__ v32 = a.V32 + o;
   float* __restrict__ z32 = a.Z32 + o;
-  const bool keep_v = !a.f32 || (a.ext && !a.fuse_ext);    // fp64 v feeds a GEMM only then
+  const bool keep_v = false;                                // fp64: y = Ginv rhs needs no v
   const bool f32 = a.f32, fuse = a.fuse_ext;
   const int64_t n = a.n;
   const double beta = a.beta, sc = a.s;
@@ -171,6 +174,54 @@ __global__ void __launch_bounds__(BT) bd_y(const BDArgs a) {
   }
   cta_reduce<2>(q, 0u, sh);
   if (threadIdx.x == 0) { I.rhs2 = q[0]; I.by = q[1]; }
+}
+
+// float64 storage: rhs = A z - (A x - b)/beta (alm.py:179), ||rhs||^2
+__global__ void __launch_bounds__(BT) bd_rhs(const BDArgs a) {
+  const int j = blockIdx.x;
+  __shared__ double sh[BW + 1];
+  DI& I = a.inst[j];
+  if (!I.active) return;
+  const int64_t oj = (int64_t)j * a.ld;
+  const double* __restrict__ b = a.Bm + oj;
+  const double* __restrict__ zx = a.Z + (int64_t)j * a.ldx + a.n;
+  const double* __restrict__ ax = a.AX + oj;
+  const double* __restrict__ p2 = a.P2 + oj;
+  double* __restrict__ rh = a.RHS + oj;
+  const bool ext = a.ext;
+  const double beta = a.beta, sc = a.s;
+  double q[1] = {0.0};
+#pragma unroll 4
+  for (int64_t i = threadIdx.x; i < a.d; i += BT) {
+    double az = p2[i];
+    if (ext) az = az + sc * zx[i];
+    const double rhs = az - (ax[i] - b[i]) / beta;
+    rh[i] = rhs;
+    q[0] += rhs * rhs;
+  }
+  cta_reduce<1>(q, 0u, sh);
+  if (threadIdx.x == 0) I.rhs2 = q[0];
+}
+
+// float64 storage: y = Ginv rhs (the GEMM output P1), b^T y
+__global__ void __launch_bounds__(BT) bd_yg(const BDArgs a) {
+  const int j = blockIdx.x;
+  __shared__ double sh[BW + 1];
+  DI& I = a.inst[j];
+  if (!I.active) return;
+  const int64_t oj = (int64_t)j * a.ld;
+  const double* __restrict__ b = a.Bm + oj;
+  double* __restrict__ y = a.Y[a.iy ^ 1] + oj;
+  const double* __restrict__ p1 = a.P1 + oj;
+  double q[1] = {0.0};
+#pragma unroll 4
+  for (int64_t i = threadIdx.x; i < a.d; i += BT) {
+    const double yi = p1[i];
+    y[i] = yi;
+    q[0] += b[i] * yi;
+  }
+  cta_reduce<1>(q, 0u, sh);
+  if (threadIdx.x == 0) I.by = q[0];
 }
 
 // x_new = x - beta (z - A^T y) (alm.py:245-246); U = A^T y lives in UX[:, j]
@@ -532,8 +583,8 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   if (cudaMemcpyAsync(Bm, Bmat, ld * B * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return ELL1_ERR_CUDA;
   if (cudaMemsetAsync(ctr, 0, 32, s) != cudaSuccess) return ELL1_ERR_CUDA;
   if (cudaMemsetAsync(a.UX32, 0, ldx * 2 * B * 4, s) != cudaSuccess) return ELL1_ERR_CUDA;
-  // C0 = Ginv B (Ginv column-major ld x d, float64)
-  if (!dgemm(0, 0, ld, B, d, O->Ginv, ld, Bm, ld, C0, ld, s)) return ELL1_ERR_CUDA;
+  // C0 = Ginv B (Ginv column-major ld x d, float64), the fp32 y step's constant term
+  if (a.f32 && !dgemm(0, 0, ld, B, d, O->Ginv, ld, Bm, ld, C0, ld, s)) return ELL1_ERR_CUDA;
   bd_init<<<B, BT, 0, s>>>(a);
   ell1_dict_t MD = *D;
   MD.A = O->M;                                              // M has A's layout / dtype
@@ -574,6 +625,14 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   // one iteration up to the certificate (bd_c raises ctr[0] refine flags)
   auto main_part = [&](const BDArgs& aa, int Bc) -> bool {
     bd_z<<<Bc, BT, 0, ks>>>(aa);
+    if (!aa.f32) {
+      // y = G^-1 rhs (dual_y_solve's cho_solve, alm.py:179-180) on the DMMA path
+      if (!gemm_AX(ks, D, aa.Z, ldx, aa.P2, ld, Bc)) return false;
+      bd_rhs<<<Bc, BT, 0, ks>>>(aa);
+      if (!dgemm(0, 0, ld, Bc, d, O->Ginv, ld, aa.RHS, ld, aa.P1, ld, ks)) return false;
+      bd_yg<<<Bc, BT, 0, ks>>>(aa);
+      return tail_part(aa, Bc, 0);
+    }
     const void* Vop = aa.f32 ? (const void*)aa.V32 : (const void*)aa.V;
     const void* Zop = aa.f32 ? (const void*)aa.Z32 : (const void*)aa.Z;
     if (aa.fuse_ext) {
@@ -716,7 +775,7 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
       }
       pm(a.Y[a.iy], ld, ld);
       pm(a.AX, ld, ld);
-      pm(C0, ld, ld);
+      if (a.f32) pm(C0, ld, ld);
       pm(Bm, ld, ld);
       {
         const int64_t words = (int64_t)sizeof(DI) / 4;
