@@ -514,6 +514,10 @@ size_t ell1_align_stage_bytes(int32_t kind, int32_t count, int32_t d, int32_t m)
  * image, B row-major d x m (ldb), m <= 32; w_next (m), e_next (d) device outputs */
 int ell1_align_ist_step(int32_t d, int32_t m, const double* B, int64_t ldb, const double* b, const double* w,
                         const double* e, double lam, double alpha, double* w_next, double* e_next, void* stream);
+/* test hook: 1 routes every alignment launch through the large-image variant
+ * (d <= 8192, 32 rows per thread) — bit-identical to the default variant where
+ * both apply; 0 restores the size-based choice */
+void ell1_test_align_large_rows(int32_t on);
 /* align_palm_solve per image (robust.py:470-515) */
 int ell1_align_palm_batch(const ell1_align_t* A, void* stream);
 /* align_ist_solve per image (robust.py:427-467) */

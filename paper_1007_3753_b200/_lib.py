@@ -259,6 +259,7 @@ _SIGS = {
     "ell1_align_ist_step": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64] +
                             [ctypes.c_void_p] * 3 + [ctypes.c_double] * 2 + [ctypes.c_void_p] * 3),
     "ell1_align_stage_bytes": (ctypes.c_size_t, [ctypes.c_int32] * 4),
+    "ell1_test_align_large_rows": (None, [ctypes.c_int32]),
     "ell1_align_palm_batch": (ctypes.c_int, [P(Align), ctypes.c_void_p]),
     "ell1_align_ist_batch": (ctypes.c_int, [P(Align), ctypes.c_void_p]),
     "ell1_align_homotopy_batch": (ctypes.c_int, [P(Align), ctypes.c_void_p]),

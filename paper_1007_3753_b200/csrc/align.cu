@@ -8,7 +8,8 @@
 //   * B (row-major, numpy's layout) is staged in shared memory once as columns
 //     of d + 1 doubles (odd stride: conflict-free staging and column walks);
 //     the d-vectors (b, e, y / w-step residuals) live in registers, a fixed
-//     set of rows per thread (RPT rows, 256 threads apart);
+//     set of rows per thread (RPT rows, 256 threads apart; RPT = 8 up to
+//     d = 2048, 32 up to d = 8192);
 //   * the column Gram G = B^T B is formed by fixed-order block reductions and
 //     factored G = R^T R by warp 0 (not PD -> IllConditionedError, robust.py:254-258);
 //   * every B^T v is one m-wide block reduction (lanes -> xor tree -> warps,
@@ -26,7 +27,12 @@ namespace {
 constexpr int AT = 256;                 // threads per image
 constexpr int AW = AT / 32;
 constexpr int MAXM = 32;                // columns of B (parameters) supported
-constexpr int RPT = 8;                  // rows per thread kept in registers (d <= AT * RPT = 2048)
+// rows per thread kept in registers: RPT_S (d <= AT * RPT_S = 2048) for the
+// common image sizes; RPT_L (d <= 8192) for large images (the d-vectors then
+// partly live in local memory — correct, slower)
+constexpr int RPT_S = 8;
+constexpr int RPT_L = 32;
+constexpr int MAXD = AT * RPT_L;
 
 struct AlignSh {
   double red[AW][MAXM + 2];
@@ -56,6 +62,7 @@ __device__ __forceinline__ void block_sum(AlignSh& S, double* v, int k) {
 }
 
 // g = B^T v for the rows this thread holds; result in S.out[0..m)
+template <int RPT>
 __device__ __forceinline__ void bt_times(AlignSh& S, const double* Bs, int d, int m, const double (&v)[RPT]) {
   double p[MAXM];
   for (int c = 0; c < m; ++c) {
@@ -102,6 +109,7 @@ __device__ __forceinline__ double soft(double x, double a) {
 }
 
 // stage B, form G = B^T B, factor; returns false (status set) when not PD
+template <int RPT>
 __device__ bool setup(AlignSh& S, double* Bs, const ell1_align_t& a, int j, double (&b)[RPT]) {
   const int d = a.d, m = a.m;
   const double* Bj = a.B + (int64_t)j * a.b_stride;
@@ -159,6 +167,7 @@ __device__ bool setup(AlignSh& S, double* Bs, const ell1_align_t& a, int j, doub
   return true;
 }
 
+template <int RPT>
 __device__ __forceinline__ void store_out(const ell1_align_t& a, int j, const AlignSh& S, const double (&e)[RPT]) {
   if ((int)threadIdx.x < a.m) a.w[(int64_t)j * a.m + threadIdx.x] = S.w[threadIdx.x];
 #pragma unroll
@@ -171,6 +180,7 @@ __device__ __forceinline__ void store_out(const ell1_align_t& a, int j, const Al
 // ---------------------------------------------------------------- PALM
 // robust.py:470-515: w = G^{-1} B^T (b - e + y/mu); e = soft(b - Bw + y/mu, 1/mu)
 // (inner sweeps to 1e-2/mu relative change, <= 100 per mu), y += mu r, mu *= rho
+template <int RPT>
 __global__ void __launch_bounds__(AT) align_palm_kernel(const ell1_align_t a) {
   extern __shared__ double Bsm[];
   double* const Bs = stage_ptr(a, Bsm);
@@ -238,6 +248,7 @@ __global__ void __launch_bounds__(AT) align_palm_kernel(const ell1_align_t a) {
 // when max|B^T r| <= tol and kkt(e, r, lam) <= tol lam.  alpha = 1.01 (||B||^2 + 1)
 // with ||B||^2 from the reference's power iteration (numerics.py:224-261) run on
 // B^T (B v) from the host-drawn start vectors.
+template <int RPT>
 __global__ void __launch_bounds__(AT) align_ist_kernel(const ell1_align_t a) {
   extern __shared__ double Bsm[];
   double* const Bs = stage_ptr(a, Bsm);
@@ -379,6 +390,7 @@ __device__ __forceinline__ void block_min2(AlignSh& S, double v0, double v1) {
   __syncthreads();
 }
 
+template <int RPT>
 __global__ void __launch_bounds__(AT) align_homotopy_kernel(const ell1_align_t a) {
   extern __shared__ double Bsm[];
   double* const Bs = stage_ptr(a, Bsm);
@@ -482,6 +494,7 @@ __device__ __forceinline__ double block_sum1(AlignSh& S, double v) {
 }
 
 // upper Cholesky of the weighted Gram B^T diag(wt) B into S.R; false if not PD
+template <int RPT>
 __device__ bool weighted_gram_factor(AlignSh& S, const double* Bs, int d, int m, const double (&wt)[RPT]) {
   for (int c = 0; c < m; ++c) {
     double p[MAXM];
@@ -522,6 +535,7 @@ __device__ bool weighted_gram_factor(AlignSh& S, const double* Bs, int d, int m,
   return !S.flag;
 }
 
+template <int RPT>
 __global__ void __launch_bounds__(AT) align_gp_kernel(const ell1_align_t a) {
   extern __shared__ double Bsm[];
   double* const Bs = stage_ptr(a, Bsm);
@@ -769,11 +783,23 @@ __global__ void __launch_bounds__(AT) align_ist_step_kernel(int d, int m, const 
   if ((int)threadIdx.x < m) w_next[threadIdx.x] = S.w[threadIdx.x] + S.out[threadIdx.x] / alpha;
 }
 
-const void* align_kernel(int kind) {
-  return kind == 0   ? (const void*)align_palm_kernel
-         : kind == 1 ? (const void*)align_ist_kernel
-         : kind == 2 ? (const void*)align_homotopy_kernel
-                     : (const void*)align_gp_kernel;
+template <int RPT>
+const void* align_kernel_t(int kind) {
+  return kind == 0   ? (const void*)align_palm_kernel<RPT>
+         : kind == 1 ? (const void*)align_ist_kernel<RPT>
+         : kind == 2 ? (const void*)align_homotopy_kernel<RPT>
+                     : (const void*)align_gp_kernel<RPT>;
+}
+
+// test hook (ell1_test_align_large_rows): run every image through the
+// RPT_L variant — bit-identical to RPT_S where both apply (same row map and
+// accumulation order; the extra row slots are masked)
+int g_force_large = 0;
+
+bool use_large(int d) { return g_force_large || d > AT * RPT_S; }
+
+const void* align_kernel(int kind, int d) {
+  return use_large(d) ? align_kernel_t<RPT_L>(kind) : align_kernel_t<RPT_S>(kind);
 }
 
 // launch geometry: shared-memory staging when it fits next to the kernel's
@@ -785,7 +811,7 @@ struct AlignPlan {
 };
 
 bool align_plan(int kind, int count, int d, int m, AlignPlan& P) {
-  const void* k = align_kernel(kind);
+  const void* k = align_kernel(kind, d);
   int dev = 0, sms = 148, optin = 0, per = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -805,7 +831,7 @@ bool align_plan(int kind, int count, int d, int m, AlignPlan& P) {
 }
 
 int launch_align(int kind, const ell1_align_t* A, void* stream) {
-  if (!A || A->count < 0 || A->m < 1 || A->m > MAXM || A->d <= A->m || A->d > AT * RPT || !A->B || !A->rhs ||
+  if (!A || A->count < 0 || A->m < 1 || A->m > MAXM || A->d <= A->m || A->d > MAXD || !A->B || !A->rhs ||
       !A->w || !A->e || !A->status || A->ldb < A->m || A->ld_rhs < A->d || A->b_stride < A->ldb * A->d)
     return ELL1_ERR_ARG;
   if (kind == 1 && !A->v0) return ELL1_ERR_ARG;
@@ -816,10 +842,17 @@ int launch_align(int kind, const ell1_align_t* A, void* stream) {
   if (P.stage == 0) a.Bstage = nullptr;
   else if (!A->Bstage) return ELL1_ERR_ARG;            // caller must provide ell1_align_stage_bytes()
   cudaStream_t s = (cudaStream_t)stream;
-  if (kind == 0) align_palm_kernel<<<P.grid, AT, P.smem, s>>>(a);
-  else if (kind == 1) align_ist_kernel<<<P.grid, AT, P.smem, s>>>(a);
-  else if (kind == 2) align_homotopy_kernel<<<P.grid, AT, P.smem, s>>>(a);
-  else align_gp_kernel<<<P.grid, AT, P.smem, s>>>(a);
+  if (!use_large(a.d)) {
+    if (kind == 0) align_palm_kernel<RPT_S><<<P.grid, AT, P.smem, s>>>(a);
+    else if (kind == 1) align_ist_kernel<RPT_S><<<P.grid, AT, P.smem, s>>>(a);
+    else if (kind == 2) align_homotopy_kernel<RPT_S><<<P.grid, AT, P.smem, s>>>(a);
+    else align_gp_kernel<RPT_S><<<P.grid, AT, P.smem, s>>>(a);
+  } else {
+    if (kind == 0) align_palm_kernel<RPT_L><<<P.grid, AT, P.smem, s>>>(a);
+    else if (kind == 1) align_ist_kernel<RPT_L><<<P.grid, AT, P.smem, s>>>(a);
+    else if (kind == 2) align_homotopy_kernel<RPT_L><<<P.grid, AT, P.smem, s>>>(a);
+    else align_gp_kernel<RPT_L><<<P.grid, AT, P.smem, s>>>(a);
+  }
   return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
 }
 
@@ -827,7 +860,7 @@ int launch_align(int kind, const ell1_align_t* A, void* stream) {
 }  // namespace ell1
 
 extern "C" size_t ell1_align_stage_bytes(int32_t kind, int32_t count, int32_t d, int32_t m) {
-  if (kind < 0 || kind > 3 || count <= 0 || m < 1 || m > ell1::MAXM || d <= m || d > ell1::AT * ell1::RPT) return 0;
+  if (kind < 0 || kind > 3 || count <= 0 || m < 1 || m > ell1::MAXM || d <= m || d > ell1::MAXD) return 0;
   ell1::AlignPlan P;
   if (!ell1::align_plan(kind, count, d, m, P)) return 0;
   return P.stage;
@@ -842,6 +875,8 @@ extern "C" int ell1_align_ist_step(int32_t d, int32_t m, const double* B, int64_
                                                                         e_next);
   return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
 }
+
+extern "C" void ell1_test_align_large_rows(int32_t on) { ell1::g_force_large = on != 0; }
 
 extern "C" int ell1_align_palm_batch(const ell1_align_t* A, void* stream) {
   return ell1::launch_align(0, A, stream);

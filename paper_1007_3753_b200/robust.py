@@ -278,8 +278,8 @@ def align_batch_device(kind, Bd, bd, config, lam=None, v0=None):
     count, d, m = (int(x) for x in Bd.shape)
     if d <= m:
         raise ValueError("B must be tall: more rows than columns")
-    if m > 32 or d > 2048:
-        raise ValueError("batched alignment supports m <= 32 parameters and d <= 2048 rows")
+    if m > 32 or d > 8192:
+        raise ValueError("device alignment supports m <= 32 parameters and d <= 8192 rows")
     dev = Bd.device
     Bd = Bd.to(torch.float64).contiguous()
     bd = bd.to(device=dev, dtype=torch.float64).contiguous()

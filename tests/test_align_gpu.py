@@ -132,7 +132,7 @@ def test_ist_block_step_matches_reference_formula():
         ist_block_step(B, b, w, e, lam, 0.0)
 
 
-@pytest.mark.parametrize("d,m", [(1024, 32), (2048, 16)])
+@pytest.mark.parametrize("d,m", [(1024, 32), (2048, 16), (2304, 8), (5000, 6)])
 def test_align_large_images_stage_b_in_global_memory(d, m):
     """Images whose (d+1) m doubles exceed the SM's shared memory:
     B is staged in global memory; results equal the numpy PALM restatement."""
@@ -149,3 +149,27 @@ def test_align_large_images_stage_b_in_global_memory(d, m):
         w_ref, e_ref = align_palm(Bs[j], bs[j], tol=1e-8, max_iter=5000)
         assert _rel(W[j], w_ref) <= 1e-9
         assert _rel(E[j], e_ref) <= 1e-9
+
+
+@pytest.mark.parametrize("solver", ["palm", "ist", "homotopy", "gp"])
+def test_large_image_variant_bit_identical(solver):
+    """The large-image kernels (32 rows per thread, d <= 8192; ADVICE r01:
+    the reference accepts any tall B) forced onto the golden cases give the
+    same bits as the default variant: same row map and accumulation order."""
+    _cuda()
+    from paper_1007_3753_b200 import _lib, robust
+    from paper_1007_3753_b200.model import SolverConfig
+    insts = [align_instance(seed=700 + j, d=120, m=11, frac=0.1) for j in range(4)]
+    Bs = np.stack([B for B, _ in insts])
+    bs = np.stack([b for _, b in insts])
+    cfg = SolverConfig(tol=1e-8, max_iter=5000)
+    lam = 0.05 if solver in ("ist", "gp") else None
+    L = _lib.lib()
+    try:
+        W0, E0, I0 = robust._align_batch(solver, Bs, bs, cfg, lam)
+        L.ell1_test_align_large_rows(1)
+        W1, E1, I1 = robust._align_batch(solver, Bs, bs, cfg, lam)
+    finally:
+        L.ell1_test_align_large_rows(0)
+    assert np.array_equal(I0, I1)
+    assert np.array_equal(W0, W1) and np.array_equal(E0, E1)
