@@ -17,6 +17,7 @@
 // fp32 dictionaries are widened once to fp64 (the path's breakpoint tests
 // are exact comparisons; every product runs in fp64).
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 #include "batched.cuh"
 #include "factor.cuh"
@@ -25,14 +26,12 @@
 
 namespace ell1 {
 
-// Threads per instance CTA.  Measured at config 5 (B=256): 512 beats 128 —
+// Threads per instance CTA (NT, picked per round by hb_threads).  Measured at config 5 (B=256): 512 beats 128 —
 // the row / column sweeps of an instance dominate its dependent chains, and
 // two 512-thread CTAs per SM already hold every instance of a 296-wide wave.
-constexpr int HBT = 512;
-constexpr int HBW = HBT / 32;
 
 // fixed-order CTA reduction of K values (sum / max by mask); all threads get them
-template <int K>
+template <int K, int NT>
 __device__ __forceinline__ void hb_reduce(double (&v)[K], unsigned maxmask, double* sh) {
 #pragma unroll
   for (int k = 0; k < K; ++k) v[k] = ((maxmask >> k) & 1u) ? warp_max(v[k]) : warp_sum(v[k]);
@@ -44,7 +43,7 @@ __device__ __forceinline__ void hb_reduce(double (&v)[K], unsigned maxmask, doub
   for (int k = 0; k < K; ++k) {
     const bool mx = (maxmask >> k) & 1u;
     double s = sh[k];
-    for (int w = 1; w < HBW; ++w) s = mx ? nmax(s, sh[w * K + k]) : s + sh[w * K + k];
+    for (int w = 1; w < (NT / 32); ++w) s = mx ? nmax(s, sh[w * K + k]) : s + sh[w * K + k];
     v[k] = s;
   }
   __syncthreads();
@@ -85,6 +84,7 @@ __device__ __forceinline__ void argmin_pair(double& v, int& i, double v2, int i2
 }
 
 // CTA argmin of (value, index): smallest value, lowest index among ties
+template <int NT>
 __device__ void cta_argmin(double& v, int& i, double* shv, int* shi) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -95,18 +95,19 @@ __device__ void cta_argmin(double& v, int& i, double* shv, int* shi) {
   if (lnx() == 0) { shv[wpx()] = v; shi[wpx()] = i; }
   __syncthreads();
   v = shv[0]; i = shi[0];
-  for (int w = 1; w < HBW; ++w) argmin_pair(v, i, shv[w], shi[w]);
+  for (int w = 1; w < (NT / 32); ++w) argmin_pair(v, i, shv[w], shi[w]);
   __syncthreads();
 }
 
 // Dense upper Cholesky of A_I^T A_I (+ shift I) with the Gram rows formed on
 // the fly (row k: one warp per column, lanes over the d rows): no m x m
 // scratch.  numpy.linalg.cholesky semantics; false when not PD.
+template <int NT>
 __device__ bool gram_chol(const HB& a, const int* sup, int m, double shift, double* R, int ldr,
                           double* row, double* sc) {
   for (int k = 0; k < m; ++k) {
     const double* ak = a.A + (int64_t)sup[k] * a.ld;
-    for (int j = k + wpx(); j < m; j += HBW) {
+    for (int j = k + wpx(); j < m; j += (NT / 32)) {
       const double* aj = a.A + (int64_t)sup[j] * a.ld;
       double acc = 0.0;
       for (int64_t i = lnx(); i < a.d; i += 32) acc = fma(ak[i], aj[i], acc);
@@ -122,7 +123,7 @@ __device__ bool gram_chol(const HB& a, const int* sup, int m, double shift, doub
     __syncthreads();
     if (!(sc[0] > 0.0)) return false;
     const double rkk = sqrt(sc[0]);
-    for (int j = k + tix(); j < m; j += HBT) {
+    for (int j = k + tix(); j < m; j += NT) {
       if (j == k) { R[(size_t)k * ldr + k] = rkk; continue; }
       double s = row[j];
       for (int i = 0; i < k; ++i) s -= R[(size_t)i * ldr + k] * R[(size_t)i * ldr + j];
@@ -134,9 +135,10 @@ __device__ bool gram_chol(const HB& a, const int* sup, int m, double shift, doub
 }
 
 // ridge factor (homotopy.py:118-125): G + 1e-12 max(tr G, 1) I
+template <int NT>
 __device__ bool ridge_chol(const HB& a, const int* sup, int m, double* R, int ldr, double* row, double* sc) {
   double tr[1] = {0.0};
-  for (int p = wpx(); p < m; p += HBW) {
+  for (int p = wpx(); p < m; p += (NT / 32)) {
     const double* ap = a.A + (int64_t)sup[p] * a.ld;
     double acc = 0.0;
     for (int64_t i = lnx(); i < a.d; i += 32) acc = fma(ap[i], ap[i], acc);
@@ -151,33 +153,34 @@ __device__ bool ridge_chol(const HB& a, const int* sup, int m, double* R, int ld
   }
   __syncthreads();
   (void)tr;
-  return gram_chol(a, sup, m, sc[3], R, ldr, row, sc);
+  return gram_chol<NT>(a, sup, m, sc[3], R, ldr, row, sc);
 }
 
 // sum_p A[sup[p], i] * w[p] in support order (same rounding as the plain
-// loop), 8 column loads in flight per thread
+// loop), 16 column loads in flight per thread
 __device__ __forceinline__ double sup_dot(const double* A, int64_t ld, const int* sup, int m, int64_t i,
                                           const double* w) {
   double acc = 0.0;
   int p = 0;
-  for (; p + 8 <= m; p += 8) {
-    double av[8];
+  for (; p + 16 <= m; p += 16) {
+    double av[16];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) av[u] = A[(int64_t)sup[p + u] * ld + i];
+    for (int u = 0; u < 16; ++u) av[u] = A[(int64_t)sup[p + u] * ld + i];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc = fma(av[u], w[p + u], acc);
+    for (int u = 0; u < 16; ++u) acc = fma(av[u], w[p + u], acc);
   }
   for (; p < m; ++p) acc = fma(A[(int64_t)sup[p] * ld + i], w[p], acc);
   return acc;
 }
 
 // ---- setup: lambda0, first atom (homotopy.py:142-177); C holds A^T b (slot = instance)
-__global__ void __launch_bounds__(HBT) hb_init(HB a, int B) {
+template <int NT>
+__global__ void __launch_bounds__(NT) hb_init(HB a, int B) {
   const int j = blockIdx.x;
   if (j >= B) return;
-  __shared__ double sh[HBW * 4 + 8];
-  __shared__ double shv[HBW];
-  __shared__ int shi[HBW];
+  __shared__ double sh[(NT / 32) * 4 + 8];
+  __shared__ double shv[(NT / 32)];
+  __shared__ int shi[(NT / 32)];
   HI& S = a.st[j];
   const double* c = a.C + (int64_t)j * a.n;
   double* X = a.X + (int64_t)j * a.n;
@@ -185,19 +188,19 @@ __global__ void __launch_bounds__(HBT) hb_init(HB a, int B) {
   int* pos = a.posof + (int64_t)j * a.n;
   const double* b = a.Bm + (int64_t)j * a.ld;
   double v[2] = {0.0, 0.0};
-  for (int64_t k = tix(); k < a.n; k += HBT) {
+  for (int64_t k = tix(); k < a.n; k += NT) {
     const double ck = c[k];
     Ci[k] = ck; X[k] = 0.0; pos[k] = -1;
     v[0] = nmax(v[0], fabs(ck));
   }
-  for (int64_t i = tix(); i < a.d; i += HBT) v[1] += b[i] * b[i];
-  hb_reduce<2>(v, 1u, sh);
+  for (int64_t i = tix(); i < a.d; i += NT) v[1] += b[i] * b[i];
+  hb_reduce<2, NT>(v, 1u, sh);
   const double lam0 = v[0];
   double bv = INFINITY;
   int bi = 0x7fffffff;
-  for (int64_t k = tix(); k < a.n; k += HBT)
+  for (int64_t k = tix(); k < a.n; k += NT)
     if (fabs(c[k]) == lam0) argmin_pair(bv, bi, 0.0, (int)k);
-  cta_argmin(bv, bi, shv, shi);
+  cta_argmin<NT>(bv, bi, shv, shi);
   const double bn = sqrt(v[1]);
   if (lam0 <= a.target || lam0 == 0.0) {                 // homotopy.py:161-166
     T0 {
@@ -214,8 +217,8 @@ __global__ void __launch_bounds__(HBT) hb_init(HB a, int B) {
   // first atom: R = [||a_j0||]
   const double* col = a.A + (int64_t)bi * a.ld;
   double q[1] = {0.0};
-  for (int64_t i = tix(); i < a.d; i += HBT) q[0] += col[i] * col[i];
-  hb_reduce<1>(q, 0u, sh);
+  for (int64_t i = tix(); i < a.d; i += NT) q[0] += col[i] * col[i];
+  hb_reduce<1, NT>(q, 0u, sh);
   T0 {
     S.lam = lam0; S.lam0 = lam0; S.floor = pymax(a.target, 1e-12 * lam0);
     S.it = 0; S.m = 1; S.conv = 0; S.done = 0; S.note = 0; S.pend = 0; S.redo = 0; S.ridge = 0;
@@ -229,11 +232,12 @@ __global__ void __launch_bounds__(HBT) hb_init(HB a, int B) {
 }
 
 // ---- finalise the previous breakpoint, then the direction of the next one
-__global__ void __launch_bounds__(HBT) hb_dir(HB a, int nact) {
+template <int NT>
+__global__ void __launch_bounds__(NT) hb_dir(HB a, int nact) {
   const int s = blockIdx.x;
   if (s >= nact) return;
   extern __shared__ __align__(16) double dsm[];
-  __shared__ double sh[HBW * 4 + 8];
+  __shared__ double sh[(NT / 32) * 4 + 8];
   __shared__ int flag;
   const int j = a.act[s];
   HI& S = a.st[j];
@@ -246,12 +250,12 @@ __global__ void __launch_bounds__(HBT) hb_dir(HB a, int nact) {
     // fresh correlations (homotopy.py:224-234)
     const double* c = a.C + (int64_t)s * a.n;
     double v[1] = {0.0};
-    for (int64_t k = tix(); k < a.n; k += HBT) {
+    for (int64_t k = tix(); k < a.n; k += NT) {
       const double ck = c[k];
       Ci[k] = ck;
       v[0] = nmax(v[0], fabs(ck));
     }
-    hb_reduce<1>(v, 1u, sh);
+    hb_reduce<1, NT>(v, 1u, sh);
     T0 {
       double lam;
       if (S.finish) lam = a.target;
@@ -281,20 +285,20 @@ __global__ void __launch_bounds__(HBT) hb_dir(HB a, int nact) {
   }
   __syncthreads();
   if (flag) {
-    for (int64_t i = tix(); i < a.ld; i += HBT) Vs[i] = 0.0;
+    for (int64_t i = tix(); i < a.ld; i += NT) Vs[i] = 0.0;
     return;
   }
   const int m = S.m;
   const int* sup = a.sup + (size_t)j * a.mmax;
   const double* R = a.R + (size_t)j * a.mmax * a.mmax;
   double* dI = a.dI + (size_t)j * a.mmax;
-  for (int p = tix(); p < m; p += HBT) zs[p] = sgn(Ci[sup[p]]);
+  for (int p = tix(); p < m; p += NT) zs[p] = sgn(Ci[sup[p]]);
   __syncthreads();
-  trsv_RT<HBT>(R, ldr, m, zs, tile);
-  trsv_R<HBT>(R, ldr, m, zs, tile);
-  for (int p = tix(); p < m; p += HBT) dI[p] = zs[p];
+  trsv_RT<NT>(R, ldr, m, zs, tile);
+  trsv_R<NT>(R, ldr, m, zs, tile);
+  for (int p = tix(); p < m; p += NT) dI[p] = zs[p];
   // v = A_I d_I (rows over threads, support columns in order)
-  for (int64_t i = tix(); i < a.ld; i += HBT) {
+  for (int64_t i = tix(); i < a.ld; i += NT) {
     double acc = 0.0;
     if (i < a.d)
       acc = sup_dot(a.A, a.ld, sup, m, i, zs);
@@ -303,13 +307,14 @@ __global__ void __launch_bounds__(HBT) hb_dir(HB a, int nact) {
 }
 
 // ---- drift check, step lengths, event, factor update, residual
-__global__ void __launch_bounds__(HBT) hb_step(HB a, int nact) {
+template <int NT>
+__global__ void __launch_bounds__(NT) hb_step(HB a, int nact) {
   const int s = blockIdx.x;
   if (s >= nact) return;
   extern __shared__ __align__(16) double dsm[];
-  __shared__ double sh[HBW * 8 + 16];
-  __shared__ double shv[HBW];
-  __shared__ int shi[HBW];
+  __shared__ double sh[(NT / 32) * 8 + 16];
+  __shared__ double shv[(NT / 32)];
+  __shared__ int shi[(NT / 32)];
   __shared__ double sc[4];
   __shared__ int dec[4];               // 0: refactor, 1: event(0 add / 1 remove / 2 finish), 2: ip, 3: im
   const int j = a.act[s];
@@ -328,7 +333,7 @@ __global__ void __launch_bounds__(HBT) hb_step(HB a, int nact) {
   const double* dI = a.dI + (size_t)j * a.mmax;
   const double* b = a.Bm + (int64_t)j * a.ld;
   if (S.done) {
-    for (int64_t i = tix(); i < a.ld; i += HBT) Rs[i] = 0.0;
+    for (int64_t i = tix(); i < a.ld; i += NT) Rs[i] = 0.0;
     return;
   }
   const int m = S.m;
@@ -336,13 +341,13 @@ __global__ void __launch_bounds__(HBT) hb_step(HB a, int nact) {
   // drift ||w_I - sgn||, ||sgn|| (homotopy.py:48-52; w_I == A_I^T v)
   {
     double q[2] = {0.0, 0.0};
-    for (int p = tix(); p < m; p += HBT) {
+    for (int p = tix(); p < m; p += NT) {
       const double sg = sgn(Ci[sup[p]]);
       const double e = w[sup[p]] - sg;
       q[0] += e * e;
       q[1] += sg * sg;
     }
-    hb_reduce<2>(q, 0u, sh);
+    hb_reduce<2, NT>(q, 0u, sh);
     T0 {
       const double tol = 1e-6 * pymax(1.0, sqrt(q[1]));
       dec[0] = (!(sqrt(q[0]) <= tol) && S.ridge != 2) ? 1 : 0;
@@ -352,18 +357,18 @@ __global__ void __launch_bounds__(HBT) hb_step(HB a, int nact) {
   if (dec[0]) {
     // dense refactorisation; a second failure (or a singular Gram) -> ridge
     bool ok = false;
-    if (S.ridge == 0) ok = gram_chol(a, sup, m, 0.0, R, ldr, row, sc);
+    if (S.ridge == 0) ok = gram_chol<NT>(a, sup, m, 0.0, R, ldr, row, sc);
     if (ok) {
       T0 S.ridge = 1;
     } else {
-      const bool ok2 = ridge_chol(a, sup, m, R, ldr, row, sc);
+      const bool ok2 = ridge_chol<NT>(a, sup, m, R, ldr, row, sc);
       T0 {
         S.ridge = 2; S.note = 1;
         if (!ok2) { S.status = ELL1_NOT_PD; S.done = 1; }
       }
     }
     T0 S.redo = 1;
-    for (int64_t i = tix(); i < a.ld; i += HBT) Rs[i] = 0.0;
+    for (int64_t i = tix(); i < a.ld; i += NT) Rs[i] = 0.0;
     return;
   }
   // step lengths (homotopy.py:78-105): gamma+ over the inactive set, gamma- over the support
@@ -371,7 +376,7 @@ __global__ void __launch_bounds__(HBT) hb_step(HB a, int nact) {
     const double floor = 1e-10 * pymax(lam, 1e-30);
     double v1 = INFINITY, v2 = INFINITY, vm = INFINITY;
     int i1 = 0x7fffffff, i2 = 0x7fffffff, im = 0x7fffffff;
-    for (int64_t k = tix(); k < a.n; k += HBT) {
+    for (int64_t k = tix(); k < a.n; k += NT) {
       const int p = pos[k];
       const double wk = w[k];
       if (p >= 0) {
@@ -385,9 +390,9 @@ __global__ void __launch_bounds__(HBT) hb_step(HB a, int nact) {
         if (isfinite(r2) && r2 > floor) argmin_pair(v2, i2, r2, (int)k);
       }
     }
-    cta_argmin(v1, i1, shv, shi);
-    cta_argmin(v2, i2, shv, shi);
-    cta_argmin(vm, im, shv, shi);
+    cta_argmin<NT>(v1, i1, shv, shi);
+    cta_argmin<NT>(v2, i2, shv, shi);
+    cta_argmin<NT>(vm, im, shv, shi);
     T0 {
       double gp = v1;
       int ip = isfinite(v1) ? i1 : -1;
@@ -410,7 +415,7 @@ __global__ void __launch_bounds__(HBT) hb_step(HB a, int nact) {
   }
   const double gamma = sc[0];
   const int ev = dec[1];
-  for (int p = tix(); p < m; p += HBT) X[sup[p]] = X[sup[p]] + gamma * dI[p];
+  for (int p = tix(); p < m; p += NT) X[sup[p]] = X[sup[p]] + gamma * dI[p];
   __syncthreads();
   int mn = m;
   if (ev == 1) {
@@ -420,7 +425,7 @@ __global__ void __launch_bounds__(HBT) hb_step(HB a, int nact) {
     T0 X[im] = 0.0;
     // rows above: shift columns > p0 left — a warp per row, each 32-column
     // chunk read before any lane writes (row-local, so rows run in parallel)
-    for (int i = wpx(); i < p0; i += HBW) {
+    for (int i = wpx(); i < p0; i += (NT / 32)) {
       double* Ri = R + (size_t)i * ldr;
       for (int j0 = p0 + 1; j0 < m; j0 += 32) {
         const int jj = j0 + lnx();
@@ -433,9 +438,9 @@ __global__ void __launch_bounds__(HBT) hb_step(HB a, int nact) {
     __syncthreads();
     if (p0 < m - 1) {
       const int mt = m - p0 - 1;
-      for (int jj = tix(); jj < mt; jj += HBT) zs[jj] = R[(size_t)p0 * ldr + p0 + 1 + jj];
+      for (int jj = tix(); jj < mt; jj += NT) zs[jj] = R[(size_t)p0 * ldr + p0 + 1 + jj];
       __syncthreads();
-      chol_update_shift<HBT>(R, ldr, p0 + 1, p0, mt, zs, sc);
+      chol_update_shift<NT>(R, ldr, p0 + 1, p0, mt, zs, sc);
     }
     T0 {
       for (int p = p0; p < m - 1; ++p) { const int c = sup[p + 1]; sup[p] = c; pos[c] = p; }
@@ -446,7 +451,7 @@ __global__ void __launch_bounds__(HBT) hb_step(HB a, int nact) {
     // add ip: chol_append (numerics.py:115-137); NotPD -> ridge over the grown support
     const int ip = dec[2];
     const double* acol = a.A + (int64_t)ip * a.ld;
-    for (int p = wpx(); p < m; p += HBW) {
+    for (int p = wpx(); p < m; p += (NT / 32)) {
       const double* ap = a.A + (int64_t)sup[p] * a.ld;
       double acc = 0.0;
       for (int64_t i = lnx(); i < a.d; i += 32) acc = fma(ap[i], acol[i], acc);
@@ -454,16 +459,16 @@ __global__ void __launch_bounds__(HBT) hb_step(HB a, int nact) {
       if (lnx() == 0) zs[p] = acc;
     }
     double q[1] = {0.0};
-    for (int64_t i = tix(); i < a.d; i += HBT) q[0] += acol[i] * acol[i];
-    hb_reduce<1>(q, 0u, sh);
-    trsv_RT<HBT>(R, ldr, m, zs, tile);
+    for (int64_t i = tix(); i < a.d; i += NT) q[0] += acol[i] * acol[i];
+    hb_reduce<1, NT>(q, 0u, sh);
+    trsv_RT<NT>(R, ldr, m, zs, tile);
     double uu[1] = {0.0};
-    for (int p = tix(); p < m; p += HBT) uu[0] += zs[p] * zs[p];
-    hb_reduce<1>(uu, 0u, sh);
+    for (int p = tix(); p < m; p += NT) uu[0] += zs[p] * zs[p];
+    hb_reduce<1, NT>(uu, 0u, sh);
     const double d2 = q[0] - uu[0];
     const bool fits = m < ldr;
     if (d2 > 0.0 && fits) {
-      for (int p = tix(); p < m; p += HBT) R[(size_t)p * ldr + m] = zs[p];
+      for (int p = tix(); p < m; p += NT) R[(size_t)p * ldr + m] = zs[p];
       T0 {
         R[(size_t)m * ldr + m] = sqrt(d2);
         sup[m] = ip; pos[ip] = m;
@@ -475,7 +480,7 @@ __global__ void __launch_bounds__(HBT) hb_step(HB a, int nact) {
     } else {
       T0 { sup[m] = ip; pos[ip] = m; }
       __syncthreads();
-      const bool ok2 = ridge_chol(a, sup, m + 1, R, ldr, row, sc);
+      const bool ok2 = ridge_chol<NT>(a, sup, m + 1, R, ldr, row, sc);
       T0 { S.note = 1; if (!ok2) { S.status = ELL1_NOT_PD; S.done = 1; } }
     }
     if (fits) mn = m + 1;
@@ -483,10 +488,10 @@ __global__ void __launch_bounds__(HBT) hb_step(HB a, int nact) {
   __syncthreads();
   T0 S.m = mn;
   // r = b - A_I x_I, ||r||^2, ||x||_1, max|x|, support count (homotopy.py:224-226)
-  for (int p = tix(); p < mn; p += HBT) row[p] = X[sup[p]];
+  for (int p = tix(); p < mn; p += NT) row[p] = X[sup[p]];
   __syncthreads();
   double q3[3] = {0.0, 0.0, 0.0};
-  for (int64_t i = tix(); i < a.ld; i += HBT) {
+  for (int64_t i = tix(); i < a.ld; i += NT) {
     double r = 0.0;
     if (i < a.d) {
       double acc = 0.0;
@@ -496,12 +501,12 @@ __global__ void __launch_bounds__(HBT) hb_step(HB a, int nact) {
     }
     Rs[i] = r;
   }
-  for (int64_t k = tix(); k < a.n; k += HBT) { const double xk = fabs(X[k]); q3[1] += xk; q3[2] = nmax(q3[2], xk); }
-  hb_reduce<3>(q3, 0x4u, sh);
+  for (int64_t k = tix(); k < a.n; k += NT) { const double xk = fabs(X[k]); q3[1] += xk; q3[2] = nmax(q3[2], xk); }
+  hb_reduce<3, NT>(q3, 0x4u, sh);
   const double cut = 1e-10 * pymax(q3[2], 1.0);
   double c1[1] = {0.0};
-  for (int64_t k = tix(); k < a.n; k += HBT) if (fabs(X[k]) > cut) c1[0] += 1.0;
-  hb_reduce<1>(c1, 0u, sh);
+  for (int64_t k = tix(); k < a.n; k += NT) if (fabs(X[k]) > cut) c1[0] += 1.0;
+  hb_reduce<1, NT>(c1, 0u, sh);
   T0 { S.rr = q3[0]; S.l1 = q3[1]; S.top = q3[2]; S.cnt = c1[0]; S.pend = 1; }
 }
 
@@ -556,6 +561,39 @@ __global__ void hb_out(HB a, int B, double* x, int32_t* its, int32_t* conv, int3
 __global__ void widen_kernel(const float* src, double* dst, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = (double)src[i];
+}
+
+template <int NT>
+bool hb_smem_attr(size_t smem) {
+  return cudaFuncSetAttribute(hb_dir<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
+         cudaFuncSetAttribute(hb_step<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
+}
+
+// threads per instance for a round of nact instances
+int hb_threads(int nact) {
+  static int force = -1;
+  if (force < 0) {
+    const char* e = getenv("ELL1_HB_NT");                  // diagnostics: 128 / 256 / 512
+    force = e ? atoi(e) : 0;
+  }
+  if (force == 128 || force == 256 || force == 512) return force;
+  // few instances: wide CTAs shorten each instance's sweeps; many: narrow CTAs
+  // keep more instances resident so their dependent chains overlap
+  // (tools/hb_nt_ab.py: B=256 512 > 256 > 128; B=4096 128 > 256 > 512)
+  return nact > 2048 ? 128 : nact > 512 ? 256 : 512;
+}
+
+void hb_launch(int which, int nt, int nact, size_t smem, cudaStream_t s, const HB& a) {
+  if (nt == 128) {
+    if (which == 0) hb_dir<128><<<nact, 128, smem, s>>>(a, nact);
+    else hb_step<128><<<nact, 128, smem, s>>>(a, nact);
+  } else if (nt == 256) {
+    if (which == 0) hb_dir<256><<<nact, 256, smem, s>>>(a, nact);
+    else hb_step<256><<<nact, 256, smem, s>>>(a, nact);
+  } else {
+    if (which == 0) hb_dir<512><<<nact, 512, smem, s>>>(a, nact);
+    else hb_step<512><<<nact, 512, smem, s>>>(a, nact);
+  }
 }
 
 inline bool dgemm_AtX(cudaStream_t st, const HB& a, const double* X, double* Y, int B) {
@@ -637,7 +675,7 @@ extern "C" int ell1_batch_homotopy(const ell1_dict_t* D, const double* Bmat, int
   if (cudaMemcpyAsync(Bm, Bmat, ld * B * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return ELL1_ERR_CUDA;
   // c = A^T b for every instance, then lambda0 / first atom
   if (!dgemm_AtX(s, a, Bm, a.C, B)) return ELL1_ERR_CUDA;
-  hb_init<<<B, HBT, 0, s>>>(a, B);
+  hb_init<512><<<B, 512, 0, s>>>(a, B);
   // identity active list
   {
     std::vector<int> ident(B);
@@ -647,9 +685,7 @@ extern "C" int ell1_batch_homotopy(const ell1_dict_t* D, const double* Bmat, int
     if (cudaStreamSynchronize(s) != cudaSuccess) return ELL1_ERR_CUDA;
   }
   const size_t smem = (size_t)(HB_SMEM_FIXED + 2 * mm) * 8;
-  if (cudaFuncSetAttribute(hb_dir, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-      cudaFuncSetAttribute(hb_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return ELL1_ERR_CUDA;
+  if (!hb_smem_attr<128>(smem) || !hb_smem_attr<256>(smem) || !hb_smem_attr<512>(smem)) return ELL1_ERR_CUDA;
   int nact = B;
   int* act = act1;
   int* actn = act2;
@@ -658,7 +694,7 @@ extern "C" int ell1_batch_homotopy(const ell1_dict_t* D, const double* Bmat, int
   while (nact > 0) {
     a.act = act;
     a.V = Vcur;
-    hb_dir<<<nact, HBT, smem, s>>>(a, nact);
+    hb_launch(0, hb_threads(nact), nact, smem, s, a);
     // drop finished instances from the GEMM operands
     hb_scan<<<1, 1024, 0, s>>>(a.st, act, nact, perm, ctr);
     int* box = host_mailbox();
@@ -676,7 +712,7 @@ extern "C" int ell1_batch_homotopy(const ell1_dict_t* D, const double* Bmat, int
       a.V = Vcur;
     }
     if (!dgemm_AtX(s, a, a.V, a.W, nact)) return ELL1_ERR_CUDA;
-    hb_step<<<nact, HBT, smem, s>>>(a, nact);
+    hb_launch(1, hb_threads(nact), nact, smem, s, a);
     if (!dgemm_AtX(s, a, a.Rr, a.C, nact)) return ELL1_ERR_CUDA;
   }
   hb_out<<<B, 256, 0, s>>>(a, B, out->x, out->iterations, out->converged, out->status, notes);
