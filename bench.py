@@ -550,6 +550,8 @@ def leg_cfg3(torch, dev, queries=1024):
     # batched iteration at 1024 queries); the identity block costs nothing
     d_, nA = 1024, 1216
     tfl = float(its.sum()) * (4.0 * d_ * nA + 2.0 * d_ * d_) / t / 1e12
+    exec_per = 2.0 * d_ * (nA + d_) + 2.0 * d_ * nA + 2.0 * nA * d_ + 4.0 * d_ * nA
+    tfl_exec = float(its.sum()) * exec_per / t / 1e12
     peaks = gemm_peaks(torch, dev)
     return {"workload": "cfg3: CAB [A I] 1024 x 2240, %d queries, batched DALM fp32 storage, "
                         "tol 1e-4, min-class-residual labels" % queries,
@@ -558,7 +560,13 @@ def leg_cfg3(torch, dev, queries=1024):
                          "peak_source": "cuBLAS TF32 8192^3 (profiles/r02_gemm_peaks.json)",
                          "algorithmic": "SURVEY 8(d): (4 d n_A + 2 d^2) flops per query-iteration, x3 TF32 "
                                         "MMAs per fp32-accurate product",
-                         "fp32_accurate_tflops": tfl},
+                         "fp32_accurate_tflops": tfl,
+                         # the products the batched iteration actually runs (batch_dalm.cu main_part /
+                         # tail_part, fp32 [A, sI]): [M | Ginv] V (K = n_A + d), A Z, A^T Y, A [U | x_new]
+                         "executed_mma_tflops": 3 * tfl_exec,
+                         "executed_frac": 3 * tfl_exec / peaks["tf32_tflops"],
+                         "executed": "2 d (n_A + d) + 2 d n_A + 2 n_A d + 4 d n_A = %.2f MFLOP per "
+                                     "query-iteration (x3 MMAs)" % (exec_per / 1e6)},
             "queries_per_sec": queries / t, "ms_per_batch": 1e3 * t,
             "mean_iterations": float(its.mean()), "max_iterations": int(its.max()),
             "accuracy_vs_truth": float(np.mean(labels == truth)),

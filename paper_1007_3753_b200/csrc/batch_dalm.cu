@@ -28,6 +28,7 @@ struct DI {
 struct BDArgs {
   int64_t d, n, N, ld, ldx;
   int ext, f32, cg;
+  int vec;                   // fp32 storage with even n, d, ld: paired loads / stores in the epilogues
   int fuse_ext;              // fp32 [A, sI]: [M | Ginv] V as one tensor-core GEMM (no GEXT)
   int gcert;                 // certificate from G y (the opts carry G): P2[:, j] = G y_j already
                              // includes the [A, sI] block, only A x_new needs the s x_e term
@@ -54,6 +55,18 @@ struct BDArgs {
   double* trace;            // [B0][max_iter + 1][4]
   int ix, iy;
 };
+
+// paired (16-byte fp64 / 8-byte fp32) accesses of the fp32-storage epilogues
+// (BDArgs::vec: n, d, ld even, so no pair straddles a block boundary)
+__device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ float2 ldf2(const float* p) { return *reinterpret_cast<const float2*>(p); }
+__device__ __forceinline__ void st2(double* p, double u, double v) {
+  *reinterpret_cast<double2*>(p) = make_double2(u, v);
+}
+__device__ __forceinline__ void stf2(float* p, double u, double v) {
+  *reinterpret_cast<float2*>(p) = make_float2((float)u, (float)v);
+}
+__device__ __forceinline__ double clamp1(double t) { return t > 1.0 ? 1.0 : (t < -1.0 ? -1.0 : t); }
 
 __device__ __forceinline__ double bd_rd(const BDArgs& a, const double* p64, const float* p32, int64_t i) {
   return a.f32 ? (double)p32[i] : p64[i];
@@ -100,11 +113,47 @@ __global__ void __launch_bounds__(BT) bd_init(const BDArgs a) {
 }
 
 // z = clamp(A^T y + x/beta), v = z - x/beta (alm.py:239)
+template <bool VEC>
 __global__ void __launch_bounds__(BT) bd_z(const BDArgs a) {
   const int j = blockIdx.x;
   DI& I = a.inst[j];
   if (!I.active) return;
   if (threadIdx.x == 0) { I.it++; I.refine = 0; }
+  if constexpr (VEC) {
+    const int64_t o = (int64_t)j * a.ldx;
+    const double* __restrict__ x = a.X[a.ix] + o;
+    const float* __restrict__ u32 = a.UT32 + (int64_t)j * a.n;
+    const double* __restrict__ ycur = a.Y[a.iy] + (int64_t)j * a.ld;
+    double* __restrict__ zo = a.Z + o;
+    float* __restrict__ v32 = a.V32 + o;
+    float* __restrict__ z32 = a.Z32 + o;
+    const bool fuse = a.fuse_ext;
+    const int64_t n = a.n, h = a.N / 2;
+    const double beta = a.beta, sc = a.s;
+#pragma unroll 4
+    for (int64_t t = threadIdx.x; t < h; t += BT) {
+      const int64_t k = 2 * t;
+      const double2 xx = ld2(x + k);
+      double u0, u1;
+      if (k < n) {
+        const float2 uu = ldf2(u32 + k);
+        u0 = uu.x; u1 = uu.y;
+      } else {
+        const double2 yy = ld2(ycur + (k - n));
+        u0 = sc * yy.x; u1 = sc * yy.y;
+      }
+      const double xb0 = xx.x / beta, xb1 = xx.y / beta;
+      const double z0 = clamp1(u0 + xb0), z1 = clamp1(u1 + xb1);
+      st2(zo + k, z0, z1);
+      if (k < n) {
+        stf2(v32 + k, z0 - xb0, z1 - xb1);
+        stf2(z32 + k, z0, z1);
+      } else if (fuse) {
+        stf2(v32 + k, sc * (z0 - xb0), sc * (z1 - xb1));
+      }
+    }
+    return;
+  }
   const int64_t o = (int64_t)j * a.ldx;
   const double* __restrict__ x = a.X[a.ix] + o;
   const double* __restrict__ u = a.UX + o;
@@ -134,6 +183,7 @@ __global__ void __launch_bounds__(BT) bd_z(const BDArgs a) {
 }
 
 // y = M v + Ginv b / beta; rhs = A z - (A x - b)/beta (alm.py:179-180)
+template <bool VEC>
 __global__ void __launch_bounds__(BT) bd_y(const BDArgs a) {
   const int j = blockIdx.x;
   __shared__ double sh[BW * 2 + 2];
@@ -157,6 +207,28 @@ __global__ void __launch_bounds__(BT) bd_y(const BDArgs a) {
   const bool f32 = a.f32, addg = a.ext && !a.fuse_ext, ext = a.ext;
   const double beta = a.beta, sc = a.s;
   double q[2] = {0.0, 0.0};
+  if constexpr (VEC) {
+    const int64_t h = a.d / 2;
+#pragma unroll 4
+    for (int64_t t = threadIdx.x; t < h; t += BT) {
+      const int64_t i = 2 * t;
+      const float2 m2 = ldf2(p1f + i);
+      double mv0 = m2.x, mv1 = m2.y;
+      if (addg) { const double2 g = ld2(gx + i); mv0 = mv0 + g.x; mv1 = mv1 + g.y; }
+      const double2 c = ld2(c0 + i);
+      const double y0 = mv0 + c.x / beta, y1 = mv1 + c.y / beta;
+      const float2 a2 = ldf2(p2f + i);
+      double az0 = a2.x, az1 = a2.y;
+      if (ext) { const double2 zz = ld2(zx + i); az0 = az0 + sc * zz.x; az1 = az1 + sc * zz.y; }
+      const double2 bb = ld2(b + i), xx = ld2(ax + i);
+      const double r0 = az0 - (xx.x - bb.x) / beta, r1 = az1 - (xx.y - bb.y) / beta;
+      st2(y + i, y0, y1);
+      stf2(y32 + i, y0, y1);
+      st2(rh + i, r0, r1);
+      q[0] += r0 * r0; q[0] += r1 * r1;
+      q[1] += bb.x * y0; q[1] += bb.y * y1;
+    }
+  } else
 #pragma unroll 4
   for (int64_t i = threadIdx.x; i < a.d; i += BT) {
     double mv = f32 ? (double)p1f[i] : p1[i];
@@ -225,6 +297,7 @@ __global__ void __launch_bounds__(BT) bd_yg(const BDArgs a) {
 }
 
 // x_new = x - beta (z - A^T y) (alm.py:245-246); U = A^T y lives in UX[:, j]
+template <bool VEC>
 __global__ void __launch_bounds__(BT) bd_x(const BDArgs a, const double* Ut, const float* Ut32, int refine_only) {
   const int j = blockIdx.x;
   __shared__ double sh[BW * 6 + 6];
@@ -246,6 +319,36 @@ __global__ void __launch_bounds__(BT) bd_x(const BDArgs a, const double* Ut, con
   const int64_t n = a.n;
   const double beta = a.beta, sc = a.s;
   double s[6] = {0, 0, 0, 0, 0, 0};                       // l1, max|Aty|, max|x|, dx2, xp2, -
+  if constexpr (VEC) {
+    const int64_t h = a.N / 2;
+#pragma unroll 4
+    for (int64_t t = threadIdx.x; t < h; t += BT) {
+      const int64_t k = 2 * t;
+      double u0, u1;
+      if (k < n) {
+        const float2 uu = ldf2(ut32 + k);
+        u0 = uu.x; u1 = uu.y;
+      } else {
+        const double2 yy = ld2(y + (k - n));
+        u0 = sc * yy.x; u1 = sc * yy.y;
+      }
+      const double2 xo = ld2(x + k), z2 = ld2(zz + k);
+      const double v0 = xo.x - beta * (z2.x - u0), v1 = xo.y - beta * (z2.y - u1);
+      st2(xw + k, v0, v1);
+      if (k < n) {
+        stf2(ux32 + k, u0, u1);
+        stf2(xn32 + k, v0, v1);
+      }
+      s[0] += fabs(v0); s[0] += fabs(v1);
+      s[1] = nmax(nmax(s[1], fabs(u0)), fabs(u1));
+      s[2] = nmax(nmax(s[2], fabs(v0)), fabs(v1));
+      if (relest) {
+        const double d0 = v0 - xo.x, d1 = v1 - xo.y;
+        s[3] += d0 * d0; s[3] += d1 * d1;
+        s[4] += xo.x * xo.x; s[4] += xo.y * xo.y;
+      }
+    }
+  } else
 #pragma unroll 4
   for (int64_t k = threadIdx.x; k < a.N; k += BT) {
     double uk;
@@ -270,6 +373,7 @@ __global__ void __launch_bounds__(BT) bd_x(const BDArgs a, const double* Ut, con
 }
 
 // certificate, residual, trace, convergence (alm.py:181-188, 249-268)
+template <bool VEC>
 __global__ void __launch_bounds__(BT) bd_c(const BDArgs a, int refine_only) {
   const int j = blockIdx.x;
   const int B = gridDim.x;
@@ -299,6 +403,39 @@ __global__ void __launch_bounds__(BT) bd_c(const BDArgs a, int refine_only) {
     double* __restrict__ axo = a.AX + oj;
     const bool f32 = a.f32, ext = a.ext;
     const double sc = a.s;
+    if constexpr (VEC) {
+      const int64_t h = a.d / 2;
+      const bool gc = a.gcert;
+#pragma unroll 4
+      for (int64_t t = threadIdx.x; t < h; t += BT) {
+        const int64_t i = 2 * t;
+        const float2 u2 = ldf2(pu + i), x2 = ldf2(px + i);
+        double au0 = u2.x, au1 = u2.y, ax0 = x2.x, ax1 = x2.y;
+        if (ext) {
+          if (!gc) {
+            const double2 yy = ld2(yn + i);
+            au0 = au0 + sc * (sc * yy.x); au1 = au1 + sc * (sc * yy.y);
+          }
+          const double2 xx = ld2(xe + i);
+          ax0 = ax0 + sc * xx.x; ax1 = ax1 + sc * xx.y;
+        }
+        const double2 r2 = ld2(rh + i), b2 = ld2(bb + i);
+        const double e0 = r2.x - au0, e1 = r2.y - au1;
+        st2(res + i, e0, e1);
+        st2(axo + i, ax0, ax1);
+        const double q0 = b2.x - ax0, q1 = b2.y - ax1;
+        q[0] += e0 * e0; q[0] += e1 * e1;
+        q[1] += q0 * q0; q[1] += q1 * q1;
+      }
+      const double* __restrict__ xs = xn;
+      const int64_t hN = a.N / 2;
+#pragma unroll 4
+      for (int64_t t = threadIdx.x; t < hN; t += BT) {
+        const double2 v = ld2(xs + 2 * t);
+        if (fabs(v.x) > cut) q[2] += 1.0;
+        if (fabs(v.y) > cut) q[2] += 1.0;
+      }
+    } else {
 #pragma unroll 4
     for (int64_t i = threadIdx.x; i < a.d; i += BT) {
       double aau = f32 ? (double)pu[i] : pu64[i];
@@ -317,6 +454,7 @@ __global__ void __launch_bounds__(BT) bd_c(const BDArgs a, int refine_only) {
     const double* __restrict__ xs = xn;
 #pragma unroll 4
     for (int64_t k = threadIdx.x; k < a.N; k += BT) if (fabs(xs[k]) > cut) q[2] += 1.0;
+    }
   }
   cta_reduce<3>(q, 0u, sh);
   if (threadIdx.x == 0) {
@@ -518,6 +656,7 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   BDArgs a;
   a.d = d; a.n = D->n; a.N = N; a.ld = ld; a.ldx = ldx;
   a.ext = D->ext; a.f32 = D->dtype == ELL1_F32; a.cg = O->y_cg_step; a.fuse_ext = 0;
+  a.vec = a.f32 && D->n % 2 == 0 && D->d % 2 == 0 && D->ld % 2 == 0;
   a.gcert = O->G != nullptr;
   a.s = D->ext_scale; a.beta = O->beta; a.ytol = O->y_tol;
   a.C = *C;
@@ -603,7 +742,8 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
     if (!gemm_AtR(ks, D, aa.f32 ? (const void*)aa.Y32 : (const void*)aa.Y[aa.iy ^ 1], ld, Ut, D->n, Bc, pA))
       return false;
     // [U | x_new] for the Bc instances: the x_new block starts at column Bc
-    bd_x<<<Bc, BT, 0, ks>>>(aa, (const double*)Ut, (const float*)Ut, refine_only);
+    if (aa.vec) bd_x<true><<<Bc, BT, 0, ks>>>(aa, (const double*)Ut, (const float*)Ut, refine_only);
+    else bd_x<false><<<Bc, BT, 0, ks>>>(aa, (const double*)Ut, (const float*)Ut, refine_only);
     if (aa.gcert) {
       // certificate A A^T y as G y (d^2 per instance instead of d n) and A x_new
       if (aa.f32) {
@@ -619,12 +759,14 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
       if (!gemm_AX(ks, D, aa.UX, ldx, aa.P2, ld, 2 * Bc)) return false;
     }
     if (cudaMemsetAsync(ctr, 0, 4, ks) != cudaSuccess) return false;
-    bd_c<<<Bc, BT, 0, ks>>>(aa, refine_only);
+    if (aa.vec) bd_c<true><<<Bc, BT, 0, ks>>>(aa, refine_only);
+    else bd_c<false><<<Bc, BT, 0, ks>>>(aa, refine_only);
     return cudaGetLastError() == cudaSuccess;
   };
   // one iteration up to the certificate (bd_c raises ctr[0] refine flags)
   auto main_part = [&](const BDArgs& aa, int Bc) -> bool {
-    bd_z<<<Bc, BT, 0, ks>>>(aa);
+    if (aa.vec) bd_z<true><<<Bc, BT, 0, ks>>>(aa);
+    else bd_z<false><<<Bc, BT, 0, ks>>>(aa);
     if (!aa.f32) {
       // y = G^-1 rhs (dual_y_solve's cho_solve, alm.py:179-180) on the DMMA path
       if (!gemm_AX(ks, D, aa.Z, ldx, aa.P2, ld, Bc)) return false;
@@ -647,7 +789,8 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
       // identity block of M: s Ginv v_ext (s folded into v_ext by bd_z)
       if (!dgemm(0, 0, ld, Bc, d, O->Ginv, ld, aa.V + D->n, ldx, aa.GEXT, ld, ks)) return false;
     }
-    bd_y<<<Bc, BT, 0, ks>>>(aa);
+    if (aa.vec) bd_y<true><<<Bc, BT, 0, ks>>>(aa);
+    else bd_y<false><<<Bc, BT, 0, ks>>>(aa);
     return tail_part(aa, Bc, 0);
   };
   // y += Ginv resid for the flagged instances (alm.py:184), then their certificate again
