@@ -46,6 +46,8 @@ struct BDArgs {
   double* P1; double* P2;   // GEMM outputs ld x B / ld x 2B (fp64)
   double* GEXT;             // ld x B (Ginv v_ext)
   float* V32; float* Z32; float* UX32; float* Y32; float* P1f; float* P2f; float* P3f;
+  float* V32l; float* Z32l; float* UX32l; float* Y32l;   // pre: lo halves (the arrays above hold rna_tf32 hi)
+  int pre;                   // vec path writes the GEMM operands pre-split (3xTF32 hi / lo, no in-GEMM split)
   float* UT32;               // fp32 storage: U = A^T y (n x B, pitch n), the GEMM output itself;
                              // the fp64 copies of U and x_new in UX are then not kept
   DI* inst;
@@ -65,6 +67,18 @@ __device__ __forceinline__ void st2(double* p, double u, double v) {
 }
 __device__ __forceinline__ void stf2(float* p, double u, double v) {
   *reinterpret_cast<float2*>(p) = make_float2((float)u, (float)v);
+}
+// GEMM operand pair store: plain fp32, or the 3xTF32 split (hi = rna_tf32(x),
+// lo = rna_tf32(x - hi): the same bits as the GEMM's in-kernel split)
+__device__ __forceinline__ void stf2s(float* h, float* l, bool pre, double u, double v) {
+  const float fu = (float)u, fv = (float)v;
+  if (!pre) {
+    *reinterpret_cast<float2*>(h) = make_float2(fu, fv);
+    return;
+  }
+  const float hu = tf32_rna(fu), hv = tf32_rna(fv);
+  *reinterpret_cast<float2*>(h) = make_float2(hu, hv);
+  *reinterpret_cast<float2*>(l) = make_float2(tf32_rna(fu - hu), tf32_rna(fv - hv));
 }
 __device__ __forceinline__ double clamp1(double t) { return t > 1.0 ? 1.0 : (t < -1.0 ? -1.0 : t); }
 
@@ -127,7 +141,9 @@ __global__ void __launch_bounds__(BT) bd_z(const BDArgs a) {
     double* __restrict__ zo = a.Z + o;
     float* __restrict__ v32 = a.V32 + o;
     float* __restrict__ z32 = a.Z32 + o;
-    const bool fuse = a.fuse_ext;
+    float* __restrict__ v32l = a.V32l + o;
+    float* __restrict__ z32l = a.Z32l + o;
+    const bool fuse = a.fuse_ext, pre = a.pre;
     const int64_t n = a.n, h = a.N / 2;
     const double beta = a.beta, sc = a.s;
 #pragma unroll 4
@@ -146,10 +162,10 @@ __global__ void __launch_bounds__(BT) bd_z(const BDArgs a) {
       const double z0 = clamp1(u0 + xb0), z1 = clamp1(u1 + xb1);
       st2(zo + k, z0, z1);
       if (k < n) {
-        stf2(v32 + k, z0 - xb0, z1 - xb1);
-        stf2(z32 + k, z0, z1);
+        stf2s(v32 + k, v32l + k, pre, z0 - xb0, z1 - xb1);
+        stf2s(z32 + k, z32l + k, pre, z0, z1);
       } else if (fuse) {
-        stf2(v32 + k, sc * (z0 - xb0), sc * (z1 - xb1));
+        stf2s(v32 + k, v32l + k, pre, sc * (z0 - xb0), sc * (z1 - xb1));
       }
     }
     return;
@@ -223,7 +239,7 @@ __global__ void __launch_bounds__(BT) bd_y(const BDArgs a) {
       const double2 bb = ld2(b + i), xx = ld2(ax + i);
       const double r0 = az0 - (xx.x - bb.x) / beta, r1 = az1 - (xx.y - bb.y) / beta;
       st2(y + i, y0, y1);
-      stf2(y32 + i, y0, y1);
+      stf2s(y32 + i, a.Y32l + oj + i, a.pre, y0, y1);
       st2(rh + i, r0, r1);
       q[0] += r0 * r0; q[0] += r1 * r1;
       q[1] += bb.x * y0; q[1] += bb.y * y1;
@@ -336,8 +352,8 @@ __global__ void __launch_bounds__(BT) bd_x(const BDArgs a, const double* Ut, con
       const double v0 = xo.x - beta * (z2.x - u0), v1 = xo.y - beta * (z2.y - u1);
       st2(xw + k, v0, v1);
       if (k < n) {
-        stf2(ux32 + k, u0, u1);
-        stf2(xn32 + k, v0, v1);
+        stf2s(ux32 + k, a.UX32l + o + k, a.pre, u0, u1);
+        stf2s(xn32 + k, a.UX32l + ((int64_t)gridDim.x + j) * a.ldx + k, a.pre, v0, v1);
       }
       s[0] += fabs(v0); s[0] += fabs(v1);
       s[1] = nmax(nmax(s[1], fabs(u0)), fabs(u1));
@@ -513,7 +529,16 @@ __global__ void __launch_bounds__(BT) bd_refine(const BDArgs a, const double* de
   for (int64_t i = threadIdx.x; i < a.d; i += BT) {
     const double yi = y[i] + delta[oj + i];
     y[i] = yi;
-    if (a.f32) a.Y32[oj + i] = (float)yi;
+    if (a.f32) {
+      const float f = (float)yi;
+      if (a.pre) {
+        const float h = tf32_rna(f);
+        a.Y32[oj + i] = h;
+        a.Y32l[oj + i] = tf32_rna(f - h);
+      } else {
+        a.Y32[oj + i] = f;
+      }
+    }
     q[0] += b[i] * yi;
   }
   cta_reduce<1>(q, 0u, sh);
@@ -638,6 +663,8 @@ extern "C" size_t ell1_batch_dalm_workspace(const ell1_dict_t* D, int32_t B) {
   s += align_up(ldx * B * 4, 256) * 3 + align_up(ldx * 2 * B * 4, 256) + align_up(ld * B * 4, 256) * 3 +
        align_up(ld * 2 * B * 4, 256);
   s += 2 * align_up((int64_t)sizeof(DI) * B, 256) + align_up(B * 4, 256) + align_up(ldx * B * 8, 256);
+  if (D->dtype == ELL1_F32)                                  // producer-split operand lo halves
+    s += align_up(ldx * B * 4, 256) * 2 + align_up(ldx * 2 * B * 4, 256) + align_up(ld * B * 4, 256);
   if (D->dtype == ELL1_F32)                                  // splits of A and M + operand scratch
     s += (size_t)(f32split_floats(D, (ldx > ld ? ldx : ld) * 2 * B) + f32split_dict_floats(D) +
                   2 * align_up(ld * ld, 64) + 2 * align_up(ld * align_up(ld, 4), 64) + align_up(ld * ld, 64) +
@@ -676,6 +703,13 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   float* T32 = cv.take<float>(ldx * B);
   a.UX32 = cv.take<float>(ldx * 2 * B);
   a.Y32 = cv.take<float>(ld * B); a.P1f = cv.take<float>(ld * B); a.P3f = cv.take<float>(ld * B);
+  a.pre = a.vec;
+  if (const char* e = getenv("ELL1_BD_PRE")) a.pre = a.pre && e[0] != '0';   // diagnostics (A/B)
+  a.V32l = a.Z32l = a.UX32l = a.Y32l = nullptr;
+  if (a.pre) {
+    a.V32l = cv.take<float>(ldx * B); a.Z32l = cv.take<float>(ldx * B);
+    a.UX32l = cv.take<float>(ldx * 2 * B); a.Y32l = cv.take<float>(ld * B);
+  }
   a.P2f = cv.take<float>(ld * 2 * B);
   a.inst = cv.take<DI>(B);
   DI* inst2 = cv.take<DI>(B);
@@ -722,6 +756,7 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   if (cudaMemcpyAsync(Bm, Bmat, ld * B * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return ELL1_ERR_CUDA;
   if (cudaMemsetAsync(ctr, 0, 32, s) != cudaSuccess) return ELL1_ERR_CUDA;
   if (cudaMemsetAsync(a.UX32, 0, ldx * 2 * B * 4, s) != cudaSuccess) return ELL1_ERR_CUDA;
+  if (a.pre && cudaMemsetAsync(a.UX32l, 0, ldx * 2 * B * 4, s) != cudaSuccess) return ELL1_ERR_CUDA;
   // C0 = Ginv B (Ginv column-major ld x d, float64), the fp32 y step's constant term
   if (a.f32 && !dgemm(0, 0, ld, B, d, O->Ginv, ld, Bm, ld, C0, ld, s)) return ELL1_ERR_CUDA;
   bd_init<<<B, BT, 0, s>>>(a);
@@ -739,7 +774,8 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
   // U = A^T y_new (n x B), x_new, A [U | x_new], certificate (refine_only: flagged instances)
   auto tail_part = [&](const BDArgs& aa, int Bc, int refine_only) -> bool {
     void* Ut = aa.f32 ? (void*)T32 : (void*)scratch;
-    if (!gemm_AtR(ks, D, aa.f32 ? (const void*)aa.Y32 : (const void*)aa.Y[aa.iy ^ 1], ld, Ut, D->n, Bc, pA))
+    if (!gemm_AtR(ks, D, aa.f32 ? (const void*)aa.Y32 : (const void*)aa.Y[aa.iy ^ 1], ld, Ut, D->n, Bc, pA,
+                  aa.Y32l))
       return false;
     // [U | x_new] for the Bc instances: the x_new block starts at column Bc
     if (aa.vec) bd_x<true><<<Bc, BT, 0, ks>>>(aa, (const double*)Ut, (const float*)Ut, refine_only);
@@ -747,14 +783,16 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
     if (aa.gcert) {
       // certificate A A^T y as G y (d^2 per instance instead of d n) and A x_new
       if (aa.f32) {
-        if (!sgemm_split(ks, 0, (int)ld, Bc, (int)d, &spG, aa.Y32, ld, aa.P2f, ld)) return false;
-        if (!gemm_AX(ks, D, aa.UX32 + (int64_t)Bc * ldx, ldx, aa.P2f + (int64_t)Bc * ld, ld, Bc, pA)) return false;
+        if (!sgemm_split(ks, 0, (int)ld, Bc, (int)d, &spG, aa.Y32, ld, aa.P2f, ld, aa.Y32l)) return false;
+        if (!gemm_AX(ks, D, aa.UX32 + (int64_t)Bc * ldx, ldx, aa.P2f + (int64_t)Bc * ld, ld, Bc, pA,
+                     aa.pre ? aa.UX32l + (int64_t)Bc * ldx : nullptr))
+          return false;
       } else {
         if (!dgemm(0, 0, ld, Bc, d, O->G, ld, aa.Y[aa.iy ^ 1], ld, aa.P2, ld, ks)) return false;
         if (!gemm_AX(ks, D, aa.UX + (int64_t)Bc * ldx, ldx, aa.P2 + (int64_t)Bc * ld, ld, Bc)) return false;
       }
     } else if (aa.f32) {
-      if (!gemm_AX(ks, D, aa.UX32, ldx, aa.P2f, ld, 2 * Bc, pA)) return false;
+      if (!gemm_AX(ks, D, aa.UX32, ldx, aa.P2f, ld, 2 * Bc, pA, aa.UX32l)) return false;
     } else {
       if (!gemm_AX(ks, D, aa.UX, ldx, aa.P2, ld, 2 * Bc)) return false;
     }
@@ -779,12 +817,12 @@ extern "C" int ell1_batch_dalm(const ell1_dict_t* D, const double* Bmat, int32_t
     const void* Zop = aa.f32 ? (const void*)aa.Z32 : (const void*)aa.Z;
     if (aa.fuse_ext) {
       // P1 = [M | Ginv] V over K = n + d (V's identity block already carries s)
-      if (!sgemm_split(ks, 0, (int)ld, Bc, (int)N, &spX, aa.V32, ldx, aa.P1f, ld))
+      if (!sgemm_split(ks, 0, (int)ld, Bc, (int)N, &spX, aa.V32, ldx, aa.P1f, ld, aa.V32l))
         return false;
-    } else if (!gemm_AX(ks, &MD, Vop, ldx, aa.f32 ? (void*)aa.P1f : (void*)aa.P1, ld, Bc, pM)) {
+    } else if (!gemm_AX(ks, &MD, Vop, ldx, aa.f32 ? (void*)aa.P1f : (void*)aa.P1, ld, Bc, pM, aa.V32l)) {
       return false;
     }
-    if (!gemm_AX(ks, D, Zop, ldx, aa.f32 ? (void*)aa.P2f : (void*)aa.P2, ld, Bc, pA)) return false;
+    if (!gemm_AX(ks, D, Zop, ldx, aa.f32 ? (void*)aa.P2f : (void*)aa.P2, ld, Bc, pA, aa.Z32l)) return false;
     if (aa.ext && !aa.fuse_ext) {
       // identity block of M: s Ginv v_ext (s folded into v_ext by bd_z)
       if (!dgemm(0, 0, ld, Bc, d, O->Ginv, ld, aa.V + D->n, ldx, aa.GEXT, ld, ks)) return false;

@@ -127,29 +127,30 @@ inline bool split_tf32(const float* src, float* hi, float* lo, int64_t n, cudaSt
 }
 
 // Y (m x B) = op(A) X with fp32 operands through the 3xTF32 split of A (sp)
+// Xlo (optional): X arrives split by its producer (X = rna_tf32 hi, Xlo = lo)
 inline bool sgemm_split(cudaStream_t st, int transA, int m, int B, int k, const F32Split* sp, const float* X,
-                        int64_t ldx, float* Y, int64_t ldy) {
+                        int64_t ldx, float* Y, int64_t ldy, const float* Xlo = nullptr) {
   if (!sp) return false;
-  return transA ? tc3_gemm(m, B, k, sp->Ahi, sp->Alo, sp->pc, X, ldx, Y, ldy, st)
-                : tc3_gemm(m, B, k, sp->Arhi, sp->Arlo, sp->pr, X, ldx, Y, ldy, st);
+  return transA ? tc3_gemm(m, B, k, sp->Ahi, sp->Alo, sp->pc, X, ldx, Y, ldy, st, Xlo)
+                : tc3_gemm(m, B, k, sp->Arhi, sp->Arlo, sp->pr, X, ldx, Y, ldy, st, Xlo);
 }
 
 // Y(ld x B) = A(ld x n, column-major) X(n x B, ldx)      (A columns only)
 inline bool gemm_AX(cudaStream_t st, const ell1_dict_t* D, const void* X, int64_t ldx, void* Y, int64_t ldy,
-                    int B, const F32Split* sp = nullptr) {
+                    int B, const F32Split* sp = nullptr, const float* Xlo = nullptr) {
   if (B <= 0) return true;
   if (D->dtype == ELL1_F64)
     return dgemm(0, 0, D->ld, B, D->n, (const double*)D->A, D->ld, (const double*)X, ldx, (double*)Y, ldy, st);
-  return sgemm_split(st, 0, (int)D->ld, B, (int)D->n, sp, (const float*)X, ldx, (float*)Y, ldy);
+  return sgemm_split(st, 0, (int)D->ld, B, (int)D->n, sp, (const float*)X, ldx, (float*)Y, ldy, Xlo);
 }
 
 // G(n x B) = A^T R(ld x B)
 inline bool gemm_AtR(cudaStream_t st, const ell1_dict_t* D, const void* R, int64_t ldr, void* G, int64_t ldg,
-                     int B, const F32Split* sp = nullptr) {
+                     int B, const F32Split* sp = nullptr, const float* Rlo = nullptr) {
   if (B <= 0) return true;
   if (D->dtype == ELL1_F64)
     return dgemm(1, 0, D->n, B, D->ld, (const double*)D->A, D->ld, (const double*)R, ldr, (double*)G, ldg, st);
-  return sgemm_split(st, 1, (int)D->n, B, (int)D->ld, sp, (const float*)R, ldr, (float*)G, ldg);
+  return sgemm_split(st, 1, (int)D->n, B, (int)D->ld, sp, (const float*)R, ldr, (float*)G, ldg, Rlo);
 }
 
 // workspace floats for one dictionary split (both orientations)
