@@ -23,6 +23,8 @@ KEYS = {
     "launch__grid_size": "grid",
     "launch__block_size": "block",
     "sm__cycles_elapsed.avg": "cycles",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed": "tensor_pipe_active_pct",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active": "tensor_pipe_active_pct_of_active",
 }
 STALLS = ["barrier", "long_scoreboard", "short_scoreboard", "mio_throttle", "wait", "math_pipe_throttle",
           "selected", "not_selected", "no_instructions", "branch_resolving", "lg_throttle", "membar",
