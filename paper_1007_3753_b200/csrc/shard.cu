@@ -92,21 +92,24 @@ __global__ void __launch_bounds__(NTHR, 1) gemv_t_kernel(const __grid_constant__
 // ring (mbarrier complete_tx); 16 consumer warps accumulate the CB column dots
 // in fp64 registers (row pairs strided over the consumers) and release the slot.  Each
 // column block ends in one fixed-order block reduction, so the result is
-// deterministic.  3 stages x (16 columns x 1024 rows) = 192 KB of A in flight
-// per SM keeps HBM busy: 7.1 TB/s at d = 65536 (the register-staged engine
-// path holds ~32 KB per SM and reached 4.8 TB/s; 8-column x 4-stage 5.9,
-// 16 x 512-row stages 4.2 — measured with tools/gemv_bench.py).
+// deterministic.  2 stages x (4 columns x 4096 rows) = 128 KB of A (+ 64 KB
+// of r) in flight per SM keeps HBM busy, and each copy is a 16 KB contiguous
+// run of one column: over the whole 64 GiB single-GPU dictionary that beats
+// 16 columns x 1024 rows (4 KB runs in 16 places 256 KB apart) by 12%, 6.73
+// vs 5.99 TB/s, and equals it at the 8 GiB 8-way shard (7.04 vs 7.05;
+// tools/gts_variants.sh).  The register-staged engine path holds ~32 KB per
+// SM and reached 4.8 TB/s.
 namespace gts {
 #ifndef ELL1_GTS_CB
-#define ELL1_GTS_CB 16
+#define ELL1_GTS_CB 4
 #endif
 #ifndef ELL1_GTS_RC
-#define ELL1_GTS_RC 1024
+#define ELL1_GTS_RC 4096
 #endif
 constexpr int CB = ELL1_GTS_CB;           // columns per block
-constexpr int RC = ELL1_GTS_RC;           // rows per chunk (2 per consumer thread)
+constexpr int RC = ELL1_GTS_RC;           // rows per chunk (row pairs strided over the consumers)
 #ifndef ELL1_GTS_ST
-#define ELL1_GTS_ST 3
+#define ELL1_GTS_ST 2
 #endif
 constexpr int ST = ELL1_GTS_ST;           // ring depth
 constexpr int CW = 16;                    // consumer warps
