@@ -1014,10 +1014,10 @@ def run_b200(args):
         peaks = json.load(open(peaks_path)) if os.path.exists(peaks_path) else {}
         peak = float(peaks.get("hbm_gbs", 6650.0))
         traffic = None
-        prof = os.path.join(ROOT, "profiles", "r02_ncu_cfg4_kernels.json")
+        prof = os.path.join(ROOT, "profiles", "r02_ncu_cfg4_full.json")
         if os.path.exists(prof):
             try:
-                # ncu dram read+write per pass, measured on the 8 GiB shard, scaled to this run's shard
+                # ncu dram read+write per pass over the whole 64 GiB dictionary, scaled to this run's shard
                 traffic = json.load(open(prof))["traffic_over_algorithmic"] * h["shard_bytes"]
             except (ValueError, KeyError):
                 traffic = None
@@ -1035,17 +1035,21 @@ def run_b200(args):
                "e2e": h["e2e"],
                "roofline": {"bound": "hbm", "achieved": h["achieved_gbs"], "peak": peak, "unit": "GB/s",
                             "frac": h["achieved_gbs"] / peak, "traffic": traffic,
-                            "kernel": "the two dictionary passes: gemv_partial_kernel<float> (A_r x) and "
-                                      "gemv_t_stream_kernel (A_r^T r), with the elementwise round kernels",
+                            "kernel": "the two dictionary passes: gemv_stream_kernel (A_r x partials + the "
+                                      "fixed-order row reduction) and gemv_t_stream_kernel (A_r^T r), with the "
+                                      "elementwise round kernels",
                             "algorithmic": "d * n_local * 4 bytes per pass (%d bytes); passes = 1 A_r x per "
                                            "trial + 1 A_r^T r per accepted iteration; time = CUDA events "
                                            "around ell1_sfista_pre + ell1_sfista_post of every timed round "
                                            "(collective excluded)" % h["shard_bytes"],
                             "step_gbs": h["step_gbs"],
-                            "traffic_source": "profiles/r02_ncu_cfg4_kernels.json: dram__bytes_read.sum + "
+                            "traffic_source": "profiles/r02_ncu_cfg4_full.json: dram__bytes_read.sum + "
                                               "dram__bytes_write.sum per pass (mean of the two passes) / "
                                               "algorithmic bytes, x this run's bytes per pass",
-                            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"
+                            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write); the passes are "
+                                           "read-only streams, which run slightly above a copy (frac can "
+                                           "exceed 1: 7.0 TB/s for one 64 GiB read pass alone, "
+                                           "tools/gemv_bench.py --full)"
                             if "hbm_gbs" in peaks else "fallback"},
                "headline_detail": {k: h[k] for k in ("iterations", "passes_per_iteration", "trials_per_iteration",
                                                       "rounds_per_solve", "kernel_seconds", "gen_seconds",

@@ -234,6 +234,127 @@ __global__ void __launch_bounds__(gts::THREADS, 1)
   }
 }
 
+// ---- GEMV partials for long fp32 columns (config 4: A_r x over the whole
+// dictionary).  The same bulk-copy ring as the GEMV^T: per stage CB columns x
+// RC rows (16 KB contiguous runs of each column); CTA b walks its balanced
+// column range one RC-row chunk at a time, 16 consumer warps accumulate the
+// chunk's rows (row pairs strided over the threads) across the range's
+// columns in column order, then write them slice-major into the partial
+// buffer the fixed-order gemv_reduce_kernel folds (the engine's layout).
+namespace gvs {
+constexpr int CB = 4;                     // columns per stage
+constexpr int RC = 4096;                  // rows per chunk
+constexpr int ST = 3;                     // ring depth
+constexpr int CW = 16;                    // consumer warps
+constexpr int THREADS = (CW + 1) * 32;
+constexpr int KP = RC / (2 * CW * 32);    // row pairs per consumer thread and chunk
+constexpr int A_BYTES = CB * RC * 4;
+constexpr int SMEM = ST * A_BYTES + 2 * ST * 8 + 64;
+}  // namespace gvs
+
+__global__ void __launch_bounds__(gvs::THREADS, 1)
+    gemv_stream_kernel(const float* __restrict__ A, int64_t ld, int64_t d, int64_t n, const double* __restrict__ x,
+                       double* __restrict__ part, int rp, const int* gate) {
+  using namespace gvs;
+  if (gated_off(gate)) return;
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* full = (uint64_t*)(sm + ST * A_BYTES);
+  uint64_t* empty = full + ST;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = gridDim.x, b = blockIdx.x;
+  const int64_t c0 = (n * b) / nb, c1 = (n * (b + 1)) / nb;
+  const int64_t nblk = (c1 - c0 + CB - 1) / CB;
+  const int nch = (int)((d + RC - 1) / RC);
+  const int64_t total = nblk * nch;                       // (row chunk, column block) steps, blocks inner
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < ST; ++k) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(full + k)), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(empty + k)), "r"(CW));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto wait = [](uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
+        "@!p bra W_%=;\n\t}" ::"r"(su32(bar)),
+        "r"(parity)
+        : "memory");
+  };
+  if (warp == CW) {
+    if (lane == 0) {
+      for (int64_t t = 0; t < total; ++t) {
+        const int s = (int)(t % ST);
+        const int64_t u = t / ST;
+        if (u > 0) wait(empty + s, (unsigned)((u - 1) & 1));
+        const int ch = (int)(t / nblk);
+        const int64_t blk = t % nblk;
+        const int64_t row0 = (int64_t)ch * RC;
+        const int rows = (int)((ld - row0) < RC ? (ld - row0) : RC);   // padded rows: 16-byte multiples
+        const int64_t cb = c0 + blk * CB;
+        const int cols = (int)((c1 - cb) < CB ? (c1 - cb) : CB);
+        unsigned char* st = sm + (size_t)s * A_BYTES;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full + s)),
+                     "r"((unsigned)(cols * rows * 4))
+                     : "memory");
+        for (int c = 0; c < cols; ++c)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  su32(st + (size_t)c * RC * 4)),
+              "l"(A + (cb + c) * ld + row0), "r"(rows * 4), "r"(su32(full + s))
+              : "memory");
+      }
+    }
+    return;
+  }
+  const int tc = threadIdx.x;                            // 0 .. CW*32-1
+  const int64_t reg = (int64_t)nb * rp;
+  double acc[KP][2];
+#pragma unroll
+  for (int k = 0; k < KP; ++k) acc[k][0] = acc[k][1] = 0.0;
+  for (int64_t t = 0; t < total; ++t) {
+    const int s = (int)(t % ST);
+    const int ch = (int)(t / nblk);
+    const int64_t blk = t % nblk;
+    const int64_t cb = c0 + blk * CB;
+    const int cols = (int)((c1 - cb) < CB ? (c1 - cb) : CB);
+    double xv[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) xv[c] = c < cols ? __ldg(x + cb + c) : 0.0;
+    wait(full + s, (unsigned)((t / ST) & 1));
+    const unsigned char* st = sm + (size_t)s * A_BYTES;
+#pragma unroll
+    for (int c = 0; c < CB; ++c) {
+      if (c < cols) {
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+          const float2 v = *reinterpret_cast<const float2*>(st + ((size_t)c * RC + 2 * tc + 2 * CW * 32 * k) * 4);
+          acc[k][0] = fma((double)v.x, xv[c], acc[k][0]);
+          acc[k][1] = fma((double)v.y, xv[c], acc[k][1]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(empty + s)) : "memory");
+    if (blk == nblk - 1) {
+      // row chunk done: this CTA's partial of its rows, slice-major
+      const int64_t row0 = (int64_t)ch * RC;
+#pragma unroll
+      for (int k = 0; k < KP; ++k)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t i = row0 + 2 * tc + 2 * CW * 32 * k + e;
+          if (i < d) {
+            const int64_t o = slice_owner(d, nb, i);
+            part[o * reg + (int64_t)b * rp + (i - slice_r0(d, nb, o))] = acc[k][e];
+          }
+          acc[k][e] = 0.0;
+        }
+    }
+  }
+}
+
 static bool gemv_t_stream_ok(const ell1_dict_t* D) {
   return D->dtype == ELL1_F32 && !D->ext && D->d >= 4096 && D->d % 32 == 0 && D->ld % 4 == 0;
 }
@@ -533,6 +654,28 @@ using namespace ell1;
 static int launch_gemv(const ell1_dict_t* D, const double* x, double* y, void* ws, size_t wsb, cudaStream_t s,
                        const int* gate) {
   const int nb = pick_blocks(D->n, 0);
+  if (gemv_t_stream_ok(D) && D->d * D->n >= (int64_t(1) << 32) && !getenv("ELL1_GEMV_PANEL")) {
+    // long fp32 columns of a >= 16 GiB dictionary: the bulk-copy ring (the
+    // partial layout is the engine's).  64 GiB: 7.02 vs 6.36-6.74 TB/s for the
+    // panel pass; at <= 8 GiB the panel pass is as fast or faster
+    // (tools/gemv_bench.py, ELL1_GEMV_PANEL=1 forces the panel pass).
+    GridBufs g;
+    Carve cv(ws, wsb);
+    if (!carve_grid(cv, g, nb, D->d, 1)) return ELL1_ERR_ARG;
+    static unsigned attr = 0;                              // per-device bit
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr >> (dev & 31) & 1u)) {
+      if (cudaFuncSetAttribute(gemv_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gvs::SMEM) !=
+          cudaSuccess)
+        return ELL1_ERR_CUDA;
+      attr |= 1u << (dev & 31);
+    }
+    gemv_stream_kernel<<<nb, gvs::THREADS, gvs::SMEM, s>>>((const float*)D->A, D->ld, D->d, D->n, x, g.part, g.rp,
+                                                           gate);
+    gemv_reduce_kernel<<<nb, NTHR, 0, s>>>(g.part, g.rp, nb, D->d, y, gate);
+    return cudaGetLastError() == cudaSuccess ? ELL1_OK : ELL1_ERR_CUDA;
+  }
   GvArgs a;
   a.D = to_raw(D);
   a.D.ext = 0;
