@@ -235,16 +235,26 @@ __global__ void __launch_bounds__(gts::THREADS, 1)
 }
 
 // ---- GEMV partials for long fp32 columns (config 4: A_r x over the whole
-// dictionary).  The same bulk-copy ring as the GEMV^T: per stage CB columns x
-// RC rows (16 KB contiguous runs of each column); CTA b walks its balanced
+// dictionary).  The same bulk-copy ring as the GEMV^T: per stage CB = 2
+// columns x RC = 8192 rows (32 KB contiguous runs; over 64 GiB 7.21 TB/s vs
+// 6.92 for 4 x 4096 and 6.93 for 8 x 2048, tools/gvs_variants.sh); CTA b walks its balanced
 // column range one RC-row chunk at a time, 16 consumer warps accumulate the
 // chunk's rows (row pairs strided over the threads) across the range's
 // columns in column order, then write them slice-major into the partial
 // buffer the fixed-order gemv_reduce_kernel folds (the engine's layout).
 namespace gvs {
-constexpr int CB = 4;                     // columns per stage
-constexpr int RC = 4096;                  // rows per chunk
-constexpr int ST = 3;                     // ring depth
+#ifndef ELL1_GVS_CB
+#define ELL1_GVS_CB 2
+#endif
+#ifndef ELL1_GVS_RC
+#define ELL1_GVS_RC 8192
+#endif
+#ifndef ELL1_GVS_ST
+#define ELL1_GVS_ST 3
+#endif
+constexpr int CB = ELL1_GVS_CB;           // columns per stage
+constexpr int RC = ELL1_GVS_RC;           // rows per chunk
+constexpr int ST = ELL1_GVS_ST;           // ring depth
 constexpr int CW = 16;                    // consumer warps
 constexpr int THREADS = (CW + 1) * 32;
 constexpr int KP = RC / (2 * CW * 32);    // row pairs per consumer thread and chunk
@@ -656,7 +666,7 @@ static int launch_gemv(const ell1_dict_t* D, const double* x, double* y, void* w
   const int nb = pick_blocks(D->n, 0);
   if (gemv_t_stream_ok(D) && D->d * D->n >= (int64_t(1) << 32) && !getenv("ELL1_GEMV_PANEL")) {
     // long fp32 columns of a >= 16 GiB dictionary: the bulk-copy ring (the
-    // partial layout is the engine's).  64 GiB: 7.02 vs 6.36-6.74 TB/s for the
+    // partial layout is the engine's).  64 GiB: 7.2 vs 6.36-6.74 TB/s for the
     // panel pass; at <= 8 GiB the panel pass is as fast or faster
     // (tools/gemv_bench.py, ELL1_GEMV_PANEL=1 forces the panel pass).
     GridBufs g;

@@ -6,7 +6,7 @@
 set -e
 cd "$(dirname "$0")/.."
 F="-gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC -fmad=false --expt-relaxed-constexpr -Iinclude -shared -lcuda"
-for v in "16 1024 3" "8 2048 2" "8 1024 4" "4 4096 2" "16 512 6" "32 512 3"; do
+for v in "4 4096 2" "16 1024 3" "8 2048 2" "6 2048 3" "3 4096 2" "2 4096 3"; do
   set -- $v
   nvcc $F -DELL1_GTS_CB=$1 -DELL1_GTS_RC=$2 -DELL1_GTS_ST=$3 paper_1007_3753_b200/csrc/shard.cu -o /tmp/libgts_$1_$2_$3.so
   echo "CB=$1 RC=$2 ST=$3"
