@@ -97,8 +97,9 @@ __global__ void __launch_bounds__(NTHR, 1) gemv_t_kernel(const __grid_constant__
 // run of one column: over the whole 64 GiB single-GPU dictionary that beats
 // 16 columns x 1024 rows (4 KB runs in 16 places 256 KB apart) by 12%, 6.73
 // vs 5.99 TB/s, and equals it at the 8 GiB 8-way shard (7.04 vs 7.05;
-// tools/gts_variants.sh).  The register-staged engine path holds ~32 KB per
-// SM and reached 4.8 TB/s.
+// tools/gts_variants.sh).  Each staged r chunk serves GB = 4 column blocks
+// (the r reads from L2 drop 4x): 6.73 -> 6.95 TB/s over 64 GiB.  The
+// register-staged engine path holds ~32 KB per SM and reached 4.8 TB/s.
 namespace gts {
 #ifndef ELL1_GTS_CB
 #define ELL1_GTS_CB 4
@@ -106,41 +107,56 @@ namespace gts {
 #ifndef ELL1_GTS_RC
 #define ELL1_GTS_RC 4096
 #endif
-constexpr int CB = ELL1_GTS_CB;           // columns per block
-constexpr int RC = ELL1_GTS_RC;           // rows per chunk (row pairs strided over the consumers)
-#ifndef ELL1_GTS_ST
-#define ELL1_GTS_ST 2
+#ifndef ELL1_GTS_GB
+#define ELL1_GTS_GB 4
 #endif
-constexpr int ST = ELL1_GTS_ST;           // ring depth
+constexpr int CB = ELL1_GTS_CB;           // columns per A stage
+constexpr int RC = ELL1_GTS_RC;           // rows per chunk (row pairs strided over the consumers)
+constexpr int GB = ELL1_GTS_GB;           // A stages (column blocks) sharing one staged r chunk
+constexpr int STA = 2;                    // A ring depth
+constexpr int STR = 2;                    // r ring depth
 constexpr int CW = 16;                    // consumer warps
 constexpr int THREADS = (CW + 1) * 32;    // + producer warp
+constexpr int KP = RC / (2 * CW * 32);    // row pairs per consumer thread and chunk
 constexpr int A_BYTES = CB * RC * 4;
 constexpr int R_BYTES = RC * 8;
-constexpr int STAGE = A_BYTES + R_BYTES;
-constexpr int SMEM = ST * STAGE + 2 * ST * 8 + CW * CB * 8 + 64;
+constexpr int SMEM = STA * A_BYTES + STR * R_BYTES + 2 * (STA + STR) * 8 + CW * CB * GB * 8 + 64;
 }  // namespace gts
 
 __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
+// Column groups of GB blocks x CB columns walk the rows chunk by chunk; each
+// r chunk is staged once per group and serves its GB column blocks (the r
+// traffic from L2 is n / (GB CB) x d x 8 bytes per pass).  Per column, a
+// thread accumulates its rows in increasing order over the chunks, then one
+// fixed-order block reduction per group: bit-identical for any GB.
 __global__ void __launch_bounds__(gts::THREADS, 1)
     gemv_t_stream_kernel(const float* __restrict__ A, int64_t ld, int64_t d, int64_t n, const double* __restrict__ r,
                          double* __restrict__ g, const int* gate) {
   using namespace gts;
   if (gated_off(gate)) return;
   extern __shared__ __align__(128) unsigned char sm[];
-  uint64_t* full = (uint64_t*)(sm + ST * STAGE);
-  uint64_t* empty = full + ST;
-  double* red = (double*)(empty + ST);                  // [CW][CB]
+  unsigned char* abuf = sm;                                     // [STA][A_BYTES]
+  unsigned char* rbuf = sm + STA * A_BYTES;                     // [STR][R_BYTES]
+  uint64_t* afull = (uint64_t*)(rbuf + STR * R_BYTES);
+  uint64_t* aempty = afull + STA;
+  uint64_t* rfull = aempty + STA;
+  uint64_t* rempty = rfull + STR;
+  double* red = (double*)(rempty + STR);                        // [CW][GB * CB]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // balanced contiguous column ranges per CTA, in blocks of CB
+  // balanced contiguous column ranges per CTA, in blocks of CB, grouped by GB
   const int64_t nblk = (n + CB - 1) / CB;
   const int64_t b0 = nblk * blockIdx.x / gridDim.x, b1 = nblk * (blockIdx.x + 1) / gridDim.x;
+  const int64_t ngrp = (b1 - b0 + GB - 1) / GB;
   const int nch = (int)((d + RC - 1) / RC);
-  const int64_t total = (b1 - b0) * nch;                  // (block, chunk) steps of this CTA
   if (threadIdx.x == 0) {
-    for (int s = 0; s < ST; ++s) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(full + s)), "r"(1));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(empty + s)), "r"(CW));
+    for (int s = 0; s < STA; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(afull + s)), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(aempty + s)), "r"(CW));
+    }
+    for (int s = 0; s < STR; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(rfull + s)), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(rempty + s)), "r"(CW));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -156,81 +172,119 @@ __global__ void __launch_bounds__(gts::THREADS, 1)
   if (warp == CW) {
     if (lane == 0) {
       // ---- producer
-      for (int64_t t = 0; t < total; ++t) {
-        const int s = (int)(t % ST);
-        const int64_t u = t / ST;
-        if (u > 0) wait(empty + s, (unsigned)((u - 1) & 1));
-        const int64_t blk = b0 + t / nch;
-        const int ch = (int)(t % nch);
-        const int64_t row0 = (int64_t)ch * RC;
-        const int rows = (int)((d - row0) < RC ? (d - row0) : RC);
-        const int64_t c0 = blk * CB;
-        const int cols = (int)((n - c0) < CB ? (n - c0) : CB);
-        unsigned char* st = sm + (size_t)s * STAGE;
-        const unsigned bytes = (unsigned)(cols * rows * 4 + rows * 8);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full + s)), "r"(bytes)
-                     : "memory");
-        for (int c = 0; c < cols; ++c)
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  su32(st + (size_t)c * RC * 4)),
-              "l"(A + (c0 + c) * ld + row0), "r"(rows * 4), "r"(su32(full + s))
-              : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         su32(st + A_BYTES)),
-                     "l"(r + row0), "r"(rows * 8), "r"(su32(full + s))
-                     : "memory");
+      int64_t as = 0, rs = 0;                                 // A / r steps issued
+      for (int64_t gp = 0; gp < ngrp; ++gp) {
+        const int64_t gb0 = b0 + gp * GB;
+        const int nbg = (int)((b1 - gb0) < GB ? (b1 - gb0) : GB);
+        for (int ch = 0; ch < nch; ++ch, ++rs) {
+          const int64_t row0 = (int64_t)ch * RC;
+          const int rows = (int)((d - row0) < RC ? (d - row0) : RC);
+          {
+            const int s = (int)(rs % STR);
+            if (rs >= STR) wait(rempty + s, (unsigned)(((rs / STR) - 1) & 1));
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(rfull + s)),
+                         "r"((unsigned)(rows * 8))
+                         : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    su32(rbuf + (size_t)s * R_BYTES)),
+                "l"(r + row0), "r"(rows * 8), "r"(su32(rfull + s))
+                : "memory");
+          }
+          for (int bi = 0; bi < nbg; ++bi, ++as) {
+            const int s = (int)(as % STA);
+            if (as >= STA) wait(aempty + s, (unsigned)(((as / STA) - 1) & 1));
+            const int64_t c0 = (gb0 + bi) * CB;
+            const int cols = (int)((n - c0) < CB ? (n - c0) : CB);
+            unsigned char* st = abuf + (size_t)s * A_BYTES;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(afull + s)),
+                         "r"((unsigned)(cols * rows * 4))
+                         : "memory");
+            for (int c = 0; c < cols; ++c)
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                      su32(st + (size_t)c * RC * 4)),
+                  "l"(A + (c0 + c) * ld + row0), "r"(rows * 4), "r"(su32(afull + s))
+                  : "memory");
+          }
+        }
       }
     }
     return;
   }
-  // ---- consumers: thread t owns rows 2t, 2t+1 of every chunk
+  // ---- consumers: thread t owns rows 2t, 2t + 1 (+ 1024 k) of every chunk
   const int tc = threadIdx.x;                           // 0 .. CW*32-1
-  double acc[CB];
-  for (int64_t t = 0; t < total; ++t) {
-    const int s = (int)(t % ST);
-    const int64_t u = t / ST;
-    const int ch = (int)(t % nch);
-    const int64_t blk = b0 + t / nch;
-    const int64_t row0 = (int64_t)ch * RC;
-    const int rows = (int)((d - row0) < RC ? (d - row0) : RC);
-    const int64_t c0 = blk * CB;
-    const int cols = (int)((n - c0) < CB ? (n - c0) : CB);
-    if (ch == 0)
+  int64_t as = 0, rs = 0;
+  for (int64_t gp = 0; gp < ngrp; ++gp) {
+    const int64_t gb0 = b0 + gp * GB;
+    const int nbg = (int)((b1 - gb0) < GB ? (b1 - gb0) : GB);
+    double acc[GB][CB];
 #pragma unroll
-      for (int c = 0; c < CB; ++c) acc[c] = 0.0;
-    wait(full + s, (unsigned)(u & 1));
-    const unsigned char* st = sm + (size_t)s * STAGE;
-    for (int i = 2 * tc; i < rows; i += 2 * CW * 32) {
-      const double2 rv = *reinterpret_cast<const double2*>(st + A_BYTES + (size_t)i * 8);
+    for (int bi = 0; bi < GB; ++bi)
 #pragma unroll
-      for (int c = 0; c < CB; ++c) {
-        if (c < cols) {
-          const float2 av = *reinterpret_cast<const float2*>(st + ((size_t)c * RC + i) * 4);
-          acc[c] = fma((double)av.x, rv.x, acc[c]);
-          acc[c] = fma((double)av.y, rv.y, acc[c]);
+      for (int c = 0; c < CB; ++c) acc[bi][c] = 0.0;
+    for (int ch = 0; ch < nch; ++ch, ++rs) {
+      const int64_t row0 = (int64_t)ch * RC;
+      const int rows = (int)((d - row0) < RC ? (d - row0) : RC);
+      const int sr = (int)(rs % STR);
+      wait(rfull + sr, (unsigned)((rs / STR) & 1));
+      const unsigned char* rst = rbuf + (size_t)sr * R_BYTES;
+      double2 rv[KP];
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        const int i = 2 * tc + 2 * CW * 32 * k;
+        rv[k] = i < rows ? *reinterpret_cast<const double2*>(rst + (size_t)i * 8) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int bi = 0; bi < GB; ++bi) {
+        if (bi < nbg) {
+          const int sa = (int)(as % STA);
+          wait(afull + sa, (unsigned)((as / STA) & 1));
+          const unsigned char* st = abuf + (size_t)sa * A_BYTES;
+          const int64_t c0 = (gb0 + bi) * CB;
+          const int cols = (int)((n - c0) < CB ? (n - c0) : CB);
+#pragma unroll
+          for (int k = 0; k < KP; ++k) {
+            const int i = 2 * tc + 2 * CW * 32 * k;
+            if (i < rows) {
+#pragma unroll
+              for (int c = 0; c < CB; ++c) {
+                if (c < cols) {
+                  const float2 av = *reinterpret_cast<const float2*>(st + ((size_t)c * RC + i) * 4);
+                  acc[bi][c] = fma((double)av.x, rv[k].x, acc[bi][c]);
+                  acc[bi][c] = fma((double)av.y, rv[k].y, acc[bi][c]);
+                }
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(aempty + sa)) : "memory");
+          ++as;
         }
       }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(rempty + sr)) : "memory");
     }
-    __syncwarp();
-    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(empty + s)) : "memory");
-    if (ch == nch - 1) {
-      // column block done: fixed-order reduction (lanes -> xor tree, then warps in order)
+    // column group done: fixed-order reduction (lanes -> xor tree, then warps in order)
+#pragma unroll
+    for (int bi = 0; bi < GB; ++bi)
 #pragma unroll
       for (int c = 0; c < CB; ++c) {
-        double v = acc[c];
+        double v = acc[bi][c];
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) red[warp * CB + c] = v;
+        if (lane == 0) red[warp * GB * CB + bi * CB + c] = v;
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(CW * 32) : "memory");
-      if (tc < cols) {
-        double v = red[tc];
-        for (int w = 1; w < CW; ++w) v += red[w * CB + tc];
-        g[c0 + tc] = v;
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(CW * 32) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(CW * 32) : "memory");
+    const int64_t gc0 = gb0 * CB;
+    const int64_t gcols = ((b1 * CB < n ? b1 * CB : n) - gc0) < GB * CB ? ((b1 * CB < n ? b1 * CB : n) - gc0)
+                                                                        : GB * CB;
+    if (tc < gcols) {
+      double v = red[tc];
+      for (int w = 1; w < CW; ++w) v += red[w * GB * CB + tc];
+      g[gc0 + tc] = v;
     }
+    asm volatile("bar.sync 1, %0;" ::"n"(CW * 32) : "memory");
   }
 }
 
