@@ -1001,6 +1001,7 @@ def run_b200(args):
                 "cfg5_sweep": lambda: leg_cfg5_sweep(torch, dev),
                 "solvers_cfg2": lambda: leg_solvers_cfg2(torch, make_instance(rank)),
                 "cfg4": lambda: headline_cfg4(torch, dev, ws, rank, args),
+                "stream": lambda: stream_roofline(torch, dev),
                 "proxy": lambda: _proxy_parity(torch, dev)}
         r = legs[args.only_leg]()
         if rank == 0:

@@ -770,6 +770,104 @@ __device__ void panel_gemv(const Ctx& E, const DictV<TA>& D, const Panel<TA>& P,
       return;
     }
   }
+  if (nvec >= 2 * NTHR && w - rc >= 8) {
+    // Long mostly-streamed columns: each thread takes two consecutive row
+    // vectors, so the CTA reads 2 x 8 KB-per-column runs as one contiguous
+    // 16 KB run (HBM streams these faster than scattered 8 KB pieces).  The
+    // per-row sum runs over the columns in the same order as below: the
+    // result bits do not change.
+    for (int64_t q0 = 2 * (int64_t)tix(); q0 < nvec; q0 += 2 * NTHR) {
+      const bool has1 = q0 + 1 < nvec;
+      double acc[2][NV][VW];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+          for (int e = 0; e < VW; ++e) acc[h][v][e] = 0.0;
+      const unsigned p = (unsigned)__cvta_generic_to_shared(P.sm + q0 * VW);
+      const unsigned cst = (unsigned)(D.ld * sizeof(TA));
+      const TA* pg = P.gl + q0 * VW;
+      int j = 0;
+      for (; j < rc; ++j) {
+        TA a[2][VW];
+        ld16_sa<TA>(p + (unsigned)j * cst, a[0]);
+        if (has1) ld16_sa<TA>(p + (unsigned)j * cst + 16u, a[1]);
+        else {
+#pragma unroll
+          for (int e = 0; e < VW; ++e) a[1][e] = (TA)0;
+        }
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const double xv = xs[v][j];
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int e = 0; e < VW; ++e) acc[h][v][e] = fma((double)a[h][e], xv, acc[h][v][e]);
+        }
+      }
+      for (; j + 4 <= w; j += 4) {
+        TA a[4][2][VW];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          ld16_g<TA>(pg + (int64_t)(j + u) * D.ld, a[u][0]);
+          if (has1) ld16_g<TA>(pg + (int64_t)(j + u) * D.ld + VW, a[u][1]);
+          else {
+#pragma unroll
+            for (int e = 0; e < VW; ++e) a[u][1][e] = (TA)0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const double xv = xs[v][j + u];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int e = 0; e < VW; ++e) acc[h][v][e] = fma((double)a[u][h][e], xv, acc[h][v][e]);
+          }
+      }
+      for (; j < w; ++j) {
+        TA a[2][VW];
+        ld16_g<TA>(pg + (int64_t)j * D.ld, a[0]);
+        if (has1) ld16_g<TA>(pg + (int64_t)j * D.ld + VW, a[1]);
+        else {
+#pragma unroll
+          for (int e = 0; e < VW; ++e) a[1][e] = (TA)0;
+        }
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const double xv = xs[v][j];
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int e = 0; e < VW; ++e) acc[h][v][e] = fma((double)a[h][e], xv, acc[h][v][e]);
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t i0 = (q0 + h) * VW;
+        if (h == 1 && !has1) break;
+        int64_t ow = i0 < D.d ? slice_owner(D.d, E.nb, i0) : 0;
+        int64_t r0 = slice_r0(D.d, E.nb, ow), r1 = slice_r0(D.d, E.nb, ow + 1);
+#pragma unroll
+        for (int e = 0; e < VW; ++e) {
+          const int64_t i = i0 + e;
+          if (i < D.d) {
+            while (i >= r1) { ++ow; r0 = r1; r1 = slice_r0(D.d, E.nb, ow + 1); }
+            double* o = out + ow * reg + (i - r0);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+              double* ov = o + (size_t)v * E.pvec;
+              *ov = accumulate ? *ov + acc[h][v][e] : acc[h][v][e];
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
   for (int64_t q = tix(); q < nvec; q += NTHR) {
     double acc[NV][VW];
 #pragma unroll
