@@ -244,3 +244,52 @@ def test_sharded_homotopy_matches_golden(cid, world):
     for res, lam_r in results:
         assert_parity(res.x_star, res.iterations, res.converged, res.trace, gold, 1e-8)
         np.testing.assert_array_equal(res.x_star, results[0][0].x_star)
+
+
+def test_gemv_stream_pass_at_16gib():
+    """The streamed A x pass that config 4's >= 16 GiB dictionaries take
+    (shard.cu gemv_stream_kernel + the fixed-order row reduction) and the
+    grouped streamed A^T r pass, against a chunked fp64 torch product on a
+    65536 x 65536 fp32 dictionary (16 GiB), and A x against the engine panel
+    pass (ELL1_GEMV_PANEL) to rounding level."""
+    import os
+    import torch
+    from paper_1007_3753_b200 import _lib, device
+    dev = torch.device("cuda", 0)
+    d = n = 65536
+    g = torch.Generator(device=dev)
+    g.manual_seed(11)
+    st = torch.empty(n, d, device=dev, dtype=torch.float32)
+    for c0 in range(0, n, 8192):
+        st[c0:c0 + 8192].normal_(generator=g)
+    D = device.DeviceDictionary.wrap(st, d)
+    v = D.view()
+    L = _lib.lib()
+    wsb = L.ell1_gemv_workspace(ctypes.byref(v))
+    ws = device.alloc_bytes(wsb, dev)
+    x = torch.randn(n, dtype=torch.float64, device=dev, generator=g)
+    r = torch.randn(D.ld, dtype=torch.float64, device=dev, generator=g)
+    y = torch.zeros(D.ld, dtype=torch.float64, device=dev)
+    y2 = torch.zeros(D.ld, dtype=torch.float64, device=dev)
+    gg = torch.zeros(n, dtype=torch.float64, device=dev)
+    s = device.stream_ptr(dev)
+    _lib.check(L.ell1_gemv(ctypes.byref(v), device.ptr(x), device.ptr(y), device.ptr(ws), wsb, s), "gemv")
+    _lib.check(L.ell1_gemv_t(ctypes.byref(v), device.ptr(r), device.ptr(gg), device.ptr(ws), wsb, s), "gemv_t")
+    os.environ["ELL1_GEMV_PANEL"] = "1"
+    try:
+        _lib.check(L.ell1_gemv(ctypes.byref(v), device.ptr(x), device.ptr(y2), device.ptr(ws), wsb, s), "gemv")
+    finally:
+        del os.environ["ELL1_GEMV_PANEL"]
+    yref = torch.zeros(d, dtype=torch.float64, device=dev)
+    gref = torch.empty(n, dtype=torch.float64, device=dev)
+    for c0 in range(0, n, 4096):
+        blk = st[c0:c0 + 4096].double()                       # (4096 columns) x d, row-major = A[:, c].T
+        yref += blk.t() @ x[c0:c0 + 4096]
+        gref[c0:c0 + 4096] = blk @ r[:d]
+        del blk
+    torch.cuda.synchronize()
+    scale_y = float(torch.abs(st).sum(0).max()) * float(torch.abs(x).max())
+    scale_g = float(torch.abs(st).sum(1).max()) * float(torch.abs(r).max())
+    assert float(torch.abs(y[:d] - yref).max()) <= 1e-13 * scale_y
+    assert float(torch.abs(y[:d] - y2[:d]).max()) <= 1e-13 * scale_y
+    assert float(torch.abs(gg - gref).max()) <= 1e-13 * scale_g
