@@ -11,7 +11,7 @@ import threading
 from paper_1007_3753_b200.exceptions import DeviceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libell1b200.so")
+LIB_PATH = os.environ.get("ELL1_LIB_PATH") or os.path.join(_HERE, "libell1b200.so")   # override: diagnostics
 
 OK, ZERO_DATA, LAMBDA_NONPOS, BREAKDOWN, ILL_CONDITIONED, NOT_PD, DEGENERATE, RUNNING = range(8)
 ERR_ARG, ERR_CUDA, ERR_TIMEOUT, ERR_NOCOOP = -1, -2, -3, -4
