@@ -113,7 +113,10 @@ namespace gts {
 constexpr int CB = ELL1_GTS_CB;           // columns per A stage
 constexpr int RC = ELL1_GTS_RC;           // rows per chunk (row pairs strided over the consumers)
 constexpr int GB = ELL1_GTS_GB;           // A stages (column blocks) sharing one staged r chunk
-constexpr int STA = 2;                    // A ring depth
+#ifndef ELL1_GTS_STA
+#define ELL1_GTS_STA 2
+#endif
+constexpr int STA = ELL1_GTS_STA;         // A ring depth
 constexpr int STR = 2;                    // r ring depth
 constexpr int CW = 16;                    // consumer warps
 constexpr int THREADS = (CW + 1) * 32;    // + producer warp
