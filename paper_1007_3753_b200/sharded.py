@@ -134,6 +134,18 @@ class TorchCollective:
         return out
 
 
+class SoloCollective:
+    """One process, whatever torch.distributed says: a single-GPU solve of
+    the whole dictionary (shrinkage.fista_solve's streaming route)."""
+    world, rank = 1, 0
+
+    def allreduce_(self, t):
+        pass
+
+    def all_gather(self, t):
+        return t.clone()
+
+
 def _world(group):
     try:
         import torch.distributed as dist

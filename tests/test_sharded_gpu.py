@@ -293,3 +293,26 @@ def test_gemv_stream_pass_at_16gib():
     assert float(torch.abs(y[:d] - yref).max()) <= 1e-13 * scale_y
     assert float(torch.abs(y[:d] - y2[:d]).max()) <= 1e-13 * scale_y
     assert float(torch.abs(gg - gref).max()) <= 1e-13 * scale_g
+
+
+def test_fista_solve_streams_large_fp32_dictionaries():
+    """shrinkage.fista_solve on a >= 1 GiB float32 dictionary (the config-4
+    proxy, d=8192, n=32768) takes the streaming route (the sharded rounds at
+    world 1): same answer as the persistent kernel and as the reference
+    golden; an observer keeps the persistent kernel."""
+    from paper_1007_3753_b200 import shrinkage
+    from paper_1007_3753_b200.model import ProblemInstance, SolverConfig, StoppingRule
+    from tests.gpu_util import rel_err, support
+    A, b, gold = _cfg4_proxy()
+    cfg = SolverConfig(lam=None, tol=1e-6, max_iter=5000,
+                       stopping=StoppingRule("relative-estimate", 1e-6), options={"dtype": "float32"})
+    P = ProblemInstance(A, b)
+    assert shrinkage._stream_route(P, cfg, None)
+    assert not shrinkage._stream_route(P, cfg, lambda *a: None)
+    routed = shrinkage.fista_solve(P, cfg)
+    engine = shrinkage.FistaPlan(P, cfg).solve(None)
+    assert routed.iterations == engine.iterations
+    assert rel_err(routed.x_star, engine.x_star) <= 1e-9
+    assert [t.iteration for t in routed.trace] == [t.iteration for t in engine.trace]
+    assert rel_err(routed.x_star, gold["x"]) <= 1e-4
+    assert support(routed.x_star) == support(gold["x"])
