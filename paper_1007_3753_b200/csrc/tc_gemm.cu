@@ -112,8 +112,11 @@ struct Smem {
 // split the raw B tile in place (hi) and into the lo tile; every KC k-blocks
 // the drain warps add the tensor pipe's TMEM partial product into fp32 registers (the tensor
 // core's own accumulation spans only KC*32 products, the running sum is IEEE
-// fp32: keeps the SIMT SGEMM's accuracy).  TMEM holds two BN-column partial
-// buffers (the MMA fills one while the other drains).
+// fp32: keeps the SIMT SGEMM's accuracy).  TMEM holds four BN-column partial
+// buffers (BN <= 128; the MMA runs up to three k-blocks ahead of the drain).  On
+// pre-split operands (PRE) the split warps have nothing to split and drain the
+// upper half of the tile columns instead: each drain thread then keeps BN/2
+// sums and issues all its tcgen05.ld before one wait.
 // SK = 2 splits K over a 2-CTA cluster (small GEMMs: bigger tiles, same CTA
 // count); rank 1 hands its fp32 sums to rank 0 through distributed shared
 // memory and rank 0 adds them in a fixed order (deterministic) and writes C.
@@ -133,9 +136,13 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* full = (uint64_t*)(smem + ST * S::STAGE);
   uint64_t* conv = full + ST;
   uint64_t* empty = conv + ST;
-  uint64_t* tfull = empty + ST;       // [2]
-  uint64_t* tempty = tfull + 2;       // [2]
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  constexpr int NBUF = 4 * BN <= 512 ? 4 : 2;   // TMEM partial buffers (BN columns each)
+  constexpr int DG = PRE ? 2 : 1;               // drain warp groups (PRE: the idle split warps drain too)
+  constexpr int DC = BN / DG;                   // accumulator columns per drain thread
+  static_assert(DC % 16 == 0, "drain columns");
+  uint64_t* tfull = empty + ST;       // [NBUF]
+  uint64_t* tempty = tfull + NBUF;    // [NBUF]
+  uint32_t* tmem_slot = (uint32_t*)(tempty + NBUF);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * TM, n0 = blockIdx.y * BN;
   const int nkb_all = (K + TK - 1) / TK;
@@ -143,7 +150,7 @@ __global__ void __launch_bounds__(320, 1)
   const int kh = (nkb_all + SK - 1) / SK;
   const int kb0 = kz * kh;
   const int nkb = (nkb_all - kb0 < kh ? nkb_all - kb0 : kh);   // >= 1 when K > TK * (SK - 1)
-  constexpr uint32_t TCOLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 256;
+  constexpr uint32_t TCOLS = NBUF * BN <= 32 ? 32 : NBUF * BN <= 64 ? 64 : NBUF * BN <= 128 ? 128 : NBUF * BN <= 256 ? 256 : 512;
 
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&mAh) : "memory");
@@ -155,9 +162,9 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(conv + s, 128);
       mbar_init(empty + s, 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NBUF; ++b) {
       mbar_init(tfull + b, 1);
-      mbar_init(tempty + b, 128);
+      mbar_init(tempty + b, 128 * DG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -170,10 +177,12 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  float acc[BN];
+  float acc[DC];
 #pragma unroll
-  for (int j = 0; j < BN; ++j) acc[j] = 0.f;
+  for (int j = 0; j < DC; ++j) acc[j] = 0.f;
   const int q = warp & 3;                                    // TMEM lane quarter of a drain warp
+  const bool drainw = warp >= 2 && warp < (PRE ? 10 : 6);
+  const int cb = (DG == 2 && warp >= 6) ? DC : 0;            // first tile column of this drain thread
 
   if (warp == 0) {
     if (lane == 0) {
@@ -194,7 +203,7 @@ __global__ void __launch_bounds__(320, 1)
       // ---- MMA issuer: one fresh partial per KC k-blocks, lo*hi + hi*lo + hi*hi
       constexpr uint32_t idesc = instr_desc<BN>();
       for (int i = 0; i < nkb; ++i) {
-        const int s = i % ST, u = i / ST, p = i / KC, buf = p & 1, ub = p >> 1;
+        const int s = i % ST, u = i / ST, p = i / KC, buf = p % NBUF, ub = p / NBUF;
         const bool first = i % KC == 0, last = i % KC == KC - 1 || i == nkb - 1;
         if (first && ub > 0) TW(1, true, mbar_wait(tempty + buf, (ub - 1) & 1));
         TW(2, true, mbar_wait((PRE ? full : conv) + s, u & 1));
@@ -214,18 +223,19 @@ __global__ void __launch_bounds__(320, 1)
         if (last) umma_commit(tfull + buf);
       }
     }
-  } else if (warp < 6) {
-    // ---- drain warps (2..5): TMEM partials -> fp32 registers
-    const uint32_t tlane = tmem + ((uint32_t)(q * 32) << 16);
+  } else if (drainw) {
+    // ---- drain warps (2..5, and 6..9 on pre-split operands): TMEM partials -> fp32 registers
+    const uint32_t tlane = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)cb;
+    constexpr int CH = DC <= 64 ? DC : 32;                   // columns in flight per tcgen05.wait::ld
     for (int p = 0; p < (nkb + KC - 1) / KC; ++p) {
-      const int buf = p & 1;
-      TW(3, threadIdx.x == 64, mbar_wait(tfull + buf, (p >> 1) & 1));
+      const int buf = p % NBUF;
+      TW(3, threadIdx.x == 64, mbar_wait(tfull + buf, (p / NBUF) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t r[32];
+      for (int c0 = 0; c0 < DC; c0 += CH) {
+        uint32_t r[CH];
 #pragma unroll
-        for (int c = 0; c < 32; c += 16) {
+        for (int c = 0; c < CH; c += 16) {
           asm volatile(
               "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
               "[%16];"
@@ -236,7 +246,7 @@ __global__ void __launch_bounds__(320, 1)
         }
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc[c0 + j] += __uint_as_float(r[j]);
+        for (int j = 0; j < CH; ++j) acc[c0 + j] += __uint_as_float(r[j]);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(tempty + buf);
@@ -264,7 +274,6 @@ __global__ void __launch_bounds__(320, 1)
       mbar_arrive(conv + s);
     }
   }
-  const bool drainw = warp >= 2 && warp < 6;
   const int row_l = q * 32 + lane;                           // tile row of a drain thread
   if constexpr (SK == 2) {
     // rank 1 -> rank 0 partial sums through DSMEM (the operand ring is idle now)
@@ -276,17 +285,17 @@ __global__ void __launch_bounds__(320, 1)
       uint32_t rbuf;
       asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rbuf) : "r"(xbuf));
 #pragma unroll
-      for (int j = 0; j < BN; ++j)
-        asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(rbuf + (uint32_t)((j * TM + row_l) * 4)), "f"(acc[j])
+      for (int j = 0; j < DC; ++j)
+        asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(rbuf + (uint32_t)(((cb + j) * TM + row_l) * 4)), "f"(acc[j])
                      : "memory");
     }
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     if (kz == 0 && drainw) {
 #pragma unroll
-      for (int j = 0; j < BN; ++j) {
+      for (int j = 0; j < DC; ++j) {
         float v;
-        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(xbuf + (uint32_t)((j * TM + row_l) * 4)));
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(xbuf + (uint32_t)(((cb + j) * TM + row_l) * 4)));
         acc[j] += v;
       }
     }
@@ -295,8 +304,8 @@ __global__ void __launch_bounds__(320, 1)
     const int row = m0 + row_l;
     if (row < M) {
 #pragma unroll
-      for (int j = 0; j < BN; ++j) {
-        const int col = n0 + j;
+      for (int j = 0; j < DC; ++j) {
+        const int col = n0 + cb + j;
         if (col < N) C[(int64_t)col * ldc + row] = acc[j];
       }
     }
