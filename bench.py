@@ -764,8 +764,18 @@ def leg_cfg5_sweep(torch, dev, sizes=(1, 16, 256, 1024, 8192)):
             torch.cuda.synchronize()
             t = s.elapsed_time(e) / 1e3
             row[name] = {"solves_per_sec": B / t, "iterations_per_sec": float(r.iterations.sum()) / t}
+            # SURVEY 8(d) tensor fraction: 4 d n flops per instance-iteration (both products of an
+            # iteration), x3 TF32 MMAs per fp32-accurate product, against the library peak of the pipe
+            tfl = float(r.iterations.sum()) * 4.0 * d * n / t / 1e12
+            pk = gemm_peaks(torch, dev)
+            if name == "fista_f32":
+                row[name]["tensor_frac"] = 3.0 * tfl / pk["tf32_tflops"]
+            else:
+                row[name]["tensor_frac"] = tfl / pk["dgemm_tflops"]
         rows.append(row)
-    return {"workload": "cfg5 sweep: shared A 512 x 2048, k~U[16,256], lambda 1e-3", "rows": rows}
+    return {"workload": "cfg5 sweep: shared A 512 x 2048, k~U[16,256], lambda 1e-3", "rows": rows,
+            "tensor_frac": "4 d n flops per instance-iteration (SURVEY 8(d)); fp32 x3 (3xTF32 MMAs) over the "
+                           "cuBLAS TF32 peak, fp64 over the cuBLAS DGEMM peak (profiles/r02_gemm_peaks.json)"}
 
 
 def leg_align(torch, count=4096, d=1024, m=11, cpu_sample=64):

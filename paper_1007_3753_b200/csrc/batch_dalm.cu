@@ -19,6 +19,14 @@
 
 namespace ell1 {
 
+// min CTAs per SM of the y / x epilogues (88 / 74 registers uncapped: 2-3 CTAs per SM)
+#ifndef BD_MINB
+#define BD_MINB 4
+#endif
+#ifndef BD_MINB_ZC
+#define BD_MINB_ZC 1
+#endif
+
 struct DI {
   double bn, l1_prev, by, rhs2, resid2, rr, l1, maxu;
   double S[6];
@@ -128,7 +136,7 @@ __global__ void __launch_bounds__(BT) bd_init(const BDArgs a) {
 
 // z = clamp(A^T y + x/beta), v = z - x/beta (alm.py:239)
 template <bool VEC>
-__global__ void __launch_bounds__(BT) bd_z(const BDArgs a) {
+__global__ void __launch_bounds__(BT, BD_MINB_ZC) bd_z(const BDArgs a) {
   const int j = blockIdx.x;
   DI& I = a.inst[j];
   if (!I.active) return;
@@ -200,7 +208,7 @@ __global__ void __launch_bounds__(BT) bd_z(const BDArgs a) {
 
 // y = M v + Ginv b / beta; rhs = A z - (A x - b)/beta (alm.py:179-180)
 template <bool VEC>
-__global__ void __launch_bounds__(BT) bd_y(const BDArgs a) {
+__global__ void __launch_bounds__(BT, BD_MINB) bd_y(const BDArgs a) {
   const int j = blockIdx.x;
   __shared__ double sh[BW * 2 + 2];
   DI& I = a.inst[j];
@@ -314,7 +322,7 @@ __global__ void __launch_bounds__(BT) bd_yg(const BDArgs a) {
 
 // x_new = x - beta (z - A^T y) (alm.py:245-246); U = A^T y lives in UX[:, j]
 template <bool VEC>
-__global__ void __launch_bounds__(BT) bd_x(const BDArgs a, const double* Ut, const float* Ut32, int refine_only) {
+__global__ void __launch_bounds__(BT, BD_MINB) bd_x(const BDArgs a, const double* Ut, const float* Ut32, int refine_only) {
   const int j = blockIdx.x;
   __shared__ double sh[BW * 6 + 6];
   DI& I = a.inst[j];
@@ -390,7 +398,7 @@ __global__ void __launch_bounds__(BT) bd_x(const BDArgs a, const double* Ut, con
 
 // certificate, residual, trace, convergence (alm.py:181-188, 249-268)
 template <bool VEC>
-__global__ void __launch_bounds__(BT) bd_c(const BDArgs a, int refine_only) {
+__global__ void __launch_bounds__(BT, BD_MINB_ZC) bd_c(const BDArgs a, int refine_only) {
   const int j = blockIdx.x;
   const int B = gridDim.x;
   __shared__ double sh[BW * 3 + 3];

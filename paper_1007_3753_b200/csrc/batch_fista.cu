@@ -5,7 +5,8 @@
 //   bf_step   accepted last round: KKT, support, trace, stopping rules,
 //             continuation of that iteration, then the next momentum point;
 //             retrying: undo the global ring rotation for this instance
-//             (copies); then soft-threshold + backtracking reductions
+//             (copies) and rebuild the momentum point from the rings; then
+//             soft-threshold + backtracking reductions
 //   GEMM      A X_next
 //   bf_resid  r_next, F, Q: accept, or grow L and mark the instance for a retry
 //   GEMM      A^T R_next  (speculative for instances that will retry)
@@ -29,11 +30,13 @@ struct BFArgs {
   int f32;
   const double* Bm;           // ld x B (b columns)
   double* X[3];               // ldx x B
-  double* G[2];               // ldx x B
+  double* G[3];               // ldx x B: g(x_k), g(x_{k-1}) and the slot the speculative A^T r_next fills
   double* R[3];               // ld x B
   double* AX;                 // raw GEMM1 output (fp64 mode) ld x B
-  double* Y; double* GY;      // momentum point and its gradient (ldx x B), kept for retries
   float* X32; float* R32; float* AX32; float* G32;   // fp32 GEMM operands
+  float* G32r[3];             // fp32 storage without the [A, sI] block: the gradient ring IS the GEMM
+                              // output (fp32 values, n x B, pitch n): no fp64 copy is written or read
+  int g32ring;
   BI* inst;
   ell1_ctrl_t C;
   ell1_fista_opts_t O;
@@ -41,7 +44,7 @@ struct BFArgs {
   double* x_out;              // N x B0 (original order)
   int* it_out; int* conv_out; int* status_out;
   double* trace;              // optional [B0][max_iter][4]
-  int ix, ixp, ixn, igx, igxp, irx, irxp, irn;
+  int ix, ixp, ixn, igx, igxp, ign, irx, irxp, irn;
 };
 
 __global__ void __launch_bounds__(BT) bf_init(const BFArgs a, const double* CT, const float* CT32, int B) {
@@ -56,8 +59,8 @@ __global__ void __launch_bounds__(BT) bf_init(const BFArgs a, const double* CT, 
     else c = a.s * b[k - a.n];
     v[0] = nmax(v[0], fabs(c));
     for (int r = 0; r < 3; ++r) a.X[r][(int64_t)j * a.ldx + k] = 0.0;
-    a.G[0][(int64_t)j * a.ldx + k] = -c;
-    a.G[1][(int64_t)j * a.ldx + k] = -c;
+    if (a.g32ring) for (int r = 0; r < 3; ++r) a.G32r[r][(int64_t)j * a.n + k] = (float)-c;
+    else for (int r = 0; r < 3; ++r) a.G[r][(int64_t)j * a.ldx + k] = -c;
   }
   for (int64_t i = threadIdx.x; i < a.ld; i += BT) {
     const double bi = i < a.d ? b[i] : 0.0;
@@ -122,9 +125,20 @@ struct ProxAcc {
 
 // UNROLL independent elements per thread and trip: all loads of a trip are
 // issued before any use, so each CTA keeps UNROLL x BT loads in flight.
-constexpr int UNROLL = 4;
+// bf_step is latency-bound, not bandwidth-bound: at 128 registers only two
+// 256-thread CTAs fit an SM and each spends most of its life in its serial
+// prologue / reduction / epilogue.  Capping it at 64 registers (four CTAs per
+// SM, two elements per trip) is 1.6x faster at B = 8192 despite a few spills
+// (sweep over 3-6 CTAs x 1/2/4 elements: tools/bf_variants.sh)
+#ifndef BF_UNROLL
+#define BF_UNROLL 2
+#endif
+#ifndef BF_MINB
+#define BF_MINB 4
+#endif
+constexpr int UNROLL = BF_UNROLL;
 
-__global__ void __launch_bounds__(BT) bf_step(const BFArgs a) {
+__global__ void __launch_bounds__(BT, BF_MINB) bf_step(const BFArgs a) {
   const int j = blockIdx.x;
   __shared__ double sh[BW * 12 + 12];
   __shared__ double sc[6];
@@ -160,9 +174,9 @@ __global__ void __launch_bounds__(BT) bf_step(const BFArgs a) {
     double* __restrict__ gc = a.G[a.igx] + o;
     const double* __restrict__ gxp = a.G[a.igxp] + o;
     const double* __restrict__ rc = a.R[a.irx] + orr;
-    const float* __restrict__ g32 = a.f32 ? a.G32 + (int64_t)j * a.n : nullptr;
-    double* __restrict__ Y = a.Y + o;
-    double* __restrict__ GY = a.GY + o;
+    const bool ring32 = a.g32ring;
+    const float* __restrict__ g32 = a.f32 ? (ring32 ? a.G32r[a.igx] : a.G32) + (int64_t)j * a.n : nullptr;
+    const float* __restrict__ gq32 = ring32 ? a.G32r[a.igxp] + (int64_t)j * a.n : nullptr;
     double k5[5] = {0, 0, 0, 0, 0};
     ProxAcc P;
     P.zero();
@@ -176,21 +190,20 @@ __global__ void __launch_bounds__(BT) bf_step(const BFArgs a) {
           else g[u] = a.s * rc[k - a.n];
           xk[u] = xc[k];
           xq[u] = xp[k];
-          gq[u] = gxp[k];
+          gq[u] = ring32 ? (double)gq32[k] : gxp[k];
         }
       }
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u) {
         const int64_t k = base + u * BT;
         if (k >= N) continue;
-        if (g32 || k >= a.n) gc[k] = g[u];
+        if (!ring32 && (g32 || k >= a.n)) gc[k] = g[u];
         const double c = -g[u];
         if (xk[u] != 0.0) { k5[0] = nmax(k5[0], fabs(c - lam * sgn(xk[u]))); k5[2] = 1.0; }
         else { k5[1] = nmax(k5[1], fabs(c)); k5[3] = 1.0; }
         if (fabs(xk[u]) > cut) k5[4] += 1.0;
         const double yk = xk[u] + m * (xk[u] - xq[u]);                 // shrinkage.py:270
         const double gk = (1.0 + m) * g[u] - m * gq[u];               // A^T(A y - b)
-        Y[k] = yk; GY[k] = gk;
         const double un = soft1(yk - gk / L, thr);                      // shrinkage.py:204
         xn[k] = un;
         if (a.f32 && k < a.n) a.X32[(int64_t)j * a.ldx + k] = (float)un;
@@ -249,7 +262,16 @@ __global__ void __launch_bounds__(BT) bf_step(const BFArgs a) {
     for (int64_t k = threadIdx.x; k < N; k += BT) {
       a.X[a.ix][o + k] = a.X[a.ixp][o + k];
       a.X[a.ixp][o + k] = a.X[a.ixn][o + k];
-      a.G[a.igx][o + k] = a.G[a.igxp][o + k];
+      // both gradients survive a failed trial (its speculative A^T r went into the
+      // ring's third slot): the retry recomputes y and A^T(A y - b) from them
+      if (a.g32ring) {
+        const int64_t og = (int64_t)j * a.n + k;
+        a.G32r[a.igx][og] = a.G32r[a.igxp][og];
+        a.G32r[a.igxp][og] = a.G32r[a.ign][og];
+      } else {
+        a.G[a.igx][o + k] = a.G[a.igxp][o + k];
+        a.G[a.igxp][o + k] = a.G[a.ign][o + k];
+      }
     }
     for (int64_t i = threadIdx.x; i < a.ld; i += BT) {
       a.R[a.irx][orr + i] = a.R[a.irxp][orr + i];
@@ -272,26 +294,23 @@ __global__ void __launch_bounds__(BT) bf_step(const BFArgs a) {
   }
   __syncthreads();
   const double m = sc[0], L = sc[1], thr = sc[2];
-  const bool fr = mode == 0;
   const double* __restrict__ x = a.X[a.ix] + o;
   const double* __restrict__ xp = a.X[a.ixp] + o;
   double* __restrict__ xn = a.X[a.ixn] + o;
   const double* __restrict__ gx = a.G[a.igx] + o;
   const double* __restrict__ gxp = a.G[a.igxp] + o;
-  double* __restrict__ Y = a.Y + o;
-  double* __restrict__ GY = a.GY + o;
+  const float* __restrict__ gx32 = a.g32ring ? a.G32r[a.igx] + (int64_t)j * a.n : nullptr;
+  const float* __restrict__ gxp32 = a.g32ring ? a.G32r[a.igxp] + (int64_t)j * a.n : nullptr;
   ProxAcc P;
   P.zero();
+  // a retry (larger L) rebuilds the momentum point and its gradient from the same
+  // x_k, x_{k-1}, g(x_k), g(x_{k-1}) the first trial used: the same bits, and no
+  // y / g_y arrays to write on every accepted iteration
   for (int64_t k = threadIdx.x; k < N; k += BT) {
     const double xk = x[k];
-    double yk, gk;
-    if (fr) {
-      yk = xk + m * (xk - xp[k]);                           // shrinkage.py:270
-      gk = (1.0 + m) * gx[k] - m * gxp[k];                  // A^T(A y - b)
-      Y[k] = yk; GY[k] = gk;
-    } else {
-      yk = Y[k]; gk = GY[k];
-    }
+    const double yk = xk + m * (xk - xp[k]);                // shrinkage.py:270
+    const double gxk = gx32 ? (double)gx32[k] : gx[k], gpk = gx32 ? (double)gxp32[k] : gxp[k];
+    const double gk = (1.0 + m) * gxk - m * gpk;            // A^T(A y - b)
     const double u = soft1(yk - gk / L, thr);                // shrinkage.py:204
     xn[k] = u;
     if (a.f32 && k < a.n) a.X32[(int64_t)j * a.ldx + k] = (float)u;
@@ -403,10 +422,10 @@ extern "C" size_t ell1_batch_fista_workspace(const ell1_dict_t* D, int32_t B) {
   if (!dict_ok(D) || B < 1) return 0;
   const int64_t N = ncols_of(D), ldx = round4(N), ld = D->ld;
   size_t s = 0;
-  s += 7 * align_up(ldx * B * 8, 256) + 4 * align_up(ld * B * 8, 256);     // X, G, Y, GY, R, AX / Bm
+  s += 6 * align_up(ldx * B * 8, 256) + 4 * align_up(ld * B * 8, 256);     // X, G, R, AX / Bm
   s += align_up(ld * B * 8, 256);                                           // Bm
   s += align_up((int64_t)sizeof(BI) * B, 256) * 2;
-  s += align_up(ldx * B * 4, 256) * 2 + align_up(ld * B * 4, 256) * 2;       // fp32 operands
+  s += align_up(ldx * B * 4, 256) * 4 + align_up(ld * B * 4, 256) * 2;       // fp32 operands, fp32 gradient ring
   s += align_up((ldx > ld ? ldx : ld) * B * 8, 256);                        // compaction scratch
   s += align_up(B * 4, 256) + 4096;
   if (D->dtype == ELL1_F32) s += (size_t)f32split_floats(D, (ldx > ld ? ldx : ld) * B) * 4 + 1024;
@@ -427,15 +446,16 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
   a.C = *C; a.O = *O;
   Carve cv(ws, wsb);
   for (int k = 0; k < 3; ++k) a.X[k] = cv.take<double>(ldx * B);
-  for (int k = 0; k < 2; ++k) a.G[k] = cv.take<double>(ldx * B);
-  a.Y = cv.take<double>(ldx * B);
-  a.GY = cv.take<double>(ldx * B);
+  for (int k = 0; k < 3; ++k) a.G[k] = cv.take<double>(ldx * B);
   for (int k = 0; k < 3; ++k) a.R[k] = cv.take<double>(ld * B);
   a.AX = cv.take<double>(ld * B);
   double* Bm = cv.take<double>(ld * B);
   a.inst = cv.take<BI>(B);
   BI* inst2 = cv.take<BI>(B);
   a.X32 = cv.take<float>(ldx * B); a.G32 = cv.take<float>(ldx * B);
+  a.g32ring = a.f32 && !a.ext;
+  a.G32r[0] = a.G32;
+  for (int k = 1; k < 3; ++k) a.G32r[k] = a.g32ring ? cv.take<float>(ldx * B) : a.G32;
   a.R32 = cv.take<float>(ld * B); a.AX32 = cv.take<float>(ld * B);
   double* scratch = cv.take<double>((ldx > ld ? ldx : ld) * B);
   int* perm = cv.take<int>(B);
@@ -456,7 +476,7 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
   if (a.f32) {
     if (cudaMemsetAsync(a.X32, 0, ldx * B * 4, s) != cudaSuccess) return ELL1_ERR_CUDA;
   }
-  a.ix = 0; a.ixp = 1; a.ixn = 2; a.igx = 0; a.igxp = 1; a.irx = 0; a.irxp = 1; a.irn = 2;
+  a.ix = 0; a.ixp = 1; a.ixn = 2; a.igx = 0; a.igxp = 1; a.ign = 2; a.irx = 0; a.irxp = 1; a.irn = 2;
   // c = A^T b for every instance (GEMM), then per-instance setup
   {
     const void* Bop = Bm;
@@ -472,7 +492,7 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
   int Bcur = B;
   int* h_ctr = host_mailbox();
   h_ctr[0] = h_ctr[1] = 0;
-  // rounds between reads of the active count: a multiple of 6 (the period of
+  // rounds between reads of the active count: a multiple of 3 (the period of
   // the x / r / g ring rotations), so R rounds leave the ring indices as they
   // were and one recorded graph per batch size replays them
   constexpr int R = 12;
@@ -486,12 +506,12 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
     bf_resid<<<Bcur, BT, 0, ks>>>(aa);
     // g_next = A^T r_next into the g ring's free slot (speculative for retries)
     if (!gemm_AtR(ks, D, aa.f32 ? (const void*)aa.R32 : (const void*)aa.R[aa.irn], ld,
-                  aa.f32 ? (void*)aa.G32 : (void*)aa.G[aa.igxp], aa.f32 ? D->n : ldx, Bcur, spp))
+                  aa.f32 ? (void*)aa.G32r[aa.g32ring ? aa.ign : 0] : (void*)aa.G[aa.ign], aa.f32 ? D->n : ldx, Bcur, spp))
       return false;
     // rotate the rings (shrinkage.py:283-284); bf_step undoes it for retrying instances
     { int t = aa.ixp; aa.ixp = aa.ix; aa.ix = aa.ixn; aa.ixn = t; }
     { int t = aa.irxp; aa.irxp = aa.irx; aa.irx = aa.irn; aa.irn = t; }
-    { int t = aa.igxp; aa.igxp = aa.igx; aa.igx = t; }
+    { int t = aa.igxp; aa.igxp = aa.igx; aa.igx = aa.ign; aa.ign = t; }
     return cudaGetLastError() == cudaSuccess;
   };
   bool use_graph = true;
@@ -517,16 +537,17 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
         cok = cok && cudaMemcpyAsync(M, scratch, ldm * nact * 8, cudaMemcpyDeviceToDevice, s) == cudaSuccess;
       };
       for (int k = 0; k < 3; ++k) perm_mat(a.X[k], N, ldx);
-      for (int k = 0; k < 2; ++k) perm_mat(a.G[k], N, ldx);
-      perm_mat(a.Y, N, ldx);
-      perm_mat(a.GY, N, ldx);
+      if (!a.g32ring)
+        for (int k = 0; k < 3; ++k) perm_mat(a.G[k], N, ldx);
       for (int k = 0; k < 3; ++k) perm_mat(a.R[k], ld, ld);
       perm_mat(Bm, ld, ld);
-      if (a.f32) {                  // g_next of the last round (fp32 GEMM output) is still pending
+      // fp32 storage: g_next of the last round (the GEMM output) is still pending; without the
+      // [A, sI] block all three slots of the fp32 gradient ring are state
+      for (int k = 0; k < (a.g32ring ? 3 : a.f32 ? 1 : 0); ++k) {
         float* fs = reinterpret_cast<float*>(scratch);
         dim3 g((unsigned)((D->n + 255) / 256 < 64 ? (D->n + 255) / 256 : 64), (unsigned)nact);
-        gather_cols<float><<<g, 256, 0, s>>>(a.G32, fs, D->n, D->n, perm, nact);
-        cok = cok && cudaMemcpyAsync(a.G32, fs, D->n * nact * 4, cudaMemcpyDeviceToDevice, s) == cudaSuccess;
+        gather_cols<float><<<g, 256, 0, s>>>(a.G32r[k], fs, D->n, D->n, perm, nact);
+        cok = cok && cudaMemcpyAsync(a.G32r[k], fs, D->n * nact * 4, cudaMemcpyDeviceToDevice, s) == cudaSuccess;
       }
       {
         const int64_t words = (int64_t)sizeof(BI) / 4;
