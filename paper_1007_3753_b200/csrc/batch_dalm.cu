@@ -24,7 +24,7 @@ namespace ell1 {
 #define BD_MINB 4
 #endif
 #ifndef BD_MINB_ZC
-#define BD_MINB_ZC 1
+#define BD_MINB_ZC 4
 #endif
 
 struct DI {
