@@ -24,6 +24,11 @@
 
 #define T0 if (threadIdx.x == 0)
 
+// resident threads per SM the direction / step kernels are compiled for (register cap 65536 / HB_TPSM)
+#ifndef HB_TPSM
+#define HB_TPSM 1024
+#endif
+
 namespace ell1 {
 
 // Threads per instance CTA (NT, picked per round by hb_threads).  Measured at config 5 (B=256): 512 beats 128 —
@@ -233,7 +238,7 @@ __global__ void __launch_bounds__(NT) hb_init(HB a, int B) {
 
 // ---- finalise the previous breakpoint, then the direction of the next one
 template <int NT>
-__global__ void __launch_bounds__(NT) hb_dir(HB a, int nact) {
+__global__ void __launch_bounds__(NT, HB_TPSM / NT) hb_dir(HB a, int nact) {
   const int s = blockIdx.x;
   if (s >= nact) return;
   extern __shared__ __align__(16) double dsm[];
@@ -308,7 +313,7 @@ __global__ void __launch_bounds__(NT) hb_dir(HB a, int nact) {
 
 // ---- drift check, step lengths, event, factor update, residual
 template <int NT>
-__global__ void __launch_bounds__(NT) hb_step(HB a, int nact) {
+__global__ void __launch_bounds__(NT, HB_TPSM / NT) hb_step(HB a, int nact) {
   const int s = blockIdx.x;
   if (s >= nact) return;
   extern __shared__ __align__(16) double dsm[];

@@ -20,9 +20,16 @@ def main():
         kk = int(rng.integers(16, 257))
         X[rng.choice(2048, kk, replace=False), j] = rng.standard_normal(kk)
     D = dv.DeviceDictionary(A5)
-    r = homotopy_solve_batch(D, A5 @ X, 1e-3, SolverConfig())
+    Bm = A5 @ X
+    homotopy_solve_batch(D, np.ascontiguousarray(Bm[:, :16]), 1e-3, SolverConfig())
     torch.cuda.synchronize()
-    print("mean breakpoints", r.iterations.mean())
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    r = homotopy_solve_batch(D, Bm, 1e-3, SolverConfig())
+    e.record()
+    torch.cuda.synchronize()
+    print("B=%d %.1f ms %.0f solves/s mean breakpoints %.1f" % (B, s.elapsed_time(e), B / s.elapsed_time(e) * 1e3,
+                                                               r.iterations.mean()))
 
 
 if __name__ == "__main__":
