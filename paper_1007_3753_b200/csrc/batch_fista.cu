@@ -34,6 +34,8 @@ struct BFArgs {
   double* R[3];               // ld x B
   double* AX;                 // raw GEMM1 output (fp64 mode) ld x B
   float* X32; float* R32; float* AX32; float* G32;   // fp32 GEMM operands
+  float* X32l; float* R32l;   // the step / residual kernels write the GEMM operands pre-split (3xTF32 hi in
+                              // X32 / R32, lo here: the same bits as the GEMM's in-kernel split)
   float* G32r[3];             // fp32 storage without the [A, sI] block: the gradient ring IS the GEMM
                               // output (fp32 values, n x B, pitch n): no fp64 copy is written or read
   int g32ring;
@@ -106,6 +108,13 @@ __global__ void __launch_bounds__(BT) bf_init(const BFArgs a, const double* CT, 
 //   first round         -> first prox trial
 // One prox trial element (shrinkage.py:204-207 + the backtracking / stopping
 // partial sums), shared by the fused and the plain passes.
+// fp32 GEMM operand element as its 3xTF32 split
+__device__ __forceinline__ void st_split(float* hi, float* lo, int64_t i, float x) {
+  const float h = tf32_rna(x);
+  hi[i] = h;
+  lo[i] = tf32_rna(x - h);
+}
+
 struct ProxAcc {
   double s[7];
   __device__ __forceinline__ void zero() {
@@ -206,7 +215,7 @@ __global__ void __launch_bounds__(BT, BF_MINB) bf_step(const BFArgs a) {
         const double gk = (1.0 + m) * g[u] - m * gq[u];               // A^T(A y - b)
         const double un = soft1(yk - gk / L, thr);                      // shrinkage.py:204
         xn[k] = un;
-        if (a.f32 && k < a.n) a.X32[(int64_t)j * a.ldx + k] = (float)un;
+        if (a.f32 && k < a.n) st_split(a.X32, a.X32l, (int64_t)j * a.ldx + k, (float)un);
         P.add(un, yk, gk, xk[u], relest, gtr, gtr ? gtj[k] : 0.0);
       }
     }
@@ -313,7 +322,7 @@ __global__ void __launch_bounds__(BT, BF_MINB) bf_step(const BFArgs a) {
     const double gk = (1.0 + m) * gxk - m * gpk;            // A^T(A y - b)
     const double u = soft1(yk - gk / L, thr);                // shrinkage.py:204
     xn[k] = u;
-    if (a.f32 && k < a.n) a.X32[(int64_t)j * a.ldx + k] = (float)u;
+    if (a.f32 && k < a.n) st_split(a.X32, a.X32l, (int64_t)j * a.ldx + k, (float)u);
     P.add(u, yk, gk, xk, relest, gtr, gtr ? gtj[k] : 0.0);
   }
   cta_reduce<7>(P.s, 1u << 3, sh);
@@ -337,7 +346,7 @@ __global__ void __launch_bounds__(BT) bf_resid(const BFArgs a) {
     if (a.ext) ax = ax + a.s * xn[a.n + i];                 // robust.py:93
     const double r = ax - b[i];                             // shrinkage.py:205
     rn[i] = r;
-    if (a.f32) a.R32[(int64_t)j * a.ld + i] = (float)r;
+    if (a.f32) st_split(a.R32, a.R32l, (int64_t)j * a.ld + i, (float)r);
     q[0] += r * r;
     const double ry = (1.0 + mn) * r - mn * rx[i];
     q[1] += ry * ry;
@@ -425,7 +434,7 @@ extern "C" size_t ell1_batch_fista_workspace(const ell1_dict_t* D, int32_t B) {
   s += 6 * align_up(ldx * B * 8, 256) + 4 * align_up(ld * B * 8, 256);     // X, G, R, AX / Bm
   s += align_up(ld * B * 8, 256);                                           // Bm
   s += align_up((int64_t)sizeof(BI) * B, 256) * 2;
-  s += align_up(ldx * B * 4, 256) * 4 + align_up(ld * B * 4, 256) * 2;       // fp32 operands, fp32 gradient ring
+  s += align_up(ldx * B * 4, 256) * 5 + align_up(ld * B * 4, 256) * 3;       // fp32 operands (hi / lo), fp32 gradient ring
   s += align_up((ldx > ld ? ldx : ld) * B * 8, 256);                        // compaction scratch
   s += align_up(B * 4, 256) + 4096;
   if (D->dtype == ELL1_F32) s += (size_t)f32split_floats(D, (ldx > ld ? ldx : ld) * B) * 4 + 1024;
@@ -457,6 +466,7 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
   a.G32r[0] = a.G32;
   for (int k = 1; k < 3; ++k) a.G32r[k] = a.g32ring ? cv.take<float>(ldx * B) : a.G32;
   a.R32 = cv.take<float>(ld * B); a.AX32 = cv.take<float>(ld * B);
+  a.X32l = cv.take<float>(ldx * B); a.R32l = cv.take<float>(ld * B);
   double* scratch = cv.take<double>((ldx > ld ? ldx : ld) * B);
   int* perm = cv.take<int>(B);
   int* ctr = cv.take<int>(8);
@@ -475,6 +485,7 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
   if (cudaMemsetAsync(ctr, 0, 32, s) != cudaSuccess) return ELL1_ERR_CUDA;
   if (a.f32) {
     if (cudaMemsetAsync(a.X32, 0, ldx * B * 4, s) != cudaSuccess) return ELL1_ERR_CUDA;
+    if (cudaMemsetAsync(a.X32l, 0, ldx * B * 4, s) != cudaSuccess) return ELL1_ERR_CUDA;
   }
   a.ix = 0; a.ixp = 1; a.ixn = 2; a.igx = 0; a.igxp = 1; a.ign = 2; a.irx = 0; a.irxp = 1; a.irn = 2;
   // c = A^T b for every instance (GEMM), then per-instance setup
@@ -501,12 +512,13 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
     // ---- finish last round's accepted iterations, then one backtracking trial each
     bf_step<<<Bcur, BT, 0, ks>>>(aa);
     if (!gemm_AX(ks, D, aa.f32 ? (const void*)aa.X32 : (const void*)aa.X[aa.ixn], ldx,
-                 aa.f32 ? (void*)aa.AX32 : (void*)aa.AX, ld, Bcur, spp))
+                 aa.f32 ? (void*)aa.AX32 : (void*)aa.AX, ld, Bcur, spp, aa.f32 ? aa.X32l : nullptr))
       return false;
     bf_resid<<<Bcur, BT, 0, ks>>>(aa);
     // g_next = A^T r_next into the g ring's free slot (speculative for retries)
     if (!gemm_AtR(ks, D, aa.f32 ? (const void*)aa.R32 : (const void*)aa.R[aa.irn], ld,
-                  aa.f32 ? (void*)aa.G32r[aa.g32ring ? aa.ign : 0] : (void*)aa.G[aa.ign], aa.f32 ? D->n : ldx, Bcur, spp))
+                  aa.f32 ? (void*)aa.G32r[aa.g32ring ? aa.ign : 0] : (void*)aa.G[aa.ign], aa.f32 ? D->n : ldx, Bcur, spp,
+                  aa.f32 ? aa.R32l : nullptr))
       return false;
     // rotate the rings (shrinkage.py:283-284); bf_step undoes it for retrying instances
     { int t = aa.ixp; aa.ixp = aa.ix; aa.ix = aa.ixn; aa.ixn = t; }
