@@ -37,39 +37,36 @@ __global__ void chol_copy_kernel(int64_t d, const double* __restrict__ M, int64_
 __global__ void __launch_bounds__(PT) chol_panel_kernel(double* __restrict__ L, int64_t ld, int64_t kb, int nb,
                                                         int* status) {
   __shared__ double T[NB][NB + 1];
-  __shared__ int bad;
   if (*(volatile int*)status != 0) return;
   for (int t = threadIdx.x; t < nb * nb; t += PT) {
     const int c = t / nb, r = t - c * nb;
     T[r][c] = L[(kb + c) * ld + kb + r];
   }
-  if (threadIdx.x == 0) bad = 0;
   __syncthreads();
+  // two barriers per column: every thread reads the pivot itself (no thread-0
+  // section), and the trailing update maps thread -> (row, column group) with no
+  // index divisions; T[r][c] with r across lanes is conflict-free (pitch NB + 1)
+  static_assert(PT == 4 * NB, "row x column-group mapping");
+  const int r = threadIdx.x & (NB - 1), c0 = threadIdx.x >> 6;
   for (int j = 0; j < nb; ++j) {
-    if (threadIdx.x == 0) {
-      const double dj = T[j][j];
-      if (!(dj > 0.0) || !isfinite(dj)) bad = (int)(kb + j) + 1;
-      else T[j][j] = sqrt(dj);
+    const double dj = T[j][j];
+    if (!(dj > 0.0) || !isfinite(dj)) {                       // uniform: every thread sees the same pivot
+      if (threadIdx.x == 0) *status = (int)(kb + j) + 1;
+      return;
     }
-    __syncthreads();
-    if (bad) break;
-    const double piv = T[j][j];
+    const double piv = sqrt(dj);
     for (int i = j + 1 + threadIdx.x; i < nb; i += PT) T[i][j] /= piv;
     __syncthreads();
-    const int m = nb - j - 1;
-    for (int t = threadIdx.x; t < m * m; t += PT) {
-      const int c = t / m, r = t - c * m;
-      if (r >= c) T[j + 1 + r][j + 1 + c] -= T[j + 1 + r][j] * T[j + 1 + c][j];
+    if (threadIdx.x == 0) T[j][j] = piv;
+    if (r > j && r < nb) {
+      const double lr = T[r][j];
+      for (int c = j + 1 + c0; c <= r; c += 4) T[r][c] -= lr * T[c][j];
     }
     __syncthreads();
   }
-  if (bad) {
-    if (threadIdx.x == 0) *status = bad;
-    return;
-  }
   for (int t = threadIdx.x; t < nb * nb; t += PT) {
-    const int c = t / nb, r = t - c * nb;
-    if (r >= c) L[(kb + c) * ld + kb + r] = T[r][c];
+    const int c = t / nb, r2 = t - c * nb;
+    if (r2 >= c) L[(kb + c) * ld + kb + r2] = T[r2][c];
   }
 }
 
@@ -108,23 +105,37 @@ __global__ void __launch_bounds__(1024) chol_solve_kernel(int64_t d, const doubl
                                                           const double* __restrict__ rhs_all, int64_t ldr,
                                                           double* __restrict__ x_all, int64_t ldx) {
   extern __shared__ double y[];
+  // the 32 x 32 diagonal block of the current step, staged by the whole CTA with
+  // one coalesced load (double-buffered: the next block is fetched while the
+  // rank-32 update runs), so the warp's 32 dependent steps read shared memory
+  // instead of waiting on global memory twice per step
+  __shared__ double Dg[2][32][33];
   const double* __restrict__ rhs = rhs_all + (int64_t)blockIdx.x * ldr;
   double* __restrict__ x = x_all + (int64_t)blockIdx.x * ldx;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  auto stage = [&](int buf, int64_t jb, int w) {          // Dg[buf][r][c] = L[jb + r, jb + c], r >= c
+    for (int t = tid; t < 32 * 32; t += blockDim.x) {
+      const int c = t >> 5, r = t & 31;
+      if (r < w && c < w && r >= c) Dg[buf][r][c] = L[(jb + c) * ld + jb + r];
+    }
+  };
   for (int64_t i = tid; i < d; i += blockDim.x) y[i] = rhs[i];
+  stage(0, 0, (int)(d < 32 ? d : 32));
   __syncthreads();
   // forward: L y = rhs, 32-column blocks
-  for (int64_t jb = 0; jb < d; jb += 32) {
+  int buf = 0;
+  for (int64_t jb = 0; jb < d; jb += 32, buf ^= 1) {
     const int w = (int)((d - jb) < 32 ? (d - jb) : 32);
     if (warp == 0) {
       double v = lane < w ? y[jb + lane] : 0.0;
       for (int j = 0; j < w; ++j) {
-        const double xj = __shfl_sync(0xffffffffu, v, j) / L[(jb + j) * ld + jb + j];
+        const double xj = __shfl_sync(0xffffffffu, v, j) / Dg[buf][j][j];
         if (lane == j) v = xj;
-        if (lane > j && lane < w) v -= L[(jb + j) * ld + jb + lane] * xj;
+        if (lane > j && lane < w) v -= Dg[buf][lane][j] * xj;
       }
       if (lane < w) y[jb + lane] = v;
     }
+    if (jb + 32 < d) stage(buf ^ 1, jb + 32, (int)((d - jb - 32) < 32 ? (d - jb - 32) : 32));
     __syncthreads();
     for (int64_t i = jb + w + tid; i < d; i += blockDim.x) {
       double s = y[i];
@@ -134,17 +145,27 @@ __global__ void __launch_bounds__(1024) chol_solve_kernel(int64_t d, const doubl
     __syncthreads();
   }
   // backward: L^T x = y, blocks from the end; x_i = (y_i - sum_{j>i} L_ji x_j) / L_ii
-  for (int64_t je = d; je > 0; je -= 32) {
+  {
+    const int64_t je = d, jb = je >= 32 ? je - 32 : 0;
+    buf = 0;
+    stage(0, jb, (int)(je - jb));
+    __syncthreads();
+  }
+  for (int64_t je = d; je > 0; je -= 32, buf ^= 1) {
     const int64_t jb = je >= 32 ? je - 32 : 0;
     const int w = (int)(je - jb);
     if (warp == 0) {
       double v = lane < w ? y[jb + lane] : 0.0;
       for (int j = w - 1; j >= 0; --j) {
-        const double xj = __shfl_sync(0xffffffffu, v, j) / L[(jb + j) * ld + jb + j];
+        const double xj = __shfl_sync(0xffffffffu, v, j) / Dg[buf][j][j];
         if (lane == j) v = xj;
-        if (lane < j) v -= L[(jb + lane) * ld + jb + j] * xj;
+        if (lane < j) v -= Dg[buf][j][lane] * xj;
       }
       if (lane < w) y[jb + lane] = v;
+    }
+    if (jb > 0) {
+      const int64_t jb2 = jb >= 32 ? jb - 32 : 0;
+      stage(buf ^ 1, jb2, (int)(jb - jb2));
     }
     __syncthreads();
     // y_i -= sum_{j in block} L_ji x_j for i < jb: one warp per column i (coalesced in j)
