@@ -50,6 +50,29 @@ def test_batch_fista_equals_single_instances(bt, dtype):
             np.testing.assert_allclose(tr, np.array(ref.trace), rtol=1e-9, atol=1e-12)
 
 
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_batch_fista_many_backtracking_retries(bt, dtype):
+    """L0 far too small and a slow growth factor: every instance retries its first
+    trials many times in a row (the retry path rebuilds the momentum point from the
+    x / gradient rings after the host's ring rotation) and again whenever the
+    majorisation fails later.  Same iterations and trace as the reference recipe."""
+    from paper_1007_3753_b200.model import SolverConfig, StoppingRule
+    A, Bm, _ = _batch(96, 320, [4, 9, 17, 2, 30, 12, 6])
+    opts = {"L0": 1e-3, "eta": 1.2}
+    cfg = SolverConfig(lam=1e-3, tol=1e-6, stopping=StoppingRule("relative-estimate", 1e-6),
+                       options=dict(opts, dtype=dtype))
+    res = bt.fista_solve_batch(A, Bm, cfg, with_trace=True).results()
+    Ah = A if dtype == "float64" else A.astype(np.float32).astype(np.float64)
+    for j in range(Bm.shape[1]):
+        ref = oracle.fista(Ah, Bm[:, j], lam=1e-3, tol=1e-6, stop=("relative-estimate", 1e-6), opts=opts)
+        assert rel_err(res[j].x_star, ref.x) <= (1e-6 if dtype == "float64" else 1e-4), j
+        assert support(res[j].x_star) == support(ref.x), j
+        if dtype == "float64":
+            assert res[j].iterations == ref.iterations, (j, res[j].iterations, ref.iterations)
+            tr = np.array([tuple(t) for t in res[j].trace])
+            np.testing.assert_allclose(tr, np.array(ref.trace), rtol=1e-9, atol=1e-12)
+
+
 def test_batch_fista_default_lambda_and_budget(bt):
     from paper_1007_3753_b200.model import SolverConfig
     A, Bm, _ = _batch(64, 200, [3, 5, 9, 2], noise=0.01)
