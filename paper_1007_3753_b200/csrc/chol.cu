@@ -118,28 +118,37 @@ __global__ void __launch_bounds__(1024) chol_solve_kernel(int64_t d, const doubl
                                                           const double* __restrict__ rhs_all, int64_t ldr,
                                                           double* __restrict__ x_all, int64_t ldx) {
   extern __shared__ double y[];
-  // the 32 x 32 diagonal block of the current step, staged by the whole CTA with
-  // one coalesced load (double-buffered: the next block is fetched while the
-  // rank-32 update runs), so the warp's 32 dependent steps read shared memory
-  // instead of waiting on global memory twice per step
+  // the 32 x 32 diagonal block of a step, staged one step ahead (double-buffered)
+  // so the warp's 32 dependent steps read shared memory, not global memory
   __shared__ double Dg[2][32][33];
   const double* __restrict__ rhs = rhs_all + (int64_t)blockIdx.x * ldr;
   double* __restrict__ x = x_all + (int64_t)blockIdx.x * ldx;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  auto stage = [&](int buf, int64_t jb, int w) {          // Dg[buf][r][c] = L[jb + r, jb + c], r >= c
-    for (int t = tid; t < 32 * 32; t += blockDim.x) {
+  auto stage = [&](int buf, int64_t jb, int w, int t0, int nt) {   // Dg[buf][r][c] = L[jb + r, jb + c], r >= c
+    for (int t = t0; t < 32 * 32; t += nt) {
       const int c = t >> 5, r = t & 31;
       if (r < w && c < w && r >= c) Dg[buf][r][c] = L[(jb + c) * ld + jb + r];
     }
   };
   for (int64_t i = tid; i < d; i += blockDim.x) y[i] = rhs[i];
-  stage(0, 0, (int)(d < 32 ? d : 32));
+  stage(0, 0, (int)(d < 32 ? d : 32), tid, blockDim.x);
   __syncthreads();
-  // forward: L y = rhs, 32-column blocks
+  // Forward L y = rhs in 32-column blocks with one step of lookahead: in step k
+  // warp 0 applies block k-1 to the 32 rows of block k and solves their triangle
+  // while the other warps apply block k-1 to the rows below and stage the next
+  // diagonal block — one barrier per block, the triangle off the update's
+  // critical path.  Every y_i still receives the blocks in ascending order.
   int buf = 0;
   for (int64_t jb = 0; jb < d; jb += 32, buf ^= 1) {
     const int w = (int)((d - jb) < 32 ? (d - jb) : 32);
+    const int64_t jp = jb - 32;
     if (warp == 0) {
+      if (jb > 0 && lane < w) {
+        double s = y[jb + lane];
+        for (int j = 0; j < 32; ++j) s -= L[(jp + j) * ld + jb + lane] * y[jp + j];
+        y[jb + lane] = s;
+      }
+      __syncwarp();
       double v = lane < w ? y[jb + lane] : 0.0;
       const double dl = lane < w ? Dg[buf][lane][lane] : 1.0, rl = 1.0 / dl;
       for (int j = 0; j < w; ++j) {
@@ -149,27 +158,42 @@ __global__ void __launch_bounds__(1024) chol_solve_kernel(int64_t d, const doubl
         if (lane > j && lane < w) v -= Dg[buf][lane][j] * xj;
       }
       if (lane < w) y[jb + lane] = v;
-    }
-    if (jb + 32 < d) stage(buf ^ 1, jb + 32, (int)((d - jb - 32) < 32 ? (d - jb - 32) : 32));
-    __syncthreads();
-    for (int64_t i = jb + w + tid; i < d; i += blockDim.x) {
-      double s = y[i];
-      for (int j = 0; j < w; ++j) s -= L[(jb + j) * ld + i] * y[jb + j];
-      y[i] = s;
+    } else {
+      if (jb > 0)
+        for (int64_t i = jb + 32 + (tid - 32); i < d; i += blockDim.x - 32) {
+          double s = y[i];
+          for (int j = 0; j < 32; ++j) s -= L[(jp + j) * ld + i] * y[jp + j];
+          y[i] = s;
+        }
+      if (jb + 32 < d) stage(buf ^ 1, jb + 32, (int)((d - jb - 32) < 32 ? (d - jb - 32) : 32), tid - 32, blockDim.x - 32);
     }
     __syncthreads();
   }
-  // backward: L^T x = y, blocks from the end; x_i = (y_i - sum_{j>i} L_ji x_j) / L_ii
+  // Backward L^T x = y, blocks from the end, the same lookahead:
+  // x_i = (y_i - sum_{j>i} L_ji x_j) / L_ii
   {
-    const int64_t je = d, jb = je >= 32 ? je - 32 : 0;
+    const int64_t jb = d >= 32 ? d - 32 : 0;
     buf = 0;
-    stage(0, jb, (int)(je - jb));
+    stage(0, jb, (int)(d - jb), tid, blockDim.x);
     __syncthreads();
   }
   for (int64_t je = d; je > 0; je -= 32, buf ^= 1) {
     const int64_t jb = je >= 32 ? je - 32 : 0;
     const int w = (int)(je - jb);
+    const int64_t pb = je;                                    // previous (higher) block [pb, pb + pw)
+    const int pw = (int)((d - pb) < 32 ? (d - pb) : 32);
     if (warp == 0) {
+      if (je < d) {
+        // y_i -= sum_{j in previous block} L_ji x_j for the rows of this block
+        for (int r = 0; r < w; ++r) {
+          const int64_t i = jb + r;
+          double s = lane < pw ? L[i * ld + pb + lane] * y[pb + lane] : 0.0;
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+          if (lane == 0) y[i] -= s;
+        }
+        __syncwarp();
+      }
       double v = lane < w ? y[jb + lane] : 0.0;
       const double dl = lane < w ? Dg[buf][lane][lane] : 1.0, rl = 1.0 / dl;
       for (int j = w - 1; j >= 0; --j) {
@@ -179,18 +203,18 @@ __global__ void __launch_bounds__(1024) chol_solve_kernel(int64_t d, const doubl
         if (lane < j) v -= Dg[buf][j][lane] * xj;
       }
       if (lane < w) y[jb + lane] = v;
-    }
-    if (jb > 0) {
-      const int64_t jb2 = jb >= 32 ? jb - 32 : 0;
-      stage(buf ^ 1, jb2, (int)(jb - jb2));
-    }
-    __syncthreads();
-    // y_i -= sum_{j in block} L_ji x_j for i < jb: one warp per column i (coalesced in j)
-    for (int64_t i = warp; i < jb; i += nw) {
-      double s = lane < w ? L[i * ld + jb + lane] * y[jb + lane] : 0.0;
+    } else {
+      if (je < d)
+        for (int64_t i = warp - 1; i < jb; i += nw - 1) {     // one warp per row i (coalesced in j)
+          double s = lane < pw ? L[i * ld + pb + lane] * y[pb + lane] : 0.0;
 #pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) y[i] -= s;
+          for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+          if (lane == 0) y[i] -= s;
+        }
+      if (jb > 0) {
+        const int64_t jb2 = jb >= 32 ? jb - 32 : 0;
+        stage(buf ^ 1, jb2, (int)(jb - jb2), tid - 32, blockDim.x - 32);
+      }
     }
     __syncthreads();
   }

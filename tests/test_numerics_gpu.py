@@ -85,6 +85,47 @@ def test_chol_factor_and_solve():
         numerics.chol_factor(np.diag([1.0, -1.0]))
 
 
+@pytest.mark.parametrize("d", [1, 5, 31, 32, 33, 64, 70, 257, 1024])
+def test_dense_cholesky_abi_ragged_sizes(d):
+    """ell1_chol_factor_dense / ell1_chol_solve_dense(_multi) through the C ABI
+    (pdipa.py:43-62's factor + solve; chol.cu): blocked 64-column panels and the
+    32-column solve blocks with one step of lookahead, at sizes that are not
+    multiples of either block, against numpy's factor and solve."""
+    import ctypes
+    import torch
+    from paper_1007_3753_b200 import _lib
+    L_ = _lib.lib()
+    rng = np.random.default_rng(100 + d)
+    M = spd(rng, d)
+    dev = torch.device("cuda", 0)
+    Md = torch.from_numpy(M).to(dev)                          # symmetric: row- or column-major alike
+    Lf = torch.zeros((d, d), dtype=torch.float64, device=dev)
+    info = torch.zeros(1, dtype=torch.int32, device=dev)
+    st = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())               # noqa: E731
+    assert L_.ell1_chol_factor_dense(d, P(Md), d, 0.0, P(Lf), d, P(info), st) == 0
+    assert int(info.item()) == 0
+    Lh = np.tril(Lf.cpu().numpy().T)                          # column-major lower factor
+    np.testing.assert_allclose(Lh, np.linalg.cholesky(M), rtol=1e-11, atol=1e-12)
+    nrhs = 3
+    R = rng.standard_normal((nrhs, d))                        # nrhs right-hand sides, pitch d
+    Rd = torch.from_numpy(R).to(dev)
+    Xd = torch.empty_like(Rd)
+    assert L_.ell1_chol_solve_dense_multi(d, P(Lf), d, nrhs, P(Rd), d, P(Xd), d, st) == 0
+    X = Xd.cpu().numpy()
+    for k in range(nrhs):
+        np.testing.assert_allclose(X[k], np.linalg.solve(M, R[k]), rtol=1e-9, atol=1e-12)
+    x1 = torch.empty(d, dtype=torch.float64, device=dev)
+    assert L_.ell1_chol_solve_dense(d, P(Lf), d, P(Rd), P(x1), st) == 0
+    np.testing.assert_array_equal(x1.cpu().numpy(), X[0])
+    # not positive definite: LAPACK's status convention (failing column + 1)
+    Mb = M.copy()
+    k = d // 2
+    Mb[k, k] = -1.0
+    assert L_.ell1_chol_factor_dense(d, P(torch.from_numpy(Mb).to(dev)), d, 0.0, P(Lf), d, P(info), st) == 0
+    assert int(info.item()) == k + 1
+
+
 def test_chol_rank1_append_delete():
     from paper_1007_3753_b200 import numerics
     from paper_1007_3753_b200.exceptions import NotPositiveDefiniteError
