@@ -36,6 +36,7 @@ struct BFArgs {
   float* X32; float* R32; float* AX32; float* G32;   // fp32 GEMM operands
   float* X32l; float* R32l;   // the step / residual kernels write the GEMM operands pre-split (3xTF32 hi in
                               // X32 / R32, lo here: the same bits as the GEMM's in-kernel split)
+  int stage;                  // bf_step stages its four input rows in shared memory by bulk copies
   float* G32r[3];             // fp32 storage without the [A, sI] block: the gradient ring IS the GEMM
                               // output (fp32 values, n x B, pitch n): no fp64 copy is written or read
   int g32ring;
@@ -165,6 +166,34 @@ __global__ void __launch_bounds__(BT, BF_MINB) bf_step(const BFArgs a) {
     // in the same pass, the next iteration's first prox trial with the momentum
     // parameters it would use (they do not depend on the KKT outcome; discarded
     // when the instance stops)
+    // Staged inputs (no [A, sI] block, rows 16-byte sized): one thread starts bulk
+    // copies of the instance's four input rows (x_k, x_{k-1}, g(x_k), g(x_{k-1}))
+    // into shared memory before anything else, so all of the CTA's bytes are in
+    // flight at once at no register cost; the loop below then reads shared memory.
+    extern __shared__ __align__(16) unsigned char bf_dyn[];
+    __shared__ uint64_t stage_bar;
+    const bool staged = a.stage;
+    double* sxc = reinterpret_cast<double*>(bf_dyn);
+    double* sxp = sxc + N;
+    if (staged && threadIdx.x == 0) {
+      const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&stage_bar);
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(1));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      const uint32_t xb = (uint32_t)(N * 8), gb = a.f32 ? (uint32_t)(N * 4) : xb;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * xb + 2 * gb) : "memory");
+      const void* srcs[4] = {a.X[a.ix] + o, a.X[a.ixp] + o,
+                             a.f32 ? (const void*)(a.G32r[a.igx] + (int64_t)j * a.n) : (const void*)(a.G[a.igx] + o),
+                             a.f32 ? (const void*)(a.G32r[a.igxp] + (int64_t)j * a.n) : (const void*)(a.G[a.igxp] + o)};
+      const uint32_t dst0 = (uint32_t)__cvta_generic_to_shared(bf_dyn);
+      const uint32_t dsts[4] = {dst0, dst0 + xb, dst0 + 2 * xb, dst0 + 2 * xb + gb};
+      const uint32_t szs[4] = {xb, xb, gb, gb};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         dsts[q]),
+                     "l"(srcs[q]), "r"(szs[q]), "r"(bar)
+                     : "memory");
+    }
     if (threadIdx.x == 0) {
       const double tp = I.tc, tc = I.tn;
       const double tn = fista_t_next(tc);
@@ -177,15 +206,27 @@ __global__ void __launch_bounds__(BT, BF_MINB) bf_step(const BFArgs a) {
     }
     __syncthreads();
     const double m = sc[0], L = I.L, thr = sc[2], cut = sc[3], lam = I.lam;
-    const double* __restrict__ xc = a.X[a.ix] + o;
-    const double* __restrict__ xp = a.X[a.ixp] + o;
+    const double* __restrict__ xc = staged ? sxc : a.X[a.ix] + o;
+    const double* __restrict__ xp = staged ? sxp : a.X[a.ixp] + o;
     double* __restrict__ xn = a.X[a.ixn] + o;
     double* __restrict__ gc = a.G[a.igx] + o;
-    const double* __restrict__ gxp = a.G[a.igxp] + o;
+    const double* __restrict__ gcr = staged ? sxp + N : gc;                    // g(x_k) as read (fp64 storage)
+    const double* __restrict__ gxp = staged ? sxp + 2 * N : a.G[a.igxp] + o;
     const double* __restrict__ rc = a.R[a.irx] + orr;
     const bool ring32 = a.g32ring;
-    const float* __restrict__ g32 = a.f32 ? (ring32 ? a.G32r[a.igx] : a.G32) + (int64_t)j * a.n : nullptr;
-    const float* __restrict__ gq32 = ring32 ? a.G32r[a.igxp] + (int64_t)j * a.n : nullptr;
+    const float* __restrict__ sg32 = reinterpret_cast<const float*>(sxp + N);
+    const float* __restrict__ g32 =
+        a.f32 ? (staged ? sg32 : (ring32 ? a.G32r[a.igx] : a.G32) + (int64_t)j * a.n) : nullptr;
+    const float* __restrict__ gq32 = ring32 ? (staged ? sg32 + N : a.G32r[a.igxp] + (int64_t)j * a.n) : nullptr;
+    if (staged) {
+      const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&stage_bar);
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "BFWAIT_%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0, 1000000;\n\t"
+          "@!p bra BFWAIT_%=;\n\t}" ::"r"(bar)
+          : "memory");
+    }
     double k5[5] = {0, 0, 0, 0, 0};
     ProxAcc P;
     P.zero();
@@ -195,7 +236,7 @@ __global__ void __launch_bounds__(BT, BF_MINB) bf_step(const BFArgs a) {
       for (int u = 0; u < UNROLL; ++u) {
         const int64_t k = base + u * BT;
         if (k < N) {
-          if (k < a.n) g[u] = g32 ? (double)g32[k] : gc[k];
+          if (k < a.n) g[u] = g32 ? (double)g32[k] : gcr[k];
           else g[u] = a.s * rc[k - a.n];
           xk[u] = xc[k];
           xq[u] = xp[k];
@@ -500,6 +541,16 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
     if (!gemm_AtR(s, D, Bop, ld, CT, D->n, B, spp)) return ELL1_ERR_CUDA;
     bf_init<<<B, BT, 0, s>>>(a, (const double*)CT, (const float*)CT, B);
   }
+  // bf_step input staging: fp32 storage (24 bytes per element: 48 KB at n = 2048, four CTAs per SM still
+  // fit), rows of 16-byte multiples, no [A, sI] block.  fp64 storage would need 32 bytes per element
+  // (three CTAs per SM at n = 2048): measured slower at B = 1024 (92 -> 133 ms per solve in bf_step) and
+  // level at B = 8192, so it keeps the direct loads (the kernel supports both).
+  const size_t stage_bytes = (size_t)N * (a.f32 ? 24 : 32);
+  a.stage = a.f32 && a.g32ring && !a.ext && N % 4 == 0 && stage_bytes <= 56 * 1024;
+  if (const char* e = getenv("ELL1_BF_STAGE")) a.stage = a.stage && e[0] != '0';    // diagnostics
+  if (a.stage && stage_bytes > 40 * 1024 &&
+      cudaFuncSetAttribute(bf_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage_bytes) != cudaSuccess)
+    return ELL1_ERR_CUDA;
   int Bcur = B;
   int* h_ctr = host_mailbox();
   h_ctr[0] = h_ctr[1] = 0;
@@ -510,7 +561,7 @@ extern "C" int ell1_batch_fista(const ell1_dict_t* D, const double* Bmat, int32_
   cudaStream_t ks = s;
   auto one_round = [&](BFArgs& aa) -> bool {
     // ---- finish last round's accepted iterations, then one backtracking trial each
-    bf_step<<<Bcur, BT, 0, ks>>>(aa);
+    bf_step<<<Bcur, BT, aa.stage ? stage_bytes : 0, ks>>>(aa);
     if (!gemm_AX(ks, D, aa.f32 ? (const void*)aa.X32 : (const void*)aa.X[aa.ixn], ldx,
                  aa.f32 ? (void*)aa.AX32 : (void*)aa.AX, ld, Bcur, spp, aa.f32 ? aa.X32l : nullptr))
       return false;
