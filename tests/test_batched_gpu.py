@@ -73,6 +73,26 @@ def test_batch_fista_many_backtracking_retries(bt, dtype):
             np.testing.assert_allclose(tr, np.array(ref.trace), rtol=1e-9, atol=1e-12)
 
 
+@pytest.mark.parametrize("shape", [(65, 130), (64, 132), (33, 75), (96, 256)])
+def test_batch_fista_fp32_ragged_shapes(bt, shape):
+    """fp32 storage at row lengths that are / are not 16-byte multiples: the step
+    kernel stages its input rows with bulk copies only when every row is a whole
+    number of 16-byte units (n % 4 == 0) and falls back to direct loads otherwise;
+    both must give the fp32-storage answer of the reference recipe."""
+    from paper_1007_3753_b200.model import SolverConfig, StoppingRule
+    d, n = shape
+    A, Bm, _ = _batch(d, n, [3, 7, 2, 9, 5, 4], seed=11)
+    cfg = SolverConfig(lam=1e-3, tol=1e-6, stopping=StoppingRule("relative-estimate", 1e-6),
+                       options={"dtype": "float32"})
+    res = bt.fista_solve_batch(A, Bm, cfg).results()
+    Ah = A.astype(np.float32).astype(np.float64)
+    for j in range(Bm.shape[1]):
+        ref = oracle.fista(Ah, Bm[:, j], lam=1e-3, tol=1e-6, stop=("relative-estimate", 1e-6))
+        assert rel_err(res[j].x_star, ref.x) <= 1e-4, (shape, j)
+        assert support(res[j].x_star) == support(ref.x), (shape, j)
+        assert res[j].converged == ref.converged
+
+
 def test_batch_fista_default_lambda_and_budget(bt):
     from paper_1007_3753_b200.model import SolverConfig
     A, Bm, _ = _batch(64, 200, [3, 5, 9, 2], noise=0.01)
