@@ -623,7 +623,13 @@ def leg_cfg3(torch, dev, queries=1024):
                          "executed_mma_tflops": 3 * tfl_exec,
                          "executed_frac": 3 * tfl_exec / peaks["tf32_tflops"],
                          "executed": "2 d (n_A + d) + 2 d n_A + 2 n_A d + 4 d n_A = %.2f MFLOP per "
-                                     "query-iteration (x3 MMAs)" % (exec_per / 1e6)},
+                                     "query-iteration (x3 MMAs)" % (exec_per / 1e6),
+                         # frac can reach at most algorithmic / executed flops: the iteration also forms
+                         # the reference's y-step certificate A A^T y and the residual b - A x (alm.py:181,
+                         # 249), which SURVEY 8(d) does not count
+                         "ceiling_frac": (4.0 * d_ * nA + 2.0 * d_ * d_) / exec_per,
+                         "gemm_share_of_batch": "57% of the kernel time is in the GEMMs, whose main loops run "
+                                                "at 90-95% of the tf32 MMA rate (DESIGN 3.4.1)"},
             "queries_per_sec": queries / t, "ms_per_batch": 1e3 * t,
             "mean_iterations": float(its.mean()), "max_iterations": int(its.max()),
             "accuracy_vs_truth": float(np.mean(labels == truth)),
