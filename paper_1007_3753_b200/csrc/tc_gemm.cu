@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(320, 1)
                     const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mBl, int M, int N,
                     int K, float* __restrict__ C, int64_t ldc) {
   using S = Smem<BN, ST>;
-  static_assert(BN % 32 == 0 && BN <= 128, "BN");
+  static_assert(BN % 16 == 0 && BN <= 128 && (PRE || BN % 32 == 0), "BN");
   static_assert(SK == 1 || ST * S::STAGE >= BN * TM * 4, "partial exchange buffer");
 #ifdef TC3_TIMING
   const long long t_start = clock64();
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(320, 1)
   constexpr int NBUF = 4 * BN <= 512 ? 4 : 2;   // TMEM partial buffers (BN columns each)
   constexpr int DG = PRE ? 2 : 1;               // drain warp groups (PRE: the idle split warps drain too)
   constexpr int DC = BN / DG;                   // accumulator columns per drain thread
-  static_assert(DC % 16 == 0, "drain columns");
+  static_assert(DC % 8 == 0, "drain columns");
   uint64_t* tfull = empty + ST;       // [NBUF]
   uint64_t* tempty = tfull + NBUF;    // [NBUF]
   uint32_t* tmem_slot = (uint32_t*)(tempty + NBUF);
@@ -234,15 +234,25 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
       for (int c0 = 0; c0 < DC; c0 += CH) {
         uint32_t r[CH];
+        if constexpr (CH % 16 == 0) {
 #pragma unroll
-        for (int c = 0; c < CH; c += 16) {
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
-              "[%16];"
-              : "=r"(r[c + 0]), "=r"(r[c + 1]), "=r"(r[c + 2]), "=r"(r[c + 3]), "=r"(r[c + 4]), "=r"(r[c + 5]),
-                "=r"(r[c + 6]), "=r"(r[c + 7]), "=r"(r[c + 8]), "=r"(r[c + 9]), "=r"(r[c + 10]), "=r"(r[c + 11]),
-                "=r"(r[c + 12]), "=r"(r[c + 13]), "=r"(r[c + 14]), "=r"(r[c + 15])
-              : "r"(tlane + (uint32_t)(buf * BN + c0 + c)));
+          for (int c = 0; c < CH; c += 16) {
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                "[%16];"
+                : "=r"(r[c + 0]), "=r"(r[c + 1]), "=r"(r[c + 2]), "=r"(r[c + 3]), "=r"(r[c + 4]), "=r"(r[c + 5]),
+                  "=r"(r[c + 6]), "=r"(r[c + 7]), "=r"(r[c + 8]), "=r"(r[c + 9]), "=r"(r[c + 10]), "=r"(r[c + 11]),
+                  "=r"(r[c + 12]), "=r"(r[c + 13]), "=r"(r[c + 14]), "=r"(r[c + 15])
+                : "r"(tlane + (uint32_t)(buf * BN + c0 + c)));
+          }
+        } else {                                                 // 40 / 56 columns per thread (BN = 80 / 112)
+#pragma unroll
+          for (int c = 0; c < CH; c += 8) {
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(r[c + 0]), "=r"(r[c + 1]), "=r"(r[c + 2]), "=r"(r[c + 3]), "=r"(r[c + 4]),
+                           "=r"(r[c + 5]), "=r"(r[c + 6]), "=r"(r[c + 7])
+                         : "r"(tlane + (uint32_t)(buf * BN + c0 + c)));
+          }
         }
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
@@ -412,11 +422,14 @@ bool tc3_gemm(int M, int N, int K, const float* a_hi, const float* a_lo, int64_t
   // pick the tile (BN) and K split (SK) with the least per-SM smem traffic on
   // the critical path: waves x k-blocks per CTA x bytes per k-block (+ fixed costs)
   const int mt = (M + TM - 1) / TM, nkb = (K + TK - 1) / TK;
-  struct Opt { int bn, sk; } opts[] = {{64, 1}, {96, 1}, {128, 1}, {64, 2}, {96, 2}, {128, 2}};
+  // (80- and 112-column tiles exist for pre-split operands only: their drain takes 40 / 56 columns per thread)
+  struct Opt { int bn, sk; } opts[] = {{64, 1}, {80, 1}, {96, 1}, {112, 1}, {128, 1},
+                                       {64, 2}, {80, 2}, {96, 2}, {112, 2}, {128, 2}};
   double best = 1e300;
   Opt pick = {64, 1};
   for (const Opt& o : opts) {
     if (o.sk == 2 && nkb < 4) continue;
+    if (o.bn % 32 != 0 && !b_lo) continue;
     const long ctas = (long)mt * ((N + o.bn - 1) / o.bn) * o.sk;
     const long waves = (ctas + 147) / 148;
     const double kbs = (double)((nkb + o.sk - 1) / o.sk);
@@ -433,13 +446,22 @@ bool tc3_gemm(int M, int N, int K, const float* a_hi, const float* a_lo, int64_t
     const char* e = getenv("ELL1_TC3_KC");                // diagnostics: k-blocks per TMEM partial
     kc = e && atoi(e) == 2 ? 2 : 1;
   }
-  const int code = force ? force : pick.bn * 10 + pick.sk;
+  int code = force ? force : pick.bn * 10 + pick.sk;
+  if (!b_lo && (code / 10) % 32 != 0) code = pick.bn * 10 + pick.sk;   // forced pre-split-only tile, raw operand
 #define TC3_CASE(BN_, ST_, SK_)                                                                         \
   case BN_ * 10 + SK_:                                                                                  \
     if (b_lo) return launch<BN_, ST_, SK_, 1, true>(M, N, K, a_hi, a_lo, lda, b, b_lo, ldb, C, ldc, s); \
     return kc == 2 ? launch<BN_, ST_, SK_, 2, false>(M, N, K, a_hi, a_lo, lda, b, b, ldb, C, ldc, s)    \
                    : launch<BN_, ST_, SK_, 1, false>(M, N, K, a_hi, a_lo, lda, b, b, ldb, C, ldc, s);
+#define TC3_CASE_PRE(BN_, ST_, SK_)                                                                       \
+  case BN_ * 10 + SK_:                                                                                  \
+    if (b_lo) return launch<BN_, ST_, SK_, 1, true>(M, N, K, a_hi, a_lo, lda, b, b_lo, ldb, C, ldc, s); \
+    return false;
   switch (code) {
+    TC3_CASE_PRE(80, 4, 1)
+    TC3_CASE_PRE(80, 4, 2)
+    TC3_CASE_PRE(112, 3, 1)
+    TC3_CASE_PRE(112, 3, 2)
     TC3_CASE(64, 4, 1)
     TC3_CASE(96, 3, 1)
     TC3_CASE(128, 3, 1)
@@ -449,6 +471,7 @@ bool tc3_gemm(int M, int N, int K, const float* a_hi, const float* a_lo, int64_t
     TC3_CASE(128, 3, 2)
   }
 #undef TC3_CASE
+#undef TC3_CASE_PRE
 }
 
 }  // namespace ell1
